@@ -1,0 +1,119 @@
+/*
+ * xpcs_b200.h -- C ABI of the B200-native XPCS correlation hot path.
+ *
+ * This is the drop-in boundary for the reference's operator API
+ * (namespace xpcs, /root/reference/proj/include/xpcsvd/{correlate,compress,
+ * model}.hpp).  The reference has no FFI of its own; its C++ API is bound
+ * one-to-one by the C++ facade in include/xpcs_b200.hpp (and by
+ * paper_2407_20356_b200/_abi.py through ctypes), see INTEGRATION.md.
+ *
+ * Conventions
+ *   - plain pointers + sizes, no exceptions cross this boundary;
+ *   - every entry returns an xg_status; on error xg_last_error() gives the
+ *     message, xg_last_error_payload() the frame index (NormalizationError
+ *     frame_index, errors.hpp:36-45) / achievable rank (RankError);
+ *   - the caller owns host buffers, the library owns device buffers behind
+ *     the opaque handles; `*_on_device` flags say whether a pointer is a
+ *     device pointer (0 = host);
+ *   - a context is bound to one device and one CUDA stream and is not
+ *     re-entrant (single writer, like CompressedSeries, model.hpp:85-122).
+ *   - matrices are row-major; TTC values are returned as the reference's
+ *     f64 (or f32 / exact int32 Gram on request).
+ */
+#ifndef XPCS_B200_H_
+#define XPCS_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define XG_API __attribute__((visibility("default")))
+#else
+#define XG_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes: one per xpcs::Error subclass (errors.hpp:11-74). */
+typedef enum xg_status {
+  XG_OK = 0,
+  XG_ERR_SHAPE = 1,          /* xpcs::ShapeError */
+  XG_ERR_CONTRACT = 2,       /* xpcs::ContractError */
+  XG_ERR_MASK = 3,           /* xpcs::MaskError */
+  XG_ERR_NORMALIZATION = 4,  /* xpcs::NormalizationError (payload = frame) */
+  XG_ERR_RANK = 5,           /* xpcs::RankError (payload = achievable rank) */
+  XG_ERR_BINDING = 6,        /* xpcs::BindingError */
+  XG_ERR_FORMAT = 7,         /* xpcs::FormatError */
+  XG_ERR_CUDA = 100,         /* CUDA runtime / launch failure */
+  XG_ERR_DEVICE = 101,       /* no sm_100 device, or kernel self-check failed */
+  XG_ERR_INVALID = 102       /* bad handle / null pointer */
+} xg_status;
+
+/* Output element types for TTC readback. */
+typedef enum xg_dtype { XG_F64 = 0, XG_F32 = 1, XG_I32_GRAM = 2 } xg_dtype;
+
+/* Flags */
+#define XG_STRICT 0x1u      /* zero-norm frame -> XG_ERR_NORMALIZATION (reference
+                              behaviour, linalg.cpp:446-449); default flags the
+                              frame and excludes it from g2 instead */
+#define XG_NO_G2 0x2u       /* skip the g2 reduction */
+
+typedef struct xg_ctx xg_ctx;
+typedef struct xg_layout xg_layout;
+typedef struct xg_series xg_series;
+typedef struct xg_basis xg_basis;
+typedef struct xg_stream xg_stream;
+
+/* ---- library / context ------------------------------------------------ */
+XG_API int xg_version(void);
+/* device: CUDA ordinal; stream: a cudaStream_t (NULL = library-owned). */
+XG_API int xg_ctx_create(int device, void* stream, xg_ctx** out);
+XG_API void xg_ctx_destroy(xg_ctx* ctx);
+XG_API const char* xg_last_error(const xg_ctx* ctx);
+XG_API int64_t xg_last_error_payload(const xg_ctx* ctx, int32_t* ring);
+XG_API int xg_synchronize(xg_ctx* ctx);
+/* Number of kernels this library launched on ctx since creation. */
+XG_API int64_t xg_kernel_launches(const xg_ctx* ctx);
+
+/* ---- q-ring layout ----------------------------------------------------
+ * A set of PixelMask (model.hpp:16-24, model.cpp:10-26): ring r selects
+ * mask_indices[mask_offsets[r] .. mask_offsets[r+1]), strictly ascending and
+ * < full_pixels.  Replaces the per-ring apply_mask column gather
+ * (model.cpp:42-59) by one device permutation into a ring-major, zero-padded
+ * u8 layout. */
+XG_API int xg_layout_create(xg_ctx* ctx, int64_t full_pixels, int32_t n_rings,
+                     const int64_t* mask_offsets, const int64_t* mask_indices,
+                     xg_layout** out);
+XG_API void xg_layout_destroy(xg_layout* layout);
+XG_API int64_t xg_layout_ring_pixels(const xg_layout* layout, int32_t ring);
+
+/* ---- batch series (FrameSeries + TTC per ring) ------------------------ */
+XG_API int xg_series_create(xg_ctx* ctx, const xg_layout* layout, int64_t max_frames,
+                     xg_series** out);
+XG_API void xg_series_destroy(xg_series* s);
+/* frames: n_frames x full_pixels u8 photon counts (raster order).  Ingest:
+ * [H2D] + ring permutation + per-(frame, ring) statistics. */
+XG_API int xg_series_load_frames(xg_series* s, const uint8_t* frames, int64_t n_frames,
+                          int frames_on_device);
+/* Raw two-time correlation of every ring (ttc_raw, correlate.cpp:19-25):
+ * exact u8 x u8 -> int32 Gram on tcgen05 tensor cores, f64 normalisation and
+ * g2 (g2_from_ttc, correlate.cpp:67-85) on the device. */
+XG_API int xg_ttc_raw(xg_series* s, uint32_t flags);
+/* Readback.  dtype XG_F64/XG_F32: C = G_ij / (|x_i| |x_j|) (full symmetric
+ * n x n, ld elements per row); XG_I32_GRAM: the exact integer Gram. */
+XG_API int xg_series_get_ttc(xg_series* s, int32_t ring, int32_t dtype, void* out, int64_t ld,
+                      int out_on_device);
+/* g2 values (n), counts (n; N-d, or fewer when frames were flagged), lags in
+ * frames (multiply by frame_period for seconds). */
+XG_API int xg_series_get_g2(xg_series* s, int32_t ring, double* values, int64_t* counts);
+/* f64 frame norms |x_t| of ring (n) and the count of zero-norm frames. */
+XG_API int xg_series_get_norms(xg_series* s, int32_t ring, double* norms, int64_t* n_zero);
+XG_API int64_t xg_series_frames(const xg_series* s);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* XPCS_B200_H_ */

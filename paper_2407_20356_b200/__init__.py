@@ -1,0 +1,238 @@
+"""B200-native XPCS two-time correlation (arXiv 2407.20356 hot path).
+
+Python host mirror of the reference's operator API (namespace ``xpcs``,
+/root/reference/proj/include/xpcsvd/*.hpp) over the C ABI of
+``libxpcs_b200.so``.  Every numeric result is computed by the sm_100a
+kernels of that library; this module only marshals buffers and maps status
+codes onto the reference's exception hierarchy (errors.hpp:11-74).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Sequence
+
+import numpy as np
+
+from . import _abi
+from ._abi import lib
+
+
+# ----------------------------------------------------------------- errors
+class Error(RuntimeError):
+    """xpcs::Error"""
+
+
+class ShapeError(Error):
+    """xpcs::ShapeError"""
+
+
+class ContractError(Error):
+    """xpcs::ContractError"""
+
+
+class MaskError(Error):
+    """xpcs::MaskError"""
+
+
+class NormalizationError(Error):
+    """xpcs::NormalizationError; ``frame_index`` (+ ``ring`` for batched rings)."""
+
+    def __init__(self, msg: str, frame_index: int, ring: int = -1):
+        super().__init__(msg)
+        self.frame_index = frame_index
+        self.ring = ring
+
+
+class RankError(Error):
+    def __init__(self, msg: str, achievable_rank: int):
+        super().__init__(msg)
+        self.achievable_rank = achievable_rank
+
+
+class BindingError(Error):
+    pass
+
+
+class FormatError(Error):
+    pass
+
+
+class DeviceError(Error):
+    """CUDA failure, missing sm_100 device, or a kernel self-check failure."""
+
+
+_ERRS = {
+    _abi.ERR_SHAPE: ShapeError,
+    _abi.ERR_CONTRACT: ContractError,
+    _abi.ERR_MASK: MaskError,
+    _abi.ERR_BINDING: BindingError,
+    _abi.ERR_FORMAT: FormatError,
+}
+
+
+def _check(ctx_handle, rc: int) -> None:
+    if rc == _abi.OK:
+        return
+    msg = lib.xg_last_error(ctx_handle).decode() if ctx_handle else f"status {rc}"
+    if rc == _abi.ERR_NORMALIZATION:
+        ring = C.c_int32(-1)
+        frame = lib.xg_last_error_payload(ctx_handle, C.byref(ring))
+        raise NormalizationError(msg, int(frame), int(ring.value))
+    if rc == _abi.ERR_RANK:
+        raise RankError(msg, int(lib.xg_last_error_payload(ctx_handle, None)))
+    raise _ERRS.get(rc, DeviceError)(msg or f"status {rc}")
+
+
+def _ptr(a: np.ndarray) -> C.c_void_p:
+    return C.c_void_p(a.ctypes.data)
+
+
+# ---------------------------------------------------------------- context
+class Context:
+    """One device + one CUDA stream (xg_ctx).  ``stream`` may be a raw
+    cudaStream_t handle (int) such as ``torch.cuda.current_stream().cuda_stream``."""
+
+    def __init__(self, device: int = 0, stream: int | None = None):
+        h = C.c_void_p()
+        rc = lib.xg_ctx_create(device, C.c_void_p(stream) if stream else None, C.byref(h))
+        if rc != _abi.OK:
+            raise DeviceError(f"xg_ctx_create(device={device}) failed with status {rc} "
+                              "(an sm_100 B200 GPU is required; there is no CPU path)")
+        self.h = h
+        self.device = device
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            lib.xg_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+    def synchronize(self) -> None:
+        _check(self.h, lib.xg_synchronize(self.h))
+
+    @property
+    def kernel_launches(self) -> int:
+        return int(lib.xg_kernel_launches(self.h))
+
+
+# ----------------------------------------------------------------- layout
+class RingLayout:
+    """A set of q-ring ``PixelMask``s (model.hpp:16-24) over a detector of
+    ``full_pixels`` pixels.  ``masks[r]`` are strictly ascending indices."""
+
+    def __init__(self, ctx: Context, full_pixels: int, masks: Sequence[np.ndarray]):
+        self.ctx = ctx
+        self.full_pixels = int(full_pixels)
+        self.masks = [np.ascontiguousarray(m, dtype=np.int64) for m in masks]
+        offs = np.zeros(len(self.masks) + 1, np.int64)
+        offs[1:] = np.cumsum([m.size for m in self.masks])
+        idx = np.concatenate(self.masks) if self.masks else np.zeros(0, np.int64)
+        idx = np.ascontiguousarray(idx, dtype=np.int64)
+        h = C.c_void_p()
+        _check(ctx.h, lib.xg_layout_create(ctx.h, self.full_pixels, len(self.masks),
+                                           offs.ctypes.data_as(_abi.PI64),
+                                           idx.ctypes.data_as(_abi.PI64), C.byref(h)))
+        self.h = h
+
+    @classmethod
+    def from_ring_map(cls, ctx: Context, ring_of_pixel: np.ndarray, n_rings: int):
+        ring_of_pixel = np.asarray(ring_of_pixel).ravel()
+        masks = [np.nonzero(ring_of_pixel == r)[0] for r in range(n_rings)]
+        return cls(ctx, ring_of_pixel.size, masks)
+
+    @property
+    def n_rings(self) -> int:
+        return len(self.masks)
+
+    def ring_pixels(self, r: int) -> int:
+        return int(lib.xg_layout_ring_pixels(self.h, r))
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib.xg_layout_destroy(self.h)
+            self.h = None
+
+
+# ----------------------------------------------------------------- series
+class FrameSeries:
+    """Device-resident photon-count frames of one detector, correlated per
+    q-ring (the reference's ``FrameSeries`` + ``apply_mask`` per ring,
+    model.hpp:26-40).  Frames are u8 counts in raster order."""
+
+    def __init__(self, layout: RingLayout, max_frames: int, frame_period: float = 1.0):
+        if not (frame_period > 0.0):
+            raise ContractError("frame_period must be positive and finite")
+        self.layout = layout
+        self.ctx = layout.ctx
+        self.max_frames = int(max_frames)
+        self.frame_period = float(frame_period)
+        h = C.c_void_p()
+        _check(self.ctx.h, lib.xg_series_create(self.ctx.h, layout.h, self.max_frames,
+                                                C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib.xg_series_destroy(self.h)
+            self.h = None
+
+    @property
+    def n_frames(self) -> int:
+        return int(lib.xg_series_frames(self.h))
+
+    def load(self, frames, n_frames: int | None = None) -> "FrameSeries":
+        """Ingest ``frames`` (n x full_pixels u8): a numpy array (host, copied
+        H2D) or any object exposing ``data_ptr()`` (a CUDA torch tensor)."""
+        if hasattr(frames, "data_ptr"):
+            n = int(frames.shape[0]) if n_frames is None else n_frames
+            if frames.numel() < n * self.layout.full_pixels:
+                raise ShapeError("frames tensor smaller than n x full_pixels")
+            _check(self.ctx.h, lib.xg_series_load_frames(self.h, C.c_void_p(frames.data_ptr()),
+                                                         n, 1))
+            return self
+        a = np.ascontiguousarray(frames, dtype=np.uint8)
+        if a.ndim != 2 or a.shape[1] != self.layout.full_pixels:
+            raise ShapeError(f"frames must be n x {self.layout.full_pixels}, got {a.shape}")
+        _check(self.ctx.h, lib.xg_series_load_frames(self.h, _ptr(a), a.shape[0], 0))
+        self._keep = a
+        return self
+
+    def ttc_raw(self, strict: bool = False, g2: bool = True) -> "FrameSeries":
+        """Raw TTC of every ring (ttc_raw, correlate.cpp:19-25)."""
+        flags = (_abi.STRICT if strict else 0) | (0 if g2 else _abi.NO_G2)
+        _check(self.ctx.h, lib.xg_ttc_raw(self.h, flags))
+        return self
+
+    def ttc(self, ring: int, dtype: str = "f64") -> np.ndarray:
+        code = {"f64": _abi.F64, "f32": _abi.F32, "gram": _abi.I32_GRAM}[dtype]
+        n = self.n_frames
+        npd = {"f64": np.float64, "f32": np.float32, "gram": np.int32}[dtype]
+        out = np.empty((n, n), npd)
+        _check(self.ctx.h, lib.xg_series_get_ttc(self.h, ring, code, _ptr(out), n, 0))
+        return out
+
+    def g2(self, ring: int):
+        """(lags [s], values, counts) like G2Curve (model.hpp:142-146)."""
+        n = self.n_frames
+        vals = np.empty(n, np.float64)
+        cnt = np.empty(n, np.int64)
+        _check(self.ctx.h, lib.xg_series_get_g2(self.h, ring, vals.ctypes.data_as(_abi.PD),
+                                                cnt.ctypes.data_as(_abi.PI64)))
+        lags = np.arange(n, dtype=np.float64) * self.frame_period
+        return lags, vals, cnt
+
+    def norms(self, ring: int):
+        n = self.n_frames
+        out = np.empty(n, np.float64)
+        nz = C.c_int64(0)
+        _check(self.ctx.h, lib.xg_series_get_norms(self.h, ring, out.ctypes.data_as(_abi.PD),
+                                                   C.byref(nz)))
+        return out, int(nz.value)
+
+
+__all__ = [
+    "Context", "RingLayout", "FrameSeries", "Error", "ShapeError", "ContractError", "MaskError",
+    "NormalizationError", "RankError", "BindingError", "FormatError", "DeviceError",
+]

@@ -1,0 +1,81 @@
+"""ctypes binding of the C ABI in include/xpcs_b200.h (libxpcs_b200.so).
+
+The shared library is built in-tree by ``__graft_entry__.build()`` (or
+``make -C paper_2407_20356_b200/csrc``).  There is no fallback: if the
+library is missing, importing the package raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import re
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libxpcs_b200.so")
+HEADER = os.path.join(os.path.dirname(HERE), "include", "xpcs_b200.h")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build the sm_100a library first "
+        "(python -c 'import __graft_entry__ as g; g.build()'). There is no CPU fallback."
+    )
+
+lib = C.CDLL(LIB_PATH)
+
+P = C.c_void_p
+I32 = C.c_int32
+I64 = C.c_int64
+U32 = C.c_uint32
+PI64 = C.POINTER(C.c_int64)
+PI32 = C.POINTER(C.c_int32)
+PD = C.POINTER(C.c_double)
+
+_sigs = {
+    "xg_version": (C.c_int, []),
+    "xg_ctx_create": (C.c_int, [C.c_int, P, C.POINTER(P)]),
+    "xg_ctx_destroy": (None, [P]),
+    "xg_last_error": (C.c_char_p, [P]),
+    "xg_last_error_payload": (I64, [P, PI32]),
+    "xg_synchronize": (C.c_int, [P]),
+    "xg_kernel_launches": (I64, [P]),
+    "xg_layout_create": (C.c_int, [P, I64, I32, PI64, PI64, C.POINTER(P)]),
+    "xg_layout_destroy": (None, [P]),
+    "xg_layout_ring_pixels": (I64, [P, I32]),
+    "xg_series_create": (C.c_int, [P, P, I64, C.POINTER(P)]),
+    "xg_series_destroy": (None, [P]),
+    "xg_series_load_frames": (C.c_int, [P, P, I64, C.c_int]),
+    "xg_ttc_raw": (C.c_int, [P, U32]),
+    "xg_series_get_ttc": (C.c_int, [P, I32, I32, P, I64, C.c_int]),
+    "xg_series_get_g2": (C.c_int, [P, I32, PD, PI64]),
+    "xg_series_get_norms": (C.c_int, [P, I32, PD, PI64]),
+    "xg_series_frames": (I64, [P]),
+}
+
+for _name, (_res, _args) in _sigs.items():
+    _f = getattr(lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+
+
+def header_symbols(path: str = HEADER) -> list[str]:
+    """Every function the public header declares (for the export test)."""
+    text = open(path).read()
+    return sorted(set(re.findall(r"XG_API\s+[\w\s\*]+?\b(xg_\w+)\s*\(", text)))
+
+
+# status codes (xg_status)
+OK = 0
+ERR_SHAPE = 1
+ERR_CONTRACT = 2
+ERR_MASK = 3
+ERR_NORMALIZATION = 4
+ERR_RANK = 5
+ERR_BINDING = 6
+ERR_FORMAT = 7
+ERR_CUDA = 100
+ERR_DEVICE = 101
+ERR_INVALID = 102
+
+F64, F32, I32_GRAM = 0, 1, 2
+STRICT = 0x1
+NO_G2 = 0x2

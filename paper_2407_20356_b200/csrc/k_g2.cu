@@ -1,0 +1,139 @@
+// k_g2.cu -- K7: g2(tau) diagonal averages and TTC readback expansion.
+//
+// g2 replaces `g2_from_ttc` (src/correlate.cpp:67-85): g2[d] is the mean of
+// C(t, t+d) over t, accumulated in ascending t like the reference.  Each
+// thread owns one lag d of one ring and one segment of `seg` frames; a warp
+// covers 32 consecutive lags so every step of the t-loop is one coalesced
+// 128-byte row read of the Gram.  C(t,t+d) is formed in f64 from the exact
+// integer Gram and the f64 norms (so the only rounding is the normalisation
+// and the sums).  Segment partials are combined in ascending segment order:
+// the result is deterministic and independent of launch geometry.
+//
+// Zero-norm frames (inv = 0) are excluded from both the sum and the count;
+// without them count[d] = N - d exactly as in the reference.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "xg_kernels.h"
+
+namespace xg {
+
+namespace {
+
+template <int MODE>
+__global__ void __launch_bounds__(128) k_g2_partial(G2Params p) {
+  const int64_t d = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int s = blockIdx.y;
+  const int r = blockIdx.z;
+  if (d >= p.n_frames) return;
+  const int64_t t_begin = static_cast<int64_t>(s) * p.seg;
+  int64_t t_end = t_begin + p.seg;
+  if (t_end > p.n_frames - d) t_end = p.n_frames - d;
+  double acc = 0.0;
+  int64_t cnt = 0;
+  const double* inv = p.inv + r * p.inv_ld;
+  if (MODE == 0) {
+    const int32_t* g = p.gram + r * p.ring_stride + d;
+#pragma unroll 4
+    for (int64_t t = t_begin; t < t_end; ++t) {
+      const double a = inv[t], b = inv[t + d];
+      const int32_t v = __ldcs(g + t * (p.ld + 1));
+      acc += static_cast<double>(v) * (a * b);
+      cnt += (a != 0.0 && b != 0.0);
+    }
+  } else {
+    const float* c = p.cf32 + r * p.ring_stride + d;
+#pragma unroll 4
+    for (int64_t t = t_begin; t < t_end; ++t) {
+      acc += static_cast<double>(__ldcs(c + t * (p.ld + 1)));
+      ++cnt;
+    }
+  }
+  const int64_t o = (static_cast<int64_t>(r) * p.n_seg + s) * p.n_frames + d;
+  p.partial[o] = acc;
+  p.pcount[o] = cnt;
+}
+
+__global__ void k_g2_final(G2Params p) {
+  const int64_t d = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int r = blockIdx.y;
+  if (d >= p.n_frames) return;
+  double acc = 0.0;
+  int64_t cnt = 0;
+  for (int s = 0; s < p.n_seg; ++s) {
+    const int64_t o = (static_cast<int64_t>(r) * p.n_seg + s) * p.n_frames + d;
+    if (static_cast<int64_t>(s) * p.seg < p.n_frames - d) {
+      acc += p.partial[o];
+      cnt += p.pcount[o];
+    }
+  }
+  p.g2[r * p.g2_ld + d] = cnt > 0 ? acc / static_cast<double>(cnt) : 0.0;
+  p.counts[r * p.g2_ld + d] = cnt;
+}
+
+// Full symmetric readback of one ring: out(i,j) from the upper triangle
+// (i <= j) of the source, through a 32 x 33 shared tile so that lower-
+// triangle tiles are read coalesced and written transposed.
+__global__ void k_expand(ExpandParams p, int src_mode) {
+  __shared__ double tile[32][33];
+  const int64_t i0 = static_cast<int64_t>(blockIdx.y) * 32;
+  const int64_t j0 = static_cast<int64_t>(blockIdx.x) * 32;
+  const bool lower = i0 > j0;  // whole tile below the diagonal (tiles are aligned)
+  // source tile origin in the upper triangle
+  const int64_t si0 = lower ? j0 : i0, sj0 = lower ? i0 : j0;
+  for (int rr = threadIdx.y; rr < 32; rr += blockDim.y) {
+    const int64_t si = si0 + rr, sj = sj0 + threadIdx.x;
+    double v = 0.0;
+    if (si < p.n && sj < p.n) {
+      // inside a diagonal tile the lower half is taken from its mirror
+      const int64_t a = si <= sj ? si : sj, b = si <= sj ? sj : si;
+      if (src_mode == 0) {
+        const int32_t g = p.gram[a * p.ld + b];
+        v = p.out_dtype == 2 ? static_cast<double>(g)
+                             : static_cast<double>(g) * (p.inv[a] * p.inv[b]);
+      } else {
+        v = static_cast<double>(p.cf32[a * p.ld + b]);
+      }
+    }
+    tile[rr][threadIdx.x] = v;
+  }
+  __syncthreads();
+  for (int rr = threadIdx.y; rr < 32; rr += blockDim.y) {
+    const int64_t i = i0 + rr, j = j0 + threadIdx.x;
+    if (i >= p.n || j >= p.n) continue;
+    const double v = lower ? tile[threadIdx.x][rr] : tile[rr][threadIdx.x];
+    const int64_t o = i * p.out_ld + j;
+    if (p.out_dtype == 0)
+      static_cast<double*>(p.out)[o] = v;
+    else if (p.out_dtype == 1)
+      static_cast<float*>(p.out)[o] = static_cast<float>(v);
+    else
+      static_cast<int32_t*>(p.out)[o] = static_cast<int32_t>(v);
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_g2(const G2Params& p, int mode, cudaStream_t s) {
+  dim3 grid(static_cast<unsigned>((p.n_frames + 127) / 128), p.n_seg, p.n_rings);
+  if (mode == 0)
+    k_g2_partial<0><<<grid, 128, 0, s>>>(p);
+  else
+    k_g2_partial<1><<<grid, 128, 0, s>>>(p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  dim3 g2grid(static_cast<unsigned>((p.n_frames + 127) / 128), p.n_rings);
+  k_g2_final<<<g2grid, 128, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_expand(const ExpandParams& p, int src_mode, cudaStream_t s) {
+  const unsigned nt = static_cast<unsigned>((p.n + 31) / 32);
+  dim3 grid(nt, nt);
+  dim3 block(32, 8);
+  k_expand<<<grid, block, 0, s>>>(p, src_mode);
+  return cudaGetLastError();
+}
+
+}  // namespace xg

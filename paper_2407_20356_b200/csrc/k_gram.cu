@@ -1,0 +1,206 @@
+// k_gram.cu -- K2: per-ring raw two-time Gram G_q = X_q X_q^T on tcgen05.
+//
+// Replaces the reference's hot loop `gram` (src/linalg.cpp:127-156) as used by
+// `ttc_raw` (src/correlate.cpp:19-25).  Photon counts are u8, so the Gram is
+// computed EXACTLY as u8 x u8 -> s32 (tcgen05.mma kind::i8) and equals
+// xpcs::gram of the same counts bit for bit (all partial sums are integers
+// < 2^31, checked by the host from the diagonal bound 255^2 * M_q or the
+// ingest statistics).
+//
+// Design (sm_100a):
+//   * persistent kernel, one CTA per SM, static round-robin over a host-built
+//     list of upper-triangle tiles (ring, i0, j0) of 128 x 256 outputs;
+//   * warp 0: TMA producer (128-byte swizzled K-major boxes of the ring-major
+//     frame matrix, 4-stage smem ring, mbarrier full/empty pipeline);
+//   * warp 1: single-thread tcgen05.mma issuer, accumulator in TMEM
+//     (2 x 256 columns, double buffered so the epilogue of tile n overlaps the
+//     MMAs of tile n+1);
+//   * warp 2: TMEM allocator;  warps 4-7: epilogue, tcgen05.ld -> int32 rows
+//     -> 128-byte vector stores of the exact Gram tile.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "xg_kernels.h"
+#include "xg_ptx.cuh"
+
+namespace xg {
+
+namespace {
+
+constexpr int BM = 128;                    // tile rows   (frames t1)
+constexpr int BN = 256;                    // tile cols   (frames t2)
+constexpr int BK = 128;                    // bytes of K per stage (= 4 MMAs of K=32)
+constexpr int STAGES = 4;
+constexpr int A_BYTES = BM * BK;           // 16 KB
+constexpr int B_BYTES = BN * BK;           // 32 KB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int TMEM_COLS = 512;             // 2 accumulators x 256 s32 columns
+constexpr int NUM_THREADS = 256;
+constexpr uint32_t IDESC = idesc_i8(BM, BN, false);
+
+struct __align__(8) GramSmemTail {
+  uint64_t full[STAGES];
+  uint64_t empty[STAGES];
+  uint64_t tfull[2];
+  uint64_t tempty[2];
+  uint32_t tmem_base;
+};
+
+}  // namespace
+
+size_t gram_u8_smem_bytes() { return 1024 + STAGES * STAGE_BYTES + sizeof(GramSmemTail); }
+
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    k_gram_u8(const __grid_constant__ CUtensorMap tmX, GramParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * A_BYTES;
+  GramSmemTail* tail = reinterpret_cast<GramSmemTail*>(smem + STAGES * STAGE_BYTES);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&tail->full[s], 1);
+      mbar_init(&tail->empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tail->tfull[a], 1);
+      mbar_init(&tail->tempty[a], 4);  // one arrive per epilogue warp
+    }
+    fence_barrier_init();
+    tma_prefetch(&tmX);
+  }
+  if (warp == 2) tmem_alloc(&tail->tmem_base, TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = tail->tmem_base;
+
+  if (warp == 0) {
+    // ------------------------------------------------------- TMA producer
+    if (elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
+        const TileDesc td = p.tiles[t];
+        const int koff = p.ring_koff[td.ring];
+        const int nkb = p.ring_nkb[td.ring];
+        for (int kb = 0; kb < nkb; ++kb) {
+          if (!mbar_wait(&tail->empty[stage], phase ^ 1, p.err)) goto producer_done;
+          mbar_arrive_expect_tx(&tail->full[stage], STAGE_BYTES);
+          const int kc = koff + kb * BK;
+          tma_load_2d(sA + stage * A_BYTES, &tmX, &tail->full[stage], kc, td.i0);
+          tma_load_2d(sB + stage * B_BYTES, &tmX, &tail->full[stage], kc, td.j0);
+          tma_load_2d(sB + stage * B_BYTES + BK * 128, &tmX, &tail->full[stage], kc,
+                      td.j0 + 128);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    producer_done:;
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------- MMA issuer
+    if (elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
+        const TileDesc td = p.tiles[t];
+        const int nkb = p.ring_nkb[td.ring];
+        if (!mbar_wait(&tail->tempty[acc], acc_phase ^ 1, p.err)) break;
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + static_cast<uint32_t>(acc * BN);
+        bool ok = true;
+        for (int kb = 0; kb < nkb; ++kb) {
+          if (!mbar_wait(&tail->full[stage], phase, p.err)) {
+            ok = false;
+            break;
+          }
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + stage * A_BYTES);
+          const uint32_t b0 = smem_u32(sB + stage * B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 32; ++k) {
+            mma_i8(tmem_d, sdesc_k128(a0 + k * 32), sdesc_k128(b0 + k * 32), IDESC,
+                   (kb | k) != 0 ? 1u : 0u);
+          }
+          tc_commit(&tail->empty[stage]);  // smem slot free once these MMAs retire
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        if (!ok) break;
+        tc_commit(&tail->tfull[acc]);  // accumulator ready for the epilogue
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------- epilogue
+    const int sub = warp & 3;  // TMEM lane quarter this warp may access
+    const int row = sub * 32 + lane;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
+      const TileDesc td = p.tiles[t];
+      if (!mbar_wait(&tail->tfull[acc], acc_phase, p.err)) break;
+      tc_fence_after();
+      int32_t* gout = p.gram + static_cast<int64_t>(td.ring) * p.ring_stride +
+                      static_cast<int64_t>(td.i0 + row) * p.ld + td.j0;
+      const uint32_t tbase =
+          tmem_base + static_cast<uint32_t>(acc * BN) + (static_cast<uint32_t>(sub * 32) << 16);
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld32(tbase + c * 32, r);
+        tmem_ld_wait();
+        int4* dst = reinterpret_cast<int4*>(gout + c * 32);
+#pragma unroll
+        for (int v = 0; v < 8; ++v)
+          dst[v] = make_int4(static_cast<int>(r[4 * v]), static_cast<int>(r[4 * v + 1]),
+                             static_cast<int>(r[4 * v + 2]), static_cast<int>(r[4 * v + 3]));
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tail->tempty[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, TMEM_COLS);
+  }
+}
+
+cudaError_t launch_gram_u8(const CUtensorMap& tmX, const GramParams& p, int num_sms,
+                           cudaStream_t stream) {
+  const size_t smem = gram_u8_smem_bytes();
+  cudaError_t e =
+      cudaFuncSetAttribute(k_gram_u8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int grid = p.ntiles < num_sms ? p.ntiles : num_sms;
+  if (grid <= 0) return cudaSuccess;
+  k_gram_u8<<<grid, NUM_THREADS, smem, stream>>>(tmX, p);
+  return cudaGetLastError();
+}
+
+}  // namespace xg

@@ -1,0 +1,648 @@
+// xg_api.cu -- host runtime behind the C ABI (include/xpcs_b200.h).
+//
+// Owns device memory, the CUDA stream, TMA tensor maps and the tile lists;
+// validates arguments with the reference's error taxonomy
+// (include/xpcsvd/errors.hpp) and launches the sm_100a kernels.  There is no
+// CPU compute path: every numeric result comes from a kernel in this library.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/xpcs_b200.h"
+#include "xg_kernels.h"
+
+using namespace xg;
+
+namespace {
+
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                    const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                    CUtensorMapFloatOOBfill);
+
+struct Status {
+  int code;
+};
+
+}  // namespace
+
+struct xg_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int num_sms = 0;
+  std::string err;
+  int64_t payload = -1;
+  int32_t payload_ring = -1;
+  int* d_err = nullptr;  // device error word (pipeline timeouts, overflow)
+  int64_t launches = 0;
+  PFN_encodeTiled encode = nullptr;
+};
+
+struct xg_layout {
+  xg_ctx* ctx = nullptr;
+  int64_t pixels = 0;
+  int32_t rings = 0;
+  int32_t band = 8192;
+  int32_t n_bands = 0;
+  int64_t ktot = 0;
+  int32_t max_tab = 0;
+  std::vector<int64_t> ring_pixels, kpad, koff;
+  int32_t* d_band_seg = nullptr;
+  Segment* d_segs = nullptr;
+  int32_t* d_band_tab = nullptr;
+  uint16_t* d_tab = nullptr;
+  int32_t* d_ring_koff = nullptr;
+  int32_t* d_ring_nkb = nullptr;
+};
+
+struct xg_series {
+  xg_ctx* ctx = nullptr;
+  const xg_layout* L = nullptr;
+  int64_t tmax = 0;
+  int64_t t = 0;
+  int64_t tp = 0;  // padded frame count (Gram leading dimension)
+  uint8_t* d_raster = nullptr;
+  uint8_t* d_x = nullptr;
+  int64_t* d_norm2 = nullptr;
+  int64_t* d_sum1 = nullptr;
+  int32_t* d_maxc = nullptr;
+  double* d_norms = nullptr;
+  double* d_inv = nullptr;
+  int64_t* d_zero = nullptr;
+  int64_t* d_first_zero = nullptr;
+  int32_t* d_gram = nullptr;
+  double* d_g2 = nullptr;
+  int64_t* d_g2cnt = nullptr;
+  double* d_g2part = nullptr;
+  int64_t* d_g2pcnt = nullptr;
+  TileDesc* d_tiles = nullptr;
+  int32_t ntiles = 0;
+  int64_t tiles_for_t = -1;
+  bool have_raw = false;
+};
+
+namespace {
+
+int fail(xg_ctx* c, int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) {
+    c->err = buf;
+    if (code != XG_ERR_NORMALIZATION && code != XG_ERR_RANK) {
+      c->payload = -1;
+      c->payload_ring = -1;
+    }
+  }
+  return code;
+}
+
+int cuda_fail(xg_ctx* c, cudaError_t e, const char* what) {
+  return fail(c, XG_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+#define XG_CUDA(c, expr)                                  \
+  do {                                                    \
+    cudaError_t _e = (expr);                              \
+    if (_e != cudaSuccess) return cuda_fail((c), _e, #expr); \
+  } while (0)
+
+template <class T>
+cudaError_t dalloc(T** p, size_t count) {
+  *p = nullptr;
+  if (count == 0) count = 1;
+  return cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T));
+}
+
+template <class T>
+void dfree(T*& p) {
+  if (p) cudaFree(p);
+  p = nullptr;
+}
+
+int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+int make_map_u8(xg_ctx* c, CUtensorMap* map, const void* base, int64_t cols, int64_t rows,
+                int64_t row_stride, uint32_t box_cols, uint32_t box_rows) {
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(row_stride)};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = c->encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims,
+                         strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(c, XG_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return XG_OK;
+}
+
+// Device error word: bit0 pipeline timeout, bit2 int32 Gram overflow.
+int check_device_error(xg_ctx* c) {
+  int h = 0;
+  XG_CUDA(c, cudaMemcpyAsync(&h, c->d_err, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  XG_CUDA(c, cudaStreamSynchronize(c->stream));
+  if (h & 1) {
+    cudaMemsetAsync(c->d_err, 0, sizeof(int), c->stream);
+    return fail(c, XG_ERR_DEVICE, "tensor-core pipeline self-check failed (mbarrier timeout)");
+  }
+  if (h & 4) {
+    cudaMemsetAsync(c->d_err, 0, sizeof(int), c->stream);
+    return fail(c, XG_ERR_CONTRACT,
+                "ttc_raw: a frame norm^2 exceeds 2^31-1; the exact int32 Gram would overflow");
+  }
+  return XG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int xg_version(void) { return 100; }
+
+int xg_ctx_create(int device, void* stream, xg_ctx** out) {
+  if (!out) return XG_ERR_INVALID;
+  *out = nullptr;
+  xg_ctx* c = new xg_ctx();
+  c->device = device;
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) {
+    delete c;
+    return XG_ERR_CUDA;
+  }
+  cudaDeviceProp prop;
+  e = cudaGetDeviceProperties(&prop, device);
+  if (e != cudaSuccess || prop.major != 10) {
+    delete c;
+    return XG_ERR_DEVICE;  // sm_100a kernels only
+  }
+  c->num_sms = prop.multiProcessorCount;
+  if (stream) {
+    c->stream = static_cast<cudaStream_t>(stream);
+  } else {
+    cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    c->own_stream = true;
+  }
+  cudaDriverEntryPointQueryResult q;
+  void* fn = nullptr;
+  e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+  if (e != cudaSuccess || !fn) {
+    delete c;
+    return XG_ERR_CUDA;
+  }
+  c->encode = reinterpret_cast<PFN_encodeTiled>(fn);
+  if (cudaMalloc(&c->d_err, sizeof(int)) != cudaSuccess) {
+    delete c;
+    return XG_ERR_CUDA;
+  }
+  cudaMemset(c->d_err, 0, sizeof(int));
+  *out = c;
+  return XG_OK;
+}
+
+void xg_ctx_destroy(xg_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->d_err) cudaFree(c->d_err);
+  if (c->own_stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+const char* xg_last_error(const xg_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+int64_t xg_last_error_payload(const xg_ctx* c, int32_t* ring) {
+  if (!c) return -1;
+  if (ring) *ring = c->payload_ring;
+  return c->payload;
+}
+
+int xg_synchronize(xg_ctx* c) {
+  if (!c) return XG_ERR_INVALID;
+  XG_CUDA(c, cudaStreamSynchronize(c->stream));
+  return check_device_error(c);
+}
+
+int64_t xg_kernel_launches(const xg_ctx* c) { return c ? c->launches : -1; }
+
+// ------------------------------------------------------------------ layout
+int xg_layout_create(xg_ctx* c, int64_t full_pixels, int32_t n_rings,
+                     const int64_t* offsets, const int64_t* indices, xg_layout** out) {
+  if (!c || !out || !offsets || !indices) return XG_ERR_INVALID;
+  *out = nullptr;
+  if (full_pixels < 1) return fail(c, XG_ERR_CONTRACT, "layout: full_pixels must be >= 1");
+  if (n_rings < 1) return fail(c, XG_ERR_CONTRACT, "layout: need at least one ring");
+  // PixelMask validation (model.cpp:10-26) for every ring.
+  for (int32_t r = 0; r < n_rings; ++r) {
+    const int64_t b = offsets[r], e = offsets[r + 1];
+    if (e <= b) return fail(c, XG_ERR_MASK, "pixel mask %d selects no pixels", r);
+    for (int64_t i = b; i < e; ++i) {
+      if (indices[i] < 0 || indices[i] >= full_pixels)
+        return fail(c, XG_ERR_MASK, "mask %d index %lld out of range for %lld pixels", r,
+                    (long long)indices[i], (long long)full_pixels);
+      if (i > b && indices[i] <= indices[i - 1])
+        return fail(c, XG_ERR_MASK, "mask %d indices not strictly ascending at position %lld",
+                    r, (long long)(i - b));
+    }
+  }
+  xg_layout* L = new xg_layout();
+  L->ctx = c;
+  L->pixels = full_pixels;
+  L->rings = n_rings;
+  L->band = static_cast<int32_t>(std::min<int64_t>(8192, round_up(full_pixels, 16)));
+  L->n_bands = static_cast<int32_t>((full_pixels + L->band - 1) / L->band);
+  const int32_t nb = L->n_bands;
+  // count[r][b] pixels of ring r in band b (indices ascending -> bands ascending)
+  std::vector<int64_t> cnt(static_cast<size_t>(n_rings) * nb, 0);
+  for (int32_t r = 0; r < n_rings; ++r)
+    for (int64_t i = offsets[r]; i < offsets[r + 1]; ++i) cnt[(size_t)r * nb + indices[i] / L->band]++;
+  L->ring_pixels.resize(n_rings);
+  L->kpad.resize(n_rings);
+  L->koff.resize(n_rings);
+  std::vector<int64_t> segoff(static_cast<size_t>(n_rings) * nb, 0);
+  int64_t koff = 0;
+  for (int32_t r = 0; r < n_rings; ++r) {
+    int64_t k = 0;
+    for (int32_t b = 0; b < nb; ++b) {
+      segoff[(size_t)r * nb + b] = k;
+      k += round_up(cnt[(size_t)r * nb + b], 16);
+    }
+    L->ring_pixels[r] = offsets[r + 1] - offsets[r];
+    L->kpad[r] = std::max<int64_t>(128, round_up(k, 128));
+    L->koff[r] = koff;
+    koff += L->kpad[r];
+  }
+  L->ktot = koff;
+  if (L->ktot > INT32_MAX) {
+    delete L;
+    return fail(c, XG_ERR_CONTRACT, "layout: padded ring width exceeds 2^31 bytes");
+  }
+  // Per band: segments (ring order) and the u16 source table.
+  std::vector<int32_t> band_seg(nb + 1, 0), band_tab(nb + 1, 0);
+  std::vector<Segment> segs;
+  std::vector<uint16_t> tab;
+  // bucket indices per (band, ring) without a second pass over rings:
+  std::vector<int64_t> cursor(static_cast<size_t>(n_rings), 0);
+  for (int32_t r = 0; r < n_rings; ++r) cursor[r] = offsets[r];
+  for (int32_t b = 0; b < nb; ++b) {
+    band_seg[b] = static_cast<int32_t>(segs.size());
+    band_tab[b] = static_cast<int32_t>(tab.size());
+    int32_t local = 0;
+    for (int32_t r = 0; r < n_rings; ++r) {
+      const int64_t n = cnt[(size_t)r * nb + b];
+      if (n == 0) continue;
+      const int64_t len = round_up(n, 16);
+      Segment s;
+      s.ring = r;
+      s.dst = static_cast<int32_t>(L->koff[r] + segoff[(size_t)r * nb + b]);
+      s.len = static_cast<int32_t>(len);
+      s.taboff = local;
+      segs.push_back(s);
+      for (int64_t i = 0; i < n; ++i)
+        tab.push_back(static_cast<uint16_t>(indices[cursor[r] + i] - (int64_t)b * L->band));
+      for (int64_t i = n; i < len; ++i) tab.push_back(0xFFFF);
+      cursor[r] += n;
+      local += static_cast<int32_t>(len);
+    }
+    L->max_tab = std::max(L->max_tab, local);
+  }
+  band_seg[nb] = static_cast<int32_t>(segs.size());
+  band_tab[nb] = static_cast<int32_t>(tab.size());
+  std::vector<int32_t> rk(n_rings), rn(n_rings);
+  for (int32_t r = 0; r < n_rings; ++r) {
+    rk[r] = static_cast<int32_t>(L->koff[r]);
+    rn[r] = static_cast<int32_t>(L->kpad[r] / 128);
+  }
+  cudaError_t e = cudaSuccess;
+  if ((e = dalloc(&L->d_band_seg, band_seg.size())) != cudaSuccess ||
+      (e = dalloc(&L->d_segs, segs.size())) != cudaSuccess ||
+      (e = dalloc(&L->d_band_tab, band_tab.size())) != cudaSuccess ||
+      (e = dalloc(&L->d_tab, tab.size())) != cudaSuccess ||
+      (e = dalloc(&L->d_ring_koff, rk.size())) != cudaSuccess ||
+      (e = dalloc(&L->d_ring_nkb, rn.size())) != cudaSuccess) {
+    xg_layout_destroy(L);
+    return cuda_fail(c, e, "layout alloc");
+  }
+  cudaMemcpy(L->d_band_seg, band_seg.data(), band_seg.size() * 4, cudaMemcpyHostToDevice);
+  cudaMemcpy(L->d_segs, segs.data(), segs.size() * sizeof(Segment), cudaMemcpyHostToDevice);
+  cudaMemcpy(L->d_band_tab, band_tab.data(), band_tab.size() * 4, cudaMemcpyHostToDevice);
+  cudaMemcpy(L->d_tab, tab.data(), tab.size() * 2, cudaMemcpyHostToDevice);
+  cudaMemcpy(L->d_ring_koff, rk.data(), rk.size() * 4, cudaMemcpyHostToDevice);
+  e = cudaMemcpy(L->d_ring_nkb, rn.data(), rn.size() * 4, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    xg_layout_destroy(L);
+    return cuda_fail(c, e, "layout upload");
+  }
+  *out = L;
+  return XG_OK;
+}
+
+void xg_layout_destroy(xg_layout* L) {
+  if (!L) return;
+  dfree(L->d_band_seg);
+  dfree(L->d_segs);
+  dfree(L->d_band_tab);
+  dfree(L->d_tab);
+  dfree(L->d_ring_koff);
+  dfree(L->d_ring_nkb);
+  delete L;
+}
+
+int64_t xg_layout_ring_pixels(const xg_layout* L, int32_t ring) {
+  if (!L || ring < 0 || ring >= L->rings) return -1;
+  return L->ring_pixels[ring];
+}
+
+// ------------------------------------------------------------------ series
+int xg_series_create(xg_ctx* c, const xg_layout* L, int64_t max_frames, xg_series** out) {
+  if (!c || !L || !out) return XG_ERR_INVALID;
+  *out = nullptr;
+  if (max_frames < 2) return fail(c, XG_ERR_CONTRACT, "series: need at least 2 frames");
+  xg_series* s = new xg_series();
+  s->ctx = c;
+  s->L = L;
+  s->tmax = max_frames;
+  s->tp = round_up(max_frames, 256);
+  const int64_t Q = L->rings;
+  cudaError_t e = cudaSuccess;
+  if ((e = dalloc(&s->d_raster, (size_t)max_frames * L->pixels)) != cudaSuccess ||
+      (e = dalloc(&s->d_x, (size_t)max_frames * L->ktot)) != cudaSuccess ||
+      (e = dalloc(&s->d_norm2, (size_t)max_frames * Q)) != cudaSuccess ||
+      (e = dalloc(&s->d_sum1, (size_t)max_frames * Q)) != cudaSuccess ||
+      (e = dalloc(&s->d_maxc, (size_t)max_frames * Q)) != cudaSuccess ||
+      (e = dalloc(&s->d_norms, (size_t)s->tp * Q)) != cudaSuccess ||
+      (e = dalloc(&s->d_inv, (size_t)s->tp * Q)) != cudaSuccess ||
+      (e = dalloc(&s->d_zero, (size_t)Q)) != cudaSuccess ||
+      (e = dalloc(&s->d_first_zero, (size_t)Q)) != cudaSuccess ||
+      (e = dalloc(&s->d_gram, (size_t)Q * s->tp * s->tp)) != cudaSuccess ||
+      (e = dalloc(&s->d_g2, (size_t)Q * s->tp)) != cudaSuccess ||
+      (e = dalloc(&s->d_g2cnt, (size_t)Q * s->tp)) != cudaSuccess) {
+    xg_series_destroy(s);
+    return cuda_fail(c, e, "series alloc");
+  }
+  // padding columns of the ring-major rows must stay zero forever
+  e = cudaMemsetAsync(s->d_x, 0, (size_t)max_frames * L->ktot, c->stream);
+  if (e != cudaSuccess) {
+    xg_series_destroy(s);
+    return cuda_fail(c, e, "series memset");
+  }
+  *out = s;
+  return XG_OK;
+}
+
+void xg_series_destroy(xg_series* s) {
+  if (!s) return;
+  dfree(s->d_raster);
+  dfree(s->d_x);
+  dfree(s->d_norm2);
+  dfree(s->d_sum1);
+  dfree(s->d_maxc);
+  dfree(s->d_norms);
+  dfree(s->d_inv);
+  dfree(s->d_zero);
+  dfree(s->d_first_zero);
+  dfree(s->d_gram);
+  dfree(s->d_g2);
+  dfree(s->d_g2cnt);
+  dfree(s->d_g2part);
+  dfree(s->d_g2pcnt);
+  dfree(s->d_tiles);
+  delete s;
+}
+
+int64_t xg_series_frames(const xg_series* s) { return s ? s->t : -1; }
+
+int xg_series_load_frames(xg_series* s, const uint8_t* frames, int64_t n, int on_device) {
+  if (!s || !frames) return XG_ERR_INVALID;
+  xg_ctx* c = s->ctx;
+  const xg_layout* L = s->L;
+  if (n < 1 || n > s->tmax)
+    return fail(c, XG_ERR_SHAPE, "load_frames: %lld frames, capacity %lld", (long long)n,
+                (long long)s->tmax);
+  const uint8_t* src = frames;
+  if (!on_device) {
+    XG_CUDA(c, cudaMemcpyAsync(s->d_raster, frames, (size_t)n * L->pixels,
+                               cudaMemcpyHostToDevice, c->stream));
+    src = s->d_raster;
+  }
+  const size_t statn = (size_t)n * L->rings;
+  XG_CUDA(c, cudaMemsetAsync(s->d_norm2, 0, statn * 8, c->stream));
+  XG_CUDA(c, cudaMemsetAsync(s->d_sum1, 0, statn * 8, c->stream));
+  XG_CUDA(c, cudaMemsetAsync(s->d_maxc, 0, statn * 4, c->stream));
+  IngestParams p;
+  p.raster = src;
+  p.x = s->d_x;
+  p.pixels = L->pixels;
+  p.ktot = L->ktot;
+  p.band = L->band;
+  p.n_bands = L->n_bands;
+  p.n_rings = L->rings;
+  p.band_seg = L->d_band_seg;
+  p.segs = L->d_segs;
+  p.band_tab = L->d_band_tab;
+  p.tab = L->d_tab;
+  p.max_tab = L->max_tab;
+  p.t0 = 0;
+  p.n_frames = n;
+  // enough CTAs for ~4 waves of 148 SMs
+  const int64_t want = std::max<int64_t>(1, (int64_t)c->num_sms * 8 / std::max(1, L->n_bands));
+  p.frames_per_cta = static_cast<int32_t>(std::max<int64_t>(1, (n + want - 1) / want));
+  p.norm2 = s->d_norm2;
+  p.sum1 = s->d_sum1;
+  p.maxc = s->d_maxc;
+  XG_CUDA(c, launch_ingest(p, c->stream));
+  c->launches++;
+  s->t = n;
+  s->have_raw = false;
+  NormParams np;
+  np.norm2 = s->d_norm2;
+  np.n_frames = n;
+  np.ld = s->tp;
+  np.n_rings = L->rings;
+  np.norms = s->d_norms;
+  np.inv = s->d_inv;
+  np.zero_count = s->d_zero;
+  np.first_zero = s->d_first_zero;
+  np.err = c->d_err;
+  XG_CUDA(c, cudaMemsetAsync(s->d_zero, 0, (size_t)L->rings * 8, c->stream));
+  std::vector<int64_t> big(L->rings, INT64_MAX);
+  XG_CUDA(c, cudaMemcpyAsync(s->d_first_zero, big.data(), (size_t)L->rings * 8,
+                             cudaMemcpyHostToDevice, c->stream));
+  XG_CUDA(c, cudaStreamSynchronize(c->stream));  // `big` is pageable host memory
+  XG_CUDA(c, launch_norms(np, c->stream));
+  c->launches++;
+  return XG_OK;
+}
+
+static int build_tiles(xg_series* s) {
+  xg_ctx* c = s->ctx;
+  if (s->tiles_for_t == s->t) return XG_OK;
+  std::vector<TileDesc> tiles;
+  const int64_t nbi = (s->t + 127) / 128, nbj = (s->t + 255) / 256;
+  for (int32_t r = 0; r < s->L->rings; ++r)
+    for (int64_t ib = 0; ib < nbi; ++ib)
+      for (int64_t jb = (ib * 128) / 256; jb < nbj; ++jb) {
+        TileDesc d;
+        d.ring = r;
+        d.i0 = static_cast<int32_t>(ib * 128);
+        d.j0 = static_cast<int32_t>(jb * 256);
+        d.pad = 0;
+        tiles.push_back(d);
+      }
+  dfree(s->d_tiles);
+  XG_CUDA(c, dalloc(&s->d_tiles, tiles.size()));
+  XG_CUDA(c, cudaMemcpy(s->d_tiles, tiles.data(), tiles.size() * sizeof(TileDesc),
+                        cudaMemcpyHostToDevice));
+  s->ntiles = static_cast<int32_t>(tiles.size());
+  s->tiles_for_t = s->t;
+  return XG_OK;
+}
+
+static int run_g2(xg_series* s, int mode) {
+  xg_ctx* c = s->ctx;
+  const int32_t seg = 1024;
+  const int32_t nseg = static_cast<int32_t>((s->t + seg - 1) / seg);
+  const size_t need = (size_t)s->L->rings * nseg * s->t;
+  dfree(s->d_g2part);
+  dfree(s->d_g2pcnt);
+  XG_CUDA(c, dalloc(&s->d_g2part, need));
+  XG_CUDA(c, dalloc(&s->d_g2pcnt, need));
+  G2Params g;
+  g.gram = s->d_gram;
+  g.cf32 = nullptr;
+  g.ring_stride = s->tp * s->tp;
+  g.ld = static_cast<int32_t>(s->tp);
+  g.inv = s->d_inv;
+  g.inv_ld = s->tp;
+  g.n_frames = s->t;
+  g.n_rings = s->L->rings;
+  g.seg = seg;
+  g.n_seg = nseg;
+  g.partial = s->d_g2part;
+  g.pcount = s->d_g2pcnt;
+  g.g2 = s->d_g2;
+  g.counts = s->d_g2cnt;
+  g.g2_ld = s->tp;
+  XG_CUDA(c, launch_g2(g, mode, c->stream));
+  c->launches += 2;
+  return XG_OK;
+}
+
+int xg_ttc_raw(xg_series* s, uint32_t flags) {
+  if (!s) return XG_ERR_INVALID;
+  xg_ctx* c = s->ctx;
+  if (s->t < 2) return fail(c, XG_ERR_CONTRACT, "ttc_raw: need at least 2 frames");
+  const xg_layout* L = s->L;
+  if (flags & XG_STRICT) {
+    // reference semantics: first zero-norm frame raises (linalg.cpp:446-449)
+    std::vector<int64_t> fz(L->rings);
+    XG_CUDA(c, cudaMemcpyAsync(fz.data(), s->d_first_zero, fz.size() * 8,
+                               cudaMemcpyDeviceToHost, c->stream));
+    XG_CUDA(c, cudaStreamSynchronize(c->stream));
+    for (int32_t r = 0; r < L->rings; ++r)
+      if (fz[r] != INT64_MAX) {
+        c->payload = fz[r];
+        c->payload_ring = r;
+        return fail(c, XG_ERR_NORMALIZATION, "row_normalize: frame %lld of ring %d has zero norm",
+                    (long long)fz[r], r);
+      }
+  }
+  int rc = build_tiles(s);
+  if (rc) return rc;
+  CUtensorMap map;
+  rc = make_map_u8(c, &map, s->d_x, L->ktot, s->t, L->ktot, 128, 128);
+  if (rc) return rc;
+  GramParams gp;
+  gp.tiles = s->d_tiles;
+  gp.ntiles = s->ntiles;
+  gp.ring_koff = L->d_ring_koff;
+  gp.ring_nkb = L->d_ring_nkb;
+  gp.gram = s->d_gram;
+  gp.ring_stride = s->tp * s->tp;
+  gp.ld = static_cast<int32_t>(s->tp);
+  gp.err = c->d_err;
+  XG_CUDA(c, launch_gram_u8(map, gp, c->num_sms, c->stream));
+  c->launches++;
+  if (!(flags & XG_NO_G2)) {
+    rc = run_g2(s, 0);
+    if (rc) return rc;
+  }
+  s->have_raw = true;
+  return XG_OK;
+}
+
+int xg_series_get_ttc(xg_series* s, int32_t ring, int32_t dtype, void* out, int64_t ld,
+                      int out_on_device) {
+  if (!s || !out) return XG_ERR_INVALID;
+  xg_ctx* c = s->ctx;
+  if (ring < 0 || ring >= s->L->rings) return fail(c, XG_ERR_SHAPE, "ring %d out of range", ring);
+  if (!s->have_raw) return fail(c, XG_ERR_CONTRACT, "get_ttc: no TTC computed yet");
+  if (dtype < 0 || dtype > 2) return fail(c, XG_ERR_CONTRACT, "get_ttc: bad dtype");
+  if (ld < s->t) return fail(c, XG_ERR_SHAPE, "get_ttc: ld < n");
+  const size_t esz = dtype == 0 ? 8 : 4;
+  const size_t bytes = (size_t)s->t * ld * esz;
+  void* dst = out;
+  void* tmp = nullptr;
+  if (!out_on_device) {
+    XG_CUDA(c, cudaMalloc(&tmp, bytes));
+    dst = tmp;
+  }
+  ExpandParams p;
+  p.gram = s->d_gram + (int64_t)ring * s->tp * s->tp;
+  p.cf32 = nullptr;
+  p.ring_stride = 0;
+  p.ld = static_cast<int32_t>(s->tp);
+  p.inv = s->d_inv + (int64_t)ring * s->tp;
+  p.n = s->t;
+  p.out = dst;
+  p.out_ld = ld;
+  p.out_dtype = dtype;
+  cudaError_t e = launch_expand(p, 0, c->stream);
+  c->launches++;
+  if (e == cudaSuccess && tmp) {
+    e = cudaMemcpyAsync(out, tmp, bytes, cudaMemcpyDeviceToHost, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  }
+  if (tmp) cudaFree(tmp);
+  if (e != cudaSuccess) return cuda_fail(c, e, "get_ttc");
+  return check_device_error(c);
+}
+
+int xg_series_get_g2(xg_series* s, int32_t ring, double* values, int64_t* counts) {
+  if (!s || !values) return XG_ERR_INVALID;
+  xg_ctx* c = s->ctx;
+  if (ring < 0 || ring >= s->L->rings) return fail(c, XG_ERR_SHAPE, "ring %d out of range", ring);
+  if (!s->have_raw) return fail(c, XG_ERR_CONTRACT, "get_g2: no TTC computed yet");
+  XG_CUDA(c, cudaMemcpyAsync(values, s->d_g2 + (int64_t)ring * s->tp, (size_t)s->t * 8,
+                             cudaMemcpyDeviceToHost, c->stream));
+  if (counts)
+    XG_CUDA(c, cudaMemcpyAsync(counts, s->d_g2cnt + (int64_t)ring * s->tp, (size_t)s->t * 8,
+                               cudaMemcpyDeviceToHost, c->stream));
+  XG_CUDA(c, cudaStreamSynchronize(c->stream));
+  return check_device_error(c);
+}
+
+int xg_series_get_norms(xg_series* s, int32_t ring, double* norms, int64_t* n_zero) {
+  if (!s) return XG_ERR_INVALID;
+  xg_ctx* c = s->ctx;
+  if (ring < 0 || ring >= s->L->rings) return fail(c, XG_ERR_SHAPE, "ring %d out of range", ring);
+  if (norms)
+    XG_CUDA(c, cudaMemcpyAsync(norms, s->d_norms + (int64_t)ring * s->tp, (size_t)s->t * 8,
+                               cudaMemcpyDeviceToHost, c->stream));
+  if (n_zero)
+    XG_CUDA(c, cudaMemcpyAsync(n_zero, s->d_zero + ring, 8, cudaMemcpyDeviceToHost, c->stream));
+  XG_CUDA(c, cudaStreamSynchronize(c->stream));
+  return check_device_error(c);
+}
+
+}  // extern "C"

@@ -1,0 +1,117 @@
+// xg_kernels.h -- device-kernel launch interface shared by the host runtime
+// (xg_api.cu) and the kernel translation units.  Internal; not installed.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+namespace xg {
+
+// ---------------------------------------------------------------- K1 ingest
+// One "segment" = the pixels of one ring inside one detector band, padded to
+// a multiple of 16 bytes, written to a contiguous range of the ring-major row.
+struct Segment {
+  int32_t ring;
+  int32_t dst;     // byte column in the ring-major row (multiple of 16)
+  int32_t len;     // bytes incl. zero padding (multiple of 16)
+  int32_t taboff;  // offset of this segment's source table within its band
+};
+
+struct IngestParams {
+  const uint8_t* raster;     // n_frames x pixels (device)
+  uint8_t* x;                // n_frames x ktot ring-major (device)
+  int64_t pixels;
+  int64_t ktot;
+  int32_t band;              // pixels per band
+  int32_t n_bands;
+  int32_t n_rings;
+  const int32_t* band_seg;   // n_bands + 1 segment ranges
+  const Segment* segs;
+  const int32_t* band_tab;   // n_bands + 1 table ranges (u16 entries)
+  const uint16_t* tab;       // source offsets within the band, 0xFFFF = zero pad
+  int32_t max_tab;           // largest band table (entries)
+  int64_t t0;                // first frame index written
+  int64_t n_frames;
+  int32_t frames_per_cta;
+  int64_t* norm2;            // [frame][ring] sum of squares (exact)
+  int64_t* sum1;             // [frame][ring] sum of counts
+  int32_t* maxc;             // [frame][ring] max count
+};
+cudaError_t launch_ingest(const IngestParams& p, cudaStream_t s);
+
+// --------------------------------------------------------- per-ring norms
+// norms[r][t] = sqrt(norm2[t][r]), inv = 1/norms (0 for zero frames);
+// counts zero frames per ring and flags int32-Gram overflow (norm2 >= 2^31).
+struct NormParams {
+  const int64_t* norm2;
+  int64_t n_frames;
+  int64_t ld;                // frame stride of norms/inv (>= n_frames)
+  int32_t n_rings;
+  double* norms;             // [ring][ld]
+  double* inv;               // [ring][ld]
+  int64_t* zero_count;       // [ring]
+  int64_t* first_zero;       // [ring] smallest zero-norm frame (or INT64_MAX)
+  int* err;                  // bit 2: overflow
+};
+cudaError_t launch_norms(const NormParams& p, cudaStream_t s);
+
+// ------------------------------------------------------------ K2 raw Gram
+struct TileDesc {
+  int32_t ring;
+  int32_t i0;
+  int32_t j0;
+  int32_t pad;
+};
+struct GramParams {
+  const TileDesc* tiles;
+  int32_t ntiles;
+  const int32_t* ring_koff;  // byte column of each ring in the ring-major row
+  const int32_t* ring_nkb;   // 128-byte K blocks per ring
+  int32_t* gram;             // [ring][ld][ld] exact int32 Gram (upper tiles)
+  int64_t ring_stride;
+  int32_t ld;
+  int* err;                  // bit 0: pipeline timeout
+};
+size_t gram_u8_smem_bytes();
+cudaError_t launch_gram_u8(const CUtensorMap& tmX, const GramParams& p, int num_sms,
+                           cudaStream_t stream);
+
+// --------------------------------------------------------------- K7 g2
+// g2[r][d] = sum_{t} G(t,t+d) inv_t inv_{t+d} / count, ascending t within
+// segments of `seg` frames, segments combined in ascending order.
+struct G2Params {
+  const int32_t* gram;       // int32 Gram source (mode 0) ...
+  const float* cf32;         // ... or an already normalised f32 C (mode 1)
+  int64_t ring_stride;
+  int32_t ld;
+  const double* inv;         // [ring][inv_ld] (mode 0)
+  int64_t inv_ld;
+  int64_t n_frames;
+  int32_t n_rings;
+  int32_t seg;
+  int32_t n_seg;
+  double* partial;           // [ring][n_seg][n_frames]
+  int64_t* pcount;           // [ring][n_seg][n_frames]
+  double* g2;                // [ring][g2_ld]
+  int64_t* counts;           // [ring][g2_ld]
+  int64_t g2_ld;
+};
+cudaError_t launch_g2(const G2Params& p, int mode, cudaStream_t s);
+
+// ---------------------------------------------------- TTC readback expand
+struct ExpandParams {
+  const int32_t* gram;       // mode int: exact Gram, normalised with inv
+  const float* cf32;         // mode f32 source (already normalised)
+  int64_t ring_stride;
+  int32_t ld;
+  const double* inv;         // [n] for this ring
+  int64_t n;
+  void* out;
+  int64_t out_ld;
+  int32_t out_dtype;         // 0 f64, 1 f32, 2 i32 (raw Gram)
+};
+cudaError_t launch_expand(const ExpandParams& p, int src_mode, cudaStream_t s);
+
+}  // namespace xg

@@ -1,0 +1,75 @@
+"""Raw TTC parity on the GPU (K1 ingest + K2 tcgen05 int8 Gram + K7 g2)
+against the CPU oracle, through the C ABI.
+
+Bar: (i) the int32 Gram equals xpcs::gram(counts) bitwise;
+(ii) the normalised C is within 1e-12 abs of ttc_raw (reference tolerance,
+test_correlate.cpp:43); g2 within 1e-12 of g2_from_ttc(ttc_raw)."""
+import numpy as np
+import pytest
+
+import paper_2407_20356_b200 as xg
+
+pytestmark = pytest.mark.gpu
+
+
+def _data(orc, t, h, w, q, mu, seed):
+    frames = orc.gen_speckle(t, h, w, q, mu, seed)
+    ring, _ = orc.ring_map(h, w, q)
+    return frames, ring
+
+
+@pytest.mark.parametrize("t,h,w,q,mu,seed", [
+    (300, 64, 64, 8, 0.1, 11),     # partial 128/256 tiles
+    (64, 32, 48, 3, 0.5, 12),      # single tile, non-square detector
+    (520, 96, 96, 5, 0.08, 13),    # several tile rows/cols
+])
+def test_raw_gram_bitwise_and_ttc(ctx, orc, t, h, w, q, mu, seed):
+    frames, ring = _data(orc, t, h, w, q, mu, seed)
+    lay = xg.RingLayout.from_ring_map(ctx, ring, q)
+    s = xg.FrameSeries(lay, t).load(frames).ttc_raw()
+    for r in range(q):
+        idx = np.nonzero(ring == r)[0]
+        xq = frames[:, idx]
+        g_ref = orc.gram_u8(xq)
+        g_gpu = s.ttc(r, "gram")
+        assert np.array_equal(g_gpu.astype(np.int64), g_ref), f"ring {r}: int Gram mismatch"
+        c_gpu = s.ttc(r, "f64")
+        c_ref = orc.ttc_raw(xq.astype(np.float64))
+        assert np.abs(c_gpu - c_ref).max() <= 1e-12
+        assert np.array_equal(c_gpu, c_gpu.T)
+        _, g2_ref, cnt_ref = orc.g2_from_ttc(c_ref)
+        _, g2_gpu, cnt_gpu = s.g2(r)
+        assert np.array_equal(cnt_gpu, cnt_ref)
+        assert np.abs(g2_gpu - g2_ref).max() <= 1e-12
+        norms, nz = s.norms(r)
+        assert nz == 0
+        assert np.array_equal(norms, np.sqrt((xq.astype(np.float64) ** 2).sum(1)))
+
+
+def test_raw_against_reference_library(ctx, orc, ref):
+    """Same check against the UNMODIFIED reference (oracle/_ref)."""
+    t, h, w, q = 200, 48, 48, 4
+    frames, ring = _data(orc, t, h, w, q, 0.1, 21)
+    lay = xg.RingLayout.from_ring_map(ctx, ring, q)
+    s = xg.FrameSeries(lay, t).load(frames).ttc_raw()
+    for r in range(q):
+        xq = frames[:, ring == r].astype(np.float64)
+        assert np.array_equal(s.ttc(r, "gram").astype(np.float64), ref.gram(xq))
+        c_ref = ref.ttc_raw(xq)
+        assert np.abs(s.ttc(r, "f64") - c_ref).max() <= 1e-12
+
+
+def test_zero_frame_strict_and_flagged(ctx, orc):
+    t, h, w, q = 40, 16, 16, 2
+    frames, ring = _data(orc, t, h, w, q, 0.3, 5)
+    frames[7, ring == 0] = 0
+    lay = xg.RingLayout.from_ring_map(ctx, ring, q)
+    s = xg.FrameSeries(lay, t).load(frames)
+    with pytest.raises(xg.NormalizationError) as ei:
+        s.ttc_raw(strict=True)
+    assert ei.value.frame_index == 7 and ei.value.ring == 0
+    s.ttc_raw()
+    _, nz = s.norms(0)
+    assert nz == 1
+    _, _, cnt = s.g2(0)
+    assert cnt[0] == t - 1
