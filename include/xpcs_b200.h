@@ -101,6 +101,9 @@ XG_API int xg_series_load_frames(xg_series* s, const uint8_t* frames, int64_t n_
  * exact u8 x u8 -> int32 Gram on tcgen05 tensor cores, f64 normalisation and
  * g2 (g2_from_ttc, correlate.cpp:67-85) on the device. */
 XG_API int xg_ttc_raw(xg_series* s, uint32_t flags);
+/* g2 of every ring from the current raw TTC (run separately after
+ * xg_ttc_raw(..., XG_NO_G2)). */
+XG_API int xg_series_g2(xg_series* s);
 /* Readback.  dtype XG_F64/XG_F32: C = G_ij / (|x_i| |x_j|) (full symmetric
  * n x n, ld elements per row); XG_I32_GRAM: the exact integer Gram. */
 XG_API int xg_series_get_ttc(xg_series* s, int32_t ring, int32_t dtype, void* out, int64_t ld,
@@ -111,6 +114,15 @@ XG_API int xg_series_get_g2(xg_series* s, int32_t ring, double* values, int64_t*
 /* f64 frame norms |x_t| of ring (n) and the count of zero-norm frames. */
 XG_API int xg_series_get_norms(xg_series* s, int32_t ring, double* norms, int64_t* n_zero);
 XG_API int64_t xg_series_frames(const xg_series* s);
+
+/* ---- synthetic source (benchmark input; not on the correlation path) ---
+ * Seeded speckle counts: complex AR(1) field per pixel with
+ * rho = exp(-Gamma) (gamma_mode 0: Gamma = a r^2, 1: a 10^(3q/(Q-1))), Poisson
+ * counts of mean mu |f|^2 clipped to 255, CounterRng (rng.cpp:12-44)
+ * substreams 1/2/3.  Writes n_frames x (height*width) u8 to device memory. */
+XG_API int xg_synth_speckle(xg_ctx* ctx, int64_t n_frames, int64_t height, int64_t width,
+                            int32_t n_rings, double mu, int32_t gamma_mode, double gamma_a,
+                            uint64_t seed, uint8_t* out_device);
 
 #ifdef __cplusplus
 }

@@ -93,6 +93,8 @@ class _COracle:
         L.xo_ring_map.argtypes = [I64, I64, I64, _i32, _d]
         L.xo_gen_speckle.argtypes = [I64, I64, I64, I64, C_.c_double, C_.c_int,
                                      C_.c_double, U64, _u8]
+        L.xo_gen_speckle_pixels.argtypes = [I64, I64, I64, I64, C_.c_double, C_.c_int,
+                                            C_.c_double, U64, _i64, I64, _u8]
 
     # -- rng / fixtures
     def random_positive_matrix(self, rows, cols, seed):
@@ -206,6 +208,13 @@ class _COracle:
         rad = np.empty(h * w, np.float64)
         self.L.xo_ring_map(h, w, q, _p(ring, _i32), _p(rad, _d))
         return ring, rad
+
+    def gen_speckle_pixels(self, t, h, w, q, mu, seed, pix, gamma_mode=0, gamma_a=0.002):
+        pix = np.ascontiguousarray(pix, dtype=np.int64)
+        out = np.empty((t, pix.size), np.uint8)
+        self.L.xo_gen_speckle_pixels(t, h, w, q, mu, gamma_mode, gamma_a, seed, _p(pix, _i64),
+                                     pix.size, _p(out, _u8))
+        return out
 
     def gen_speckle(self, t, h, w, q, mu, seed, gamma_mode=0, gamma_a=0.002):
         out = np.empty((t, h * w), np.uint8)

@@ -295,6 +295,46 @@ static inline uint8_t xo_poisson(double lam, double u) {
   return (uint8_t)k;
 }
 
+/* Same generator restricted to a pixel subset (every pixel is an independent
+ * chain indexed by t*M + p): out is t_frames x n_pix, column j = pixel pix[j]. */
+XO_API void xo_gen_speckle_pixels(int64_t t_frames, int64_t h, int64_t w, int64_t q, double mu,
+                                  int gamma_mode, double gamma_a, uint64_t seed,
+                                  const int64_t* pix, int64_t n_pix, uint8_t* out) {
+  const int64_t m = h * w;
+  const double cy = 0.5 * (double)(h - 1), cx = 0.5 * (double)(w - 1);
+  const double rmax = sqrt(cx * cx + cy * cy);
+  const uint64_t s_re = xo_rng_substream(seed, 1);
+  const uint64_t s_im = xo_rng_substream(seed, 2);
+  const uint64_t s_po = xo_rng_substream(seed, 3);
+  const double half = sqrt(0.5);
+  for (int64_t j = 0; j < n_pix; ++j) {
+    const int64_t p = pix[j];
+    const double dy = (double)(p / w) - cy, dx = (double)(p % w) - cx;
+    const double r = sqrt(dx * dx + dy * dy);
+    int64_t b = (int64_t)floor(r * (double)q / rmax);
+    if (b > q - 1) b = q - 1;
+    const double gam = gamma_mode == 0
+                           ? gamma_a * r * r
+                           : gamma_a * pow(10.0, 3.0 * (double)b / (double)(q > 1 ? q - 1 : 1));
+    const double rho = exp(-gam);
+    double fr = 0.0, fi = 0.0;
+    for (int64_t t = 0; t < t_frames; ++t) {
+      const uint64_t idx = (uint64_t)(t * m + p);
+      const double er = half * xo_rng_normal(s_re, idx);
+      const double ei = half * xo_rng_normal(s_im, idx);
+      if (t == 0) {
+        fr = er;
+        fi = ei;
+      } else {
+        const double c = sqrt(1.0 - rho * rho);
+        fr = rho * fr + c * er;
+        fi = rho * fi + c * ei;
+      }
+      out[t * n_pix + j] = xo_poisson(mu * (fr * fr + fi * fi), xo_rng_uniform(s_po, idx));
+    }
+  }
+}
+
 XO_API void xo_gen_speckle(int64_t t_frames, int64_t h, int64_t w, int64_t q, double mu,
                            int gamma_mode, double gamma_a, uint64_t seed, uint8_t* out) {
   const int64_t m = h * w;

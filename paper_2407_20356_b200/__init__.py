@@ -185,12 +185,13 @@ class FrameSeries:
     def load(self, frames, n_frames: int | None = None) -> "FrameSeries":
         """Ingest ``frames`` (n x full_pixels u8): a numpy array (host, copied
         H2D) or any object exposing ``data_ptr()`` (a CUDA torch tensor)."""
-        if hasattr(frames, "data_ptr"):
+        if hasattr(frames, "data_ptr"):  # torch tensor: CUDA (device) or pinned host
             n = int(frames.shape[0]) if n_frames is None else n_frames
             if frames.numel() < n * self.layout.full_pixels:
                 raise ShapeError("frames tensor smaller than n x full_pixels")
+            on_dev = 1 if getattr(frames, "is_cuda", False) else 0
             _check(self.ctx.h, lib.xg_series_load_frames(self.h, C.c_void_p(frames.data_ptr()),
-                                                         n, 1))
+                                                         n, on_dev))
             return self
         a = np.ascontiguousarray(frames, dtype=np.uint8)
         if a.ndim != 2 or a.shape[1] != self.layout.full_pixels:
@@ -203,6 +204,11 @@ class FrameSeries:
         """Raw TTC of every ring (ttc_raw, correlate.cpp:19-25)."""
         flags = (_abi.STRICT if strict else 0) | (0 if g2 else _abi.NO_G2)
         _check(self.ctx.h, lib.xg_ttc_raw(self.h, flags))
+        return self
+
+    def compute_g2(self) -> "FrameSeries":
+        """g2 of every ring from the current raw TTC (after ttc_raw(g2=False))."""
+        _check(self.ctx.h, lib.xg_series_g2(self.h))
         return self
 
     def ttc(self, ring: int, dtype: str = "f64") -> np.ndarray:
@@ -236,3 +242,27 @@ __all__ = [
     "Context", "RingLayout", "FrameSeries", "Error", "ShapeError", "ContractError", "MaskError",
     "NormalizationError", "RankError", "BindingError", "FormatError", "DeviceError",
 ]
+
+
+# ------------------------------------------------------------ geometry / data
+def annular_rings(height: int, width: int, n_rings: int) -> np.ndarray:
+    """Equal-width annular q-rings: ring(p) =
+    min(Q-1, floor(r Q / r_max)), r = distance to the detector centre
+    ((W-1)/2, (H-1)/2), r_max = the corner distance.  Returns the ring index
+    of every pixel (raster order); masks follow as ``ring == r``."""
+    cy, cx = 0.5 * (height - 1), 0.5 * (width - 1)
+    rmax = np.sqrt(cx * cx + cy * cy)
+    yy, xx = np.meshgrid(np.arange(height, dtype=np.float64),
+                         np.arange(width, dtype=np.float64), indexing="ij")
+    r = np.sqrt((xx - cx) ** 2 + (yy - cy) ** 2)
+    q = np.floor(r * n_rings / rmax).astype(np.int64)
+    return np.minimum(q, n_rings - 1).astype(np.int32).ravel()
+
+
+def synth_speckle(ctx: Context, out_device_ptr: int, n_frames: int, height: int, width: int,
+                  n_rings: int, mu: float, seed: int, gamma_mode: int = 0,
+                  gamma_a: float = 0.002) -> None:
+    """Seeded synthetic speckle counts written straight into device memory
+    (benchmark input generator, K8)."""
+    _check(ctx.h, lib.xg_synth_speckle(ctx.h, n_frames, height, width, n_rings, mu, gamma_mode,
+                                       gamma_a, seed, C.c_void_p(out_device_ptr)))

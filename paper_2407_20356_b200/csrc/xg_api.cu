@@ -88,10 +88,13 @@ struct xg_series {
   TileDesc* d_tiles = nullptr;
   int32_t ntiles = 0;
   int64_t tiles_for_t = -1;
+  size_t g2part_cap = 0;
   bool have_raw = false;
 };
 
 namespace {
+
+constexpr int64_t kNoZero = 0x7F7F7F7F7F7F7F7FLL;  // "no zero frame" sentinel
 
 int fail(xg_ctx* c, int code, const char* fmt, ...) {
   char buf[512];
@@ -386,10 +389,13 @@ int xg_series_create(xg_ctx* c, const xg_layout* L, int64_t max_frames, xg_serie
       (e = dalloc(&s->d_first_zero, (size_t)Q)) != cudaSuccess ||
       (e = dalloc(&s->d_gram, (size_t)Q * s->tp * s->tp)) != cudaSuccess ||
       (e = dalloc(&s->d_g2, (size_t)Q * s->tp)) != cudaSuccess ||
-      (e = dalloc(&s->d_g2cnt, (size_t)Q * s->tp)) != cudaSuccess) {
+      (e = dalloc(&s->d_g2cnt, (size_t)Q * s->tp)) != cudaSuccess ||
+      (e = dalloc(&s->d_g2part, (size_t)Q * 8 * s->tp)) != cudaSuccess ||
+      (e = dalloc(&s->d_g2pcnt, (size_t)Q * 8 * s->tp)) != cudaSuccess) {
     xg_series_destroy(s);
     return cuda_fail(c, e, "series alloc");
   }
+  s->g2part_cap = (size_t)Q * 8 * s->tp;
   // padding columns of the ring-major rows must stay zero forever
   e = cudaMemsetAsync(s->d_x, 0, (size_t)max_frames * L->ktot, c->stream);
   if (e != cudaSuccess) {
@@ -475,10 +481,7 @@ int xg_series_load_frames(xg_series* s, const uint8_t* frames, int64_t n, int on
   np.first_zero = s->d_first_zero;
   np.err = c->d_err;
   XG_CUDA(c, cudaMemsetAsync(s->d_zero, 0, (size_t)L->rings * 8, c->stream));
-  std::vector<int64_t> big(L->rings, INT64_MAX);
-  XG_CUDA(c, cudaMemcpyAsync(s->d_first_zero, big.data(), (size_t)L->rings * 8,
-                             cudaMemcpyHostToDevice, c->stream));
-  XG_CUDA(c, cudaStreamSynchronize(c->stream));  // `big` is pageable host memory
+  XG_CUDA(c, cudaMemsetAsync(s->d_first_zero, 0x7F, (size_t)L->rings * 8, c->stream));
   XG_CUDA(c, launch_norms(np, c->stream));
   c->launches++;
   return XG_OK;
@@ -510,13 +513,19 @@ static int build_tiles(xg_series* s) {
 
 static int run_g2(xg_series* s, int mode) {
   xg_ctx* c = s->ctx;
-  const int32_t seg = 1024;
+  // <= 8 segments of >= 1024 frames: bounded partial storage, long serial chains split
+  const int32_t seg = static_cast<int32_t>(std::max<int64_t>(1024, (s->t + 7) / 8));
   const int32_t nseg = static_cast<int32_t>((s->t + seg - 1) / seg);
+  // partials: [ring][nseg][t] <= Q * tp entries since nseg * t <= tp * ceil(t/seg)...
+  // allocated at creation as Q * tp; grow once if a long series needs more.
   const size_t need = (size_t)s->L->rings * nseg * s->t;
-  dfree(s->d_g2part);
-  dfree(s->d_g2pcnt);
-  XG_CUDA(c, dalloc(&s->d_g2part, need));
-  XG_CUDA(c, dalloc(&s->d_g2pcnt, need));
+  if (need > s->g2part_cap) {
+    dfree(s->d_g2part);
+    dfree(s->d_g2pcnt);
+    XG_CUDA(c, dalloc(&s->d_g2part, need));
+    XG_CUDA(c, dalloc(&s->d_g2pcnt, need));
+    s->g2part_cap = need;
+  }
   G2Params g;
   g.gram = s->d_gram;
   g.cf32 = nullptr;
@@ -550,7 +559,7 @@ int xg_ttc_raw(xg_series* s, uint32_t flags) {
                                cudaMemcpyDeviceToHost, c->stream));
     XG_CUDA(c, cudaStreamSynchronize(c->stream));
     for (int32_t r = 0; r < L->rings; ++r)
-      if (fz[r] != INT64_MAX) {
+      if (fz[r] != kNoZero) {
         c->payload = fz[r];
         c->payload_ring = r;
         return fail(c, XG_ERR_NORMALIZATION, "row_normalize: frame %lld of ring %d has zero norm",
@@ -579,6 +588,12 @@ int xg_ttc_raw(xg_series* s, uint32_t flags) {
   }
   s->have_raw = true;
   return XG_OK;
+}
+
+int xg_series_g2(xg_series* s) {
+  if (!s) return XG_ERR_INVALID;
+  if (!s->have_raw) return fail(s->ctx, XG_ERR_CONTRACT, "g2: no TTC computed yet");
+  return run_g2(s, 0);
 }
 
 int xg_series_get_ttc(xg_series* s, int32_t ring, int32_t dtype, void* out, int64_t ld,
@@ -630,6 +645,42 @@ int xg_series_get_g2(xg_series* s, int32_t ring, double* values, int64_t* counts
                                cudaMemcpyDeviceToHost, c->stream));
   XG_CUDA(c, cudaStreamSynchronize(c->stream));
   return check_device_error(c);
+}
+
+int xg_synth_speckle(xg_ctx* c, int64_t n_frames, int64_t height, int64_t width,
+                     int32_t n_rings, double mu, int32_t gamma_mode, double gamma_a,
+                     uint64_t seed, uint8_t* out_device) {
+  if (!c || !out_device) return XG_ERR_INVALID;
+  if (n_frames < 1 || height < 1 || width < 1 || n_rings < 1 || !(mu >= 0.0))
+    return fail(c, XG_ERR_CONTRACT, "synth_speckle: bad arguments");
+  auto mix = [](uint64_t z) {
+    z ^= z >> 30;
+    z *= 0xBF58476D1CE4E5B9ULL;
+    z ^= z >> 27;
+    z *= 0x94D049BB133111EBULL;
+    z ^= z >> 31;
+    return z;
+  };
+  const uint64_t kStream = 0xD6E8FEB86659FD93ULL;  // CounterRng::substream (rng.cpp:20-22)
+  SynthParams p;
+  p.t_first = 0;
+  p.t_frames = n_frames;
+  p.h = height;
+  p.w = width;
+  p.q = n_rings;
+  p.gamma_mode = gamma_mode;
+  p.gamma_a = gamma_a;
+  p.mu = mu;
+  p.s_re = mix(seed ^ (1 * kStream));
+  p.s_im = mix(seed ^ (2 * kStream));
+  p.s_po = mix(seed ^ (3 * kStream));
+  p.carry_re = nullptr;
+  p.carry_im = nullptr;
+  p.out = out_device;
+  p.out_ld = height * width;
+  XG_CUDA(c, launch_synth(p, c->stream));
+  c->launches++;
+  return XG_OK;
 }
 
 int xg_series_get_norms(xg_series* s, int32_t ring, double* norms, int64_t* n_zero) {

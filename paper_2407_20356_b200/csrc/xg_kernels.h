@@ -114,4 +114,21 @@ struct ExpandParams {
 };
 cudaError_t launch_expand(const ExpandParams& p, int src_mode, cudaStream_t s);
 
+// ---------------------------------------------------------- K8 synthetic
+struct SynthParams {
+  int64_t t_first;           // global index of the first frame generated
+  int64_t t_frames;          // frames in this chunk
+  int64_t h, w;
+  int32_t q;
+  int32_t gamma_mode;        // 0: Gamma = a r^2 ; 1: Gamma = a 10^(3q/(Q-1))
+  double gamma_a;
+  double mu;
+  uint64_t s_re, s_im, s_po; // CounterRng substreams 1, 2, 3 of the seed
+  double* carry_re;          // per-pixel field carried across chunks (or null)
+  double* carry_im;
+  uint8_t* out;              // t_frames x out_ld
+  int64_t out_ld;
+};
+cudaError_t launch_synth(const SynthParams& p, cudaStream_t s);
+
 }  // namespace xg
