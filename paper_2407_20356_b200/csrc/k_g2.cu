@@ -113,7 +113,57 @@ __global__ void k_expand(ExpandParams p, int src_mode) {
   }
 }
 
+// Fold of the K2 epilogue's per-tile diagonal sums (fused g2).  For lag d
+// the contributing tiles are those with 128 * (2 jb - ib) in [d-255, d+127];
+// they are visited in ascending (delta, ib) order, so the sum order is fixed.
+__global__ void k_g2_fold(G2FoldParams p) {
+  const int64_t d = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int r = blockIdx.y;
+  if (d >= p.n_frames) return;
+  const double* part = p.g2_partial + static_cast<int64_t>(r) * p.tiles_per_ring * 384;
+  double acc = 0.0;
+  // delta range: ceil((d-255)/128) .. floor((d+127)/128)
+  const int64_t dlo = (d - 255 >= 0) ? (d - 255 + 127) / 128 : -((255 - d) / 128);
+  const int64_t dhi = (d + 127) / 128;
+  for (int64_t delta = dlo; delta <= dhi; ++delta) {
+    const int dl = static_cast<int>(d - 128 * delta + 127);
+    if (dl < 0 || dl >= 383) continue;
+    int ib = static_cast<int>(((delta % 2) + 2) % 2);  // (delta + ib) even
+    for (; ib < p.nbi; ib += 2) {
+      const int64_t jb = (delta + ib) / 2;
+      if (jb < ib / 2) continue;
+      if (jb >= p.nbj) break;
+      const int64_t tile = p.ib_tile_off[ib] + (jb - ib / 2);
+      acc += part[tile * 384 + dl];
+    }
+  }
+  // valid pairs: sum_t nz(t) nz(t+d), t <= T-1-d
+  const uint32_t* W = p.nz_bits + static_cast<int64_t>(r) * p.nz_words;
+  int64_t cnt = 0;
+  const int64_t last = p.n_frames - 1 - d;
+  for (int i = 0; i < p.nz_words; ++i) {
+    const int64_t t0 = 32ll * i;
+    if (t0 > last) break;
+    const int64_t sft = t0 + d;
+    const int w0 = static_cast<int>(sft >> 5), sh = static_cast<int>(sft & 31);
+    const uint32_t lo = w0 < p.nz_words ? W[w0] : 0u;
+    const uint32_t hi = w0 + 1 < p.nz_words ? W[w0 + 1] : 0u;
+    uint32_t m = W[i] & __funnelshift_r(lo, hi, sh);
+    const int64_t lim = last - t0;
+    if (lim < 31) m &= (2u << lim) - 1u;
+    cnt += __popc(m);
+  }
+  p.g2[r * p.g2_ld + d] = cnt > 0 ? acc / static_cast<double>(cnt) : 0.0;
+  p.counts[r * p.g2_ld + d] = cnt;
+}
+
 }  // namespace
+
+cudaError_t launch_g2_fold(const G2FoldParams& p, cudaStream_t s) {
+  dim3 grid(static_cast<unsigned>((p.n_frames + 127) / 128), p.n_rings);
+  k_g2_fold<<<grid, 128, 0, s>>>(p);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_g2(const G2Params& p, int mode, cudaStream_t s) {
   dim3 grid(static_cast<unsigned>((p.n_frames + 127) / 128), p.n_seg, p.n_rings);

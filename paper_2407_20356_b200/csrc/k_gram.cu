@@ -40,13 +40,26 @@ constexpr int TMEM_COLS = 512;             // 2 accumulators x 256 s32 columns
 constexpr int NUM_THREADS = 256;
 constexpr uint32_t IDESC = idesc_i8(BM, BN, false);
 
-struct __align__(8) GramSmemTail {
+constexpr int NDIAG = BM + BN - 1;         // tile diagonals j-i in [-127, 255]
+constexpr int NDIAG_PAD = 384;
+
+struct __align__(16) GramSmemTail {
   uint64_t full[STAGES];
   uint64_t empty[STAGES];
   uint64_t tfull[2];
   uint64_t tempty[2];
   uint32_t tmem_base;
+  uint32_t pad_;
+  // fused-g2 epilogue scratch
+  double inv_row[BM];                      // 1/|x_i| of the tile rows (0 beyond T / zero frame)
+  double inv_col[BN];                      // 1/|x_j| of the tile columns
+  double acc[4][NDIAG_PAD];                // per-warp diagonal sums of the tile
+  int32_t stage[4][32][33];                // per-warp 32x32 chunk of the Gram
 };
+
+__device__ __forceinline__ void epi_bar() {  // the 4 epilogue warps only
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+}
 
 }  // namespace
 
@@ -150,20 +163,42 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------- epilogue
+    // TMEM -> registers -> exact int32 Gram rows (global) and, when g2 is
+    // fused, the per-tile diagonal sums of C(i,j) = G_ij / (|x_i||x_j|) for
+    // j >= i: each 32x32 chunk goes through shared memory and lane L sums
+    // the chunk diagonals m = L-31 and m = L+1 in ascending row order; the
+    // four warps' tile sums are folded in warp order -> deterministic.
     const int sub = warp & 3;  // TMEM lane quarter this warp may access
     const int row = sub * 32 + lane;
+    const int etid = threadIdx.x - 128;
     int acc = 0;
     uint32_t acc_phase = 0;
+    bool ok = true;  // after a pipeline failure keep hitting the named barriers
     for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
       const TileDesc td = p.tiles[t];
-      if (!mbar_wait(&tail->tfull[acc], acc_phase, p.err)) break;
-      tc_fence_after();
+      if (ok) ok = mbar_wait(&tail->tfull[acc], acc_phase, p.err);
+      ok = __all_sync(0xffffffffu, ok);
+      if (ok) tc_fence_after();
+      if (p.g2_partial) {
+        epi_bar();  // previous tile's fold has finished with inv/acc
+        const double* inv = p.inv + static_cast<int64_t>(td.ring) * p.inv_ld;
+        for (int e = etid; e < BM + BN; e += 128) {
+          const int idx = e < BM ? td.i0 + e : td.j0 + (e - BM);
+          const double v = idx < p.n_frames ? inv[idx] : 0.0;
+          if (e < BM)
+            tail->inv_row[e] = v;
+          else
+            tail->inv_col[e - BM] = v;
+        }
+        for (int e = lane; e < NDIAG_PAD; e += 32) tail->acc[sub][e] = 0.0;
+        epi_bar();
+      }
       int32_t* gout = p.gram + static_cast<int64_t>(td.ring) * p.ring_stride +
                       static_cast<int64_t>(td.i0 + row) * p.ld + td.j0;
       const uint32_t tbase =
           tmem_base + static_cast<uint32_t>(acc * BN) + (static_cast<uint32_t>(sub * 32) << 16);
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = 0; ok && c < BN / 32; ++c) {
         uint32_t r[32];
         tmem_ld32(tbase + c * 32, r);
         tmem_ld_wait();
@@ -172,10 +207,46 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int v = 0; v < 8; ++v)
           dst[v] = make_int4(static_cast<int>(r[4 * v]), static_cast<int>(r[4 * v + 1]),
                              static_cast<int>(r[4 * v + 2]), static_cast<int>(r[4 * v + 3]));
+        if (p.g2_partial) {
+          int32_t(*S)[33] = tail->stage[sub];
+#pragma unroll
+          for (int k = 0; k < 32; ++k) S[lane][k] = static_cast<int32_t>(r[k]);
+          __syncwarp();
+          // global lag of chunk element (l, k): D0 + (k - l)
+          const int D0 = td.j0 + 32 * c - td.i0 - 32 * sub;
+          const double* ir = tail->inv_row + 32 * sub;
+          const double* ic = tail->inv_col + 32 * c;
+          double sa = 0.0, sb = 0.0;
+          const int ma = lane - 31;  // l in [31-lane, 31], k = l + ma
+          if (D0 + ma >= 0) {
+            for (int l = 31 - lane; l < 32; ++l)
+              sa += static_cast<double>(S[l][l + ma]) * (ir[l] * ic[l + ma]);
+          }
+          const int mb = lane + 1;   // l in [0, 30-lane], k = l + mb
+          if (lane < 31 && D0 + mb >= 0) {
+            for (int l = 0; l < 31 - lane; ++l)
+              sb += static_cast<double>(S[l][l + mb]) * (ir[l] * ic[l + mb]);
+          }
+          // tile diagonal index (j-i) + 127
+          const int base = 32 * c - 32 * sub + 127;
+          tail->acc[sub][base + ma] += sa;
+          if (lane < 31) tail->acc[sub][base + mb] += sb;
+          __syncwarp();
+        }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tail->tempty[acc]);
+      if (ok) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tail->tempty[acc]);  // TMEM buffer free for tile n+2
+      }
+      if (p.g2_partial) {
+        epi_bar();
+        if (ok) {
+          double* out = p.g2_partial + static_cast<int64_t>(t) * NDIAG_PAD;
+          for (int e = etid; e < NDIAG; e += 128)
+            out[e] = ((tail->acc[0][e] + tail->acc[1][e]) + tail->acc[2][e]) + tail->acc[3][e];
+        }
+      }
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;

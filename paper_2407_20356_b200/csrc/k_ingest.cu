@@ -4,15 +4,18 @@
 // the norm pass of `row_normalize` (src/linalg.cpp:441-456, the dot at :445):
 // one pass over the raw frames writes every q-ring's pixels (in mask order,
 // i.e. ascending pixel index) into its own 16-byte aligned column range of a
-// frame-major row, and accumulates per (frame, ring) the exact sum of squares
-// (|x_t|^2, integer), the sum and the max count.
+// frame-major row, and records per (frame, segment) the exact sum of squares
+// and sum of the counts.  K1b (k_norms) folds segments into per-(frame, ring)
+// norms in a fixed order -- no atomics anywhere, so the statistics are exact
+// and deterministic.
 //
-// HBM-bound: reads M bytes and writes ~M bytes per frame.  A CTA owns one
-// detector band (8192 pixels) and loops over frames: the band is staged in
-// shared memory with 16-byte loads, its gather table (u16 source offset per
-// output byte, padding = 0xFFFF) stays resident in shared memory, and each
-// warp emits whole ring segments with coalesced 4-byte-per-lane stores, so
-// the per-(frame, ring) statistics need one warp reduction per segment.
+// HBM-bound (reads M bytes, writes ~M bytes per frame).  A CTA owns one
+// detector band (8192 pixels) and a run of frames: band bytes are
+// double-buffered in shared memory with cp.async (next frame in flight while
+// the current one is permuted), the band's gather table (u16 source offset
+// per output byte, 0xFFFF = zero padding) stays resident in shared memory,
+// and each warp emits whole ring segments, 8 output bytes per lane per step,
+// as coalesced 256-byte warp stores.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -29,12 +32,25 @@ __device__ __forceinline__ uint32_t pick(const uint8_t* band, uint32_t e) {
   return e == 0xFFFFu ? 0u : static_cast<uint32_t>(band[e]);
 }
 
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 __global__ void __launch_bounds__(INGEST_THREADS)
     k_ingest(IngestParams p) {
   extern __shared__ uint4 ismem[];
   const int b = blockIdx.x;
-  uint8_t* band = reinterpret_cast<uint8_t*>(ismem);
-  uint16_t* tab = reinterpret_cast<uint16_t*>(band + ((p.band + 15) & ~15));
+  const int bstride = (p.band + 15) & ~15;
+  uint8_t* bufs = reinterpret_cast<uint8_t*>(ismem);  // 2 x bstride
+  uint16_t* tab = reinterpret_cast<uint16_t*>(bufs + 2 * bstride);
 
   const int tab0 = p.band_tab[b];
   const int ntab = p.band_tab[b + 1] - tab0;
@@ -43,65 +59,87 @@ __global__ void __launch_bounds__(INGEST_THREADS)
   const int seg0 = p.band_seg[b];
   const int nseg = p.band_seg[b + 1] - seg0;
   const int64_t pix0 = static_cast<int64_t>(b) * p.band;
-  const int64_t blen = (p.pixels - pix0) < p.band ? (p.pixels - pix0) : p.band;
+  const int blen = static_cast<int>((p.pixels - pix0) < p.band ? (p.pixels - pix0) : p.band);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nwarps = blockDim.x >> 5;
+  const bool vec = ((p.pixels | blen) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(p.raster) & 15) == 0;
 
   const int64_t f_begin = static_cast<int64_t>(blockIdx.y) * p.frames_per_cta;
   int64_t f_end = f_begin + p.frames_per_cta;
   if (f_end > p.n_frames) f_end = p.n_frames;
+  if (f_begin >= f_end) return;
 
-  for (int64_t f = f_begin; f < f_end; ++f) {
-    __syncthreads();  // previous frame fully consumed (and table loaded)
+  auto fetch = [&](int64_t f, uint8_t* dst) {
     const uint8_t* src = p.raster + f * p.pixels + pix0;
-    if (((reinterpret_cast<uintptr_t>(src) | blen) & 15) == 0) {
-      const uint4* s4 = reinterpret_cast<const uint4*>(src);
-      uint4* d4 = reinterpret_cast<uint4*>(band);
-      for (int i = threadIdx.x; i < blen / 16; i += blockDim.x) d4[i] = __ldcs(s4 + i);
+    if (vec) {
+      for (int i = threadIdx.x; i < blen / 16; i += blockDim.x) cp_async16(dst + 16 * i, src + 16 * i);
     } else {
-      for (int i = threadIdx.x; i < blen; i += blockDim.x) band[i] = src[i];
+      for (int i = threadIdx.x; i < blen; i += blockDim.x) dst[i] = src[i];
     }
-    __syncthreads();
+    cp_async_commit();
+  };
+
+  fetch(f_begin, bufs);
+  for (int64_t f = f_begin; f < f_end; ++f) {
+    uint8_t* band = bufs + ((f - f_begin) & 1) * bstride;
+    if (f + 1 < f_end) {
+      fetch(f + 1, bufs + ((f + 1 - f_begin) & 1) * bstride);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();  // band f (and the table) visible to every warp
 
     const int64_t t = p.t0 + f;
     uint8_t* xrow = p.x + t * p.ktot;
+    uint2* srow = p.seg_stats + t * p.n_segs + seg0;
     for (int s = warp; s < nseg; s += nwarps) {
       const Segment sg = p.segs[seg0 + s];
       const uint16_t* st = tab + sg.taboff;
-      uint32_t sq = 0, sm = 0, mx = 0;
-      for (int off = lane * 4; off < sg.len; off += 128) {
-        const uint2 e = *reinterpret_cast<const uint2*>(st + off);
+      uint32_t sq = 0, sm = 0;
+      for (int off = lane * 8; off < sg.len; off += 256) {
+        const uint4 e = *reinterpret_cast<const uint4*>(st + off);
         const uint32_t v0 = pick(band, e.x & 0xFFFFu), v1 = pick(band, e.x >> 16);
         const uint32_t v2 = pick(band, e.y & 0xFFFFu), v3 = pick(band, e.y >> 16);
-        *reinterpret_cast<uint32_t*>(xrow + sg.dst + off) = v0 | (v1 << 8) | (v2 << 16) | (v3 << 24);
-        sq += v0 * v0 + v1 * v1 + v2 * v2 + v3 * v3;
-        sm += v0 + v1 + v2 + v3;
-        mx = max(max(mx, max(v0, v1)), max(v2, v3));
+        const uint32_t v4 = pick(band, e.z & 0xFFFFu), v5 = pick(band, e.z >> 16);
+        const uint32_t v6 = pick(band, e.w & 0xFFFFu), v7 = pick(band, e.w >> 16);
+        uint2 w;
+        w.x = v0 | (v1 << 8) | (v2 << 16) | (v3 << 24);
+        w.y = v4 | (v5 << 8) | (v6 << 16) | (v7 << 24);
+        *reinterpret_cast<uint2*>(xrow + sg.dst + off) = w;
+        sq += v0 * v0 + v1 * v1 + v2 * v2 + v3 * v3 + v4 * v4 + v5 * v5 + v6 * v6 + v7 * v7;
+        sm += v0 + v1 + v2 + v3 + v4 + v5 + v6 + v7;
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         sq += __shfl_xor_sync(0xffffffffu, sq, o);
         sm += __shfl_xor_sync(0xffffffffu, sm, o);
-        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
       }
-      if (lane == 0 && sm != 0) {
-        const int64_t k = t * p.n_rings + sg.ring;
-        atomicAdd(reinterpret_cast<unsigned long long*>(p.norm2 + k), sq);
-        atomicAdd(reinterpret_cast<unsigned long long*>(p.sum1 + k), sm);
-        atomicMax(p.maxc + k, static_cast<int>(mx));
-      }
+      if (lane == 0) srow[s] = make_uint2(sq, sm);
     }
+    __syncthreads();  // everyone done with `band` before it is refilled
   }
 }
 
+// Per (frame, ring): fold the ring's segments in ascending band order.
 __global__ void k_norms(NormParams p) {
   const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int r = blockIdx.y;
   if (t >= p.n_frames) return;
-  const int64_t n2 = p.norm2[t * p.n_rings + r];
+  const uint2* srow = p.seg_stats + t * p.n_segs;
+  int64_t n2 = 0, s1 = 0;
+  for (int i = p.ring_seg_begin[r]; i < p.ring_seg_begin[r + 1]; ++i) {
+    const uint2 v = srow[p.ring_seg_list[i]];
+    n2 += v.x;
+    s1 += v.y;
+  }
+  p.norm2[t * p.n_rings + r] = n2;
+  p.sum1[t * p.n_rings + r] = s1;
   const double nrm = sqrt(static_cast<double>(n2));
   p.norms[r * p.ld + t] = nrm;
   p.inv[r * p.ld + t] = n2 > 0 ? 1.0 / nrm : 0.0;
+  if (n2 > 0) atomicOr(p.nz_bits + static_cast<int64_t>(r) * p.nz_words + (t >> 5), 1u << (t & 31));
   if (n2 == 0) {
     atomicAdd(reinterpret_cast<unsigned long long*>(p.zero_count + r), 1ull);
     atomicMin(reinterpret_cast<long long*>(p.first_zero + r), static_cast<long long>(t));
@@ -112,7 +150,8 @@ __global__ void k_norms(NormParams p) {
 }  // namespace
 
 cudaError_t launch_ingest(const IngestParams& p, cudaStream_t s) {
-  const size_t smem = ((p.band + 15) & ~15) + static_cast<size_t>(p.max_tab) * 2 + 16;
+  const size_t smem = 2 * static_cast<size_t>((p.band + 15) & ~15) +
+                      static_cast<size_t>(p.max_tab) * 2 + 16;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k_ingest, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));

@@ -63,6 +63,9 @@ struct xg_layout {
   uint16_t* d_tab = nullptr;
   int32_t* d_ring_koff = nullptr;
   int32_t* d_ring_nkb = nullptr;
+  int32_t n_segs = 0;
+  int32_t* d_ring_seg_begin = nullptr;
+  int32_t* d_ring_seg_list = nullptr;
 };
 
 struct xg_series {
@@ -75,7 +78,7 @@ struct xg_series {
   uint8_t* d_x = nullptr;
   int64_t* d_norm2 = nullptr;
   int64_t* d_sum1 = nullptr;
-  int32_t* d_maxc = nullptr;
+  uint2* d_seg_stats = nullptr;
   double* d_norms = nullptr;
   double* d_inv = nullptr;
   int64_t* d_zero = nullptr;
@@ -85,6 +88,11 @@ struct xg_series {
   int64_t* d_g2cnt = nullptr;
   double* d_g2part = nullptr;
   int64_t* d_g2pcnt = nullptr;
+  uint32_t* d_nz_bits = nullptr;   // [ring][nz_words] nonzero-frame bitmask
+  int32_t nz_words = 0;
+  double* d_g2tile = nullptr;      // [ntiles][384] fused-g2 tile diagonal sums
+  int32_t* d_ib_tile_off = nullptr;
+  int32_t tiles_per_ring = 0;
   TileDesc* d_tiles = nullptr;
   int32_t ntiles = 0;
   int64_t tiles_for_t = -1;
@@ -321,6 +329,15 @@ int xg_layout_create(xg_ctx* c, int64_t full_pixels, int32_t n_rings,
   }
   band_seg[nb] = static_cast<int32_t>(segs.size());
   band_tab[nb] = static_cast<int32_t>(tab.size());
+  L->n_segs = static_cast<int32_t>(segs.size());
+  // ring -> its segments in ascending band order (fixed fold order for norms)
+  std::vector<int32_t> rs_begin(n_rings + 1, 0), rs_list(segs.size());
+  for (const Segment& sg : segs) rs_begin[sg.ring + 1]++;
+  for (int32_t r = 0; r < n_rings; ++r) rs_begin[r + 1] += rs_begin[r];
+  {
+    std::vector<int32_t> fill(rs_begin.begin(), rs_begin.end() - 1);
+    for (size_t i = 0; i < segs.size(); ++i) rs_list[fill[segs[i].ring]++] = static_cast<int32_t>(i);
+  }
   std::vector<int32_t> rk(n_rings), rn(n_rings);
   for (int32_t r = 0; r < n_rings; ++r) {
     rk[r] = static_cast<int32_t>(L->koff[r]);
@@ -332,7 +349,9 @@ int xg_layout_create(xg_ctx* c, int64_t full_pixels, int32_t n_rings,
       (e = dalloc(&L->d_band_tab, band_tab.size())) != cudaSuccess ||
       (e = dalloc(&L->d_tab, tab.size())) != cudaSuccess ||
       (e = dalloc(&L->d_ring_koff, rk.size())) != cudaSuccess ||
-      (e = dalloc(&L->d_ring_nkb, rn.size())) != cudaSuccess) {
+      (e = dalloc(&L->d_ring_nkb, rn.size())) != cudaSuccess ||
+      (e = dalloc(&L->d_ring_seg_begin, rs_begin.size())) != cudaSuccess ||
+      (e = dalloc(&L->d_ring_seg_list, rs_list.size())) != cudaSuccess) {
     xg_layout_destroy(L);
     return cuda_fail(c, e, "layout alloc");
   }
@@ -341,7 +360,9 @@ int xg_layout_create(xg_ctx* c, int64_t full_pixels, int32_t n_rings,
   cudaMemcpy(L->d_band_tab, band_tab.data(), band_tab.size() * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(L->d_tab, tab.data(), tab.size() * 2, cudaMemcpyHostToDevice);
   cudaMemcpy(L->d_ring_koff, rk.data(), rk.size() * 4, cudaMemcpyHostToDevice);
-  e = cudaMemcpy(L->d_ring_nkb, rn.data(), rn.size() * 4, cudaMemcpyHostToDevice);
+  cudaMemcpy(L->d_ring_nkb, rn.data(), rn.size() * 4, cudaMemcpyHostToDevice);
+  cudaMemcpy(L->d_ring_seg_begin, rs_begin.data(), rs_begin.size() * 4, cudaMemcpyHostToDevice);
+  e = cudaMemcpy(L->d_ring_seg_list, rs_list.data(), rs_list.size() * 4, cudaMemcpyHostToDevice);
   if (e != cudaSuccess) {
     xg_layout_destroy(L);
     return cuda_fail(c, e, "layout upload");
@@ -358,6 +379,8 @@ void xg_layout_destroy(xg_layout* L) {
   dfree(L->d_tab);
   dfree(L->d_ring_koff);
   dfree(L->d_ring_nkb);
+  dfree(L->d_ring_seg_begin);
+  dfree(L->d_ring_seg_list);
   delete L;
 }
 
@@ -382,7 +405,7 @@ int xg_series_create(xg_ctx* c, const xg_layout* L, int64_t max_frames, xg_serie
       (e = dalloc(&s->d_x, (size_t)max_frames * L->ktot)) != cudaSuccess ||
       (e = dalloc(&s->d_norm2, (size_t)max_frames * Q)) != cudaSuccess ||
       (e = dalloc(&s->d_sum1, (size_t)max_frames * Q)) != cudaSuccess ||
-      (e = dalloc(&s->d_maxc, (size_t)max_frames * Q)) != cudaSuccess ||
+      (e = dalloc(&s->d_seg_stats, (size_t)max_frames * L->n_segs)) != cudaSuccess ||
       (e = dalloc(&s->d_norms, (size_t)s->tp * Q)) != cudaSuccess ||
       (e = dalloc(&s->d_inv, (size_t)s->tp * Q)) != cudaSuccess ||
       (e = dalloc(&s->d_zero, (size_t)Q)) != cudaSuccess ||
@@ -391,7 +414,8 @@ int xg_series_create(xg_ctx* c, const xg_layout* L, int64_t max_frames, xg_serie
       (e = dalloc(&s->d_g2, (size_t)Q * s->tp)) != cudaSuccess ||
       (e = dalloc(&s->d_g2cnt, (size_t)Q * s->tp)) != cudaSuccess ||
       (e = dalloc(&s->d_g2part, (size_t)Q * 8 * s->tp)) != cudaSuccess ||
-      (e = dalloc(&s->d_g2pcnt, (size_t)Q * 8 * s->tp)) != cudaSuccess) {
+      (e = dalloc(&s->d_g2pcnt, (size_t)Q * 8 * s->tp)) != cudaSuccess ||
+      (e = dalloc(&s->d_nz_bits, (size_t)Q * (s->tp / 32))) != cudaSuccess) {
     xg_series_destroy(s);
     return cuda_fail(c, e, "series alloc");
   }
@@ -412,7 +436,7 @@ void xg_series_destroy(xg_series* s) {
   dfree(s->d_x);
   dfree(s->d_norm2);
   dfree(s->d_sum1);
-  dfree(s->d_maxc);
+  dfree(s->d_seg_stats);
   dfree(s->d_norms);
   dfree(s->d_inv);
   dfree(s->d_zero);
@@ -423,6 +447,9 @@ void xg_series_destroy(xg_series* s) {
   dfree(s->d_g2part);
   dfree(s->d_g2pcnt);
   dfree(s->d_tiles);
+  dfree(s->d_nz_bits);
+  dfree(s->d_g2tile);
+  dfree(s->d_ib_tile_off);
   delete s;
 }
 
@@ -441,10 +468,6 @@ int xg_series_load_frames(xg_series* s, const uint8_t* frames, int64_t n, int on
                                cudaMemcpyHostToDevice, c->stream));
     src = s->d_raster;
   }
-  const size_t statn = (size_t)n * L->rings;
-  XG_CUDA(c, cudaMemsetAsync(s->d_norm2, 0, statn * 8, c->stream));
-  XG_CUDA(c, cudaMemsetAsync(s->d_sum1, 0, statn * 8, c->stream));
-  XG_CUDA(c, cudaMemsetAsync(s->d_maxc, 0, statn * 4, c->stream));
   IngestParams p;
   p.raster = src;
   p.x = s->d_x;
@@ -463,15 +486,19 @@ int xg_series_load_frames(xg_series* s, const uint8_t* frames, int64_t n, int on
   // enough CTAs for ~4 waves of 148 SMs
   const int64_t want = std::max<int64_t>(1, (int64_t)c->num_sms * 8 / std::max(1, L->n_bands));
   p.frames_per_cta = static_cast<int32_t>(std::max<int64_t>(1, (n + want - 1) / want));
-  p.norm2 = s->d_norm2;
-  p.sum1 = s->d_sum1;
-  p.maxc = s->d_maxc;
+  p.n_segs = L->n_segs;
+  p.seg_stats = s->d_seg_stats;
   XG_CUDA(c, launch_ingest(p, c->stream));
   c->launches++;
   s->t = n;
   s->have_raw = false;
   NormParams np;
+  np.seg_stats = s->d_seg_stats;
+  np.n_segs = L->n_segs;
+  np.ring_seg_begin = L->d_ring_seg_begin;
+  np.ring_seg_list = L->d_ring_seg_list;
   np.norm2 = s->d_norm2;
+  np.sum1 = s->d_sum1;
   np.n_frames = n;
   np.ld = s->tp;
   np.n_rings = L->rings;
@@ -479,6 +506,10 @@ int xg_series_load_frames(xg_series* s, const uint8_t* frames, int64_t n, int on
   np.inv = s->d_inv;
   np.zero_count = s->d_zero;
   np.first_zero = s->d_first_zero;
+  s->nz_words = static_cast<int32_t>((n + 31) / 32);
+  np.nz_bits = s->d_nz_bits;
+  np.nz_words = s->nz_words;
+  XG_CUDA(c, cudaMemsetAsync(s->d_nz_bits, 0, (size_t)L->rings * s->nz_words * 4, c->stream));
   np.err = c->d_err;
   XG_CUDA(c, cudaMemsetAsync(s->d_zero, 0, (size_t)L->rings * 8, c->stream));
   XG_CUDA(c, cudaMemsetAsync(s->d_first_zero, 0x7F, (size_t)L->rings * 8, c->stream));
@@ -502,10 +533,19 @@ static int build_tiles(xg_series* s) {
         d.pad = 0;
         tiles.push_back(d);
       }
+  // tile offset of each tile row within a ring (for the fixed-order g2 fold)
+  std::vector<int32_t> iboff(nbi + 1, 0);
+  for (int64_t ib = 0; ib < nbi; ++ib) iboff[ib + 1] = iboff[ib] + static_cast<int32_t>(nbj - ib / 2);
+  s->tiles_per_ring = iboff[nbi];
   dfree(s->d_tiles);
+  dfree(s->d_g2tile);
+  dfree(s->d_ib_tile_off);
   XG_CUDA(c, dalloc(&s->d_tiles, tiles.size()));
+  XG_CUDA(c, dalloc(&s->d_g2tile, tiles.size() * 384));
+  XG_CUDA(c, dalloc(&s->d_ib_tile_off, iboff.size()));
   XG_CUDA(c, cudaMemcpy(s->d_tiles, tiles.data(), tiles.size() * sizeof(TileDesc),
                         cudaMemcpyHostToDevice));
+  XG_CUDA(c, cudaMemcpy(s->d_ib_tile_off, iboff.data(), iboff.size() * 4, cudaMemcpyHostToDevice));
   s->ntiles = static_cast<int32_t>(tiles.size());
   s->tiles_for_t = s->t;
   return XG_OK;
@@ -580,11 +620,29 @@ int xg_ttc_raw(xg_series* s, uint32_t flags) {
   gp.ring_stride = s->tp * s->tp;
   gp.ld = static_cast<int32_t>(s->tp);
   gp.err = c->d_err;
+  const bool g2 = !(flags & XG_NO_G2);
+  gp.inv = s->d_inv;
+  gp.inv_ld = s->tp;
+  gp.n_frames = s->t;
+  gp.g2_partial = g2 ? s->d_g2tile : nullptr;
   XG_CUDA(c, launch_gram_u8(map, gp, c->num_sms, c->stream));
   c->launches++;
-  if (!(flags & XG_NO_G2)) {
-    rc = run_g2(s, 0);
-    if (rc) return rc;
+  if (g2) {
+    G2FoldParams f;
+    f.g2_partial = s->d_g2tile;
+    f.ib_tile_off = s->d_ib_tile_off;
+    f.tiles_per_ring = s->tiles_per_ring;
+    f.nbi = static_cast<int32_t>((s->t + 127) / 128);
+    f.nbj = static_cast<int32_t>((s->t + 255) / 256);
+    f.n_frames = s->t;
+    f.n_rings = L->rings;
+    f.nz_bits = s->d_nz_bits;
+    f.nz_words = s->nz_words;
+    f.g2 = s->d_g2;
+    f.counts = s->d_g2cnt;
+    f.g2_ld = s->tp;
+    XG_CUDA(c, launch_g2_fold(f, c->stream));
+    c->launches++;
   }
   s->have_raw = true;
   return XG_OK;

@@ -35,9 +35,8 @@ struct IngestParams {
   int64_t t0;                // first frame index written
   int64_t n_frames;
   int32_t frames_per_cta;
-  int64_t* norm2;            // [frame][ring] sum of squares (exact)
-  int64_t* sum1;             // [frame][ring] sum of counts
-  int32_t* maxc;             // [frame][ring] max count
+  int32_t n_segs;            // segments over all bands
+  uint2* seg_stats;          // [frame][segment] {sum of squares, sum} (exact)
 };
 cudaError_t launch_ingest(const IngestParams& p, cudaStream_t s);
 
@@ -45,14 +44,21 @@ cudaError_t launch_ingest(const IngestParams& p, cudaStream_t s);
 // norms[r][t] = sqrt(norm2[t][r]), inv = 1/norms (0 for zero frames);
 // counts zero frames per ring and flags int32-Gram overflow (norm2 >= 2^31).
 struct NormParams {
-  const int64_t* norm2;
+  const uint2* seg_stats;    // [frame][segment]
+  int32_t n_segs;
+  const int32_t* ring_seg_begin;  // CSR: segments of each ring, ascending band
+  const int32_t* ring_seg_list;
+  int64_t* norm2;            // [frame][ring] |x|^2 (exact)
+  int64_t* sum1;             // [frame][ring] sum of counts
   int64_t n_frames;
   int64_t ld;                // frame stride of norms/inv (>= n_frames)
   int32_t n_rings;
   double* norms;             // [ring][ld]
   double* inv;               // [ring][ld]
   int64_t* zero_count;       // [ring]
-  int64_t* first_zero;       // [ring] smallest zero-norm frame (or INT64_MAX)
+  int64_t* first_zero;       // [ring] smallest zero-norm frame (sentinel if none)
+  uint32_t* nz_bits;         // [ring][nz_words] nonzero-frame bitmask (pre-zeroed)
+  int32_t nz_words;
   int* err;                  // bit 2: overflow
 };
 cudaError_t launch_norms(const NormParams& p, cudaStream_t s);
@@ -73,8 +79,31 @@ struct GramParams {
   int64_t ring_stride;
   int32_t ld;
   int* err;                  // bit 0: pipeline timeout
+  // fused g2 (null g2_partial = off): per tile, the sums over each tile
+  // diagonal (j - i + 127 in [0, 383)) of C(i,j) = G_ij inv_i inv_j, j >= i
+  const double* inv;         // [ring][inv_ld]
+  int64_t inv_ld;
+  int64_t n_frames;
+  double* g2_partial;        // [ntiles][384]
 };
 size_t gram_u8_smem_bytes();
+
+// Fold the per-tile diagonal sums of K2 into g2[ring][d] (fixed order) and
+// count the valid (t, t+d) pairs from the nonzero-frame bitmask.
+struct G2FoldParams {
+  const double* g2_partial;  // [ntiles][384]
+  const int32_t* ib_tile_off;  // [nbi+1] tile offset of tile row ib within a ring
+  int32_t tiles_per_ring;
+  int32_t nbi, nbj;
+  int64_t n_frames;
+  int32_t n_rings;
+  const uint32_t* nz_bits;   // [ring][nz_words] bit t = frame t has nonzero norm
+  int32_t nz_words;
+  double* g2;                // [ring][g2_ld]
+  int64_t* counts;
+  int64_t g2_ld;
+};
+cudaError_t launch_g2_fold(const G2FoldParams& p, cudaStream_t s);
 cudaError_t launch_gram_u8(const CUtensorMap& tmX, const GramParams& p, int num_sms,
                            cudaStream_t stream);
 

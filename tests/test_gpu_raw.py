@@ -73,3 +73,22 @@ def test_zero_frame_strict_and_flagged(ctx, orc):
     assert nz == 1
     _, _, cnt = s.g2(0)
     assert cnt[0] == t - 1
+
+
+def test_fused_g2_matches_standalone_pass(ctx, orc):
+    """g2 from the K2 epilogue (per-tile diagonal sums + fold) equals the
+    independent standalone pass over the stored Gram to rounding, and both
+    hit the oracle."""
+    t, h, w, q = 700, 64, 64, 3
+    frames, ring = _data(orc, t, h, w, q, 0.1, 31)
+    lay = xg.RingLayout.from_ring_map(ctx, ring, q)
+    s = xg.FrameSeries(lay, t).load(frames).ttc_raw()
+    fused = [s.g2(r) for r in range(q)]
+    s.compute_g2()
+    for r in range(q):
+        _, v2, c2 = s.g2(r)
+        _, v1, c1 = fused[r]
+        assert np.array_equal(c1, c2)
+        assert np.abs(v1 - v2).max() <= 1e-13
+        c_ref = orc.ttc_raw(frames[:, ring == r].astype(np.float64))
+        assert np.abs(v1 - orc.g2_from_ttc(c_ref)[1]).max() <= 1e-12
