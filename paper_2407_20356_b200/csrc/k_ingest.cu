@@ -11,8 +11,8 @@
 //
 // HBM-bound (reads M bytes, writes ~M bytes per frame).  A CTA owns one
 // detector band (8192 pixels) and a run of frames: band bytes are
-// double-buffered in shared memory with cp.async (next frame in flight while
-// the current one is permuted), the band's gather table (u16 source offset
+// streamed into a 4-deep ring of shared-memory buffers by TMA bulk copies
+// (cp.async.bulk + mbarrier: 4 frames in flight per CTA), the band's gather table (u16 source offset
 // per output byte, 0xFFFF = zero padding) stays resident in shared memory,
 // and each warp emits whole ring segments, 8 output bytes per lane per step,
 // as coalesced 256-byte warp stores.
@@ -27,34 +27,31 @@ namespace xg {
 namespace {
 
 constexpr int INGEST_THREADS = 256;
+constexpr int NBUF = 4;  // frames in flight per CTA
 
-__device__ __forceinline__ uint32_t pick(const uint8_t* band, uint32_t e) {
-  return e == 0xFFFFu ? 0u : static_cast<uint32_t>(band[e]);
-}
-
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
-                   static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
-               "l"(src)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
 __global__ void __launch_bounds__(INGEST_THREADS)
     k_ingest(IngestParams p) {
   extern __shared__ uint4 ismem[];
+  __shared__ __align__(8) uint64_t full[NBUF];
   const int b = blockIdx.x;
-  const int bstride = (p.band + 15) & ~15;
-  uint8_t* bufs = reinterpret_cast<uint8_t*>(ismem);  // 2 x bstride
-  uint16_t* tab = reinterpret_cast<uint16_t*>(bufs + 2 * bstride);
+  // band buffer stride: band bytes + 16 zero bytes (padding entries point there)
+  const int bstride = ((p.band + 15) & ~15) + 16;
+  uint8_t* bufs = reinterpret_cast<uint8_t*>(ismem);  // NBUF x bstride
+  uint16_t* tab = reinterpret_cast<uint16_t*>(bufs + NBUF * bstride);
 
   const int tab0 = p.band_tab[b];
   const int ntab = p.band_tab[b + 1] - tab0;
-  for (int i = threadIdx.x; i < ntab; i += blockDim.x) tab[i] = p.tab[tab0 + i];
+  const int zero_at = bstride - 16;
+  for (int i = threadIdx.x; i < ntab; i += blockDim.x) {
+    const uint16_t e = p.tab[tab0 + i];
+    tab[i] = e == 0xFFFFu ? static_cast<uint16_t>(zero_at) : e;
+  }
+  if (threadIdx.x < NBUF * 4)
+    reinterpret_cast<uint32_t*>(bufs + (threadIdx.x >> 2) * bstride + zero_at)[threadIdx.x & 3] = 0;
 
   const int seg0 = p.band_seg[b];
   const int nseg = p.band_seg[b + 1] - seg0;
@@ -62,34 +59,63 @@ __global__ void __launch_bounds__(INGEST_THREADS)
   const int blen = static_cast<int>((p.pixels - pix0) < p.band ? (p.pixels - pix0) : p.band);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nwarps = blockDim.x >> 5;
-  const bool vec = ((p.pixels | blen) & 15) == 0 &&
-                   (reinterpret_cast<uintptr_t>(p.raster) & 15) == 0;
+  const bool bulk = ((p.pixels | blen) & 15) == 0 &&
+                    (reinterpret_cast<uintptr_t>(p.raster) & 15) == 0;
 
   const int64_t f_begin = static_cast<int64_t>(blockIdx.y) * p.frames_per_cta;
   int64_t f_end = f_begin + p.frames_per_cta;
   if (f_end > p.n_frames) f_end = p.n_frames;
   if (f_begin >= f_end) return;
+  const int64_t nf = f_end - f_begin;
 
-  auto fetch = [&](int64_t f, uint8_t* dst) {
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NBUF; ++i)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&full[i])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  // one thread streams band bytes of frame f into buffer f % NBUF (TMA bulk copy)
+  auto issue = [&](int64_t f) {
+    const int slot = static_cast<int>((f - f_begin) % NBUF);
+    uint8_t* dst = bufs + slot * bstride;
     const uint8_t* src = p.raster + f * p.pixels + pix0;
-    if (vec) {
-      for (int i = threadIdx.x; i < blen / 16; i += blockDim.x) cp_async16(dst + 16 * i, src + 16 * i);
-    } else {
-      for (int i = threadIdx.x; i < blen; i += blockDim.x) dst[i] = src[i];
+    if (bulk) {
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                       smem_addr(&full[slot])),
+                   "r"(blen)
+                   : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              smem_addr(dst)),
+          "l"(src), "r"(blen), "r"(smem_addr(&full[slot]))
+          : "memory");
     }
-    cp_async_commit();
   };
+  if (bulk && threadIdx.x == 0)
+    for (int64_t f = f_begin; f < f_begin + NBUF && f < f_end; ++f) issue(f);
 
-  fetch(f_begin, bufs);
-  for (int64_t f = f_begin; f < f_end; ++f) {
-    uint8_t* band = bufs + ((f - f_begin) & 1) * bstride;
-    if (f + 1 < f_end) {
-      fetch(f + 1, bufs + ((f + 1 - f_begin) & 1) * bstride);
-      cp_async_wait<1>();
+  for (int64_t i = 0; i < nf; ++i) {
+    const int64_t f = f_begin + i;
+    const int slot = static_cast<int>(i % NBUF);
+    uint8_t* band = bufs + slot * bstride;
+    if (bulk) {
+      const uint32_t parity = static_cast<uint32_t>((i / NBUF) & 1);
+      uint32_t ok = 0;
+      while (!ok) {
+        asm volatile(
+            "{\n\t.reg .pred P;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, P;\n\t}"
+            : "=r"(ok)
+            : "r"(smem_addr(&full[slot])), "r"(parity)
+            : "memory");
+      }
     } else {
-      cp_async_wait<0>();
+      const uint8_t* src = p.raster + f * p.pixels + pix0;
+      for (int k = threadIdx.x; k < blen; k += blockDim.x) band[k] = src[k];
+      __syncthreads();
     }
-    __syncthreads();  // band f (and the table) visible to every warp
 
     const int64_t t = p.t0 + f;
     uint8_t* xrow = p.x + t * p.ktot;
@@ -100,10 +126,10 @@ __global__ void __launch_bounds__(INGEST_THREADS)
       uint32_t sq = 0, sm = 0;
       for (int off = lane * 8; off < sg.len; off += 256) {
         const uint4 e = *reinterpret_cast<const uint4*>(st + off);
-        const uint32_t v0 = pick(band, e.x & 0xFFFFu), v1 = pick(band, e.x >> 16);
-        const uint32_t v2 = pick(band, e.y & 0xFFFFu), v3 = pick(band, e.y >> 16);
-        const uint32_t v4 = pick(band, e.z & 0xFFFFu), v5 = pick(band, e.z >> 16);
-        const uint32_t v6 = pick(band, e.w & 0xFFFFu), v7 = pick(band, e.w >> 16);
+        const uint32_t v0 = band[e.x & 0xFFFFu], v1 = band[e.x >> 16];
+        const uint32_t v2 = band[e.y & 0xFFFFu], v3 = band[e.y >> 16];
+        const uint32_t v4 = band[e.z & 0xFFFFu], v5 = band[e.z >> 16];
+        const uint32_t v6 = band[e.w & 0xFFFFu], v7 = band[e.w >> 16];
         uint2 w;
         w.x = v0 | (v1 << 8) | (v2 << 16) | (v3 << 24);
         w.y = v4 | (v5 << 8) | (v6 << 16) | (v7 << 24);
@@ -118,7 +144,8 @@ __global__ void __launch_bounds__(INGEST_THREADS)
       }
       if (lane == 0) srow[s] = make_uint2(sq, sm);
     }
-    __syncthreads();  // everyone done with `band` before it is refilled
+    __syncthreads();  // every warp is done with this buffer
+    if (bulk && threadIdx.x == 0 && f + NBUF < f_end) issue(f + NBUF);
   }
 }
 
@@ -150,7 +177,7 @@ __global__ void k_norms(NormParams p) {
 }  // namespace
 
 cudaError_t launch_ingest(const IngestParams& p, cudaStream_t s) {
-  const size_t smem = 2 * static_cast<size_t>((p.band + 15) & ~15) +
+  const size_t smem = NBUF * (static_cast<size_t>((p.band + 15) & ~15) + 16) +
                       static_cast<size_t>(p.max_tab) * 2 + 16;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k_ingest, cudaFuncAttributeMaxDynamicSharedMemorySize,

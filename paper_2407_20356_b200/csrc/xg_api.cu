@@ -483,8 +483,8 @@ int xg_series_load_frames(xg_series* s, const uint8_t* frames, int64_t n, int on
   p.max_tab = L->max_tab;
   p.t0 = 0;
   p.n_frames = n;
-  // enough CTAs for ~4 waves of 148 SMs
-  const int64_t want = std::max<int64_t>(1, (int64_t)c->num_sms * 8 / std::max(1, L->n_bands));
+  // one wave of ~4 resident CTAs per SM, each streaming a run of frames of one band
+  const int64_t want = std::max<int64_t>(1, (int64_t)c->num_sms * 4 / std::max(1, L->n_bands));
   p.frames_per_cta = static_cast<int32_t>(std::max<int64_t>(1, (n + want - 1) / want));
   p.n_segs = L->n_segs;
   p.seg_stats = s->d_seg_stats;
