@@ -68,8 +68,10 @@ size_t gram_u8_smem_bytes() { return 1024 + STAGES * STAGE_BYTES + sizeof(GramSm
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     k_gram_u8(const __grid_constant__ CUtensorMap tmX, GramParams p) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~static_cast<uintptr_t>(1023));
+  // 1024-byte alignment for the 128B-swizzle atoms; offsetting the shared
+  // array itself (not a uintptr_t round trip) keeps accesses in the shared
+  // state space (LDS/STS rather than generic LD/ST).
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * A_BYTES;
   GramSmemTail* tail = reinterpret_cast<GramSmemTail*>(smem + STAGES * STAGE_BYTES);
@@ -216,17 +218,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const int D0 = td.j0 + 32 * c - td.i0 - 32 * sub;
           const double* ir = tail->inv_row + 32 * sub;
           const double* ic = tail->inv_col + 32 * c;
-          double sa = 0.0, sb = 0.0;
-          const int ma = lane - 31;  // l in [31-lane, 31], k = l + ma
-          if (D0 + ma >= 0) {
-            for (int l = 31 - lane; l < 32; ++l)
-              sa += static_cast<double>(S[l][l + ma]) * (ir[l] * ic[l + ma]);
+          // Lane L sums chunk diagonals m_B = L+1 (rows l < 31-L) then
+          // m_A = L-31 (rows l >= 31-L): element (l, (l+L+1) mod 32) at step l,
+          // one warp-uniform 32-step loop, conflict-free rows of S.
+          double sa = 0.0, sb = 0.0, run = 0.0;
+          const int ma = lane - 31, mb = lane + 1;
+          const bool use_a = D0 + ma >= 0, use_b = lane < 31 && D0 + mb >= 0;
+#pragma unroll
+          for (int l = 0; l < 32; ++l) {
+            if (l == 31 - lane) {
+              sb = run;
+              run = 0.0;
+            }
+            const int k = (l + lane + 1) & 31;
+            run = fma(static_cast<double>(S[l][k]), ir[l] * ic[k], run);
           }
-          const int mb = lane + 1;   // l in [0, 30-lane], k = l + mb
-          if (lane < 31 && D0 + mb >= 0) {
-            for (int l = 0; l < 31 - lane; ++l)
-              sb += static_cast<double>(S[l][l + mb]) * (ir[l] * ic[l + mb]);
-          }
+          sa = run;
+          if (!use_a) sa = 0.0;
+          if (!use_b) sb = 0.0;
           // tile diagonal index (j-i) + 127
           const int base = 32 * c - 32 * sub + 127;
           tail->acc[sub][base + ma] += sa;

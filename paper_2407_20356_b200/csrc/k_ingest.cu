@@ -14,8 +14,9 @@
 // streamed into a 4-deep ring of shared-memory buffers by TMA bulk copies
 // (cp.async.bulk + mbarrier: 4 frames in flight per CTA), the band's gather table (u16 source offset
 // per output byte, 0xFFFF = zero padding) stays resident in shared memory,
-// and each warp emits whole ring segments, 8 output bytes per lane per step,
-// as coalesced 256-byte warp stores.
+// and each warp emits whole ring segments, 4 output bytes per lane per step,
+// as coalesced 128-byte warp stores.  Band pieces of 512 B sit at a 528 B
+// smem pitch so consecutive detector rows do not alias to the same banks.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -27,7 +28,14 @@ namespace xg {
 namespace {
 
 constexpr int INGEST_THREADS = 256;
-constexpr int NBUF = 4;  // frames in flight per CTA
+constexpr int NBUF = 4;      // frames in flight per CTA
+constexpr int PIECE = 512;   // band bytes per bulk copy
+constexpr int PITCH = 528;   // smem pitch of a piece: +16 B skews consecutive
+                             // 512-byte detector rows by 4 banks
+
+__host__ __device__ constexpr int band_stride(int band) {
+  return ((band + PIECE - 1) / PIECE) * PITCH + 16;  // + 16 zero bytes (padding source)
+}
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -38,8 +46,9 @@ __global__ void __launch_bounds__(INGEST_THREADS)
   extern __shared__ uint4 ismem[];
   __shared__ __align__(8) uint64_t full[NBUF];
   const int b = blockIdx.x;
-  // band buffer stride: band bytes + 16 zero bytes (padding entries point there)
-  const int bstride = ((p.band + 15) & ~15) + 16;
+  // band buffer: pieces of 512 B at a 528 B pitch, then 16 zero bytes that
+  // the padding entries of the table point to
+  const int bstride = band_stride(p.band);
   uint8_t* bufs = reinterpret_cast<uint8_t*>(ismem);  // NBUF x bstride
   uint16_t* tab = reinterpret_cast<uint16_t*>(bufs + NBUF * bstride);
 
@@ -47,11 +56,12 @@ __global__ void __launch_bounds__(INGEST_THREADS)
   const int ntab = p.band_tab[b + 1] - tab0;
   const int zero_at = bstride - 16;
   for (int i = threadIdx.x; i < ntab; i += blockDim.x) {
-    const uint16_t e = p.tab[tab0 + i];
-    tab[i] = e == 0xFFFFu ? static_cast<uint16_t>(zero_at) : e;
+    const uint32_t e = p.tab[tab0 + i];
+    tab[i] = static_cast<uint16_t>(e == 0xFFFFu ? zero_at : e + 16u * (e / PIECE));
   }
   if (threadIdx.x < NBUF * 4)
     reinterpret_cast<uint32_t*>(bufs + (threadIdx.x >> 2) * bstride + zero_at)[threadIdx.x & 3] = 0;
+  // (the table and zero bytes are published by the __syncthreads below)
 
   const int seg0 = p.band_seg[b];
   const int nseg = p.band_seg[b + 1] - seg0;
@@ -85,11 +95,14 @@ __global__ void __launch_bounds__(INGEST_THREADS)
                        smem_addr(&full[slot])),
                    "r"(blen)
                    : "memory");
-      asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-              smem_addr(dst)),
-          "l"(src), "r"(blen), "r"(smem_addr(&full[slot]))
-          : "memory");
+      for (int o = 0; o < blen; o += PIECE) {
+        const int len = blen - o < PIECE ? blen - o : PIECE;
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_addr(dst + (o / PIECE) * PITCH)),
+            "l"(src + o), "r"(len), "r"(smem_addr(&full[slot]))
+            : "memory");
+      }
     }
   };
   if (bulk && threadIdx.x == 0)
@@ -113,7 +126,7 @@ __global__ void __launch_bounds__(INGEST_THREADS)
       }
     } else {
       const uint8_t* src = p.raster + f * p.pixels + pix0;
-      for (int k = threadIdx.x; k < blen; k += blockDim.x) band[k] = src[k];
+      for (int k = threadIdx.x; k < blen; k += blockDim.x) band[k + 16 * (k / PIECE)] = src[k];
       __syncthreads();
     }
 
@@ -124,18 +137,15 @@ __global__ void __launch_bounds__(INGEST_THREADS)
       const Segment sg = p.segs[seg0 + s];
       const uint16_t* st = tab + sg.taboff;
       uint32_t sq = 0, sm = 0;
-      for (int off = lane * 8; off < sg.len; off += 256) {
-        const uint4 e = *reinterpret_cast<const uint4*>(st + off);
+      // 4 output bytes per lane: a warp reads 128 consecutive output bytes
+      // whose sources within a run are consecutive -> conflict-free LDS.U8
+      for (int off = lane * 4; off < sg.len; off += 128) {
+        const uint2 e = *reinterpret_cast<const uint2*>(st + off);
         const uint32_t v0 = band[e.x & 0xFFFFu], v1 = band[e.x >> 16];
         const uint32_t v2 = band[e.y & 0xFFFFu], v3 = band[e.y >> 16];
-        const uint32_t v4 = band[e.z & 0xFFFFu], v5 = band[e.z >> 16];
-        const uint32_t v6 = band[e.w & 0xFFFFu], v7 = band[e.w >> 16];
-        uint2 w;
-        w.x = v0 | (v1 << 8) | (v2 << 16) | (v3 << 24);
-        w.y = v4 | (v5 << 8) | (v6 << 16) | (v7 << 24);
-        *reinterpret_cast<uint2*>(xrow + sg.dst + off) = w;
-        sq += v0 * v0 + v1 * v1 + v2 * v2 + v3 * v3 + v4 * v4 + v5 * v5 + v6 * v6 + v7 * v7;
-        sm += v0 + v1 + v2 + v3 + v4 + v5 + v6 + v7;
+        *reinterpret_cast<uint32_t*>(xrow + sg.dst + off) = v0 | (v1 << 8) | (v2 << 16) | (v3 << 24);
+        sq += v0 * v0 + v1 * v1 + v2 * v2 + v3 * v3;
+        sm += v0 + v1 + v2 + v3;
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
@@ -177,7 +187,7 @@ __global__ void k_norms(NormParams p) {
 }  // namespace
 
 cudaError_t launch_ingest(const IngestParams& p, cudaStream_t s) {
-  const size_t smem = NBUF * (static_cast<size_t>((p.band + 15) & ~15) + 16) +
+  const size_t smem = NBUF * static_cast<size_t>(band_stride(p.band)) +
                       static_cast<size_t>(p.max_tab) * 2 + 16;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k_ingest, cudaFuncAttributeMaxDynamicSharedMemorySize,

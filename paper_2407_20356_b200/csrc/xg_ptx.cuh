@@ -60,8 +60,11 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
 // kernel records an error word and the caller bails out.
 __device__ __forceinline__ bool mbar_wait(uint64_t* bar, uint32_t parity, int* err) {
   const uint32_t a = smem_u32(bar);
-  for (uint32_t it = 0; it < (1u << 26); ++it) {
-    if (mbar_try_wait(a, parity)) return true;
+  if (mbar_try_wait(a, parity)) return true;
+  for (uint32_t it = 0; it < (1u << 20); ++it) {
+#pragma unroll 1
+    for (int j = 0; j < 64; ++j)
+      if (mbar_try_wait(a, parity)) return true;
     if (*(volatile int*)err) return false;
   }
   atomicExch(err, 1);
