@@ -41,10 +41,18 @@ __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-__global__ void __launch_bounds__(INGEST_THREADS)
+// Warp roles: warps 0..7 consume (each owns a fixed, length-balanced set of
+// the band's segments, assigned on the host by LPT), warp 8 produces (one
+// lane issues the TMA bulk copies).  full/empty mbarriers per ring slot let
+// the consumer warps run up to NBUF frames apart, so per-frame imbalance
+// between warps averages out instead of stalling at a block barrier.
+constexpr int CONSUMERS = 8;
+
+__global__ void __launch_bounds__(INGEST_THREADS + 32)
     k_ingest(IngestParams p) {
   extern __shared__ uint4 ismem[];
   __shared__ __align__(8) uint64_t full[NBUF];
+  __shared__ __align__(8) uint64_t empty[NBUF];
   const int b = blockIdx.x;
   // band buffer: pieces of 512 B at a 528 B pitch, then 16 zero bytes that
   // the padding entries of the table point to
@@ -61,14 +69,11 @@ __global__ void __launch_bounds__(INGEST_THREADS)
   }
   if (threadIdx.x < NBUF * 4)
     reinterpret_cast<uint32_t*>(bufs + (threadIdx.x >> 2) * bstride + zero_at)[threadIdx.x & 3] = 0;
-  // (the table and zero bytes are published by the __syncthreads below)
 
   const int seg0 = p.band_seg[b];
-  const int nseg = p.band_seg[b + 1] - seg0;
   const int64_t pix0 = static_cast<int64_t>(b) * p.band;
   const int blen = static_cast<int>((p.pixels - pix0) < p.band ? (p.pixels - pix0) : p.band);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nwarps = blockDim.x >> 5;
   const bool bulk = ((p.pixels | blen) & 15) == 0 &&
                     (reinterpret_cast<uintptr_t>(p.raster) & 15) == 0;
 
@@ -79,62 +84,75 @@ __global__ void __launch_bounds__(INGEST_THREADS)
   const int64_t nf = f_end - f_begin;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < NBUF; ++i)
+    for (int i = 0; i < NBUF; ++i) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&full[i])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(&empty[i])),
+                   "r"(CONSUMERS));
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  __syncthreads();
+  __syncthreads();  // barriers, table and zero bytes visible
 
-  // one thread streams band bytes of frame f into buffer f % NBUF (TMA bulk copy)
-  auto issue = [&](int64_t f) {
-    const int slot = static_cast<int>((f - f_begin) % NBUF);
-    uint8_t* dst = bufs + slot * bstride;
-    const uint8_t* src = p.raster + f * p.pixels + pix0;
-    if (bulk) {
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
-                       smem_addr(&full[slot])),
-                   "r"(blen)
-                   : "memory");
-      for (int o = 0; o < blen; o += PIECE) {
-        const int len = blen - o < PIECE ? blen - o : PIECE;
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                smem_addr(dst + (o / PIECE) * PITCH)),
-            "l"(src + o), "r"(len), "r"(smem_addr(&full[slot]))
-            : "memory");
-      }
+  auto wait = [](uint64_t* bar, uint32_t parity) {
+    uint32_t ok = 0;
+    while (!ok) {
+      asm volatile(
+          "{\n\t.reg .pred P;\n\t"
+          "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
+          "selp.u32 %0, 1, 0, P;\n\t}"
+          : "=r"(ok)
+          : "r"(smem_addr(bar)), "r"(parity)
+          : "memory");
     }
   };
-  if (bulk && threadIdx.x == 0)
-    for (int64_t f = f_begin; f < f_begin + NBUF && f < f_end; ++f) issue(f);
 
-  for (int64_t i = 0; i < nf; ++i) {
-    const int64_t f = f_begin + i;
-    const int slot = static_cast<int>(i % NBUF);
-    uint8_t* band = bufs + slot * bstride;
-    if (bulk) {
-      const uint32_t parity = static_cast<uint32_t>((i / NBUF) & 1);
-      uint32_t ok = 0;
-      while (!ok) {
-        asm volatile(
-            "{\n\t.reg .pred P;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, P;\n\t}"
-            : "=r"(ok)
-            : "r"(smem_addr(&full[slot])), "r"(parity)
-            : "memory");
+  if (warp == CONSUMERS) {
+    // ------------------------------------------------------------ producer
+    for (int64_t i = 0; i < nf; ++i) {
+      const int slot = static_cast<int>(i % NBUF);
+      const int64_t use = i / NBUF;
+      if (use > 0) wait(&empty[slot], static_cast<uint32_t>((use - 1) & 1));
+      uint8_t* dst = bufs + slot * bstride;
+      const uint8_t* src = p.raster + (f_begin + i) * p.pixels + pix0;
+      if (bulk) {
+        if (lane == 0) {
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                           smem_addr(&full[slot])),
+                       "r"(blen)
+                       : "memory");
+          for (int o = 0; o < blen; o += PIECE) {
+            const int len = blen - o < PIECE ? blen - o : PIECE;
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], "
+                "%2, [%3];" ::"r"(smem_addr(dst + (o / PIECE) * PITCH)),
+                "l"(src + o), "r"(len), "r"(smem_addr(&full[slot]))
+                : "memory");
+          }
+        }
+      } else {
+        for (int k = lane; k < blen; k += 32) dst[k + 16 * (k / PIECE)] = src[k];
+        __syncwarp();
+        if (lane == 0)
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&full[slot]))
+                       : "memory");
       }
-    } else {
-      const uint8_t* src = p.raster + f * p.pixels + pix0;
-      for (int k = threadIdx.x; k < blen; k += blockDim.x) band[k + 16 * (k / PIECE)] = src[k];
-      __syncthreads();
     }
+    return;
+  }
 
-    const int64_t t = p.t0 + f;
+  // -------------------------------------------------------------- consumers
+  const int w0 = p.band_wseg[b * (CONSUMERS + 1) + warp];
+  const int w1 = p.band_wseg[b * (CONSUMERS + 1) + warp + 1];
+  for (int64_t i = 0; i < nf; ++i) {
+    const int slot = static_cast<int>(i % NBUF);
+    wait(&full[slot], static_cast<uint32_t>((i / NBUF) & 1));
+    const uint8_t* band = bufs + slot * bstride;
+    const int64_t t = p.t0 + f_begin + i;
     uint8_t* xrow = p.x + t * p.ktot;
     uint2* srow = p.seg_stats + t * p.n_segs + seg0;
-    for (int s = warp; s < nseg; s += nwarps) {
-      const Segment sg = p.segs[seg0 + s];
+    for (int w = w0; w < w1; ++w) {
+      const int sidx = p.seg_order[w];  // segment index within the band
+      const Segment sg = p.segs[seg0 + sidx];
       const uint16_t* st = tab + sg.taboff;
       uint32_t sq = 0, sm = 0;
       // 4 output bytes per lane: a warp reads 128 consecutive output bytes
@@ -143,7 +161,8 @@ __global__ void __launch_bounds__(INGEST_THREADS)
         const uint2 e = *reinterpret_cast<const uint2*>(st + off);
         const uint32_t v0 = band[e.x & 0xFFFFu], v1 = band[e.x >> 16];
         const uint32_t v2 = band[e.y & 0xFFFFu], v3 = band[e.y >> 16];
-        *reinterpret_cast<uint32_t*>(xrow + sg.dst + off) = v0 | (v1 << 8) | (v2 << 16) | (v3 << 24);
+        *reinterpret_cast<uint32_t*>(xrow + sg.dst + off) =
+            __byte_perm(v0 | (v1 << 8), v2 | (v3 << 8), 0x5410);
         sq += v0 * v0 + v1 * v1 + v2 * v2 + v3 * v3;
         sm += v0 + v1 + v2 + v3;
       }
@@ -152,10 +171,12 @@ __global__ void __launch_bounds__(INGEST_THREADS)
         sq += __shfl_xor_sync(0xffffffffu, sq, o);
         sm += __shfl_xor_sync(0xffffffffu, sm, o);
       }
-      if (lane == 0) srow[s] = make_uint2(sq, sm);
+      if (lane == 0) srow[sidx] = make_uint2(sq, sm);
     }
-    __syncthreads();  // every warp is done with this buffer
-    if (bulk && threadIdx.x == 0 && f + NBUF < f_end) issue(f + NBUF);
+    __syncwarp();
+    if (lane == 0)
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&empty[slot]))
+                   : "memory");
   }
 }
 
@@ -196,7 +217,7 @@ cudaError_t launch_ingest(const IngestParams& p, cudaStream_t s) {
   }
   const int64_t groups = (p.n_frames + p.frames_per_cta - 1) / p.frames_per_cta;
   dim3 grid(p.n_bands, static_cast<unsigned>(groups));
-  k_ingest<<<grid, INGEST_THREADS, smem, s>>>(p);
+  k_ingest<<<grid, INGEST_THREADS + 32, smem, s>>>(p);
   return cudaGetLastError();
 }
 

@@ -58,6 +58,8 @@ struct xg_layout {
   int32_t max_tab = 0;
   std::vector<int64_t> ring_pixels, kpad, koff;
   int32_t* d_band_seg = nullptr;
+  int32_t* d_band_wseg = nullptr;
+  int32_t* d_seg_order = nullptr;
   Segment* d_segs = nullptr;
   int32_t* d_band_tab = nullptr;
   uint16_t* d_tab = nullptr;
@@ -328,6 +330,30 @@ int xg_layout_create(xg_ctx* c, int64_t full_pixels, int32_t n_rings,
     L->max_tab = std::max(L->max_tab, local);
   }
   band_seg[nb] = static_cast<int32_t>(segs.size());
+  // Per band, deal segments to the 8 ingest consumer warps by LPT on length.
+  constexpr int kWarps = 8;
+  std::vector<int32_t> band_wseg((size_t)nb * (kWarps + 1)), seg_order;
+  seg_order.reserve(segs.size());
+  for (int32_t b = 0; b < nb; ++b) {
+    const int32_t s0 = band_seg[b], s1 = band_seg[b + 1];
+    std::vector<int32_t> idx(s1 - s0);
+    for (int32_t i = 0; i < s1 - s0; ++i) idx[i] = i;
+    std::stable_sort(idx.begin(), idx.end(),
+                     [&](int32_t a, int32_t c) { return segs[s0 + a].len > segs[s0 + c].len; });
+    std::vector<std::vector<int32_t>> bins(kWarps);
+    std::vector<int64_t> load(kWarps, 0);
+    for (int32_t i : idx) {
+      const int w = static_cast<int>(std::min_element(load.begin(), load.end()) - load.begin());
+      bins[w].push_back(i);
+      load[w] += segs[s0 + i].len + 64;  // + per-segment overhead
+    }
+    for (int w = 0; w < kWarps; ++w) {
+      band_wseg[(size_t)b * (kWarps + 1) + w] = static_cast<int32_t>(seg_order.size());
+      std::sort(bins[w].begin(), bins[w].end());
+      for (int32_t i : bins[w]) seg_order.push_back(i);
+    }
+    band_wseg[(size_t)b * (kWarps + 1) + kWarps] = static_cast<int32_t>(seg_order.size());
+  }
   band_tab[nb] = static_cast<int32_t>(tab.size());
   L->n_segs = static_cast<int32_t>(segs.size());
   // ring -> its segments in ascending band order (fixed fold order for norms)
@@ -345,6 +371,8 @@ int xg_layout_create(xg_ctx* c, int64_t full_pixels, int32_t n_rings,
   }
   cudaError_t e = cudaSuccess;
   if ((e = dalloc(&L->d_band_seg, band_seg.size())) != cudaSuccess ||
+      (e = dalloc(&L->d_band_wseg, band_wseg.size())) != cudaSuccess ||
+      (e = dalloc(&L->d_seg_order, seg_order.size())) != cudaSuccess ||
       (e = dalloc(&L->d_segs, segs.size())) != cudaSuccess ||
       (e = dalloc(&L->d_band_tab, band_tab.size())) != cudaSuccess ||
       (e = dalloc(&L->d_tab, tab.size())) != cudaSuccess ||
@@ -356,6 +384,8 @@ int xg_layout_create(xg_ctx* c, int64_t full_pixels, int32_t n_rings,
     return cuda_fail(c, e, "layout alloc");
   }
   cudaMemcpy(L->d_band_seg, band_seg.data(), band_seg.size() * 4, cudaMemcpyHostToDevice);
+  cudaMemcpy(L->d_band_wseg, band_wseg.data(), band_wseg.size() * 4, cudaMemcpyHostToDevice);
+  cudaMemcpy(L->d_seg_order, seg_order.data(), seg_order.size() * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(L->d_segs, segs.data(), segs.size() * sizeof(Segment), cudaMemcpyHostToDevice);
   cudaMemcpy(L->d_band_tab, band_tab.data(), band_tab.size() * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(L->d_tab, tab.data(), tab.size() * 2, cudaMemcpyHostToDevice);
@@ -374,6 +404,8 @@ int xg_layout_create(xg_ctx* c, int64_t full_pixels, int32_t n_rings,
 void xg_layout_destroy(xg_layout* L) {
   if (!L) return;
   dfree(L->d_band_seg);
+  dfree(L->d_band_wseg);
+  dfree(L->d_seg_order);
   dfree(L->d_segs);
   dfree(L->d_band_tab);
   dfree(L->d_tab);
@@ -477,6 +509,8 @@ int xg_series_load_frames(xg_series* s, const uint8_t* frames, int64_t n, int on
   p.n_bands = L->n_bands;
   p.n_rings = L->rings;
   p.band_seg = L->d_band_seg;
+  p.band_wseg = L->d_band_wseg;
+  p.seg_order = L->d_seg_order;
   p.segs = L->d_segs;
   p.band_tab = L->d_band_tab;
   p.tab = L->d_tab;

@@ -29,6 +29,8 @@ struct IngestParams {
   int32_t n_rings;
   const int32_t* band_seg;   // n_bands + 1 segment ranges
   const Segment* segs;
+  const int32_t* band_wseg;  // [n_bands][9]: per consumer warp, range in seg_order
+  const int32_t* seg_order;  // segment indices (within band), LPT-balanced per warp
   const int32_t* band_tab;   // n_bands + 1 table ranges (u16 entries)
   const uint16_t* tab;       // source offsets within the band, 0xFFFF = zero pad
   int32_t max_tab;           // largest band table (entries)
