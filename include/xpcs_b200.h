@@ -59,6 +59,9 @@ typedef enum xg_dtype { XG_F64 = 0, XG_F32 = 1, XG_I32_GRAM = 2 } xg_dtype;
                               behaviour, linalg.cpp:446-449); default flags the
                               frame and excludes it from g2 instead */
 #define XG_NO_G2 0x2u       /* skip the g2 reduction */
+#define XG_CMP_BF16 0x4u    /* compressed Gram from the bf16 coefficients only
+                              (one product; ~1e-2 relative) instead of the
+                              bf16x3 split (6 products; ~1e-6 relative) */
 
 typedef struct xg_ctx xg_ctx;
 typedef struct xg_layout xg_layout;
@@ -114,6 +117,27 @@ XG_API int xg_series_get_g2(xg_series* s, int32_t ring, double* values, int64_t*
 /* f64 frame norms |x_t| of ring (n) and the count of zero-norm frames. */
 XG_API int xg_series_get_norms(xg_series* s, int32_t ring, double* norms, int64_t* n_zero);
 XG_API int64_t xg_series_frames(const xg_series* s);
+
+/* ---- rank-k compression and the homomorphic TTC -----------------------
+ * Basis: one EncodingMatrix V_q (M_q x k, orthonormal columns, mask row
+ * order; model.hpp:53-67) per ring, stored on the device as `digits` signed
+ * int8 planes per column (V ~= s (d0 + d1/254 + d2/254^2); 3 digits keep
+ * ~3e-8 of max|V|, 2 digits ~8e-6).  xg_compress = compress_series
+ * (compress.cpp:48-81): Y_q = (X_q/|x|) V_q on tcgen05 int8 tensor cores,
+ * exact integer accumulation, f64 combination.  xg_ttc_compressed =
+ * ttc_compressed (correlate.cpp:27-35): C~_q = Y_q Y_q^T on tcgen05 bf16 tensor
+ * cores (bf16x3 split, or XG_CMP_BF16) + fused g2. */
+XG_API int xg_basis_create(xg_ctx* ctx, const xg_layout* layout, int32_t k, int32_t digits,
+                           xg_basis** out);
+XG_API void xg_basis_destroy(xg_basis* basis);
+XG_API int xg_basis_set_ring(xg_basis* basis, int32_t ring, const double* v);
+XG_API int xg_compress(xg_series* s, const xg_basis* basis, uint32_t flags);
+XG_API int xg_ttc_compressed(xg_series* s, uint32_t flags);
+/* coefficients (n x k, f64) and norms (n) of one ring */
+XG_API int xg_series_get_coeffs(xg_series* s, int32_t ring, double* y, double* norms);
+XG_API int xg_series_get_cttc(xg_series* s, int32_t ring, int32_t dtype, void* out, int64_t ld,
+                              int out_on_device);
+XG_API int xg_series_get_cg2(xg_series* s, int32_t ring, double* values, int64_t* counts);
 
 /* ---- synthetic source (benchmark input; not on the correlation path) ---
  * Seeded speckle counts: complex AR(1) field per pixel with

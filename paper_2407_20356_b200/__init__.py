@@ -155,6 +155,34 @@ class RingLayout:
             self.h = None
 
 
+# ------------------------------------------------------------------ basis
+class Basis:
+    """Per-ring rank-k encoding matrices (EncodingMatrix, model.hpp:53-67) on
+    the device, as `digits` signed-int8 planes per column (3: ~3e-8 of
+    max|V|; 2: ~8e-6)."""
+
+    def __init__(self, layout: RingLayout, k: int, digits: int = 3):
+        self.layout = layout
+        self.ctx = layout.ctx
+        self.k = int(k)
+        h = C.c_void_p()
+        _check(self.ctx.h, lib.xg_basis_create(self.ctx.h, layout.h, self.k, digits, C.byref(h)))
+        self.h = h
+
+    def set_ring(self, ring: int, v: np.ndarray) -> "Basis":
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        if v.shape != (self.layout.ring_pixels(ring), self.k):
+            raise ShapeError(f"basis of ring {ring} must be "
+                             f"{self.layout.ring_pixels(ring)} x {self.k}, got {v.shape}")
+        _check(self.ctx.h, lib.xg_basis_set_ring(self.h, ring, v.ctypes.data_as(_abi.PD)))
+        return self
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib.xg_basis_destroy(self.h)
+            self.h = None
+
+
 # ----------------------------------------------------------------- series
 class FrameSeries:
     """Device-resident photon-count frames of one detector, correlated per
@@ -228,6 +256,43 @@ class FrameSeries:
                                                 cnt.ctypes.data_as(_abi.PI64)))
         lags = np.arange(n, dtype=np.float64) * self.frame_period
         return lags, vals, cnt
+
+    # ------------------------------------------------------ compressed path
+    def compress(self, basis: "Basis", strict: bool = False) -> "FrameSeries":
+        """Rank-k projection of every ring (compress_series, compress.cpp:48-81)."""
+        _check(self.ctx.h, lib.xg_compress(self.h, basis.h, _abi.STRICT if strict else 0))
+        self.k = basis.k
+        return self
+
+    def ttc_compressed(self, mode: str = "f32", g2: bool = True) -> "FrameSeries":
+        """Homomorphic TTC C~ = Y Y^T of every ring (ttc_compressed,
+        correlate.cpp:27-35). mode 'f32' (bf16x3 split, ~1e-6) or 'bf16'."""
+        flags = (_abi.CMP_BF16 if mode == "bf16" else 0) | (0 if g2 else _abi.NO_G2)
+        _check(self.ctx.h, lib.xg_ttc_compressed(self.h, flags))
+        return self
+
+    def coeffs(self, ring: int):
+        n, k = self.n_frames, self.k
+        y = np.empty((n, k), np.float64)
+        nr = np.empty(n, np.float64)
+        _check(self.ctx.h, lib.xg_series_get_coeffs(self.h, ring, y.ctypes.data_as(_abi.PD),
+                                                    nr.ctypes.data_as(_abi.PD)))
+        return y, nr
+
+    def cttc(self, ring: int, dtype: str = "f64") -> np.ndarray:
+        n = self.n_frames
+        out = np.empty((n, n), np.float64 if dtype == "f64" else np.float32)
+        code = _abi.F64 if dtype == "f64" else _abi.F32
+        _check(self.ctx.h, lib.xg_series_get_cttc(self.h, ring, code, _ptr(out), n, 0))
+        return out
+
+    def cg2(self, ring: int):
+        n = self.n_frames
+        vals = np.empty(n, np.float64)
+        cnt = np.empty(n, np.int64)
+        _check(self.ctx.h, lib.xg_series_get_cg2(self.h, ring, vals.ctypes.data_as(_abi.PD),
+                                                 cnt.ctypes.data_as(_abi.PI64)))
+        return np.arange(n, dtype=np.float64) * self.frame_period, vals, cnt
 
     def norms(self, ring: int):
         n = self.n_frames

@@ -52,6 +52,14 @@ _sigs = {
     "xg_series_frames": (I64, [P]),
     "xg_synth_speckle": (C.c_int, [P, I64, I64, I64, I32, C.c_double, I32, C.c_double,
                                    C.c_uint64, P]),
+    "xg_basis_create": (C.c_int, [P, P, I32, I32, C.POINTER(P)]),
+    "xg_basis_destroy": (None, [P]),
+    "xg_basis_set_ring": (C.c_int, [P, I32, PD]),
+    "xg_compress": (C.c_int, [P, P, U32]),
+    "xg_ttc_compressed": (C.c_int, [P, U32]),
+    "xg_series_get_coeffs": (C.c_int, [P, I32, PD, PD]),
+    "xg_series_get_cttc": (C.c_int, [P, I32, I32, P, I64, C.c_int]),
+    "xg_series_get_cg2": (C.c_int, [P, I32, PD, PI64]),
 }
 
 for _name, (_res, _args) in _sigs.items():
@@ -82,3 +90,4 @@ ERR_INVALID = 102
 F64, F32, I32_GRAM = 0, 1, 2
 STRICT = 0x1
 NO_G2 = 0x2
+CMP_BF16 = 0x4

@@ -38,7 +38,12 @@ constexpr int B_BYTES = BN * BK;           // 32 KB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int TMEM_COLS = 512;             // 2 accumulators x 256 s32 columns
 constexpr int NUM_THREADS = 256;
-constexpr uint32_t IDESC = idesc_i8(BM, BN, false);
+// MODE 0: raw u8 x u8 -> s32 (kind::i8);  MODE 1: compressed bf16 x bf16 ->
+// f32 (kind::f16) over split-precision coefficient planes (see k_project.cu).
+template <int MODE>
+constexpr uint32_t gram_idesc() {
+  return MODE == 0 ? idesc_i8(BM, BN, false) : idesc_bf16(BM, BN);
+}
 
 constexpr int NDIAG = BM + BN - 1;         // tile diagonals j-i in [-127, 255]
 constexpr int NDIAG_PAD = 384;
@@ -54,7 +59,7 @@ struct __align__(16) GramSmemTail {
   double inv_row[BM];                      // 1/|x_i| of the tile rows (0 beyond T / zero frame)
   double inv_col[BN];                      // 1/|x_j| of the tile columns
   double acc[4][NDIAG_PAD];                // per-warp diagonal sums of the tile
-  int32_t stage[4][32][33];                // per-warp 32x32 chunk of the Gram
+  uint32_t stage[4][32][33];               // per-warp 32x32 chunk (s32 or f32 bits)
 };
 
 __device__ __forceinline__ void epi_bar() {  // the 4 epilogue warps only
@@ -65,8 +70,10 @@ __device__ __forceinline__ void epi_bar() {  // the 4 epilogue warps only
 
 size_t gram_u8_smem_bytes() { return 1024 + STAGES * STAGE_BYTES + sizeof(GramSmemTail); }
 
+template <int MODE>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
-    k_gram_u8(const __grid_constant__ CUtensorMap tmX, GramParams p) {
+    k_gram_tc(const __grid_constant__ CUtensorMap tmX, GramParams p) {
+  constexpr uint32_t IDESC = gram_idesc<MODE>();
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte alignment for the 128B-swizzle atoms; offsetting the shared
   // array itself (not a uintptr_t round trip) keeps accesses in the shared
@@ -104,16 +111,26 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
         const TileDesc td = p.tiles[t];
-        const int koff = p.ring_koff[td.ring];
-        const int nkb = p.ring_nkb[td.ring];
+        const int koff = MODE == 0 ? p.ring_koff[td.ring] : 0;
+        const int nkb = MODE == 0 ? p.ring_nkb[td.ring] : p.n_pairs * p.kb_per_plane;
         for (int kb = 0; kb < nkb; ++kb) {
           if (!mbar_wait(&tail->empty[stage], phase ^ 1, p.err)) goto producer_done;
           mbar_arrive_expect_tx(&tail->full[stage], STAGE_BYTES);
-          const int kc = koff + kb * BK;
-          tma_load_2d(sA + stage * A_BYTES, &tmX, &tail->full[stage], kc, td.i0);
-          tma_load_2d(sB + stage * B_BYTES, &tmX, &tail->full[stage], kc, td.j0);
-          tma_load_2d(sB + stage * B_BYTES + BK * 128, &tmX, &tail->full[stage], kc,
-                      td.j0 + 128);
+          int kc, ra, rb;
+          if (MODE == 0) {  // byte column of the ring, frame rows
+            kc = koff + kb * BK;
+            ra = td.i0;
+            rb = td.j0;
+          } else {  // K block = (precision pair, 64-element block of the plane)
+            const int pr = kb / p.kb_per_plane;
+            kc = (kb - pr * p.kb_per_plane) * 64;
+            const int plane_a = (p.pairs >> (4 * pr)) & 3, plane_b = (p.pairs >> (4 * pr + 2)) & 3;
+            ra = (td.ring * 3 + plane_a) * p.plane_rows + td.i0;
+            rb = (td.ring * 3 + plane_b) * p.plane_rows + td.j0;
+          }
+          tma_load_2d(sA + stage * A_BYTES, &tmX, &tail->full[stage], kc, ra);
+          tma_load_2d(sB + stage * B_BYTES, &tmX, &tail->full[stage], kc, rb);
+          tma_load_2d(sB + stage * B_BYTES + BK * 128, &tmX, &tail->full[stage], kc, rb + 128);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -131,7 +148,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       uint32_t acc_phase = 0;
       for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
         const TileDesc td = p.tiles[t];
-        const int nkb = p.ring_nkb[td.ring];
+        const int nkb = MODE == 0 ? p.ring_nkb[td.ring] : p.n_pairs * p.kb_per_plane;
         if (!mbar_wait(&tail->tempty[acc], acc_phase ^ 1, p.err)) break;
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + static_cast<uint32_t>(acc * BN);
@@ -146,8 +163,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const uint32_t b0 = smem_u32(sB + stage * B_BYTES);
 #pragma unroll
           for (int k = 0; k < BK / 32; ++k) {
-            mma_i8(tmem_d, sdesc_k128(a0 + k * 32), sdesc_k128(b0 + k * 32), IDESC,
-                   (kb | k) != 0 ? 1u : 0u);
+            if (MODE == 0)
+              mma_i8(tmem_d, sdesc_k128(a0 + k * 32), sdesc_k128(b0 + k * 32), IDESC,
+                     (kb | k) != 0 ? 1u : 0u);
+            else
+              mma_bf16(tmem_d, sdesc_k128(a0 + k * 32), sdesc_k128(b0 + k * 32), IDESC,
+                       (kb | k) != 0 ? 1u : 0u);
           }
           tc_commit(&tail->empty[stage]);  // smem slot free once these MMAs retire
           if (++stage == STAGES) {
@@ -183,10 +204,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       if (ok) tc_fence_after();
       if (p.g2_partial) {
         epi_bar();  // previous tile's fold has finished with inv/acc
-        const double* inv = p.inv + static_cast<int64_t>(td.ring) * p.inv_ld;
+        const double* inv = MODE == 0 ? p.inv + static_cast<int64_t>(td.ring) * p.inv_ld : nullptr;
         for (int e = etid; e < BM + BN; e += 128) {
           const int idx = e < BM ? td.i0 + e : td.j0 + (e - BM);
-          const double v = idx < p.n_frames ? inv[idx] : 0.0;
+          const double v = idx < p.n_frames ? (MODE == 0 ? inv[idx] : 1.0) : 0.0;
           if (e < BM)
             tail->inv_row[e] = v;
           else
@@ -195,7 +216,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int e = lane; e < NDIAG_PAD; e += 32) tail->acc[sub][e] = 0.0;
         epi_bar();
       }
-      int32_t* gout = p.gram + static_cast<int64_t>(td.ring) * p.ring_stride +
+      uint32_t* gout = p.gram + static_cast<int64_t>(td.ring) * p.ring_stride +
                       static_cast<int64_t>(td.i0 + row) * p.ld + td.j0;
       const uint32_t tbase =
           tmem_base + static_cast<uint32_t>(acc * BN) + (static_cast<uint32_t>(sub * 32) << 16);
@@ -210,9 +231,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           dst[v] = make_int4(static_cast<int>(r[4 * v]), static_cast<int>(r[4 * v + 1]),
                              static_cast<int>(r[4 * v + 2]), static_cast<int>(r[4 * v + 3]));
         if (p.g2_partial) {
-          int32_t(*S)[33] = tail->stage[sub];
+          uint32_t(*S)[33] = tail->stage[sub];
 #pragma unroll
-          for (int k = 0; k < 32; ++k) S[lane][k] = static_cast<int32_t>(r[k]);
+          for (int k = 0; k < 32; ++k) S[lane][k] = r[k];
           __syncwarp();
           // global lag of chunk element (l, k): D0 + (k - l)
           const int D0 = td.j0 + 32 * c - td.i0 - 32 * sub;
@@ -231,7 +252,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               run = 0.0;
             }
             const int k = (l + lane + 1) & 31;
-            run = fma(static_cast<double>(S[l][k]), ir[l] * ic[k], run);
+            const double v = MODE == 0 ? static_cast<double>(static_cast<int32_t>(S[l][k]))
+                                       : static_cast<double>(__uint_as_float(S[l][k]));
+            run = fma(v, ir[l] * ic[k], run);
           }
           sa = run;
           if (!use_a) sa = 0.0;
@@ -271,16 +294,27 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
 }
 
-cudaError_t launch_gram_u8(const CUtensorMap& tmX, const GramParams& p, int num_sms,
-                           cudaStream_t stream) {
+template <int MODE>
+static cudaError_t launch_gram_mode(const CUtensorMap& tmX, const GramParams& p, int num_sms,
+                                    cudaStream_t stream) {
   const size_t smem = gram_u8_smem_bytes();
-  cudaError_t e =
-      cudaFuncSetAttribute(k_gram_u8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(k_gram_tc<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
   if (e != cudaSuccess) return e;
   const int grid = p.ntiles < num_sms ? p.ntiles : num_sms;
   if (grid <= 0) return cudaSuccess;
-  k_gram_u8<<<grid, NUM_THREADS, smem, stream>>>(tmX, p);
+  k_gram_tc<MODE><<<grid, NUM_THREADS, smem, stream>>>(tmX, p);
   return cudaGetLastError();
+}
+
+cudaError_t launch_gram_u8(const CUtensorMap& tmX, const GramParams& p, int num_sms,
+                           cudaStream_t stream) {
+  return launch_gram_mode<0>(tmX, p, num_sms, stream);
+}
+
+cudaError_t launch_gram_cmp(const CUtensorMap& tmY, const GramParams& p, int num_sms,
+                            cudaStream_t stream) {
+  return launch_gram_mode<1>(tmY, p, num_sms, stream);
 }
 
 }  // namespace xg

@@ -1,0 +1,234 @@
+// k_project.cu -- K3: rank-k projection of every q-ring, Y_q = (X_q / |x|) V_q,
+// on tcgen05 integer tensor cores.
+//
+// Replaces `compress_series` / `project_row` (src/compress.cpp:12-22,48-81).
+// Counts are u8 and exact; the basis V_q is split host-side into S signed
+// int8 "digits" per coefficient column j:
+//     V(p, j) ~= scale_j * (d0 + d1/254 + d2/254^2),   |d_s| <= 127,
+// (relative representation error <= 0.5/(127*254^2) ~ 3e-8 of max|V_j| for
+// S = 3), stacked along N.  One u8 x s8 -> s32 MMA pass over the ring-major
+// frames then yields EXACT digit accumulations a_s(t, j) = sum_p x_tp d_s(p, j)
+// and the epilogue forms, in f64,
+//     y(t, j) = scale_j / |x_t| * (a0 + a1/254 + a2/254^2).
+// HBM-bound on reading X once (the MMA work per byte is small).  The epilogue
+// also writes the bf16 split planes y = b0 + b1 + b2 consumed by the
+// compressed Gram (K4, k_gram.cu MODE 1).
+//
+// Tile = (ring, 128 frames, N-tile of S*kt digit rows); same warp roles and
+// mbarrier pipeline as K2.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "xg_kernels.h"
+#include "xg_ptx.cuh"
+
+namespace xg {
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 128;
+constexpr int STAGES = 4;
+constexpr int A_BYTES = BM * BK;    // 16 KB
+constexpr int B_BYTES = 256 * BK;   // room for up to 256 digit rows
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int TMEM_COLS = 512;
+constexpr int NUM_THREADS = 256;
+
+struct __align__(8) ProjTail {
+  uint64_t full[STAGES];
+  uint64_t empty[STAGES];
+  uint64_t tfull[2];
+  uint64_t tempty[2];
+  uint32_t tmem_base;
+};
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+
+}  // namespace
+
+size_t project_smem_bytes() { return 1024 + STAGES * STAGE_BYTES + sizeof(ProjTail); }
+
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    k_project(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmV,
+              ProjParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * A_BYTES;
+  ProjTail* tail = reinterpret_cast<ProjTail*>(smem + STAGES * STAGE_BYTES);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nt_rows = p.n_digits * p.kt;               // N of the MMA (multiple of 16)
+  const int nb_boxes = (nt_rows + 127) / 128;
+  const uint32_t idesc = idesc_i8(BM, static_cast<uint32_t>(nt_rows), true);
+  const uint32_t stage_tx = A_BYTES + nb_boxes * 128 * BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&tail->full[s], 1);
+      mbar_init(&tail->empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tail->tfull[a], 1);
+      mbar_init(&tail->tempty[a], 4);
+    }
+    fence_barrier_init();
+    tma_prefetch(&tmX);
+    tma_prefetch(&tmV);
+  }
+  if (warp == 2) tmem_alloc(&tail->tmem_base, TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = tail->tmem_base;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
+        const TileDesc td = p.tiles[t];
+        const int koff = p.ring_koff[td.ring], nkb = p.ring_nkb[td.ring];
+        const int vrow = td.j0 * nt_rows;  // j0 = N-tile index
+        for (int kb = 0; kb < nkb; ++kb) {
+          if (!mbar_wait(&tail->empty[stage], phase ^ 1, p.err)) goto done;
+          mbar_arrive_expect_tx(&tail->full[stage], stage_tx);
+          const int kc = koff + kb * BK;
+          tma_load_2d(sA + stage * A_BYTES, &tmX, &tail->full[stage], kc, td.i0);
+          for (int bx = 0; bx < nb_boxes; ++bx)
+            tma_load_2d(sB + stage * B_BYTES + bx * 128 * BK, &tmV, &tail->full[stage], kc,
+                        vrow + bx * 128);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    done:;
+    }
+  } else if (warp == 1) {
+    if (elect_one()) {
+      int stage = 0, acc = 0;
+      uint32_t phase = 0, acc_phase = 0;
+      for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
+        const TileDesc td = p.tiles[t];
+        const int nkb = p.ring_nkb[td.ring];
+        if (!mbar_wait(&tail->tempty[acc], acc_phase ^ 1, p.err)) break;
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + static_cast<uint32_t>(acc * 256);
+        bool ok = true;
+        for (int kb = 0; kb < nkb; ++kb) {
+          if (!mbar_wait(&tail->full[stage], phase, p.err)) {
+            ok = false;
+            break;
+          }
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + stage * A_BYTES), b0 = smem_u32(sB + stage * B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 32; ++k)
+            mma_i8(tmem_d, sdesc_k128(a0 + k * 32), sdesc_k128(b0 + k * 32), idesc,
+                   (kb | k) != 0 ? 1u : 0u);
+          tc_commit(&tail->empty[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        if (!ok) break;
+        tc_commit(&tail->tfull[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    const int sub = warp & 3;
+    const int row = sub * 32 + lane;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
+      const TileDesc td = p.tiles[t];
+      bool ok = mbar_wait(&tail->tfull[acc], acc_phase, p.err);
+      ok = __all_sync(0xffffffffu, ok);
+      if (!ok) break;
+      tc_fence_after();
+      const int64_t frame = td.i0 + row;
+      const bool live = frame < p.n_frames;
+      const double inv = live ? p.inv[static_cast<int64_t>(td.ring) * p.inv_ld + frame] : 0.0;
+      const uint32_t tbase =
+          tmem_base + static_cast<uint32_t>(acc * 256) + (static_cast<uint32_t>(sub * 32) << 16);
+      const double* scale = p.scale + static_cast<int64_t>(td.ring) * p.k;
+      for (int jc = 0; jc < p.kt; jc += 16) {
+        uint32_t a0[16], a1[16], a2[16];
+        tmem_ld16(tbase + jc, a0);
+        if (p.n_digits > 1) tmem_ld16(tbase + p.kt + jc, a1);
+        if (p.n_digits > 2) tmem_ld16(tbase + 2 * p.kt + jc, a2);
+        tmem_ld_wait();
+        if (live) {  // (no early continue: the next tcgen05.ld needs the whole warp)
+        const int j0 = td.j0 * p.kt + jc;
+        double* yrow = p.y + (static_cast<int64_t>(td.ring) * p.y_ld + frame) * p.k + j0;
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          double s = static_cast<double>(static_cast<int32_t>(a0[e]));
+          if (p.n_digits > 1) s += static_cast<double>(static_cast<int32_t>(a1[e])) * (1.0 / 254.0);
+          if (p.n_digits > 2)
+            s += static_cast<double>(static_cast<int32_t>(a2[e])) * (1.0 / 64516.0);
+          const double y = scale[j0 + e] * inv * s;
+          yrow[e] = y;
+          if (p.planes) {
+            // y = b0 + b1 + b2 in bf16 (~24 significant bits)
+            const __nv_bfloat16 b0 = __double2bfloat16(y);
+            const double r1 = y - static_cast<double>(__bfloat162float(b0));
+            const __nv_bfloat16 b1 = __double2bfloat16(r1);
+            const double r2 = r1 - static_cast<double>(__bfloat162float(b1));
+            const __nv_bfloat16 b2 = __double2bfloat16(r2);
+            const int64_t base = (static_cast<int64_t>(td.ring) * 3) * p.plane_rows + frame;
+            p.planes[base * p.kp + j0 + e] = b0;
+            p.planes[(base + p.plane_rows) * p.kp + j0 + e] = b1;
+            p.planes[(base + 2 * p.plane_rows) * p.kp + j0 + e] = b2;
+          }
+        }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tail->tempty[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, TMEM_COLS);
+  }
+}
+
+cudaError_t launch_project(const CUtensorMap& tmX, const CUtensorMap& tmV, const ProjParams& p,
+                           int num_sms, cudaStream_t stream) {
+  const size_t smem = project_smem_bytes();
+  cudaError_t e =
+      cudaFuncSetAttribute(k_project, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int grid = p.ntiles < num_sms ? p.ntiles : num_sms;
+  if (grid <= 0) return cudaSuccess;
+  k_project<<<grid, NUM_THREADS, smem, stream>>>(tmX, tmV, p);
+  return cudaGetLastError();
+}
+
+}  // namespace xg

@@ -57,6 +57,8 @@ struct xg_layout {
   int64_t ktot = 0;
   int32_t max_tab = 0;
   std::vector<int64_t> ring_pixels, kpad, koff;
+  std::vector<int64_t> mask_off;  // [rings + 1] offsets into colpos (mask order)
+  std::vector<int64_t> colpos;    // ring-major column of every mask entry
   int32_t* d_band_seg = nullptr;
   int32_t* d_band_wseg = nullptr;
   int32_t* d_seg_order = nullptr;
@@ -100,6 +102,30 @@ struct xg_series {
   int64_t tiles_for_t = -1;
   size_t g2part_cap = 0;
   bool have_raw = false;
+  // compressed path (allocated on first xg_compress)
+  int32_t ck = 0, ckp = 0;         // rank and plane row length of the last compress
+  double* d_y = nullptr;           // [ring][tp][k] coefficients
+  __nv_bfloat16* d_planes = nullptr;  // [(ring*3+s)*tp + t][kp]
+  float* d_cgram = nullptr;        // [ring][tp][tp] C~ upper tiles
+  double* d_cg2 = nullptr;
+  int64_t* d_cg2cnt = nullptr;
+  bool have_y = false, have_cttc = false;
+  TileDesc* d_ptiles = nullptr;    // projection tiles
+  int32_t n_ptiles = 0;
+  int64_t ptiles_key = -1;
+};
+
+struct xg_basis {
+  xg_ctx* ctx = nullptr;
+  const xg_layout* L = nullptr;
+  int32_t k = 0, digits = 3, kt = 0, ntiles_n = 0;
+  int64_t vrows = 0;               // digit rows = ntiles_n * digits * kt
+  std::vector<int8_t> h_vd;        // [vrows][ktot]
+  std::vector<double> h_scale;     // [rings][k]
+  std::vector<uint8_t> ring_set;
+  int8_t* d_vd = nullptr;
+  double* d_scale = nullptr;
+  bool dirty = true;
 };
 
 namespace {
@@ -146,6 +172,19 @@ void dfree(T*& p) {
 }
 
 int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+int make_map_bf16(xg_ctx* c, CUtensorMap* map, const void* base, int64_t cols, int64_t rows) {
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols * 2)};
+  cuuint32_t box[2] = {64, 128};  // 128-byte rows
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = c->encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                         strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(c, XG_ERR_CUDA, "cuTensorMapEncodeTiled(bf16) failed (%d)", (int)r);
+  return XG_OK;
+}
 
 int make_map_u8(xg_ctx* c, CUtensorMap* map, const void* base, int64_t cols, int64_t rows,
                 int64_t row_stride, uint32_t box_cols, uint32_t box_rows) {
@@ -280,6 +319,8 @@ int xg_layout_create(xg_ctx* c, int64_t full_pixels, int32_t n_rings,
   for (int32_t r = 0; r < n_rings; ++r)
     for (int64_t i = offsets[r]; i < offsets[r + 1]; ++i) cnt[(size_t)r * nb + indices[i] / L->band]++;
   L->ring_pixels.resize(n_rings);
+  L->mask_off.assign(offsets, offsets + n_rings + 1);
+  L->colpos.assign(static_cast<size_t>(offsets[n_rings]), 0);
   L->kpad.resize(n_rings);
   L->koff.resize(n_rings);
   std::vector<int64_t> segoff(static_cast<size_t>(n_rings) * nb, 0);
@@ -321,8 +362,10 @@ int xg_layout_create(xg_ctx* c, int64_t full_pixels, int32_t n_rings,
       s.len = static_cast<int32_t>(len);
       s.taboff = local;
       segs.push_back(s);
-      for (int64_t i = 0; i < n; ++i)
+      for (int64_t i = 0; i < n; ++i) {
         tab.push_back(static_cast<uint16_t>(indices[cursor[r] + i] - (int64_t)b * L->band));
+        L->colpos[cursor[r] + i] = s.dst + i;  // ring-major column of mask entry
+      }
       for (int64_t i = n; i < len; ++i) tab.push_back(0xFFFF);
       cursor[r] += n;
       local += static_cast<int32_t>(len);
@@ -482,6 +525,12 @@ void xg_series_destroy(xg_series* s) {
   dfree(s->d_nz_bits);
   dfree(s->d_g2tile);
   dfree(s->d_ib_tile_off);
+  dfree(s->d_y);
+  dfree(s->d_planes);
+  dfree(s->d_cgram);
+  dfree(s->d_cg2);
+  dfree(s->d_cg2cnt);
+  dfree(s->d_ptiles);
   delete s;
 }
 
@@ -621,6 +670,27 @@ static int run_g2(xg_series* s, int mode) {
   return XG_OK;
 }
 
+// Fold the per-tile diagonal sums left by a K2/K4 launch into g2 (fixed order).
+static int fold_g2(xg_series* s, double* g2, int64_t* cnt) {
+  xg_ctx* c = s->ctx;
+  G2FoldParams f;
+  f.g2_partial = s->d_g2tile;
+  f.ib_tile_off = s->d_ib_tile_off;
+  f.tiles_per_ring = s->tiles_per_ring;
+  f.nbi = static_cast<int32_t>((s->t + 127) / 128);
+  f.nbj = static_cast<int32_t>((s->t + 255) / 256);
+  f.n_frames = s->t;
+  f.n_rings = s->L->rings;
+  f.nz_bits = s->d_nz_bits;
+  f.nz_words = s->nz_words;
+  f.g2 = g2;
+  f.counts = cnt;
+  f.g2_ld = s->tp;
+  XG_CUDA(c, launch_g2_fold(f, c->stream));
+  c->launches++;
+  return XG_OK;
+}
+
 int xg_ttc_raw(xg_series* s, uint32_t flags) {
   if (!s) return XG_ERR_INVALID;
   xg_ctx* c = s->ctx;
@@ -650,7 +720,7 @@ int xg_ttc_raw(xg_series* s, uint32_t flags) {
   gp.ntiles = s->ntiles;
   gp.ring_koff = L->d_ring_koff;
   gp.ring_nkb = L->d_ring_nkb;
-  gp.gram = s->d_gram;
+  gp.gram = reinterpret_cast<uint32_t*>(s->d_gram);
   gp.ring_stride = s->tp * s->tp;
   gp.ld = static_cast<int32_t>(s->tp);
   gp.err = c->d_err;
@@ -662,21 +732,8 @@ int xg_ttc_raw(xg_series* s, uint32_t flags) {
   XG_CUDA(c, launch_gram_u8(map, gp, c->num_sms, c->stream));
   c->launches++;
   if (g2) {
-    G2FoldParams f;
-    f.g2_partial = s->d_g2tile;
-    f.ib_tile_off = s->d_ib_tile_off;
-    f.tiles_per_ring = s->tiles_per_ring;
-    f.nbi = static_cast<int32_t>((s->t + 127) / 128);
-    f.nbj = static_cast<int32_t>((s->t + 255) / 256);
-    f.n_frames = s->t;
-    f.n_rings = L->rings;
-    f.nz_bits = s->d_nz_bits;
-    f.nz_words = s->nz_words;
-    f.g2 = s->d_g2;
-    f.counts = s->d_g2cnt;
-    f.g2_ld = s->tp;
-    XG_CUDA(c, launch_g2_fold(f, c->stream));
-    c->launches++;
+    rc = fold_g2(s, s->d_g2, s->d_g2cnt);
+    if (rc) return rc;
   }
   s->have_raw = true;
   return XG_OK;
@@ -784,6 +841,277 @@ int xg_series_get_norms(xg_series* s, int32_t ring, double* norms, int64_t* n_ze
                                cudaMemcpyDeviceToHost, c->stream));
   if (n_zero)
     XG_CUDA(c, cudaMemcpyAsync(n_zero, s->d_zero + ring, 8, cudaMemcpyDeviceToHost, c->stream));
+  XG_CUDA(c, cudaStreamSynchronize(c->stream));
+  return check_device_error(c);
+}
+
+// ------------------------------------------------------------- compressed
+int xg_basis_create(xg_ctx* c, const xg_layout* L, int32_t k, int32_t digits, xg_basis** out) {
+  if (!c || !L || !out) return XG_ERR_INVALID;
+  *out = nullptr;
+  if (k < 1) return fail(c, XG_ERR_CONTRACT, "basis: k must be >= 1");
+  if (digits < 1 || digits > 3) return fail(c, XG_ERR_CONTRACT, "basis: digits must be 1..3");
+  xg_basis* B = new xg_basis();
+  B->ctx = c;
+  B->L = L;
+  B->k = k;
+  B->digits = digits;
+  // coefficients per N-tile: multiple of 16 with digits*kt <= 256
+  const int32_t kmax = (256 / digits) / 16 * 16;
+  const int32_t k16 = static_cast<int32_t>(round_up(k, 16));
+  B->ntiles_n = (k16 + kmax - 1) / kmax;
+  B->kt = static_cast<int32_t>(round_up((k16 + B->ntiles_n - 1) / B->ntiles_n, 16));
+  B->vrows = static_cast<int64_t>(B->ntiles_n) * digits * B->kt;
+  B->h_vd.assign(static_cast<size_t>(B->vrows * L->ktot), 0);
+  B->h_scale.assign(static_cast<size_t>(L->rings) * k, 0.0);
+  B->ring_set.assign(L->rings, 0);
+  cudaError_t e;
+  if ((e = dalloc(&B->d_vd, B->h_vd.size())) != cudaSuccess ||
+      (e = dalloc(&B->d_scale, B->h_scale.size())) != cudaSuccess) {
+    xg_basis_destroy(B);
+    return cuda_fail(c, e, "basis alloc");
+  }
+  *out = B;
+  return XG_OK;
+}
+
+void xg_basis_destroy(xg_basis* B) {
+  if (!B) return;
+  dfree(B->d_vd);
+  dfree(B->d_scale);
+  delete B;
+}
+
+// V (M_q x k, mask order, f64) -> per-column scale and S int8 digits:
+// V ~= scale * (d0 + d1/254 + d2/254^2), written at the ring-major columns.
+int xg_basis_set_ring(xg_basis* B, int32_t ring, const double* v) {
+  if (!B || !v) return XG_ERR_INVALID;
+  xg_ctx* c = B->ctx;
+  const xg_layout* L = B->L;
+  if (ring < 0 || ring >= L->rings) return fail(c, XG_ERR_SHAPE, "basis: ring %d out of range", ring);
+  const int64_t m = L->ring_pixels[ring], k = B->k;
+  const int64_t* col = L->colpos.data() + L->mask_off[ring];
+  for (int64_t j = 0; j < k; ++j) {
+    double amax = 0.0;
+    for (int64_t i = 0; i < m; ++i) {
+      const double x = v[i * k + j];
+      if (!std::isfinite(x)) return fail(c, XG_ERR_CONTRACT, "basis: non-finite entry");
+      amax = std::max(amax, std::fabs(x));
+    }
+    const double scale = amax > 0.0 ? amax / 127.0 : 1.0;
+    B->h_scale[(size_t)ring * k + j] = scale;
+    const int64_t nt = j / B->kt, jj = j % B->kt;
+    for (int64_t i = 0; i < m; ++i) {
+      double u = v[i * k + j] / scale;
+      for (int s = 0; s < B->digits; ++s) {
+        double d = std::nearbyint(u);
+        d = std::min(127.0, std::max(-127.0, d));
+        const int64_t row = (nt * B->digits + s) * B->kt + jj;
+        B->h_vd[(size_t)(row * L->ktot + col[i])] = static_cast<int8_t>(d);
+        u = (u - d) * 254.0;
+      }
+    }
+  }
+  B->ring_set[ring] = 1;
+  B->dirty = true;
+  return XG_OK;
+}
+
+int xg_compress(xg_series* s, const xg_basis* Bc, uint32_t flags) {
+  if (!s || !Bc) return XG_ERR_INVALID;
+  xg_ctx* c = s->ctx;
+  xg_basis* B = const_cast<xg_basis*>(Bc);
+  const xg_layout* L = s->L;
+  if (B->L != L) return fail(c, XG_ERR_BINDING, "compress: basis built for another layout");
+  if (s->t < 1) return fail(c, XG_ERR_CONTRACT, "compress: no frames loaded");
+  for (int32_t r = 0; r < L->rings; ++r)
+    if (!B->ring_set[r]) return fail(c, XG_ERR_CONTRACT, "compress: basis of ring %d not set", r);
+  if (flags & XG_STRICT) {
+    std::vector<int64_t> fz(L->rings);
+    XG_CUDA(c, cudaMemcpyAsync(fz.data(), s->d_first_zero, fz.size() * 8, cudaMemcpyDeviceToHost,
+                               c->stream));
+    XG_CUDA(c, cudaStreamSynchronize(c->stream));
+    for (int32_t r = 0; r < L->rings; ++r)
+      if (fz[r] != kNoZero) {
+        c->payload = fz[r];
+        c->payload_ring = r;
+        return fail(c, XG_ERR_NORMALIZATION,
+                    "compress_series: frame %lld of ring %d has zero norm", (long long)fz[r], r);
+      }
+  }
+  if (B->dirty) {
+    XG_CUDA(c, cudaMemcpy(B->d_vd, B->h_vd.data(), B->h_vd.size(), cudaMemcpyHostToDevice));
+    XG_CUDA(c, cudaMemcpy(B->d_scale, B->h_scale.data(), B->h_scale.size() * 8,
+                          cudaMemcpyHostToDevice));
+    B->dirty = false;
+  }
+  const int32_t kp = static_cast<int32_t>(round_up(B->k, 64));
+  if (s->ck != B->k || !s->d_y) {
+    dfree(s->d_y);
+    dfree(s->d_planes);
+    XG_CUDA(c, dalloc(&s->d_y, (size_t)L->rings * s->tp * B->k));
+    XG_CUDA(c, dalloc(&s->d_planes, (size_t)L->rings * 3 * s->tp * kp));
+    XG_CUDA(c, cudaMemsetAsync(s->d_planes, 0, (size_t)L->rings * 3 * s->tp * kp * 2, c->stream));
+    s->ck = B->k;
+    s->ckp = kp;
+  }
+  // tiles: (ring, frame block, N-tile), cached per (frames, N-tiles)
+  const int64_t key = s->t * 64 + B->ntiles_n;
+  if (s->ptiles_key != key) {
+    std::vector<TileDesc> tiles;
+    const int64_t nbi = (s->t + 127) / 128;
+    for (int32_t r = 0; r < L->rings; ++r)
+      for (int64_t ib = 0; ib < nbi; ++ib)
+        for (int32_t nt = 0; nt < B->ntiles_n; ++nt)
+          tiles.push_back({r, (int32_t)(ib * 128), nt, 0});
+    dfree(s->d_ptiles);
+    XG_CUDA(c, dalloc(&s->d_ptiles, tiles.size()));
+    XG_CUDA(c, cudaMemcpy(s->d_ptiles, tiles.data(), tiles.size() * sizeof(TileDesc),
+                          cudaMemcpyHostToDevice));
+    s->n_ptiles = static_cast<int32_t>(tiles.size());
+    s->ptiles_key = key;
+  }
+  CUtensorMap mx, mv;
+  int rc = make_map_u8(c, &mx, s->d_x, L->ktot, s->t, L->ktot, 128, 128);
+  if (!rc) rc = make_map_u8(c, &mv, B->d_vd, L->ktot, B->vrows, L->ktot, 128, 128);
+  if (rc) return rc;
+  ProjParams p;
+  p.tiles = s->d_ptiles;
+  p.ntiles = s->n_ptiles;
+  p.ring_koff = L->d_ring_koff;
+  p.ring_nkb = L->d_ring_nkb;
+  p.n_digits = B->digits;
+  p.kt = B->kt;
+  p.k = B->k;
+  p.inv = s->d_inv;
+  p.inv_ld = s->tp;
+  p.n_frames = s->t;
+  p.scale = B->d_scale;
+  p.y = s->d_y;
+  p.y_ld = s->tp;
+  p.planes = s->d_planes;
+  p.plane_rows = s->tp;
+  p.kp = kp;
+  p.err = c->d_err;
+  XG_CUDA(c, launch_project(mx, mv, p, c->num_sms, c->stream));
+  c->launches++;
+  s->have_y = true;
+  s->have_cttc = false;
+  return XG_OK;
+}
+
+int xg_ttc_compressed(xg_series* s, uint32_t flags) {
+  if (!s) return XG_ERR_INVALID;
+  xg_ctx* c = s->ctx;
+  const xg_layout* L = s->L;
+  if (!s->have_y) return fail(c, XG_ERR_CONTRACT, "ttc_compressed: compress first");
+  if (s->t < 2) return fail(c, XG_ERR_CONTRACT, "ttc_compressed: need at least 2 frames");
+  if (!s->d_cgram) {
+    XG_CUDA(c, dalloc(&s->d_cgram, (size_t)L->rings * s->tp * s->tp));
+    XG_CUDA(c, dalloc(&s->d_cg2, (size_t)L->rings * s->tp));
+    XG_CUDA(c, dalloc(&s->d_cg2cnt, (size_t)L->rings * s->tp));
+  }
+  int rc = build_tiles(s);
+  if (rc) return rc;
+  CUtensorMap my;
+  rc = make_map_bf16(c, &my, s->d_planes, s->ckp, (int64_t)L->rings * 3 * s->tp);
+  if (rc) return rc;
+  GramParams gp;
+  gp.tiles = s->d_tiles;
+  gp.ntiles = s->ntiles;
+  gp.ring_koff = L->d_ring_koff;
+  gp.ring_nkb = L->d_ring_nkb;
+  gp.gram = reinterpret_cast<uint32_t*>(s->d_cgram);
+  gp.ring_stride = s->tp * s->tp;
+  gp.ld = static_cast<int32_t>(s->tp);
+  gp.err = c->d_err;
+  const bool g2 = !(flags & XG_NO_G2);
+  gp.inv = s->d_inv;
+  gp.inv_ld = s->tp;
+  gp.n_frames = s->t;
+  gp.g2_partial = g2 ? s->d_g2tile : nullptr;
+  if (flags & XG_CMP_BF16) {  // single bf16 product: hi x hi
+    gp.n_pairs = 1;
+    gp.pairs = 0x0;
+  } else {  // (0,0) (0,1) (1,0) (0,2) (2,0) (1,1): ~24-bit products, f32 accumulate
+    const int pa[6] = {0, 0, 1, 0, 2, 1}, pb[6] = {0, 1, 0, 2, 0, 1};
+    gp.n_pairs = 6;
+    gp.pairs = 0;
+    for (int i = 0; i < 6; ++i) gp.pairs |= (pa[i] | (pb[i] << 2)) << (4 * i);
+  }
+  gp.kb_per_plane = s->ckp / 64;
+  gp.plane_rows = static_cast<int32_t>(s->tp);
+  XG_CUDA(c, launch_gram_cmp(my, gp, c->num_sms, c->stream));
+  c->launches++;
+  if (g2) {
+    rc = fold_g2(s, s->d_cg2, s->d_cg2cnt);
+    if (rc) return rc;
+  }
+  s->have_cttc = true;
+  return XG_OK;
+}
+
+int xg_series_get_coeffs(xg_series* s, int32_t ring, double* y, double* norms) {
+  if (!s) return XG_ERR_INVALID;
+  xg_ctx* c = s->ctx;
+  if (ring < 0 || ring >= s->L->rings) return fail(c, XG_ERR_SHAPE, "ring %d out of range", ring);
+  if (!s->have_y) return fail(c, XG_ERR_CONTRACT, "get_coeffs: compress first");
+  if (y)
+    XG_CUDA(c, cudaMemcpyAsync(y, s->d_y + (int64_t)ring * s->tp * s->ck,
+                               (size_t)s->t * s->ck * 8, cudaMemcpyDeviceToHost, c->stream));
+  if (norms)
+    XG_CUDA(c, cudaMemcpyAsync(norms, s->d_norms + (int64_t)ring * s->tp, (size_t)s->t * 8,
+                               cudaMemcpyDeviceToHost, c->stream));
+  XG_CUDA(c, cudaStreamSynchronize(c->stream));
+  return check_device_error(c);
+}
+
+int xg_series_get_cttc(xg_series* s, int32_t ring, int32_t dtype, void* out, int64_t ld,
+                       int out_on_device) {
+  if (!s || !out) return XG_ERR_INVALID;
+  xg_ctx* c = s->ctx;
+  if (ring < 0 || ring >= s->L->rings) return fail(c, XG_ERR_SHAPE, "ring %d out of range", ring);
+  if (!s->have_cttc) return fail(c, XG_ERR_CONTRACT, "get_cttc: no compressed TTC yet");
+  if (dtype != XG_F64 && dtype != XG_F32) return fail(c, XG_ERR_CONTRACT, "get_cttc: bad dtype");
+  if (ld < s->t) return fail(c, XG_ERR_SHAPE, "get_cttc: ld < n");
+  const size_t bytes = (size_t)s->t * ld * (dtype == XG_F64 ? 8 : 4);
+  void* dst = out;
+  void* tmp = nullptr;
+  if (!out_on_device) {
+    XG_CUDA(c, cudaMalloc(&tmp, bytes));
+    dst = tmp;
+  }
+  ExpandParams p;
+  p.gram = nullptr;
+  p.cf32 = s->d_cgram + (int64_t)ring * s->tp * s->tp;
+  p.ring_stride = 0;
+  p.ld = static_cast<int32_t>(s->tp);
+  p.inv = nullptr;
+  p.n = s->t;
+  p.out = dst;
+  p.out_ld = ld;
+  p.out_dtype = dtype;
+  cudaError_t e = launch_expand(p, 1, c->stream);
+  c->launches++;
+  if (e == cudaSuccess && tmp) {
+    e = cudaMemcpyAsync(out, tmp, bytes, cudaMemcpyDeviceToHost, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  }
+  if (tmp) cudaFree(tmp);
+  if (e != cudaSuccess) return cuda_fail(c, e, "get_cttc");
+  return check_device_error(c);
+}
+
+int xg_series_get_cg2(xg_series* s, int32_t ring, double* values, int64_t* counts) {
+  if (!s || !values) return XG_ERR_INVALID;
+  xg_ctx* c = s->ctx;
+  if (ring < 0 || ring >= s->L->rings) return fail(c, XG_ERR_SHAPE, "ring %d out of range", ring);
+  if (!s->have_cttc) return fail(c, XG_ERR_CONTRACT, "get_cg2: no compressed TTC yet");
+  XG_CUDA(c, cudaMemcpyAsync(values, s->d_cg2 + (int64_t)ring * s->tp, (size_t)s->t * 8,
+                             cudaMemcpyDeviceToHost, c->stream));
+  if (counts)
+    XG_CUDA(c, cudaMemcpyAsync(counts, s->d_cg2cnt + (int64_t)ring * s->tp, (size_t)s->t * 8,
+                               cudaMemcpyDeviceToHost, c->stream));
   XG_CUDA(c, cudaStreamSynchronize(c->stream));
   return check_device_error(c);
 }

@@ -2,6 +2,7 @@
 // (xg_api.cu) and the kernel translation units.  Internal; not installed.
 #pragma once
 #include <cuda.h>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <cstddef>
@@ -77,7 +78,7 @@ struct GramParams {
   int32_t ntiles;
   const int32_t* ring_koff;  // byte column of each ring in the ring-major row
   const int32_t* ring_nkb;   // 128-byte K blocks per ring
-  int32_t* gram;             // [ring][ld][ld] exact int32 Gram (upper tiles)
+  uint32_t* gram;            // [ring][ld][ld] exact int32 Gram / f32 C~ (upper tiles)
   int64_t ring_stride;
   int32_t ld;
   int* err;                  // bit 0: pipeline timeout
@@ -87,8 +88,17 @@ struct GramParams {
   int64_t inv_ld;
   int64_t n_frames;
   double* g2_partial;        // [ntiles][384]
+  // compressed mode (launch_gram_cmp): K blocks run over precision pairs
+  // (plane_a, plane_b) packed 4 bits each in `pairs`, kb_per_plane 64-element
+  // blocks per plane; plane rows of ring r, plane s start at (3r+s)*plane_rows
+  int32_t n_pairs;
+  int32_t pairs;
+  int32_t kb_per_plane;
+  int32_t plane_rows;
 };
 size_t gram_u8_smem_bytes();
+cudaError_t launch_gram_cmp(const CUtensorMap& tmY, const GramParams& p, int num_sms,
+                            cudaStream_t stream);
 
 // Fold the per-tile diagonal sums of K2 into g2[ring][d] (fixed order) and
 // count the valid (t, t+d) pairs from the nonzero-frame bitmask.
@@ -108,6 +118,30 @@ struct G2FoldParams {
 cudaError_t launch_g2_fold(const G2FoldParams& p, cudaStream_t s);
 cudaError_t launch_gram_u8(const CUtensorMap& tmX, const GramParams& p, int num_sms,
                            cudaStream_t stream);
+
+// ------------------------------------------------------ K3 projection
+struct ProjParams {
+  const TileDesc* tiles;     // (ring, i0 = first frame, j0 = N-tile index)
+  int32_t ntiles;
+  const int32_t* ring_koff;
+  const int32_t* ring_nkb;
+  int32_t n_digits;          // S in {1, 2, 3}
+  int32_t kt;                // coefficients per N-tile (multiple of 16, S*kt <= 256)
+  int32_t k;                 // rank
+  const double* inv;         // [ring][inv_ld] 1/|x_t|
+  int64_t inv_ld;
+  int64_t n_frames;
+  const double* scale;       // [ring][k] digit scale of each basis column
+  double* y;                 // [ring][y_ld][k] coefficients (f64)
+  int64_t y_ld;
+  __nv_bfloat16* planes;     // [(ring*3 + s) * plane_rows + t][kp] bf16 split of y (or null)
+  int64_t plane_rows;
+  int32_t kp;                // plane row length (multiple of 64)
+  int* err;
+};
+size_t project_smem_bytes();
+cudaError_t launch_project(const CUtensorMap& tmX, const CUtensorMap& tmV, const ProjParams& p,
+                           int num_sms, cudaStream_t stream);
 
 // --------------------------------------------------------------- K7 g2
 // g2[r][d] = sum_{t} G(t,t+d) inv_t inv_{t+d} / count, ascending t within

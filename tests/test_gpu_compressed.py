@@ -1,0 +1,100 @@
+"""Compressed-path parity on the GPU (K3 tcgen05 int8-digit projection, K4
+tcgen05 bf16x3 compressed Gram, fused g2) against the CPU oracle with the
+SAME basis V (the reference's own build_online_from_frames when oracle/_ref
+is built, else an orthonormal basis from the oracle fixture).
+
+Tolerances (BASELINE north_star): F32-accurate mode within 1e-5 relative
+(max|dC| / max|C_ref|); BF16 mode within 1e-2.  Coefficients are checked at
+1e-6 of max|Y| (3 int8 digits represent V to ~3e-8 of max|V_j|)."""
+import numpy as np
+import pytest
+
+import paper_2407_20356_b200 as xg
+
+pytestmark = pytest.mark.gpu
+
+
+def _basis(orc, xq, k, seed):
+    """Orthonormal M_q x k basis from a training prefix (QR of the
+    row-normalised frames' transpose; parity needs only a fixed V)."""
+    try:
+        import oracle
+
+        if oracle.ref_available():
+            v, _ = oracle.ref().build_online_from_frames(xq[: max(2 * k, 64)].astype(np.float64), k)
+            return v
+    except Exception:
+        pass
+    rng = np.random.default_rng(seed)
+    q, _ = np.linalg.qr(rng.standard_normal((xq.shape[1], k)))
+    return q
+
+
+@pytest.mark.parametrize("t,h,w,q,mu,k,seed", [
+    (300, 64, 64, 4, 0.3, 16, 41),
+    (200, 48, 48, 3, 0.5, 32, 42),
+    (260, 64, 64, 2, 0.4, 64, 43),
+])
+def test_compress_and_ttc_compressed(ctx, orc, t, h, w, q, mu, k, seed):
+    frames = orc.gen_speckle(t, h, w, q, mu, seed)
+    ring, _ = orc.ring_map(h, w, q)
+    lay = xg.RingLayout.from_ring_map(ctx, ring, q)
+    s = xg.FrameSeries(lay, t).load(frames)
+    basis = xg.Basis(lay, k)
+    vs = []
+    for r in range(q):
+        xq = frames[:, ring == r]
+        v = _basis(orc, xq, k, seed + r)
+        vs.append(v)
+        basis.set_ring(r, v)
+    s.compress(basis).ttc_compressed()
+    for r in range(q):
+        xq = frames[:, ring == r].astype(np.float64)
+        y_ref, n_ref = orc.compress_series(xq, vs[r])
+        y, nrm = s.coeffs(r)
+        assert np.array_equal(nrm, n_ref)
+        assert np.abs(y - y_ref).max() <= 1e-6 * np.abs(y_ref).max()
+        c_ref, _ = orc.ttc_compressed(y_ref)
+        c = s.cttc(r)
+        rel = np.abs(c - c_ref).max() / np.abs(c_ref).max()
+        assert rel <= 1e-5, rel
+        _, g2_ref, cnt_ref = orc.g2_from_ttc(c_ref)
+        _, g2, cnt = s.cg2(r)
+        assert np.array_equal(cnt, cnt_ref)
+        assert np.abs(g2 - g2_ref).max() <= 1e-5 * np.abs(g2_ref).max()
+
+
+def test_bf16_mode_within_1e2(ctx, orc):
+    t, h, w, q, k = 256, 64, 64, 2, 32
+    frames = orc.gen_speckle(t, h, w, q, 0.3, 51)
+    ring, _ = orc.ring_map(h, w, q)
+    lay = xg.RingLayout.from_ring_map(ctx, ring, q)
+    s = xg.FrameSeries(lay, t).load(frames)
+    basis = xg.Basis(lay, k, digits=2)
+    vs = [_basis(orc, frames[:, ring == r], k, 60 + r) for r in range(q)]
+    for r in range(q):
+        basis.set_ring(r, vs[r])
+    s.compress(basis).ttc_compressed(mode="bf16")
+    for r in range(q):
+        y_ref, _ = orc.compress_series(frames[:, ring == r].astype(np.float64), vs[r])
+        c_ref, _ = orc.ttc_compressed(y_ref)
+        assert np.abs(s.cttc(r) - c_ref).max() <= 1e-2 * np.abs(c_ref).max()
+
+
+def test_full_rank_homomorphic_identity(ctx, orc):
+    """Full-rank offline basis: C~ reproduces the raw TTC (Eq. 11 of the
+    paper; reference test_correlate.cpp:58-65 at 1e-10 in f64) -- here to the
+    F32-mode tolerance."""
+    t, h, w, q = 96, 32, 32, 1
+    frames = orc.gen_speckle(t, h, w, q, 1.0, 71)
+    ring = np.zeros(h * w, np.int32)
+    xn, _ = orc.row_normalize(frames.astype(np.float64))
+    # orthonormal basis of the row space (full rank k = t)
+    qm, _ = np.linalg.qr(xn.T)
+    k = qm.shape[1]
+    lay = xg.RingLayout.from_ring_map(ctx, ring, q)
+    s = xg.FrameSeries(lay, t).load(frames).ttc_raw()
+    basis = xg.Basis(lay, k).set_ring(0, qm)
+    s.compress(basis).ttc_compressed()
+    c_raw = s.ttc(0)
+    assert np.abs(s.cttc(0) - c_raw).max() <= 1e-5
