@@ -222,6 +222,80 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def run_compressed(args, torch, xg, ctx, stream, frames, series, ring, sizes, mine, world, dev):
+    """Rank-k path on the same frames: basis per ring from a 256-frame
+    training prefix (untimed, host f64 Gram-trick SVD), then per step
+    ingest (K1) -> int8-digit projection (K3) -> bf16x3 compressed Gram with
+    fused g2 (K4)."""
+    cfg = CFG
+    T, k = cfg["T"], cfg["k"]
+    t_train = 256
+    prior = frames[:t_train].cpu().numpy()
+    t0 = time.perf_counter()
+    vs = xg.build_ring_bases([prior[:, ring == r] for r in mine], k)
+    t_basis = time.perf_counter() - t0
+    basis = xg.Basis(series.layout, k)
+    for i, v in enumerate(vs):
+        basis.set_ring(i, v)
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+
+    def step(rec=None):
+        series.load(frames)
+        if rec:
+            rec[0].record(stream)
+        series.compress(basis)
+        if rec:
+            rec[1].record(stream)
+        series.ttc_compressed()
+        if rec:
+            rec[2].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    ctx.synchronize()
+    recs = [(ev(), ev(), ev()) for _ in range(args.steps)]
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    a, b = ev(), ev()
+    a.record(stream)
+    for i in range(args.steps):
+        step(recs[i])
+    b.record(stream)
+    torch.cuda.synchronize()
+    ctx.synchronize()
+    ms = a.elapsed_time(b) / args.steps
+    proj_ms = statistics.mean(r[0].elapsed_time(r[1]) for r in recs)
+    cg_ms = statistics.mean(r[1].elapsed_time(r[2]) for r in recs)
+    if world > 1:
+        tt = torch.tensor([ms, proj_ms, cg_ms], device=dev)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        ms, proj_ms, cg_ms = (float(x) for x in tt)
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    my_m = float(sum(sizes[r] for r in mine))
+    q = len(mine)
+    kp = (k + 63) // 64 * 64
+    proj_bytes = T * my_m + 3 * k * my_m + T * q * k * 8 + 3 * T * q * kp * 2
+    cg_flops_alg = q * T * (T + 1) * k
+    cg_flops_mma = 6 * q * T * (T + 1) * k
+    return {
+        "value": T / (ms / 1e3), "unit": "frames/s", "ms_per_step": ms, "k": k,
+        "mode": "F32-accurate (3 int8 digits of V; bf16x3 split Y, 6 products, fp32 accumulate)",
+        "basis": f"per ring from the first {t_train} frames (host Gram-trick SVD, {t_basis:.1f} s, untimed)",
+        "projection": {"kernel": "k_project (K3)", "bound": "hbm", "ms": proj_ms,
+                       "achieved": proj_bytes / (proj_ms / 1e3) / 1e9, "peak": peaks["hbm_gbs"],
+                       "unit": "GB/s", "frac": proj_bytes / (proj_ms / 1e3) / 1e9 / peaks["hbm_gbs"],
+                       "bytes": proj_bytes},
+        "gram": {"kernel": "k_gram_tc<1> (K4, fused g2) + fold", "bound": "tensor", "ms": cg_ms,
+                 "achieved_algorithmic": cg_flops_alg / (cg_ms / 1e3) / 1e12,
+                 "achieved_mma": cg_flops_mma / (cg_ms / 1e3) / 1e12,
+                 "peak": peaks["bf16_tflops"], "unit": "TFLOP/s (bf16)",
+                 "frac": cg_flops_mma / (cg_ms / 1e3) / 1e12 / peaks["bf16_tflops"],
+                 "c_bytes_written": q * (T * T / 2) * 4},
+    }
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -230,6 +304,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--no-compressed", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -367,6 +442,11 @@ def main():
                    "l2": f"inputs {T * P / 1e9:.2f} GB > 126 MB L2 (no flush needed)"},
         "roofline": roofline, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
     }
+
+    # ---------------------------------------------------------- compressed (rank-k)
+    if not args.no_compressed:
+        line["compressed"] = run_compressed(args, torch, xg, ctx, stream, frames, series, ring,
+                                           sizes, mine, world, dev)
 
     # ---------------------------------------------------------- CPU baseline
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

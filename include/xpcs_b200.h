@@ -127,6 +127,18 @@ XG_API int64_t xg_series_frames(const xg_series* s);
  * exact integer accumulation, f64 combination.  xg_ttc_compressed =
  * ttc_compressed (correlate.cpp:27-35): C~_q = Y_q Y_q^T on tcgen05 bf16 tensor
  * cores (bf16x3 split, or XG_CMP_BF16) + fused g2. */
+/* Basis construction (host, f64; untimed setup).  The reference's
+ * encoder_from_rows (encoder.cpp:13-28): row_normalize -> Gram-trick SVD
+ * (linalg.cpp:279-439, cyclic Jacobi, measured sigma, rank at 1e-12 sigma_max,
+ * 2x MGS, largest entry positive) -> first k right vectors.  k = 0 keeps the
+ * full numerical rank (build_offline).  Returns XG_ERR_RANK with the
+ * achievable rank in *rank_out when k exceeds it, XG_ERR_NORMALIZATION with
+ * the zero frame in *rank_out. */
+XG_API int xg_build_basis(const double* x, int64_t n, int64_t m, int32_t k, double* v_out,
+                          double* sigma_out, int64_t* rank_out);
+XG_API int xg_build_basis_batch(int32_t n_rings, const double* const* x_ring, int64_t n,
+                                const int64_t* m_ring, int32_t k, double* const* v_ring,
+                                int32_t threads, int64_t* rank_out);
 XG_API int xg_basis_create(xg_ctx* ctx, const xg_layout* layout, int32_t k, int32_t digits,
                            xg_basis** out);
 XG_API void xg_basis_destroy(xg_basis* basis);

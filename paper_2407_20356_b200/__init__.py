@@ -156,6 +156,52 @@ class RingLayout:
 
 
 # ------------------------------------------------------------------ basis
+def build_online_from_frames(prior: np.ndarray, k: int) -> np.ndarray:
+    """V (m x k) from a prior series (encoder.cpp:53-60); k = 0 -> full
+    numerical rank (build_offline, encoder.cpp:32-37).  Host f64 setup."""
+    x = np.ascontiguousarray(prior, dtype=np.float64)
+    n, m = x.shape
+    if n < 2:
+        raise ContractError("build_online_from_frames: need at least 2 frames")
+    if k < 0:
+        raise ContractError("build_online_from_frames: k must be >= 1")
+    rank = C.c_int64(0)
+    kk = k if k > 0 else n
+    v = np.empty((m, kk), np.float64)
+    sig = np.empty(n, np.float64)
+    rc = lib.xg_build_basis(x.ctypes.data_as(_abi.PD), n, m, k, v.ctypes.data_as(_abi.PD),
+                            sig.ctypes.data_as(_abi.PD), C.byref(rank))
+    if rc == _abi.ERR_RANK:
+        raise RankError(f"requested k = {k} exceeds the numerical rank {rank.value}",
+                        int(rank.value))
+    if rc == _abi.ERR_NORMALIZATION:
+        raise NormalizationError(f"frame {rank.value} has zero norm", int(rank.value))
+    if rc != _abi.OK:
+        raise ContractError(f"build_basis failed with status {rc}")
+    if k == 0:
+        v = np.ascontiguousarray(v.ravel()[: m * rank.value].reshape(m, rank.value))
+    return v
+
+
+def build_ring_bases(prior_per_ring: Sequence[np.ndarray], k: int, threads: int = 0):
+    """build_online_from_frames for every ring on parallel host threads."""
+    xs = [np.ascontiguousarray(x, dtype=np.float64) for x in prior_per_ring]
+    n = xs[0].shape[0]
+    vs = [np.empty((x.shape[1], k), np.float64) for x in xs]
+    q = len(xs)
+    xp = (_abi.PD * q)(*[x.ctypes.data_as(_abi.PD) for x in xs])
+    vp = (_abi.PD * q)(*[v.ctypes.data_as(_abi.PD) for v in vs])
+    ms = np.array([x.shape[1] for x in xs], np.int64)
+    ranks = np.zeros(q, np.int64)
+    rc = lib.xg_build_basis_batch(q, xp, n, ms.ctypes.data_as(_abi.PI64), k, vp, threads,
+                                  ranks.ctypes.data_as(_abi.PI64))
+    if rc == _abi.ERR_RANK:
+        raise RankError(f"k = {k} exceeds a ring's numerical rank", int(ranks.min()))
+    if rc != _abi.OK:
+        raise ContractError(f"build_ring_bases failed with status {rc}")
+    return vs
+
+
 class Basis:
     """Per-ring rank-k encoding matrices (EncodingMatrix, model.hpp:53-67) on
     the device, as `digits` signed-int8 planes per column (3: ~3e-8 of

@@ -52,6 +52,9 @@ _sigs = {
     "xg_series_frames": (I64, [P]),
     "xg_synth_speckle": (C.c_int, [P, I64, I64, I64, I32, C.c_double, I32, C.c_double,
                                    C.c_uint64, P]),
+    "xg_build_basis": (C.c_int, [PD, I64, I64, I32, PD, PD, PI64]),
+    "xg_build_basis_batch": (C.c_int, [I32, C.POINTER(PD), I64, PI64, I32, C.POINTER(PD), I32,
+                                       PI64]),
     "xg_basis_create": (C.c_int, [P, P, I32, I32, C.POINTER(P)]),
     "xg_basis_destroy": (None, [P]),
     "xg_basis_set_ring": (C.c_int, [P, I32, PD]),
