@@ -48,7 +48,8 @@ constexpr uint32_t gram_idesc() {
 constexpr int NDIAG = BM + BN - 1;         // tile diagonals j-i in [-127, 255]
 constexpr int NDIAG_PAD = 384;
 
-struct __align__(16) GramSmemTail {
+struct __align__(1024) GramSmemTail {
+  uint32_t stage[4][32 * 32];              // per-warp 32x32 output chunk, 128B-swizzled
   uint64_t full[STAGES];
   uint64_t empty[STAGES];
   uint64_t tfull[2];
@@ -59,7 +60,6 @@ struct __align__(16) GramSmemTail {
   double inv_row[BM];                      // 1/|x_i| of the tile rows (0 beyond T / zero frame)
   double inv_col[BN];                      // 1/|x_j| of the tile columns
   double acc[4][NDIAG_PAD];                // per-warp diagonal sums of the tile
-  uint32_t stage[4][32][33];               // per-warp 32x32 chunk (s32 or f32 bits)
 };
 
 __device__ __forceinline__ void epi_bar() {  // the 4 epilogue warps only
@@ -72,7 +72,8 @@ size_t gram_u8_smem_bytes() { return 1024 + STAGES * STAGE_BYTES + sizeof(GramSm
 
 template <int MODE>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
-    k_gram_tc(const __grid_constant__ CUtensorMap tmX, GramParams p) {
+    k_gram_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmOut,
+              GramParams p) {
   constexpr uint32_t IDESC = gram_idesc<MODE>();
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte alignment for the 128B-swizzle atoms; offsetting the shared
@@ -97,6 +98,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     fence_barrier_init();
     tma_prefetch(&tmX);
+    tma_prefetch(&tmOut);
   }
   if (warp == 2) tmem_alloc(&tail->tmem_base, TMEM_COLS);
   tc_fence_before();
@@ -216,25 +218,35 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int e = lane; e < NDIAG_PAD; e += 32) tail->acc[sub][e] = 0.0;
         epi_bar();
       }
-      uint32_t* gout = p.gram + static_cast<int64_t>(td.ring) * p.ring_stride +
-                      static_cast<int64_t>(td.i0 + row) * p.ld + td.j0;
       const uint32_t tbase =
           tmem_base + static_cast<uint32_t>(acc * BN) + (static_cast<uint32_t>(sub * 32) << 16);
+      // output rows of this warp in the [ring*ld + row][col] view of the map
+      const int out_row = td.ring * p.ld + td.i0 + 32 * sub;
+      uint32_t* S = tail->stage[sub];  // 32 rows x 128 B, 128B-swizzled
 #pragma unroll 1
       for (int c = 0; ok && c < BN / 32; ++c) {
         uint32_t r[32];
         tmem_ld32(tbase + c * 32, r);
         tmem_ld_wait();
-        int4* dst = reinterpret_cast<int4*>(gout + c * 32);
+        // the previous chunk's TMA store must have finished reading S
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncwarp();
+        // row `lane`, 16-byte chunk q stored at chunk q ^ (lane & 7)
 #pragma unroll
-        for (int v = 0; v < 8; ++v)
-          dst[v] = make_int4(static_cast<int>(r[4 * v]), static_cast<int>(r[4 * v + 1]),
-                             static_cast<int>(r[4 * v + 2]), static_cast<int>(r[4 * v + 3]));
+        for (int q = 0; q < 8; ++q)
+          *reinterpret_cast<uint4*>(S + lane * 32 + ((q ^ (lane & 7)) << 2)) =
+              make_uint4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
+        fence_proxy_async();  // generic-proxy smem writes -> visible to the TMA engine
+        __syncwarp();
+        if (lane == 0) {
+          asm volatile(
+              "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                  reinterpret_cast<uint64_t>(&tmOut)),
+              "r"(smem_u32(S)), "r"(td.j0 + 32 * c), "r"(out_row)
+              : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
         if (p.g2_partial) {
-          uint32_t(*S)[33] = tail->stage[sub];
-#pragma unroll
-          for (int k = 0; k < 32; ++k) S[lane][k] = r[k];
-          __syncwarp();
           // global lag of chunk element (l, k): D0 + (k - l)
           const int D0 = td.j0 + 32 * c - td.i0 - 32 * sub;
           const double* ir = tail->inv_row + 32 * sub;
@@ -242,21 +254,29 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           // Lane L sums chunk diagonals m_B = L+1 (rows l < 31-L) then
           // m_A = L-31 (rows l >= 31-L): element (l, (l+L+1) mod 32) at step l,
           // one warp-uniform 32-step loop, conflict-free rows of S.
-          double sa = 0.0, sb = 0.0, run = 0.0;
+          // four interleaved partial sums (l mod 4) keep the f64 chains short
+          double sa = 0.0, sb = 0.0, r0 = 0.0, r1 = 0.0, r2 = 0.0, r3 = 0.0;
           const int ma = lane - 31, mb = lane + 1;
           const bool use_a = D0 + ma >= 0, use_b = lane < 31 && D0 + mb >= 0;
 #pragma unroll
           for (int l = 0; l < 32; ++l) {
             if (l == 31 - lane) {
-              sb = run;
-              run = 0.0;
+              sb = (r0 + r1) + (r2 + r3);
+              r0 = r1 = r2 = r3 = 0.0;
             }
             const int k = (l + lane + 1) & 31;
-            const double v = MODE == 0 ? static_cast<double>(static_cast<int32_t>(S[l][k]))
-                                       : static_cast<double>(__uint_as_float(S[l][k]));
-            run = fma(v, ir[l] * ic[k], run);
+            const uint32_t w = S[l * 32 + ((((k >> 2) ^ (l & 7))) << 2) + (k & 3)];
+            double v;
+            if (MODE == 0)
+              v = static_cast<double>(static_cast<int32_t>(w)) * (ir[l] * ic[k]);
+            else  // compressed: C~ is already normalised (inv = 1 inside T)
+              v = ic[k] != 0.0 ? static_cast<double>(__uint_as_float(w)) : 0.0;
+            if ((l & 3) == 0) r0 += v;
+            else if ((l & 3) == 1) r1 += v;
+            else if ((l & 3) == 2) r2 += v;
+            else r3 += v;
           }
-          sa = run;
+          sa = (r0 + r1) + (r2 + r3);
           if (!use_a) sa = 0.0;
           if (!use_b) sb = 0.0;
           // tile diagonal index (j-i) + 127
@@ -284,6 +304,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         acc_phase ^= 1;
       }
     }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
 
   tc_fence_before();
@@ -295,26 +316,26 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 }
 
 template <int MODE>
-static cudaError_t launch_gram_mode(const CUtensorMap& tmX, const GramParams& p, int num_sms,
-                                    cudaStream_t stream) {
+static cudaError_t launch_gram_mode(const CUtensorMap& tmX, const CUtensorMap& tmOut,
+                                    const GramParams& p, int num_sms, cudaStream_t stream) {
   const size_t smem = gram_u8_smem_bytes();
   cudaError_t e = cudaFuncSetAttribute(k_gram_tc<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
   const int grid = p.ntiles < num_sms ? p.ntiles : num_sms;
   if (grid <= 0) return cudaSuccess;
-  k_gram_tc<MODE><<<grid, NUM_THREADS, smem, stream>>>(tmX, p);
+  k_gram_tc<MODE><<<grid, NUM_THREADS, smem, stream>>>(tmX, tmOut, p);
   return cudaGetLastError();
 }
 
-cudaError_t launch_gram_u8(const CUtensorMap& tmX, const GramParams& p, int num_sms,
-                           cudaStream_t stream) {
-  return launch_gram_mode<0>(tmX, p, num_sms, stream);
+cudaError_t launch_gram_u8(const CUtensorMap& tmX, const CUtensorMap& tmOut, const GramParams& p,
+                           int num_sms, cudaStream_t stream) {
+  return launch_gram_mode<0>(tmX, tmOut, p, num_sms, stream);
 }
 
-cudaError_t launch_gram_cmp(const CUtensorMap& tmY, const GramParams& p, int num_sms,
-                            cudaStream_t stream) {
-  return launch_gram_mode<1>(tmY, p, num_sms, stream);
+cudaError_t launch_gram_cmp(const CUtensorMap& tmY, const CUtensorMap& tmOut, const GramParams& p,
+                            int num_sms, cudaStream_t stream) {
+  return launch_gram_mode<1>(tmY, tmOut, p, num_sms, stream);
 }
 
 }  // namespace xg

@@ -186,6 +186,20 @@ int make_map_bf16(xg_ctx* c, CUtensorMap* map, const void* base, int64_t cols, i
   return XG_OK;
 }
 
+// 32-bit output map for the Gram epilogue's 32 x 32 TMA stores
+int make_map_out32(xg_ctx* c, CUtensorMap* map, const void* base, int64_t ld, int64_t rows) {
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(ld), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * 4)};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = c->encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<void*>(base), dims,
+                         strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(c, XG_ERR_CUDA, "cuTensorMapEncodeTiled(out) failed (%d)", (int)r);
+  return XG_OK;
+}
+
 int make_map_u8(xg_ctx* c, CUtensorMap* map, const void* base, int64_t cols, int64_t rows,
                 int64_t row_stride, uint32_t box_cols, uint32_t box_rows) {
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
@@ -729,7 +743,10 @@ int xg_ttc_raw(xg_series* s, uint32_t flags) {
   gp.inv_ld = s->tp;
   gp.n_frames = s->t;
   gp.g2_partial = g2 ? s->d_g2tile : nullptr;
-  XG_CUDA(c, launch_gram_u8(map, gp, c->num_sms, c->stream));
+  CUtensorMap omap;
+  rc = make_map_out32(c, &omap, s->d_gram, s->tp, (int64_t)L->rings * s->tp);
+  if (rc) return rc;
+  XG_CUDA(c, launch_gram_u8(map, omap, gp, c->num_sms, c->stream));
   c->launches++;
   if (g2) {
     rc = fold_g2(s, s->d_g2, s->d_g2cnt);
@@ -1041,7 +1058,10 @@ int xg_ttc_compressed(xg_series* s, uint32_t flags) {
   }
   gp.kb_per_plane = s->ckp / 64;
   gp.plane_rows = static_cast<int32_t>(s->tp);
-  XG_CUDA(c, launch_gram_cmp(my, gp, c->num_sms, c->stream));
+  CUtensorMap omap;
+  rc = make_map_out32(c, &omap, s->d_cgram, s->tp, (int64_t)L->rings * s->tp);
+  if (rc) return rc;
+  XG_CUDA(c, launch_gram_cmp(my, omap, gp, c->num_sms, c->stream));
   c->launches++;
   if (g2) {
     rc = fold_g2(s, s->d_cg2, s->d_cg2cnt);

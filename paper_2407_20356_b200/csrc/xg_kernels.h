@@ -97,8 +97,8 @@ struct GramParams {
   int32_t plane_rows;
 };
 size_t gram_u8_smem_bytes();
-cudaError_t launch_gram_cmp(const CUtensorMap& tmY, const GramParams& p, int num_sms,
-                            cudaStream_t stream);
+cudaError_t launch_gram_cmp(const CUtensorMap& tmY, const CUtensorMap& tmOut, const GramParams& p,
+                            int num_sms, cudaStream_t stream);
 
 // Fold the per-tile diagonal sums of K2 into g2[ring][d] (fixed order) and
 // count the valid (t, t+d) pairs from the nonzero-frame bitmask.
@@ -116,8 +116,10 @@ struct G2FoldParams {
   int64_t g2_ld;
 };
 cudaError_t launch_g2_fold(const G2FoldParams& p, cudaStream_t s);
-cudaError_t launch_gram_u8(const CUtensorMap& tmX, const GramParams& p, int num_sms,
-                           cudaStream_t stream);
+// tmOut: 32-bit 2D map over the output, cols = ld, rows = rings * ld, box 32 x 32,
+// 128-byte swizzle (the epilogue TMA-stores 32 x 32 chunks)
+cudaError_t launch_gram_u8(const CUtensorMap& tmX, const CUtensorMap& tmOut, const GramParams& p,
+                           int num_sms, cudaStream_t stream);
 
 // ------------------------------------------------------ K3 projection
 struct ProjParams {
