@@ -1,0 +1,79 @@
+"""Host-side checks that need no GPU: the C-ABI library loads and exports
+every symbol include/xpcs_b200.h declares, fails loudly without a B200,
+the basis builder matches the reference, geometry helpers, sharding."""
+import numpy as np
+import pytest
+
+import oracle
+import paper_2407_20356_b200 as xg
+from paper_2407_20356_b200 import _abi, dist
+
+
+def test_library_exports_every_header_symbol():
+    syms = _abi.header_symbols()
+    assert len(syms) >= 25
+    for s in syms:
+        assert hasattr(_abi.lib, s), s
+    assert _abi.lib.xg_version() >= 100
+
+
+def test_no_silent_cpu_path_without_gpu():
+    from conftest import gpu_available
+
+    if gpu_available():
+        pytest.skip("GPU present")
+    with pytest.raises(xg.DeviceError):
+        xg.Context(0)
+
+
+def test_annular_rings_match_oracle(orc):
+    for h, w, q in [(128, 128, 8), (512, 512, 32), (48, 80, 5), (1, 7, 3)]:
+        r, _ = orc.ring_map(h, w, q)
+        assert np.array_equal(xg.annular_rings(h, w, q), r)
+
+
+@pytest.mark.skipif(not oracle.ref_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("n,m,k,seed", [(16, 64, 8, 1), (40, 500, 20, 2), (64, 3000, 32, 3)])
+def test_basis_builder_matches_reference(orc, ref, n, m, k, seed):
+    x = orc.random_positive_matrix(n, m, seed)
+    v = xg.build_online_from_frames(x, k)
+    vr, _ = ref.build_online_from_frames(x, k)
+    assert np.abs(v - vr).max() <= 1e-10
+    assert np.abs(v.T @ v - np.eye(k)).max() <= 1e-10
+
+
+@pytest.mark.skipif(not oracle.ref_available(), reason="oracle/_ref not built")
+def test_basis_builder_full_rank_and_errors(orc, ref):
+    x = orc.random_positive_matrix(12, 48, 5)
+    v = xg.build_online_from_frames(x, 0)
+    assert np.abs(v - ref.build_offline(x)).max() <= 1e-10
+    with pytest.raises(xg.RankError) as ei:
+        xg.build_online_from_frames(np.ones((4, 8)), 2)      # rank-1 corpus
+    assert ei.value.achievable_rank == 1
+    z = orc.random_positive_matrix(5, 10, 1)
+    z[3] = 0.0
+    with pytest.raises(xg.NormalizationError) as ei:
+        xg.build_online_from_frames(z, 2)
+    assert ei.value.frame_index == 3
+
+
+def test_build_ring_bases_parallel_equals_serial(orc):
+    xs = [orc.random_positive_matrix(24, m, 10 + m) for m in (50, 77, 120)]
+    par = xg.build_ring_bases(xs, 6, threads=3)
+    for x, v in zip(xs, par):
+        assert np.array_equal(v, xg.build_online_from_frames(x, 6))
+
+
+def test_shard_rings_lpt():
+    costs = [5, 3, 3, 2, 2, 2, 1]
+    sh = dist.shard_rings(costs, 3)
+    assert sorted(sum(sh, [])) == list(range(len(costs)))
+    loads = [sum(costs[r] for r in s) for s in sh]
+    assert max(loads) - min(loads) <= max(costs)
+    assert dist.shard_rings(costs, 1) == [list(range(len(costs)))]
+    # C4-like: 100 rings, 8 ranks -> within 5% of perfect balance
+    ring = xg.annular_rings(1024, 1024, 100)
+    m = np.bincount(ring)
+    sh = dist.shard_rings(dist.ring_costs(m, 16384), 8)
+    loads = [m[s].sum() for s in sh]
+    assert max(loads) / (m.sum() / 8) < 1.05
