@@ -151,6 +151,27 @@ XG_API int xg_series_get_cttc(xg_series* s, int32_t ring, int32_t dtype, void* o
                               int out_on_device);
 XG_API int xg_series_get_cg2(xg_series* s, int32_t ring, double* values, int64_t* counts);
 
+/* ---- streaming (kHz) mode ---------------------------------------------
+ * Frames arrive one at a time; each push correlates the new frame against
+ * every previous frame of every ring: the exact raw column G(s,t) (u8 dp4a)
+ * and, with a basis, the projected coefficients y_t (compress_frame,
+ * compress.cpp:34-46; bitwise equal to the batch xg_compress rows) and the
+ * compressed column y_s . y_t (ttc_extend, correlate.cpp:37-65).  g2 sums
+ * are accumulated per lag as frames arrive.  Single writer. */
+#define XG_STREAM_STORE_TTC 0x1u  /* keep every column (Q x T x T) for readback */
+#define XG_STREAM_NO_RAW 0x2u     /* compressed only */
+XG_API int xg_stream_create(xg_ctx* ctx, const xg_layout* layout, const xg_basis* basis,
+                            int64_t max_frames, uint32_t flags, xg_stream** out);
+XG_API void xg_stream_destroy(xg_stream* s);
+XG_API int xg_stream_push(xg_stream* s, const uint8_t* frame, int on_device);
+XG_API int64_t xg_stream_frames(const xg_stream* s);
+/* which: 0 raw, 1 compressed */
+XG_API int xg_stream_get_g2(xg_stream* s, int32_t ring, int32_t which, double* values,
+                            int64_t* counts);
+XG_API int xg_stream_get_coeffs(xg_stream* s, int32_t ring, double* y, double* norms);
+XG_API int xg_stream_get_ttc(xg_stream* s, int32_t ring, int32_t which, int32_t dtype, void* out,
+                             int64_t ld);
+
 /* ---- synthetic source (benchmark input; not on the correlation path) ---
  * Seeded speckle counts: complex AR(1) field per pixel with
  * rho = exp(-Gamma) (gamma_mode 0: Gamma = a r^2, 1: a 10^(3q/(Q-1))), Poisson

@@ -355,6 +355,68 @@ __all__ = [
 ]
 
 
+# ---------------------------------------------------------------- streaming
+class FrameStream:
+    """kHz streaming mode: frames pushed one at a time, each correlated
+    against the whole history of every ring (raw exact column + optional
+    compressed column) -- the device-resident replacement of the reference's
+    compress_frame -> ttc_extend -> append loop (acceptance_main.cpp:329-353)."""
+
+    def __init__(self, layout: RingLayout, max_frames: int, basis: "Basis | None" = None,
+                 store_ttc: bool = False, raw: bool = True, frame_period: float = 1.0):
+        self.layout, self.ctx, self.basis = layout, layout.ctx, basis
+        self.frame_period = float(frame_period)
+        flags = (_abi.STREAM_STORE_TTC if store_ttc else 0) | (0 if raw else _abi.STREAM_NO_RAW)
+        h = C.c_void_p()
+        _check(self.ctx.h, lib.xg_stream_create(self.ctx.h, layout.h, basis.h if basis else None,
+                                                int(max_frames), flags, C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib.xg_stream_destroy(self.h)
+            self.h = None
+
+    @property
+    def n_frames(self) -> int:
+        return int(lib.xg_stream_frames(self.h))
+
+    def push(self, frame) -> None:
+        if hasattr(frame, "data_ptr"):
+            _check(self.ctx.h, lib.xg_stream_push(self.h, C.c_void_p(frame.data_ptr()),
+                                                  1 if getattr(frame, "is_cuda", False) else 0))
+            return
+        a = np.ascontiguousarray(frame, dtype=np.uint8).ravel()
+        if a.size != self.layout.full_pixels:
+            raise ShapeError(f"frame must have {self.layout.full_pixels} pixels, got {a.size}")
+        _check(self.ctx.h, lib.xg_stream_push(self.h, _ptr(a), 0))
+
+    def g2(self, ring: int, compressed: bool = False):
+        n = self.n_frames
+        vals = np.empty(n, np.float64)
+        cnt = np.empty(n, np.int64)
+        _check(self.ctx.h, lib.xg_stream_get_g2(self.h, ring, 1 if compressed else 0,
+                                                vals.ctypes.data_as(_abi.PD),
+                                                cnt.ctypes.data_as(_abi.PI64)))
+        return np.arange(n, dtype=np.float64) * self.frame_period, vals, cnt
+
+    def coeffs(self, ring: int):
+        n, k = self.n_frames, self.basis.k
+        y = np.empty((n, k), np.float64)
+        nr = np.empty(n, np.float64)
+        _check(self.ctx.h, lib.xg_stream_get_coeffs(self.h, ring, y.ctypes.data_as(_abi.PD),
+                                                    nr.ctypes.data_as(_abi.PD)))
+        return y, nr
+
+    def ttc(self, ring: int, compressed: bool = False, dtype: str = "f64") -> np.ndarray:
+        n = self.n_frames
+        code = {"f64": _abi.F64, "f32": _abi.F32, "gram": _abi.I32_GRAM}[dtype]
+        out = np.empty((n, n), {"f64": np.float64, "f32": np.float32, "gram": np.int32}[dtype])
+        _check(self.ctx.h, lib.xg_stream_get_ttc(self.h, ring, 1 if compressed else 0, code,
+                                                 _ptr(out), n))
+        return out
+
+
 # ------------------------------------------------------------ geometry / data
 def annular_rings(height: int, width: int, n_rings: int) -> np.ndarray:
     """Equal-width annular q-rings: ring(p) =

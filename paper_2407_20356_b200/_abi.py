@@ -55,6 +55,13 @@ _sigs = {
     "xg_build_basis": (C.c_int, [PD, I64, I64, I32, PD, PD, PI64]),
     "xg_build_basis_batch": (C.c_int, [I32, C.POINTER(PD), I64, PI64, I32, C.POINTER(PD), I32,
                                        PI64]),
+    "xg_stream_create": (C.c_int, [P, P, P, I64, U32, C.POINTER(P)]),
+    "xg_stream_destroy": (None, [P]),
+    "xg_stream_push": (C.c_int, [P, P, C.c_int]),
+    "xg_stream_frames": (I64, [P]),
+    "xg_stream_get_g2": (C.c_int, [P, I32, I32, PD, PI64]),
+    "xg_stream_get_coeffs": (C.c_int, [P, I32, PD, PD]),
+    "xg_stream_get_ttc": (C.c_int, [P, I32, I32, I32, P, I64]),
     "xg_basis_create": (C.c_int, [P, P, I32, I32, C.POINTER(P)]),
     "xg_basis_destroy": (None, [P]),
     "xg_basis_set_ring": (C.c_int, [P, I32, PD]),
@@ -94,3 +101,5 @@ F64, F32, I32_GRAM = 0, 1, 2
 STRICT = 0x1
 NO_G2 = 0x2
 CMP_BF16 = 0x4
+STREAM_STORE_TTC = 0x1
+STREAM_NO_RAW = 0x2

@@ -157,7 +157,19 @@ __global__ void k_g2_fold(G2FoldParams p) {
   p.counts[r * p.g2_ld + d] = cnt;
 }
 
+// Streaming g2: running lag sums / pair counts.
+__global__ void k_g2_div(const double* sum, const int64_t* cnt, double* out, int64_t n) {
+  const int64_t d = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (d < n) out[d] = cnt[d] > 0 ? sum[d] / static_cast<double>(cnt[d]) : 0.0;
+}
+
 }  // namespace
+
+cudaError_t launch_g2_div(const double* sum, const int64_t* cnt, double* out, int64_t n,
+                          cudaStream_t s) {
+  k_g2_div<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(sum, cnt, out, n);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_g2_fold(const G2FoldParams& p, cudaStream_t s) {
   dim3 grid(static_cast<unsigned>((p.n_frames + 127) / 128), p.n_rings);

@@ -182,9 +182,10 @@ __global__ void __launch_bounds__(INGEST_THREADS + 32)
 
 // Per (frame, ring): fold the ring's segments in ascending band order.
 __global__ void k_norms(NormParams p) {
-  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int r = blockIdx.y;
-  if (t >= p.n_frames) return;
+  if (i >= p.n_frames) return;
+  const int64_t t = p.t0 + i;
   const uint2* srow = p.seg_stats + t * p.n_segs;
   int64_t n2 = 0, s1 = 0;
   for (int i = p.ring_seg_begin[r]; i < p.ring_seg_begin[r + 1]; ++i) {

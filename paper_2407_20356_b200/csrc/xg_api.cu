@@ -590,6 +590,7 @@ int xg_series_load_frames(xg_series* s, const uint8_t* frames, int64_t n, int on
   s->t = n;
   s->have_raw = false;
   NormParams np;
+  np.t0 = 0;
   np.seg_stats = s->d_seg_stats;
   np.n_segs = L->n_segs;
   np.ring_seg_begin = L->d_ring_seg_begin;
@@ -1133,6 +1134,288 @@ int xg_series_get_cg2(xg_series* s, int32_t ring, double* values, int64_t* count
     XG_CUDA(c, cudaMemcpyAsync(counts, s->d_cg2cnt + (int64_t)ring * s->tp, (size_t)s->t * 8,
                                cudaMemcpyDeviceToHost, c->stream));
   XG_CUDA(c, cudaStreamSynchronize(c->stream));
+  return check_device_error(c);
+}
+
+// --------------------------------------------------------------- streaming
+}  // extern "C"
+
+struct xg_stream {
+  xg_ctx* ctx = nullptr;
+  const xg_layout* L = nullptr;
+  const xg_basis* B = nullptr;
+  uint32_t flags = 0;
+  int64_t tmax = 0, t = 0, tp = 0;
+  int64_t max_kpad = 0;
+  uint8_t* d_frame = nullptr;
+  uint8_t* d_x = nullptr;
+  uint2* d_seg_stats = nullptr;
+  int64_t *d_norm2 = nullptr, *d_sum1 = nullptr, *d_zero = nullptr, *d_first_zero = nullptr;
+  double *d_norms = nullptr, *d_inv = nullptr;
+  uint32_t* d_nz_bits = nullptr;
+  double *d_g2sum = nullptr, *d_cg2sum = nullptr, *d_g2out = nullptr;
+  int64_t *d_g2cnt = nullptr, *d_cg2cnt = nullptr;
+  int32_t* d_gcol = nullptr;
+  float* d_ccol = nullptr;
+  int8_t* d_vdt = nullptr;
+  int32_t vdt_ld = 0;
+  double* d_y = nullptr;
+};
+
+extern "C" {
+
+int xg_stream_create(xg_ctx* c, const xg_layout* L, const xg_basis* B, int64_t max_frames,
+                     uint32_t flags, xg_stream** out) {
+  if (!c || !L || !out) return XG_ERR_INVALID;
+  *out = nullptr;
+  if (max_frames < 1) return fail(c, XG_ERR_CONTRACT, "stream: max_frames must be >= 1");
+  if (B && B->L != L) return fail(c, XG_ERR_BINDING, "stream: basis built for another layout");
+  if (B)
+    for (int32_t r = 0; r < L->rings; ++r)
+      if (!B->ring_set[r]) return fail(c, XG_ERR_CONTRACT, "stream: basis of ring %d not set", r);
+  xg_stream* s = new xg_stream();
+  s->ctx = c;
+  s->L = L;
+  s->B = B;
+  s->flags = flags;
+  s->tmax = max_frames;
+  s->tp = round_up(max_frames, 32);
+  for (int32_t r = 0; r < L->rings; ++r) s->max_kpad = std::max(s->max_kpad, L->kpad[r]);
+  const int64_t Q = L->rings;
+  cudaError_t e = cudaSuccess;
+  const bool store = (flags & XG_STREAM_STORE_TTC) != 0;
+  if ((e = dalloc(&s->d_frame, (size_t)L->pixels)) != cudaSuccess ||
+      (e = dalloc(&s->d_x, (size_t)max_frames * L->ktot)) != cudaSuccess ||
+      (e = dalloc(&s->d_seg_stats, (size_t)max_frames * L->n_segs)) != cudaSuccess ||
+      (e = dalloc(&s->d_norm2, (size_t)max_frames * Q)) != cudaSuccess ||
+      (e = dalloc(&s->d_sum1, (size_t)max_frames * Q)) != cudaSuccess ||
+      (e = dalloc(&s->d_zero, (size_t)Q)) != cudaSuccess ||
+      (e = dalloc(&s->d_first_zero, (size_t)Q)) != cudaSuccess ||
+      (e = dalloc(&s->d_norms, (size_t)Q * s->tp)) != cudaSuccess ||
+      (e = dalloc(&s->d_inv, (size_t)Q * s->tp)) != cudaSuccess ||
+      (e = dalloc(&s->d_nz_bits, (size_t)Q * (s->tp / 32))) != cudaSuccess ||
+      (e = dalloc(&s->d_g2sum, (size_t)Q * s->tp)) != cudaSuccess ||
+      (e = dalloc(&s->d_g2cnt, (size_t)Q * s->tp)) != cudaSuccess ||
+      (e = dalloc(&s->d_cg2sum, (size_t)Q * s->tp)) != cudaSuccess ||
+      (e = dalloc(&s->d_cg2cnt, (size_t)Q * s->tp)) != cudaSuccess ||
+      (e = dalloc(&s->d_g2out, (size_t)s->tp)) != cudaSuccess ||
+      (store && (e = dalloc(&s->d_gcol, (size_t)Q * s->tp * s->tp)) != cudaSuccess) ||
+      (store && B && (e = dalloc(&s->d_ccol, (size_t)Q * s->tp * s->tp)) != cudaSuccess)) {
+    xg_stream_destroy(s);
+    return cuda_fail(c, e, "stream alloc");
+  }
+  cudaMemsetAsync(s->d_x, 0, (size_t)max_frames * L->ktot, c->stream);
+  cudaMemsetAsync(s->d_zero, 0, (size_t)Q * 8, c->stream);
+  cudaMemsetAsync(s->d_first_zero, 0x7F, (size_t)Q * 8, c->stream);
+  cudaMemsetAsync(s->d_nz_bits, 0, (size_t)Q * (s->tp / 32) * 4, c->stream);
+  cudaMemsetAsync(s->d_g2sum, 0, (size_t)Q * s->tp * 8, c->stream);
+  cudaMemsetAsync(s->d_g2cnt, 0, (size_t)Q * s->tp * 8, c->stream);
+  cudaMemsetAsync(s->d_cg2sum, 0, (size_t)Q * s->tp * 8, c->stream);
+  cudaMemsetAsync(s->d_cg2cnt, 0, (size_t)Q * s->tp * 8, c->stream);
+  if (B) {
+    // pixel-major copy of the basis digits: [ktot][digits * k], index s*k + j
+    xg_basis* b = const_cast<xg_basis*>(B);
+    s->vdt_ld = b->digits * b->k;
+    std::vector<int8_t> vdt((size_t)L->ktot * s->vdt_ld, 0);
+    for (int64_t row = 0; row < b->vrows; ++row) {
+      const int64_t nt = row / (b->digits * b->kt), rem = row % (b->digits * b->kt);
+      const int64_t dig = rem / b->kt, j = nt * b->kt + rem % b->kt;
+      if (j >= b->k) continue;
+      const int8_t* src = b->h_vd.data() + row * L->ktot;
+      for (int64_t col = 0; col < L->ktot; ++col)
+        if (src[col]) vdt[(size_t)col * s->vdt_ld + dig * b->k + j] = src[col];
+    }
+    if ((e = dalloc(&s->d_vdt, vdt.size())) != cudaSuccess ||
+        (e = dalloc(&s->d_y, (size_t)Q * s->tp * b->k)) != cudaSuccess ||
+        (e = cudaMemcpy(s->d_vdt, vdt.data(), vdt.size(), cudaMemcpyHostToDevice)) != cudaSuccess) {
+      xg_stream_destroy(s);
+      return cuda_fail(c, e, "stream basis");
+    }
+    if (b->dirty) {
+      cudaMemcpy(b->d_vd, b->h_vd.data(), b->h_vd.size(), cudaMemcpyHostToDevice);
+      cudaMemcpy(b->d_scale, b->h_scale.data(), b->h_scale.size() * 8, cudaMemcpyHostToDevice);
+      b->dirty = false;
+    }
+  }
+  *out = s;
+  return XG_OK;
+}
+
+void xg_stream_destroy(xg_stream* s) {
+  if (!s) return;
+  dfree(s->d_frame);
+  dfree(s->d_x);
+  dfree(s->d_seg_stats);
+  dfree(s->d_norm2);
+  dfree(s->d_sum1);
+  dfree(s->d_zero);
+  dfree(s->d_first_zero);
+  dfree(s->d_norms);
+  dfree(s->d_inv);
+  dfree(s->d_nz_bits);
+  dfree(s->d_g2sum);
+  dfree(s->d_g2cnt);
+  dfree(s->d_cg2sum);
+  dfree(s->d_cg2cnt);
+  dfree(s->d_g2out);
+  dfree(s->d_gcol);
+  dfree(s->d_ccol);
+  dfree(s->d_vdt);
+  dfree(s->d_y);
+  delete s;
+}
+
+int64_t xg_stream_frames(const xg_stream* s) { return s ? s->t : -1; }
+
+int xg_stream_push(xg_stream* s, const uint8_t* frame, int on_device) {
+  if (!s || !frame) return XG_ERR_INVALID;
+  xg_ctx* c = s->ctx;
+  const xg_layout* L = s->L;
+  if (s->t >= s->tmax) return fail(c, XG_ERR_SHAPE, "stream: capacity %lld reached", (long long)s->tmax);
+  XG_CUDA(c, cudaMemcpyAsync(s->d_frame, frame, (size_t)L->pixels,
+                             on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                             c->stream));
+  IngestParams p;
+  p.raster = s->d_frame;
+  p.x = s->d_x;
+  p.pixels = L->pixels;
+  p.ktot = L->ktot;
+  p.band = L->band;
+  p.n_bands = L->n_bands;
+  p.n_rings = L->rings;
+  p.band_seg = L->d_band_seg;
+  p.band_wseg = L->d_band_wseg;
+  p.seg_order = L->d_seg_order;
+  p.segs = L->d_segs;
+  p.band_tab = L->d_band_tab;
+  p.tab = L->d_tab;
+  p.max_tab = L->max_tab;
+  p.t0 = s->t;  // frame 0 of the staging buffer lands in history row t
+  p.n_frames = 1;
+  p.frames_per_cta = 1;
+  p.n_segs = L->n_segs;
+  p.seg_stats = s->d_seg_stats;
+  XG_CUDA(c, launch_ingest(p, c->stream));
+  NormParams np;
+  np.t0 = s->t;
+  np.seg_stats = s->d_seg_stats;
+  np.n_segs = L->n_segs;
+  np.ring_seg_begin = L->d_ring_seg_begin;
+  np.ring_seg_list = L->d_ring_seg_list;
+  np.norm2 = s->d_norm2;
+  np.sum1 = s->d_sum1;
+  np.n_frames = 1;
+  np.ld = s->tp;
+  np.n_rings = L->rings;
+  np.norms = s->d_norms;
+  np.inv = s->d_inv;
+  np.zero_count = s->d_zero;
+  np.first_zero = s->d_first_zero;
+  np.nz_bits = s->d_nz_bits;
+  np.nz_words = static_cast<int32_t>(s->tp / 32);
+  np.err = c->d_err;
+  XG_CUDA(c, launch_norms(np, c->stream));
+  c->launches += 2;
+  StreamParams sp;
+  sp.x = s->d_x;
+  sp.ktot = L->ktot;
+  sp.t = s->t;
+  sp.ring_koff = L->d_ring_koff;
+  sp.ring_nkb = L->d_ring_nkb;
+  sp.inv = s->d_inv;
+  sp.inv_ld = s->tp;
+  sp.g2sum = s->d_g2sum;
+  sp.g2cnt = s->d_g2cnt;
+  sp.cg2sum = s->d_cg2sum;
+  sp.cg2cnt = s->d_cg2cnt;
+  sp.g2_ld = s->tp;
+  sp.gcol = s->d_gcol;
+  sp.ccol = s->d_ccol;
+  sp.col_ring_stride = s->tp * s->tp;
+  sp.col_ld = s->tp;
+  sp.vdt = s->d_vdt;
+  sp.vdt_ld = s->vdt_ld;
+  sp.n_digits = s->B ? s->B->digits : 0;
+  sp.k = s->B ? s->B->k : 0;
+  sp.scale = s->B ? s->B->d_scale : nullptr;
+  sp.y = s->d_y;
+  sp.y_ld = s->tp;
+  if (!(s->flags & XG_STREAM_NO_RAW)) {
+    XG_CUDA(c, launch_stream_raw(sp, L->rings, s->max_kpad, c->stream));
+    c->launches++;
+  }
+  if (s->B) {
+    XG_CUDA(c, launch_stream_cmp(sp, L->rings, c->stream));
+    c->launches += 2;
+  }
+  s->t++;
+  return XG_OK;
+}
+
+// which: 0 raw, 1 compressed
+int xg_stream_get_g2(xg_stream* s, int32_t ring, int32_t which, double* values, int64_t* counts) {
+  if (!s || !values) return XG_ERR_INVALID;
+  xg_ctx* c = s->ctx;
+  if (ring < 0 || ring >= s->L->rings) return fail(c, XG_ERR_SHAPE, "ring %d out of range", ring);
+  if (which == 1 && !s->B) return fail(c, XG_ERR_CONTRACT, "stream has no basis");
+  if (s->t < 1) return fail(c, XG_ERR_CONTRACT, "stream is empty");
+  const double* sum = (which ? s->d_cg2sum : s->d_g2sum) + (int64_t)ring * s->tp;
+  const int64_t* cnt = (which ? s->d_cg2cnt : s->d_g2cnt) + (int64_t)ring * s->tp;
+  XG_CUDA(c, launch_g2_div(sum, cnt, s->d_g2out, s->t, c->stream));
+  c->launches++;
+  XG_CUDA(c, cudaMemcpyAsync(values, s->d_g2out, (size_t)s->t * 8, cudaMemcpyDeviceToHost,
+                             c->stream));
+  if (counts)
+    XG_CUDA(c, cudaMemcpyAsync(counts, cnt, (size_t)s->t * 8, cudaMemcpyDeviceToHost, c->stream));
+  XG_CUDA(c, cudaStreamSynchronize(c->stream));
+  return check_device_error(c);
+}
+
+int xg_stream_get_coeffs(xg_stream* s, int32_t ring, double* y, double* norms) {
+  if (!s) return XG_ERR_INVALID;
+  xg_ctx* c = s->ctx;
+  if (ring < 0 || ring >= s->L->rings) return fail(c, XG_ERR_SHAPE, "ring %d out of range", ring);
+  if (y) {
+    if (!s->B) return fail(c, XG_ERR_CONTRACT, "stream has no basis");
+    XG_CUDA(c, cudaMemcpyAsync(y, s->d_y + (int64_t)ring * s->tp * s->B->k,
+                               (size_t)s->t * s->B->k * 8, cudaMemcpyDeviceToHost, c->stream));
+  }
+  if (norms)
+    XG_CUDA(c, cudaMemcpyAsync(norms, s->d_norms + (int64_t)ring * s->tp, (size_t)s->t * 8,
+                               cudaMemcpyDeviceToHost, c->stream));
+  XG_CUDA(c, cudaStreamSynchronize(c->stream));
+  return check_device_error(c);
+}
+
+// Full n x n TTC of a ring from the stored columns (XG_STREAM_STORE_TTC).
+int xg_stream_get_ttc(xg_stream* s, int32_t ring, int32_t which, int32_t dtype, void* out,
+                      int64_t ld) {
+  if (!s || !out) return XG_ERR_INVALID;
+  xg_ctx* c = s->ctx;
+  if (ring < 0 || ring >= s->L->rings) return fail(c, XG_ERR_SHAPE, "ring %d out of range", ring);
+  if ((which == 0 && !s->d_gcol) || (which == 1 && !s->d_ccol))
+    return fail(c, XG_ERR_CONTRACT, "stream was created without XG_STREAM_STORE_TTC");
+  if (ld < s->t) return fail(c, XG_ERR_SHAPE, "get_ttc: ld < n");
+  if (which == 1 && dtype == XG_I32_GRAM) return fail(c, XG_ERR_CONTRACT, "bad dtype");
+  const size_t bytes = (size_t)s->t * ld * (dtype == XG_F64 ? 8 : 4);
+  void* tmp = nullptr;
+  XG_CUDA(c, cudaMalloc(&tmp, bytes));
+  ExpandParams p;
+  p.gram = which == 0 ? s->d_gcol + (int64_t)ring * s->tp * s->tp : nullptr;
+  p.cf32 = which == 1 ? s->d_ccol + (int64_t)ring * s->tp * s->tp : nullptr;
+  p.ring_stride = 0;
+  p.ld = static_cast<int32_t>(s->tp);
+  p.inv = s->d_inv + (int64_t)ring * s->tp;
+  p.n = s->t;
+  p.out = tmp;
+  p.out_ld = ld;
+  p.out_dtype = dtype;
+  cudaError_t e = launch_expand(p, which, c->stream);
+  c->launches++;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(out, tmp, bytes, cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  cudaFree(tmp);
+  if (e != cudaSuccess) return cuda_fail(c, e, "stream get_ttc");
   return check_device_error(c);
 }
 

@@ -47,6 +47,7 @@ cudaError_t launch_ingest(const IngestParams& p, cudaStream_t s);
 // norms[r][t] = sqrt(norm2[t][r]), inv = 1/norms (0 for zero frames);
 // counts zero frames per ring and flags int32-Gram overflow (norm2 >= 2^31).
 struct NormParams {
+  int64_t t0;                // first frame processed (streaming: the new frame)
   const uint2* seg_stats;    // [frame][segment]
   int32_t n_segs;
   const int32_t* ring_seg_begin;  // CSR: segments of each ring, ascending band
@@ -144,6 +145,38 @@ struct ProjParams {
 size_t project_smem_bytes();
 cudaError_t launch_project(const CUtensorMap& tmX, const CUtensorMap& tmV, const ProjParams& p,
                            int num_sms, cudaStream_t stream);
+
+// ------------------------------------------------------ K5/K6 streaming
+struct StreamParams {
+  const uint8_t* x;          // ring-major history [t][ktot]
+  int64_t ktot;
+  int64_t t;                 // index of the new frame
+  const int32_t* ring_koff;
+  const int32_t* ring_nkb;
+  const double* inv;         // [ring][inv_ld]
+  int64_t inv_ld;
+  double* g2sum;             // [ring][g2_ld] running sums over lag (raw)
+  int64_t* g2cnt;
+  double* cg2sum;            // compressed
+  int64_t* cg2cnt;
+  int64_t g2_ld;
+  int32_t* gcol;             // optional: exact Gram G(s,t) at [ring][s][t]
+  float* ccol;               // optional: C~(s,t)
+  int64_t col_ring_stride, col_ld;
+  // compressed
+  const int8_t* vdt;         // pixel-major basis digits [ktot][vdt_ld], index s*k + j
+  int32_t vdt_ld;
+  int32_t n_digits;
+  int32_t k;
+  const double* scale;       // [ring][k]
+  double* y;                 // [ring][y_ld][k]
+  int64_t y_ld;
+};
+cudaError_t launch_stream_raw(const StreamParams& p, int32_t n_rings, int64_t max_kpad,
+                              cudaStream_t s);
+cudaError_t launch_stream_cmp(const StreamParams& p, int32_t n_rings, cudaStream_t s);
+cudaError_t launch_g2_div(const double* sum, const int64_t* cnt, double* out, int64_t n,
+                          cudaStream_t s);
 
 // --------------------------------------------------------------- K7 g2
 // g2[r][d] = sum_{t} G(t,t+d) inv_t inv_{t+d} / count, ascending t within
