@@ -172,6 +172,34 @@ XG_API int xg_stream_get_coeffs(xg_stream* s, int32_t ring, double* y, double* n
 XG_API int xg_stream_get_ttc(xg_stream* s, int32_t ring, int32_t which, int32_t dtype, void* out,
                              int64_t ld);
 
+/* ---- reference-facing f64 entries (one per xpcs:: function) -----------
+ * Same arguments as the reference (row-major f64 host buffers, N frames x M
+ * pixels / K coefficients), same validation and errors, and the reference's
+ * exact floating-point operation order executed on the current CUDA device
+ * (no FMA contraction), so the outputs are the reference's bits:
+ *   xg_f64_ttc_raw          <- xpcs::ttc_raw          correlate.cpp:19-25
+ *   xg_f64_ttc_compressed   <- xpcs::ttc_compressed   correlate.cpp:27-35
+ *   xg_f64_ttc_extend       <- xpcs::ttc_extend       correlate.cpp:37-65
+ *   xg_f64_g2_from_ttc      <- xpcs::g2_from_ttc      correlate.cpp:67-85
+ *   xg_f64_ttc_rel_error    <- xpcs::ttc_rel_error    correlate.cpp:87-108
+ *   xg_f64_compress_series  <- xpcs::compress_series  compress.cpp:48-81
+ *   xg_f64_compress_frame   <- xpcs::compress_frame   compress.cpp:34-46
+ * Errors: xg_f64_last_error() / xg_f64_last_payload() (thread-local). */
+XG_API const char* xg_f64_last_error(void);
+XG_API int64_t xg_f64_last_payload(void);
+XG_API int xg_f64_ttc_raw(const double* x, int64_t n, int64_t m, double* out);
+XG_API int xg_f64_ttc_compressed(const double* y, int64_t n, int64_t k, double* out,
+                                 int* lossless);
+XG_API int xg_f64_ttc_extend(const double* g, int64_t n, const double* y, int64_t k,
+                             const double* row, double* out, int* lossless);
+XG_API int xg_f64_g2_from_ttc(const double* g, int64_t n, double period, double* lags,
+                              double* values, int64_t* counts);
+XG_API int xg_f64_compress_series(const double* x, int64_t n, int64_t m, const double* v,
+                                  int64_t k, double* coeffs, double* norms);
+XG_API int xg_f64_compress_frame(const double* frame, int64_t m, const double* v, int64_t k,
+                                 double* coeffs, double* norm);
+XG_API int xg_f64_ttc_rel_error(const double* a, const double* b, int64_t count, double* out);
+
 /* ---- synthetic source (benchmark input; not on the correlation path) ---
  * Seeded speckle counts: complex AR(1) field per pixel with
  * rho = exp(-Gamma) (gamma_mode 0: Gamma = a r^2, 1: a 10^(3q/(Q-1))), Poisson

@@ -417,6 +417,111 @@ class FrameStream:
         return out
 
 
+# --------------------------------------------- reference-facing f64 functions
+# One function per xpcs:: operator, same arguments and errors, computed on the
+# GPU in the reference's exact floating-point order (k_exact.cu): the results
+# are the reference's bits.  A Context (device selection) must exist.
+def _f64check(rc: int) -> None:
+    if rc == _abi.OK:
+        return
+    msg = lib.xg_f64_last_error().decode()
+    payload = int(lib.xg_f64_last_payload())
+    if rc == _abi.ERR_NORMALIZATION:
+        raise NormalizationError(msg, payload)
+    raise _ERRS.get(rc, DeviceError)(msg or f"status {rc}")
+
+
+def _d(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def ttc_raw(x) -> np.ndarray:
+    """xpcs::ttc_raw (correlate.cpp:19-25), bit-exact."""
+    x = _d(x)
+    n, m = x.shape
+    out = np.empty((n, n))
+    _f64check(lib.xg_f64_ttc_raw(x.ctypes.data_as(_abi.PD), n, m, out.ctypes.data_as(_abi.PD)))
+    return out
+
+
+def ttc_compressed(y):
+    """xpcs::ttc_compressed (correlate.cpp:27-35) -> (G~, lossless), bit-exact."""
+    y = _d(y)
+    n, k = y.shape
+    out = np.empty((n, n))
+    ll = C.c_int(0)
+    _f64check(lib.xg_f64_ttc_compressed(y.ctypes.data_as(_abi.PD), n, k,
+                                        out.ctypes.data_as(_abi.PD), C.byref(ll)))
+    return out, bool(ll.value)
+
+
+def ttc_extend(g, y, row):
+    """xpcs::ttc_extend (correlate.cpp:37-65) -> ((n+1)x(n+1), lossless)."""
+    g, y, row = _d(g), _d(y), _d(row)
+    n = g.shape[0]
+    if y.shape[0] != n:
+        raise ShapeError(f"ttc_extend: TTC covers {n} frames but store holds {y.shape[0]}")
+    if row.size != y.shape[1]:
+        raise ShapeError("ttc_extend: new row length does not match the store's k")
+    out = np.empty((n + 1, n + 1))
+    ll = C.c_int(0)
+    _f64check(lib.xg_f64_ttc_extend(g.ctypes.data_as(_abi.PD), n, y.ctypes.data_as(_abi.PD),
+                                    y.shape[1], row.ctypes.data_as(_abi.PD),
+                                    out.ctypes.data_as(_abi.PD), C.byref(ll)))
+    return out, bool(ll.value)
+
+
+def g2_from_ttc(g, frame_period: float = 1.0):
+    """xpcs::g2_from_ttc (correlate.cpp:67-85) -> (lags, values, counts)."""
+    g = _d(g)
+    n = g.shape[0]
+    lags, vals = np.empty(n), np.empty(n)
+    cnt = np.empty(n, np.int64)
+    _f64check(lib.xg_f64_g2_from_ttc(g.ctypes.data_as(_abi.PD), n, frame_period,
+                                     lags.ctypes.data_as(_abi.PD), vals.ctypes.data_as(_abi.PD),
+                                     cnt.ctypes.data_as(_abi.PI64)))
+    return lags, vals, cnt
+
+
+def compress_series(x, v):
+    """xpcs::compress_series (compress.cpp:48-81) -> (coefficients, norms)."""
+    x, v = _d(x), _d(v)
+    n, m = x.shape
+    if v.shape[0] != m:
+        raise ShapeError(f"frame has {m} pixels, encoder expects {v.shape[0]}")
+    k = v.shape[1]
+    y, nr = np.empty((n, k)), np.empty(n)
+    _f64check(lib.xg_f64_compress_series(x.ctypes.data_as(_abi.PD), n, m,
+                                         v.ctypes.data_as(_abi.PD), k, y.ctypes.data_as(_abi.PD),
+                                         nr.ctypes.data_as(_abi.PD)))
+    return y, nr
+
+
+def compress_frame(frame, v):
+    """xpcs::compress_frame (compress.cpp:34-46) -> (coefficients, norm)."""
+    frame, v = _d(frame).ravel(), _d(v)
+    if v.shape[0] != frame.size:
+        raise ShapeError(f"frame has {frame.size} pixels, encoder expects {v.shape[0]}")
+    k = v.shape[1]
+    y = np.empty(k)
+    nr = C.c_double(0)
+    _f64check(lib.xg_f64_compress_frame(frame.ctypes.data_as(_abi.PD), frame.size,
+                                        v.ctypes.data_as(_abi.PD), k, y.ctypes.data_as(_abi.PD),
+                                        C.byref(nr)))
+    return y, nr.value
+
+
+def ttc_rel_error(g, g_approx) -> float:
+    """xpcs::ttc_rel_error (correlate.cpp:87-108)."""
+    a, b = _d(g), _d(g_approx)
+    if a.shape != b.shape:
+        raise ShapeError(f"ttc_rel_error: sizes {a.shape[0]} vs {b.shape[0]}")
+    out = C.c_double(0)
+    _f64check(lib.xg_f64_ttc_rel_error(a.ctypes.data_as(_abi.PD), b.ctypes.data_as(_abi.PD),
+                                       a.size, C.byref(out)))
+    return out.value
+
+
 # ------------------------------------------------------------ geometry / data
 def annular_rings(height: int, width: int, n_rings: int) -> np.ndarray:
     """Equal-width annular q-rings: ring(p) =

@@ -62,6 +62,15 @@ _sigs = {
     "xg_stream_get_g2": (C.c_int, [P, I32, I32, PD, PI64]),
     "xg_stream_get_coeffs": (C.c_int, [P, I32, PD, PD]),
     "xg_stream_get_ttc": (C.c_int, [P, I32, I32, I32, P, I64]),
+    "xg_f64_last_error": (C.c_char_p, []),
+    "xg_f64_last_payload": (I64, []),
+    "xg_f64_ttc_raw": (C.c_int, [PD, I64, I64, PD]),
+    "xg_f64_ttc_compressed": (C.c_int, [PD, I64, I64, PD, C.POINTER(C.c_int)]),
+    "xg_f64_ttc_extend": (C.c_int, [PD, I64, PD, I64, PD, PD, C.POINTER(C.c_int)]),
+    "xg_f64_g2_from_ttc": (C.c_int, [PD, I64, C.c_double, PD, PD, PI64]),
+    "xg_f64_compress_series": (C.c_int, [PD, I64, I64, PD, I64, PD, PD]),
+    "xg_f64_compress_frame": (C.c_int, [PD, I64, PD, I64, PD, PD]),
+    "xg_f64_ttc_rel_error": (C.c_int, [PD, PD, I64, PD]),
     "xg_basis_create": (C.c_int, [P, P, I32, I32, C.POINTER(P)]),
     "xg_basis_destroy": (None, [P]),
     "xg_basis_set_ring": (C.c_int, [P, I32, PD]),

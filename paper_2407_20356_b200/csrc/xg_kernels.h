@@ -178,6 +178,19 @@ cudaError_t launch_stream_cmp(const StreamParams& p, int32_t n_rings, cudaStream
 cudaError_t launch_g2_div(const double* sum, const int64_t* cnt, double* out, int64_t n,
                           cudaStream_t s);
 
+// ------------------------------------------- K9 reference-order f64 replicas
+cudaError_t launch_exact_rownorm(const double* x, int64_t n, int64_t m, double* xn, double* norms,
+                                 unsigned long long* bad, cudaStream_t s);
+cudaError_t launch_exact_gram(const double* x, int64_t n, int64_t m, double* g, cudaStream_t s);
+cudaError_t launch_exact_extend(const double* g, int64_t n, const double* y, int64_t k,
+                                const double* row, double* out, cudaStream_t s);
+cudaError_t launch_exact_g2(const double* g, int64_t n, double period, double* lags,
+                            double* values, int64_t* counts, cudaStream_t s);
+cudaError_t launch_exact_project(const double* xn, int64_t n, int64_t m, const double* v,
+                                 int64_t k, double* coeffs, cudaStream_t s);
+cudaError_t launch_exact_relerr(const double* a, const double* b, int64_t count, double* out,
+                                cudaStream_t s);
+
 // --------------------------------------------------------------- K7 g2
 // g2[r][d] = sum_{t} G(t,t+d) inv_t inv_{t+d} / count, ascending t within
 // segments of `seg` frames, segments combined in ascending order.
