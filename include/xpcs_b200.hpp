@@ -1,0 +1,246 @@
+// xpcs_b200.hpp -- header-only C++ facade over the C ABI (xpcs_b200.h).
+//
+// Mirrors the reference's C++ operator API (namespace xpcs,
+// /root/reference/proj/include/xpcsvd/{correlate,compress,model,errors}.hpp):
+// the same exception hierarchy, and two layers:
+//   * reference-facing free functions on row-major f64 buffers with the
+//     reference's exact arithmetic (ttc_raw, ttc_compressed, ttc_extend,
+//     g2_from_ttc, ttc_rel_error, compress_series, compress_frame);
+//   * RAII handles for the high-throughput photon-count path (Context,
+//     RingLayout, Series, Basis, Stream): u8 frames in, every q-ring's TTC,
+//     compressed TTC and g2 out, computed by the sm_100a kernels.
+// No CPU compute path: every number comes from libxpcs_b200.so's kernels.
+#ifndef XPCS_B200_HPP_
+#define XPCS_B200_HPP_
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "xpcs_b200.h"
+
+namespace xpcs_b200 {
+
+// ------------------------------------------------------------- errors
+class Error : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+class ShapeError : public Error { public: using Error::Error; };
+class ContractError : public Error { public: using Error::Error; };
+class MaskError : public Error { public: using Error::Error; };
+class BindingError : public Error { public: using Error::Error; };
+class FormatError : public Error { public: using Error::Error; };
+class DeviceError : public Error { public: using Error::Error; };
+class NormalizationError : public Error {
+ public:
+  NormalizationError(const std::string& m, std::size_t frame, int ring = -1)
+      : Error(m), frame_(frame), ring_(ring) {}
+  std::size_t frame_index() const { return frame_; }
+  int ring() const { return ring_; }
+
+ private:
+  std::size_t frame_;
+  int ring_;
+};
+class RankError : public Error {
+ public:
+  RankError(const std::string& m, std::size_t rank) : Error(m), rank_(rank) {}
+  std::size_t achievable_rank() const { return rank_; }
+
+ private:
+  std::size_t rank_;
+};
+
+namespace detail {
+[[noreturn]] inline void raise(int rc, const std::string& msg, int64_t payload, int ring) {
+  switch (rc) {
+    case XG_ERR_SHAPE: throw ShapeError(msg);
+    case XG_ERR_CONTRACT: throw ContractError(msg);
+    case XG_ERR_MASK: throw MaskError(msg);
+    case XG_ERR_NORMALIZATION: throw NormalizationError(msg, static_cast<std::size_t>(payload), ring);
+    case XG_ERR_RANK: throw RankError(msg, static_cast<std::size_t>(payload));
+    case XG_ERR_BINDING: throw BindingError(msg);
+    case XG_ERR_FORMAT: throw FormatError(msg);
+    default: throw DeviceError(msg + " (status " + std::to_string(rc) + ")");
+  }
+}
+inline void f64(int rc) {
+  if (rc != XG_OK) raise(rc, xg_f64_last_error(), xg_f64_last_payload(), -1);
+}
+}  // namespace detail
+
+// ------------------------------------------ reference-facing (exact f64)
+inline std::vector<double> ttc_raw(const std::vector<double>& x, int64_t n, int64_t m) {
+  std::vector<double> g(static_cast<size_t>(n * n));
+  detail::f64(xg_f64_ttc_raw(x.data(), n, m, g.data()));
+  return g;
+}
+inline std::pair<std::vector<double>, bool> ttc_compressed(const std::vector<double>& y,
+                                                           int64_t n, int64_t k) {
+  std::vector<double> g(static_cast<size_t>(n * n));
+  int ll = 0;
+  detail::f64(xg_f64_ttc_compressed(y.data(), n, k, g.data(), &ll));
+  return {std::move(g), ll != 0};
+}
+inline std::pair<std::vector<double>, bool> ttc_extend(const std::vector<double>& g, int64_t n,
+                                                       const std::vector<double>& y, int64_t k,
+                                                       const std::vector<double>& row) {
+  std::vector<double> out(static_cast<size_t>((n + 1) * (n + 1)));
+  int ll = 0;
+  detail::f64(xg_f64_ttc_extend(g.data(), n, y.data(), k, row.data(), out.data(), &ll));
+  return {std::move(out), ll != 0};
+}
+struct G2Curve {
+  std::vector<double> lags, values;
+  std::vector<int64_t> counts;
+};
+inline G2Curve g2_from_ttc(const std::vector<double>& g, int64_t n, double frame_period) {
+  G2Curve c{std::vector<double>(n), std::vector<double>(n), std::vector<int64_t>(n)};
+  detail::f64(xg_f64_g2_from_ttc(g.data(), n, frame_period, c.lags.data(), c.values.data(),
+                                 c.counts.data()));
+  return c;
+}
+inline double ttc_rel_error(const std::vector<double>& a, const std::vector<double>& b) {
+  if (a.size() != b.size()) throw ShapeError("ttc_rel_error: size mismatch");
+  double out = 0.0;
+  detail::f64(xg_f64_ttc_rel_error(a.data(), b.data(), static_cast<int64_t>(a.size()), &out));
+  return out;
+}
+inline std::pair<std::vector<double>, std::vector<double>> compress_series(
+    const std::vector<double>& x, int64_t n, int64_t m, const std::vector<double>& v, int64_t k) {
+  std::vector<double> y(static_cast<size_t>(n * k)), norms(static_cast<size_t>(n));
+  detail::f64(xg_f64_compress_series(x.data(), n, m, v.data(), k, y.data(), norms.data()));
+  return {std::move(y), std::move(norms)};
+}
+
+// --------------------------------------------- photon-count fast path
+class Context {
+ public:
+  explicit Context(int device = 0, void* cuda_stream = nullptr) {
+    const int rc = xg_ctx_create(device, cuda_stream, &h_);
+    if (rc != XG_OK) throw DeviceError("xg_ctx_create failed (an sm_100 B200 is required)");
+  }
+  ~Context() { xg_ctx_destroy(h_); }
+  Context(const Context&) = delete;
+  Context& operator=(const Context&) = delete;
+  xg_ctx* get() const { return h_; }
+  void check(int rc) const {
+    if (rc == XG_OK) return;
+    int32_t ring = -1;
+    const int64_t payload = xg_last_error_payload(h_, &ring);
+    detail::raise(rc, xg_last_error(h_), payload, ring);
+  }
+  void synchronize() const { check(xg_synchronize(h_)); }
+
+ private:
+  xg_ctx* h_ = nullptr;
+};
+
+// A set of PixelMask (one per q-ring), each strictly ascending.
+class RingLayout {
+ public:
+  RingLayout(const Context& ctx, int64_t full_pixels, const std::vector<std::vector<int64_t>>& masks)
+      : ctx_(ctx) {
+    std::vector<int64_t> off(1, 0), idx;
+    for (const auto& m : masks) {
+      idx.insert(idx.end(), m.begin(), m.end());
+      off.push_back(static_cast<int64_t>(idx.size()));
+    }
+    ctx.check(xg_layout_create(ctx.get(), full_pixels, static_cast<int32_t>(masks.size()),
+                               off.data(), idx.data(), &h_));
+  }
+  ~RingLayout() { xg_layout_destroy(h_); }
+  RingLayout(const RingLayout&) = delete;
+  RingLayout& operator=(const RingLayout&) = delete;
+  xg_layout* get() const { return h_; }
+  const Context& ctx() const { return ctx_; }
+
+ private:
+  const Context& ctx_;
+  xg_layout* h_ = nullptr;
+};
+
+class Basis {
+ public:
+  Basis(const RingLayout& L, int32_t k, int32_t digits = 3) : L_(L) {
+    L.ctx().check(xg_basis_create(L.ctx().get(), L.get(), k, digits, &h_));
+  }
+  ~Basis() { xg_basis_destroy(h_); }
+  Basis(const Basis&) = delete;
+  Basis& operator=(const Basis&) = delete;
+  // v: M_q x k row-major, mask order
+  void set_ring(int32_t ring, const double* v) { L_.ctx().check(xg_basis_set_ring(h_, ring, v)); }
+  xg_basis* get() const { return h_; }
+
+ private:
+  const RingLayout& L_;
+  xg_basis* h_ = nullptr;
+};
+
+class Series {
+ public:
+  Series(const RingLayout& L, int64_t max_frames) : L_(L) {
+    L.ctx().check(xg_series_create(L.ctx().get(), L.get(), max_frames, &h_));
+  }
+  ~Series() { xg_series_destroy(h_); }
+  Series(const Series&) = delete;
+  Series& operator=(const Series&) = delete;
+  void load(const uint8_t* frames, int64_t n, bool on_device = false) {
+    L_.ctx().check(xg_series_load_frames(h_, frames, n, on_device ? 1 : 0));
+  }
+  void ttc_raw(uint32_t flags = 0) { L_.ctx().check(xg_ttc_raw(h_, flags)); }
+  void compress(const Basis& b, uint32_t flags = 0) { L_.ctx().check(xg_compress(h_, b.get(), flags)); }
+  void ttc_compressed(uint32_t flags = 0) { L_.ctx().check(xg_ttc_compressed(h_, flags)); }
+  int64_t frames() const { return xg_series_frames(h_); }
+  std::vector<double> ttc(int32_t ring) const {
+    const int64_t n = frames();
+    std::vector<double> out(static_cast<size_t>(n * n));
+    L_.ctx().check(xg_series_get_ttc(h_, ring, XG_F64, out.data(), n, 0));
+    return out;
+  }
+  std::vector<double> g2(int32_t ring, std::vector<int64_t>* counts = nullptr) const {
+    const int64_t n = frames();
+    std::vector<double> v(static_cast<size_t>(n));
+    std::vector<int64_t> c(static_cast<size_t>(n));
+    L_.ctx().check(xg_series_get_g2(h_, ring, v.data(), c.data()));
+    if (counts) *counts = std::move(c);
+    return v;
+  }
+  xg_series* get() const { return h_; }
+
+ private:
+  const RingLayout& L_;
+  xg_series* h_ = nullptr;
+};
+
+class Stream {
+ public:
+  Stream(const RingLayout& L, int64_t max_frames, const Basis* b = nullptr, uint32_t flags = 0)
+      : L_(L) {
+    L.ctx().check(xg_stream_create(L.ctx().get(), L.get(), b ? b->get() : nullptr, max_frames,
+                                   flags, &h_));
+  }
+  ~Stream() { xg_stream_destroy(h_); }
+  Stream(const Stream&) = delete;
+  Stream& operator=(const Stream&) = delete;
+  void push(const uint8_t* frame, bool on_device = false) {
+    L_.ctx().check(xg_stream_push(h_, frame, on_device ? 1 : 0));
+  }
+  int64_t frames() const { return xg_stream_frames(h_); }
+  std::vector<double> g2(int32_t ring, bool compressed = false) const {
+    std::vector<double> v(static_cast<size_t>(frames()));
+    L_.ctx().check(xg_stream_get_g2(h_, ring, compressed ? 1 : 0, v.data(), nullptr));
+    return v;
+  }
+
+ private:
+  const RingLayout& L_;
+  xg_stream* h_ = nullptr;
+};
+
+}  // namespace xpcs_b200
+
+#endif  // XPCS_B200_HPP_

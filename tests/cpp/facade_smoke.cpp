@@ -1,0 +1,59 @@
+// facade_smoke.cpp -- exercises include/xpcs_b200.hpp from C++ (built by
+// __graft_entry__.build(), run by tests/test_gpu_facade.py on the GPU box).
+// Reads a u8 frame file (n x m) and a ring map (m int32), prints the int
+// Gram diagonal checksum, the f64 TTC checksum and g2[0..2] of every ring.
+#include <cstdio>
+#include <fstream>
+#include <vector>
+
+#include "xpcs_b200.hpp"
+
+int main(int argc, char** argv) {
+  if (argc != 6) {
+    std::fprintf(stderr, "usage: %s frames.u8 ring.i32 n m q\n", argv[0]);
+    return 2;
+  }
+  const int64_t n = std::atoll(argv[3]), m = std::atoll(argv[4]);
+  const int q = std::atoi(argv[5]);
+  std::vector<uint8_t> frames(static_cast<size_t>(n * m));
+  std::vector<int32_t> ring(static_cast<size_t>(m));
+  std::ifstream(argv[1], std::ios::binary).read(reinterpret_cast<char*>(frames.data()), n * m);
+  std::ifstream(argv[2], std::ios::binary).read(reinterpret_cast<char*>(ring.data()), m * 4);
+  try {
+    xpcs_b200::Context ctx(0);
+    std::vector<std::vector<int64_t>> masks(q);
+    for (int64_t p = 0; p < m; ++p) masks[ring[p]].push_back(p);
+    xpcs_b200::RingLayout layout(ctx, m, masks);
+    xpcs_b200::Series s(layout, n);
+    s.load(frames.data(), n);
+    s.ttc_raw();
+    for (int r = 0; r < q; ++r) {
+      const auto c = s.ttc(r);
+      double sum = 0.0;
+      for (double v : c) sum += v;
+      const auto g2 = s.g2(r);
+      std::printf("ring %d sum %.17g g2 %.17g %.17g %.17g\n", r, sum, g2[0], g2[1], g2[2]);
+    }
+    // reference-facing exact entry on the same ring 0 data
+    std::vector<double> x0;
+    for (int64_t t = 0; t < n; ++t)
+      for (int64_t p : masks[0]) x0.push_back(frames[t * m + p]);
+    const auto g = xpcs_b200::ttc_raw(x0, n, static_cast<int64_t>(masks[0].size()));
+    double sum = 0.0;
+    for (double v : g) sum += v;
+    std::printf("exact ring 0 sum %.17g\n", sum);
+    try {
+      std::vector<double> z(static_cast<size_t>(3 * 4), 1.0);
+      for (int p = 0; p < 4; ++p) z[4 + p] = 0.0;
+      xpcs_b200::ttc_raw(z, 3, 4);
+      std::printf("missing NormalizationError\n");
+      return 1;
+    } catch (const xpcs_b200::NormalizationError& e) {
+      std::printf("NormalizationError frame %zu\n", e.frame_index());
+    }
+  } catch (const std::exception& e) {
+    std::fprintf(stderr, "error: %s\n", e.what());
+    return 1;
+  }
+  return 0;
+}
