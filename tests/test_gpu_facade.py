@@ -32,6 +32,6 @@ def test_cpp_facade(tmp_path, orc):
         g2 = orc.g2_from_ttc(c)[1]
         assert np.allclose([float(x) for x in parts[5:8]], g2[:3], atol=1e-12, rtol=0)
     c0 = orc.ttc_raw(frames[:, ring == 0].astype(np.float64))
-    assert float(lines[q].split()[-1]) == float(repr(c0.sum())) or \
-        abs(float(lines[q].split()[-1]) - c0.sum()) <= 1e-12 * c0.size
+    # the exact entry returns the reference's bits: same sum up to summation order
+    assert abs(float(lines[q].split()[-1]) - float(c0.sum())) <= 1e-12 * c0.size
     assert lines[q + 1] == "NormalizationError frame 1"
