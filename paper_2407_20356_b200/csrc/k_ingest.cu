@@ -3,7 +3,7 @@
 // Replaces the per-ring column gather `apply_mask` (src/model.cpp:42-59) and
 // the norm pass of `row_normalize` (src/linalg.cpp:441-456, the dot at :445):
 // one pass over the raw frames writes every q-ring's pixels (in mask order,
-// i.e. ascending pixel index) into its own 16-byte aligned column range of a
+// i.e. ascending pixel index) into its own 4-byte aligned column range of a
 // frame-major row, and records per (frame, segment) the exact sum of squares
 // and sum of the counts.  K1b (k_norms) folds segments into per-(frame, ring)
 // norms in a fixed order -- no atomics anywhere, so the statistics are exact

@@ -343,7 +343,7 @@ int xg_layout_create(xg_ctx* c, int64_t full_pixels, int32_t n_rings,
     int64_t k = 0;
     for (int32_t b = 0; b < nb; ++b) {
       segoff[(size_t)r * nb + b] = k;
-      k += round_up(cnt[(size_t)r * nb + b], 16);
+      k += round_up(cnt[(size_t)r * nb + b], 4);  // 4-byte segments: K1 stores words
     }
     L->ring_pixels[r] = offsets[r + 1] - offsets[r];
     L->kpad[r] = std::max<int64_t>(128, round_up(k, 128));
@@ -369,7 +369,7 @@ int xg_layout_create(xg_ctx* c, int64_t full_pixels, int32_t n_rings,
     for (int32_t r = 0; r < n_rings; ++r) {
       const int64_t n = cnt[(size_t)r * nb + b];
       if (n == 0) continue;
-      const int64_t len = round_up(n, 16);
+      const int64_t len = round_up(n, 4);
       Segment s;
       s.ring = r;
       s.dst = static_cast<int32_t>(L->koff[r] + segoff[(size_t)r * nb + b]);

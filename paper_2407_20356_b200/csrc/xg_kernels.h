@@ -12,11 +12,11 @@ namespace xg {
 
 // ---------------------------------------------------------------- K1 ingest
 // One "segment" = the pixels of one ring inside one detector band, padded to
-// a multiple of 16 bytes, written to a contiguous range of the ring-major row.
+// a multiple of 4 bytes, written to a contiguous range of the ring-major row.
 struct Segment {
   int32_t ring;
-  int32_t dst;     // byte column in the ring-major row (multiple of 16)
-  int32_t len;     // bytes incl. zero padding (multiple of 16)
+  int32_t dst;     // byte column in the ring-major row (multiple of 4)
+  int32_t len;     // bytes incl. zero padding (multiple of 4)
   int32_t taboff;  // offset of this segment's source table within its band
 };
 
