@@ -1,0 +1,378 @@
+// k_gram2.cu -- K2/K4 on CTA pairs: tcgen05.mma.cta_group::2, 256 x 256
+// tiles per cluster of 2 SMs.
+//
+// Same math, epilogue and fused-g2 contract as k_gram.cu, but each MMA is
+// M=256 x N=256 x K=32 issued by the leader CTA for the pair: CTA r of the
+// pair stages rows [i0 + 128 r, +128) of A and columns [j0 + 128 r, +128) of
+// B (half of each operand), so every SM moves half the B bytes per output of
+// the 1-CTA kernel (64 instead of 96 B/cycle of smem+L2 operand traffic at
+// full MMA rate).  Each CTA's TMEM holds its 128 rows x 256 columns; its
+// epilogue is exactly the 1-CTA epilogue on a 128 x 256 half tile, and the
+// half tile's g2 partial lands at the index the 1-CTA enumeration gives it,
+// so k_g2_fold is shared.
+//
+// Pair protocol: full barriers live in the leader (count 1, leader posts
+// expect_tx for both CTAs' bytes; both CTAs' TMA loads complete_tx there);
+// empty/tfull barriers in both CTAs are signalled by the leader's commits
+// multicast to the pair; the leader's tempty counts 8 arrivals (4 epilogue
+// warps per CTA; the peer arrives remotely).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "xg_kernels.h"
+#include "xg_ptx.cuh"
+
+namespace xg {
+
+namespace {
+
+constexpr int BM = 128;            // rows per CTA (256 per pair)
+constexpr int BN = 256;            // tile columns
+constexpr int BK = 128;            // bytes of K per stage
+constexpr int STAGES = 5;
+constexpr int A_BYTES = BM * BK;   // 16 KB
+constexpr int B_BYTES = 128 * BK;  // 16 KB: this CTA's half of the 256 columns
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int TMEM_COLS = 512;
+constexpr int NUM_THREADS = 256;
+constexpr int NDIAG = BM + BN - 1;
+constexpr int NDIAG_PAD = 384;
+constexpr uint32_t kPeerMask = 0xFEFFFFFFu;  // shared::cluster address of the pair leader
+
+template <int MODE>
+constexpr uint32_t idesc2() {
+  // M = 256 (m_dim = 16), N = 256
+  return MODE == 0 ? idesc_i8(256, BN, false) : idesc_bf16(256, BN);
+}
+
+struct __align__(1024) Tail2 {
+  uint32_t stage[4][32 * 32];
+  uint64_t full[STAGES];
+  uint64_t empty[STAGES];
+  uint64_t tfull[2];
+  uint64_t tempty[2];
+  uint32_t tmem_base;
+  uint32_t pad_;
+  double inv_row[BM];
+  double inv_col[BN];
+  double acc[4][NDIAG_PAD];
+};
+
+__device__ __forceinline__ uint32_t cta_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+__device__ __forceinline__ void tma_load_2sm(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                             int32_t c0, int32_t c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & kPeerMask), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void mma2_i8(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
+                                        uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma2_bf16(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
+                                          uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+// commit to the barrier at this offset in both CTAs of the pair
+__device__ __forceinline__ void commit2(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"(static_cast<uint16_t>(3))
+      : "memory");
+}
+__device__ __forceinline__ void arrive_leader(uint64_t* bar) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(remote) : "r"(smem_u32(bar)));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote)
+               : "memory");
+}
+
+}  // namespace
+
+size_t gram2_smem_bytes() { return 1024 + STAGES * STAGE_BYTES + sizeof(Tail2); }
+
+template <int MODE>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+    k_gram2(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmOut,
+            GramParams p) {
+  constexpr uint32_t IDESC = idesc2<MODE>();
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * A_BYTES;
+  Tail2* tail = reinterpret_cast<Tail2*>(smem + STAGES * STAGE_BYTES);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cta_rank();
+  const bool leader = rank == 0;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&tail->full[s], 1);
+      mbar_init(&tail->empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tail->tfull[a], 1);
+      mbar_init(&tail->tempty[a], 8);
+    }
+    fence_barrier_init();
+    tma_prefetch(&tmX);
+    tma_prefetch(&tmOut);
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&tail->tmem_base)),
+                 "r"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync();  // barriers of both CTAs initialised, TMEM allocated
+  tc_fence_after();
+  const uint32_t tmem_base = tail->tmem_base;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = pair; t < p.ntiles; t += npairs) {
+        const TileDesc td = p.tiles[t];
+        const int koff = MODE == 0 ? p.ring_koff[td.ring] : 0;
+        const int nkb = MODE == 0 ? p.ring_nkb[td.ring] : p.n_pairs * p.kb_per_plane;
+        for (int kb = 0; kb < nkb; ++kb) {
+          if (!mbar_wait(&tail->empty[stage], phase ^ 1, p.err)) goto producer_done;
+          if (leader) mbar_arrive_expect_tx(&tail->full[stage], 2 * STAGE_BYTES);
+          int kc, ra, rb;
+          if (MODE == 0) {
+            kc = koff + kb * BK;
+            ra = td.i0 + 128 * rank;
+            rb = td.j0 + 128 * rank;
+          } else {
+            const int pr = kb / p.kb_per_plane;
+            kc = (kb - pr * p.kb_per_plane) * 64;
+            const int pa = (p.pairs >> (4 * pr)) & 3, pb = (p.pairs >> (4 * pr + 2)) & 3;
+            ra = (td.ring * 3 + pa) * p.plane_rows + td.i0 + 128 * rank;
+            rb = (td.ring * 3 + pb) * p.plane_rows + td.j0 + 128 * rank;
+          }
+          tma_load_2sm(sA + stage * A_BYTES, &tmX, &tail->full[stage], kc, ra);
+          tma_load_2sm(sB + stage * B_BYTES, &tmX, &tail->full[stage], kc, rb);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    producer_done:;
+    }
+  } else if (warp == 1) {
+    if (leader && elect_one()) {
+      int stage = 0, acc = 0;
+      uint32_t phase = 0, acc_phase = 0;
+      for (int t = pair; t < p.ntiles; t += npairs) {
+        const TileDesc td = p.tiles[t];
+        const int nkb = MODE == 0 ? p.ring_nkb[td.ring] : p.n_pairs * p.kb_per_plane;
+        if (!mbar_wait(&tail->tempty[acc], acc_phase ^ 1, p.err)) break;
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + static_cast<uint32_t>(acc * BN);
+        bool ok = true;
+        for (int kb = 0; kb < nkb; ++kb) {
+          if (!mbar_wait(&tail->full[stage], phase, p.err)) {
+            ok = false;
+            break;
+          }
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + stage * A_BYTES), b0 = smem_u32(sB + stage * B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 32; ++k) {
+            if (MODE == 0)
+              mma2_i8(tmem_d, sdesc_k128(a0 + k * 32), sdesc_k128(b0 + k * 32), IDESC,
+                      (kb | k) != 0 ? 1u : 0u);
+            else
+              mma2_bf16(tmem_d, sdesc_k128(a0 + k * 32), sdesc_k128(b0 + k * 32), IDESC,
+                        (kb | k) != 0 ? 1u : 0u);
+          }
+          commit2(&tail->empty[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        if (!ok) break;
+        commit2(&tail->tfull[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    const int sub = warp & 3;
+    const int etid = threadIdx.x - 128;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    bool ok = true;
+    uint32_t* S = tail->stage[sub];
+    for (int t = pair; t < p.ntiles; t += npairs) {
+      const TileDesc td = p.tiles[t];
+      const int i0 = td.i0 + 128 * static_cast<int>(rank);  // this CTA's half tile
+      if (ok) ok = mbar_wait(&tail->tfull[acc], acc_phase, p.err);
+      ok = __all_sync(0xffffffffu, ok);
+      if (ok) tc_fence_after();
+      if (p.g2_partial) {
+        epi_bar();
+        const double* inv = MODE == 0 ? p.inv + static_cast<int64_t>(td.ring) * p.inv_ld : nullptr;
+        for (int e = etid; e < BM + BN; e += 128) {
+          const int idx = e < BM ? i0 + e : td.j0 + (e - BM);
+          const double v = idx < p.n_frames ? (MODE == 0 ? inv[idx] : 1.0) : 0.0;
+          if (e < BM)
+            tail->inv_row[e] = v;
+          else
+            tail->inv_col[e - BM] = v;
+        }
+        for (int e = lane; e < NDIAG_PAD; e += 32) tail->acc[sub][e] = 0.0;
+        epi_bar();
+      }
+      const uint32_t tbase =
+          tmem_base + static_cast<uint32_t>(acc * BN) + (static_cast<uint32_t>(sub * 32) << 16);
+      const int out_row = td.ring * p.ld + i0 + 32 * sub;
+#pragma unroll 1
+      for (int c = 0; ok && c < BN / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld32(tbase + c * 32, r);
+        tmem_ld_wait();
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          *reinterpret_cast<uint4*>(S + lane * 32 + ((q ^ (lane & 7)) << 2)) =
+              make_uint4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
+          asm volatile(
+              "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                  reinterpret_cast<uint64_t>(&tmOut)),
+              "r"(smem_u32(S)), "r"(td.j0 + 32 * c), "r"(out_row)
+              : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        if (p.g2_partial) {
+          const int D0 = td.j0 + 32 * c - i0 - 32 * sub;
+          const double* ir = tail->inv_row + 32 * sub;
+          const double* ic = tail->inv_col + 32 * c;
+          double sa = 0.0, sb = 0.0, r0 = 0.0, r1 = 0.0, r2 = 0.0, r3 = 0.0;
+          const int ma = lane - 31, mb = lane + 1;
+          const bool use_a = D0 + ma >= 0, use_b = lane < 31 && D0 + mb >= 0;
+#pragma unroll
+          for (int l = 0; l < 32; ++l) {
+            if (l == 31 - lane) {
+              sb = (r0 + r1) + (r2 + r3);
+              r0 = r1 = r2 = r3 = 0.0;
+            }
+            const int k = (l + lane + 1) & 31;
+            const uint32_t w = S[l * 32 + ((((k >> 2) ^ (l & 7))) << 2) + (k & 3)];
+            double v;
+            if (MODE == 0)
+              v = static_cast<double>(static_cast<int32_t>(w)) * (ir[l] * ic[k]);
+            else
+              v = ic[k] != 0.0 ? static_cast<double>(__uint_as_float(w)) : 0.0;
+            if ((l & 3) == 0) r0 += v;
+            else if ((l & 3) == 1) r1 += v;
+            else if ((l & 3) == 2) r2 += v;
+            else r3 += v;
+          }
+          sa = (r0 + r1) + (r2 + r3);
+          if (!use_a) sa = 0.0;
+          if (!use_b) sb = 0.0;
+          const int base = 32 * c - 32 * sub + 127;
+          tail->acc[sub][base + ma] += sa;
+          if (lane < 31) tail->acc[sub][base + mb] += sb;
+          __syncwarp();
+        }
+      }
+      if (ok) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (leader)
+            mbar_arrive(&tail->tempty[acc]);
+          else
+            arrive_leader(&tail->tempty[acc]);
+        }
+      }
+      if (p.g2_partial) {
+        epi_bar();
+        // the 1-CTA enumeration index of this half tile (ib = 2I + rank); a
+        // second half past the last 128-row block holds only rows >= T
+        if (ok && 2 * (td.i0 / 256) + static_cast<int>(rank) < p.g2_nbi) {
+          const int64_t half = td.pad + static_cast<int64_t>(rank) * (p.g2_nbj - td.i0 / 256);
+          double* out = p.g2_partial + half * NDIAG_PAD;
+          for (int e = etid; e < NDIAG; e += 128)
+            out[e] = ((tail->acc[0][e] + tail->acc[1][e]) + tail->acc[2][e]) + tail->acc[3][e];
+        }
+      }
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
+
+  tc_fence_before();
+  cluster_sync();  // no remote arrivals in flight, both CTAs done with TMEM
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(TMEM_COLS)
+                 : "memory");
+  }
+}
+
+template <int MODE>
+static cudaError_t launch2(const CUtensorMap& tmX, const CUtensorMap& tmOut, const GramParams& p,
+                           int num_sms, cudaStream_t stream) {
+  const size_t smem = gram2_smem_bytes();
+  cudaError_t e =
+      cudaFuncSetAttribute(k_gram2<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int pairs = num_sms / 2;
+  if (p.ntiles < pairs) pairs = p.ntiles;
+  if (pairs <= 0) return cudaSuccess;
+  k_gram2<MODE><<<2 * pairs, NUM_THREADS, smem, stream>>>(tmX, tmOut, p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gram2_u8(const CUtensorMap& tmX, const CUtensorMap& tmOut, const GramParams& p,
+                            int num_sms, cudaStream_t stream) {
+  return launch2<0>(tmX, tmOut, p, num_sms, stream);
+}
+cudaError_t launch_gram2_cmp(const CUtensorMap& tmY, const CUtensorMap& tmOut, const GramParams& p,
+                             int num_sms, cudaStream_t stream) {
+  return launch2<1>(tmY, tmOut, p, num_sms, stream);
+}
+
+}  // namespace xg

@@ -98,6 +98,8 @@ struct xg_series {
   int32_t* d_ib_tile_off = nullptr;
   int32_t tiles_per_ring = 0;
   TileDesc* d_tiles = nullptr;
+  TileDesc* d_tiles2 = nullptr;    // 256 x 256 pair tiles
+  int32_t ntiles2 = 0;
   int32_t ntiles = 0;
   int64_t tiles_for_t = -1;
   size_t g2part_cap = 0;
@@ -536,6 +538,7 @@ void xg_series_destroy(xg_series* s) {
   dfree(s->d_g2part);
   dfree(s->d_g2pcnt);
   dfree(s->d_tiles);
+  dfree(s->d_tiles2);
   dfree(s->d_nz_bits);
   dfree(s->d_g2tile);
   dfree(s->d_ib_tile_off);
@@ -645,8 +648,43 @@ static int build_tiles(xg_series* s) {
                         cudaMemcpyHostToDevice));
   XG_CUDA(c, cudaMemcpy(s->d_ib_tile_off, iboff.data(), iboff.size() * 4, cudaMemcpyHostToDevice));
   s->ntiles = static_cast<int32_t>(tiles.size());
+  // 256 x 256 pair tiles (k_gram2): pad = 1-CTA index of the upper half tile
+  std::vector<TileDesc> tiles2;
+  const int64_t nbi2 = (s->t + 255) / 256;
+  for (int32_t r = 0; r < s->L->rings; ++r)
+    for (int64_t I = 0; I < nbi2; ++I)
+      for (int64_t J = I; J < nbj; ++J) {
+        TileDesc d;
+        d.ring = r;
+        d.i0 = static_cast<int32_t>(I * 256);
+        d.j0 = static_cast<int32_t>(J * 256);
+        d.pad = static_cast<int32_t>((int64_t)r * s->tiles_per_ring + iboff[2 * I] + (J - I));
+        tiles2.push_back(d);
+      }
+  dfree(s->d_tiles2);
+  XG_CUDA(c, dalloc(&s->d_tiles2, tiles2.size()));
+  XG_CUDA(c, cudaMemcpy(s->d_tiles2, tiles2.data(), tiles2.size() * sizeof(TileDesc),
+                        cudaMemcpyHostToDevice));
+  s->ntiles2 = static_cast<int32_t>(tiles2.size());
   s->tiles_for_t = s->t;
   return XG_OK;
+}
+
+// K2/K4 launch: CTA-pair kernel (default) or the 1-CTA kernel (XG_GRAM_1CTA=1).
+static cudaError_t launch_gram_any(xg_series* s, int mode, const CUtensorMap& in,
+                                   const CUtensorMap& out, GramParams gp) {
+  static const bool one_cta = [] {
+    const char* e = std::getenv("XG_GRAM_1CTA");
+    return e && e[0] == '1';
+  }();
+  gp.g2_nbi = static_cast<int32_t>((s->t + 127) / 128);
+  gp.g2_nbj = static_cast<int32_t>((s->t + 255) / 256);
+  if (one_cta) return mode == 0 ? launch_gram_u8(in, out, gp, s->ctx->num_sms, s->ctx->stream)
+                                : launch_gram_cmp(in, out, gp, s->ctx->num_sms, s->ctx->stream);
+  gp.tiles = s->d_tiles2;
+  gp.ntiles = s->ntiles2;
+  return mode == 0 ? launch_gram2_u8(in, out, gp, s->ctx->num_sms, s->ctx->stream)
+                   : launch_gram2_cmp(in, out, gp, s->ctx->num_sms, s->ctx->stream);
 }
 
 static int run_g2(xg_series* s, int mode) {
@@ -747,7 +785,7 @@ int xg_ttc_raw(xg_series* s, uint32_t flags) {
   CUtensorMap omap;
   rc = make_map_out32(c, &omap, s->d_gram, s->tp, (int64_t)L->rings * s->tp);
   if (rc) return rc;
-  XG_CUDA(c, launch_gram_u8(map, omap, gp, c->num_sms, c->stream));
+  XG_CUDA(c, launch_gram_any(s, 0, map, omap, gp));
   c->launches++;
   if (g2) {
     rc = fold_g2(s, s->d_g2, s->d_g2cnt);
@@ -1062,7 +1100,7 @@ int xg_ttc_compressed(xg_series* s, uint32_t flags) {
   CUtensorMap omap;
   rc = make_map_out32(c, &omap, s->d_cgram, s->tp, (int64_t)L->rings * s->tp);
   if (rc) return rc;
-  XG_CUDA(c, launch_gram_cmp(my, omap, gp, c->num_sms, c->stream));
+  XG_CUDA(c, launch_gram_any(s, 1, my, omap, gp));
   c->launches++;
   if (g2) {
     rc = fold_g2(s, s->d_cg2, s->d_cg2cnt);

@@ -96,7 +96,15 @@ struct GramParams {
   int32_t pairs;
   int32_t kb_per_plane;
   int32_t plane_rows;
+  // pair kernel (k_gram2): 256 x 256 tiles, pad = 1-CTA half-tile index of
+  // the upper half; 128-row / 256-col block counts of the 1-CTA enumeration
+  int32_t g2_nbi, g2_nbj;
 };
+size_t gram2_smem_bytes();
+cudaError_t launch_gram2_u8(const CUtensorMap& tmX, const CUtensorMap& tmOut, const GramParams& p,
+                            int num_sms, cudaStream_t stream);
+cudaError_t launch_gram2_cmp(const CUtensorMap& tmY, const CUtensorMap& tmOut, const GramParams& p,
+                             int num_sms, cudaStream_t stream);
 size_t gram_u8_smem_bytes();
 cudaError_t launch_gram_cmp(const CUtensorMap& tmY, const CUtensorMap& tmOut, const GramParams& p,
                             int num_sms, cudaStream_t stream);
