@@ -36,7 +36,8 @@ constexpr int A_BYTES = BM * BK;   // 16 KB
 constexpr int B_BYTES = 128 * BK;  // 16 KB: this CTA's half of the 256 columns
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int TMEM_COLS = 512;
-constexpr int NUM_THREADS = 256;
+constexpr int EPI_WARPS = 8;        // two per TMEM lane quarter, each half the columns
+constexpr int NUM_THREADS = 128 + 32 * EPI_WARPS;
 constexpr int NDIAG = BM + BN - 1;
 constexpr int NDIAG_PAD = 384;
 constexpr uint32_t kPeerMask = 0xFEFFFFFFu;  // shared::cluster address of the pair leader
@@ -48,7 +49,7 @@ constexpr uint32_t idesc2() {
 }
 
 struct __align__(1024) Tail2 {
-  uint32_t stage[4][32 * 32];
+  uint32_t stage[EPI_WARPS][32 * 32];
   uint64_t full[STAGES];
   uint64_t empty[STAGES];
   uint64_t tfull[2];
@@ -57,7 +58,7 @@ struct __align__(1024) Tail2 {
   uint32_t pad_;
   double inv_row[BM];
   double inv_col[BN];
-  double acc[4][NDIAG_PAD];
+  double acc[EPI_WARPS][NDIAG_PAD];
 };
 
 __device__ __forceinline__ uint32_t cta_rank() {
@@ -69,7 +70,9 @@ __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::
                    : "memory");
 }
-__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+__device__ __forceinline__ void epi_bar() {
+  asm volatile("bar.sync 1, %0;" ::"n"(32 * EPI_WARPS) : "memory");
+}
 
 __device__ __forceinline__ void tma_load_2sm(void* dst, const CUtensorMap* map, uint64_t* bar,
                                              int32_t c0, int32_t c1) {
@@ -136,7 +139,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tail->tfull[a], 1);
-      mbar_init(&tail->tempty[a], 8);
+      mbar_init(&tail->tempty[a], 2 * EPI_WARPS);  // epilogue warps of both CTAs
     }
     fence_barrier_init();
     tma_prefetch(&tmX);
@@ -229,12 +232,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       }
     }
   } else if (warp >= 4) {
-    const int sub = warp & 3;
+    const int ew = warp - 4;        // epilogue warp 0..7
+    const int sub = warp & 3;       // TMEM lane quarter this warp may access
+    const int c_lo = (ew >> 2) * (BN / 32 / 2);  // its half of the 8 column chunks
     const int etid = threadIdx.x - 128;
     int acc = 0;
     uint32_t acc_phase = 0;
     bool ok = true;
-    uint32_t* S = tail->stage[sub];
+    uint32_t* S = tail->stage[ew];
     for (int t = pair; t < p.ntiles; t += npairs) {
       const TileDesc td = p.tiles[t];
       const int i0 = td.i0 + 128 * static_cast<int>(rank);  // this CTA's half tile
@@ -244,7 +249,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       if (p.g2_partial) {
         epi_bar();
         const double* inv = MODE == 0 ? p.inv + static_cast<int64_t>(td.ring) * p.inv_ld : nullptr;
-        for (int e = etid; e < BM + BN; e += 128) {
+        for (int e = etid; e < BM + BN; e += 32 * EPI_WARPS) {
           const int idx = e < BM ? i0 + e : td.j0 + (e - BM);
           const double v = idx < p.n_frames ? (MODE == 0 ? inv[idx] : 1.0) : 0.0;
           if (e < BM)
@@ -252,14 +257,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           else
             tail->inv_col[e - BM] = v;
         }
-        for (int e = lane; e < NDIAG_PAD; e += 32) tail->acc[sub][e] = 0.0;
+        for (int e = lane; e < NDIAG_PAD; e += 32) tail->acc[ew][e] = 0.0;
         epi_bar();
       }
       const uint32_t tbase =
           tmem_base + static_cast<uint32_t>(acc * BN) + (static_cast<uint32_t>(sub * 32) << 16);
       const int out_row = td.ring * p.ld + i0 + 32 * sub;
 #pragma unroll 1
-      for (int c = 0; ok && c < BN / 32; ++c) {
+      for (int c = c_lo; ok && c < c_lo + BN / 32 / 2; ++c) {
         uint32_t r[32];
         tmem_ld32(tbase + c * 32, r);
         tmem_ld_wait();
@@ -308,8 +313,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           if (!use_a) sa = 0.0;
           if (!use_b) sb = 0.0;
           const int base = 32 * c - 32 * sub + 127;
-          tail->acc[sub][base + ma] += sa;
-          if (lane < 31) tail->acc[sub][base + mb] += sb;
+          tail->acc[ew][base + ma] += sa;
+          if (lane < 31) tail->acc[ew][base + mb] += sb;
           __syncwarp();
         }
       }
@@ -330,8 +335,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         if (ok && 2 * (td.i0 / 256) + static_cast<int>(rank) < p.g2_nbi) {
           const int64_t half = td.pad + static_cast<int64_t>(rank) * (p.g2_nbj - td.i0 / 256);
           double* out = p.g2_partial + half * NDIAG_PAD;
-          for (int e = etid; e < NDIAG; e += 128)
-            out[e] = ((tail->acc[0][e] + tail->acc[1][e]) + tail->acc[2][e]) + tail->acc[3][e];
+          for (int e = etid; e < NDIAG; e += 32 * EPI_WARPS) {
+            double sum = tail->acc[0][e];  // fixed warp order
+#pragma unroll
+            for (int w = 1; w < EPI_WARPS; ++w) sum += tail->acc[w][e];
+            out[e] = sum;
+          }
         }
       }
       if (++acc == 2) {
