@@ -31,7 +31,7 @@ namespace {
 constexpr int BM = 128;            // rows per CTA (256 per pair)
 constexpr int BN = 256;            // tile columns
 constexpr int BK = 128;            // bytes of K per stage
-constexpr int STAGES = 5;
+constexpr int STAGES = 4;
 constexpr int A_BYTES = BM * BK;   // 16 KB
 constexpr int B_BYTES = 128 * BK;  // 16 KB: this CTA's half of the 256 columns
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
@@ -49,7 +49,7 @@ constexpr uint32_t idesc2() {
 }
 
 struct __align__(1024) Tail2 {
-  uint32_t stage[EPI_WARPS][32 * 32];
+  uint32_t stage[EPI_WARPS][2 * 32 * 32];  // two 32x32 chunks per warp, 128B-swizzled
   uint64_t full[STAGES];
   uint64_t empty[STAGES];
   uint64_t tfull[2];
@@ -57,7 +57,7 @@ struct __align__(1024) Tail2 {
   uint32_t tmem_base;
   uint32_t pad_;
   double inv_row[BM];
-  double inv_col[BN];
+  double inv_col_ext[BN + 64];
   double acc[EPI_WARPS][NDIAG_PAD];
 };
 
@@ -234,7 +234,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   } else if (warp >= 4) {
     const int ew = warp - 4;        // epilogue warp 0..7
     const int sub = warp & 3;       // TMEM lane quarter this warp may access
-    const int c_lo = (ew >> 2) * (BN / 32 / 2);  // its half of the 8 column chunks
     const int etid = threadIdx.x - 128;
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -249,13 +248,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       if (p.g2_partial) {
         epi_bar();
         const double* inv = MODE == 0 ? p.inv + static_cast<int64_t>(td.ring) * p.inv_ld : nullptr;
-        for (int e = etid; e < BM + BN; e += 32 * EPI_WARPS) {
-          const int idx = e < BM ? i0 + e : td.j0 + (e - BM);
-          const double v = idx < p.n_frames ? (MODE == 0 ? inv[idx] : 1.0) : 0.0;
-          if (e < BM)
-            tail->inv_row[e] = v;
-          else
-            tail->inv_col[e - BM] = v;
+        // inv_col_ext[32 + j] = 1/|x_{j0+j}| for j in [0, 256), zero for the 32
+        // columns either side (the windows reach one chunk past the tile)
+        for (int e = etid; e < BM + BN + 64; e += 32 * EPI_WARPS) {
+          if (e < BM) {
+            const int idx = i0 + e;
+            tail->inv_row[e] = idx < p.n_frames ? (MODE == 0 ? inv[idx] : 1.0) : 0.0;
+          } else {
+            const int j = e - BM - 32;
+            const int idx = td.j0 + j;
+            tail->inv_col_ext[e - BM] = (j >= 0 && j < BN && idx < p.n_frames)
+                                            ? (MODE == 0 ? inv[idx] : 1.0)
+                                            : 0.0;
+          }
         }
         for (int e = lane; e < NDIAG_PAD; e += 32) tail->acc[ew][e] = 0.0;
         epi_bar();
@@ -263,58 +268,63 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       const uint32_t tbase =
           tmem_base + static_cast<uint32_t>(acc * BN) + (static_cast<uint32_t>(sub * 32) << 16);
       const int out_row = td.ring * p.ld + i0 + 32 * sub;
+      // Column chunks c (32 wide) go through staging buffer c & 1.  Group 0
+      // stores chunks 0..3 and also loads chunk 4 (for window 4); group 1
+      // stores 4..7.  Window w spans chunks w-1 and w (64 columns): lane L
+      // sums the elements (l, 32(w-1) + L + 1 + l), l = 0..31 -- one full
+      // diagonal per lane per window, no wrap, 3 FP64 ops per element.
+      const int grp = ew >> 2;
+      const int c_first = grp ? 4 : 0, c_end = grp ? 9 : 5;  // chunk 8 = virtual zeros
 #pragma unroll 1
-      for (int c = c_lo; ok && c < c_lo + BN / 32 / 2; ++c) {
-        uint32_t r[32];
-        tmem_ld32(tbase + c * 32, r);
-        tmem_ld_wait();
-        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-        __syncwarp();
+      for (int c = c_first; ok && c < c_end; ++c) {
+        uint32_t* Sc = S + (c & 1) * 1024;
+        const bool real = c < BN / 32;
+        if (real) {
+          uint32_t r[32];
+          tmem_ld32(tbase + c * 32, r);
+          tmem_ld_wait();
+          // the TMA store issued two chunks ago from this buffer has read it
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          __syncwarp();
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
-          *reinterpret_cast<uint4*>(S + lane * 32 + ((q ^ (lane & 7)) << 2)) =
-              make_uint4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
-        fence_proxy_async();
-        __syncwarp();
-        if (lane == 0) {
-          asm volatile(
-              "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
-                  reinterpret_cast<uint64_t>(&tmOut)),
-              "r"(smem_u32(S)), "r"(td.j0 + 32 * c), "r"(out_row)
-              : "memory");
-          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        }
-        if (p.g2_partial) {
-          const int D0 = td.j0 + 32 * c - i0 - 32 * sub;
-          const double* ir = tail->inv_row + 32 * sub;
-          const double* ic = tail->inv_col + 32 * c;
-          double sa = 0.0, sb = 0.0, r0 = 0.0, r1 = 0.0, r2 = 0.0, r3 = 0.0;
-          const int ma = lane - 31, mb = lane + 1;
-          const bool use_a = D0 + ma >= 0, use_b = lane < 31 && D0 + mb >= 0;
-#pragma unroll
-          for (int l = 0; l < 32; ++l) {
-            if (l == 31 - lane) {
-              sb = (r0 + r1) + (r2 + r3);
-              r0 = r1 = r2 = r3 = 0.0;
-            }
-            const int k = (l + lane + 1) & 31;
-            const uint32_t w = S[l * 32 + ((((k >> 2) ^ (l & 7))) << 2) + (k & 3)];
-            double v;
-            if (MODE == 0)
-              v = static_cast<double>(static_cast<int32_t>(w)) * (ir[l] * ic[k]);
-            else
-              v = ic[k] != 0.0 ? static_cast<double>(__uint_as_float(w)) : 0.0;
-            if ((l & 3) == 0) r0 += v;
-            else if ((l & 3) == 1) r1 += v;
-            else if ((l & 3) == 2) r2 += v;
-            else r3 += v;
+          for (int q = 0; q < 8; ++q)
+            *reinterpret_cast<uint4*>(Sc + lane * 32 + ((q ^ (lane & 7)) << 2)) =
+                make_uint4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0 && (grp ? c >= 4 : c < 4)) {
+            asm volatile(
+                "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                    reinterpret_cast<uint64_t>(&tmOut)),
+                "r"(smem_u32(Sc)), "r"(td.j0 + 32 * c), "r"(out_row)
+                : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           }
-          sa = (r0 + r1) + (r2 + r3);
-          if (!use_a) sa = 0.0;
-          if (!use_b) sb = 0.0;
-          const int base = 32 * c - 32 * sub + 127;
-          tail->acc[ew][base + ma] += sa;
-          if (lane < 31) tail->acc[ew][base + mb] += sb;
+        }
+        const int w = c;  // window of chunks c-1, c
+        if (p.g2_partial && !(grp == 1 && w == 4)) {
+          const int lagw = td.j0 - i0 + 32 * (w - 1 - sub) + lane + 1;  // this lane's lag
+          if (lagw >= 0) {
+            const double* ir = tail->inv_row + 32 * sub;
+            const double* ic = tail->inv_col_ext + 32 * (w - 1) + 32 + lane + 1;  // col + 32 pad
+            const uint32_t* Sp = S + ((c - 1) & 1) * 1024;
+            double r0 = 0.0, r1 = 0.0;
+#pragma unroll
+            for (int l = 0; l < 32; ++l) {
+              const int cr = lane + 1 + l;  // column within the 64-wide window
+              const int kk = cr & 31;
+              const uint32_t* B = cr < 32 ? Sp : Sc;
+              const bool zero = cr < 32 ? (w == 0) : !real;
+              const uint32_t wv = zero ? 0u : B[l * 32 + (((kk >> 2) ^ (l & 7)) << 2) + (kk & 3)];
+              double v;
+              if (MODE == 0)
+                v = static_cast<double>(static_cast<int32_t>(wv)) * (ir[l] * ic[l]);
+              else
+                v = ic[l] != 0.0 ? static_cast<double>(__uint_as_float(wv)) : 0.0;
+              if (l & 1) r1 += v; else r0 += v;
+            }
+            tail->acc[ew][32 * (w - 1 - sub) + lane + 1 + 127] += r0 + r1;
+          }
           __syncwarp();
         }
       }
