@@ -31,12 +31,12 @@ namespace {
 constexpr int BM = 128;            // rows per CTA (256 per pair)
 constexpr int BN = 256;            // tile columns
 constexpr int BK = 128;            // bytes of K per stage
-constexpr int STAGES = 4;
+constexpr int STAGES = 5;
 constexpr int A_BYTES = BM * BK;   // 16 KB
 constexpr int B_BYTES = 128 * BK;  // 16 KB: this CTA's half of the 256 columns
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int TMEM_COLS = 512;
-constexpr int EPI_WARPS = 8;        // two per TMEM lane quarter, each half the columns
+constexpr int EPI_WARPS = 4;        // one per TMEM lane quarter
 constexpr int NUM_THREADS = 128 + 32 * EPI_WARPS;
 constexpr int NDIAG = BM + BN - 1;
 constexpr int NDIAG_PAD = 384;
@@ -70,6 +70,15 @@ __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::
                    : "memory");
 }
+// f32 bits -> f64 with integer ops only (normal numbers; zero and
+// denormals -> +-0, far below the compressed path's 1e-5 tolerance)
+__device__ __forceinline__ double f32_to_f64_bits(uint32_t w) {
+  const uint32_t e = (w >> 23) & 0xFFu;
+  if (e == 0u) return 0.0;
+  const uint32_t hi = (w & 0x80000000u) | ((e + 896u) << 20) | ((w >> 3) & 0xFFFFFu);
+  return __hiloint2double(static_cast<int>(hi), static_cast<int>(w << 29));
+}
+
 __device__ __forceinline__ void epi_bar() {
   asm volatile("bar.sync 1, %0;" ::"n"(32 * EPI_WARPS) : "memory");
 }
@@ -273,8 +282,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       // stores 4..7.  Window w spans chunks w-1 and w (64 columns): lane L
       // sums the elements (l, 32(w-1) + L + 1 + l), l = 0..31 -- one full
       // diagonal per lane per window, no wrap, 3 FP64 ops per element.
-      const int grp = ew >> 2;
-      const int c_first = grp ? 4 : 0, c_end = grp ? 9 : 5;  // chunk 8 = virtual zeros
+      // (with 4 epilogue warps one warp takes chunks 0..7 and windows 0..8)
+      const int grp = EPI_WARPS == 8 ? (ew >> 2) : 0;
+      const int c_first = grp ? 4 : 0;
+      const int c_end = EPI_WARPS == 8 ? (grp ? 9 : 5) : 9;  // chunk 8 = virtual zeros
 #pragma unroll 1
       for (int c = c_first; ok && c < c_end; ++c) {
         uint32_t* Sc = S + (c & 1) * 1024;
@@ -292,7 +303,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                 make_uint4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
           fence_proxy_async();
           __syncwarp();
-          if (lane == 0 && (grp ? c >= 4 : c < 4)) {
+          if (lane == 0 && (EPI_WARPS == 4 || (grp ? c >= 4 : c < 4))) {
             asm volatile(
                 "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
                     reinterpret_cast<uint64_t>(&tmOut)),
@@ -302,7 +313,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           }
         }
         const int w = c;  // window of chunks c-1, c
-        if (p.g2_partial && !(grp == 1 && w == 4)) {
+        if (p.g2_partial && !(EPI_WARPS == 8 && grp == 1 && w == 4)) {
           const int lagw = td.j0 - i0 + 32 * (w - 1 - sub) + lane + 1;  // this lane's lag
           if (lagw >= 0) {
             const double* ir = tail->inv_row + 32 * sub;
@@ -317,10 +328,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
               const bool zero = cr < 32 ? (w == 0) : !real;
               const uint32_t wv = zero ? 0u : B[l * 32 + (((kk >> 2) ^ (l & 7)) << 2) + (kk & 3)];
               double v;
-              if (MODE == 0)
-                v = static_cast<double>(static_cast<int32_t>(wv)) * (ir[l] * ic[l]);
+              if (MODE == 0)  // G >= 0, < 2^31: exact (2^52 + G) - 2^52, no I2F
+                v = (__hiloint2double(0x43300000, static_cast<int>(wv)) - 4503599627370496.0) *
+                    (ir[l] * ic[l]);
               else
-                v = ic[l] != 0.0 ? static_cast<double>(__uint_as_float(wv)) : 0.0;
+                v = ic[l] != 0.0 ? f32_to_f64_bits(wv) : 0.0;
               if (l & 1) r1 += v; else r0 += v;
             }
             tail->acc[ew][32 * (w - 1 - sub) + lane + 1 + 127] += r0 + r1;
