@@ -58,6 +58,8 @@ struct __align__(1024) Tail2 {
   uint32_t pad_;
   double inv_row[BM];
   double inv_col_ext[BN + 64];
+  float2 inv_row2[BM];            // (hi, lo) float split of the same weights
+  float2 inv_col2_ext[BN + 64];
   double acc[EPI_WARPS][NDIAG_PAD];
 };
 
@@ -244,6 +246,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     const int ew = warp - 4;        // epilogue warp 0..7
     const int sub = warp & 3;       // TMEM lane quarter this warp may access
     const int etid = threadIdx.x - 128;
+    // double-float g2 needs every count of the Gram exact in fp32 (< 2^23)
+    const bool dd_ok = p.max_norm2 != nullptr && *p.max_norm2 < (1ull << 23);
     int acc = 0;
     uint32_t acc_phase = 0;
     bool ok = true;
@@ -260,16 +264,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         // inv_col_ext[32 + j] = 1/|x_{j0+j}| for j in [0, 256), zero for the 32
         // columns either side (the windows reach one chunk past the tile)
         for (int e = etid; e < BM + BN + 64; e += 32 * EPI_WARPS) {
+          double v;
           if (e < BM) {
             const int idx = i0 + e;
-            tail->inv_row[e] = idx < p.n_frames ? (MODE == 0 ? inv[idx] : 1.0) : 0.0;
+            v = idx < p.n_frames ? (MODE == 0 ? inv[idx] : 1.0) : 0.0;
+            tail->inv_row[e] = v;
           } else {
             const int j = e - BM - 32;
             const int idx = td.j0 + j;
-            tail->inv_col_ext[e - BM] = (j >= 0 && j < BN && idx < p.n_frames)
-                                            ? (MODE == 0 ? inv[idx] : 1.0)
-                                            : 0.0;
+            v = (j >= 0 && j < BN && idx < p.n_frames) ? (MODE == 0 ? inv[idx] : 1.0) : 0.0;
+            tail->inv_col_ext[e - BM] = v;
           }
+          const float hi = static_cast<float>(v);
+          const float2 hl = make_float2(hi, static_cast<float>(v - static_cast<double>(hi)));
+          if (e < BM)
+            tail->inv_row2[e] = hl;
+          else
+            tail->inv_col2_ext[e - BM] = hl;
         }
         for (int e = lane; e < NDIAG_PAD; e += 32) tail->acc[ew][e] = 0.0;
         epi_bar();
@@ -316,26 +327,64 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         if (p.g2_partial && !(EPI_WARPS == 8 && grp == 1 && w == 4)) {
           const int lagw = td.j0 - i0 + 32 * (w - 1 - sub) + lane + 1;  // this lane's lag
           if (lagw >= 0) {
-            const double* ir = tail->inv_row + 32 * sub;
-            const double* ic = tail->inv_col_ext + 32 * (w - 1) + 32 + lane + 1;  // col + 32 pad
             const uint32_t* Sp = S + ((c - 1) & 1) * 1024;
-            double r0 = 0.0, r1 = 0.0;
+            double wsum;
+            if (MODE == 1 || dd_ok) {
+              // FP32 double-float (~48 bits): exact float G (< 2^23), error-free
+              // two-product of the (hi, lo) weights, TwoSum accumulation; the
+              // B200's FP32 pipe is far wider than its FP64 pipe.
+              const float2* ir2 = tail->inv_row2 + 32 * sub;
+              const float2* ic2 = tail->inv_col2_ext + 32 * (w - 1) + 32 + lane + 1;
+              float sh = 0.f, sl = 0.f;
 #pragma unroll
-            for (int l = 0; l < 32; ++l) {
-              const int cr = lane + 1 + l;  // column within the 64-wide window
-              const int kk = cr & 31;
-              const uint32_t* B = cr < 32 ? Sp : Sc;
-              const bool zero = cr < 32 ? (w == 0) : !real;
-              const uint32_t wv = zero ? 0u : B[l * 32 + (((kk >> 2) ^ (l & 7)) << 2) + (kk & 3)];
-              double v;
-              if (MODE == 0)  // G >= 0, < 2^31: exact (2^52 + G) - 2^52, no I2F
-                v = (__hiloint2double(0x43300000, static_cast<int>(wv)) - 4503599627370496.0) *
+              for (int l = 0; l < 32; ++l) {
+                const int cr = lane + 1 + l;  // column within the 64-wide window
+                const int kk = cr & 31;
+                const uint32_t* B = cr < 32 ? Sp : Sc;
+                const bool zero = cr < 32 ? (w == 0) : !real;
+                const uint32_t wv = zero ? 0u : B[l * 32 + (((kk >> 2) ^ (l & 7)) << 2) + (kk & 3)];
+                float qh, ql;
+                if (MODE == 0) {
+                  const float g = __fsub_rn(__int_as_float(0x4B000000 | static_cast<int>(wv)),
+                                            8388608.f);  // exact for wv < 2^23
+                  const float2 a = ir2[l], b = ic2[l];
+                  const float ph = __fmul_rn(a.x, b.x);
+                  float pe = __fmaf_rn(a.x, b.x, -ph);
+                  pe = __fmaf_rn(a.x, b.y, pe);
+                  pe = __fmaf_rn(a.y, b.x, pe);
+                  qh = __fmul_rn(g, ph);
+                  ql = __fmaf_rn(g, pe, __fmaf_rn(g, ph, -qh));
+                } else {
+                  qh = ic2[l].x != 0.f ? __uint_as_float(wv) : 0.f;
+                  ql = 0.f;
+                }
+                const float t = __fadd_rn(sh, qh);  // TwoSum(sh, qh)
+                const float z = __fsub_rn(t, sh);
+                const float er = __fadd_rn(__fsub_rn(sh, __fsub_rn(t, z)), __fsub_rn(qh, z));
+                sh = t;
+                sl = __fadd_rn(sl, __fadd_rn(er, ql));
+              }
+              wsum = static_cast<double>(sh) + static_cast<double>(sl);
+            } else {
+              // FP64 path (a frame with |x|^2 >= 2^23 in this series)
+              const double* ir = tail->inv_row + 32 * sub;
+              const double* ic = tail->inv_col_ext + 32 * (w - 1) + 32 + lane + 1;  // col + 32 pad
+              double r0 = 0.0, r1 = 0.0;
+#pragma unroll 4
+              for (int l = 0; l < 32; ++l) {
+                const int cr = lane + 1 + l;
+                const int kk = cr & 31;
+                const uint32_t* B = cr < 32 ? Sp : Sc;
+                const bool zero = cr < 32 ? (w == 0) : !real;
+                const uint32_t wv = zero ? 0u : B[l * 32 + (((kk >> 2) ^ (l & 7)) << 2) + (kk & 3)];
+                const double v =
+                    (__hiloint2double(0x43300000, static_cast<int>(wv)) - 4503599627370496.0) *
                     (ir[l] * ic[l]);
-              else
-                v = ic[l] != 0.0 ? f32_to_f64_bits(wv) : 0.0;
-              if (l & 1) r1 += v; else r0 += v;
+                if (l & 1) r1 += v; else r0 += v;
+              }
+              wsum = r0 + r1;
             }
-            tail->acc[ew][32 * (w - 1 - sub) + lane + 1 + 127] += r0 + r1;
+            tail->acc[ew][32 * (w - 1 - sub) + lane + 1 + 127] += wsum;
           }
           __syncwarp();
         }

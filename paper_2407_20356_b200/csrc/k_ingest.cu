@@ -204,6 +204,7 @@ __global__ void k_norms(NormParams p) {
     atomicMin(reinterpret_cast<long long*>(p.first_zero + r), static_cast<long long>(t));
   }
   if (n2 >= (1ll << 31)) atomicOr(p.err, 4);
+  if (p.max_norm2) atomicMax(p.max_norm2, static_cast<unsigned long long>(n2));
 }
 
 }  // namespace

@@ -87,6 +87,7 @@ struct xg_series {
   double* d_inv = nullptr;
   int64_t* d_zero = nullptr;
   int64_t* d_first_zero = nullptr;
+  int64_t* d_max_norm2 = nullptr;  // max |x_t|^2 over all frames and rings
   int32_t* d_gram = nullptr;
   double* d_g2 = nullptr;
   int64_t* d_g2cnt = nullptr;
@@ -501,6 +502,7 @@ int xg_series_create(xg_ctx* c, const xg_layout* L, int64_t max_frames, xg_serie
       (e = dalloc(&s->d_inv, (size_t)s->tp * Q)) != cudaSuccess ||
       (e = dalloc(&s->d_zero, (size_t)Q)) != cudaSuccess ||
       (e = dalloc(&s->d_first_zero, (size_t)Q)) != cudaSuccess ||
+      (e = dalloc(&s->d_max_norm2, (size_t)1)) != cudaSuccess ||
       (e = dalloc(&s->d_gram, (size_t)Q * s->tp * s->tp)) != cudaSuccess ||
       (e = dalloc(&s->d_g2, (size_t)Q * s->tp)) != cudaSuccess ||
       (e = dalloc(&s->d_g2cnt, (size_t)Q * s->tp)) != cudaSuccess ||
@@ -532,6 +534,7 @@ void xg_series_destroy(xg_series* s) {
   dfree(s->d_inv);
   dfree(s->d_zero);
   dfree(s->d_first_zero);
+  dfree(s->d_max_norm2);
   dfree(s->d_gram);
   dfree(s->d_g2);
   dfree(s->d_g2cnt);
@@ -610,6 +613,8 @@ int xg_series_load_frames(xg_series* s, const uint8_t* frames, int64_t n, int on
   s->nz_words = static_cast<int32_t>((n + 31) / 32);
   np.nz_bits = s->d_nz_bits;
   np.nz_words = s->nz_words;
+  np.max_norm2 = reinterpret_cast<unsigned long long*>(s->d_max_norm2);
+  XG_CUDA(c, cudaMemsetAsync(s->d_max_norm2, 0, 8, c->stream));
   XG_CUDA(c, cudaMemsetAsync(s->d_nz_bits, 0, (size_t)L->rings * s->nz_words * 4, c->stream));
   np.err = c->d_err;
   XG_CUDA(c, cudaMemsetAsync(s->d_zero, 0, (size_t)L->rings * 8, c->stream));
@@ -777,6 +782,7 @@ int xg_ttc_raw(xg_series* s, uint32_t flags) {
   gp.ring_stride = s->tp * s->tp;
   gp.ld = static_cast<int32_t>(s->tp);
   gp.err = c->d_err;
+  gp.max_norm2 = reinterpret_cast<const unsigned long long*>(s->d_max_norm2);
   const bool g2 = !(flags & XG_NO_G2);
   gp.inv = s->d_inv;
   gp.inv_ld = s->tp;
@@ -1081,6 +1087,7 @@ int xg_ttc_compressed(xg_series* s, uint32_t flags) {
   gp.ring_stride = s->tp * s->tp;
   gp.ld = static_cast<int32_t>(s->tp);
   gp.err = c->d_err;
+  gp.max_norm2 = reinterpret_cast<const unsigned long long*>(s->d_max_norm2);
   const bool g2 = !(flags & XG_NO_G2);
   gp.inv = s->d_inv;
   gp.inv_ld = s->tp;
@@ -1351,6 +1358,7 @@ int xg_stream_push(xg_stream* s, const uint8_t* frame, int on_device) {
   np.first_zero = s->d_first_zero;
   np.nz_bits = s->d_nz_bits;
   np.nz_words = static_cast<int32_t>(s->tp / 32);
+  np.max_norm2 = nullptr;
   np.err = c->d_err;
   XG_CUDA(c, launch_norms(np, c->stream));
   c->launches += 2;

@@ -63,6 +63,7 @@ struct NormParams {
   int64_t* first_zero;       // [ring] smallest zero-norm frame (sentinel if none)
   uint32_t* nz_bits;         // [ring][nz_words] nonzero-frame bitmask (pre-zeroed)
   int32_t nz_words;
+  unsigned long long* max_norm2;  // running max of |x|^2 (or null)
   int* err;                  // bit 2: overflow
 };
 cudaError_t launch_norms(const NormParams& p, cudaStream_t s);
@@ -99,6 +100,9 @@ struct GramParams {
   // pair kernel (k_gram2): 256 x 256 tiles, pad = 1-CTA half-tile index of
   // the upper half; 128-row / 256-col block counts of the 1-CTA enumeration
   int32_t g2_nbi, g2_nbj;
+  // max |x_t|^2 over the series (K1b): G_ij <= it, so < 2^23 lets the fused g2
+  // run in FP32 double-float arithmetic with exact float Gram values
+  const unsigned long long* max_norm2;
 };
 size_t gram2_smem_bytes();
 cudaError_t launch_gram2_u8(const CUtensorMap& tmX, const CUtensorMap& tmOut, const GramParams& p,
