@@ -424,9 +424,16 @@ def main():
     my_sizes = [sizes[r] for r in mine]
     ops = gram_ops(T, my_sizes)
     achieved = ops / (gram_ms / 1e3) / 1e12
-    roofline = {"bound": "tensor", "kernel": "k_gram_u8 (K2, fused g2 epilogue) + g2 fold", "achieved": achieved,
+    traffic = None
+    try:  # DRAM bytes of K2 from the committed ncu --set full capture (per launch)
+        tr = json.load(open(os.path.join(ROOT, "profiles", "r1_traffic.json")))["k_gram2<0>"]
+        traffic = tr["dram_read_bytes"] + tr["dram_write_bytes"]
+    except Exception:
+        pass
+    roofline = {"bound": "tensor", "kernel": "k_gram2<0> (K2 CTA-pair, fused g2 epilogue) + g2 fold", "achieved": achieved,
                 "peak": peak, "unit": "TOPS (int8)", "frac": achieved / peak,
-                "peak_source": peak_src, "traffic": None,
+                "peak_source": peak_src, "traffic": traffic,
+                "traffic_source": "profiles/r1_traffic.json (ncu dram__bytes_read+write, one launch)",
                 "work_per_launch": f"sum_q T(T+1) M_q = {ops:.4g} int8 ops",
                 "kernel_ms": gram_ms, "share_of_step": gram_ms / ms}
 

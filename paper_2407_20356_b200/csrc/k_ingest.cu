@@ -59,9 +59,13 @@ __global__ void __launch_bounds__(INGEST_THREADS + 32)
   const int bstride = band_stride(p.band);
   uint8_t* bufs = reinterpret_cast<uint8_t*>(ismem);  // NBUF x bstride
   uint16_t* tab = reinterpret_cast<uint16_t*>(bufs + NBUF * bstride);
-
   const int tab0 = p.band_tab[b];
   const int ntab = p.band_tab[b + 1] - tab0;
+  // group table: one word per 4 output bytes -- the smem source offset when
+  // the 4 sources are consecutive (fetched as two aligned words + a funnel
+  // shift), else 0x80000000 (per-byte gather through `tab`)
+  uint32_t* gtab = reinterpret_cast<uint32_t*>(tab + ((ntab + 7) & ~7));
+
   const int zero_at = bstride - 16;
   for (int i = threadIdx.x; i < ntab; i += blockDim.x) {
     const uint32_t e = p.tab[tab0 + i];
@@ -69,6 +73,11 @@ __global__ void __launch_bounds__(INGEST_THREADS + 32)
   }
   if (threadIdx.x < NBUF * 4)
     reinterpret_cast<uint32_t*>(bufs + (threadIdx.x >> 2) * bstride + zero_at)[threadIdx.x & 3] = 0;
+  __syncthreads();
+  for (int g = threadIdx.x; g < ntab / 4; g += blockDim.x) {
+    const uint32_t e0 = tab[4 * g], e1 = tab[4 * g + 1], e2 = tab[4 * g + 2], e3 = tab[4 * g + 3];
+    gtab[g] = (e1 == e0 + 1 && e2 == e0 + 2 && e3 == e0 + 3) ? e0 : 0x80000000u;
+  }
 
   const int seg0 = p.band_seg[b];
   const int64_t pix0 = static_cast<int64_t>(b) * p.band;
@@ -154,17 +163,25 @@ __global__ void __launch_bounds__(INGEST_THREADS + 32)
       const int sidx = p.seg_order[w];  // segment index within the band
       const Segment sg = p.segs[seg0 + sidx];
       const uint16_t* st = tab + sg.taboff;
+      const uint32_t* gt = gtab + sg.taboff / 4;
+      const uint32_t* band32 = reinterpret_cast<const uint32_t*>(band);
       uint32_t sq = 0, sm = 0;
-      // 4 output bytes per lane: a warp reads 128 consecutive output bytes
-      // whose sources within a run are consecutive -> conflict-free LDS.U8
+      // 4 output bytes per lane, a warp covers 128 consecutive output bytes
       for (int off = lane * 4; off < sg.len; off += 128) {
-        const uint2 e = *reinterpret_cast<const uint2*>(st + off);
-        const uint32_t v0 = band[e.x & 0xFFFFu], v1 = band[e.x >> 16];
-        const uint32_t v2 = band[e.y & 0xFFFFu], v3 = band[e.y >> 16];
-        *reinterpret_cast<uint32_t*>(xrow + sg.dst + off) =
-            __byte_perm(v0 | (v1 << 8), v2 | (v3 << 8), 0x5410);
-        sq += v0 * v0 + v1 * v1 + v2 * v2 + v3 * v3;
-        sm += v0 + v1 + v2 + v3;
+        const uint32_t e = gt[off >> 2];
+        uint32_t word;
+        if (!(e & 0x80000000u)) {  // consecutive sources: 2 aligned words
+          const uint32_t lo = band32[e >> 2], hi = band32[(e >> 2) + 1];
+          word = __funnelshift_r(lo, hi, (e & 3u) * 8u);
+        } else {                   // run boundary / padding: byte gather
+          const uint2 ee = *reinterpret_cast<const uint2*>(st + off);
+          const uint32_t v0 = band[ee.x & 0xFFFFu], v1 = band[ee.x >> 16];
+          const uint32_t v2 = band[ee.y & 0xFFFFu], v3 = band[ee.y >> 16];
+          word = __byte_perm(v0 | (v1 << 8), v2 | (v3 << 8), 0x5410);
+        }
+        *reinterpret_cast<uint32_t*>(xrow + sg.dst + off) = word;
+        sq = __dp4a(word, word, sq);
+        sm = __dp4a(word, 0x01010101u, sm);
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
@@ -211,7 +228,8 @@ __global__ void k_norms(NormParams p) {
 
 cudaError_t launch_ingest(const IngestParams& p, cudaStream_t s) {
   const size_t smem = NBUF * static_cast<size_t>(band_stride(p.band)) +
-                      static_cast<size_t>(p.max_tab) * 2 + 16;
+                      static_cast<size_t>((p.max_tab + 7) & ~7) * 2 +
+                      static_cast<size_t>(p.max_tab) + 16;  // byte table + group table
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k_ingest, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
