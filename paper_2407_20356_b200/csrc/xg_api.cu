@@ -56,6 +56,7 @@ struct xg_layout {
   int32_t n_bands = 0;
   int64_t ktot = 0;
   int32_t max_tab = 0;
+  int32_t max_band_segs = 0;
   std::vector<int64_t> ring_pixels, kpad, koff;
   std::vector<int64_t> mask_off;  // [rings + 1] offsets into colpos (mask order)
   std::vector<int64_t> colpos;    // ring-major column of every mask entry
@@ -68,8 +69,6 @@ struct xg_layout {
   int32_t* d_ring_koff = nullptr;
   int32_t* d_ring_nkb = nullptr;
   int32_t n_segs = 0;
-  int32_t* d_ring_seg_begin = nullptr;
-  int32_t* d_ring_seg_list = nullptr;
 };
 
 struct xg_series {
@@ -81,8 +80,6 @@ struct xg_series {
   uint8_t* d_raster = nullptr;
   uint8_t* d_x = nullptr;
   int64_t* d_norm2 = nullptr;
-  int64_t* d_sum1 = nullptr;
-  uint2* d_seg_stats = nullptr;
   double* d_norms = nullptr;
   double* d_inv = nullptr;
   int64_t* d_zero = nullptr;
@@ -390,40 +387,52 @@ int xg_layout_create(xg_ctx* c, int64_t full_pixels, int32_t n_rings,
     L->max_tab = std::max(L->max_tab, local);
   }
   band_seg[nb] = static_cast<int32_t>(segs.size());
-  // Per band, deal segments to the 8 ingest consumer warps by LPT on length.
+  // Cut each band's output into 8 equal runs of 4-byte groups, one per ingest
+  // consumer warp; a warp's run is a list of pieces (segment fragments), so
+  // every warp copies the same number of bytes per frame whatever the ring
+  // geometry.  Pieces replace segments from here on: per-(frame, piece) sums
+  // fold into per-ring norms exactly (integer sums).
   constexpr int kWarps = 8;
   std::vector<int32_t> band_wseg((size_t)nb * (kWarps + 1)), seg_order;
-  seg_order.reserve(segs.size());
-  for (int32_t b = 0; b < nb; ++b) {
-    const int32_t s0 = band_seg[b], s1 = band_seg[b + 1];
-    std::vector<int32_t> idx(s1 - s0);
-    for (int32_t i = 0; i < s1 - s0; ++i) idx[i] = i;
-    std::stable_sort(idx.begin(), idx.end(),
-                     [&](int32_t a, int32_t c) { return segs[s0 + a].len > segs[s0 + c].len; });
-    std::vector<std::vector<int32_t>> bins(kWarps);
-    std::vector<int64_t> load(kWarps, 0);
-    for (int32_t i : idx) {
-      const int w = static_cast<int>(std::min_element(load.begin(), load.end()) - load.begin());
-      bins[w].push_back(i);
-      load[w] += segs[s0 + i].len + 64;  // + per-segment overhead
+  {
+    std::vector<Segment> pieces;
+    std::vector<int32_t> piece_band(nb + 1, 0);
+    for (int32_t b = 0; b < nb; ++b) {
+      piece_band[b] = static_cast<int32_t>(pieces.size());
+      int64_t groups = 0;
+      for (int32_t i = band_seg[b]; i < band_seg[b + 1]; ++i) groups += segs[i].len / 4;
+      int32_t si = band_seg[b];
+      int64_t used = 0;  // groups of segment si already assigned
+      for (int w = 0; w < kWarps; ++w) {
+        band_wseg[(size_t)b * (kWarps + 1) + w] = static_cast<int32_t>(pieces.size());
+        int64_t want = groups * (w + 1) / kWarps - groups * w / kWarps;
+        while (want > 0 && si < band_seg[b + 1]) {
+          const Segment& sg = segs[si];
+          const int64_t take = std::min<int64_t>(want, sg.len / 4 - used);
+          Segment pc;
+          pc.ring = sg.ring;
+          pc.dst = static_cast<int32_t>(sg.dst + 4 * used);
+          pc.len = static_cast<int32_t>(4 * take);
+          pc.taboff = static_cast<int32_t>(sg.taboff + 4 * used);
+          pieces.push_back(pc);
+          want -= take;
+          used += take;
+          if (used == sg.len / 4) { ++si; used = 0; }
+        }
+      }
+      band_wseg[(size_t)b * (kWarps + 1) + kWarps] = static_cast<int32_t>(pieces.size());
     }
-    for (int w = 0; w < kWarps; ++w) {
-      band_wseg[(size_t)b * (kWarps + 1) + w] = static_cast<int32_t>(seg_order.size());
-      std::sort(bins[w].begin(), bins[w].end());
-      for (int32_t i : bins[w]) seg_order.push_back(i);
-    }
-    band_wseg[(size_t)b * (kWarps + 1) + kWarps] = static_cast<int32_t>(seg_order.size());
+    piece_band[nb] = static_cast<int32_t>(pieces.size());
+    for (int32_t b = 0; b < nb; ++b)
+      for (int32_t i = piece_band[b]; i < piece_band[b + 1]; ++i)
+        seg_order.push_back(i - piece_band[b]);
+    segs.swap(pieces);
+    band_seg.swap(piece_band);
   }
+  for (int32_t b = 0; b < nb; ++b)
+    L->max_band_segs = std::max(L->max_band_segs, band_seg[b + 1] - band_seg[b]);
   band_tab[nb] = static_cast<int32_t>(tab.size());
   L->n_segs = static_cast<int32_t>(segs.size());
-  // ring -> its segments in ascending band order (fixed fold order for norms)
-  std::vector<int32_t> rs_begin(n_rings + 1, 0), rs_list(segs.size());
-  for (const Segment& sg : segs) rs_begin[sg.ring + 1]++;
-  for (int32_t r = 0; r < n_rings; ++r) rs_begin[r + 1] += rs_begin[r];
-  {
-    std::vector<int32_t> fill(rs_begin.begin(), rs_begin.end() - 1);
-    for (size_t i = 0; i < segs.size(); ++i) rs_list[fill[segs[i].ring]++] = static_cast<int32_t>(i);
-  }
   std::vector<int32_t> rk(n_rings), rn(n_rings);
   for (int32_t r = 0; r < n_rings; ++r) {
     rk[r] = static_cast<int32_t>(L->koff[r]);
@@ -437,9 +446,7 @@ int xg_layout_create(xg_ctx* c, int64_t full_pixels, int32_t n_rings,
       (e = dalloc(&L->d_band_tab, band_tab.size())) != cudaSuccess ||
       (e = dalloc(&L->d_tab, tab.size())) != cudaSuccess ||
       (e = dalloc(&L->d_ring_koff, rk.size())) != cudaSuccess ||
-      (e = dalloc(&L->d_ring_nkb, rn.size())) != cudaSuccess ||
-      (e = dalloc(&L->d_ring_seg_begin, rs_begin.size())) != cudaSuccess ||
-      (e = dalloc(&L->d_ring_seg_list, rs_list.size())) != cudaSuccess) {
+      (e = dalloc(&L->d_ring_nkb, rn.size())) != cudaSuccess) {
     xg_layout_destroy(L);
     return cuda_fail(c, e, "layout alloc");
   }
@@ -450,9 +457,7 @@ int xg_layout_create(xg_ctx* c, int64_t full_pixels, int32_t n_rings,
   cudaMemcpy(L->d_band_tab, band_tab.data(), band_tab.size() * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(L->d_tab, tab.data(), tab.size() * 2, cudaMemcpyHostToDevice);
   cudaMemcpy(L->d_ring_koff, rk.data(), rk.size() * 4, cudaMemcpyHostToDevice);
-  cudaMemcpy(L->d_ring_nkb, rn.data(), rn.size() * 4, cudaMemcpyHostToDevice);
-  cudaMemcpy(L->d_ring_seg_begin, rs_begin.data(), rs_begin.size() * 4, cudaMemcpyHostToDevice);
-  e = cudaMemcpy(L->d_ring_seg_list, rs_list.data(), rs_list.size() * 4, cudaMemcpyHostToDevice);
+  e = cudaMemcpy(L->d_ring_nkb, rn.data(), rn.size() * 4, cudaMemcpyHostToDevice);
   if (e != cudaSuccess) {
     xg_layout_destroy(L);
     return cuda_fail(c, e, "layout upload");
@@ -471,8 +476,6 @@ void xg_layout_destroy(xg_layout* L) {
   dfree(L->d_tab);
   dfree(L->d_ring_koff);
   dfree(L->d_ring_nkb);
-  dfree(L->d_ring_seg_begin);
-  dfree(L->d_ring_seg_list);
   delete L;
 }
 
@@ -496,8 +499,6 @@ int xg_series_create(xg_ctx* c, const xg_layout* L, int64_t max_frames, xg_serie
   if ((e = dalloc(&s->d_raster, (size_t)max_frames * L->pixels)) != cudaSuccess ||
       (e = dalloc(&s->d_x, (size_t)max_frames * L->ktot)) != cudaSuccess ||
       (e = dalloc(&s->d_norm2, (size_t)max_frames * Q)) != cudaSuccess ||
-      (e = dalloc(&s->d_sum1, (size_t)max_frames * Q)) != cudaSuccess ||
-      (e = dalloc(&s->d_seg_stats, (size_t)max_frames * L->n_segs)) != cudaSuccess ||
       (e = dalloc(&s->d_norms, (size_t)s->tp * Q)) != cudaSuccess ||
       (e = dalloc(&s->d_inv, (size_t)s->tp * Q)) != cudaSuccess ||
       (e = dalloc(&s->d_zero, (size_t)Q)) != cudaSuccess ||
@@ -528,8 +529,6 @@ void xg_series_destroy(xg_series* s) {
   dfree(s->d_raster);
   dfree(s->d_x);
   dfree(s->d_norm2);
-  dfree(s->d_sum1);
-  dfree(s->d_seg_stats);
   dfree(s->d_norms);
   dfree(s->d_inv);
   dfree(s->d_zero);
@@ -584,25 +583,21 @@ int xg_series_load_frames(xg_series* s, const uint8_t* frames, int64_t n, int on
   p.band_tab = L->d_band_tab;
   p.tab = L->d_tab;
   p.max_tab = L->max_tab;
+  p.max_band_segs = L->max_band_segs;
   p.t0 = 0;
   p.n_frames = n;
   // one wave of ~4 resident CTAs per SM, each streaming a run of frames of one band
   const int64_t want = std::max<int64_t>(1, (int64_t)c->num_sms * 4 / std::max(1, L->n_bands));
   p.frames_per_cta = static_cast<int32_t>(std::max<int64_t>(1, (n + want - 1) / want));
-  p.n_segs = L->n_segs;
-  p.seg_stats = s->d_seg_stats;
+  p.norm2 = reinterpret_cast<unsigned long long*>(s->d_norm2);
+  XG_CUDA(c, cudaMemsetAsync(s->d_norm2, 0, (size_t)n * L->rings * 8, c->stream));
   XG_CUDA(c, launch_ingest(p, c->stream));
   c->launches++;
   s->t = n;
   s->have_raw = false;
   NormParams np;
   np.t0 = 0;
-  np.seg_stats = s->d_seg_stats;
-  np.n_segs = L->n_segs;
-  np.ring_seg_begin = L->d_ring_seg_begin;
-  np.ring_seg_list = L->d_ring_seg_list;
   np.norm2 = s->d_norm2;
-  np.sum1 = s->d_sum1;
   np.n_frames = n;
   np.ld = s->tp;
   np.n_rings = L->rings;
@@ -1194,8 +1189,7 @@ struct xg_stream {
   int64_t max_kpad = 0;
   uint8_t* d_frame = nullptr;
   uint8_t* d_x = nullptr;
-  uint2* d_seg_stats = nullptr;
-  int64_t *d_norm2 = nullptr, *d_sum1 = nullptr, *d_zero = nullptr, *d_first_zero = nullptr;
+  int64_t *d_norm2 = nullptr, *d_zero = nullptr, *d_first_zero = nullptr;
   double *d_norms = nullptr, *d_inv = nullptr;
   uint32_t* d_nz_bits = nullptr;
   double *d_g2sum = nullptr, *d_cg2sum = nullptr, *d_g2out = nullptr;
@@ -1231,9 +1225,7 @@ int xg_stream_create(xg_ctx* c, const xg_layout* L, const xg_basis* B, int64_t m
   const bool store = (flags & XG_STREAM_STORE_TTC) != 0;
   if ((e = dalloc(&s->d_frame, (size_t)L->pixels)) != cudaSuccess ||
       (e = dalloc(&s->d_x, (size_t)max_frames * L->ktot)) != cudaSuccess ||
-      (e = dalloc(&s->d_seg_stats, (size_t)max_frames * L->n_segs)) != cudaSuccess ||
       (e = dalloc(&s->d_norm2, (size_t)max_frames * Q)) != cudaSuccess ||
-      (e = dalloc(&s->d_sum1, (size_t)max_frames * Q)) != cudaSuccess ||
       (e = dalloc(&s->d_zero, (size_t)Q)) != cudaSuccess ||
       (e = dalloc(&s->d_first_zero, (size_t)Q)) != cudaSuccess ||
       (e = dalloc(&s->d_norms, (size_t)Q * s->tp)) != cudaSuccess ||
@@ -1290,9 +1282,7 @@ void xg_stream_destroy(xg_stream* s) {
   if (!s) return;
   dfree(s->d_frame);
   dfree(s->d_x);
-  dfree(s->d_seg_stats);
   dfree(s->d_norm2);
-  dfree(s->d_sum1);
   dfree(s->d_zero);
   dfree(s->d_first_zero);
   dfree(s->d_norms);
@@ -1335,20 +1325,16 @@ int xg_stream_push(xg_stream* s, const uint8_t* frame, int on_device) {
   p.band_tab = L->d_band_tab;
   p.tab = L->d_tab;
   p.max_tab = L->max_tab;
+  p.max_band_segs = L->max_band_segs;
   p.t0 = s->t;  // frame 0 of the staging buffer lands in history row t
   p.n_frames = 1;
   p.frames_per_cta = 1;
-  p.n_segs = L->n_segs;
-  p.seg_stats = s->d_seg_stats;
+  p.norm2 = reinterpret_cast<unsigned long long*>(s->d_norm2);
+  XG_CUDA(c, cudaMemsetAsync(s->d_norm2 + s->t * L->rings, 0, (size_t)L->rings * 8, c->stream));
   XG_CUDA(c, launch_ingest(p, c->stream));
   NormParams np;
   np.t0 = s->t;
-  np.seg_stats = s->d_seg_stats;
-  np.n_segs = L->n_segs;
-  np.ring_seg_begin = L->d_ring_seg_begin;
-  np.ring_seg_list = L->d_ring_seg_list;
   np.norm2 = s->d_norm2;
-  np.sum1 = s->d_sum1;
   np.n_frames = 1;
   np.ld = s->tp;
   np.n_rings = L->rings;

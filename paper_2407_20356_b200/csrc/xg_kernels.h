@@ -35,11 +35,11 @@ struct IngestParams {
   const int32_t* band_tab;   // n_bands + 1 table ranges (u16 entries)
   const uint16_t* tab;       // source offsets within the band, 0xFFFF = zero pad
   int32_t max_tab;           // largest band table (entries)
+  int32_t max_band_segs;     // most segments in one band
   int64_t t0;                // first frame index written
   int64_t n_frames;
   int32_t frames_per_cta;
-  int32_t n_segs;            // segments over all bands
-  uint2* seg_stats;          // [frame][segment] {sum of squares, sum} (exact)
+  unsigned long long* norm2;  // [frame][ring] |x|^2, accumulated per piece (rows pre-zeroed)
 };
 cudaError_t launch_ingest(const IngestParams& p, cudaStream_t s);
 
@@ -48,12 +48,7 @@ cudaError_t launch_ingest(const IngestParams& p, cudaStream_t s);
 // counts zero frames per ring and flags int32-Gram overflow (norm2 >= 2^31).
 struct NormParams {
   int64_t t0;                // first frame processed (streaming: the new frame)
-  const uint2* seg_stats;    // [frame][segment]
-  int32_t n_segs;
-  const int32_t* ring_seg_begin;  // CSR: segments of each ring, ascending band
-  const int32_t* ring_seg_list;
-  int64_t* norm2;            // [frame][ring] |x|^2 (exact)
-  int64_t* sum1;             // [frame][ring] sum of counts
+  const int64_t* norm2;      // [frame][ring] |x|^2 (exact, from K1)
   int64_t n_frames;
   int64_t ld;                // frame stride of norms/inv (>= n_frames)
   int32_t n_rings;

@@ -46,6 +46,28 @@ def test_raw_gram_bitwise_and_ttc(ctx, orc, t, h, w, q, mu, seed):
         assert np.array_equal(norms, np.sqrt((xq.astype(np.float64) ** 2).sum(1)))
 
 
+@pytest.mark.parametrize("kind", ["scattered", "thin"])
+def test_raw_gram_irregular_masks(ctx, orc, kind):
+    """Masks whose runs are shorter than 4 pixels (scattered pixels, 1-2 px
+    rings) exercise the ingest's multi-run groups and byte-gather path."""
+    t, h, w, q = 200, 100, 110, 7
+    frames = orc.gen_speckle(t, h, w, 4, 0.2, 21)
+    rng = np.random.default_rng(5)
+    if kind == "scattered":
+        ring = rng.integers(-1, q, size=h * w).astype(np.int32)
+    else:
+        yy, xx = np.mgrid[0:h, 0:w]
+        rad = np.hypot(yy - h / 2, xx - w / 2).ravel()
+        ring = np.where(rad < 2 * q * 1.5, (rad / 1.5).astype(np.int32) % q, -1).astype(np.int32)
+    lay = xg.RingLayout.from_ring_map(ctx, ring, q)
+    s = xg.FrameSeries(lay, t).load(frames).ttc_raw()
+    for r in range(q):
+        xq = frames[:, np.nonzero(ring == r)[0]]
+        assert np.array_equal(s.ttc(r, "gram").astype(np.int64), orc.gram_u8(xq)), f"ring {r}"
+        norms, _ = s.norms(r)
+        assert np.array_equal(norms, np.sqrt((xq.astype(np.float64) ** 2).sum(1)))
+
+
 def test_raw_against_reference_library(ctx, orc, ref):
     """Same check against the UNMODIFIED reference (oracle/_ref)."""
     t, h, w, q = 200, 48, 48, 4
