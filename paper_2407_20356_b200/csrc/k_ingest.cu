@@ -28,36 +28,48 @@ namespace xg {
 namespace {
 
 constexpr int INGEST_THREADS = 256;
-#ifndef XG_NBUF
-#define XG_NBUF 4
-#endif
-#ifndef XG_CPASYNC
-#define XG_CPASYNC 0
-#endif
-#ifndef XG_EXP
-#define XG_EXP 0
-#endif
-constexpr int NBUF = XG_NBUF;  // frames in flight per CTA
-#ifndef XG_PIECE
-#define XG_PIECE 512
-#endif
-constexpr int PIECE = XG_PIECE;   // band bytes per bulk copy
-constexpr int PITCH = XG_PIECE + 16;   // smem pitch of a piece: +16 B skews consecutive
-                             // 512-byte detector rows by 4 banks
-
-__host__ __device__ constexpr int band_stride(int band) {
-  return ((band + PIECE - 1) / PIECE) * PITCH + 16;  // + 16 zero bytes (padding source)
-}
+constexpr int NBUF = 4;  // frames in flight per CTA
+constexpr int PIECE = INGEST_PIECE, PITCH = INGEST_PITCH;
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds_u16(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint2 lds_v2(uint32_t a) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+  return d;
+}
+__device__ __forceinline__ void stg_u32(uint8_t* p, uint32_t v) {
+  asm volatile("st.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_add_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 
-// Warp roles: warps 0..7 consume (each owns a fixed, length-balanced set of
-// the band's segments, assigned on the host by LPT), warp 8 produces (one
-// lane issues the TMA bulk copies).  full/empty mbarriers per ring slot let
-// the consumer warps run up to NBUF frames apart, so per-frame imbalance
-// between warps averages out instead of stalling at a block barrier.
+// Warp roles: warps 0..7 consume (each owns a cost-balanced run of the band's
+// pieces, cut on the host), warp 8 produces (one lane issues the TMA bulk
+// copies).  full/empty mbarriers per ring slot let the consumer warps run up
+// to NBUF frames apart.
 constexpr int CONSUMERS = 8;
 
 __global__ void __launch_bounds__(INGEST_THREADS + 32)
@@ -66,56 +78,27 @@ __global__ void __launch_bounds__(INGEST_THREADS + 32)
   __shared__ __align__(8) uint64_t full[NBUF];
   __shared__ __align__(8) uint64_t empty[NBUF];
   const int b = blockIdx.x;
-  // band buffer: pieces of 512 B at a 528 B pitch, then 16 zero bytes that
-  // the padding entries of the table point to
-  const int bstride = band_stride(p.band);
-  uint8_t* bufs = reinterpret_cast<uint8_t*>(ismem);  // NBUF x bstride
-  // Group table: 8 bytes per 4 output bytes.  A ring's pixels arrive as runs
-  // of consecutive detector pixels (one per row crossing), so a group's bytes
-  // come from at most two runs A, B in the common case; each run is fetched
-  // as two aligned smem words + a funnel shift and a byte permute merges them:
-  //   x = word offset of A | word offset of B << 16
-  //   y = 8*(A mod 4) | 8*(B mod 4) << 8 | permute selector << 16
-  // (B = A for single-run groups).  Groups touching three or more runs (rings
-  // thinner than 4 px) hold the four byte offsets and bit 31 of y set.
-  uint2* gtab = reinterpret_cast<uint2*>(bufs + NBUF * bstride);
-  const int tab0 = p.band_tab[b];
-  const int ntab = p.band_tab[b + 1] - tab0;
+  const int bstride = ingest_band_stride(p.band);
   const int zero_at = bstride - 16;
-  auto smap = [&](uint32_t e) -> uint32_t {
-    return e == 0xFFFFu ? static_cast<uint32_t>(zero_at) : e + 16u * (e / PIECE);
-  };
-  for (int g = threadIdx.x; g < ntab / 4; g += blockDim.x) {
-    const uint2 raw = *reinterpret_cast<const uint2*>(p.tab + tab0 + 4 * g);
-    const uint32_t s0 = smap(raw.x & 0xFFFFu), s1 = smap(raw.x >> 16);
-    const uint32_t s2 = smap(raw.y & 0xFFFFu), s3 = smap(raw.y >> 16);
-    const bool c1 = s1 == s0 + 1, c2 = c1 && s2 == s0 + 2, c3 = c2 && s3 == s0 + 3;
-    const uint32_t na = 1 + c1 + c2 + c3;
-    const uint32_t sb = na == 1 ? s1 : na == 2 ? s2 : na == 3 ? s3 : s0;
-    const bool ok = na == 1 ? (s2 == s1 + 1 && s3 == s1 + 2) : na == 2 ? s3 == s2 + 1 : true;
-    uint2 ent;
-    if (ok) {
-      uint32_t sel = 0;
-      for (uint32_t j = 0; j < 4; ++j) sel |= (j < na ? j : 4 + j - na) << (4 * j);
-      ent.x = (s0 & ~3u) | ((sb & ~3u) << 16);
-      ent.y = 8 * (s0 & 3u) | (8 * (sb & 3u)) << 8 | sel << 16;
-    } else {
-      ent.x = s0 | (s1 << 16);
-      ent.y = s2 | (s3 << 16) | 0x80000000u;
-    }
-    gtab[g] = ent;
+  // shared memory: NBUF band buffers | word table | byte table | pieces
+  uint8_t* bufs = reinterpret_cast<uint8_t*>(ismem);
+  uint16_t* swords = reinterpret_cast<uint16_t*>(bufs + NBUF * bstride);
+  uint2* sbytes = reinterpret_cast<uint2*>(swords + ((p.max_words + 7) & ~7));
+  int4* spieces = reinterpret_cast<int4*>(sbytes + ((p.max_bytes + 1) & ~1));
+  {
+    const int w0 = p.band_word[b], nw = p.band_word[b + 1] - w0;
+    for (int i = threadIdx.x; i < nw; i += blockDim.x) swords[i] = p.words[w0 + i];
+    const int g0 = p.band_byte[b], ng = p.band_byte[b + 1] - g0;
+    for (int i = threadIdx.x; i < ng; i += blockDim.x)
+      sbytes[i] = reinterpret_cast<const uint2*>(p.bytes)[g0 + i];
+    const int pc0 = p.band_piece[b * (CONSUMERS + 1)];
+    const int npc = p.band_piece[b * (CONSUMERS + 1) + CONSUMERS] - pc0;
+    for (int i = threadIdx.x; i < 2 * npc; i += blockDim.x)
+      spieces[i] = reinterpret_cast<const int4*>(p.pieces + pc0)[i];
   }
   if (threadIdx.x < NBUF * 4)
     reinterpret_cast<uint32_t*>(bufs + (threadIdx.x >> 2) * bstride + zero_at)[threadIdx.x & 3] = 0;
-  // the band's segment descriptors in consumer-warp order (seg_order)
-  const int seg0 = p.band_seg[b];
-  const int wb = p.band_wseg[b * (CONSUMERS + 1)];
-  int4* sdesc = reinterpret_cast<int4*>(gtab + ((p.max_tab / 4 + 1) & ~1));
-  for (int i = threadIdx.x; i < p.band_wseg[b * (CONSUMERS + 1) + CONSUMERS] - wb;
-       i += blockDim.x) {
-    const Segment sg = p.segs[seg0 + p.seg_order[wb + i]];
-    sdesc[i] = make_int4(sg.ring, sg.dst, sg.len / 4, sg.taboff / 4);
-  }
+
   const int64_t pix0 = static_cast<int64_t>(b) * p.band;
   const int blen = static_cast<int>((p.pixels - pix0) < p.band ? (p.pixels - pix0) : p.band);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -130,25 +113,27 @@ __global__ void __launch_bounds__(INGEST_THREADS + 32)
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < NBUF; ++i) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(&full[i])),
-                   "r"(XG_CPASYNC ? 32 : 1));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&full[i])));
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(&empty[i])),
                    "r"(CONSUMERS));
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  __syncthreads();  // barriers, table and zero bytes visible
+  __syncthreads();  // barriers, tables and zero bytes visible
 
+  // waiting warps back off so they do not take issue slots from the copiers
   auto wait = [](uint64_t* bar, uint32_t parity) {
     uint32_t ok = 0;
-    while (!ok) {
+    for (;;) {
       asm volatile(
           "{\n\t.reg .pred P;\n\t"
-          "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2, 1000000;\n\t"
+          "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
           "selp.u32 %0, 1, 0, P;\n\t}"
           : "=r"(ok)
           : "r"(smem_addr(bar)), "r"(parity)
           : "memory");
+      if (ok) break;
+      __nanosleep(64);
     }
   };
 
@@ -160,16 +145,7 @@ __global__ void __launch_bounds__(INGEST_THREADS + 32)
       if (use > 0) wait(&empty[slot], static_cast<uint32_t>((use - 1) & 1));
       uint8_t* dst = bufs + slot * bstride;
       const uint8_t* src = p.raster + (f_begin + i) * p.pixels + pix0;
-      if (XG_CPASYNC && bulk) {
-        for (int o = lane * 16; o < blen; o += 512)
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
-                           smem_addr(dst + o + 16 * (o / PIECE))),
-                       "l"(src + o)
-                       : "memory");
-        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(
-                         smem_addr(&full[slot]))
-                     : "memory");
-      } else if (bulk) {
+      if (bulk) {
         if (lane == 0) {
           asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
                            smem_addr(&full[slot])),
@@ -185,7 +161,7 @@ __global__ void __launch_bounds__(INGEST_THREADS + 32)
           }
         }
       } else {
-        for (int k = lane; k < blen; k += 32) dst[k + 16 * (k / PIECE)] = src[k];
+        for (int k = lane; k < blen; k += 32) dst[ingest_smem_offset(k)] = src[k];
         __syncwarp();
         if (lane == 0)
           asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&full[slot]))
@@ -196,47 +172,46 @@ __global__ void __launch_bounds__(INGEST_THREADS + 32)
   }
 
   // -------------------------------------------------------------- consumers
-  const int w0 = p.band_wseg[b * (CONSUMERS + 1) + warp];
-  const int w1 = p.band_wseg[b * (CONSUMERS + 1) + warp + 1];
+  const int pc0 = p.band_piece[b * (CONSUMERS + 1)];
+  const int k0 = p.band_piece[b * (CONSUMERS + 1) + warp] - pc0;
+  const int k1 = p.band_piece[b * (CONSUMERS + 1) + warp + 1] - pc0;
+  const uint32_t words_s = smem_addr(swords), bytes_s = smem_addr(sbytes);
+  const uint32_t bufs_s = smem_addr(bufs);
   for (int64_t i = 0; i < nf; ++i) {
     const int slot = static_cast<int>(i % NBUF);
     wait(&full[slot], static_cast<uint32_t>((i / NBUF) & 1));
-    const uint8_t* band = bufs + slot * bstride;
+    const uint32_t band_s = bufs_s + slot * bstride;
     const int64_t t = p.t0 + f_begin + i;
     uint8_t* xrow = p.x + t * p.ktot;
     unsigned long long* nrow = p.norm2 + t * p.n_rings;
-    for (int w = w0; w < (XG_EXP == 2 ? w0 : w1); ++w) {
-      const int4 sg = sdesc[w - wb];  // {ring, dst, groups, group offset}
-      const uint2* gt = gtab + sg.w;
-      uint32_t* out = reinterpret_cast<uint32_t*>(
-          xrow + (XG_EXP == 3 ? static_cast<int64_t>(b) * p.band + 4 * sg.w
-                 : XG_EXP == 5 ? static_cast<int64_t>(b) * p.band + ((4 * sg.w) & ~127) : sg.y));
+    asm volatile("" : "+l"(xrow), "+l"(nrow));  // computed once per frame, not per piece
+    for (int k = k0; k < k1; ++k) {
+      const int4 pa = spieces[2 * k], pb = spieces[2 * k + 1];  // see Piece
+      uint8_t* out = xrow + pa.y;
       uint32_t sq = 0;
-      // 4 output bytes per lane, a warp covers 128 consecutive output bytes
-      for (int g = lane; g < sg.z; g += 32) {
-        const uint2 e = gt[g];
-        uint32_t word;
-        if (XG_EXP == 1 || XG_EXP == 3 || XG_EXP == 5) {
-          word = *reinterpret_cast<const uint32_t*>(band + ((4 * g) & 8191));
-        } else if (!(e.y & 0x80000000u)) {
-          const uint8_t* pa = band + (e.x & 0xFFFFu);
-          const uint8_t* pb = band + (e.x >> 16);
-          const uint32_t wa = __funnelshift_r(*reinterpret_cast<const uint32_t*>(pa),
-                                              *reinterpret_cast<const uint32_t*>(pa + 4), e.y);
-          const uint32_t wb = __funnelshift_r(*reinterpret_cast<const uint32_t*>(pb),
-                                              *reinterpret_cast<const uint32_t*>(pb + 4), e.y >> 8);
-          word = __byte_perm(wa, wb, e.y >> 16);
-        } else {
-          const uint32_t v0 = band[e.x & 0xFFFFu], v1 = band[e.x >> 16];
-          const uint32_t v2 = band[e.y & 0xFFFFu], v3 = band[(e.y >> 16) & 0x7FFFu];
-          word = __byte_perm(v0 | (v1 << 8), v2 | (v3 << 8), 0x5410);
-        }
-        out[g] = word;
+      // whole source words: one conflict-free 32-bit load per output word
+      const uint32_t wt = words_s + 2u * static_cast<uint32_t>(pa.w);
+#pragma unroll 1
+      for (int g = lane; g < pa.z; g += 32) {
+        const uint32_t word = lds_u32(band_s + 4u * lds_u16(wt + 2u * g));
+        stg_u32(out + 4 * g, word);
+        sq = __dp4a(word, word, sq);
+      }
+      // leftover pixels: 4-byte gather
+      out += 4 * pa.z;
+      const uint32_t bt = bytes_s + 8u * static_cast<uint32_t>(pb.y);
+#pragma unroll 1
+      for (int g = lane; g < pb.x; g += 32) {
+        const uint2 e = lds_v2(bt + 8u * g);
+        const uint32_t v0 = lds_u8(band_s + (e.x & 0xFFFFu)), v1 = lds_u8(band_s + (e.x >> 16));
+        const uint32_t v2 = lds_u8(band_s + (e.y & 0xFFFFu)), v3 = lds_u8(band_s + (e.y >> 16));
+        const uint32_t word = prmt(v0 | (v1 << 8), v2 | (v3 << 8), 0x5410);
+        stg_u32(out + 4 * g, word);
         sq = __dp4a(word, word, sq);
       }
       // exact: integer sums, any order (a piece's sum is < 2^32)
       sq = __reduce_add_sync(0xffffffffu, sq);
-      if (lane == 0) atomicAdd(nrow + sg.x, static_cast<unsigned long long>(sq));
+      if (lane == 0) red_add_u64(nrow + pa.x, sq);
     }
     __syncwarp();
     if (lane == 0)
@@ -290,9 +265,10 @@ __global__ void k_norms(NormParams p) {
 }  // namespace
 
 cudaError_t launch_ingest(const IngestParams& p, cudaStream_t s) {
-  const size_t smem = NBUF * static_cast<size_t>(band_stride(p.band)) +
-                      static_cast<size_t>((p.max_tab / 4 + 1) & ~1) * 8 +  // group table
-                      static_cast<size_t>(p.max_band_segs) * 16 + 16;       // descriptors
+  const size_t smem = NBUF * static_cast<size_t>(ingest_band_stride(p.band)) +
+                      static_cast<size_t>((p.max_words + 7) & ~7) * 2 +  // word table
+                      static_cast<size_t>((p.max_bytes + 1) & ~1) * 8 +  // byte table
+                      static_cast<size_t>(p.max_band_pieces) * sizeof(Piece);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k_ingest, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));

@@ -55,20 +55,18 @@ struct xg_layout {
   int32_t band = 8192;
   int32_t n_bands = 0;
   int64_t ktot = 0;
-  int32_t max_tab = 0;
-  int32_t max_band_segs = 0;
+  int32_t max_words = 0, max_bytes = 0, max_band_pieces = 0;
   std::vector<int64_t> ring_pixels, kpad, koff;
   std::vector<int64_t> mask_off;  // [rings + 1] offsets into colpos (mask order)
   std::vector<int64_t> colpos;    // ring-major column of every mask entry
-  int32_t* d_band_seg = nullptr;
-  int32_t* d_band_wseg = nullptr;
-  int32_t* d_seg_order = nullptr;
-  Segment* d_segs = nullptr;
-  int32_t* d_band_tab = nullptr;
-  uint16_t* d_tab = nullptr;
+  int32_t* d_band_piece = nullptr;
+  Piece* d_pieces = nullptr;
+  int32_t* d_band_word = nullptr;
+  uint16_t* d_words = nullptr;
+  int32_t* d_band_byte = nullptr;
+  uint16_t* d_bytes = nullptr;
   int32_t* d_ring_koff = nullptr;
   int32_t* d_ring_nkb = nullptr;
-  int32_t n_segs = 0;
 };
 
 struct xg_series {
@@ -355,107 +353,146 @@ int xg_layout_create(xg_ctx* c, int64_t full_pixels, int32_t n_rings,
     delete L;
     return fail(c, XG_ERR_CONTRACT, "layout: padded ring width exceeds 2^31 bytes");
   }
-  // Per band: segments (ring order) and the u16 source table.
-  std::vector<int32_t> band_seg(nb + 1, 0), band_tab(nb + 1, 0);
-  std::vector<Segment> segs;
-  std::vector<uint16_t> tab;
-  // bucket indices per (band, ring) without a second pass over rings:
+  // Per band: segments in ring order.  A segment's output is its whole
+  // source words (round-robin over smem banks, so the 32 words a warp loads
+  // at once sit in distinct banks) followed by its remaining pixels packed
+  // 4 per group; colpos records where every mask entry lands.
+  const int32_t bstride = ingest_band_stride(L->band);
+  const uint16_t zero_at = static_cast<uint16_t>(bstride - 16);
+  std::vector<int32_t> band_word(nb + 1, 0), band_byte(nb + 1, 0);
+  std::vector<uint16_t> words, bytes;
+  std::vector<Piece> pieces;
+  constexpr int kWarps = 8;
+  std::vector<int32_t> band_piece((size_t)nb * (kWarps + 1) + 1, 0);
   std::vector<int64_t> cursor(static_cast<size_t>(n_rings), 0);
   for (int32_t r = 0; r < n_rings; ++r) cursor[r] = offsets[r];
+  std::vector<int64_t> pos(static_cast<size_t>(L->band), -1);  // band pixel -> mask entry
+  struct Seg { int32_t ring, dst, nw, woff, nb, boff; };
   for (int32_t b = 0; b < nb; ++b) {
-    band_seg[b] = static_cast<int32_t>(segs.size());
-    band_tab[b] = static_cast<int32_t>(tab.size());
-    int32_t local = 0;
+    band_word[b] = static_cast<int32_t>(words.size());
+    band_byte[b] = static_cast<int32_t>(bytes.size() / 4);
+    const int64_t base = (int64_t)b * L->band;
+    std::vector<Seg> sg;
     for (int32_t r = 0; r < n_rings; ++r) {
       const int64_t n = cnt[(size_t)r * nb + b];
       if (n == 0) continue;
-      const int64_t len = round_up(n, 4);
-      Segment s;
-      s.ring = r;
-      s.dst = static_cast<int32_t>(L->koff[r] + segoff[(size_t)r * nb + b]);
-      s.len = static_cast<int32_t>(len);
-      s.taboff = local;
-      segs.push_back(s);
+      const int64_t* ix = indices + cursor[r];
+      for (int64_t i = 0; i < n; ++i) pos[ix[i] - base] = cursor[r] + i;
+      std::vector<int32_t> bank_words[32], left;
       for (int64_t i = 0; i < n; ++i) {
-        tab.push_back(static_cast<uint16_t>(indices[cursor[r] + i] - (int64_t)b * L->band));
-        L->colpos[cursor[r] + i] = s.dst + i;  // ring-major column of mask entry
-      }
-      for (int64_t i = n; i < len; ++i) tab.push_back(0xFFFF);
-      cursor[r] += n;
-      local += static_cast<int32_t>(len);
-    }
-    L->max_tab = std::max(L->max_tab, local);
-  }
-  band_seg[nb] = static_cast<int32_t>(segs.size());
-  // Cut each band's output into 8 equal runs of 4-byte groups, one per ingest
-  // consumer warp; a warp's run is a list of pieces (segment fragments), so
-  // every warp copies the same number of bytes per frame whatever the ring
-  // geometry.  Pieces replace segments from here on: per-(frame, piece) sums
-  // fold into per-ring norms exactly (integer sums).
-  constexpr int kWarps = 8;
-  std::vector<int32_t> band_wseg((size_t)nb * (kWarps + 1)), seg_order;
-  {
-    std::vector<Segment> pieces;
-    std::vector<int32_t> piece_band(nb + 1, 0);
-    for (int32_t b = 0; b < nb; ++b) {
-      piece_band[b] = static_cast<int32_t>(pieces.size());
-      int64_t groups = 0;
-      for (int32_t i = band_seg[b]; i < band_seg[b + 1]; ++i) groups += segs[i].len / 4;
-      int32_t si = band_seg[b];
-      int64_t used = 0;  // groups of segment si already assigned
-      for (int w = 0; w < kWarps; ++w) {
-        band_wseg[(size_t)b * (kWarps + 1) + w] = static_cast<int32_t>(pieces.size());
-        int64_t want = groups * (w + 1) / kWarps - groups * w / kWarps;
-        while (want > 0 && si < band_seg[b + 1]) {
-          const Segment& sg = segs[si];
-          const int64_t take = std::min<int64_t>(want, sg.len / 4 - used);
-          Segment pc;
-          pc.ring = sg.ring;
-          pc.dst = static_cast<int32_t>(sg.dst + 4 * used);
-          pc.len = static_cast<int32_t>(4 * take);
-          pc.taboff = static_cast<int32_t>(sg.taboff + 4 * used);
-          pieces.push_back(pc);
-          want -= take;
-          used += take;
-          if (used == sg.len / 4) { ++si; used = 0; }
+        const int32_t e = static_cast<int32_t>(ix[i] - base);
+        if ((e & 3) == 0 && i + 3 < n && ix[i + 3] - base == e + 3) {  // ascending => all 4 in ring
+          bank_words[(ingest_smem_offset(e) / 4) & 31].push_back(e);
+          i += 3;
+        } else {
+          left.push_back(e);
         }
       }
-      band_wseg[(size_t)b * (kWarps + 1) + kWarps] = static_cast<int32_t>(pieces.size());
+      Seg s;
+      s.ring = r;
+      s.dst = static_cast<int32_t>(L->koff[r] + segoff[(size_t)r * nb + b]);
+      s.woff = static_cast<int32_t>(words.size()) - band_word[b];
+      s.boff = static_cast<int32_t>(bytes.size() / 4) - band_byte[b];
+      int32_t g = 0;
+      size_t next[32] = {0};
+      for (bool any = true; any;) {
+        any = false;
+        for (int k = 0; k < 32; ++k) {
+          if (next[k] == bank_words[k].size()) continue;
+          const int32_t e = bank_words[k][next[k]++];
+          any = true;
+          words.push_back(static_cast<uint16_t>(ingest_smem_offset(e) / 4));
+          for (int j = 0; j < 4; ++j) L->colpos[pos[e + j]] = s.dst + 4 * g + j;
+          ++g;
+        }
+      }
+      s.nw = g;
+      const size_t nl = left.size(), nlp = static_cast<size_t>(round_up((int64_t)nl, 4));
+      for (size_t q = 0; q < nlp; ++q) {
+        if (q < nl) {
+          bytes.push_back(static_cast<uint16_t>(ingest_smem_offset(left[q])));
+          L->colpos[pos[left[q]]] = s.dst + 4 * g + static_cast<int64_t>(q);
+        } else {
+          bytes.push_back(zero_at);
+        }
+      }
+      s.nb = static_cast<int32_t>(nlp / 4);
+      sg.push_back(s);
+      cursor[r] += n;
     }
-    piece_band[nb] = static_cast<int32_t>(pieces.size());
-    for (int32_t b = 0; b < nb; ++b)
-      for (int32_t i = piece_band[b]; i < piece_band[b + 1]; ++i)
-        seg_order.push_back(i - piece_band[b]);
-    segs.swap(pieces);
-    band_seg.swap(piece_band);
+    // Split the band's groups over the consumer warps by estimated cost
+    // (a word group ~2 shared-memory wavefronts, a byte group ~5).
+    std::vector<int64_t> seg_cost(sg.size() + 1, 0);
+    for (size_t i = 0; i < sg.size(); ++i) seg_cost[i + 1] = seg_cost[i] + 2 * sg[i].nw + 5 * sg[i].nb;
+    const int64_t total = seg_cost.back();
+    size_t si = 0;
+    int32_t j0 = 0;  // next unassigned group of segment si
+    for (int w = 0; w < kWarps; ++w) {
+      band_piece[(size_t)b * (kWarps + 1) + w] = static_cast<int32_t>(pieces.size());
+      const int64_t target = total * (w + 1) / kWarps;
+      while (si < sg.size()) {
+        const Seg& s = sg[si];
+        const int32_t ng = s.nw + s.nb;
+        // groups of this segment that fit below the target
+        int32_t j1 = ng;
+        if (w + 1 < kWarps) {
+          int64_t c = seg_cost[si];
+          j1 = 0;
+          while (j1 < ng && c + (j1 < s.nw ? 2 : 5) <= target) c += (j1++ < s.nw ? 2 : 5);
+          // c now includes groups [0, j1)
+          if (j1 < j0) j1 = j0;
+        }
+        if (j1 > j0) {
+          Piece pc{};
+          pc.ring = s.ring;
+          pc.dst = s.dst + 4 * j0;
+          pc.n_word = std::max(0, std::min(j1, s.nw) - j0);
+          pc.word_off = s.woff + std::min(j0, s.nw);
+          pc.n_byte = (j1 - j0) - pc.n_word;
+          pc.byte_off = s.boff + std::max(0, j0 - s.nw);
+          pieces.push_back(pc);
+        }
+        if (j1 < ng) { j0 = j1; break; }
+        ++si;
+        j0 = 0;
+      }
+    }
+    band_piece[(size_t)b * (kWarps + 1) + kWarps] = static_cast<int32_t>(pieces.size());
+    L->max_words = std::max(L->max_words, static_cast<int32_t>(words.size()) - band_word[b]);
+    L->max_bytes =
+        std::max(L->max_bytes, static_cast<int32_t>(bytes.size() / 4) - band_byte[b]);
+    L->max_band_pieces = std::max(
+        L->max_band_pieces, band_piece[(size_t)b * (kWarps + 1) + kWarps] -
+                                band_piece[(size_t)b * (kWarps + 1)]);
   }
-  for (int32_t b = 0; b < nb; ++b)
-    L->max_band_segs = std::max(L->max_band_segs, band_seg[b + 1] - band_seg[b]);
-  band_tab[nb] = static_cast<int32_t>(tab.size());
-  L->n_segs = static_cast<int32_t>(segs.size());
+  band_word[nb] = static_cast<int32_t>(words.size());
+  band_byte[nb] = static_cast<int32_t>(bytes.size() / 4);
+  if (words.empty()) words.push_back(0);
+  if (bytes.empty()) bytes.assign(4, zero_at);
+  if (pieces.empty()) pieces.push_back(Piece{});
   std::vector<int32_t> rk(n_rings), rn(n_rings);
   for (int32_t r = 0; r < n_rings; ++r) {
     rk[r] = static_cast<int32_t>(L->koff[r]);
     rn[r] = static_cast<int32_t>(L->kpad[r] / 128);
   }
   cudaError_t e = cudaSuccess;
-  if ((e = dalloc(&L->d_band_seg, band_seg.size())) != cudaSuccess ||
-      (e = dalloc(&L->d_band_wseg, band_wseg.size())) != cudaSuccess ||
-      (e = dalloc(&L->d_seg_order, seg_order.size())) != cudaSuccess ||
-      (e = dalloc(&L->d_segs, segs.size())) != cudaSuccess ||
-      (e = dalloc(&L->d_band_tab, band_tab.size())) != cudaSuccess ||
-      (e = dalloc(&L->d_tab, tab.size())) != cudaSuccess ||
+  if ((e = dalloc(&L->d_band_piece, band_piece.size())) != cudaSuccess ||
+      (e = dalloc(&L->d_pieces, pieces.size())) != cudaSuccess ||
+      (e = dalloc(&L->d_band_word, band_word.size())) != cudaSuccess ||
+      (e = dalloc(&L->d_words, words.size())) != cudaSuccess ||
+      (e = dalloc(&L->d_band_byte, band_byte.size())) != cudaSuccess ||
+      (e = dalloc(&L->d_bytes, bytes.size())) != cudaSuccess ||
       (e = dalloc(&L->d_ring_koff, rk.size())) != cudaSuccess ||
       (e = dalloc(&L->d_ring_nkb, rn.size())) != cudaSuccess) {
     xg_layout_destroy(L);
     return cuda_fail(c, e, "layout alloc");
   }
-  cudaMemcpy(L->d_band_seg, band_seg.data(), band_seg.size() * 4, cudaMemcpyHostToDevice);
-  cudaMemcpy(L->d_band_wseg, band_wseg.data(), band_wseg.size() * 4, cudaMemcpyHostToDevice);
-  cudaMemcpy(L->d_seg_order, seg_order.data(), seg_order.size() * 4, cudaMemcpyHostToDevice);
-  cudaMemcpy(L->d_segs, segs.data(), segs.size() * sizeof(Segment), cudaMemcpyHostToDevice);
-  cudaMemcpy(L->d_band_tab, band_tab.data(), band_tab.size() * 4, cudaMemcpyHostToDevice);
-  cudaMemcpy(L->d_tab, tab.data(), tab.size() * 2, cudaMemcpyHostToDevice);
+  cudaMemcpy(L->d_band_piece, band_piece.data(), band_piece.size() * 4, cudaMemcpyHostToDevice);
+  cudaMemcpy(L->d_pieces, pieces.data(), pieces.size() * sizeof(Piece), cudaMemcpyHostToDevice);
+  cudaMemcpy(L->d_band_word, band_word.data(), band_word.size() * 4, cudaMemcpyHostToDevice);
+  cudaMemcpy(L->d_words, words.data(), words.size() * 2, cudaMemcpyHostToDevice);
+  cudaMemcpy(L->d_band_byte, band_byte.data(), band_byte.size() * 4, cudaMemcpyHostToDevice);
+  cudaMemcpy(L->d_bytes, bytes.data(), bytes.size() * 2, cudaMemcpyHostToDevice);
   cudaMemcpy(L->d_ring_koff, rk.data(), rk.size() * 4, cudaMemcpyHostToDevice);
   e = cudaMemcpy(L->d_ring_nkb, rn.data(), rn.size() * 4, cudaMemcpyHostToDevice);
   if (e != cudaSuccess) {
@@ -468,12 +505,12 @@ int xg_layout_create(xg_ctx* c, int64_t full_pixels, int32_t n_rings,
 
 void xg_layout_destroy(xg_layout* L) {
   if (!L) return;
-  dfree(L->d_band_seg);
-  dfree(L->d_band_wseg);
-  dfree(L->d_seg_order);
-  dfree(L->d_segs);
-  dfree(L->d_band_tab);
-  dfree(L->d_tab);
+  dfree(L->d_band_piece);
+  dfree(L->d_pieces);
+  dfree(L->d_band_word);
+  dfree(L->d_words);
+  dfree(L->d_band_byte);
+  dfree(L->d_bytes);
   dfree(L->d_ring_koff);
   dfree(L->d_ring_nkb);
   delete L;
@@ -576,14 +613,15 @@ int xg_series_load_frames(xg_series* s, const uint8_t* frames, int64_t n, int on
   p.band = L->band;
   p.n_bands = L->n_bands;
   p.n_rings = L->rings;
-  p.band_seg = L->d_band_seg;
-  p.band_wseg = L->d_band_wseg;
-  p.seg_order = L->d_seg_order;
-  p.segs = L->d_segs;
-  p.band_tab = L->d_band_tab;
-  p.tab = L->d_tab;
-  p.max_tab = L->max_tab;
-  p.max_band_segs = L->max_band_segs;
+  p.band_piece = L->d_band_piece;
+  p.pieces = L->d_pieces;
+  p.band_word = L->d_band_word;
+  p.words = L->d_words;
+  p.band_byte = L->d_band_byte;
+  p.bytes = L->d_bytes;
+  p.max_words = L->max_words;
+  p.max_bytes = L->max_bytes;
+  p.max_band_pieces = L->max_band_pieces;
   p.t0 = 0;
   p.n_frames = n;
   // one wave of ~4 resident CTAs per SM, each streaming a run of frames of one band
@@ -1318,14 +1356,15 @@ int xg_stream_push(xg_stream* s, const uint8_t* frame, int on_device) {
   p.band = L->band;
   p.n_bands = L->n_bands;
   p.n_rings = L->rings;
-  p.band_seg = L->d_band_seg;
-  p.band_wseg = L->d_band_wseg;
-  p.seg_order = L->d_seg_order;
-  p.segs = L->d_segs;
-  p.band_tab = L->d_band_tab;
-  p.tab = L->d_tab;
-  p.max_tab = L->max_tab;
-  p.max_band_segs = L->max_band_segs;
+  p.band_piece = L->d_band_piece;
+  p.pieces = L->d_pieces;
+  p.band_word = L->d_band_word;
+  p.words = L->d_words;
+  p.band_byte = L->d_band_byte;
+  p.bytes = L->d_bytes;
+  p.max_words = L->max_words;
+  p.max_bytes = L->max_bytes;
+  p.max_band_pieces = L->max_band_pieces;
   p.t0 = s->t;  // frame 0 of the staging buffer lands in history row t
   p.n_frames = 1;
   p.frames_per_cta = 1;

@@ -11,13 +11,30 @@
 namespace xg {
 
 // ---------------------------------------------------------------- K1 ingest
-// One "segment" = the pixels of one ring inside one detector band, padded to
-// a multiple of 4 bytes, written to a contiguous range of the ring-major row.
-struct Segment {
+// A detector band (8192 pixels) is staged in shared memory as 512-byte pieces
+// at a 528-byte pitch (+16 zero bytes that padding entries point to).
+constexpr int INGEST_PIECE = 512;
+constexpr int INGEST_PITCH = 528;
+__host__ __device__ constexpr int ingest_band_stride(int band) {
+  return ((band + INGEST_PIECE - 1) / INGEST_PIECE) * INGEST_PITCH + 16;
+}
+__host__ __device__ constexpr int ingest_smem_offset(int e) {  // band byte -> smem byte
+  return e + (INGEST_PITCH - INGEST_PIECE) * (e / INGEST_PIECE);
+}
+
+// The pixels of one ring inside one band form a "segment" of the ring-major
+// row: first every source word whose 4 pixels all belong to the ring (copied
+// as a word), then the remaining pixels packed 4 per group (gathered byte by
+// byte, zero padded).  A "piece" is the part of a segment one consumer warp
+// handles; pieces are balanced across the band's 8 consumer warps.
+struct Piece {
   int32_t ring;
-  int32_t dst;     // byte column in the ring-major row (multiple of 4)
-  int32_t len;     // bytes incl. zero padding (multiple of 4)
-  int32_t taboff;  // offset of this segment's source table within its band
+  int32_t dst;       // first output byte column (multiple of 4)
+  int32_t n_word;    // whole-word groups
+  int32_t word_off;  // into the band's word table (u16 smem word index each)
+  int32_t n_byte;    // byte-gathered groups (after the word groups)
+  int32_t byte_off;  // into the band's byte table (4 u16 smem byte offsets each)
+  int32_t pad0, pad1;
 };
 
 struct IngestParams {
@@ -28,14 +45,15 @@ struct IngestParams {
   int32_t band;              // pixels per band
   int32_t n_bands;
   int32_t n_rings;
-  const int32_t* band_seg;   // n_bands + 1 segment ranges
-  const Segment* segs;
-  const int32_t* band_wseg;  // [n_bands][9]: per consumer warp, range in seg_order
-  const int32_t* seg_order;  // segment indices (within band), LPT-balanced per warp
-  const int32_t* band_tab;   // n_bands + 1 table ranges (u16 entries)
-  const uint16_t* tab;       // source offsets within the band, 0xFFFF = zero pad
-  int32_t max_tab;           // largest band table (entries)
-  int32_t max_band_segs;     // most segments in one band
+  const int32_t* band_piece; // [n_bands][9]: piece range of each consumer warp
+  const Piece* pieces;
+  const int32_t* band_word;  // n_bands + 1 ranges of `words`
+  const uint16_t* words;
+  const int32_t* band_byte;  // n_bands + 1 ranges of `bytes` (in groups)
+  const uint16_t* bytes;     // 4 per group
+  int32_t max_words;         // largest band word table
+  int32_t max_bytes;         // largest band byte table (groups)
+  int32_t max_band_pieces;
   int64_t t0;                // first frame index written
   int64_t n_frames;
   int32_t frames_per_cta;
