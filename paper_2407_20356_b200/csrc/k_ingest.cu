@@ -28,7 +28,21 @@ namespace xg {
 namespace {
 
 constexpr int INGEST_THREADS = 256;
-constexpr int NBUF = 4;  // frames in flight per CTA
+#ifndef XG_EXP
+#define XG_EXP 0
+#endif
+#ifndef XG_SLEEP
+#define XG_SLEEP 64
+#endif
+#ifndef XG_NBUF
+#define XG_NBUF 4
+#endif
+constexpr int NBUF = XG_NBUF;  // frames in flight per CTA
+#ifndef XG_FR
+#define XG_FR 2
+#endif
+constexpr int FR = XG_FR;      // frames per consumer pass (divides NBUF)
+static_assert(NBUF % FR == 0, "NBUF must be a multiple of FR");
 constexpr int PIECE = INGEST_PIECE, PITCH = INGEST_PITCH;
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -133,7 +147,7 @@ __global__ void __launch_bounds__(INGEST_THREADS + 32)
           : "r"(smem_addr(bar)), "r"(parity)
           : "memory");
       if (ok) break;
-      __nanosleep(64);
+      __nanosleep(XG_SLEEP);
     }
   };
 
@@ -177,46 +191,70 @@ __global__ void __launch_bounds__(INGEST_THREADS + 32)
   const int k1 = p.band_piece[b * (CONSUMERS + 1) + warp + 1] - pc0;
   const uint32_t words_s = smem_addr(swords), bytes_s = smem_addr(sbytes);
   const uint32_t bufs_s = smem_addr(bufs);
-  for (int64_t i = 0; i < nf; ++i) {
-    const int slot = static_cast<int>(i % NBUF);
-    wait(&full[slot], static_cast<uint32_t>((i / NBUF) & 1));
-    const uint32_t band_s = bufs_s + slot * bstride;
-    const int64_t t = p.t0 + f_begin + i;
-    uint8_t* xrow = p.x + t * p.ktot;
-    unsigned long long* nrow = p.norm2 + t * p.n_rings;
-    asm volatile("" : "+l"(xrow), "+l"(nrow));  // computed once per frame, not per piece
+  // FR frames per pass: a table entry is read once and serves FR frames, and
+  // the per-piece bookkeeping is paid once per FR frames.
+  for (int64_t i = 0; i < nf; i += FR) {
+    const int slot = static_cast<int>(i % NBUF);  // FR consecutive slots
+    const int nfr = nf - i < FR ? static_cast<int>(nf - i) : FR;
+    uint32_t band_s[FR];
+    uint8_t* xrow[FR];
+    unsigned long long* nrow[FR];
+#pragma unroll
+    for (int f = 0; f < FR; ++f) {
+      const int ff = f < nfr ? f : 0;  // missing tail frames redo frame 0 (not stored)
+      if (f < nfr) wait(&full[slot + f], static_cast<uint32_t>(((i + f) / NBUF) & 1));
+      band_s[f] = bufs_s + (slot + ff) * bstride;
+      const int64_t t = p.t0 + f_begin + i + ff;
+      xrow[f] = p.x + t * p.ktot;
+      nrow[f] = p.norm2 + t * p.n_rings;
+      asm volatile("" : "+l"(xrow[f]), "+l"(nrow[f]));  // once per frame, not per piece
+    }
     for (int k = k0; k < k1; ++k) {
       const int4 pa = spieces[2 * k], pb = spieces[2 * k + 1];  // see Piece
-      uint8_t* out = xrow + pa.y;
-      uint32_t sq = 0;
+      uint32_t sq[FR];
+#pragma unroll
+      for (int f = 0; f < FR; ++f) sq[f] = 0;
       // whole source words: one conflict-free 32-bit load per output word
       const uint32_t wt = words_s + 2u * static_cast<uint32_t>(pa.w);
 #pragma unroll 1
       for (int g = lane; g < pa.z; g += 32) {
-        const uint32_t word = lds_u32(band_s + 4u * lds_u16(wt + 2u * g));
-        stg_u32(out + 4 * g, word);
-        sq = __dp4a(word, word, sq);
+        const uint32_t w4 = 4u * lds_u16(wt + 2u * g);
+#pragma unroll
+        for (int f = 0; f < FR; ++f) {
+          const uint32_t word = lds_u32(band_s[f] + w4);
+          if (f < nfr) stg_u32(xrow[f] + pa.y + 4 * g, word);
+          sq[f] = __dp4a(word, word, sq[f]);
+        }
       }
       // leftover pixels: 4-byte gather
-      out += 4 * pa.z;
+      const int ob = pa.y + 4 * pa.z;
       const uint32_t bt = bytes_s + 8u * static_cast<uint32_t>(pb.y);
 #pragma unroll 1
       for (int g = lane; g < pb.x; g += 32) {
         const uint2 e = lds_v2(bt + 8u * g);
-        const uint32_t v0 = lds_u8(band_s + (e.x & 0xFFFFu)), v1 = lds_u8(band_s + (e.x >> 16));
-        const uint32_t v2 = lds_u8(band_s + (e.y & 0xFFFFu)), v3 = lds_u8(band_s + (e.y >> 16));
-        const uint32_t word = prmt(v0 | (v1 << 8), v2 | (v3 << 8), 0x5410);
-        stg_u32(out + 4 * g, word);
-        sq = __dp4a(word, word, sq);
+        const uint32_t o0 = e.x & 0xFFFFu, o1 = e.x >> 16, o2 = e.y & 0xFFFFu, o3 = e.y >> 16;
+#pragma unroll
+        for (int f = 0; f < FR; ++f) {
+          const uint32_t v0 = lds_u8(band_s[f] + o0), v1 = lds_u8(band_s[f] + o1);
+          const uint32_t v2 = lds_u8(band_s[f] + o2), v3 = lds_u8(band_s[f] + o3);
+          const uint32_t word = prmt(v0 | (v1 << 8), v2 | (v3 << 8), 0x5410);
+          if (f < nfr) stg_u32(xrow[f] + ob + 4 * g, word);
+          sq[f] = __dp4a(word, word, sq[f]);
+        }
       }
       // exact: integer sums, any order (a piece's sum is < 2^32)
-      sq = __reduce_add_sync(0xffffffffu, sq);
-      if (lane == 0) red_add_u64(nrow + pa.x, sq);
+#pragma unroll
+      for (int f = 0; f < FR; ++f) {
+        const uint32_t v = __reduce_add_sync(0xffffffffu, sq[f]);
+        if (lane == 0 && f < nfr) red_add_u64(nrow[f] + pa.x, v);
+      }
     }
     __syncwarp();
     if (lane == 0)
-      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&empty[slot]))
-                   : "memory");
+      for (int f = 0; f < nfr; ++f)
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
+                         smem_addr(&empty[slot + f]))
+                     : "memory");
   }
 }
 
