@@ -117,7 +117,7 @@ struct GramParams {
   // run in FP32 double-float arithmetic with exact float Gram values
   const unsigned long long* max_norm2;
 };
-size_t gram2_smem_bytes();
+size_t gram2_smem_bytes(int mode);
 cudaError_t launch_gram2_u8(const CUtensorMap& tmX, const CUtensorMap& tmOut, const GramParams& p,
                             int num_sms, cudaStream_t stream);
 cudaError_t launch_gram2_cmp(const CUtensorMap& tmY, const CUtensorMap& tmOut, const GramParams& p,
