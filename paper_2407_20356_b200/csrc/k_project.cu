@@ -31,20 +31,35 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 128;
-constexpr int STAGES = 4;
+constexpr int MAX_STAGES = 4;
 constexpr int A_BYTES = BM * BK;    // 16 KB
-constexpr int B_BYTES = 256 * BK;   // room for up to 256 digit rows
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int TMEM_COLS = 512;
 constexpr int NUM_THREADS = 256;
+constexpr int SMEM_LIMIT = 227 * 1024;
+
+// Epilogue staging per epilogue warp (32 frames x 16 coefficients): the f64
+// coefficients transposed through shared memory (row pitch 17 doubles) so the
+// global stores are row-contiguous, and the three bf16 planes as dense
+// 32 x 32-byte boxes for TMA tensor stores (double-buffered).
+struct __align__(16) EpiStage {
+  double y[32 * 17];
+  uint32_t planes[2][3][32 * 8];
+};
 
 struct __align__(8) ProjTail {
-  uint64_t full[STAGES];
-  uint64_t empty[STAGES];
+  uint64_t full[MAX_STAGES];
+  uint64_t empty[MAX_STAGES];
   uint64_t tfull[2];
   uint64_t tempty[2];
   uint32_t tmem_base;
 };
+
+__host__ __device__ inline int proj_stage_bytes(int nt_rows) { return A_BYTES + nt_rows * BK; }
+__host__ __device__ inline int proj_stages(int nt_rows) {
+  const int fixed = 1024 + 4 * static_cast<int>(sizeof(EpiStage)) + static_cast<int>(sizeof(ProjTail));
+  const int st = (SMEM_LIMIT - fixed) / proj_stage_bytes(nt_rows);
+  return st < MAX_STAGES ? st : MAX_STAGES;
+}
 
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile(
@@ -58,21 +73,26 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
 
 }  // namespace
 
-size_t project_smem_bytes() { return 1024 + STAGES * STAGE_BYTES + sizeof(ProjTail); }
+size_t project_smem_bytes(int nt_rows) {
+  return 1024 + static_cast<size_t>(proj_stages(nt_rows)) * proj_stage_bytes(nt_rows) +
+         4 * sizeof(EpiStage) + sizeof(ProjTail);
+}
 
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     k_project(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmV,
-              ProjParams p) {
+              const __grid_constant__ CUtensorMap tmP, ProjParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  const int nt_rows = p.n_digits * p.kt;               // N of the MMA (multiple of 16)
+  const int STAGES = proj_stages(nt_rows);
+  const int B_BYTES = nt_rows * BK;                    // multiple of 2 KB
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * A_BYTES;
-  ProjTail* tail = reinterpret_cast<ProjTail*>(smem + STAGES * STAGE_BYTES);
+  EpiStage* epi = reinterpret_cast<EpiStage*>(sB + STAGES * B_BYTES);
+  ProjTail* tail = reinterpret_cast<ProjTail*>(epi + 4);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nt_rows = p.n_digits * p.kt;               // N of the MMA (multiple of 16)
-  const int nb_boxes = (nt_rows + 127) / 128;
   const uint32_t idesc = idesc_i8(BM, static_cast<uint32_t>(nt_rows), true);
-  const uint32_t stage_tx = A_BYTES + nb_boxes * 128 * BK;
+  const uint32_t stage_tx = A_BYTES + nt_rows * BK;  // one box of all digit rows
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -106,9 +126,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           mbar_arrive_expect_tx(&tail->full[stage], stage_tx);
           const int kc = koff + kb * BK;
           tma_load_2d(sA + stage * A_BYTES, &tmX, &tail->full[stage], kc, td.i0);
-          for (int bx = 0; bx < nb_boxes; ++bx)
-            tma_load_2d(sB + stage * B_BYTES + bx * 128 * BK, &tmV, &tail->full[stage], kc,
-                        vrow + bx * 128);
+          tma_load_2d(sB + stage * B_BYTES, &tmV, &tail->full[stage], kc, vrow);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -170,37 +188,81 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const uint32_t tbase =
           tmem_base + static_cast<uint32_t>(acc * 256) + (static_cast<uint32_t>(sub * 32) << 16);
       const double* scale = p.scale + static_cast<int64_t>(td.ring) * p.k;
+      EpiStage* es = epi + sub;
       for (int jc = 0; jc < p.kt; jc += 16) {
         uint32_t a0[16], a1[16], a2[16];
         tmem_ld16(tbase + jc, a0);
         if (p.n_digits > 1) tmem_ld16(tbase + p.kt + jc, a1);
         if (p.n_digits > 2) tmem_ld16(tbase + 2 * p.kt + jc, a2);
         tmem_ld_wait();
-        if (live) {  // (no early continue: the next tcgen05.ld needs the whole warp)
-        const int j0 = td.j0 * p.kt + jc;
-        double* yrow = p.y + (static_cast<int64_t>(td.ring) * p.y_ld + frame) * p.k + j0;
+        const int j0 = td.j0 * p.kt + jc;  // first coefficient of this chunk
+        const int pb = (jc >> 4) & 1;      // planes staging buffer
+        // the TMA stores issued from this buffer two chunks ago have read it
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        __syncwarp();
+        uint32_t pk[3][8];
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
-          double s = static_cast<double>(static_cast<int32_t>(a0[e]));
-          if (p.n_digits > 1) s += static_cast<double>(static_cast<int32_t>(a1[e])) * (1.0 / 254.0);
-          if (p.n_digits > 2)
-            s += static_cast<double>(static_cast<int32_t>(a2[e])) * (1.0 / 64516.0);
-          const double y = scale[j0 + e] * inv * s;
-          yrow[e] = y;
-          if (p.planes) {
-            // y = b0 + b1 + b2 in bf16 (~24 significant bits)
-            const __nv_bfloat16 b0 = __double2bfloat16(y);
-            const double r1 = y - static_cast<double>(__bfloat162float(b0));
-            const __nv_bfloat16 b1 = __double2bfloat16(r1);
-            const double r2 = r1 - static_cast<double>(__bfloat162float(b1));
-            const __nv_bfloat16 b2 = __double2bfloat16(r2);
-            const int64_t base = (static_cast<int64_t>(td.ring) * 3) * p.plane_rows + frame;
-            p.planes[base * p.kp + j0 + e] = b0;
-            p.planes[(base + p.plane_rows) * p.kp + j0 + e] = b1;
-            p.planes[(base + 2 * p.plane_rows) * p.kp + j0 + e] = b2;
+          double y = 0.0;
+          if (live && j0 + e < p.k) {
+            y = combine_digits(static_cast<int32_t>(a0[e]),
+                               p.n_digits > 1 ? static_cast<int32_t>(a1[e]) : 0,
+                               p.n_digits > 2 ? static_cast<int32_t>(a2[e]) : 0, p.n_digits,
+                               scale[j0 + e], inv);
+          }
+          es->y[lane * 17 + e] = y;
+          // y = b0 + b1 + b2 in bf16 (~24 significant bits)
+          const __nv_bfloat16 b0 = __double2bfloat16(y);
+          const double r1 = y - static_cast<double>(__bfloat162float(b0));
+          const __nv_bfloat16 b1 = __double2bfloat16(r1);
+          const double r2 = r1 - static_cast<double>(__bfloat162float(b1));
+          const __nv_bfloat16 b2 = __double2bfloat16(r2);
+          const uint32_t sh = (e & 1) * 16;
+          const uint32_t u0 = __bfloat16_as_ushort(b0), u1 = __bfloat16_as_ushort(b1),
+                         u2 = __bfloat16_as_ushort(b2);
+          if (e & 1) {
+            pk[0][e >> 1] |= u0 << sh;
+            pk[1][e >> 1] |= u1 << sh;
+            pk[2][e >> 1] |= u2 << sh;
+          } else {
+            pk[0][e >> 1] = u0;
+            pk[1][e >> 1] = u1;
+            pk[2][e >> 1] = u2;
           }
         }
+        if (p.planes) {
+#pragma unroll
+          for (int q = 0; q < 3; ++q) {
+            uint4* dst = reinterpret_cast<uint4*>(es->planes[pb][q] + lane * 8);
+            dst[0] = make_uint4(pk[q][0], pk[q][1], pk[q][2], pk[q][3]);
+            dst[1] = make_uint4(pk[q][4], pk[q][5], pk[q][6], pk[q][7]);
+          }
+          fence_proxy_async();
         }
+        __syncwarp();
+        if (p.planes && lane == 0) {
+          const int row0 = static_cast<int>((static_cast<int64_t>(td.ring) * 3) * p.plane_rows) +
+                           td.i0 + 32 * sub;
+#pragma unroll
+          for (int q = 0; q < 3; ++q)
+            asm volatile(
+                "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                    reinterpret_cast<uint64_t>(&tmP)),
+                "r"(smem_u32(es->planes[pb][q])), "r"(j0),
+                "r"(row0 + q * static_cast<int>(p.plane_rows))
+                : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        // coefficients: two frames' 16-value runs per warp store
+        const int c = lane & 15;
+#pragma unroll 4
+        for (int it = 0; it < 16; ++it) {
+          const int r = 2 * it + (lane >> 4);
+          const int64_t f = td.i0 + 32 * sub + r;
+          if (f < p.n_frames && j0 + c < p.k)
+            p.y[(static_cast<int64_t>(td.ring) * p.y_ld + f) * p.k + j0 + c] = es->y[r * 17 + c];
+        }
+        __syncwarp();  // es->y is rewritten by the next chunk
       }
       tc_fence_before();
       __syncwarp();
@@ -210,6 +272,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         acc_phase ^= 1;
       }
     }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   tc_fence_before();
   __syncthreads();
@@ -219,15 +282,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
 }
 
-cudaError_t launch_project(const CUtensorMap& tmX, const CUtensorMap& tmV, const ProjParams& p,
-                           int num_sms, cudaStream_t stream) {
-  const size_t smem = project_smem_bytes();
+cudaError_t launch_project(const CUtensorMap& tmX, const CUtensorMap& tmV, const CUtensorMap& tmP,
+                           const ProjParams& p, int num_sms, cudaStream_t stream) {
+  const size_t smem = project_smem_bytes(p.n_digits * p.kt);
   cudaError_t e =
       cudaFuncSetAttribute(k_project, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const int grid = p.ntiles < num_sms ? p.ntiles : num_sms;
   if (grid <= 0) return cudaSuccess;
-  k_project<<<grid, NUM_THREADS, smem, stream>>>(tmX, tmV, p);
+  k_project<<<grid, NUM_THREADS, smem, stream>>>(tmX, tmV, tmP, p);
   return cudaGetLastError();
 }
 

@@ -125,11 +125,9 @@ __global__ void __launch_bounds__(512) k_stream_project(StreamParams p) {
   const double inv = p.inv[static_cast<int64_t>(r) * p.inv_ld + p.t];
   for (int j = threadIdx.x; j < p.k; j += blockDim.x) {
     // same f64 expression as k_project's epilogue (bitwise-equal coefficients)
-    double s = static_cast<double>(accs[j]);
-    if (p.n_digits > 1) s += static_cast<double>(accs[p.k + j]) * (1.0 / 254.0);
-    if (p.n_digits > 2) s += static_cast<double>(accs[2 * p.k + j]) * (1.0 / 64516.0);
-    p.y[(static_cast<int64_t>(r) * p.y_ld + p.t) * p.k + j] =
-        p.scale[static_cast<int64_t>(r) * p.k + j] * inv * s;
+    p.y[(static_cast<int64_t>(r) * p.y_ld + p.t) * p.k + j] = combine_digits(
+        accs[j], p.n_digits > 1 ? accs[p.k + j] : 0, p.n_digits > 2 ? accs[2 * p.k + j] : 0,
+        p.n_digits, p.scale[static_cast<int64_t>(r) * p.k + j], inv);
   }
 }
 

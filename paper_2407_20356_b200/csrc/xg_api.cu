@@ -171,6 +171,19 @@ void dfree(T*& p) {
 
 int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 
+int make_map_bf16_box(xg_ctx* c, CUtensorMap* map, const void* base, int64_t cols, int64_t rows,
+                      uint32_t box_cols, uint32_t box_rows, CUtensorMapSwizzle swz) {
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols * 2)};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = c->encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                         strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(c, XG_ERR_CUDA, "cuTensorMapEncodeTiled(bf16) failed (%d)", (int)r);
+  return XG_OK;
+}
+
 int make_map_bf16(xg_ctx* c, CUtensorMap* map, const void* base, int64_t cols, int64_t rows) {
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
   cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols * 2)};
@@ -1068,9 +1081,14 @@ int xg_compress(xg_series* s, const xg_basis* Bc, uint32_t flags) {
     s->n_ptiles = static_cast<int32_t>(tiles.size());
     s->ptiles_key = key;
   }
-  CUtensorMap mx, mv;
+  CUtensorMap mx, mv, mp;
   int rc = make_map_u8(c, &mx, s->d_x, L->ktot, s->t, L->ktot, 128, 128);
-  if (!rc) rc = make_map_u8(c, &mv, B->d_vd, L->ktot, B->vrows, L->ktot, 128, 128);
+  // bf16 planes: 16 coefficients x 32 frames boxes, stored by the K3 epilogue
+  if (!rc)
+    rc = make_map_bf16_box(c, &mp, s->d_planes, kp, (int64_t)L->rings * 3 * s->tp, 16, 32,
+                           CU_TENSOR_MAP_SWIZZLE_NONE);
+  // one box = all S*kt digit rows of an N-tile (<= 256)
+  if (!rc) rc = make_map_u8(c, &mv, B->d_vd, L->ktot, B->vrows, L->ktot, 128, B->digits * B->kt);
   if (rc) return rc;
   ProjParams p;
   p.tiles = s->d_ptiles;
@@ -1090,7 +1108,7 @@ int xg_compress(xg_series* s, const xg_basis* Bc, uint32_t flags) {
   p.plane_rows = s->tp;
   p.kp = kp;
   p.err = c->d_err;
-  XG_CUDA(c, launch_project(mx, mv, p, c->num_sms, c->stream));
+  XG_CUDA(c, launch_project(mx, mv, mp, p, c->num_sms, c->stream));
   c->launches++;
   s->have_y = true;
   s->have_cttc = false;

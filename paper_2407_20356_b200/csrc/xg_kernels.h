@@ -148,6 +148,18 @@ cudaError_t launch_gram_u8(const CUtensorMap& tmX, const CUtensorMap& tmOut, con
                            int num_sms, cudaStream_t stream);
 
 // ------------------------------------------------------ K3 projection
+#ifdef __CUDACC__
+// y = scale / |x| * (a0 + a1/254 + a2/254^2) with every rounding explicit, so
+// the batch (K3) and streaming (K5) projections agree bitwise.
+__device__ __forceinline__ double combine_digits(int32_t a0, int32_t a1, int32_t a2, int n_digits,
+                                                 double scale, double inv) {
+  double s = static_cast<double>(a0);
+  if (n_digits > 1) s = __dadd_rn(s, __dmul_rn(static_cast<double>(a1), 1.0 / 254.0));
+  if (n_digits > 2) s = __dadd_rn(s, __dmul_rn(static_cast<double>(a2), 1.0 / 64516.0));
+  return __dmul_rn(__dmul_rn(scale, inv), s);
+}
+#endif
+
 struct ProjParams {
   const TileDesc* tiles;     // (ring, i0 = first frame, j0 = N-tile index)
   int32_t ntiles;
@@ -167,9 +179,9 @@ struct ProjParams {
   int32_t kp;                // plane row length (multiple of 64)
   int* err;
 };
-size_t project_smem_bytes();
-cudaError_t launch_project(const CUtensorMap& tmX, const CUtensorMap& tmV, const ProjParams& p,
-                           int num_sms, cudaStream_t stream);
+size_t project_smem_bytes(int nt_rows);
+cudaError_t launch_project(const CUtensorMap& tmX, const CUtensorMap& tmV, const CUtensorMap& tmP,
+                           const ProjParams& p, int num_sms, cudaStream_t stream);
 
 // ------------------------------------------------------ K5/K6 streaming
 struct StreamParams {

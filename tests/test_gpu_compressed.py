@@ -34,6 +34,9 @@ def _basis(orc, xq, k, seed):
     (300, 64, 64, 4, 0.3, 16, 41),
     (200, 48, 48, 3, 0.5, 32, 42),
     (260, 64, 64, 2, 0.4, 64, 43),
+    (150, 40, 40, 2, 0.4, 10, 44),    # rank not a multiple of 16
+    (130, 48, 48, 2, 0.5, 5, 45),     # odd rank
+    (300, 64, 64, 1, 0.4, 100, 46),   # two N-tiles of coefficients
 ])
 def test_compress_and_ttc_compressed(ctx, orc, t, h, w, q, mu, k, seed):
     frames = orc.gen_speckle(t, h, w, q, mu, seed)

@@ -17,8 +17,9 @@ import paper_2407_20356_b200 as xg
 pytestmark = pytest.mark.gpu
 
 
-def test_stream_raw_and_compressed(ctx, orc):
-    t, h, w, q, k = 150, 48, 48, 3, 16
+@pytest.mark.parametrize("k", [16, 5, 37])
+def test_stream_raw_and_compressed(ctx, orc, k):
+    t, h, w, q = 150, 48, 48, 3
     frames = orc.gen_speckle(t, h, w, q, 0.4, 77)
     ring, _ = orc.ring_map(h, w, q)
     lay = xg.RingLayout.from_ring_map(ctx, ring, q)
