@@ -141,6 +141,8 @@ __global__ void k_g2_fold(G2FoldParams p) {
   const uint32_t* W = p.nz_bits + static_cast<int64_t>(r) * p.nz_words;
   int64_t cnt = 0;
   const int64_t last = p.n_frames - 1 - d;
+  if (p.zero_count[r] == 0) cnt = last + 1;  // no zero-norm frame in this ring
+  else
   for (int i = 0; i < p.nz_words; ++i) {
     const int64_t t0 = 32ll * i;
     if (t0 > last) break;

@@ -789,6 +789,7 @@ static int fold_g2(xg_series* s, double* g2, int64_t* cnt) {
   f.n_rings = s->L->rings;
   f.nz_bits = s->d_nz_bits;
   f.nz_words = s->nz_words;
+  f.zero_count = s->d_zero;
   f.g2 = g2;
   f.counts = cnt;
   f.g2_ld = s->tp;

@@ -137,6 +137,7 @@ struct G2FoldParams {
   int32_t n_rings;
   const uint32_t* nz_bits;   // [ring][nz_words] bit t = frame t has nonzero norm
   int32_t nz_words;
+  const int64_t* zero_count; // [ring] zero-norm frames (0: every count is T - d)
   double* g2;                // [ring][g2_ld]
   int64_t* counts;
   int64_t g2_ld;
