@@ -1,0 +1,37 @@
+"""Regenerate profiles/<round>_summary.txt from the
+ncu reports and launch list committed under profiles/ (run here, no GPU).
+
+    python tools/make_summary.py r1
+"""
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+PROF = os.path.join(ROOT, "profiles")
+
+
+def run(*args):
+    return subprocess.run([sys.executable, *args], capture_output=True, text=True,
+                          cwd=ROOT).stdout
+
+
+def main():
+    rnd = sys.argv[1] if len(sys.argv) > 1 else "r1"
+    lines = [f"# {rnd} launch list: ncu --metrics gpu__time_duration.sum --clock-control none "
+             "(cold, serialised; compare SHARES)",
+             "# command: python bench.py --steps 3 --warmup 3 --no-cpu-baseline",
+             run("tools/launches.py", os.path.join(PROF, f"{rnd}_launches.csv")).rstrip(), ""]
+    for name in ("ingest", "gram_raw", "project", "gram_cmp"):
+        rep = os.path.join(PROF, f"{rnd}_{name}.ncu-rep")
+        if not os.path.exists(rep):
+            continue
+        lines.append(f"# {rnd}_{name}.ncu-rep (ncu --set full --import-source on)")
+        lines.append(run("tools/ncu_summary.py", rep).rstrip())
+        lines.append("")
+    open(os.path.join(PROF, f"{rnd}_summary.txt"), "w").write("\n".join(lines) + "\n")
+    print("\n".join(lines))
+
+
+if __name__ == "__main__":
+    main()
