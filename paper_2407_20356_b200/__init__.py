@@ -83,6 +83,24 @@ def _check(ctx_handle, rc: int) -> None:
     raise _ERRS.get(rc, DeviceError)(msg or f"status {rc}")
 
 
+def _as_counts_u8(frames) -> np.ndarray:
+    """Photon counts as contiguous u8.  Wider integer or float input is
+    accepted when every value is an integer in [0, 255]; anything else raises
+    ContractError instead of wrapping (the u8 path has no counts > 255)."""
+    a = np.asarray(frames)
+    if a.dtype == np.uint8:
+        return np.ascontiguousarray(a)
+    if a.size:
+        if a.dtype.kind == "f" and not np.all(np.isfinite(a)):
+            raise ContractError("frames contain non-finite values")
+        lo, hi = a.min(), a.max()
+        if lo < 0 or hi > 255:
+            raise ContractError(f"frame counts must lie in [0, 255] (got [{lo}, {hi}])")
+        if a.dtype.kind == "f" and not np.array_equal(a, np.rint(a)):
+            raise ContractError("frames must hold integer photon counts")
+    return np.ascontiguousarray(a, dtype=np.uint8)
+
+
 def _ptr(a: np.ndarray) -> C.c_void_p:
     return C.c_void_p(a.ctypes.data)
 
@@ -260,6 +278,8 @@ class FrameSeries:
         """Ingest ``frames`` (n x full_pixels u8): a numpy array (host, copied
         H2D) or any object exposing ``data_ptr()`` (a CUDA torch tensor)."""
         if hasattr(frames, "data_ptr"):  # torch tensor: CUDA (device) or pinned host
+            if str(getattr(frames, "dtype", "torch.uint8")) != "torch.uint8":
+                raise ContractError("frames tensor must be uint8 photon counts")
             n = int(frames.shape[0]) if n_frames is None else n_frames
             if frames.numel() < n * self.layout.full_pixels:
                 raise ShapeError("frames tensor smaller than n x full_pixels")
@@ -267,7 +287,7 @@ class FrameSeries:
             _check(self.ctx.h, lib.xg_series_load_frames(self.h, C.c_void_p(frames.data_ptr()),
                                                          n, on_dev))
             return self
-        a = np.ascontiguousarray(frames, dtype=np.uint8)
+        a = _as_counts_u8(frames)
         if a.ndim != 2 or a.shape[1] != self.layout.full_pixels:
             raise ShapeError(f"frames must be n x {self.layout.full_pixels}, got {a.shape}")
         _check(self.ctx.h, lib.xg_series_load_frames(self.h, _ptr(a), a.shape[0], 0))
@@ -383,10 +403,12 @@ class FrameStream:
 
     def push(self, frame) -> None:
         if hasattr(frame, "data_ptr"):
+            if str(getattr(frame, "dtype", "torch.uint8")) != "torch.uint8":
+                raise ContractError("frame tensor must be uint8 photon counts")
             _check(self.ctx.h, lib.xg_stream_push(self.h, C.c_void_p(frame.data_ptr()),
                                                   1 if getattr(frame, "is_cuda", False) else 0))
             return
-        a = np.ascontiguousarray(frame, dtype=np.uint8).ravel()
+        a = _as_counts_u8(frame).ravel()
         if a.size != self.layout.full_pixels:
             raise ShapeError(f"frame must have {self.layout.full_pixels} pixels, got {a.size}")
         _check(self.ctx.h, lib.xg_stream_push(self.h, _ptr(a), 0))

@@ -77,3 +77,16 @@ def test_shard_rings_lpt():
     sh = dist.shard_rings(dist.ring_costs(m, 16384), 8)
     loads = [m[s].sum() for s in sh]
     assert max(loads) / (m.sum() / 8) < 1.05
+
+
+def test_frame_counts_are_validated_not_wrapped():
+    """Counts above 255 (u16 detectors) or non-integer values raise
+    ContractError instead of silently wrapping into the u8 path."""
+    from paper_2407_20356_b200 import ContractError, _as_counts_u8
+    ok = _as_counts_u8(np.array([[0, 3, 255]], dtype=np.uint16))
+    assert ok.dtype == np.uint8 and ok.tolist() == [[0, 3, 255]]
+    assert _as_counts_u8(np.array([[1.0, 2.0]])).tolist() == [[1, 2]]
+    for bad in (np.array([[0, 256]], dtype=np.uint16), np.array([[-1, 2]]),
+                np.array([[0.5, 1.0]]), np.array([[np.nan, 1.0]])):
+        with pytest.raises(ContractError):
+            _as_counts_u8(bad)
