@@ -120,7 +120,7 @@ __global__ void k_g2_fold(G2FoldParams p) {
   const int64_t d = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int r = blockIdx.y;
   if (d >= p.n_frames) return;
-  const double* part = p.g2_partial + static_cast<int64_t>(r) * p.tiles_per_ring * 384;
+  const float2* part = p.g2_partial + static_cast<int64_t>(r) * p.tiles_per_ring * 384;
   double acc = 0.0;
   // delta range: ceil((d-255)/128) .. floor((d+127)/128)
   const int64_t dlo = (d - 255 >= 0) ? (d - 255 + 127) / 128 : -((255 - d) / 128);
@@ -134,7 +134,8 @@ __global__ void k_g2_fold(G2FoldParams p) {
       if (jb < ib / 2) continue;
       if (jb >= p.nbj) break;
       const int64_t tile = p.ib_tile_off[ib] + (jb - ib / 2);
-      acc += part[tile * 384 + dl];
+      const float2 v = part[tile * 384 + dl];
+      acc += static_cast<double>(v.x) + static_cast<double>(v.y);
     }
   }
   // valid pairs: sum_t nz(t) nz(t+d), t <= T-1-d

@@ -294,9 +294,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       if (p.g2_partial) {
         epi_bar();
         if (ok) {
-          double* out = p.g2_partial + static_cast<int64_t>(t) * NDIAG_PAD;
-          for (int e = etid; e < NDIAG; e += 128)
-            out[e] = ((tail->acc[0][e] + tail->acc[1][e]) + tail->acc[2][e]) + tail->acc[3][e];
+          float2* out = p.g2_partial + static_cast<int64_t>(t) * NDIAG_PAD;
+          for (int e = etid; e < NDIAG; e += 128) {
+            const double v = ((tail->acc[0][e] + tail->acc[1][e]) + tail->acc[2][e]) + tail->acc[3][e];
+            const float hi = static_cast<float>(v);
+            out[e] = make_float2(hi, static_cast<float>(v - static_cast<double>(hi)));
+          }
         }
       }
       if (++acc == 2) {

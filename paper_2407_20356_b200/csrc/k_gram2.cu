@@ -67,7 +67,7 @@ struct __align__(1024) Tail2 {
   double inv_col_ext[BN + 64];
   float2 inv_row2[BM];            // (hi, lo) float split of the same weights
   float2 inv_col2_ext[BN + 64];
-  double acc[EPI_WARPS][NDIAG_PAD];
+  float2 acc[EPI_WARPS][NDIAG_PAD];  // per-diagonal (hi, lo) double-float sums
 };
 
 __device__ __forceinline__ uint32_t cta_rank() {
@@ -86,6 +86,17 @@ __device__ __forceinline__ double f32_to_f64_bits(uint32_t w) {
   if (e == 0u) return 0.0;
   const uint32_t hi = (w & 0x80000000u) | ((e + 896u) << 20) | ((w >> 3) & 0xFFFFFu);
   return __hiloint2double(static_cast<int>(hi), static_cast<int>(w << 29));
+}
+
+// (a.x + a.y) + (bh + bl) in FP32 double-float (~48 bits): TwoSum of the high
+// parts, low parts added into the error, renormalised.
+__device__ __forceinline__ float2 dd_add(float2 a, float bh, float bl) {
+  const float s = __fadd_rn(a.x, bh);
+  const float bb = __fsub_rn(s, a.x);
+  float e = __fadd_rn(__fsub_rn(a.x, __fsub_rn(s, bb)), __fsub_rn(bh, bb));
+  e = __fadd_rn(e, __fadd_rn(a.y, bl));
+  const float hi = __fadd_rn(s, e);
+  return make_float2(hi, __fsub_rn(e, __fsub_rn(hi, s)));
 }
 
 template <int EPI_WARPS>
@@ -141,6 +152,9 @@ constexpr size_t smem2_bytes() {
 }
 size_t gram2_smem_bytes(int mode) { return mode == 0 ? smem2_bytes<0>() : smem2_bytes<1>(); }
 
+#ifndef XG_G2EXP
+#define XG_G2EXP 0
+#endif
 template <int MODE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THREADS, 1)
     k_gram2(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmOut,
@@ -276,8 +290,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
       if (p.g2_partial) {
         epi_bar<EPI_WARPS>();
         const double* inv = MODE == 0 ? p.inv + static_cast<int64_t>(td.ring) * p.inv_ld : nullptr;
+        const float2* inv2 = MODE == 0 ? p.inv2 + static_cast<int64_t>(td.ring) * p.inv_ld : nullptr;
         // inv_col_ext[32 + j] = 1/|x_{j0+j}| for j in [0, 256), zero for the 32
-        // columns either side (the windows reach one chunk past the tile)
+        // columns either side (the windows reach one chunk past the tile).
+        // The double-float path takes the precomputed (hi, lo) split: no FP64
+        // here (FP64 work in this kernel stalls the tensor-core pipeline).
+        if (MODE == 1 || dd_ok) {
+          for (int e = etid; e < BM + BN + 64; e += 32 * EPI_WARPS) {
+            const int j = e - BM - 32;
+            const int idx = e < BM ? i0 + e : td.j0 + j;
+            const bool in = idx < p.n_frames && (e < BM || (j >= 0 && j < BN));
+            const float2 hl = in ? (MODE == 0 ? inv2[idx] : make_float2(1.f, 0.f))
+                                 : make_float2(0.f, 0.f);
+            if (e < BM)
+              tail->inv_row2[e] = hl;
+            else
+              tail->inv_col2_ext[e - BM] = hl;
+          }
+        } else
         for (int e = etid; e < BM + BN + 64; e += 32 * EPI_WARPS) {
           double v;
           if (e < BM) {
@@ -297,7 +327,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
           else
             tail->inv_col2_ext[e - BM] = hl;
         }
-        for (int e = lane; e < NDIAG_PAD; e += 32) tail->acc[ew][e] = 0.0;
+        for (int e = lane; e < NDIAG_PAD; e += 32) tail->acc[ew][e] = make_float2(0.f, 0.f);
         epi_bar<EPI_WARPS>();
       }
       const uint32_t tbase =
@@ -339,11 +369,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
           }
         }
         const int w = c;  // window of chunks c-1, c
-        if (p.g2_partial && !(EPI_WARPS == 8 && grp == 1 && w == 4)) {
+        if (XG_G2EXP != 2 && p.g2_partial && !(EPI_WARPS == 8 && grp == 1 && w == 4)) {
           const int lagw = td.j0 - i0 + 32 * (w - 1 - sub) + lane + 1;  // this lane's lag
           if (lagw >= 0) {
             const uint32_t* Sp = S + ((c - 1) & 1) * 1024;
-            double wsum;
+            float wh, wl;  // this window's diagonal sum as (hi, lo)
             if (MODE == 1 || dd_ok) {
               // FP32 double-float (~48 bits): exact float G (< 2^23), error-free
               // two-product of the (hi, lo) weights, TwoSum accumulation; the
@@ -362,7 +392,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
                 if (MODE == 0) {
                   const float g = __fsub_rn(__int_as_float(0x4B000000 | static_cast<int>(wv)),
                                             8388608.f);  // exact for wv < 2^23
-                  const float2 a = ir2[l], b = ic2[l];
+                  const float2 a = ir2[l], b = XG_G2EXP == 1 ? make_float2(1.f, 0.f) : ic2[l];
                   const float ph = __fmul_rn(a.x, b.x);
                   float pe = __fmaf_rn(a.x, b.x, -ph);
                   pe = __fmaf_rn(a.x, b.y, pe);
@@ -381,7 +411,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
                 sh = t;
                 sl = __fadd_rn(sl, __fadd_rn(er, ql));
               }
-              wsum = static_cast<double>(sh) + static_cast<double>(sl);
+              wh = sh;
+              wl = sl;
             } else {
               // FP64 path (a frame with |x|^2 >= 2^23 in this series)
               const double* ir = tail->inv_row + 32 * sub;
@@ -399,9 +430,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
                     (ir[l] * ic[l]);
                 if (l & 1) r1 += v; else r0 += v;
               }
-              wsum = r0 + r1;
+              const double ws = r0 + r1;
+              wh = static_cast<float>(ws);
+              wl = static_cast<float>(ws - static_cast<double>(wh));
             }
-            tail->acc[ew][32 * (w - 1 - sub) + lane + 1 + 127] += wsum;
+            // double-float accumulation: the FP64 pipe stalls the tensor-core
+            // pipeline on this part, FP32 does not
+            float2* ap = &tail->acc[ew][32 * (w - 1 - sub) + lane + 1 + 127];
+            *ap = dd_add(*ap, wh, wl);
           }
           __syncwarp();
         }
@@ -422,11 +458,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
         // second half past the last 128-row block holds only rows >= T
         if (ok && 2 * (td.i0 / 256) + static_cast<int>(rank) < p.g2_nbi) {
           const int64_t half = td.pad + static_cast<int64_t>(rank) * (p.g2_nbj - td.i0 / 256);
-          double* out = p.g2_partial + half * NDIAG_PAD;
+          float2* out = p.g2_partial + half * NDIAG_PAD;
           for (int e = etid; e < NDIAG; e += 32 * EPI_WARPS) {
-            double sum = tail->acc[0][e];  // fixed warp order
+            float2 sum = tail->acc[0][e];  // fixed warp order
 #pragma unroll
-            for (int w = 1; w < EPI_WARPS; ++w) sum += tail->acc[w][e];
+            for (int w = 1; w < EPI_WARPS; ++w) sum = dd_add(sum, tail->acc[w][e].x, tail->acc[w][e].y);
             out[e] = sum;
           }
         }

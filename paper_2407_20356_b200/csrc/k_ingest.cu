@@ -269,7 +269,12 @@ __global__ void k_norms(NormParams p) {
   if (valid) {
     const double nrm = sqrt(static_cast<double>(n2));
     p.norms[r * p.ld + t] = nrm;
-    p.inv[r * p.ld + t] = n2 > 0 ? 1.0 / nrm : 0.0;
+    const double iv = n2 > 0 ? 1.0 / nrm : 0.0;
+    p.inv[r * p.ld + t] = iv;
+    if (p.inv2) {
+      const float hi = static_cast<float>(iv);
+      p.inv2[r * p.ld + t] = make_float2(hi, static_cast<float>(iv - static_cast<double>(hi)));
+    }
   }
   // warp-aggregated bookkeeping: one atomic per warp, not per frame
   const uint32_t nz = __ballot_sync(0xffffffffu, valid && n2 > 0);

@@ -80,6 +80,7 @@ struct xg_series {
   int64_t* d_norm2 = nullptr;
   double* d_norms = nullptr;
   double* d_inv = nullptr;
+  float2* d_inv2 = nullptr;        // (hi, lo) split of d_inv for the FP32 g2
   int64_t* d_zero = nullptr;
   int64_t* d_first_zero = nullptr;
   int64_t* d_max_norm2 = nullptr;  // max |x_t|^2 over all frames and rings
@@ -90,7 +91,7 @@ struct xg_series {
   int64_t* d_g2pcnt = nullptr;
   uint32_t* d_nz_bits = nullptr;   // [ring][nz_words] nonzero-frame bitmask
   int32_t nz_words = 0;
-  double* d_g2tile = nullptr;      // [ntiles][384] fused-g2 tile diagonal sums
+  float2* d_g2tile = nullptr;      // [ntiles][384] fused-g2 tile diagonal sums (hi, lo)
   int32_t* d_ib_tile_off = nullptr;
   int32_t tiles_per_ring = 0;
   TileDesc* d_tiles = nullptr;
@@ -551,6 +552,7 @@ int xg_series_create(xg_ctx* c, const xg_layout* L, int64_t max_frames, xg_serie
       (e = dalloc(&s->d_norm2, (size_t)max_frames * Q)) != cudaSuccess ||
       (e = dalloc(&s->d_norms, (size_t)s->tp * Q)) != cudaSuccess ||
       (e = dalloc(&s->d_inv, (size_t)s->tp * Q)) != cudaSuccess ||
+      (e = dalloc(&s->d_inv2, (size_t)s->tp * Q)) != cudaSuccess ||
       (e = dalloc(&s->d_zero, (size_t)Q)) != cudaSuccess ||
       (e = dalloc(&s->d_first_zero, (size_t)Q)) != cudaSuccess ||
       (e = dalloc(&s->d_max_norm2, (size_t)1)) != cudaSuccess ||
@@ -581,6 +583,7 @@ void xg_series_destroy(xg_series* s) {
   dfree(s->d_norm2);
   dfree(s->d_norms);
   dfree(s->d_inv);
+  dfree(s->d_inv2);
   dfree(s->d_zero);
   dfree(s->d_first_zero);
   dfree(s->d_max_norm2);
@@ -656,6 +659,7 @@ int xg_series_load_frames(xg_series* s, const uint8_t* frames, int64_t n, int on
   np.n_rings = L->rings;
   np.norms = s->d_norms;
   np.inv = s->d_inv;
+  np.inv2 = s->d_inv2;
   np.zero_count = s->d_zero;
   np.first_zero = s->d_first_zero;
   s->nz_words = static_cast<int32_t>((n + 31) / 32);
@@ -834,6 +838,7 @@ int xg_ttc_raw(xg_series* s, uint32_t flags) {
   gp.max_norm2 = reinterpret_cast<const unsigned long long*>(s->d_max_norm2);
   const bool g2 = !(flags & XG_NO_G2);
   gp.inv = s->d_inv;
+  gp.inv2 = s->d_inv2;
   gp.inv_ld = s->tp;
   gp.n_frames = s->t;
   gp.g2_partial = g2 ? s->d_g2tile : nullptr;
@@ -1144,6 +1149,7 @@ int xg_ttc_compressed(xg_series* s, uint32_t flags) {
   gp.max_norm2 = reinterpret_cast<const unsigned long long*>(s->d_max_norm2);
   const bool g2 = !(flags & XG_NO_G2);
   gp.inv = s->d_inv;
+  gp.inv2 = s->d_inv2;
   gp.inv_ld = s->tp;
   gp.n_frames = s->t;
   gp.g2_partial = g2 ? s->d_g2tile : nullptr;
@@ -1400,6 +1406,7 @@ int xg_stream_push(xg_stream* s, const uint8_t* frame, int on_device) {
   np.n_rings = L->rings;
   np.norms = s->d_norms;
   np.inv = s->d_inv;
+  np.inv2 = nullptr;
   np.zero_count = s->d_zero;
   np.first_zero = s->d_first_zero;
   np.nz_bits = s->d_nz_bits;

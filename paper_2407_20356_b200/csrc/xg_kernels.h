@@ -72,6 +72,7 @@ struct NormParams {
   int32_t n_rings;
   double* norms;             // [ring][ld]
   double* inv;               // [ring][ld]
+  float2* inv2;              // [ring][ld] (hi, lo) float split of inv (or null)
   int64_t* zero_count;       // [ring]
   int64_t* first_zero;       // [ring] smallest zero-norm frame (sentinel if none)
   uint32_t* nz_bits;         // [ring][nz_words] nonzero-frame bitmask (pre-zeroed)
@@ -100,9 +101,10 @@ struct GramParams {
   // fused g2 (null g2_partial = off): per tile, the sums over each tile
   // diagonal (j - i + 127 in [0, 383)) of C(i,j) = G_ij inv_i inv_j, j >= i
   const double* inv;         // [ring][inv_ld]
+  const float2* inv2;        // [ring][inv_ld] (hi, lo) float split of inv
   int64_t inv_ld;
   int64_t n_frames;
-  double* g2_partial;        // [ntiles][384]
+  float2* g2_partial;        // [ntiles][384] (hi, lo) double-float diagonal sums
   // compressed mode (launch_gram_cmp): K blocks run over precision pairs
   // (plane_a, plane_b) packed 4 bits each in `pairs`, kb_per_plane 64-element
   // blocks per plane; plane rows of ring r, plane s start at (3r+s)*plane_rows
@@ -129,7 +131,7 @@ cudaError_t launch_gram_cmp(const CUtensorMap& tmY, const CUtensorMap& tmOut, co
 // Fold the per-tile diagonal sums of K2 into g2[ring][d] (fixed order) and
 // count the valid (t, t+d) pairs from the nonzero-frame bitmask.
 struct G2FoldParams {
-  const double* g2_partial;  // [ntiles][384]
+  const float2* g2_partial;  // [ntiles][384] (hi, lo)
   const int32_t* ib_tile_off;  // [nbi+1] tile offset of tile row ib within a ring
   int32_t tiles_per_ring;
   int32_t nbi, nbj;
