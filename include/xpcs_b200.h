@@ -136,6 +136,10 @@ XG_API int64_t xg_series_frames(const xg_series* s);
  * the zero frame in *rank_out. */
 XG_API int xg_build_basis(const double* x, int64_t n, int64_t m, int32_t k, double* v_out,
                           double* sigma_out, int64_t* rank_out);
+/* content_hash_u64 (model.cpp:99-114): 64-bit FNV-1a over "XENC", the mode
+ * byte (0 offline, 1 online-related, 2 online-unrelated), n_pixels, k and the
+ * f64 bits of V (m x k row-major), little-endian.  The store binding id. */
+XG_API uint64_t xg_content_hash(const double* v, int64_t m, int64_t k, int32_t mode);
 XG_API int xg_build_basis_batch(int32_t n_rings, const double* const* x_ring, int64_t n,
                                 const int64_t* m_ring, int32_t k, double* const* v_ring,
                                 int32_t threads, int64_t* rank_out);

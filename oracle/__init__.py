@@ -242,6 +242,7 @@ class _RefOracle:
         L.ref_build_online_from_frames.argtypes = [_d, I64, I64, I64, _d, _d, _i64]
         L.ref_build_offline.argtypes = [_d, I64, I64, _d, _i64]
         L.ref_apply_mask.argtypes = [_d, I64, I64, _i64, I64, _d]
+        L.ref_content_hash.argtypes = [_d, I64, I64, C_.c_int, C_.POINTER(U64)]
         L.ref_rng_bits.restype = U64
         L.ref_rng_bits.argtypes = [U64, U64, U64]
         L.ref_rng_normal.restype = C_.c_double
@@ -293,6 +294,12 @@ class _RefOracle:
         self._chk(self.L.ref_g2_from_ttc(_p(g, _d), n, period, _p(lags, _d), _p(vals, _d),
                                          _p(counts, _i64)))
         return lags, vals, counts
+
+    def content_hash(self, v, mode):
+        v = _f64(v)
+        out = U64(0)
+        self._chk(self.L.ref_content_hash(_p(v, _d), v.shape[0], v.shape[1], mode, C_.byref(out)))
+        return int(out.value)
 
     def ttc_rel_error(self, a, b):
         a, b = _f64(a), _f64(b)

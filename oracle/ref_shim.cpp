@@ -140,6 +140,14 @@ int ref_g2_from_ttc(const double* g, int64_t n, double period, double* lags, dou
   });
 }
 
+// content_hash_u64 (model.cpp:99-114) of an encoder with this V and mode.
+int ref_content_hash(const double* v, int64_t m, int64_t k, int mode, uint64_t* out) {
+  return guarded([&] {
+    EncodingMatrix e(to_matrix(v, m, k), std::vector<double>(k, 1.0), static_cast<EncoderMode>(mode));
+    *out = content_hash_u64(e);
+  });
+}
+
 int ref_ttc_rel_error(const double* a, const double* b, int64_t n, double* out) {
   return guarded([&] { *out = ttc_rel_error(to_matrix(a, n, n), to_matrix(b, n, n)); });
 }

@@ -484,7 +484,8 @@ def ttc_extend(g, y, row):
     if y.shape[0] != n:
         raise ShapeError(f"ttc_extend: TTC covers {n} frames but store holds {y.shape[0]}")
     if row.size != y.shape[1]:
-        raise ShapeError("ttc_extend: new row length does not match the store's k")
+        raise ShapeError(f"ttc_extend: new row has {row.size} coefficients, store holds "
+                         f"k = {y.shape[1]}")
     out = np.empty((n + 1, n + 1))
     ll = C.c_int(0)
     _f64check(lib.xg_f64_ttc_extend(g.ctypes.data_as(_abi.PD), n, y.ctypes.data_as(_abi.PD),

@@ -53,6 +53,7 @@ _sigs = {
     "xg_synth_speckle": (C.c_int, [P, I64, I64, I64, I32, C.c_double, I32, C.c_double,
                                    C.c_uint64, P]),
     "xg_build_basis": (C.c_int, [PD, I64, I64, I32, PD, PD, PI64]),
+    "xg_content_hash": (C.c_uint64, [PD, I64, I64, I32]),
     "xg_build_basis_batch": (C.c_int, [I32, C.POINTER(PD), I64, PI64, I32, C.POINTER(PD), I32,
                                        PI64]),
     "xg_stream_create": (C.c_int, [P, P, P, I64, U32, C.POINTER(P)]),

@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstring>
 #include <numeric>
 #include <thread>
 #include <vector>
@@ -171,6 +172,32 @@ Svd gram_svd(const double* x, int64_t n, int64_t m, double rel_tol) {
 }  // namespace
 
 extern "C" {
+
+XG_API uint64_t xg_content_hash(const double* v, int64_t m, int64_t k, int32_t mode) {
+  uint64_t h = 0xCBF29CE484222325ULL;
+  auto feed = [&](const unsigned char* p, size_t n) {
+    for (size_t i = 0; i < n; ++i) {
+      h ^= p[i];
+      h *= 0x100000001B3ULL;
+    }
+  };
+  auto feed_u64 = [&](uint64_t x) {
+    unsigned char b[8];
+    for (int i = 0; i < 8; ++i) b[i] = static_cast<unsigned char>(x >> (8 * i));
+    feed(b, 8);
+  };
+  feed(reinterpret_cast<const unsigned char*>("XENC"), 4);
+  const unsigned char md = static_cast<unsigned char>(mode);
+  feed(&md, 1);
+  feed_u64(static_cast<uint64_t>(m));
+  feed_u64(static_cast<uint64_t>(k));
+  for (int64_t i = 0; i < m * k; ++i) {
+    uint64_t bits;
+    std::memcpy(&bits, v + i, 8);
+    feed_u64(bits);
+  }
+  return h;
+}
 
 // build_online_from_frames (encoder.cpp:53-60) / build_offline (k = 0: full
 // numerical rank) for one ring: training frames x (n x m, f64, mask order).

@@ -90,3 +90,43 @@ def test_frame_counts_are_validated_not_wrapped():
                 np.array([[0.5, 1.0]]), np.array([[np.nan, 1.0]])):
         with pytest.raises(ContractError):
             _as_counts_u8(bad)
+
+
+def test_content_hash_matches_reference(ref):
+    """xg_content_hash == the reference's content_hash_u64 (model.cpp:99-114),
+    which binds a compressed store to its encoder."""
+    import paper_2407_20356_b200.xpcsvd as xv
+    rng = np.random.default_rng(4)
+    for m, k, mode in ((40, 3, 0), (17, 5, 1), (64, 1, 2)):
+        v, _ = np.linalg.qr(rng.standard_normal((m, k)))
+        enc = xv.EncodingMatrix(v, np.linspace(2.0, 1.0, k), mode)
+        assert int(xv.content_hash(enc), 16) == ref.content_hash(v, mode)
+
+
+def test_pyapi_host_contracts():
+    """The xpcsvd-shaped module's host-side validation follows model.cpp."""
+    import paper_2407_20356_b200.xpcsvd as xv
+    with pytest.raises(xv.MaskError):
+        xv.PixelMask(8, [])
+    with pytest.raises(xv.MaskError):
+        xv.PixelMask(8, [3, 3])
+    with pytest.raises(xv.ContractError):
+        xv.FrameSeries(np.ones((3, 4)), 0.0)
+    with pytest.raises(xv.ContractError):
+        xv.FrameSeries(-np.ones((3, 4)), 1.0)
+    f = xv.FrameSeries(np.arange(12.0).reshape(3, 4), 1.0)
+    m = xv.apply_mask(f, xv.PixelMask(4, [1, 3]))
+    assert m.n_pixels == 2 and np.array_equal(m.intensities, f.intensities[:, [1, 3]])
+    with pytest.raises(xv.MaskError):
+        xv.apply_mask(m, xv.PixelMask(2, [0]))
+    s = xv.CompressedSeries(2, 7)
+    with pytest.raises(xv.ShapeError):
+        s.append([0.1, 0.2, 0.3], 1.0)
+    with pytest.raises(xv.ContractError):
+        s.append([0.9, 0.9], 1.0)
+    s.append([0.6, 0.8], 2.0)
+    assert s.n_frames == 1 and s.encoder_id == 7
+    with pytest.raises(xv.ContractError):
+        xv.TTCMatrix(np.array([[1.0, 0.5], [0.4, 1.0]]), True)
+    with pytest.raises(xv.ContractError):
+        xv.TTCMatrix(np.array([[0.9, 0.5], [0.5, 1.0]]), True)
