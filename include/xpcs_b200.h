@@ -164,6 +164,8 @@ XG_API int xg_series_get_cg2(xg_series* s, int32_t ring, double* values, int64_t
  * are accumulated per lag as frames arrive.  Single writer. */
 #define XG_STREAM_STORE_TTC 0x1u  /* keep every column (Q x T x T) for readback */
 #define XG_STREAM_NO_RAW 0x2u     /* compressed only */
+#define XG_STREAM_SPARSE 0x4u     /* raw columns from the new frame's nonzeros (pixel-major
+                                     history): nnz*t bytes per frame instead of M*t */
 XG_API int xg_stream_create(xg_ctx* ctx, const xg_layout* layout, const xg_basis* basis,
                             int64_t max_frames, uint32_t flags, xg_stream** out);
 XG_API void xg_stream_destroy(xg_stream* s);

@@ -383,10 +383,15 @@ class FrameStream:
     compress_frame -> ttc_extend -> append loop (acceptance_main.cpp:329-353)."""
 
     def __init__(self, layout: RingLayout, max_frames: int, basis: "Basis | None" = None,
-                 store_ttc: bool = False, raw: bool = True, frame_period: float = 1.0):
+                 store_ttc: bool = False, raw: bool = True, frame_period: float = 1.0,
+                 sparse: bool = False):
+        """``sparse``: raw columns from the new frame's nonzero pixels over a
+        pixel-major history (nnz * t bytes per frame instead of M * t; same
+        results bitwise) -- the photon-event mode for low count rates."""
         self.layout, self.ctx, self.basis = layout, layout.ctx, basis
         self.frame_period = float(frame_period)
-        flags = (_abi.STREAM_STORE_TTC if store_ttc else 0) | (0 if raw else _abi.STREAM_NO_RAW)
+        flags = ((_abi.STREAM_STORE_TTC if store_ttc else 0) | (0 if raw else _abi.STREAM_NO_RAW)
+                 | (_abi.STREAM_SPARSE if sparse else 0))
         h = C.c_void_p()
         _check(self.ctx.h, lib.xg_stream_create(self.ctx.h, layout.h, basis.h if basis else None,
                                                 int(max_frames), flags, C.byref(h)))

@@ -113,3 +113,4 @@ NO_G2 = 0x2
 CMP_BF16 = 0x4
 STREAM_STORE_TTC = 0x1
 STREAM_NO_RAW = 0x2
+STREAM_SPARSE = 0x4

@@ -160,6 +160,99 @@ __global__ void __launch_bounds__(SR_THREADS) k_stream_cmp(StreamParams p) {
 
 }  // namespace
 
+// K5s-a: one CTA per ring.  The new frame's nonzero ring columns (any order:
+// the column sums below are integer, so order-free) and their scatter into
+// the pixel-major history.
+__global__ void __launch_bounds__(512) k_stream_sparse_gather(StreamParams p) {
+  __shared__ int cnt;
+  const int r = blockIdx.x;
+  const int koff = p.ring_koff[r];
+  const int n = p.ring_nkb[r] * 128;
+  const uint8_t* row = p.x + p.t * p.ktot + koff;
+  if (threadIdx.x == 0) cnt = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  for (int i0 = 0; i0 < n; i0 += 4 * blockDim.x) {
+    const int i = i0 + 4 * threadIdx.x;
+    const uint32_t w = i < n ? *reinterpret_cast<const uint32_t*>(row + i) : 0u;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t v = (w >> (8 * j)) & 0xFFu;
+      const uint32_t m = __ballot_sync(0xffffffffu, v != 0u);
+      int base = 0;
+      if (lane == 0 && m) base = atomicAdd(&cnt, __popc(m));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (v) {
+        const int pos = base + __popc(m & ((1u << lane) - 1u));
+        const int c = koff + i + j;
+        p.nz_col[koff + pos] = c;
+        p.nz_val[koff + pos] = static_cast<uint8_t>(v);
+        p.hist[static_cast<int64_t>(c) * p.hp + p.t] = static_cast<uint8_t>(v);
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) p.nz_n[r] = cnt;
+}
+
+// K5s-b: grid (ceil((t+1)/1024), rings); a thread owns 4 consecutive history
+// frames s and walks the ring's nonzeros: one coalesced 32-bit load of
+// hist[c][s..s+3] per nonzero.  Same C, g2 and column outputs as K5.
+constexpr int SS_THREADS = 256;
+constexpr int SS_CHUNK = 1024;
+__global__ void __launch_bounds__(SS_THREADS) k_stream_sparse_col(StreamParams p) {
+  __shared__ int32_t sc[SS_CHUNK];
+  __shared__ uint32_t sv[SS_CHUNK];
+  const int r = blockIdx.y;
+  const int koff = p.ring_koff[r];
+  const int n = p.nz_n[r];
+  const int64_t s0 = static_cast<int64_t>(blockIdx.x) * (4 * SS_THREADS) + 4 * threadIdx.x;
+  uint32_t acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0;
+  for (int c0 = 0; c0 < n; c0 += SS_CHUNK) {
+    const int cn = n - c0 < SS_CHUNK ? n - c0 : SS_CHUNK;
+    __syncthreads();
+    for (int i = threadIdx.x; i < cn; i += SS_THREADS) {
+      sc[i] = p.nz_col[koff + c0 + i];
+      sv[i] = p.nz_val[koff + c0 + i];
+    }
+    __syncthreads();
+    if (s0 <= p.t) {
+      const uint8_t* h = p.hist + s0;
+#pragma unroll 4
+      for (int i = 0; i < cn; ++i) {
+        const uint32_t w = __ldcs(reinterpret_cast<const uint32_t*>(h + static_cast<int64_t>(sc[i]) * p.hp));
+        const uint32_t v = sv[i];
+        acc0 += v * (w & 0xFFu);
+        acc1 += v * ((w >> 8) & 0xFFu);
+        acc2 += v * ((w >> 16) & 0xFFu);
+        acc3 += v * (w >> 24);
+      }
+    }
+  }
+  const double inv_t = p.inv[static_cast<int64_t>(r) * p.inv_ld + p.t];
+  const uint32_t acc[4] = {acc0, acc1, acc2, acc3};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int64_t s = s0 + j;
+    if (s > p.t) break;
+    const double inv_s = p.inv[static_cast<int64_t>(r) * p.inv_ld + s];
+    const int64_t gi = static_cast<int64_t>(r) * p.g2_ld + (p.t - s);
+    p.g2sum[gi] += static_cast<double>(static_cast<int>(acc[j])) * (inv_s * inv_t);
+    p.g2cnt[gi] += (inv_s != 0.0 && inv_t != 0.0) ? 1 : 0;
+    if (p.gcol) p.gcol[static_cast<int64_t>(r) * p.col_ring_stride + s * p.col_ld + p.t] =
+        static_cast<int>(acc[j]);
+  }
+}
+
+cudaError_t launch_stream_sparse(const StreamParams& p, int32_t n_rings, cudaStream_t s) {
+  k_stream_sparse_gather<<<n_rings, 512, 0, s>>>(p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  dim3 grid(static_cast<unsigned>((p.t + 1 + 4 * SS_THREADS - 1) / (4 * SS_THREADS)), n_rings);
+  k_stream_sparse_col<<<grid, SS_THREADS, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_stream_raw(const StreamParams& p, int32_t n_rings, int64_t max_kpad,
                               cudaStream_t s) {
   const size_t smem = static_cast<size_t>(max_kpad);

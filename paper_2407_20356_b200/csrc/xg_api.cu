@@ -1264,6 +1264,11 @@ struct xg_stream {
   int8_t* d_vdt = nullptr;
   int32_t vdt_ld = 0;
   double* d_y = nullptr;
+  uint8_t* d_hist = nullptr;  // sparse mode: pixel-major history [ktot][hp]
+  int64_t hp = 0;
+  int32_t* d_nz_col = nullptr;
+  uint8_t* d_nz_val = nullptr;
+  int32_t* d_nz_n = nullptr;
 };
 
 extern "C" {
@@ -1305,6 +1310,17 @@ int xg_stream_create(xg_ctx* c, const xg_layout* L, const xg_basis* B, int64_t m
       (store && B && (e = dalloc(&s->d_ccol, (size_t)Q * s->tp * s->tp)) != cudaSuccess)) {
     xg_stream_destroy(s);
     return cuda_fail(c, e, "stream alloc");
+  }
+  if (flags & XG_STREAM_SPARSE) {
+    s->hp = round_up(max_frames, 16);
+    if ((e = dalloc(&s->d_hist, (size_t)L->ktot * s->hp)) != cudaSuccess ||
+        (e = dalloc(&s->d_nz_col, (size_t)L->ktot)) != cudaSuccess ||
+        (e = dalloc(&s->d_nz_val, (size_t)L->ktot)) != cudaSuccess ||
+        (e = dalloc(&s->d_nz_n, (size_t)Q)) != cudaSuccess) {
+      xg_stream_destroy(s);
+      return cuda_fail(c, e, "stream sparse history alloc");
+    }
+    cudaMemsetAsync(s->d_hist, 0, (size_t)L->ktot * s->hp, c->stream);
   }
   cudaMemsetAsync(s->d_x, 0, (size_t)max_frames * L->ktot, c->stream);
   cudaMemsetAsync(s->d_zero, 0, (size_t)Q * 8, c->stream);
@@ -1362,6 +1378,10 @@ void xg_stream_destroy(xg_stream* s) {
   dfree(s->d_ccol);
   dfree(s->d_vdt);
   dfree(s->d_y);
+  dfree(s->d_hist);
+  dfree(s->d_nz_col);
+  dfree(s->d_nz_val);
+  dfree(s->d_nz_n);
   delete s;
 }
 
@@ -1439,9 +1459,19 @@ int xg_stream_push(xg_stream* s, const uint8_t* frame, int on_device) {
   sp.scale = s->B ? s->B->d_scale : nullptr;
   sp.y = s->d_y;
   sp.y_ld = s->tp;
+  sp.hist = s->d_hist;
+  sp.hp = s->hp;
+  sp.nz_col = s->d_nz_col;
+  sp.nz_val = s->d_nz_val;
+  sp.nz_n = s->d_nz_n;
   if (!(s->flags & XG_STREAM_NO_RAW)) {
-    XG_CUDA(c, launch_stream_raw(sp, L->rings, s->max_kpad, c->stream));
-    c->launches++;
+    if (s->flags & XG_STREAM_SPARSE) {
+      XG_CUDA(c, launch_stream_sparse(sp, L->rings, c->stream));
+      c->launches += 2;
+    } else {
+      XG_CUDA(c, launch_stream_raw(sp, L->rings, s->max_kpad, c->stream));
+      c->launches++;
+    }
   }
   if (s->B) {
     XG_CUDA(c, launch_stream_cmp(sp, L->rings, c->stream));

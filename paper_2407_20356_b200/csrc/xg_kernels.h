@@ -211,7 +211,17 @@ struct StreamParams {
   const double* scale;       // [ring][k]
   double* y;                 // [ring][y_ld][k]
   int64_t y_ld;
+  // sparse raw mode: pixel-major history hist[c][hp] (u8, column c of the
+  // ring-major layout, frame s) and the new frame's nonzeros per ring
+  uint8_t* hist;
+  int64_t hp;                // frames per pixel row (multiple of 16)
+  int32_t* nz_col;           // [ktot]: ring r's nonzero columns at [koff_r, ...)
+  uint8_t* nz_val;           // [ktot]
+  int32_t* nz_n;             // [ring]
 };
+// Sparse raw streaming (photon-event data): the new column costs nnz * t
+// bytes instead of M * t; results equal the dense kernel's bitwise.
+cudaError_t launch_stream_sparse(const StreamParams& p, int32_t n_rings, cudaStream_t s);
 cudaError_t launch_stream_raw(const StreamParams& p, int32_t n_rings, int64_t max_kpad,
                               cudaStream_t s);
 cudaError_t launch_stream_cmp(const StreamParams& p, int32_t n_rings, cudaStream_t s);

@@ -70,3 +70,27 @@ def test_stream_capacity_and_zero_frame(ctx, orc):
         st.push(frames[0])
     _, g2, cnt = st.g2(1)
     assert cnt[0] == t - 1 and cnt[1] == t - 3
+
+
+@pytest.mark.parametrize("mu", [0.05, 0.8])
+def test_sparse_stream_equals_dense(ctx, orc, mu):
+    """Sparse raw streaming (pixel-major history, nonzeros only) gives the
+    dense stream's exact Gram columns and g2 bitwise, at low and high
+    occupancy (incl. an all-zero frame)."""
+    t, h, w, q = 90, 40, 44, 3
+    frames = orc.gen_speckle(t, h, w, q, mu, 81)
+    frames[17] = 0
+    ring, _ = orc.ring_map(h, w, q)
+    lay = xg.RingLayout.from_ring_map(ctx, ring, q)
+    dense = xg.FrameStream(lay, t, store_ttc=True)
+    sparse = xg.FrameStream(lay, t, store_ttc=True, sparse=True)
+    for i in range(t):
+        dense.push(frames[i])
+        sparse.push(frames[i])
+    for r in range(q):
+        gd, gs = dense.ttc(r, dtype="gram"), sparse.ttc(r, dtype="gram")
+        assert np.array_equal(gs, gd)
+        assert np.array_equal(gs.astype(np.int64), orc.gram_u8(frames[:, ring == r]))
+        _, g2d, cd = dense.g2(r)
+        _, g2s, cs = sparse.g2(r)
+        assert np.array_equal(g2s, g2d) and np.array_equal(cs, cd)
