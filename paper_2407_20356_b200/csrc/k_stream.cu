@@ -160,56 +160,71 @@ __global__ void __launch_bounds__(SR_THREADS) k_stream_cmp(StreamParams p) {
 
 }  // namespace
 
-// K5s-a: one CTA per ring.  The new frame's nonzero ring columns (any order:
-// the column sums below are integer, so order-free) and their scatter into
-// the pixel-major history.
-__global__ void __launch_bounds__(512) k_stream_sparse_gather(StreamParams p) {
-  __shared__ int cnt;
-  const int r = blockIdx.x;
-  const int koff = p.ring_koff[r];
-  const int n = p.ring_nkb[r] * 128;
-  const uint8_t* row = p.x + p.t * p.ktot + koff;
-  if (threadIdx.x == 0) cnt = 0;
-  __syncthreads();
-  const int lane = threadIdx.x & 31;
-  for (int i0 = 0; i0 < n; i0 += 4 * blockDim.x) {
-    const int i = i0 + 4 * threadIdx.x;
-    const uint32_t w = i < n ? *reinterpret_cast<const uint32_t*>(row + i) : 0u;
+// K1s: one warp per 128-column block of the ring-major row (blocks never
+// straddle rings).  Lane l packs columns 4l..4l+3 from the raster through the
+// column -> pixel table, stores them, and adds the block's exact |x|^2 into
+// its ring.  Sparse mode: nonzero columns are compacted per ring (positions
+// from one atomic per warp; any order, the column sums are integer) and
+// scattered into the pixel-major history.
+__global__ void __launch_bounds__(128) k_stream_ingest(StreamParams p) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t blk = static_cast<int64_t>(blockIdx.x) * 4 + warp;
+  if (blk * 128 >= p.ktot) return;  // warp-uniform
+  const int64_t c = blk * 128 + lane * 4;
+  const int4 px = *reinterpret_cast<const int4*>(p.colpix + c);
+  const uint32_t v0 = px.x >= 0 ? p.frame[px.x] : 0u, v1 = px.y >= 0 ? p.frame[px.y] : 0u;
+  const uint32_t v2 = px.z >= 0 ? p.frame[px.z] : 0u, v3 = px.w >= 0 ? p.frame[px.w] : 0u;
+  const uint32_t word = v0 | (v1 << 8) | (v2 << 16) | (v3 << 24);
+  *reinterpret_cast<uint32_t*>(const_cast<uint8_t*>(p.x) + p.t * p.ktot + c) = word;  // the stream owns x
+  const uint32_t sq = __reduce_add_sync(0xffffffffu, __dp4a(word, word, 0u));
+  const int r = p.blk_ring[blk];
+  if (lane == 0 && sq) atomicAdd(p.norm2 + p.t * p.n_rings + r, static_cast<unsigned long long>(sq));
+  if (p.hist) {
+    const int cnt = (v0 != 0u) + (v1 != 0u) + (v2 != 0u) + (v3 != 0u);
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int n = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += n;
+    }
+    const int tot = __shfl_sync(0xffffffffu, incl, 31);
+    if (tot == 0) return;
+    int base = 0;
+    if (lane == 31) base = atomicAdd(p.nz_n + r, tot);
+    base = __shfl_sync(0xffffffffu, base, 31);
+    int pos = p.ring_koff[r] + base + incl - cnt;
+    const uint32_t v[4] = {v0, v1, v2, v3};
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const uint32_t v = (w >> (8 * j)) & 0xFFu;
-      const uint32_t m = __ballot_sync(0xffffffffu, v != 0u);
-      int base = 0;
-      if (lane == 0 && m) base = atomicAdd(&cnt, __popc(m));
-      base = __shfl_sync(0xffffffffu, base, 0);
-      if (v) {
-        const int pos = base + __popc(m & ((1u << lane) - 1u));
-        const int c = koff + i + j;
-        p.nz_col[koff + pos] = c;
-        p.nz_val[koff + pos] = static_cast<uint8_t>(v);
-        p.hist[static_cast<int64_t>(c) * p.hp + p.t] = static_cast<uint8_t>(v);
+      if (v[j]) {
+        p.nz_col[pos] = static_cast<int32_t>(c + j);
+        p.nz_val[pos] = static_cast<uint8_t>(v[j]);
+        p.hist[(c + j) * p.hp + p.t] = static_cast<uint8_t>(v[j]);
+        ++pos;
       }
     }
   }
-  __syncthreads();
-  if (threadIdx.x == 0) p.nz_n[r] = cnt;
 }
 
-// K5s-b: grid (ceil((t+1)/1024), rings); a thread owns 4 consecutive history
-// frames s and walks the ring's nonzeros: one coalesced 32-bit load of
-// hist[c][s..s+3] per nonzero.  Same C, g2 and column outputs as K5.
+// K5s-b: grid (ceil((t+1)/1024), rings, SS_Z).  A thread owns 4 consecutive
+// history frames s and walks its z-slice of the ring's nonzeros: one
+// coalesced 32-bit load of hist[c][s..s+3] per nonzero; the slices' partial
+// integer sums meet in colbuf (integer atomics: exact, order-free).
 constexpr int SS_THREADS = 256;
 constexpr int SS_CHUNK = 1024;
+constexpr int SS_Z = 4;
 __global__ void __launch_bounds__(SS_THREADS) k_stream_sparse_col(StreamParams p) {
   __shared__ int32_t sc[SS_CHUNK];
   __shared__ uint32_t sv[SS_CHUNK];
   const int r = blockIdx.y;
   const int koff = p.ring_koff[r];
   const int n = p.nz_n[r];
+  const int zb = static_cast<int>((static_cast<int64_t>(n) * blockIdx.z) / SS_Z);
+  const int ze = static_cast<int>((static_cast<int64_t>(n) * (blockIdx.z + 1)) / SS_Z);
   const int64_t s0 = static_cast<int64_t>(blockIdx.x) * (4 * SS_THREADS) + 4 * threadIdx.x;
   uint32_t acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0;
-  for (int c0 = 0; c0 < n; c0 += SS_CHUNK) {
-    const int cn = n - c0 < SS_CHUNK ? n - c0 : SS_CHUNK;
+  for (int c0 = zb; c0 < ze; c0 += SS_CHUNK) {
+    const int cn = ze - c0 < SS_CHUNK ? ze - c0 : SS_CHUNK;
     __syncthreads();
     for (int i = threadIdx.x; i < cn; i += SS_THREADS) {
       sc[i] = p.nz_col[koff + c0 + i];
@@ -218,7 +233,8 @@ __global__ void __launch_bounds__(SS_THREADS) k_stream_sparse_col(StreamParams p
     __syncthreads();
     if (s0 <= p.t) {
       const uint8_t* h = p.hist + s0;
-#pragma unroll 4
+      // latency-bound on the scattered history rows: keep 16 loads in flight
+#pragma unroll 16
       for (int i = 0; i < cn; ++i) {
         const uint32_t w = __ldcs(reinterpret_cast<const uint32_t*>(h + static_cast<int64_t>(sc[i]) * p.hp));
         const uint32_t v = sv[i];
@@ -229,27 +245,46 @@ __global__ void __launch_bounds__(SS_THREADS) k_stream_sparse_col(StreamParams p
       }
     }
   }
+  if (s0 > p.t) return;
+  int32_t* col = p.colbuf + static_cast<int64_t>(r) * p.hp + s0;
+  if (acc0) atomicAdd(col, static_cast<int>(acc0));
+  if (acc1 && s0 + 1 <= p.t) atomicAdd(col + 1, static_cast<int>(acc1));
+  if (acc2 && s0 + 2 <= p.t) atomicAdd(col + 2, static_cast<int>(acc2));
+  if (acc3 && s0 + 3 <= p.t) atomicAdd(col + 3, static_cast<int>(acc3));
+}
+
+// K5s-c: the finished column -> C, g2 lag sums and the optional stored column
+// (the dense K5's expressions, so equal bitwise); resets colbuf and nz_n.
+__global__ void __launch_bounds__(256) k_stream_sparse_fin(StreamParams p) {
+  const int r = blockIdx.y;
+  const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (blockIdx.x == 0 && threadIdx.x == 0) p.nz_n[r] = 0;
+  if (s > p.t) return;
+  int32_t* col = p.colbuf + static_cast<int64_t>(r) * p.hp + s;
+  const int acc = *col;
+  *col = 0;
   const double inv_t = p.inv[static_cast<int64_t>(r) * p.inv_ld + p.t];
-  const uint32_t acc[4] = {acc0, acc1, acc2, acc3};
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int64_t s = s0 + j;
-    if (s > p.t) break;
-    const double inv_s = p.inv[static_cast<int64_t>(r) * p.inv_ld + s];
-    const int64_t gi = static_cast<int64_t>(r) * p.g2_ld + (p.t - s);
-    p.g2sum[gi] += static_cast<double>(static_cast<int>(acc[j])) * (inv_s * inv_t);
-    p.g2cnt[gi] += (inv_s != 0.0 && inv_t != 0.0) ? 1 : 0;
-    if (p.gcol) p.gcol[static_cast<int64_t>(r) * p.col_ring_stride + s * p.col_ld + p.t] =
-        static_cast<int>(acc[j]);
-  }
+  const double inv_s = p.inv[static_cast<int64_t>(r) * p.inv_ld + s];
+  const int64_t gi = static_cast<int64_t>(r) * p.g2_ld + (p.t - s);
+  p.g2sum[gi] += static_cast<double>(acc) * (inv_s * inv_t);
+  p.g2cnt[gi] += (inv_s != 0.0 && inv_t != 0.0) ? 1 : 0;
+  if (p.gcol) p.gcol[static_cast<int64_t>(r) * p.col_ring_stride + s * p.col_ld + p.t] = acc;
+}
+
+cudaError_t launch_stream_ingest(const StreamParams& p, cudaStream_t s) {
+  const unsigned blocks = static_cast<unsigned>((p.ktot / 128 + 3) / 4);
+  k_stream_ingest<<<blocks, 128, 0, s>>>(p);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_stream_sparse(const StreamParams& p, int32_t n_rings, cudaStream_t s) {
-  k_stream_sparse_gather<<<n_rings, 512, 0, s>>>(p);
+  dim3 grid(static_cast<unsigned>((p.t + 1 + 4 * SS_THREADS - 1) / (4 * SS_THREADS)), n_rings,
+            SS_Z);
+  k_stream_sparse_col<<<grid, SS_THREADS, 0, s>>>(p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  dim3 grid(static_cast<unsigned>((p.t + 1 + 4 * SS_THREADS - 1) / (4 * SS_THREADS)), n_rings);
-  k_stream_sparse_col<<<grid, SS_THREADS, 0, s>>>(p);
+  dim3 g2(static_cast<unsigned>((p.t + 1 + 255) / 256), n_rings);
+  k_stream_sparse_fin<<<g2, 256, 0, s>>>(p);
   return cudaGetLastError();
 }
 

@@ -59,6 +59,7 @@ struct xg_layout {
   std::vector<int64_t> ring_pixels, kpad, koff;
   std::vector<int64_t> mask_off;  // [rings + 1] offsets into colpos (mask order)
   std::vector<int64_t> colpos;    // ring-major column of every mask entry
+  std::vector<int32_t> colpix;    // [ktot] detector pixel of every column (-1 = padding)
   int32_t* d_band_piece = nullptr;
   Piece* d_pieces = nullptr;
   int32_t* d_band_word = nullptr;
@@ -479,6 +480,8 @@ int xg_layout_create(xg_ctx* c, int64_t full_pixels, int32_t n_rings,
         L->max_band_pieces, band_piece[(size_t)b * (kWarps + 1) + kWarps] -
                                 band_piece[(size_t)b * (kWarps + 1)]);
   }
+  L->colpix.assign(static_cast<size_t>(L->ktot), -1);
+  for (int64_t i = 0; i < offsets[n_rings]; ++i) L->colpix[L->colpos[i]] = static_cast<int32_t>(indices[i]);
   band_word[nb] = static_cast<int32_t>(words.size());
   band_byte[nb] = static_cast<int32_t>(bytes.size() / 4);
   if (words.empty()) words.push_back(0);
@@ -1265,6 +1268,9 @@ struct xg_stream {
   int32_t vdt_ld = 0;
   double* d_y = nullptr;
   uint8_t* d_hist = nullptr;  // sparse mode: pixel-major history [ktot][hp]
+  int32_t* d_colpix = nullptr;  // [ktot] detector pixel of each column (-1 = padding)
+  int32_t* d_blk_ring = nullptr;  // [ktot/128] ring of each 128-column block
+  int32_t* d_colbuf = nullptr;  // sparse mode: [ring][hp] partial column sums
   int64_t hp = 0;
   int32_t* d_nz_col = nullptr;
   uint8_t* d_nz_val = nullptr;
@@ -1321,6 +1327,27 @@ int xg_stream_create(xg_ctx* c, const xg_layout* L, const xg_basis* B, int64_t m
       return cuda_fail(c, e, "stream sparse history alloc");
     }
     cudaMemsetAsync(s->d_hist, 0, (size_t)L->ktot * s->hp, c->stream);
+    if ((e = dalloc(&s->d_colbuf, (size_t)Q * s->hp)) != cudaSuccess) {
+      xg_stream_destroy(s);
+      return cuda_fail(c, e, "stream sparse column alloc");
+    }
+    cudaMemsetAsync(s->d_colbuf, 0, (size_t)Q * s->hp * 4, c->stream);
+    cudaMemsetAsync(s->d_nz_n, 0, (size_t)Q * 4, c->stream);
+  }
+  {
+    // column -> pixel and 128-column block -> ring tables for the one-frame ingest
+    std::vector<int32_t> br(static_cast<size_t>(L->ktot / 128));
+    for (int32_t r = 0; r < L->rings; ++r)
+      for (int64_t b = L->koff[r] / 128; b < (L->koff[r] + L->kpad[r]) / 128; ++b) br[b] = r;
+    if ((e = dalloc(&s->d_colpix, (size_t)L->ktot)) != cudaSuccess ||
+        (e = dalloc(&s->d_blk_ring, br.size())) != cudaSuccess ||
+        (e = cudaMemcpy(s->d_colpix, L->colpix.data(), (size_t)L->ktot * 4,
+                        cudaMemcpyHostToDevice)) != cudaSuccess ||
+        (e = cudaMemcpy(s->d_blk_ring, br.data(), br.size() * 4, cudaMemcpyHostToDevice)) !=
+            cudaSuccess) {
+      xg_stream_destroy(s);
+      return cuda_fail(c, e, "stream ingest tables");
+    }
   }
   cudaMemsetAsync(s->d_x, 0, (size_t)max_frames * L->ktot, c->stream);
   cudaMemsetAsync(s->d_zero, 0, (size_t)Q * 8, c->stream);
@@ -1379,6 +1406,9 @@ void xg_stream_destroy(xg_stream* s) {
   dfree(s->d_vdt);
   dfree(s->d_y);
   dfree(s->d_hist);
+  dfree(s->d_colpix);
+  dfree(s->d_blk_ring);
+  dfree(s->d_colbuf);
   dfree(s->d_nz_col);
   dfree(s->d_nz_val);
   dfree(s->d_nz_n);
@@ -1395,46 +1425,6 @@ int xg_stream_push(xg_stream* s, const uint8_t* frame, int on_device) {
   XG_CUDA(c, cudaMemcpyAsync(s->d_frame, frame, (size_t)L->pixels,
                              on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
                              c->stream));
-  IngestParams p;
-  p.raster = s->d_frame;
-  p.x = s->d_x;
-  p.pixels = L->pixels;
-  p.ktot = L->ktot;
-  p.band = L->band;
-  p.n_bands = L->n_bands;
-  p.n_rings = L->rings;
-  p.band_piece = L->d_band_piece;
-  p.pieces = L->d_pieces;
-  p.band_word = L->d_band_word;
-  p.words = L->d_words;
-  p.band_byte = L->d_band_byte;
-  p.bytes = L->d_bytes;
-  p.max_words = L->max_words;
-  p.max_bytes = L->max_bytes;
-  p.max_band_pieces = L->max_band_pieces;
-  p.t0 = s->t;  // frame 0 of the staging buffer lands in history row t
-  p.n_frames = 1;
-  p.frames_per_cta = 1;
-  p.norm2 = reinterpret_cast<unsigned long long*>(s->d_norm2);
-  XG_CUDA(c, cudaMemsetAsync(s->d_norm2 + s->t * L->rings, 0, (size_t)L->rings * 8, c->stream));
-  XG_CUDA(c, launch_ingest(p, c->stream));
-  NormParams np;
-  np.t0 = s->t;
-  np.norm2 = s->d_norm2;
-  np.n_frames = 1;
-  np.ld = s->tp;
-  np.n_rings = L->rings;
-  np.norms = s->d_norms;
-  np.inv = s->d_inv;
-  np.inv2 = nullptr;
-  np.zero_count = s->d_zero;
-  np.first_zero = s->d_first_zero;
-  np.nz_bits = s->d_nz_bits;
-  np.nz_words = static_cast<int32_t>(s->tp / 32);
-  np.max_norm2 = nullptr;
-  np.err = c->d_err;
-  XG_CUDA(c, launch_norms(np, c->stream));
-  c->launches += 2;
   StreamParams sp;
   sp.x = s->d_x;
   sp.ktot = L->ktot;
@@ -1464,6 +1454,31 @@ int xg_stream_push(xg_stream* s, const uint8_t* frame, int on_device) {
   sp.nz_col = s->d_nz_col;
   sp.nz_val = s->d_nz_val;
   sp.nz_n = s->d_nz_n;
+  sp.colbuf = s->d_colbuf;
+  sp.frame = s->d_frame;
+  sp.colpix = s->d_colpix;
+  sp.blk_ring = s->d_blk_ring;
+  sp.n_rings = L->rings;
+  sp.norm2 = reinterpret_cast<unsigned long long*>(s->d_norm2);
+  XG_CUDA(c, cudaMemsetAsync(s->d_norm2 + s->t * L->rings, 0, (size_t)L->rings * 8, c->stream));
+  XG_CUDA(c, launch_stream_ingest(sp, c->stream));
+  NormParams np;
+  np.t0 = s->t;
+  np.norm2 = s->d_norm2;
+  np.n_frames = 1;
+  np.ld = s->tp;
+  np.n_rings = L->rings;
+  np.norms = s->d_norms;
+  np.inv = s->d_inv;
+  np.inv2 = nullptr;
+  np.zero_count = s->d_zero;
+  np.first_zero = s->d_first_zero;
+  np.nz_bits = s->d_nz_bits;
+  np.nz_words = static_cast<int32_t>(s->tp / 32);
+  np.max_norm2 = nullptr;
+  np.err = c->d_err;
+  XG_CUDA(c, launch_norms(np, c->stream));
+  c->launches += 2;
   if (!(s->flags & XG_STREAM_NO_RAW)) {
     if (s->flags & XG_STREAM_SPARSE) {
       XG_CUDA(c, launch_stream_sparse(sp, L->rings, c->stream));
