@@ -78,57 +78,53 @@ __global__ void __launch_bounds__(SR_THREADS) k_stream_raw(StreamParams p) {
   }
 }
 
-// K6a: one CTA per ring; threads own (digit, coefficient) accumulators.
-__global__ void __launch_bounds__(512) k_stream_project(StreamParams p) {
-  __shared__ int32_t nz_col[1024];
-  __shared__ int32_t nz_val[1024];
-  __shared__ int nz_count;
-  __shared__ int32_t accs[3 * 256];
+// K6a: grid (rings, PZ).  A CTA takes a slice of the ring's nonzero pixels
+// (compacted by the one-frame ingest -- the reference's project_row skips
+// zeros too, compress.cpp:17) and accumulates x * digit for every (digit,
+// coefficient) pair from the pixel-major int8 digits; slices meet in pacc
+// (integer atomics: exact, order-free).
+constexpr int PZ = 8;
+__global__ void __launch_bounds__(256) k_stream_proj_acc(StreamParams p) {
   const int r = blockIdx.x;
-  const int64_t koff = p.ring_koff[r];
-  const int64_t kpad = static_cast<int64_t>(p.ring_nkb[r]) * 128;
+  const int koff = p.ring_koff[r];
+  const int n = p.nz_n[r];
+  const int zb = static_cast<int>((static_cast<int64_t>(n) * blockIdx.y) / PZ);
+  const int ze = static_cast<int>((static_cast<int64_t>(n) * (blockIdx.y + 1)) / PZ);
   const int nacc = p.n_digits * p.k;  // <= 768
-  const uint8_t* xrow = p.x + p.t * p.ktot + koff;
-  int32_t acc0 = 0, acc1 = 0;  // thread owns entries tid and tid + blockDim
-  for (int64_t c0 = 0; c0 < kpad; c0 += 1024) {  // <= 1024 nonzeros per chunk
-    if (threadIdx.x == 0) nz_count = 0;
-    __syncthreads();
-    // compact the nonzero pixels of this chunk (16 bytes per thread step)
-    for (int64_t v = c0 / 16 + threadIdx.x; v < (c0 + 1024) / 16 && v < kpad / 16;
-         v += blockDim.x) {
-      const uint4 w = reinterpret_cast<const uint4*>(xrow)[v];
-      if ((w.x | w.y | w.z | w.w) == 0u) continue;
-      const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-      for (int b = 0; b < 16; ++b) {
-        const uint32_t val = (ws[b >> 2] >> (8 * (b & 3))) & 0xFFu;
-        if (val) {
-          const int slot = atomicAdd(&nz_count, 1);
-          nz_col[slot] = static_cast<int32_t>(v * 16 + b);
-          nz_val[slot] = static_cast<int32_t>(val);
-        }
-      }
+  int32_t acc[3] = {0, 0, 0};
+#pragma unroll 4
+  for (int e = zb; e < ze; ++e) {
+    const int8_t* vd = p.vdt + static_cast<int64_t>(p.nz_col[koff + e]) * p.vdt_ld;
+    const int xv = p.nz_val[koff + e];
+#pragma unroll
+    for (int m = 0; m < 3; ++m) {
+      const int j = threadIdx.x + 256 * m;
+      if (j < nacc) acc[m] += xv * vd[j];
     }
-    __syncthreads();
-    const int n = nz_count;
-    // integer accumulation: order-free, exact
-    for (int e = 0; e < n; ++e) {
-      const int8_t* vd = p.vdt + (koff + nz_col[e]) * static_cast<int64_t>(p.vdt_ld);
-      const int xv = nz_val[e];
-      if (static_cast<int>(threadIdx.x) < nacc) acc0 += xv * vd[threadIdx.x];
-      if (static_cast<int>(threadIdx.x + blockDim.x) < nacc) acc1 += xv * vd[threadIdx.x + blockDim.x];
-    }
-    __syncthreads();
   }
-  if (static_cast<int>(threadIdx.x) < nacc) accs[threadIdx.x] = acc0;
-  if (static_cast<int>(threadIdx.x + blockDim.x) < nacc) accs[threadIdx.x + blockDim.x] = acc1;
-  __syncthreads();
+  int32_t* pa = p.pacc + static_cast<int64_t>(r) * 768;
+#pragma unroll
+  for (int m = 0; m < 3; ++m) {
+    const int j = threadIdx.x + 256 * m;
+    if (j < nacc && acc[m]) atomicAdd(pa + j, acc[m]);
+  }
+}
+
+// K6a': digit sums -> coefficients with the batch projection's expression
+// (bitwise-equal rows); resets pacc (and nz_n when this is the last pass).
+__global__ void __launch_bounds__(128) k_stream_proj_fin(StreamParams p) {
+  const int r = blockIdx.x;
+  int32_t* pa = p.pacc + static_cast<int64_t>(r) * 768;
   const double inv = p.inv[static_cast<int64_t>(r) * p.inv_ld + p.t];
   for (int j = threadIdx.x; j < p.k; j += blockDim.x) {
-    // same f64 expression as k_project's epilogue (bitwise-equal coefficients)
-    p.y[(static_cast<int64_t>(r) * p.y_ld + p.t) * p.k + j] = combine_digits(
-        accs[j], p.n_digits > 1 ? accs[p.k + j] : 0, p.n_digits > 2 ? accs[2 * p.k + j] : 0,
-        p.n_digits, p.scale[static_cast<int64_t>(r) * p.k + j], inv);
+    const int32_t a0 = pa[j], a1 = p.n_digits > 1 ? pa[p.k + j] : 0;
+    const int32_t a2 = p.n_digits > 2 ? pa[2 * p.k + j] : 0;
+    p.y[(static_cast<int64_t>(r) * p.y_ld + p.t) * p.k + j] =
+        combine_digits(a0, a1, a2, p.n_digits, p.scale[static_cast<int64_t>(r) * p.k + j], inv);
   }
+  __syncthreads();
+  for (int j = threadIdx.x; j < p.n_digits * p.k; j += blockDim.x) pa[j] = 0;
+  if (threadIdx.x == 0 && p.nz_reset == 2) p.nz_n[r] = 0;
 }
 
 // K6b: grid (ceil((t+1)/SR_ROWS), rings); a warp per history row.
@@ -179,7 +175,7 @@ __global__ void __launch_bounds__(128) k_stream_ingest(StreamParams p) {
   const uint32_t sq = __reduce_add_sync(0xffffffffu, __dp4a(word, word, 0u));
   const int r = p.blk_ring[blk];
   if (lane == 0 && sq) atomicAdd(p.norm2 + p.t * p.n_rings + r, static_cast<unsigned long long>(sq));
-  if (p.hist) {
+  if (p.nz_n) {
     const int cnt = (v0 != 0u) + (v1 != 0u) + (v2 != 0u) + (v3 != 0u);
     int incl = cnt;
 #pragma unroll
@@ -199,7 +195,7 @@ __global__ void __launch_bounds__(128) k_stream_ingest(StreamParams p) {
       if (v[j]) {
         p.nz_col[pos] = static_cast<int32_t>(c + j);
         p.nz_val[pos] = static_cast<uint8_t>(v[j]);
-        p.hist[(c + j) * p.hp + p.t] = static_cast<uint8_t>(v[j]);
+        if (p.hist) p.hist[(c + j) * p.hp + p.t] = static_cast<uint8_t>(v[j]);
         ++pos;
       }
     }
@@ -258,7 +254,7 @@ __global__ void __launch_bounds__(SS_THREADS) k_stream_sparse_col(StreamParams p
 __global__ void __launch_bounds__(256) k_stream_sparse_fin(StreamParams p) {
   const int r = blockIdx.y;
   const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (blockIdx.x == 0 && threadIdx.x == 0) p.nz_n[r] = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && p.nz_reset == 1) p.nz_n[r] = 0;
   if (s > p.t) return;
   int32_t* col = p.colbuf + static_cast<int64_t>(r) * p.hp + s;
   const int acc = *col;
@@ -302,8 +298,11 @@ cudaError_t launch_stream_raw(const StreamParams& p, int32_t n_rings, int64_t ma
 }
 
 cudaError_t launch_stream_cmp(const StreamParams& p, int32_t n_rings, cudaStream_t s) {
-  k_stream_project<<<n_rings, 512, 0, s>>>(p);
+  k_stream_proj_acc<<<dim3(n_rings, PZ), 256, 0, s>>>(p);
   cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  k_stream_proj_fin<<<n_rings, 128, 0, s>>>(p);
+  e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   dim3 grid(static_cast<unsigned>((p.t + 1 + SR_ROWS - 1) / SR_ROWS), n_rings);
   k_stream_cmp<<<grid, SR_THREADS, 0, s>>>(p);

@@ -1271,6 +1271,7 @@ struct xg_stream {
   int32_t* d_colpix = nullptr;  // [ktot] detector pixel of each column (-1 = padding)
   int32_t* d_blk_ring = nullptr;  // [ktot/128] ring of each 128-column block
   int32_t* d_colbuf = nullptr;  // sparse mode: [ring][hp] partial column sums
+  int32_t* d_pacc = nullptr;    // with a basis: [ring][768] projection digit sums
   int64_t hp = 0;
   int32_t* d_nz_col = nullptr;
   uint8_t* d_nz_val = nullptr;
@@ -1319,10 +1320,7 @@ int xg_stream_create(xg_ctx* c, const xg_layout* L, const xg_basis* B, int64_t m
   }
   if (flags & XG_STREAM_SPARSE) {
     s->hp = round_up(max_frames, 16);
-    if ((e = dalloc(&s->d_hist, (size_t)L->ktot * s->hp)) != cudaSuccess ||
-        (e = dalloc(&s->d_nz_col, (size_t)L->ktot)) != cudaSuccess ||
-        (e = dalloc(&s->d_nz_val, (size_t)L->ktot)) != cudaSuccess ||
-        (e = dalloc(&s->d_nz_n, (size_t)Q)) != cudaSuccess) {
+    if ((e = dalloc(&s->d_hist, (size_t)L->ktot * s->hp)) != cudaSuccess) {
       xg_stream_destroy(s);
       return cuda_fail(c, e, "stream sparse history alloc");
     }
@@ -1332,7 +1330,18 @@ int xg_stream_create(xg_ctx* c, const xg_layout* L, const xg_basis* B, int64_t m
       return cuda_fail(c, e, "stream sparse column alloc");
     }
     cudaMemsetAsync(s->d_colbuf, 0, (size_t)Q * s->hp * 4, c->stream);
+  }
+  if ((flags & XG_STREAM_SPARSE) || B) {
+    // the new frame's nonzeros per ring (sparse raw column, sparse projection)
+    if ((e = dalloc(&s->d_nz_col, (size_t)L->ktot)) != cudaSuccess ||
+        (e = dalloc(&s->d_nz_val, (size_t)L->ktot)) != cudaSuccess ||
+        (e = dalloc(&s->d_nz_n, (size_t)Q)) != cudaSuccess ||
+        (B && (e = dalloc(&s->d_pacc, (size_t)Q * 768)) != cudaSuccess)) {
+      xg_stream_destroy(s);
+      return cuda_fail(c, e, "stream nonzero lists alloc");
+    }
     cudaMemsetAsync(s->d_nz_n, 0, (size_t)Q * 4, c->stream);
+    if (B) cudaMemsetAsync(s->d_pacc, 0, (size_t)Q * 768 * 4, c->stream);
   }
   {
     // column -> pixel and 128-column block -> ring tables for the one-frame ingest
@@ -1409,6 +1418,7 @@ void xg_stream_destroy(xg_stream* s) {
   dfree(s->d_colpix);
   dfree(s->d_blk_ring);
   dfree(s->d_colbuf);
+  dfree(s->d_pacc);
   dfree(s->d_nz_col);
   dfree(s->d_nz_val);
   dfree(s->d_nz_n);
@@ -1455,6 +1465,8 @@ int xg_stream_push(xg_stream* s, const uint8_t* frame, int on_device) {
   sp.nz_val = s->d_nz_val;
   sp.nz_n = s->d_nz_n;
   sp.colbuf = s->d_colbuf;
+  sp.pacc = s->d_pacc;
+  sp.nz_reset = s->B ? 2 : 1;
   sp.frame = s->d_frame;
   sp.colpix = s->d_colpix;
   sp.blk_ring = s->d_blk_ring;

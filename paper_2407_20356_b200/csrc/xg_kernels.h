@@ -219,6 +219,8 @@ struct StreamParams {
   uint8_t* nz_val;           // [ktot]
   int32_t* nz_n;             // [ring] (zero on entry; reset by the column pass)
   int32_t* colbuf;           // [ring][hp] partial column sums (zero on entry)
+  int32_t* pacc;             // [ring][768] projection digit sums (zero on entry)
+  int32_t nz_reset;          // which pass resets nz_n: 1 sparse column, 2 projection
   // one-frame ingest
   const uint8_t* frame;      // raster of the new frame
   const int32_t* colpix;     // [ktot] detector pixel of each column (-1 = padding)

@@ -26,8 +26,16 @@ def main():
     ring = xg.annular_rings(H, W, Q)
     lay = xg.RingLayout(ctx, H * W, [np.nonzero(ring == r)[0] for r in range(Q)])
     nnz = float((frames[:256] != 0).float().mean()) * H * W
+    k = int(os.environ.get("K", 0))
+    basis = None
+    if k:
+        basis = xg.Basis(lay, k)
+        rng = np.random.default_rng(1)
+        for r in range(Q):
+            qm, _ = np.linalg.qr(rng.standard_normal((int((ring == r).sum()), k)))
+            basis.set_ring(r, qm)
     for sparse in (True, False):
-        s = xg.FrameStream(lay, T, sparse=sparse)
+        s = xg.FrameStream(lay, T, sparse=sparse, basis=basis)
         t0 = time.perf_counter()
         for i in range(depth):
             s.push(frames[i])
