@@ -10,14 +10,17 @@
 //             g2sum[d = t-s] += C -- lags accumulate in ascending t exactly
 //             like g2_from_ttc's sequential sum (correlate.cpp:67-85).
 //             HBM-bound: t * M bytes per frame, 128-bit coalesced loads.
+//   K5s sparse raw (XG_STREAM_SPARSE): the same column from the new frame's
+//             nonzeros over a pixel-major history: nnz * t bytes per frame.
 //   K6a proj: y_t = (x_t/|x_t|) V from the NONZERO pixels of the new frame
 //             only (the reference's project_row skips zeros too,
 //             compress.cpp:17) against a pixel-major copy of the int8 basis
 //             digits; the f64 combination is the same expression as the
 //             batch projection (k_project.cu), so streamed coefficients equal
 //             batch coefficients bitwise.
-//   K6b cmp:  C~(s,t) = y_s . y_t (f64) for s <= t over the coefficient
-//             history, g2 accumulated like K5.  HBM-bound: t * Q * k * 8 B.
+//   K6b cmp:  C~(s,t) = y_s . y_t over an fp32 copy of the coefficient
+//             history (C~ is fp32-accurate by contract), g2 accumulated like
+//             K5 in f64.  HBM-bound: t * Q * k * 4 B.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -91,15 +94,26 @@ __global__ void __launch_bounds__(256) k_stream_proj_acc(StreamParams p) {
   const int zb = static_cast<int>((static_cast<int64_t>(n) * blockIdx.y) / PZ);
   const int ze = static_cast<int>((static_cast<int64_t>(n) * (blockIdx.y + 1)) / PZ);
   const int nacc = p.n_digits * p.k;  // <= 768
+  __shared__ int32_t sc[256];
+  __shared__ int32_t sv[256];
   int32_t acc[3] = {0, 0, 0};
-#pragma unroll 4
-  for (int e = zb; e < ze; ++e) {
-    const int8_t* vd = p.vdt + static_cast<int64_t>(p.nz_col[koff + e]) * p.vdt_ld;
-    const int xv = p.nz_val[koff + e];
+  for (int c0 = zb; c0 < ze; c0 += 256) {
+    const int cn = ze - c0 < 256 ? ze - c0 : 256;
+    __syncthreads();
+    if (static_cast<int>(threadIdx.x) < cn) {
+      sc[threadIdx.x] = p.nz_col[koff + c0 + threadIdx.x];
+      sv[threadIdx.x] = p.nz_val[koff + c0 + threadIdx.x];
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int e = 0; e < cn; ++e) {
+      const int8_t* vd = p.vdt + static_cast<int64_t>(sc[e]) * p.vdt_ld;
+      const int xv = sv[e];
 #pragma unroll
-    for (int m = 0; m < 3; ++m) {
-      const int j = threadIdx.x + 256 * m;
-      if (j < nacc) acc[m] += xv * vd[j];
+      for (int m = 0; m < 3; ++m) {
+        const int j = threadIdx.x + 256 * m;
+        if (j < nacc) acc[m] += xv * vd[j];
+      }
     }
   }
   int32_t* pa = p.pacc + static_cast<int64_t>(r) * 768;
@@ -119,8 +133,10 @@ __global__ void __launch_bounds__(128) k_stream_proj_fin(StreamParams p) {
   for (int j = threadIdx.x; j < p.k; j += blockDim.x) {
     const int32_t a0 = pa[j], a1 = p.n_digits > 1 ? pa[p.k + j] : 0;
     const int32_t a2 = p.n_digits > 2 ? pa[2 * p.k + j] : 0;
-    p.y[(static_cast<int64_t>(r) * p.y_ld + p.t) * p.k + j] =
+    const double y =
         combine_digits(a0, a1, a2, p.n_digits, p.scale[static_cast<int64_t>(r) * p.k + j], inv);
+    p.y[(static_cast<int64_t>(r) * p.y_ld + p.t) * p.k + j] = y;
+    p.yf[(static_cast<int64_t>(r) * p.y_ld + p.t) * p.k + j] = static_cast<float>(y);
   }
   __syncthreads();
   for (int j = threadIdx.x; j < p.n_digits * p.k; j += blockDim.x) pa[j] = 0;
@@ -129,28 +145,46 @@ __global__ void __launch_bounds__(128) k_stream_proj_fin(StreamParams p) {
 
 // K6b: grid (ceil((t+1)/SR_ROWS), rings); a warp per history row.
 __global__ void __launch_bounds__(SR_THREADS) k_stream_cmp(StreamParams p) {
-  __shared__ double yt[1024];
+  // fp32 coefficient history (C~ is fp32-accurate by contract): half the
+  // bytes of the f64 rows; products summed in fp32 over k, lags in f64
+  __shared__ float yt[1024];
   const int r = blockIdx.y;
-  const double* ybase = p.y + static_cast<int64_t>(r) * p.y_ld * p.k;
+  const float* ybase = p.yf + static_cast<int64_t>(r) * p.y_ld * p.k;
   for (int j = threadIdx.x; j < p.k; j += blockDim.x) yt[j] = ybase[p.t * p.k + j];
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const double inv_t = p.inv[static_cast<int64_t>(r) * p.inv_ld + p.t];
-  const int64_t s_begin = static_cast<int64_t>(blockIdx.x) * SR_ROWS;
-  for (int64_t s = s_begin + warp; s < s_begin + SR_ROWS && s <= p.t; s += SR_THREADS / 32) {
-    const double* ys = ybase + s * p.k;
-    double acc = 0.0;
-    for (int j = lane; j < p.k; j += 32) acc = fma(__ldcs(ys + j), yt[j], acc);
+  // a warp's 8 rows are independent: all their loads go out before any
+  // reduction, and lanes 0..7 then update the 8 lags in parallel
+  constexpr int RPW = SR_ROWS / (SR_THREADS / 32);
+  const int64_t s_first = static_cast<int64_t>(blockIdx.x) * SR_ROWS + warp * RPW;
+  float part[RPW];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) {
-      const double inv_s = p.inv[static_cast<int64_t>(r) * p.inv_ld + s];
-      const int64_t gi = static_cast<int64_t>(r) * p.g2_ld + (p.t - s);
-      p.cg2sum[gi] += acc;
-      p.cg2cnt[gi] += (inv_s != 0.0 && inv_t != 0.0) ? 1 : 0;
-      if (p.ccol) p.ccol[static_cast<int64_t>(r) * p.col_ring_stride + s * p.col_ld + p.t] =
-          static_cast<float>(acc);
+  for (int q = 0; q < RPW; ++q) {
+    const int64_t s = s_first + q;
+    float a = 0.f;
+    if (s <= p.t) {
+      const float* ys = ybase + s * p.k;
+      for (int j = lane; j < p.k; j += 32) a = fmaf(__ldcs(ys + j), yt[j], a);
     }
+    part[q] = a;
+  }
+  float mine = 0.f;
+#pragma unroll
+  for (int q = 0; q < RPW; ++q) {
+    float a = part[q];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (lane == q) mine = a;
+  }
+  const int64_t s = s_first + lane;
+  if (lane < RPW && s <= p.t) {
+    const double acc = mine;
+    const double inv_s = p.inv[static_cast<int64_t>(r) * p.inv_ld + s];
+    const int64_t gi = static_cast<int64_t>(r) * p.g2_ld + (p.t - s);
+    p.cg2sum[gi] += acc;
+    p.cg2cnt[gi] += (inv_s != 0.0 && inv_t != 0.0) ? 1 : 0;
+    if (p.ccol) p.ccol[static_cast<int64_t>(r) * p.col_ring_stride + s * p.col_ld + p.t] = mine;
   }
 }
 
@@ -202,11 +236,12 @@ __global__ void __launch_bounds__(128) k_stream_ingest(StreamParams p) {
   }
 }
 
-// K5s-b: grid (ceil((t+1)/1024), rings, SS_Z).  A thread owns 4 consecutive
+// K5s-b: grid (ceil((t+1)/2048), rings, SS_Z).  A thread owns 8 consecutive
 // history frames s and walks its z-slice of the ring's nonzeros: one
-// coalesced 32-bit load of hist[c][s..s+3] per nonzero; the slices' partial
+// coalesced 64-bit load of hist[c][s..s+7] per nonzero; the slices' partial
 // integer sums meet in colbuf (integer atomics: exact, order-free).
 constexpr int SS_THREADS = 256;
+constexpr int SS_S = 8;             // history frames per thread
 constexpr int SS_CHUNK = 1024;
 constexpr int SS_Z = 4;
 __global__ void __launch_bounds__(SS_THREADS) k_stream_sparse_col(StreamParams p) {
@@ -217,8 +252,10 @@ __global__ void __launch_bounds__(SS_THREADS) k_stream_sparse_col(StreamParams p
   const int n = p.nz_n[r];
   const int zb = static_cast<int>((static_cast<int64_t>(n) * blockIdx.z) / SS_Z);
   const int ze = static_cast<int>((static_cast<int64_t>(n) * (blockIdx.z + 1)) / SS_Z);
-  const int64_t s0 = static_cast<int64_t>(blockIdx.x) * (4 * SS_THREADS) + 4 * threadIdx.x;
-  uint32_t acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0;
+  const int64_t s0 = static_cast<int64_t>(blockIdx.x) * (SS_S * SS_THREADS) + SS_S * threadIdx.x;
+  uint32_t acc[SS_S];
+#pragma unroll
+  for (int j = 0; j < SS_S; ++j) acc[j] = 0;
   for (int c0 = zb; c0 < ze; c0 += SS_CHUNK) {
     const int cn = ze - c0 < SS_CHUNK ? ze - c0 : SS_CHUNK;
     __syncthreads();
@@ -229,24 +266,24 @@ __global__ void __launch_bounds__(SS_THREADS) k_stream_sparse_col(StreamParams p
     __syncthreads();
     if (s0 <= p.t) {
       const uint8_t* h = p.hist + s0;
-      // latency-bound on the scattered history rows: keep 16 loads in flight
-#pragma unroll 16
+      // latency-bound on the scattered history rows: keep 8 loads in flight
+#pragma unroll 8
       for (int i = 0; i < cn; ++i) {
-        const uint32_t w = __ldcs(reinterpret_cast<const uint32_t*>(h + static_cast<int64_t>(sc[i]) * p.hp));
+        const uint2 w = __ldcs(reinterpret_cast<const uint2*>(h + static_cast<int64_t>(sc[i]) * p.hp));
         const uint32_t v = sv[i];
-        acc0 += v * (w & 0xFFu);
-        acc1 += v * ((w >> 8) & 0xFFu);
-        acc2 += v * ((w >> 16) & 0xFFu);
-        acc3 += v * (w >> 24);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          acc[j] += v * ((w.x >> (8 * j)) & 0xFFu);
+          acc[4 + j] += v * ((w.y >> (8 * j)) & 0xFFu);
+        }
       }
     }
   }
   if (s0 > p.t) return;
   int32_t* col = p.colbuf + static_cast<int64_t>(r) * p.hp + s0;
-  if (acc0) atomicAdd(col, static_cast<int>(acc0));
-  if (acc1 && s0 + 1 <= p.t) atomicAdd(col + 1, static_cast<int>(acc1));
-  if (acc2 && s0 + 2 <= p.t) atomicAdd(col + 2, static_cast<int>(acc2));
-  if (acc3 && s0 + 3 <= p.t) atomicAdd(col + 3, static_cast<int>(acc3));
+#pragma unroll
+  for (int j = 0; j < SS_S; ++j)
+    if (acc[j] && s0 + j <= p.t) atomicAdd(col + j, static_cast<int>(acc[j]));
 }
 
 // K5s-c: the finished column -> C, g2 lag sums and the optional stored column
@@ -274,8 +311,8 @@ cudaError_t launch_stream_ingest(const StreamParams& p, cudaStream_t s) {
 }
 
 cudaError_t launch_stream_sparse(const StreamParams& p, int32_t n_rings, cudaStream_t s) {
-  dim3 grid(static_cast<unsigned>((p.t + 1 + 4 * SS_THREADS - 1) / (4 * SS_THREADS)), n_rings,
-            SS_Z);
+  dim3 grid(static_cast<unsigned>((p.t + 1 + SS_S * SS_THREADS - 1) / (SS_S * SS_THREADS)),
+            n_rings, SS_Z);
   k_stream_sparse_col<<<grid, SS_THREADS, 0, s>>>(p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;

@@ -1267,6 +1267,7 @@ struct xg_stream {
   int8_t* d_vdt = nullptr;
   int32_t vdt_ld = 0;
   double* d_y = nullptr;
+  float* d_yf = nullptr;
   uint8_t* d_hist = nullptr;  // sparse mode: pixel-major history [ktot][hp]
   int32_t* d_colpix = nullptr;  // [ktot] detector pixel of each column (-1 = padding)
   int32_t* d_blk_ring = nullptr;  // [ktot/128] ring of each 128-column block
@@ -1381,6 +1382,7 @@ int xg_stream_create(xg_ctx* c, const xg_layout* L, const xg_basis* B, int64_t m
     }
     if ((e = dalloc(&s->d_vdt, vdt.size())) != cudaSuccess ||
         (e = dalloc(&s->d_y, (size_t)Q * s->tp * b->k)) != cudaSuccess ||
+        (e = dalloc(&s->d_yf, (size_t)Q * s->tp * b->k)) != cudaSuccess ||
         (e = cudaMemcpy(s->d_vdt, vdt.data(), vdt.size(), cudaMemcpyHostToDevice)) != cudaSuccess) {
       xg_stream_destroy(s);
       return cuda_fail(c, e, "stream basis");
@@ -1414,6 +1416,7 @@ void xg_stream_destroy(xg_stream* s) {
   dfree(s->d_ccol);
   dfree(s->d_vdt);
   dfree(s->d_y);
+  dfree(s->d_yf);
   dfree(s->d_hist);
   dfree(s->d_colpix);
   dfree(s->d_blk_ring);
@@ -1458,6 +1461,7 @@ int xg_stream_push(xg_stream* s, const uint8_t* frame, int on_device) {
   sp.k = s->B ? s->B->k : 0;
   sp.scale = s->B ? s->B->d_scale : nullptr;
   sp.y = s->d_y;
+  sp.yf = s->d_yf;
   sp.y_ld = s->tp;
   sp.hist = s->d_hist;
   sp.hp = s->hp;
