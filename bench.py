@@ -287,12 +287,79 @@ def run_compressed(args, torch, xg, ctx, stream, frames, series, ring, sizes, mi
                        "achieved": proj_bytes / (proj_ms / 1e3) / 1e9, "peak": peaks["hbm_gbs"],
                        "unit": "GB/s", "frac": proj_bytes / (proj_ms / 1e3) / 1e9 / peaks["hbm_gbs"],
                        "bytes": proj_bytes},
-        "gram": {"kernel": "k_gram_tc<1> (K4, fused g2) + fold", "bound": "tensor", "ms": cg_ms,
+        "gram": {"kernel": "k_gram2<1> (K4, CTA-pair, fused g2) + fold", "bound": "tensor", "ms": cg_ms,
                  "achieved_algorithmic": cg_flops_alg / (cg_ms / 1e3) / 1e12,
                  "achieved_mma": cg_flops_mma / (cg_ms / 1e3) / 1e12,
                  "peak": peaks["bf16_tflops"], "unit": "TFLOP/s (bf16)",
                  "frac": cg_flops_mma / (cg_ms / 1e3) / 1e12 / peaks["bf16_tflops"],
                  "c_bytes_written": q * (T * T / 2) * 4},
+    }
+
+
+def run_streaming(args, torch, xg, ctx, stream):
+    """configs[2] (C3) streaming mode at a bounded history depth: 1024^2
+    detector, Q=64 rings, mu=0.02, k=128.  Frames are pushed one at a time
+    (the public FrameStream API, frames already on the device); each push
+    ingests the frame and correlates it against the whole history of every
+    ring.  Timed: n pushes at history depth D after an untimed fill."""
+    H = W = 1024
+    Q, mu, k, n = 64, 0.02, 128, 64
+    D = args.stream_depth
+    dev = torch.device("cuda", torch.cuda.current_device())
+    frames = torch.empty((D + n, H * W), dtype=torch.uint8, device=dev)
+    xg.synth_speckle(ctx, frames.data_ptr(), D + n, H, W, Q, mu, 7)
+    ring = xg.annular_rings(H, W, Q)
+    lay = xg.RingLayout(ctx, H * W, [np.nonzero(ring == r)[0] for r in range(Q)])
+    rng = np.random.default_rng(3)
+    basis = xg.Basis(lay, k)
+    for r in range(Q):  # timing does not depend on the basis values
+        qm, _ = np.linalg.qr(rng.standard_normal((int((ring == r).sum()), k)))
+        basis.set_ring(r, qm)
+    nnz = float((frames[:256] != 0).float().mean()) * H * W
+    m_total = sum(lay.ring_pixels(r) for r in range(Q))
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+
+    def timed(depth, **kw):
+        s = xg.FrameStream(lay, depth + n, **kw)
+        for i in range(depth):
+            s.push(frames[i])
+        torch.cuda.synchronize()
+        ctx.synchronize()
+        a, b = ev(), ev()
+        a.record(stream)
+        for i in range(depth, depth + n):
+            s.push(frames[i])
+        b.record(stream)
+        torch.cuda.synchronize()
+        ctx.synchronize()
+        ms = a.elapsed_time(b) / n
+        del s
+        return ms
+
+    peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+    t_mid = D + n / 2
+    ms_s = timed(D, sparse=True)
+    ms_c = timed(D, sparse=True, basis=basis)
+    d_dense = min(D, 4096)
+    ms_d = timed(d_dense)
+    dense_bytes = m_total * (d_dense + n / 2)
+    sparse_bytes = nnz * t_mid
+    cmp_bytes = t_mid * Q * k * 4
+    return {
+        "workload": f"C3: 1024x1024, Q={Q}, mu={mu}, k={k}; {n} pushes timed at history depth {D}",
+        "nnz_per_frame": nnz,
+        "raw_sparse": {"frames_per_s": 1e3 / ms_s, "ms_per_frame": ms_s,
+                       "column_bytes_per_frame": sparse_bytes,
+                       "achieved_gbs": sparse_bytes / (ms_s / 1e3) / 1e9},
+        "raw_sparse_plus_compressed": {
+            "frames_per_s": 1e3 / ms_c, "ms_per_frame": ms_c,
+            "bytes_per_frame": sparse_bytes + cmp_bytes,
+            "achieved_gbs": (sparse_bytes + cmp_bytes) / (ms_c / 1e3) / 1e9},
+        "raw_dense": {"depth": d_dense, "frames_per_s": 1e3 / ms_d, "ms_per_frame": ms_d,
+                      "roofline": {"kernel": "k_stream_raw (K5, whole push timed)", "bound": "hbm",
+                                   "achieved": dense_bytes / (ms_d / 1e3) / 1e9, "peak": peak,
+                                   "unit": "GB/s",
+                                   "frac": dense_bytes / (ms_d / 1e3) / 1e9 / peak}},
     }
 
 
@@ -305,6 +372,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--no-compressed", action="store_true")
+    ap.add_argument("--no-stream", action="store_true")
+    ap.add_argument("--stream-depth", type=int, default=8192)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -454,6 +523,13 @@ def main():
     if not args.no_compressed:
         line["compressed"] = run_compressed(args, torch, xg, ctx, stream, frames, series, ring,
                                            sizes, mine, world, dev)
+
+    # ---------------------------------------------------------- streaming (C3)
+    if not args.no_stream and world == 1:
+        try:
+            line["streaming"] = run_streaming(args, torch, xg, ctx, stream)
+        except Exception as e:  # keep the main line
+            line["streaming"] = {"failed": str(e)}
 
     # ---------------------------------------------------------- CPU baseline
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
