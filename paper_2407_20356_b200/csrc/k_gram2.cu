@@ -152,9 +152,6 @@ constexpr size_t smem2_bytes() {
 }
 size_t gram2_smem_bytes(int mode) { return mode == 0 ? smem2_bytes<0>() : smem2_bytes<1>(); }
 
-#ifndef XG_G2EXP
-#define XG_G2EXP 0
-#endif
 template <int MODE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THREADS, 1)
     k_gram2(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmOut,
@@ -369,7 +366,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
           }
         }
         const int w = c;  // window of chunks c-1, c
-        if (XG_G2EXP != 2 && p.g2_partial && !(EPI_WARPS == 8 && grp == 1 && w == 4)) {
+        if (p.g2_partial && !(EPI_WARPS == 8 && grp == 1 && w == 4)) {
           const int lagw = td.j0 - i0 + 32 * (w - 1 - sub) + lane + 1;  // this lane's lag
           if (lagw >= 0) {
             const uint32_t* Sp = S + ((c - 1) & 1) * 1024;
@@ -392,7 +389,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
                 if (MODE == 0) {
                   const float g = __fsub_rn(__int_as_float(0x4B000000 | static_cast<int>(wv)),
                                             8388608.f);  // exact for wv < 2^23
-                  const float2 a = ir2[l], b = XG_G2EXP == 1 ? make_float2(1.f, 0.f) : ic2[l];
+                  const float2 a = ir2[l], b = ic2[l];
                   const float ph = __fmul_rn(a.x, b.x);
                   float pe = __fmaf_rn(a.x, b.x, -ph);
                   pe = __fmaf_rn(a.x, b.y, pe);

@@ -2,21 +2,24 @@
 //
 // Replaces the per-ring column gather `apply_mask` (src/model.cpp:42-59) and
 // the norm pass of `row_normalize` (src/linalg.cpp:441-456, the dot at :445):
-// one pass over the raw frames writes every q-ring's pixels (in mask order,
-// i.e. ascending pixel index) into its own 4-byte aligned column range of a
-// frame-major row, and records per (frame, segment) the exact sum of squares
-// and sum of the counts.  K1b (k_norms) folds segments into per-(frame, ring)
-// norms in a fixed order -- no atomics anywhere, so the statistics are exact
-// and deterministic.
+// one pass over the raw frames writes every q-ring's pixels into its own
+// column range of a frame-major row and accumulates the exact |x|^2 of every
+// (frame, ring).  K1b (k_norms) turns those into norms, 1/|x| (f64 and its
+// (hi, lo) float split for the FP32 fused g2) and the zero-frame bookkeeping.
 //
 // HBM-bound (reads M bytes, writes ~M bytes per frame).  A CTA owns one
-// detector band (8192 pixels) and a run of frames: band bytes are
-// streamed into a 4-deep ring of shared-memory buffers by TMA bulk copies
-// (cp.async.bulk + mbarrier: 4 frames in flight per CTA), the band's gather table (u16 source offset
-// per output byte, 0xFFFF = zero padding) stays resident in shared memory,
-// and each warp emits whole ring segments, 4 output bytes per lane per step,
-// as coalesced 128-byte warp stores.  Band pieces of 512 B sit at a 528 B
-// smem pitch so consecutive detector rows do not alias to the same banks.
+// detector band (8192 pixels) and a run of frames.  Warp 8 streams band
+// bytes into a 4-deep ring of shared-memory buffers with TMA bulk copies
+// (cp.async.bulk + full/empty mbarriers); 512-byte pieces sit at a 528-byte
+// pitch so consecutive detector rows land 4 banks apart.  The band's output
+// is a list of segments (one per ring), each = whole source words (all 4
+// pixels in the ring; copied with one bank-conflict-free 32-bit load, the
+// host orders them round-robin over banks) followed by the leftover pixels
+// packed 4 per group (byte gather).  The host cuts every band into 8
+// cost-balanced runs of "pieces" (segment fragments), one per consumer warp;
+// each consumer pass serves two frames, so a table entry and the piece
+// bookkeeping are paid once per two frames.  |x|^2 per piece: __dp4a + warp
+// redux + an integer red.add into the (frame, ring) total (exact, order-free).
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -28,20 +31,8 @@ namespace xg {
 namespace {
 
 constexpr int INGEST_THREADS = 256;
-#ifndef XG_EXP
-#define XG_EXP 0
-#endif
-#ifndef XG_SLEEP
-#define XG_SLEEP 64
-#endif
-#ifndef XG_NBUF
-#define XG_NBUF 4
-#endif
-constexpr int NBUF = XG_NBUF;  // frames in flight per CTA
-#ifndef XG_FR
-#define XG_FR 2
-#endif
-constexpr int FR = XG_FR;      // frames per consumer pass (divides NBUF)
+constexpr int NBUF = 4;  // frames in flight per CTA
+constexpr int FR = 2;    // frames per consumer pass (divides NBUF)
 static_assert(NBUF % FR == 0, "NBUF must be a multiple of FR");
 constexpr int PIECE = INGEST_PIECE, PITCH = INGEST_PITCH;
 
@@ -147,7 +138,7 @@ __global__ void __launch_bounds__(INGEST_THREADS + 32)
           : "r"(smem_addr(bar)), "r"(parity)
           : "memory");
       if (ok) break;
-      __nanosleep(XG_SLEEP);
+      __nanosleep(64);
     }
   };
 

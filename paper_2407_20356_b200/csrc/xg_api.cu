@@ -644,9 +644,7 @@ int xg_series_load_frames(xg_series* s, const uint8_t* frames, int64_t n, int on
   p.t0 = 0;
   p.n_frames = n;
   // one wave of ~4 resident CTAs per SM, each streaming a run of frames of one band
-  static const int ctas_per_sm = getenv("XG_INGEST_CTAS") ? atoi(getenv("XG_INGEST_CTAS")) : 4;
-  const int64_t want =
-      std::max<int64_t>(1, (int64_t)c->num_sms * ctas_per_sm / std::max(1, L->n_bands));
+  const int64_t want = std::max<int64_t>(1, (int64_t)c->num_sms * 4 / std::max(1, L->n_bands));
   p.frames_per_cta = static_cast<int32_t>(std::max<int64_t>(1, (n + want - 1) / want));
   p.norm2 = reinterpret_cast<unsigned long long*>(s->d_norm2);
   XG_CUDA(c, cudaMemsetAsync(s->d_norm2, 0, (size_t)n * L->rings * 8, c->stream));
