@@ -330,6 +330,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
       const uint32_t tbase =
           tmem_base + static_cast<uint32_t>(acc * BN) + (static_cast<uint32_t>(sub * 32) << 16);
       const int out_row = td.ring * p.ld + i0 + 32 * sub;
+      const bool full_cols = td.j0 + BN <= p.n_frames;  // every tile column is a frame
       // Column chunks c (32 wide) go through staging buffer c & 1.  Group 0
       // stores chunks 0..3 and also loads chunk 4 (for window 4); group 1
       // stores 4..7.  Window w spans chunks w-1 and w (64 columns): lane L
@@ -378,6 +379,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
               const float2* ir2 = tail->inv_row2 + 32 * sub;
               const float2* ic2 = tail->inv_col2_ext + 32 * (w - 1) + 32 + lane + 1;
               float sh = 0.f, sl = 0.f;
+              if (MODE == 1 && full_cols) {
+                // every tile column is a frame: plain fp32 sum, no mask
+#pragma unroll
+                for (int l = 0; l < 32; ++l) {
+                  const int cr = lane + 1 + l;
+                  const int kk = cr & 31;
+                  const uint32_t* B = cr < 32 ? Sp : Sc;
+                  const bool zero = cr < 32 ? (w == 0) : !real;
+                  const uint32_t wv =
+                      zero ? 0u : B[l * 32 + (((kk >> 2) ^ (l & 7)) << 2) + (kk & 3)];
+                  sh += __uint_as_float(wv);
+                }
+              } else
 #pragma unroll
               for (int l = 0; l < 32; ++l) {
                 const int cr = lane + 1 + l;  // column within the 64-wide window
