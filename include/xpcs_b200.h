@@ -102,7 +102,11 @@ XG_API int xg_series_load_frames(xg_series* s, const uint8_t* frames, int64_t n_
                           int frames_on_device);
 /* Raw two-time correlation of every ring (ttc_raw, correlate.cpp:19-25):
  * exact u8 x u8 -> int32 Gram on tcgen05 tensor cores, f64 normalisation and
- * g2 (g2_from_ttc, correlate.cpp:67-85) on the device. */
+ * g2 (g2_from_ttc, correlate.cpp:67-85) on the device.  Asynchronous: a
+ * contract violation found on the device (a frame with |x|^2 >= 2^31, which
+ * the int32 Gram cannot hold) is returned as XG_ERR_CONTRACT by the next
+ * synchronising call (any readback, xg_synchronize).  XG_STRICT checks the
+ * zero-frame rule (NormalizationError) before launching. */
 XG_API int xg_ttc_raw(xg_series* s, uint32_t flags);
 /* g2 of every ring from the current raw TTC (run separately after
  * xg_ttc_raw(..., XG_NO_G2)). */

@@ -114,3 +114,57 @@ def test_fused_g2_matches_standalone_pass(ctx, orc):
         assert np.abs(v1 - v2).max() <= 1e-13
         c_ref = orc.ttc_raw(frames[:, ring == r].astype(np.float64))
         assert np.abs(v1 - orc.g2_from_ttc(c_ref)[1]).max() <= 1e-12
+
+
+@pytest.mark.parametrize("t,h,w", [(2, 3, 5), (3, 1, 7), (129, 17, 31), (257, 130, 130)])
+def test_raw_tiny_and_odd_shapes(ctx, orc, t, h, w):
+    """Smallest series (T=2), detectors smaller than one 16-byte vector or not
+    a multiple of 16 pixels (the ingest's non-bulk band copy), single-pixel
+    rings, tile-edge frame counts (T = 128k+1, 256k+1) and band edges."""
+    rng = np.random.default_rng(t + h + w)
+    frames = rng.integers(0, 4, size=(t, h * w), dtype=np.uint8)
+    frames[:, 0] = 1  # ring 0 below has one pixel, keep it nonzero
+    m = h * w
+    masks = [np.array([0]), np.arange(1, m, 2), np.arange(2, m, 2)]
+    masks = [mk for mk in masks if mk.size]
+    lay = xg.RingLayout(ctx, m, masks)
+    s = xg.FrameSeries(lay, t).load(frames).ttc_raw()
+    for r, mk in enumerate(masks):
+        xq = frames[:, mk]
+        assert np.array_equal(s.ttc(r, "gram").astype(np.int64), orc.gram_u8(xq)), f"ring {r}"
+        c = s.ttc(r, "f64")
+        assert np.abs(c - orc.ttc_raw(xq.astype(np.float64))).max() <= 1e-12
+        _, g2, cnt = s.g2(r)
+        _, g2_ref, cnt_ref = orc.g2_from_ttc(orc.ttc_raw(xq.astype(np.float64)))
+        assert np.array_equal(cnt, cnt_ref) and np.abs(g2 - g2_ref).max() <= 1e-12
+
+
+def test_raw_rejects_single_frame_and_bad_masks(ctx):
+    lay = xg.RingLayout(ctx, 16, [np.arange(4)])
+    with pytest.raises(xg.ContractError):
+        xg.FrameSeries(lay, 1).load(np.ones((1, 16), np.uint8)).ttc_raw()
+    with pytest.raises(xg.MaskError):
+        xg.RingLayout(ctx, 16, [np.array([3, 3])])
+    with pytest.raises(xg.MaskError):
+        xg.RingLayout(ctx, 16, [np.array([16])])
+    with pytest.raises(xg.MaskError):
+        xg.RingLayout(ctx, 16, [np.array([], dtype=np.int64)])
+    with pytest.raises(xg.ShapeError):
+        xg.FrameSeries(lay, 4).load(np.ones((5, 16), np.uint8))
+
+
+def test_int32_gram_overflow_is_a_contract_error(ctx):
+    """The exact int32 Gram holds |x|^2 < 2^31 (255^2 * 33025 pixels); a
+    brighter ring is refused with ContractError (SURVEY 8 K2 int32 overflow),
+    never wrapped.  Just below the limit stays exact."""
+    m = 34000
+    lay = xg.RingLayout(ctx, m, [np.arange(m)])
+    hot = np.full((2, m), 255, np.uint8)
+    s = xg.FrameSeries(lay, 2).load(hot)
+    with pytest.raises(xg.ContractError):  # device-detected: raised by the next sync
+        s.ttc_raw()
+        s.ttc(0, "gram")
+    ok = hot.copy()
+    ok[:, 33000:] = 0  # 255^2 * 33000 < 2^31
+    s = xg.FrameSeries(lay, 2).load(ok).ttc_raw()
+    assert s.ttc(0, "gram")[0, 1] == 255 * 255 * 33000
