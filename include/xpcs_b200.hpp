@@ -191,6 +191,21 @@ class Series {
   void load(const uint8_t* frames, int64_t n, bool on_device = false) {
     L_.ctx().check(xg_series_load_frames(h_, frames, n, on_device ? 1 : 0));
   }
+  // The reference's f64 FrameSeries intensities (model.hpp:26-36): accepted
+  // when every value is an integer photon count in [0, 255] (packed to u8
+  // here, exact); anything else is a ContractError, never a silent wrap.
+  void load(const double* intensities, int64_t n, int64_t full_pixels) {
+    std::vector<uint8_t> u8(static_cast<size_t>(n * full_pixels));
+    for (size_t i = 0; i < u8.size(); ++i) {
+      const double v = intensities[i];
+      if (!(v >= 0.0 && v <= 255.0) || v != static_cast<double>(static_cast<int>(v)))
+        throw ContractError("frame intensities must be integer photon counts in [0, 255] for "
+                            "the u8 tensor-core path (value " + std::to_string(v) + " at " +
+                            std::to_string(i) + ")");
+      u8[i] = static_cast<uint8_t>(v);
+    }
+    load(u8.data(), n, false);
+  }
   void ttc_raw(uint32_t flags = 0) { L_.ctx().check(xg_ttc_raw(h_, flags)); }
   void compress(const Basis& b, uint32_t flags = 0) { L_.ctx().check(xg_compress(h_, b.get(), flags)); }
   void ttc_compressed(uint32_t flags = 0) { L_.ctx().check(xg_ttc_compressed(h_, flags)); }

@@ -42,6 +42,23 @@ int main(int argc, char** argv) {
     double sum = 0.0;
     for (double v : g) sum += v;
     std::printf("exact ring 0 sum %.17g\n", sum);
+    // f64 intensities: integral counts load through the u8 path (same C)
+    {
+      std::vector<double> fd(frames.begin(), frames.end());
+      xpcs_b200::Series s2(layout, n);
+      s2.load(fd.data(), n, m);
+      s2.ttc_raw();
+      const auto c0 = s2.ttc(0), c1 = s.ttc(0);
+      std::printf("f64 load %s\n", c0 == c1 ? "equal" : "DIFFERENT");
+      fd[3] = 1.5;
+      try {
+        s2.load(fd.data(), n, m);
+        std::printf("missing ContractError\n");
+        return 1;
+      } catch (const xpcs_b200::ContractError&) {
+        std::printf("ContractError non-integer\n");
+      }
+    }
     try {
       std::vector<double> z(static_cast<size_t>(3 * 4), 1.0);
       for (int p = 0; p < 4; ++p) z[4 + p] = 0.0;

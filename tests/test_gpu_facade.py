@@ -34,4 +34,6 @@ def test_cpp_facade(tmp_path, orc):
     c0 = orc.ttc_raw(frames[:, ring == 0].astype(np.float64))
     # the exact entry returns the reference's bits: same sum up to summation order
     assert abs(float(lines[q].split()[-1]) - float(c0.sum())) <= 1e-12 * c0.size
-    assert lines[q + 1] == "NormalizationError frame 1"
+    assert lines[q + 1] == "f64 load equal"
+    assert lines[q + 2] == "ContractError non-integer"
+    assert lines[q + 3] == "NormalizationError frame 1"
