@@ -37,10 +37,10 @@ constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int TMEM_COLS = 512;
 // K2 (raw, long K loop): 5 stages, 4 epilogue warps (one per TMEM lane
 // quarter).  K4 (compressed, K = 6 x 64): the MMA is short and the epilogue
-// dominates, so 3 stages and 8 epilogue warps (two per lane quarter, each
+// dominates, so 4 stages and 8 epilogue warps (two per lane quarter, each
 // taking half the columns).
 template <int MODE> struct Cfg2 {
-  static constexpr int STAGES = MODE == 0 ? 5 : 3;
+  static constexpr int STAGES = MODE == 0 ? 5 : 4;
   static constexpr int EPI_WARPS = MODE == 0 ? 4 : 8;
   static constexpr int NUM_THREADS = 128 + 32 * EPI_WARPS;
 };
