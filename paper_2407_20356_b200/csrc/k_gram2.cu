@@ -168,6 +168,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
   const uint32_t rank = cta_rank();
   const bool leader = rank == 0;
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  int n_planes = 1;  // K4: bf16 planes the precision pairs touch
+  if (MODE == 1)
+    for (int pr = 0; pr < p.n_pairs; ++pr) {
+      const int pa = (p.pairs >> (4 * pr)) & 3, pb = (p.pairs >> (4 * pr + 2)) & 3;
+      n_planes = max(n_planes, max(pa, pb) + 1);
+    }
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -201,7 +207,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
       for (int t = pair; t < p.ntiles; t += npairs) {
         const TileDesc td = p.tiles[t];
         const int koff = MODE == 0 ? p.ring_koff[td.ring] : 0;
-        const int nkb = MODE == 0 ? p.ring_nkb[td.ring] : p.n_pairs * p.kb_per_plane;
+        // K4: per 64-coefficient block, one stage per bf16 plane (A and B
+        // rows of that plane); the MMA warp forms every precision pair from
+        // the resident planes, so each plane block is fetched once, not once
+        // per pair
+        const int nkb = MODE == 0 ? p.ring_nkb[td.ring] : p.kb_per_plane * n_planes;
         for (int kb = 0; kb < nkb; ++kb) {
           if (!mbar_wait(&tail->empty[stage], phase ^ 1, p.err)) goto producer_done;
           if (leader) mbar_arrive_expect_tx(&tail->full[stage], 2 * STAGE_BYTES);
@@ -211,11 +221,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
             ra = td.i0 + 128 * rank;
             rb = td.j0 + 128 * rank;
           } else {
-            const int pr = kb / p.kb_per_plane;
-            kc = (kb - pr * p.kb_per_plane) * 64;
-            const int pa = (p.pairs >> (4 * pr)) & 3, pb = (p.pairs >> (4 * pr + 2)) & 3;
-            ra = (td.ring * 3 + pa) * p.plane_rows + td.i0 + 128 * rank;
-            rb = (td.ring * 3 + pb) * p.plane_rows + td.j0 + 128 * rank;
+            const int q = kb % n_planes;
+            kc = (kb / n_planes) * 64;
+            ra = (td.ring * 3 + q) * p.plane_rows + td.i0 + 128 * rank;
+            rb = (td.ring * 3 + q) * p.plane_rows + td.j0 + 128 * rank;
           }
           tma_load_2sm(sA + stage * A_BYTES, &tmX, &tail->full[stage], kc, ra);
           tma_load_2sm(sB + stage * B_BYTES, &tmX, &tail->full[stage], kc, rb);
@@ -233,11 +242,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
       uint32_t phase = 0, acc_phase = 0;
       for (int t = pair; t < p.ntiles; t += npairs) {
         const TileDesc td = p.tiles[t];
-        const int nkb = MODE == 0 ? p.ring_nkb[td.ring] : p.n_pairs * p.kb_per_plane;
+        const int nkb = MODE == 0 ? p.ring_nkb[td.ring] : p.kb_per_plane;
         if (!mbar_wait(&tail->tempty[acc], acc_phase ^ 1, p.err)) break;
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + static_cast<uint32_t>(acc * BN);
         bool ok = true;
+        if (MODE == 1) {
+          for (int kb = 0; ok && kb < nkb; ++kb) {
+            int st[3];
+            for (int q = 0; q < n_planes; ++q) {
+              if (!mbar_wait(&tail->full[stage], phase, p.err)) {
+                ok = false;
+                break;
+              }
+              st[q] = stage;
+              if (++stage == STAGES) {
+                stage = 0;
+                phase ^= 1;
+              }
+            }
+            if (!ok) break;
+            tc_fence_after();
+            for (int pr = 0; pr < p.n_pairs; ++pr) {
+              const int pa = (p.pairs >> (4 * pr)) & 3, pb = (p.pairs >> (4 * pr + 2)) & 3;
+              const uint32_t a0 = smem_u32(sA + st[pa] * A_BYTES);
+              const uint32_t b0 = smem_u32(sB + st[pb] * B_BYTES);
+#pragma unroll
+              for (int k = 0; k < BK / 32; ++k)
+                mma2_bf16(tmem_d, sdesc_k128(a0 + k * 32), sdesc_k128(b0 + k * 32), IDESC,
+                          (kb | pr | k) != 0 ? 1u : 0u);
+            }
+            for (int q = 0; q < n_planes; ++q) commit2(&tail->empty[st[q]]);
+          }
+        } else
         for (int kb = 0; kb < nkb; ++kb) {
           if (!mbar_wait(&tail->full[stage], phase, p.err)) {
             ok = false;
