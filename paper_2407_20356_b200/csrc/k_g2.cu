@@ -117,6 +117,10 @@ __global__ void k_expand(ExpandParams p, int src_mode) {
 // the contributing tiles are those with 128 * (2 jb - ib) in [d-255, d+127];
 // they are visited in ascending (delta, ib) order, so the sum order is fixed.
 __global__ void k_g2_fold(G2FoldParams p) {
+  __shared__ int32_t tile_off[257];  // ib_tile_off, staged (nbi <= 256 here)
+  for (int i = threadIdx.x; i <= p.nbi && i < 257; i += blockDim.x) tile_off[i] = p.ib_tile_off[i];
+  __syncthreads();
+  const int32_t* ib_tile_off = p.nbi < 257 ? tile_off : p.ib_tile_off;
   const int64_t d = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int r = blockIdx.y;
   if (d >= p.n_frames) return;
@@ -128,12 +132,13 @@ __global__ void k_g2_fold(G2FoldParams p) {
   for (int64_t delta = dlo; delta <= dhi; ++delta) {
     const int dl = static_cast<int>(d - 128 * delta + 127);
     if (dl < 0 || dl >= 383) continue;
-    int ib = static_cast<int>(((delta % 2) + 2) % 2);  // (delta + ib) even
-    for (; ib < p.nbi; ib += 2) {
+    if (delta < -1) continue;  // jb = (delta + ib) / 2 would fall below ib / 2
+    // (delta + ib) even; jb < nbj  <=>  ib < 2 nbj - delta: a branch-free run
+    const int ib_end = static_cast<int>(min(static_cast<int64_t>(p.nbi), 2 * p.nbj - delta));
+#pragma unroll 4
+    for (int ib = static_cast<int>(delta & 1); ib < ib_end; ib += 2) {
       const int64_t jb = (delta + ib) / 2;
-      if (jb < ib / 2) continue;
-      if (jb >= p.nbj) break;
-      const int64_t tile = p.ib_tile_off[ib] + (jb - ib / 2);
+      const int64_t tile = ib_tile_off[ib] + (jb - ib / 2);
       const float2 v = part[tile * 384 + dl];
       acc += static_cast<double>(v.x) + static_cast<double>(v.y);
     }
