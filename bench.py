@@ -477,10 +477,9 @@ def main():
     g2_out = np.empty(T)
 
     def step_e2e():
-        series.load(host)  # pinned H2D inside
-        series.ttc_raw()
-        for r in range(len(mine)):
-            series.g2(r)  # D2H of g2 values + counts per ring
+        # pinned H2D in chunks, overlapped with ingest + Gram (one public call)
+        series.ttc_raw_host(host)
+        series.g2_all()  # D2H of every ring's g2 values + counts
 
     for _ in range(2):
         step_e2e()

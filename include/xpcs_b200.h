@@ -108,6 +108,11 @@ XG_API int xg_series_load_frames(xg_series* s, const uint8_t* frames, int64_t n_
  * synchronising call (any readback, xg_synchronize).  XG_STRICT checks the
  * zero-frame rule (NormalizationError) before launching. */
 XG_API int xg_ttc_raw(xg_series* s, uint32_t flags);
+/* xg_series_load_frames + xg_ttc_raw for frames in host memory (pinned for
+ * full overlap): chunked H2D on a second stream overlapped with ingest and
+ * the Gram tiles each arrived chunk completes.  Same results. */
+XG_API int xg_series_ttc_raw_host(xg_series* s, const uint8_t* frames, int64_t n_frames,
+                                  uint32_t flags);
 /* g2 of every ring from the current raw TTC (run separately after
  * xg_ttc_raw(..., XG_NO_G2)). */
 XG_API int xg_series_g2(xg_series* s);
@@ -118,6 +123,8 @@ XG_API int xg_series_get_ttc(xg_series* s, int32_t ring, int32_t dtype, void* ou
 /* g2 values (n), counts (n; N-d, or fewer when frames were flagged), lags in
  * frames (multiply by frame_period for seconds). */
 XG_API int xg_series_get_g2(xg_series* s, int32_t ring, double* values, int64_t* counts);
+/* g2 and pair counts of every ring in one transfer: [ring][n_frames] each */
+XG_API int xg_series_get_g2_all(xg_series* s, double* values, int64_t* counts);
 /* f64 frame norms |x_t| of ring (n) and the count of zero-norm frames. */
 XG_API int xg_series_get_norms(xg_series* s, int32_t ring, double* norms, int64_t* n_zero);
 XG_API int64_t xg_series_frames(const xg_series* s);

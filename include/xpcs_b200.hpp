@@ -207,6 +207,10 @@ class Series {
     load(u8.data(), n, false);
   }
   void ttc_raw(uint32_t flags = 0) { L_.ctx().check(xg_ttc_raw(h_, flags)); }
+  // load + ttc_raw for host frames: PCIe transfer overlapped with the compute
+  void ttc_raw_host(const uint8_t* frames, int64_t n, uint32_t flags = 0) {
+    L_.ctx().check(xg_series_ttc_raw_host(h_, frames, n, flags));
+  }
   void compress(const Basis& b, uint32_t flags = 0) { L_.ctx().check(xg_compress(h_, b.get(), flags)); }
   void ttc_compressed(uint32_t flags = 0) { L_.ctx().check(xg_ttc_compressed(h_, flags)); }
   int64_t frames() const { return xg_series_frames(h_); }

@@ -300,6 +300,30 @@ class FrameSeries:
         _check(self.ctx.h, lib.xg_ttc_raw(self.h, flags))
         return self
 
+    def ttc_raw_host(self, frames, strict: bool = False, g2: bool = True) -> "FrameSeries":
+        """load() + ttc_raw() for frames in HOST memory, with the PCIe transfer
+        overlapped with ingest and the Gram (xg_series_ttc_raw_host).  Pass a
+        pinned torch tensor (``pin_memory=True``) for full overlap; numpy
+        arrays work too.  Same results as the two calls."""
+        flags = (_abi.STRICT if strict else 0) | (0 if g2 else _abi.NO_G2)
+        if hasattr(frames, "data_ptr"):
+            if getattr(frames, "is_cuda", False):
+                raise ContractError("ttc_raw_host takes host frames; use load() for device ones")
+            if str(getattr(frames, "dtype", "torch.uint8")) != "torch.uint8":
+                raise ContractError("frames tensor must be uint8 photon counts")
+            n = int(frames.shape[0])
+            if frames.numel() < n * self.layout.full_pixels:
+                raise ShapeError("frames tensor smaller than n x full_pixels")
+            _check(self.ctx.h, lib.xg_series_ttc_raw_host(self.h, C.c_void_p(frames.data_ptr()),
+                                                          n, flags))
+            return self
+        a = _as_counts_u8(frames)
+        if a.ndim != 2 or a.shape[1] != self.layout.full_pixels:
+            raise ShapeError(f"frames must be n x {self.layout.full_pixels}, got {a.shape}")
+        _check(self.ctx.h, lib.xg_series_ttc_raw_host(self.h, _ptr(a), a.shape[0], flags))
+        self._keep = a
+        return self
+
     def compute_g2(self) -> "FrameSeries":
         """g2 of every ring from the current raw TTC (after ttc_raw(g2=False))."""
         _check(self.ctx.h, lib.xg_series_g2(self.h))
@@ -322,6 +346,15 @@ class FrameSeries:
                                                 cnt.ctypes.data_as(_abi.PI64)))
         lags = np.arange(n, dtype=np.float64) * self.frame_period
         return lags, vals, cnt
+
+    def g2_all(self):
+        """(lags, values [ring][n], counts [ring][n]) of every ring, one transfer."""
+        n, q = self.n_frames, self.layout.n_rings
+        vals = np.empty((q, n), np.float64)
+        cnt = np.empty((q, n), np.int64)
+        _check(self.ctx.h, lib.xg_series_get_g2_all(self.h, vals.ctypes.data_as(_abi.PD),
+                                                    cnt.ctypes.data_as(_abi.PI64)))
+        return np.arange(n, dtype=np.float64) * self.frame_period, vals, cnt
 
     # ------------------------------------------------------ compressed path
     def compress(self, basis: "Basis", strict: bool = False) -> "FrameSeries":

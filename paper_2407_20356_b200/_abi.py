@@ -45,9 +45,11 @@ _sigs = {
     "xg_series_destroy": (None, [P]),
     "xg_series_load_frames": (C.c_int, [P, P, I64, C.c_int]),
     "xg_ttc_raw": (C.c_int, [P, U32]),
+    "xg_series_ttc_raw_host": (C.c_int, [P, P, I64, U32]),
     "xg_series_g2": (C.c_int, [P]),
     "xg_series_get_ttc": (C.c_int, [P, I32, I32, P, I64, C.c_int]),
     "xg_series_get_g2": (C.c_int, [P, I32, PD, PI64]),
+    "xg_series_get_g2_all": (C.c_int, [P, PD, PI64]),
     "xg_series_get_norms": (C.c_int, [P, I32, PD, PI64]),
     "xg_series_frames": (I64, [P]),
     "xg_synth_speckle": (C.c_int, [P, I64, I64, I64, I32, C.c_double, I32, C.c_double,

@@ -46,6 +46,8 @@ struct xg_ctx {
   int* d_err = nullptr;  // device error word (pipeline timeouts, overflow)
   int64_t launches = 0;
   PFN_encodeTiled encode = nullptr;
+  cudaStream_t copy_stream = nullptr;    // host -> device copies overlapped with compute
+  std::vector<cudaEvent_t> events;       // chunk-arrival events (reused)
 };
 
 struct xg_layout {
@@ -98,6 +100,8 @@ struct xg_series {
   TileDesc* d_tiles = nullptr;
   TileDesc* d_tiles2 = nullptr;    // 256 x 256 pair tiles
   int32_t ntiles2 = 0;
+  TileDesc* d_tiles2_j = nullptr;  // the same tiles ordered by column block J
+  std::vector<int32_t> tiles2_joff;  // [nbj + 1] offsets of each J in d_tiles2_j
   int32_t ntiles = 0;
   int64_t tiles_for_t = -1;
   size_t g2part_cap = 0;
@@ -295,6 +299,8 @@ void xg_ctx_destroy(xg_ctx* c) {
   cudaSetDevice(c->device);
   if (c->d_err) cudaFree(c->d_err);
   if (c->own_stream) cudaStreamDestroy(c->stream);
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  for (cudaEvent_t ev : c->events) cudaEventDestroy(ev);
   delete c;
 }
 
@@ -597,6 +603,7 @@ void xg_series_destroy(xg_series* s) {
   dfree(s->d_g2pcnt);
   dfree(s->d_tiles);
   dfree(s->d_tiles2);
+  dfree(s->d_tiles2_j);
   dfree(s->d_nz_bits);
   dfree(s->d_g2tile);
   dfree(s->d_ib_tile_off);
@@ -611,21 +618,14 @@ void xg_series_destroy(xg_series* s) {
 
 int64_t xg_series_frames(const xg_series* s) { return s ? s->t : -1; }
 
-int xg_series_load_frames(xg_series* s, const uint8_t* frames, int64_t n, int on_device) {
-  if (!s || !frames) return XG_ERR_INVALID;
+// Ingest frames [t0, t0 + n) from a device raster whose first frame is t0:
+// K1 (ring permutation + |x|^2 per (frame, ring)) and K1b (norms, 1/|x|,
+// zero-frame bookkeeping).  reset_stats() must have run for this series.
+static int ingest_range(xg_series* s, const uint8_t* raster, int64_t t0, int64_t n) {
   xg_ctx* c = s->ctx;
   const xg_layout* L = s->L;
-  if (n < 1 || n > s->tmax)
-    return fail(c, XG_ERR_SHAPE, "load_frames: %lld frames, capacity %lld", (long long)n,
-                (long long)s->tmax);
-  const uint8_t* src = frames;
-  if (!on_device) {
-    XG_CUDA(c, cudaMemcpyAsync(s->d_raster, frames, (size_t)n * L->pixels,
-                               cudaMemcpyHostToDevice, c->stream));
-    src = s->d_raster;
-  }
   IngestParams p;
-  p.raster = src;
+  p.raster = raster;
   p.x = s->d_x;
   p.pixels = L->pixels;
   p.ktot = L->ktot;
@@ -641,19 +641,16 @@ int xg_series_load_frames(xg_series* s, const uint8_t* frames, int64_t n, int on
   p.max_words = L->max_words;
   p.max_bytes = L->max_bytes;
   p.max_band_pieces = L->max_band_pieces;
-  p.t0 = 0;
+  p.t0 = t0;
   p.n_frames = n;
   // one wave of ~4 resident CTAs per SM, each streaming a run of frames of one band
   const int64_t want = std::max<int64_t>(1, (int64_t)c->num_sms * 4 / std::max(1, L->n_bands));
   p.frames_per_cta = static_cast<int32_t>(std::max<int64_t>(1, (n + want - 1) / want));
   p.norm2 = reinterpret_cast<unsigned long long*>(s->d_norm2);
-  XG_CUDA(c, cudaMemsetAsync(s->d_norm2, 0, (size_t)n * L->rings * 8, c->stream));
+  XG_CUDA(c, cudaMemsetAsync(s->d_norm2 + t0 * L->rings, 0, (size_t)n * L->rings * 8, c->stream));
   XG_CUDA(c, launch_ingest(p, c->stream));
-  c->launches++;
-  s->t = n;
-  s->have_raw = false;
   NormParams np;
-  np.t0 = 0;
+  np.t0 = t0;
   np.norm2 = s->d_norm2;
   np.n_frames = n;
   np.ld = s->tp;
@@ -663,17 +660,46 @@ int xg_series_load_frames(xg_series* s, const uint8_t* frames, int64_t n, int on
   np.inv2 = s->d_inv2;
   np.zero_count = s->d_zero;
   np.first_zero = s->d_first_zero;
-  s->nz_words = static_cast<int32_t>((n + 31) / 32);
   np.nz_bits = s->d_nz_bits;
   np.nz_words = s->nz_words;
   np.max_norm2 = reinterpret_cast<unsigned long long*>(s->d_max_norm2);
+  np.err = c->d_err;
+  XG_CUDA(c, launch_norms(np, c->stream));
+  c->launches += 2;
+  return XG_OK;
+}
+
+// Series-wide statistics that the per-range ingests accumulate into.
+static int reset_stats(xg_series* s, int64_t n) {
+  xg_ctx* c = s->ctx;
+  const xg_layout* L = s->L;
+  s->nz_words = static_cast<int32_t>((n + 31) / 32);
   XG_CUDA(c, cudaMemsetAsync(s->d_max_norm2, 0, 8, c->stream));
   XG_CUDA(c, cudaMemsetAsync(s->d_nz_bits, 0, (size_t)L->rings * s->nz_words * 4, c->stream));
-  np.err = c->d_err;
   XG_CUDA(c, cudaMemsetAsync(s->d_zero, 0, (size_t)L->rings * 8, c->stream));
   XG_CUDA(c, cudaMemsetAsync(s->d_first_zero, 0x7F, (size_t)L->rings * 8, c->stream));
-  XG_CUDA(c, launch_norms(np, c->stream));
-  c->launches++;
+  return XG_OK;
+}
+
+int xg_series_load_frames(xg_series* s, const uint8_t* frames, int64_t n, int on_device) {
+  if (!s || !frames) return XG_ERR_INVALID;
+  xg_ctx* c = s->ctx;
+  const xg_layout* L = s->L;
+  if (n < 1 || n > s->tmax)
+    return fail(c, XG_ERR_SHAPE, "load_frames: %lld frames, capacity %lld", (long long)n,
+                (long long)s->tmax);
+  const uint8_t* src = frames;
+  if (!on_device) {
+    XG_CUDA(c, cudaMemcpyAsync(s->d_raster, frames, (size_t)n * L->pixels,
+                               cudaMemcpyHostToDevice, c->stream));
+    src = s->d_raster;
+  }
+  int rc = reset_stats(s, n);
+  if (rc) return rc;
+  rc = ingest_range(s, src, 0, n);
+  if (rc) return rc;
+  s->t = n;
+  s->have_raw = false;
   return XG_OK;
 }
 
@@ -724,23 +750,44 @@ static int build_tiles(xg_series* s) {
   XG_CUDA(c, cudaMemcpy(s->d_tiles2, tiles2.data(), tiles2.size() * sizeof(TileDesc),
                         cudaMemcpyHostToDevice));
   s->ntiles2 = static_cast<int32_t>(tiles2.size());
+  // the same tiles grouped by column block J: a tile needs frames < 256 (J+1)
+  // only, so the host-overlapped path runs group J as soon as those arrive
+  std::vector<TileDesc> byj;
+  s->tiles2_joff.assign(static_cast<size_t>(nbj + 1), 0);
+  for (int64_t J = 0; J < nbj; ++J) {
+    s->tiles2_joff[J] = static_cast<int32_t>(byj.size());
+    for (const TileDesc& d : tiles2)
+      if (d.j0 == J * 256) byj.push_back(d);
+  }
+  s->tiles2_joff[nbj] = static_cast<int32_t>(byj.size());
+  dfree(s->d_tiles2_j);
+  XG_CUDA(c, dalloc(&s->d_tiles2_j, byj.size()));
+  XG_CUDA(c, cudaMemcpy(s->d_tiles2_j, byj.data(), byj.size() * sizeof(TileDesc),
+                        cudaMemcpyHostToDevice));
   s->tiles_for_t = s->t;
   return XG_OK;
 }
 
 // K2/K4 launch: CTA-pair kernel (default) or the 1-CTA kernel (XG_GRAM_1CTA=1).
-static cudaError_t launch_gram_any(xg_series* s, int mode, const CUtensorMap& in,
-                                   const CUtensorMap& out, GramParams gp) {
-  static const bool one_cta = [] {
+static bool gram_one_cta() {
+  static const bool one = [] {
     const char* e = std::getenv("XG_GRAM_1CTA");
     return e && e[0] == '1';
   }();
+  return one;
+}
+
+static cudaError_t launch_gram_any(xg_series* s, int mode, const CUtensorMap& in,
+                                   const CUtensorMap& out, GramParams gp,
+                                   const TileDesc* tiles2 = nullptr, int32_t ntiles2 = -1) {
+  const bool one_cta = gram_one_cta();
   gp.g2_nbi = static_cast<int32_t>((s->t + 127) / 128);
   gp.g2_nbj = static_cast<int32_t>((s->t + 255) / 256);
   if (one_cta) return mode == 0 ? launch_gram_u8(in, out, gp, s->ctx->num_sms, s->ctx->stream)
                                 : launch_gram_cmp(in, out, gp, s->ctx->num_sms, s->ctx->stream);
-  gp.tiles = s->d_tiles2;
-  gp.ntiles = s->ntiles2;
+  gp.tiles = tiles2 ? tiles2 : s->d_tiles2;
+  gp.ntiles = ntiles2 >= 0 ? ntiles2 : s->ntiles2;
+  if (gp.ntiles == 0) return cudaSuccess;
   return mode == 0 ? launch_gram2_u8(in, out, gp, s->ctx->num_sms, s->ctx->stream)
                    : launch_gram2_cmp(in, out, gp, s->ctx->num_sms, s->ctx->stream);
 }
@@ -803,6 +850,32 @@ static int fold_g2(xg_series* s, double* g2, int64_t* cnt) {
   return XG_OK;
 }
 
+// K2 launch parameters and tensor maps of a raw pass over the series.
+static int raw_gram_setup(xg_series* s, bool g2, GramParams& gp, CUtensorMap& map,
+                          CUtensorMap& omap) {
+  xg_ctx* c = s->ctx;
+  const xg_layout* L = s->L;
+  int rc = build_tiles(s);
+  if (rc) return rc;
+  rc = make_map_u8(c, &map, s->d_x, L->ktot, s->t, L->ktot, 128, 128);
+  if (rc) return rc;
+  gp.tiles = s->d_tiles;
+  gp.ntiles = s->ntiles;
+  gp.ring_koff = L->d_ring_koff;
+  gp.ring_nkb = L->d_ring_nkb;
+  gp.gram = reinterpret_cast<uint32_t*>(s->d_gram);
+  gp.ring_stride = s->tp * s->tp;
+  gp.ld = static_cast<int32_t>(s->tp);
+  gp.err = c->d_err;
+  gp.max_norm2 = reinterpret_cast<const unsigned long long*>(s->d_max_norm2);
+  gp.inv = s->d_inv;
+  gp.inv2 = s->d_inv2;
+  gp.inv_ld = s->tp;
+  gp.n_frames = s->t;
+  gp.g2_partial = g2 ? s->d_g2tile : nullptr;
+  return make_map_out32(c, &omap, s->d_gram, s->tp, (int64_t)L->rings * s->tp);
+}
+
 int xg_ttc_raw(xg_series* s, uint32_t flags) {
   if (!s) return XG_ERR_INVALID;
   xg_ctx* c = s->ctx;
@@ -822,32 +895,74 @@ int xg_ttc_raw(xg_series* s, uint32_t flags) {
                     (long long)fz[r], r);
       }
   }
-  int rc = build_tiles(s);
-  if (rc) return rc;
-  CUtensorMap map;
-  rc = make_map_u8(c, &map, s->d_x, L->ktot, s->t, L->ktot, 128, 128);
-  if (rc) return rc;
-  GramParams gp;
-  gp.tiles = s->d_tiles;
-  gp.ntiles = s->ntiles;
-  gp.ring_koff = L->d_ring_koff;
-  gp.ring_nkb = L->d_ring_nkb;
-  gp.gram = reinterpret_cast<uint32_t*>(s->d_gram);
-  gp.ring_stride = s->tp * s->tp;
-  gp.ld = static_cast<int32_t>(s->tp);
-  gp.err = c->d_err;
-  gp.max_norm2 = reinterpret_cast<const unsigned long long*>(s->d_max_norm2);
   const bool g2 = !(flags & XG_NO_G2);
-  gp.inv = s->d_inv;
-  gp.inv2 = s->d_inv2;
-  gp.inv_ld = s->tp;
-  gp.n_frames = s->t;
-  gp.g2_partial = g2 ? s->d_g2tile : nullptr;
-  CUtensorMap omap;
-  rc = make_map_out32(c, &omap, s->d_gram, s->tp, (int64_t)L->rings * s->tp);
+  GramParams gp;
+  CUtensorMap map, omap;
+  int rc = raw_gram_setup(s, g2, gp, map, omap);
   if (rc) return rc;
   XG_CUDA(c, launch_gram_any(s, 0, map, omap, gp));
   c->launches++;
+  if (g2) {
+    rc = fold_g2(s, s->d_g2, s->d_g2cnt);
+    if (rc) return rc;
+  }
+  s->have_raw = true;
+  return XG_OK;
+}
+
+// load_frames + ttc_raw for frames in HOST memory (pinned for full overlap):
+// the frames cross PCIe in chunks on a copy stream while the compute stream
+// ingests each arrived chunk and runs the pair tiles whose columns it
+// completes (a tile of column block J needs frames < 256 (J+1) only), so
+// K1 and K2 hide behind the transfer.  Same results as the two calls.
+int xg_series_ttc_raw_host(xg_series* s, const uint8_t* frames, int64_t n, uint32_t flags) {
+  if (!s || !frames) return XG_ERR_INVALID;
+  xg_ctx* c = s->ctx;
+  const xg_layout* L = s->L;
+  if (n < 1 || n > s->tmax)
+    return fail(c, XG_ERR_SHAPE, "load_frames: %lld frames, capacity %lld", (long long)n,
+                (long long)s->tmax);
+  if (n < 2) return fail(c, XG_ERR_CONTRACT, "ttc_raw: need at least 2 frames");
+  if ((flags & XG_STRICT) || gram_one_cta()) {  // strict needs every frame before the Gram
+    int rc = xg_series_load_frames(s, frames, n, 0);
+    return rc ? rc : xg_ttc_raw(s, flags);
+  }
+  if (!c->copy_stream) XG_CUDA(c, cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+  // ~8 chunks of whole 256-frame column blocks
+  const int64_t nbj = (n + 255) / 256;
+  const int64_t jb_per = std::max<int64_t>(1, (nbj + 7) / 8);
+  const int64_t nchunks = (nbj + jb_per - 1) / jb_per;
+  while ((int64_t)c->events.size() < nchunks + 1) {
+    cudaEvent_t ev;
+    XG_CUDA(c, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    c->events.push_back(ev);
+  }
+  int rc = reset_stats(s, n);
+  if (rc) return rc;
+  s->t = n;
+  s->have_raw = false;
+  const bool g2 = !(flags & XG_NO_G2);
+  GramParams gp;
+  CUtensorMap map, omap;
+  rc = raw_gram_setup(s, g2, gp, map, omap);
+  if (rc) return rc;
+  // the staging raster may still be read by earlier work on the compute stream
+  XG_CUDA(c, cudaEventRecord(c->events[nchunks], c->stream));
+  XG_CUDA(c, cudaStreamWaitEvent(c->copy_stream, c->events[nchunks], 0));
+  for (int64_t k = 0; k < nchunks; ++k) {
+    const int64_t jb0 = k * jb_per, jb1 = std::min(nbj, jb0 + jb_per);
+    const int64_t t0 = jb0 * 256, t1 = std::min(n, jb1 * 256);
+    XG_CUDA(c, cudaMemcpyAsync(s->d_raster + t0 * L->pixels, frames + t0 * L->pixels,
+                               (size_t)(t1 - t0) * L->pixels, cudaMemcpyHostToDevice,
+                               c->copy_stream));
+    XG_CUDA(c, cudaEventRecord(c->events[k], c->copy_stream));
+    XG_CUDA(c, cudaStreamWaitEvent(c->stream, c->events[k], 0));
+    rc = ingest_range(s, s->d_raster + t0 * L->pixels, t0, t1 - t0);
+    if (rc) return rc;
+    const int32_t o0 = s->tiles2_joff[jb0], o1 = s->tiles2_joff[jb1];
+    XG_CUDA(c, launch_gram_any(s, 0, map, omap, gp, s->d_tiles2_j + o0, o1 - o0));
+    c->launches++;
+  }
   if (g2) {
     rc = fold_g2(s, s->d_g2, s->d_g2cnt);
     if (rc) return rc;
@@ -909,6 +1024,21 @@ int xg_series_get_g2(xg_series* s, int32_t ring, double* values, int64_t* counts
   if (counts)
     XG_CUDA(c, cudaMemcpyAsync(counts, s->d_g2cnt + (int64_t)ring * s->tp, (size_t)s->t * 8,
                                cudaMemcpyDeviceToHost, c->stream));
+  XG_CUDA(c, cudaStreamSynchronize(c->stream));
+  return check_device_error(c);
+}
+
+// g2 of every ring in one transfer: values[r * n + d], counts likewise.
+int xg_series_get_g2_all(xg_series* s, double* values, int64_t* counts) {
+  if (!s || !values) return XG_ERR_INVALID;
+  xg_ctx* c = s->ctx;
+  if (!s->have_raw) return fail(c, XG_ERR_CONTRACT, "get_g2: no TTC computed yet");
+  const int64_t n = s->t;
+  XG_CUDA(c, cudaMemcpy2DAsync(values, (size_t)n * 8, s->d_g2, (size_t)s->tp * 8, (size_t)n * 8,
+                               s->L->rings, cudaMemcpyDeviceToHost, c->stream));
+  if (counts)
+    XG_CUDA(c, cudaMemcpy2DAsync(counts, (size_t)n * 8, s->d_g2cnt, (size_t)s->tp * 8,
+                                 (size_t)n * 8, s->L->rings, cudaMemcpyDeviceToHost, c->stream));
   XG_CUDA(c, cudaStreamSynchronize(c->stream));
   return check_device_error(c);
 }

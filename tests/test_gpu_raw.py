@@ -168,3 +168,23 @@ def test_int32_gram_overflow_is_a_contract_error(ctx):
     ok[:, 33000:] = 0  # 255^2 * 33000 < 2^31
     s = xg.FrameSeries(lay, 2).load(ok).ttc_raw()
     assert s.ttc(0, "gram")[0, 1] == 255 * 255 * 33000
+
+
+def test_host_overlapped_path_equals_two_calls(ctx, orc):
+    """ttc_raw_host (chunked H2D overlapped with ingest and per-column-block
+    Gram launches) gives bitwise the same Gram, C and g2 as load + ttc_raw."""
+    t, h, w, q = 1300, 40, 40, 3
+    frames, ring = _data(orc, t, h, w, q, 0.3, 41)
+    lay = xg.RingLayout.from_ring_map(ctx, ring, q)
+    a = xg.FrameSeries(lay, t).load(frames).ttc_raw()
+    b = xg.FrameSeries(lay, t).ttc_raw_host(frames)
+    for r in range(q):
+        assert np.array_equal(a.ttc(r, "gram"), b.ttc(r, "gram"))
+        assert np.array_equal(a.ttc(r, "f64"), b.ttc(r, "f64"))
+        _, ga, ca = a.g2(r)
+        _, gb, cb = b.g2(r)
+        assert np.array_equal(ga, gb) and np.array_equal(ca, cb)
+    _, gall, call = b.g2_all()
+    for r in range(q):
+        _, gr, cr = b.g2(r)
+        assert np.array_equal(gall[r], gr) and np.array_equal(call[r], cr)
