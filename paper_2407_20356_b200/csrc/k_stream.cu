@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(128) k_stream_ingest(StreamParams p) {
 constexpr int SS_THREADS = 256;
 constexpr int SS_S = 8;             // history frames per thread
 constexpr int SS_CHUNK = 1024;
-constexpr int SS_Z = 4;
+constexpr int SS_Z = 8;
 __global__ void __launch_bounds__(SS_THREADS) k_stream_sparse_col(StreamParams p) {
   __shared__ int32_t sc[SS_CHUNK];
   __shared__ uint32_t sv[SS_CHUNK];
@@ -266,8 +266,8 @@ __global__ void __launch_bounds__(SS_THREADS) k_stream_sparse_col(StreamParams p
     __syncthreads();
     if (s0 <= p.t) {
       const uint8_t* h = p.hist + s0;
-      // latency-bound on the scattered history rows: keep 8 loads in flight
-#pragma unroll 8
+      // latency-bound on the scattered history rows: keep 16 loads in flight
+#pragma unroll 16
       for (int i = 0; i < cn; ++i) {
         const uint2 w = __ldcs(reinterpret_cast<const uint2*>(h + static_cast<int64_t>(sc[i]) * p.hp));
         const uint32_t v = sv[i];
