@@ -62,6 +62,10 @@ typedef enum xg_dtype { XG_F64 = 0, XG_F32 = 1, XG_I32_GRAM = 2 } xg_dtype;
 #define XG_CMP_BF16 0x4u    /* compressed Gram from the bf16 coefficients only
                               (one product; ~1e-2 relative) instead of the
                               bf16x3 split (6 products; ~1e-6 relative) */
+#define XG_NO_STORE 0x8u    /* g2 only: the TTC tiles never leave the chip (no
+                              Q x T x T buffer is allocated or written; TTC
+                              readback then fails) -- series whose TTC outgrows
+                              HBM */
 
 typedef struct xg_ctx xg_ctx;
 typedef struct xg_layout xg_layout;

@@ -294,18 +294,22 @@ class FrameSeries:
         self._keep = a
         return self
 
-    def ttc_raw(self, strict: bool = False, g2: bool = True) -> "FrameSeries":
-        """Raw TTC of every ring (ttc_raw, correlate.cpp:19-25)."""
-        flags = (_abi.STRICT if strict else 0) | (0 if g2 else _abi.NO_G2)
+    def ttc_raw(self, strict: bool = False, g2: bool = True, store: bool = True) -> "FrameSeries":
+        """Raw TTC of every ring (ttc_raw, correlate.cpp:19-25).  store=False
+        keeps only g2 (the TTC tiles never leave the chip)."""
+        flags = ((_abi.STRICT if strict else 0) | (0 if g2 else _abi.NO_G2)
+                 | (0 if store else _abi.NO_STORE))
         _check(self.ctx.h, lib.xg_ttc_raw(self.h, flags))
         return self
 
-    def ttc_raw_host(self, frames, strict: bool = False, g2: bool = True) -> "FrameSeries":
+    def ttc_raw_host(self, frames, strict: bool = False, g2: bool = True,
+                     store: bool = True) -> "FrameSeries":
         """load() + ttc_raw() for frames in HOST memory, with the PCIe transfer
         overlapped with ingest and the Gram (xg_series_ttc_raw_host).  Pass a
         pinned torch tensor (``pin_memory=True``) for full overlap; numpy
         arrays work too.  Same results as the two calls."""
-        flags = (_abi.STRICT if strict else 0) | (0 if g2 else _abi.NO_G2)
+        flags = ((_abi.STRICT if strict else 0) | (0 if g2 else _abi.NO_G2)
+                 | (0 if store else _abi.NO_STORE))
         if hasattr(frames, "data_ptr"):
             if getattr(frames, "is_cuda", False):
                 raise ContractError("ttc_raw_host takes host frames; use load() for device ones")
@@ -363,10 +367,13 @@ class FrameSeries:
         self.k = basis.k
         return self
 
-    def ttc_compressed(self, mode: str = "f32", g2: bool = True) -> "FrameSeries":
+    def ttc_compressed(self, mode: str = "f32", g2: bool = True,
+                       store: bool = True) -> "FrameSeries":
         """Homomorphic TTC C~ = Y Y^T of every ring (ttc_compressed,
-        correlate.cpp:27-35). mode 'f32' (bf16x3 split, ~1e-6) or 'bf16'."""
-        flags = (_abi.CMP_BF16 if mode == "bf16" else 0) | (0 if g2 else _abi.NO_G2)
+        correlate.cpp:27-35). mode 'f32' (bf16x3 split, ~1e-6) or 'bf16';
+        store=False keeps only g2."""
+        flags = ((_abi.CMP_BF16 if mode == "bf16" else 0) | (0 if g2 else _abi.NO_G2)
+                 | (0 if store else _abi.NO_STORE))
         _check(self.ctx.h, lib.xg_ttc_compressed(self.h, flags))
         return self
 

@@ -113,6 +113,7 @@ F64, F32, I32_GRAM = 0, 1, 2
 STRICT = 0x1
 NO_G2 = 0x2
 CMP_BF16 = 0x4
+NO_STORE = 0x8
 STREAM_STORE_TTC = 0x1
 STREAM_NO_RAW = 0x2
 STREAM_SPARSE = 0x4

@@ -238,7 +238,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               make_uint4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
         fence_proxy_async();  // generic-proxy smem writes -> visible to the TMA engine
         __syncwarp();
-        if (lane == 0) {
+        if (lane == 0 && p.store) {
           asm volatile(
               "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
                   reinterpret_cast<uint64_t>(&tmOut)),

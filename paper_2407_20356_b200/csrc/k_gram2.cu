@@ -394,7 +394,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
                 make_uint4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
           fence_proxy_async();
           __syncwarp();
-          if (lane == 0 && (EPI_WARPS == 4 || (grp ? c >= 4 : c < 4))) {
+          if (lane == 0 && p.store && (EPI_WARPS == 4 || (grp ? c >= 4 : c < 4))) {
             asm volatile(
                 "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
                     reinterpret_cast<uint64_t>(&tmOut)),

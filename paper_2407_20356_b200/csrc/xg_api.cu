@@ -106,6 +106,7 @@ struct xg_series {
   int64_t tiles_for_t = -1;
   size_t g2part_cap = 0;
   bool have_raw = false;
+  bool raw_stored = false, cmp_stored = false;  // TTC tiles written (not XG_NO_STORE)
   // compressed path (allocated on first xg_compress)
   int32_t ck = 0, ckp = 0;         // rank and plane row length of the last compress
   double* d_y = nullptr;           // [ring][tp][k] coefficients
@@ -565,7 +566,6 @@ int xg_series_create(xg_ctx* c, const xg_layout* L, int64_t max_frames, xg_serie
       (e = dalloc(&s->d_zero, (size_t)Q)) != cudaSuccess ||
       (e = dalloc(&s->d_first_zero, (size_t)Q)) != cudaSuccess ||
       (e = dalloc(&s->d_max_norm2, (size_t)1)) != cudaSuccess ||
-      (e = dalloc(&s->d_gram, (size_t)Q * s->tp * s->tp)) != cudaSuccess ||
       (e = dalloc(&s->d_g2, (size_t)Q * s->tp)) != cudaSuccess ||
       (e = dalloc(&s->d_g2cnt, (size_t)Q * s->tp)) != cudaSuccess ||
       (e = dalloc(&s->d_g2part, (size_t)Q * 8 * s->tp)) != cudaSuccess ||
@@ -851,10 +851,12 @@ static int fold_g2(xg_series* s, double* g2, int64_t* cnt) {
 }
 
 // K2 launch parameters and tensor maps of a raw pass over the series.
-static int raw_gram_setup(xg_series* s, bool g2, GramParams& gp, CUtensorMap& map,
+static int raw_gram_setup(xg_series* s, bool g2, bool store, GramParams& gp, CUtensorMap& map,
                           CUtensorMap& omap) {
   xg_ctx* c = s->ctx;
   const xg_layout* L = s->L;
+  if (store && !s->d_gram)  // the Q x T x T int32 TTC, allocated on first use
+    XG_CUDA(c, dalloc(&s->d_gram, (size_t)L->rings * s->tp * s->tp));
   int rc = build_tiles(s);
   if (rc) return rc;
   rc = make_map_u8(c, &map, s->d_x, L->ktot, s->t, L->ktot, 128, 128);
@@ -873,6 +875,10 @@ static int raw_gram_setup(xg_series* s, bool g2, GramParams& gp, CUtensorMap& ma
   gp.inv_ld = s->tp;
   gp.n_frames = s->t;
   gp.g2_partial = g2 ? s->d_g2tile : nullptr;
+  gp.store = store ? 1 : 0;
+  s->raw_stored = store;
+  if (!store)  // a valid (never written) map over the frames buffer
+    return make_map_out32(c, &omap, s->d_x, 32, 32);
   return make_map_out32(c, &omap, s->d_gram, s->tp, (int64_t)L->rings * s->tp);
 }
 
@@ -898,7 +904,7 @@ int xg_ttc_raw(xg_series* s, uint32_t flags) {
   const bool g2 = !(flags & XG_NO_G2);
   GramParams gp;
   CUtensorMap map, omap;
-  int rc = raw_gram_setup(s, g2, gp, map, omap);
+  int rc = raw_gram_setup(s, g2, !(flags & XG_NO_STORE), gp, map, omap);
   if (rc) return rc;
   XG_CUDA(c, launch_gram_any(s, 0, map, omap, gp));
   c->launches++;
@@ -944,7 +950,7 @@ int xg_series_ttc_raw_host(xg_series* s, const uint8_t* frames, int64_t n, uint3
   const bool g2 = !(flags & XG_NO_G2);
   GramParams gp;
   CUtensorMap map, omap;
-  rc = raw_gram_setup(s, g2, gp, map, omap);
+  rc = raw_gram_setup(s, g2, !(flags & XG_NO_STORE), gp, map, omap);
   if (rc) return rc;
   // the staging raster may still be read by earlier work on the compute stream
   XG_CUDA(c, cudaEventRecord(c->events[nchunks], c->stream));
@@ -974,6 +980,7 @@ int xg_series_ttc_raw_host(xg_series* s, const uint8_t* frames, int64_t n, uint3
 int xg_series_g2(xg_series* s) {
   if (!s) return XG_ERR_INVALID;
   if (!s->have_raw) return fail(s->ctx, XG_ERR_CONTRACT, "g2: no TTC computed yet");
+  if (!s->raw_stored) return fail(s->ctx, XG_ERR_CONTRACT, "g2: TTC computed with XG_NO_STORE");
   return run_g2(s, 0);
 }
 
@@ -983,6 +990,7 @@ int xg_series_get_ttc(xg_series* s, int32_t ring, int32_t dtype, void* out, int6
   xg_ctx* c = s->ctx;
   if (ring < 0 || ring >= s->L->rings) return fail(c, XG_ERR_SHAPE, "ring %d out of range", ring);
   if (!s->have_raw) return fail(c, XG_ERR_CONTRACT, "get_ttc: no TTC computed yet");
+  if (!s->raw_stored) return fail(c, XG_ERR_CONTRACT, "get_ttc: computed with XG_NO_STORE");
   if (dtype < 0 || dtype > 2) return fail(c, XG_ERR_CONTRACT, "get_ttc: bad dtype");
   if (ld < s->t) return fail(c, XG_ERR_SHAPE, "get_ttc: ld < n");
   const size_t esz = dtype == 0 ? 8 : 4;
@@ -1258,11 +1266,12 @@ int xg_ttc_compressed(xg_series* s, uint32_t flags) {
   const xg_layout* L = s->L;
   if (!s->have_y) return fail(c, XG_ERR_CONTRACT, "ttc_compressed: compress first");
   if (s->t < 2) return fail(c, XG_ERR_CONTRACT, "ttc_compressed: need at least 2 frames");
-  if (!s->d_cgram) {
-    XG_CUDA(c, dalloc(&s->d_cgram, (size_t)L->rings * s->tp * s->tp));
+  const bool store = !(flags & XG_NO_STORE);
+  if (!s->d_cg2) {
     XG_CUDA(c, dalloc(&s->d_cg2, (size_t)L->rings * s->tp));
     XG_CUDA(c, dalloc(&s->d_cg2cnt, (size_t)L->rings * s->tp));
   }
+  if (store && !s->d_cgram) XG_CUDA(c, dalloc(&s->d_cgram, (size_t)L->rings * s->tp * s->tp));
   int rc = build_tiles(s);
   if (rc) return rc;
   CUtensorMap my;
@@ -1295,8 +1304,11 @@ int xg_ttc_compressed(xg_series* s, uint32_t flags) {
   }
   gp.kb_per_plane = s->ckp / 64;
   gp.plane_rows = static_cast<int32_t>(s->tp);
+  gp.store = store ? 1 : 0;
+  s->cmp_stored = store;
   CUtensorMap omap;
-  rc = make_map_out32(c, &omap, s->d_cgram, s->tp, (int64_t)L->rings * s->tp);
+  rc = store ? make_map_out32(c, &omap, s->d_cgram, s->tp, (int64_t)L->rings * s->tp)
+             : make_map_out32(c, &omap, s->d_x, 32, 32);
   if (rc) return rc;
   XG_CUDA(c, launch_gram_any(s, 1, my, omap, gp));
   c->launches++;
@@ -1329,6 +1341,7 @@ int xg_series_get_cttc(xg_series* s, int32_t ring, int32_t dtype, void* out, int
   xg_ctx* c = s->ctx;
   if (ring < 0 || ring >= s->L->rings) return fail(c, XG_ERR_SHAPE, "ring %d out of range", ring);
   if (!s->have_cttc) return fail(c, XG_ERR_CONTRACT, "get_cttc: no compressed TTC yet");
+  if (!s->cmp_stored) return fail(c, XG_ERR_CONTRACT, "get_cttc: computed with XG_NO_STORE");
   if (dtype != XG_F64 && dtype != XG_F32) return fail(c, XG_ERR_CONTRACT, "get_cttc: bad dtype");
   if (ld < s->t) return fail(c, XG_ERR_SHAPE, "get_cttc: ld < n");
   const size_t bytes = (size_t)s->t * ld * (dtype == XG_F64 ? 8 : 4);

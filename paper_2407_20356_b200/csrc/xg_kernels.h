@@ -105,6 +105,7 @@ struct GramParams {
   int64_t inv_ld;
   int64_t n_frames;
   float2* g2_partial;        // [ntiles][384] (hi, lo) double-float diagonal sums
+  int32_t store;             // 0: g2 only, the TTC tiles are not written
   // compressed mode (launch_gram_cmp): K blocks run over precision pairs
   // (plane_a, plane_b) packed 4 bits each in `pairs`, kb_per_plane 64-element
   // blocks per plane; plane rows of ring r, plane s start at (3r+s)*plane_rows

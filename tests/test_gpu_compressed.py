@@ -101,3 +101,19 @@ def test_full_rank_homomorphic_identity(ctx, orc):
     s.compress(basis).ttc_compressed()
     c_raw = s.ttc(0)
     assert np.abs(s.cttc(0) - c_raw).max() <= 1e-5
+
+
+def test_compressed_g2_only_mode(ctx, orc):
+    t, h, w, q, k = 300, 48, 48, 2, 16
+    frames = orc.gen_speckle(t, h, w, q, 0.4, 52)
+    ring, _ = orc.ring_map(h, w, q)
+    lay = xg.RingLayout.from_ring_map(ctx, ring, q)
+    basis = xg.Basis(lay, k)
+    for r in range(q):
+        basis.set_ring(r, _basis(orc, frames[:, ring == r], k, 70 + r))
+    a = xg.FrameSeries(lay, t).load(frames).compress(basis).ttc_compressed()
+    b = xg.FrameSeries(lay, t).load(frames).compress(basis).ttc_compressed(store=False)
+    for r in range(q):
+        assert np.array_equal(a.cg2(r)[1], b.cg2(r)[1])
+    with pytest.raises(xg.ContractError):
+        b.cttc(0)

@@ -188,3 +188,19 @@ def test_host_overlapped_path_equals_two_calls(ctx, orc):
     for r in range(q):
         _, gr, cr = b.g2(r)
         assert np.array_equal(gall[r], gr) and np.array_equal(call[r], cr)
+
+
+def test_g2_only_mode_equals_stored_mode(ctx, orc):
+    """store=False (XG_NO_STORE): the fused g2 without writing any TTC tile
+    equals the stored run's g2 bitwise; TTC readback is refused."""
+    t, h, w, q = 400, 40, 40, 3
+    frames, ring = _data(orc, t, h, w, q, 0.2, 51)
+    lay = xg.RingLayout.from_ring_map(ctx, ring, q)
+    a = xg.FrameSeries(lay, t).load(frames).ttc_raw()
+    b = xg.FrameSeries(lay, t).load(frames).ttc_raw(store=False)
+    for r in range(q):
+        _, ga, ca = a.g2(r)
+        _, gb, cb = b.g2(r)
+        assert np.array_equal(ga, gb) and np.array_equal(ca, cb)
+    with pytest.raises(xg.ContractError):
+        b.ttc(0)
