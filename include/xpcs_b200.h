@@ -62,6 +62,7 @@ typedef enum xg_dtype { XG_F64 = 0, XG_F32 = 1, XG_I32_GRAM = 2 } xg_dtype;
 #define XG_CMP_BF16 0x4u    /* compressed Gram from the bf16 coefficients only
                               (one product; ~1e-2 relative) instead of the
                               bf16x3 split (6 products; ~1e-6 relative) */
+#define XG_CHUNK_FIRST 0x10u /* xg_series_compress_chunk: first chunk of a series */
 #define XG_NO_STORE 0x8u    /* g2 only: the TTC tiles never leave the chip (no
                               Q x T x T buffer is allocated or written; TTC
                               readback then fails) -- series whose TTC outgrows
@@ -99,6 +100,11 @@ XG_API int64_t xg_layout_ring_pixels(const xg_layout* layout, int32_t ring);
 /* ---- batch series (FrameSeries + TTC per ring) ------------------------ */
 XG_API int xg_series_create(xg_ctx* ctx, const xg_layout* layout, int64_t max_frames,
                      xg_series** out);
+/* A series of up to max_frames whose ring-major frame buffer holds only
+ * x_frames (<= max_frames): for series larger than HBM, frames are fed in
+ * chunks through xg_series_compress_chunk (compressed path only). */
+XG_API int xg_series_create2(xg_ctx* ctx, const xg_layout* layout, int64_t max_frames,
+                             int64_t x_frames, xg_series** out);
 XG_API void xg_series_destroy(xg_series* s);
 /* frames: n_frames x full_pixels u8 photon counts (raster order).  Ingest:
  * [H2D] + ring permutation + per-(frame, ring) statistics. */
@@ -163,6 +169,11 @@ XG_API int xg_basis_create(xg_ctx* ctx, const xg_layout* layout, int32_t k, int3
 XG_API void xg_basis_destroy(xg_basis* basis);
 XG_API int xg_basis_set_ring(xg_basis* basis, int32_t ring, const double* v);
 XG_API int xg_compress(xg_series* s, const xg_basis* basis, uint32_t flags);
+/* Append n frames (u8 raster) to a chunked series and compress them:
+ * series rows [t, t + n) get norms, coefficients and bf16 planes; the frames
+ * themselves are not kept.  XG_CHUNK_FIRST starts a new series. */
+XG_API int xg_series_compress_chunk(xg_series* s, const xg_basis* basis, const uint8_t* frames,
+                                    int64_t n_frames, int frames_on_device, uint32_t flags);
 XG_API int xg_ttc_compressed(xg_series* s, uint32_t flags);
 /* coefficients (n x k, f64) and norms (n) of one ring */
 XG_API int xg_series_get_coeffs(xg_series* s, int32_t ring, double* y, double* norms);

@@ -253,7 +253,11 @@ class FrameSeries:
     q-ring (the reference's ``FrameSeries`` + ``apply_mask`` per ring,
     model.hpp:26-40).  Frames are u8 counts in raster order."""
 
-    def __init__(self, layout: RingLayout, max_frames: int, frame_period: float = 1.0):
+    def __init__(self, layout: RingLayout, max_frames: int, frame_period: float = 1.0,
+                 x_frames: int | None = None):
+        """``x_frames`` < max_frames: the frame buffer holds only that many
+        frames; feed the series with compress_chunk() (compressed path only)
+        -- for series larger than HBM."""
         if not (frame_period > 0.0):
             raise ContractError("frame_period must be positive and finite")
         self.layout = layout
@@ -261,8 +265,8 @@ class FrameSeries:
         self.max_frames = int(max_frames)
         self.frame_period = float(frame_period)
         h = C.c_void_p()
-        _check(self.ctx.h, lib.xg_series_create(self.ctx.h, layout.h, self.max_frames,
-                                                C.byref(h)))
+        _check(self.ctx.h, lib.xg_series_create2(self.ctx.h, layout.h, self.max_frames,
+                                                 int(x_frames or max_frames), C.byref(h)))
         self.h = h
 
     def __del__(self):
@@ -364,6 +368,28 @@ class FrameSeries:
     def compress(self, basis: "Basis", strict: bool = False) -> "FrameSeries":
         """Rank-k projection of every ring (compress_series, compress.cpp:48-81)."""
         _check(self.ctx.h, lib.xg_compress(self.h, basis.h, _abi.STRICT if strict else 0))
+        self.k = basis.k
+        return self
+
+    def compress_chunk(self, basis: "Basis", frames, first: bool = False,
+                       strict: bool = False) -> "FrameSeries":
+        """Append a chunk of frames and compress it (xg_series_compress_chunk):
+        norms, coefficients and planes land at the next series rows; the
+        frames are not kept.  ``first`` starts a new series."""
+        flags = (_abi.CHUNK_FIRST if first else 0) | (_abi.STRICT if strict else 0)
+        if hasattr(frames, "data_ptr"):
+            if str(getattr(frames, "dtype", "torch.uint8")) != "torch.uint8":
+                raise ContractError("frames tensor must be uint8 photon counts")
+            n = int(frames.shape[0])
+            on_dev = 1 if getattr(frames, "is_cuda", False) else 0
+            _check(self.ctx.h, lib.xg_series_compress_chunk(
+                self.h, basis.h, C.c_void_p(frames.data_ptr()), n, on_dev, flags))
+        else:
+            a = _as_counts_u8(frames)
+            if a.ndim != 2 or a.shape[1] != self.layout.full_pixels:
+                raise ShapeError(f"frames must be n x {self.layout.full_pixels}, got {a.shape}")
+            _check(self.ctx.h, lib.xg_series_compress_chunk(self.h, basis.h, _ptr(a), a.shape[0],
+                                                            0, flags))
         self.k = basis.k
         return self
 

@@ -42,6 +42,7 @@ _sigs = {
     "xg_layout_destroy": (None, [P]),
     "xg_layout_ring_pixels": (I64, [P, I32]),
     "xg_series_create": (C.c_int, [P, P, I64, C.POINTER(P)]),
+    "xg_series_create2": (C.c_int, [P, P, I64, I64, C.POINTER(P)]),
     "xg_series_destroy": (None, [P]),
     "xg_series_load_frames": (C.c_int, [P, P, I64, C.c_int]),
     "xg_ttc_raw": (C.c_int, [P, U32]),
@@ -78,6 +79,7 @@ _sigs = {
     "xg_basis_destroy": (None, [P]),
     "xg_basis_set_ring": (C.c_int, [P, I32, PD]),
     "xg_compress": (C.c_int, [P, P, U32]),
+    "xg_series_compress_chunk": (C.c_int, [P, P, P, I64, C.c_int, U32]),
     "xg_ttc_compressed": (C.c_int, [P, U32]),
     "xg_series_get_coeffs": (C.c_int, [P, I32, PD, PD]),
     "xg_series_get_cttc": (C.c_int, [P, I32, I32, P, I64, C.c_int]),
@@ -114,6 +116,7 @@ STRICT = 0x1
 NO_G2 = 0x2
 CMP_BF16 = 0x4
 NO_STORE = 0x8
+CHUNK_FIRST = 0x10
 STREAM_STORE_TTC = 0x1
 STREAM_NO_RAW = 0x2
 STREAM_SPARSE = 0x4

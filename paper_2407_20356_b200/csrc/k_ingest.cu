@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(INGEST_THREADS + 32)
       if (f < nfr) wait(&full[slot + f], static_cast<uint32_t>(((i + f) / NBUF) & 1));
       band_s[f] = bufs_s + (slot + ff) * bstride;
       const int64_t t = p.t0 + f_begin + i + ff;
-      xrow[f] = p.x + t * p.ktot;
+      xrow[f] = p.x + (t - p.x_row0) * p.ktot;
       nrow[f] = p.norm2 + t * p.n_rings;
       asm volatile("" : "+l"(xrow[f]), "+l"(nrow[f]));  // once per frame, not per piece
     }

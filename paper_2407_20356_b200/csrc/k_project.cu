@@ -182,9 +182,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       ok = __all_sync(0xffffffffu, ok);
       if (!ok) break;
       tc_fence_after();
-      const int64_t frame = td.i0 + row;
+      const int64_t frame = td.i0 + row;  // row of x; series frame p.t0 + frame
       const bool live = frame < p.n_frames;
-      const double inv = live ? p.inv[static_cast<int64_t>(td.ring) * p.inv_ld + frame] : 0.0;
+      const double inv =
+          live ? p.inv[static_cast<int64_t>(td.ring) * p.inv_ld + p.t0 + frame] : 0.0;
       const uint32_t tbase =
           tmem_base + static_cast<uint32_t>(acc * 256) + (static_cast<uint32_t>(sub * 32) << 16);
       const double* scale = p.scale + static_cast<int64_t>(td.ring) * p.k;
@@ -241,8 +242,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         __syncwarp();
         if (p.planes && lane == 0) {
-          const int row0 = static_cast<int>((static_cast<int64_t>(td.ring) * 3) * p.plane_rows) +
-                           td.i0 + 32 * sub;
+          const int row0 = static_cast<int>((static_cast<int64_t>(td.ring) * 3) * p.plane_rows +
+                                            p.t0) + td.i0 + 32 * sub;
 #pragma unroll
           for (int q = 0; q < 3; ++q)
             asm volatile(
@@ -260,7 +261,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const int r = 2 * it + (lane >> 4);
           const int64_t f = td.i0 + 32 * sub + r;
           if (f < p.n_frames && j0 + c < p.k)
-            p.y[(static_cast<int64_t>(td.ring) * p.y_ld + f) * p.k + j0 + c] = es->y[r * 17 + c];
+            p.y[(static_cast<int64_t>(td.ring) * p.y_ld + p.t0 + f) * p.k + j0 + c] = es->y[r * 17 + c];
         }
         __syncwarp();  // es->y is rewritten by the next chunk
       }

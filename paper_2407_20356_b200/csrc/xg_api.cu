@@ -107,6 +107,8 @@ struct xg_series {
   size_t g2part_cap = 0;
   bool have_raw = false;
   bool raw_stored = false, cmp_stored = false;  // TTC tiles written (not XG_NO_STORE)
+  int64_t xmax = 0;    // frames the ring-major buffer holds (= tmax unless chunked)
+  int64_t x_row0 = 0;  // series frame index of ring-major row 0  // TTC tiles written (not XG_NO_STORE)
   // compressed path (allocated on first xg_compress)
   int32_t ck = 0, ckp = 0;         // rank and plane row length of the last compress
   double* d_y = nullptr;           // [ring][tp][k] coefficients
@@ -547,18 +549,26 @@ int64_t xg_layout_ring_pixels(const xg_layout* L, int32_t ring) {
 
 // ------------------------------------------------------------------ series
 int xg_series_create(xg_ctx* c, const xg_layout* L, int64_t max_frames, xg_series** out) {
+  return xg_series_create2(c, L, max_frames, max_frames, out);
+}
+
+int xg_series_create2(xg_ctx* c, const xg_layout* L, int64_t max_frames, int64_t x_frames,
+                      xg_series** out) {
   if (!c || !L || !out) return XG_ERR_INVALID;
   *out = nullptr;
   if (max_frames < 2) return fail(c, XG_ERR_CONTRACT, "series: need at least 2 frames");
+  if (x_frames < 1 || x_frames > max_frames)
+    return fail(c, XG_ERR_CONTRACT, "series: x_frames must be in [1, max_frames]");
   xg_series* s = new xg_series();
   s->ctx = c;
   s->L = L;
   s->tmax = max_frames;
+  s->xmax = x_frames;
   s->tp = round_up(max_frames, 256);
   const int64_t Q = L->rings;
   cudaError_t e = cudaSuccess;
-  if ((e = dalloc(&s->d_raster, (size_t)max_frames * L->pixels)) != cudaSuccess ||
-      (e = dalloc(&s->d_x, (size_t)max_frames * L->ktot)) != cudaSuccess ||
+  if ((e = dalloc(&s->d_raster, (size_t)x_frames * L->pixels)) != cudaSuccess ||
+      (e = dalloc(&s->d_x, (size_t)x_frames * L->ktot)) != cudaSuccess ||
       (e = dalloc(&s->d_norm2, (size_t)max_frames * Q)) != cudaSuccess ||
       (e = dalloc(&s->d_norms, (size_t)s->tp * Q)) != cudaSuccess ||
       (e = dalloc(&s->d_inv, (size_t)s->tp * Q)) != cudaSuccess ||
@@ -576,7 +586,7 @@ int xg_series_create(xg_ctx* c, const xg_layout* L, int64_t max_frames, xg_serie
   }
   s->g2part_cap = (size_t)Q * 8 * s->tp;
   // padding columns of the ring-major rows must stay zero forever
-  e = cudaMemsetAsync(s->d_x, 0, (size_t)max_frames * L->ktot, c->stream);
+  e = cudaMemsetAsync(s->d_x, 0, (size_t)x_frames * L->ktot, c->stream);
   if (e != cudaSuccess) {
     xg_series_destroy(s);
     return cuda_fail(c, e, "series memset");
@@ -642,6 +652,7 @@ static int ingest_range(xg_series* s, const uint8_t* raster, int64_t t0, int64_t
   p.max_bytes = L->max_bytes;
   p.max_band_pieces = L->max_band_pieces;
   p.t0 = t0;
+  p.x_row0 = s->x_row0;
   p.n_frames = n;
   // one wave of ~4 resident CTAs per SM, each streaming a run of frames of one band
   const int64_t want = std::max<int64_t>(1, (int64_t)c->num_sms * 4 / std::max(1, L->n_bands));
@@ -685,9 +696,10 @@ int xg_series_load_frames(xg_series* s, const uint8_t* frames, int64_t n, int on
   if (!s || !frames) return XG_ERR_INVALID;
   xg_ctx* c = s->ctx;
   const xg_layout* L = s->L;
-  if (n < 1 || n > s->tmax)
+  if (n < 1 || n > s->xmax)
     return fail(c, XG_ERR_SHAPE, "load_frames: %lld frames, capacity %lld", (long long)n,
-                (long long)s->tmax);
+                (long long)s->xmax);
+  s->x_row0 = 0;
   const uint8_t* src = frames;
   if (!on_device) {
     XG_CUDA(c, cudaMemcpyAsync(s->d_raster, frames, (size_t)n * L->pixels,
@@ -886,6 +898,9 @@ int xg_ttc_raw(xg_series* s, uint32_t flags) {
   if (!s) return XG_ERR_INVALID;
   xg_ctx* c = s->ctx;
   if (s->t < 2) return fail(c, XG_ERR_CONTRACT, "ttc_raw: need at least 2 frames");
+  if (s->x_row0 != 0 || s->t > s->xmax)
+    return fail(c, XG_ERR_CONTRACT, "ttc_raw: the raw TTC needs every frame resident "
+                                    "(series loaded in chunks; use the compressed path)");
   const xg_layout* L = s->L;
   if (flags & XG_STRICT) {
     // reference semantics: first zero-norm frame raises (linalg.cpp:446-449)
@@ -925,10 +940,11 @@ int xg_series_ttc_raw_host(xg_series* s, const uint8_t* frames, int64_t n, uint3
   if (!s || !frames) return XG_ERR_INVALID;
   xg_ctx* c = s->ctx;
   const xg_layout* L = s->L;
-  if (n < 1 || n > s->tmax)
+  if (n < 1 || n > s->xmax)
     return fail(c, XG_ERR_SHAPE, "load_frames: %lld frames, capacity %lld", (long long)n,
-                (long long)s->tmax);
+                (long long)s->xmax);
   if (n < 2) return fail(c, XG_ERR_CONTRACT, "ttc_raw: need at least 2 frames");
+  s->x_row0 = 0;
   if ((flags & XG_STRICT) || gram_one_cta()) {  // strict needs every frame before the Gram
     int rc = xg_series_load_frames(s, frames, n, 0);
     return rc ? rc : xg_ttc_raw(s, flags);
@@ -1172,28 +1188,29 @@ int xg_basis_set_ring(xg_basis* B, int32_t ring, const double* v) {
   return XG_OK;
 }
 
-int xg_compress(xg_series* s, const xg_basis* Bc, uint32_t flags) {
-  if (!s || !Bc) return XG_ERR_INVALID;
+// Zero-norm check of XG_STRICT (reference semantics, compress.cpp:48-81 via
+// row_normalize): the first zero frame of any ring raises.
+static int strict_zero_check(xg_series* s, const char* what) {
   xg_ctx* c = s->ctx;
-  xg_basis* B = const_cast<xg_basis*>(Bc);
   const xg_layout* L = s->L;
-  if (B->L != L) return fail(c, XG_ERR_BINDING, "compress: basis built for another layout");
-  if (s->t < 1) return fail(c, XG_ERR_CONTRACT, "compress: no frames loaded");
+  std::vector<int64_t> fz(L->rings);
+  XG_CUDA(c, cudaMemcpyAsync(fz.data(), s->d_first_zero, fz.size() * 8, cudaMemcpyDeviceToHost,
+                             c->stream));
+  XG_CUDA(c, cudaStreamSynchronize(c->stream));
   for (int32_t r = 0; r < L->rings; ++r)
-    if (!B->ring_set[r]) return fail(c, XG_ERR_CONTRACT, "compress: basis of ring %d not set", r);
-  if (flags & XG_STRICT) {
-    std::vector<int64_t> fz(L->rings);
-    XG_CUDA(c, cudaMemcpyAsync(fz.data(), s->d_first_zero, fz.size() * 8, cudaMemcpyDeviceToHost,
-                               c->stream));
-    XG_CUDA(c, cudaStreamSynchronize(c->stream));
-    for (int32_t r = 0; r < L->rings; ++r)
-      if (fz[r] != kNoZero) {
-        c->payload = fz[r];
-        c->payload_ring = r;
-        return fail(c, XG_ERR_NORMALIZATION,
-                    "compress_series: frame %lld of ring %d has zero norm", (long long)fz[r], r);
-      }
-  }
+    if (fz[r] != kNoZero) {
+      c->payload = fz[r];
+      c->payload_ring = r;
+      return fail(c, XG_ERR_NORMALIZATION, "%s: frame %lld of ring %d has zero norm", what,
+                  (long long)fz[r], r);
+    }
+  return XG_OK;
+}
+
+// K3 over the n ring-major rows in x, which hold series frames [t0, t0 + n).
+static int compress_rows(xg_series* s, xg_basis* B, int64_t t0, int64_t n) {
+  xg_ctx* c = s->ctx;
+  const xg_layout* L = s->L;
   if (B->dirty) {
     XG_CUDA(c, cudaMemcpy(B->d_vd, B->h_vd.data(), B->h_vd.size(), cudaMemcpyHostToDevice));
     XG_CUDA(c, cudaMemcpy(B->d_scale, B->h_scale.data(), B->h_scale.size() * 8,
@@ -1210,11 +1227,11 @@ int xg_compress(xg_series* s, const xg_basis* Bc, uint32_t flags) {
     s->ck = B->k;
     s->ckp = kp;
   }
-  // tiles: (ring, frame block, N-tile), cached per (frames, N-tiles)
-  const int64_t key = s->t * 64 + B->ntiles_n;
+  // tiles: (ring, frame block of x, N-tile), cached per (rows, N-tiles)
+  const int64_t key = n * 64 + B->ntiles_n;
   if (s->ptiles_key != key) {
     std::vector<TileDesc> tiles;
-    const int64_t nbi = (s->t + 127) / 128;
+    const int64_t nbi = (n + 127) / 128;
     for (int32_t r = 0; r < L->rings; ++r)
       for (int64_t ib = 0; ib < nbi; ++ib)
         for (int32_t nt = 0; nt < B->ntiles_n; ++nt)
@@ -1227,7 +1244,7 @@ int xg_compress(xg_series* s, const xg_basis* Bc, uint32_t flags) {
     s->ptiles_key = key;
   }
   CUtensorMap mx, mv, mp;
-  int rc = make_map_u8(c, &mx, s->d_x, L->ktot, s->t, L->ktot, 128, 128);
+  int rc = make_map_u8(c, &mx, s->d_x, L->ktot, n, L->ktot, 128, 128);
   // bf16 planes: 16 coefficients x 32 frames boxes, stored by the K3 epilogue
   if (!rc)
     rc = make_map_bf16_box(c, &mp, s->d_planes, kp, (int64_t)L->rings * 3 * s->tp, 16, 32,
@@ -1237,6 +1254,7 @@ int xg_compress(xg_series* s, const xg_basis* Bc, uint32_t flags) {
   if (rc) return rc;
   ProjParams p;
   p.tiles = s->d_ptiles;
+  p.t0 = t0;
   p.ntiles = s->n_ptiles;
   p.ring_koff = L->d_ring_koff;
   p.ring_nkb = L->d_ring_nkb;
@@ -1245,7 +1263,7 @@ int xg_compress(xg_series* s, const xg_basis* Bc, uint32_t flags) {
   p.k = B->k;
   p.inv = s->d_inv;
   p.inv_ld = s->tp;
-  p.n_frames = s->t;
+  p.n_frames = n;
   p.scale = B->d_scale;
   p.y = s->d_y;
   p.y_ld = s->tp;
@@ -1255,6 +1273,71 @@ int xg_compress(xg_series* s, const xg_basis* Bc, uint32_t flags) {
   p.err = c->d_err;
   XG_CUDA(c, launch_project(mx, mv, mp, p, c->num_sms, c->stream));
   c->launches++;
+  return XG_OK;
+}
+
+static int check_basis(xg_series* s, const xg_basis* B) {
+  xg_ctx* c = s->ctx;
+  if (B->L != s->L) return fail(c, XG_ERR_BINDING, "compress: basis built for another layout");
+  for (int32_t r = 0; r < s->L->rings; ++r)
+    if (!B->ring_set[r]) return fail(c, XG_ERR_CONTRACT, "compress: basis of ring %d not set", r);
+  return XG_OK;
+}
+
+int xg_compress(xg_series* s, const xg_basis* Bc, uint32_t flags) {
+  if (!s || !Bc) return XG_ERR_INVALID;
+  xg_ctx* c = s->ctx;
+  xg_basis* B = const_cast<xg_basis*>(Bc);
+  if (s->t < 1) return fail(c, XG_ERR_CONTRACT, "compress: no frames loaded");
+  if (s->x_row0 != 0 || s->t > s->xmax)
+    return fail(c, XG_ERR_CONTRACT, "compress: series loaded in chunks; compress each chunk");
+  int rc = check_basis(s, B);
+  if (rc) return rc;
+  if ((flags & XG_STRICT) && (rc = strict_zero_check(s, "compress_series"))) return rc;
+  rc = compress_rows(s, B, 0, s->t);
+  if (rc) return rc;
+  s->have_y = true;
+  s->have_cttc = false;
+  return XG_OK;
+}
+
+// One chunk of a series larger than the ring-major buffer: frames [t, t + n)
+// (t = frames so far) are ingested into x, their norms land at series rows
+// t.., and K3 writes their coefficients/planes at rows t..; the frames are not
+// kept.  Chunk 0 resets the series.  Only the compressed path follows.
+int xg_series_compress_chunk(xg_series* s, const xg_basis* Bc, const uint8_t* frames, int64_t n,
+                             int on_device, uint32_t flags) {
+  if (!s || !Bc || !frames) return XG_ERR_INVALID;
+  xg_ctx* c = s->ctx;
+  const xg_layout* L = s->L;
+  xg_basis* B = const_cast<xg_basis*>(Bc);
+  int rc = check_basis(s, B);
+  if (rc) return rc;
+  const int64_t t0 = (flags & XG_CHUNK_FIRST) ? 0 : s->t;
+  if (n < 1 || n > s->xmax)
+    return fail(c, XG_ERR_SHAPE, "compress_chunk: %lld frames, buffer %lld", (long long)n,
+                (long long)s->xmax);
+  if (t0 + n > s->tmax)
+    return fail(c, XG_ERR_SHAPE, "compress_chunk: %lld frames exceed capacity %lld",
+                (long long)(t0 + n), (long long)s->tmax);
+  const uint8_t* src = frames;
+  if (!on_device) {
+    XG_CUDA(c, cudaMemcpyAsync(s->d_raster, frames, (size_t)n * L->pixels,
+                               cudaMemcpyHostToDevice, c->stream));
+    src = s->d_raster;
+  }
+  if (t0 == 0) {
+    rc = reset_stats(s, s->tmax);
+    if (rc) return rc;
+    s->have_raw = false;
+  }
+  s->x_row0 = t0;
+  rc = ingest_range(s, src, t0, n);
+  if (rc) return rc;
+  if ((flags & XG_STRICT) && (rc = strict_zero_check(s, "compress_series"))) return rc;
+  rc = compress_rows(s, B, t0, n);
+  if (rc) return rc;
+  s->t = t0 + n;
   s->have_y = true;
   s->have_cttc = false;
   return XG_OK;

@@ -54,7 +54,8 @@ struct IngestParams {
   int32_t max_words;         // largest band word table
   int32_t max_bytes;         // largest band byte table (groups)
   int32_t max_band_pieces;
-  int64_t t0;                // first frame index written
+  int64_t t0;                // first frame index written (statistics row)
+  int64_t x_row0;            // frame index of row 0 of x (chunked series; else 0)
   int64_t n_frames;
   int32_t frames_per_cta;
   unsigned long long* norm2;  // [frame][ring] |x|^2, accumulated per piece (rows pre-zeroed)
@@ -165,7 +166,8 @@ __device__ __forceinline__ double combine_digits(int32_t a0, int32_t a1, int32_t
 #endif
 
 struct ProjParams {
-  const TileDesc* tiles;     // (ring, i0 = first frame, j0 = N-tile index)
+  const TileDesc* tiles;     // (ring, i0 = first frame of x, j0 = N-tile index)
+  int64_t t0;                // series frame index of x row 0 (chunked compress; else 0)
   int32_t ntiles;
   const int32_t* ring_koff;
   const int32_t* ring_nkb;

@@ -117,3 +117,31 @@ def test_compressed_g2_only_mode(ctx, orc):
         assert np.array_equal(a.cg2(r)[1], b.cg2(r)[1])
     with pytest.raises(xg.ContractError):
         b.cttc(0)
+
+
+def test_chunked_compress_equals_one_shot(ctx, orc):
+    """A series fed in chunks through a frame buffer smaller than the series
+    (xg_series_compress_chunk) gives bitwise the batch coefficients, C~ and
+    g2; the raw path is refused on it."""
+    t, h, w, q, k = 700, 48, 48, 2, 32
+    frames = orc.gen_speckle(t, h, w, q, 0.4, 61)
+    frames[300] = 0  # a zero frame inside a chunk
+    ring, _ = orc.ring_map(h, w, q)
+    lay = xg.RingLayout.from_ring_map(ctx, ring, q)
+    basis = xg.Basis(lay, k)
+    for r in range(q):
+        basis.set_ring(r, _basis(orc, frames[:, ring == r], k, 80 + r))
+    one = xg.FrameSeries(lay, t).load(frames).compress(basis).ttc_compressed()
+    ch = xg.FrameSeries(lay, t, x_frames=256)
+    for i, t0 in enumerate(range(0, t, 250)):
+        ch.compress_chunk(basis, frames[t0:t0 + 250], first=(i == 0))
+    ch.ttc_compressed()
+    for r in range(q):
+        y1, n1 = one.coeffs(r)
+        y2, n2 = ch.coeffs(r)
+        assert np.array_equal(y1, y2) and np.array_equal(n1, n2)
+        assert np.array_equal(one.cttc(r), ch.cttc(r))
+        assert np.array_equal(one.cg2(r)[1], ch.cg2(r)[1])
+        assert np.array_equal(one.cg2(r)[2], ch.cg2(r)[2])
+    with pytest.raises(xg.ContractError):
+        ch.ttc_raw()

@@ -44,6 +44,7 @@ def main():
     print("cgram+g2    %.3f ms" % timed(lambda: s.ttc_compressed()))
     print("cgram only  %.3f ms" % timed(lambda: s.ttc_compressed(g2=False)))
     print("bf16 +g2    %.3f ms" % timed(lambda: s.ttc_compressed(mode="bf16")))
+    print("g2 only     %.3f ms" % timed(lambda: s.ttc_compressed(store=False)))
     ctx.synchronize()
 
 

@@ -38,6 +38,7 @@ def main():
     print("ingest      %.3f ms" % timed(lambda: s.load(frames)))
     print("gram+g2     %.3f ms" % timed(lambda: s.ttc_raw()))
     print("gram only   %.3f ms" % timed(lambda: s.ttc_raw(g2=False)))
+    print("g2 only     %.3f ms" % timed(lambda: s.ttc_raw(store=False)))
     ctx.synchronize()
 
 
