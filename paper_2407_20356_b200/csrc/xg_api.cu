@@ -764,14 +764,14 @@ static int build_tiles(xg_series* s) {
   s->ntiles2 = static_cast<int32_t>(tiles2.size());
   // the same tiles grouped by column block J: a tile needs frames < 256 (J+1)
   // only, so the host-overlapped path runs group J as soon as those arrive
-  std::vector<TileDesc> byj;
   s->tiles2_joff.assign(static_cast<size_t>(nbj + 1), 0);
-  for (int64_t J = 0; J < nbj; ++J) {
-    s->tiles2_joff[J] = static_cast<int32_t>(byj.size());
-    for (const TileDesc& d : tiles2)
-      if (d.j0 == J * 256) byj.push_back(d);
+  for (const TileDesc& d : tiles2) s->tiles2_joff[d.j0 / 256 + 1]++;
+  for (int64_t J = 0; J < nbj; ++J) s->tiles2_joff[J + 1] += s->tiles2_joff[J];
+  std::vector<TileDesc> byj(tiles2.size());
+  {
+    std::vector<int32_t> fill(s->tiles2_joff.begin(), s->tiles2_joff.end() - 1);
+    for (const TileDesc& d : tiles2) byj[fill[d.j0 / 256]++] = d;  // stable within J
   }
-  s->tiles2_joff[nbj] = static_cast<int32_t>(byj.size());
   dfree(s->d_tiles2_j);
   XG_CUDA(c, dalloc(&s->d_tiles2_j, byj.size()));
   XG_CUDA(c, cudaMemcpy(s->d_tiles2_j, byj.data(), byj.size() * sizeof(TileDesc),
