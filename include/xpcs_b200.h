@@ -135,6 +135,10 @@ XG_API int xg_series_get_ttc(xg_series* s, int32_t ring, int32_t dtype, void* ou
 XG_API int xg_series_get_g2(xg_series* s, int32_t ring, double* values, int64_t* counts);
 /* g2 and pair counts of every ring in one transfer: [ring][n_frames] each */
 XG_API int xg_series_get_g2_all(xg_series* s, double* values, int64_t* counts);
+/* Deviation of the homomorphic path per ring (ttc_rel_error, correlate.cpp:
+ * 87-108): ||C - C~||_F / ||C||_F over the full symmetric matrices, from the
+ * stored raw TTC and compressed TTC (both computed, not XG_NO_STORE). */
+XG_API int xg_series_rel_error(xg_series* s, double* out_per_ring);
 /* f64 frame norms |x_t| of ring (n) and the count of zero-norm frames. */
 XG_API int xg_series_get_norms(xg_series* s, int32_t ring, double* norms, int64_t* n_zero);
 XG_API int64_t xg_series_frames(const xg_series* s);

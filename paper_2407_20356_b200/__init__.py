@@ -371,6 +371,13 @@ class FrameSeries:
         self.k = basis.k
         return self
 
+    def rel_error(self) -> np.ndarray:
+        """Per-ring ttc_rel_error(raw C, compressed C~) (correlate.cpp:87-108):
+        the homomorphic path's deviation report, computed on the device."""
+        out = np.empty(self.layout.n_rings, np.float64)
+        _check(self.ctx.h, lib.xg_series_rel_error(self.h, out.ctypes.data_as(_abi.PD)))
+        return out
+
     def compress_chunk(self, basis: "Basis", frames, first: bool = False,
                        strict: bool = False) -> "FrameSeries":
         """Append a chunk of frames and compress it (xg_series_compress_chunk):

@@ -171,7 +171,57 @@ __global__ void k_g2_div(const double* sum, const int64_t* cnt, double* out, int
   if (d < n) out[d] = cnt[d] > 0 ? sum[d] / static_cast<double>(cnt[d]) : 0.0;
 }
 
+// Block b of ring r takes rows b, b + REL_BLOCKS, ... of the upper triangle
+// (balanced: row a has n - a entries); off-diagonal entries count twice.
+__global__ void __launch_bounds__(256) k_rel_error(RelErrParams p) {
+  __shared__ double2 red[256];
+  const int r = blockIdx.y;
+  const int32_t* g = p.gram + r * p.ring_stride;
+  const float* cf = p.cgram + r * p.ring_stride;
+  const double* inv = p.inv + static_cast<int64_t>(r) * p.inv_ld;
+  double num = 0.0, den = 0.0;
+  for (int64_t a = blockIdx.x; a < p.n; a += REL_BLOCKS) {
+    const double ia = inv[a];
+    for (int64_t b = a + threadIdx.x; b < p.n; b += blockDim.x) {
+      const double c = static_cast<double>(g[a * p.ld + b]) * (ia * inv[b]);
+      const double e = c - static_cast<double>(cf[a * p.ld + b]);
+      const double w = a == b ? 1.0 : 2.0;
+      num += w * e * e;
+      den += w * c * c;
+    }
+  }
+  red[threadIdx.x] = make_double2(num, den);
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (static_cast<int>(threadIdx.x) < o) {
+      red[threadIdx.x].x += red[threadIdx.x + o].x;
+      red[threadIdx.x].y += red[threadIdx.x + o].y;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) p.partial[static_cast<int64_t>(r) * REL_BLOCKS + blockIdx.x] = red[0];
+}
+
+__global__ void k_rel_error_fin(RelErrParams p) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= p.n_rings) return;
+  double num = 0.0, den = 0.0;
+  for (int b = 0; b < REL_BLOCKS; ++b) {
+    num += p.partial[static_cast<int64_t>(r) * REL_BLOCKS + b].x;
+    den += p.partial[static_cast<int64_t>(r) * REL_BLOCKS + b].y;
+  }
+  p.out[r] = den > 0.0 ? sqrt(num / den) : -1.0;  // -1: all-zero reference TTC
+}
+
 }  // namespace
+
+cudaError_t launch_rel_error(const RelErrParams& p, cudaStream_t s) {
+  k_rel_error<<<dim3(REL_BLOCKS, p.n_rings), 256, 0, s>>>(p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  k_rel_error_fin<<<(p.n_rings + 127) / 128, 128, 0, s>>>(p);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_g2_div(const double* sum, const int64_t* cnt, double* out, int64_t n,
                           cudaStream_t s) {

@@ -1000,6 +1000,44 @@ int xg_series_g2(xg_series* s) {
   return run_g2(s, 0);
 }
 
+// Deviation report of the homomorphic path (north star; ttc_rel_error,
+// correlate.cpp:87-108): per ring ||C - C~||_F / ||C||_F from the stored TTCs.
+int xg_series_rel_error(xg_series* s, double* out) {
+  if (!s || !out) return XG_ERR_INVALID;
+  xg_ctx* c = s->ctx;
+  const xg_layout* L = s->L;
+  if (!s->have_raw || !s->raw_stored)
+    return fail(c, XG_ERR_CONTRACT, "rel_error: needs a stored raw TTC (ttc_raw)");
+  if (!s->have_cttc || !s->cmp_stored)
+    return fail(c, XG_ERR_CONTRACT, "rel_error: needs a stored compressed TTC");
+  double2* part = nullptr;
+  double* d_out = nullptr;
+  XG_CUDA(c, cudaMalloc(&part, (size_t)L->rings * REL_BLOCKS * sizeof(double2)));
+  XG_CUDA(c, cudaMalloc(&d_out, (size_t)L->rings * 8));
+  RelErrParams p;
+  p.gram = s->d_gram;
+  p.cgram = s->d_cgram;
+  p.ring_stride = s->tp * s->tp;
+  p.ld = static_cast<int32_t>(s->tp);
+  p.inv = s->d_inv;
+  p.inv_ld = s->tp;
+  p.n = s->t;
+  p.n_rings = L->rings;
+  p.partial = part;
+  p.out = d_out;
+  cudaError_t e = launch_rel_error(p, c->stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(out, d_out, (size_t)L->rings * 8, cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  cudaFree(part);
+  cudaFree(d_out);
+  if (e != cudaSuccess) return cuda_fail(c, e, "rel_error");
+  c->launches += 2;
+  for (int32_t r = 0; r < L->rings; ++r)
+    if (out[r] < 0.0) return fail(c, XG_ERR_CONTRACT, "ttc_rel_error: reference TTC is all zero");
+  return check_device_error(c);
+}
+
 int xg_series_get_ttc(xg_series* s, int32_t ring, int32_t dtype, void* out, int64_t ld,
                       int out_on_device) {
   if (!s || !out) return XG_ERR_INVALID;

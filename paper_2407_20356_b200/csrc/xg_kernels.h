@@ -294,6 +294,24 @@ struct ExpandParams {
 };
 cudaError_t launch_expand(const ExpandParams& p, int src_mode, cudaStream_t s);
 
+// ttc_rel_error (correlate.cpp:87-108) of every ring between the stored raw
+// TTC (exact Gram * 1/|x_i| 1/|x_j|) and the stored compressed C~, over the
+// full symmetric matrices; fixed-order reductions (deterministic).
+struct RelErrParams {
+  const int32_t* gram;       // [ring][ld][ld] upper tiles
+  const float* cgram;        // [ring][ld][ld] upper tiles
+  int64_t ring_stride;
+  int32_t ld;
+  const double* inv;         // [ring][inv_ld]
+  int64_t inv_ld;
+  int64_t n;
+  int32_t n_rings;
+  double2* partial;          // [ring][REL_BLOCKS] (num, den)
+  double* out;               // [ring]
+};
+constexpr int REL_BLOCKS = 64;
+cudaError_t launch_rel_error(const RelErrParams& p, cudaStream_t s);
+
 // ---------------------------------------------------------- K8 synthetic
 struct SynthParams {
   int64_t t_first;           // global index of the first frame generated

@@ -145,3 +145,21 @@ def test_chunked_compress_equals_one_shot(ctx, orc):
         assert np.array_equal(one.cg2(r)[2], ch.cg2(r)[2])
     with pytest.raises(xg.ContractError):
         ch.ttc_raw()
+
+
+def test_rel_error_report_matches_oracle(ctx, orc):
+    """Device ttc_rel_error(raw C, compressed C~) per ring equals the oracle's
+    ttc_rel_error on the same two matrices (sum order differs: 1e-12 rel)."""
+    t, h, w, q, k = 300, 48, 48, 3, 8
+    frames = orc.gen_speckle(t, h, w, q, 0.4, 91)
+    ring, _ = orc.ring_map(h, w, q)
+    lay = xg.RingLayout.from_ring_map(ctx, ring, q)
+    basis = xg.Basis(lay, k)
+    for r in range(q):
+        basis.set_ring(r, _basis(orc, frames[:, ring == r], k, 90 + r))
+    s = xg.FrameSeries(lay, t).load(frames).ttc_raw().compress(basis).ttc_compressed()
+    rel = s.rel_error()
+    for r in range(q):
+        ref = orc.ttc_rel_error(s.ttc(r, "f64"), s.cttc(r).astype(np.float64))
+        assert abs(rel[r] - ref) <= 1e-12 * ref + 1e-15, (r, rel[r], ref)
+        assert 0.0 < rel[r] < 1.0
