@@ -31,7 +31,7 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 128;
-constexpr int MAX_STAGES = 4;
+constexpr int MAX_STAGES = 6;
 constexpr int A_BYTES = BM * BK;    // 16 KB
 constexpr int TMEM_COLS = 512;
 constexpr int NUM_THREADS = 256;
@@ -54,7 +54,9 @@ struct __align__(8) ProjTail {
   uint32_t tmem_base;
 };
 
-__host__ __device__ inline int proj_stage_bytes(int nt_rows) { return A_BYTES + nt_rows * BK; }
+// per CTA: its 128 frame rows + half of the digit rows (the pair's MMA
+// reads the other half from the peer CTA)
+__host__ __device__ inline int proj_stage_bytes(int nt_rows) { return A_BYTES + nt_rows / 2 * BK; }
 __host__ __device__ inline int proj_stages(int nt_rows) {
   const int fixed = 1024 + 4 * static_cast<int>(sizeof(EpiStage)) + static_cast<int>(sizeof(ProjTail));
   const int st = (SMEM_LIMIT - fixed) / proj_stage_bytes(nt_rows);
@@ -78,21 +80,29 @@ size_t project_smem_bytes(int nt_rows) {
          4 * sizeof(EpiStage) + sizeof(ProjTail);
 }
 
-__global__ void __launch_bounds__(NUM_THREADS, 1)
+// CTA pairs (cluster of 2): tcgen05.mma.cta_group::2 with M = 256 frames x
+// N = S*kt digit rows; each CTA stages its 128 frame rows and half of the
+// digit rows, so every SM fetches half the basis bytes per frame of a 1-CTA
+// tile (the basis is re-read from L2 by every frame block).
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     k_project(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmV,
               const __grid_constant__ CUtensorMap tmP, ProjParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int nt_rows = p.n_digits * p.kt;               // N of the MMA (multiple of 16)
+  const int half_rows = nt_rows / 2;                   // digit rows staged by this CTA
   const int STAGES = proj_stages(nt_rows);
-  const int B_BYTES = nt_rows * BK;                    // multiple of 2 KB
+  const int B_BYTES = half_rows * BK;                  // multiple of 1 KB
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * A_BYTES;
   EpiStage* epi = reinterpret_cast<EpiStage*>(sB + STAGES * B_BYTES);
   ProjTail* tail = reinterpret_cast<ProjTail*>(epi + 4);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t idesc = idesc_i8(BM, static_cast<uint32_t>(nt_rows), true);
-  const uint32_t stage_tx = A_BYTES + nt_rows * BK;  // one box of all digit rows
+  const uint32_t rank = cta_rank();
+  const bool leader = rank == 0;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const uint32_t idesc = idesc_i8(2 * BM, static_cast<uint32_t>(nt_rows), true);
+  const uint32_t stage_tx = 2 * (A_BYTES + B_BYTES);  // both CTAs' bytes, on the leader
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -101,15 +111,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tail->tfull[a], 1);
-      mbar_init(&tail->tempty[a], 4);
+      mbar_init(&tail->tempty[a], 8);  // 4 epilogue warps in each CTA of the pair
     }
     fence_barrier_init();
     tma_prefetch(&tmX);
     tma_prefetch(&tmV);
   }
-  if (warp == 2) tmem_alloc(&tail->tmem_base, TMEM_COLS);
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&tail->tmem_base)),
+                 "r"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
   tc_fence_before();
-  __syncthreads();
+  cluster_sync();  // barriers of both CTAs initialised, TMEM allocated
   tc_fence_after();
   const uint32_t tmem_base = tail->tmem_base;
 
@@ -117,16 +133,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
+      for (int t = pair; t < p.ntiles; t += npairs) {
         const TileDesc td = p.tiles[t];
         const int koff = p.ring_koff[td.ring], nkb = p.ring_nkb[td.ring];
-        const int vrow = td.j0 * nt_rows;  // j0 = N-tile index
+        const int vrow = td.j0 * nt_rows + static_cast<int>(rank) * half_rows;
         for (int kb = 0; kb < nkb; ++kb) {
           if (!mbar_wait(&tail->empty[stage], phase ^ 1, p.err)) goto done;
-          mbar_arrive_expect_tx(&tail->full[stage], stage_tx);
+          if (leader) mbar_arrive_expect_tx(&tail->full[stage], stage_tx);
           const int kc = koff + kb * BK;
-          tma_load_2d(sA + stage * A_BYTES, &tmX, &tail->full[stage], kc, td.i0);
-          tma_load_2d(sB + stage * B_BYTES, &tmV, &tail->full[stage], kc, vrow);
+          tma_load_2sm(sA + stage * A_BYTES, &tmX, &tail->full[stage], kc,
+                       td.i0 + BM * static_cast<int>(rank));
+          tma_load_2sm(sB + stage * B_BYTES, &tmV, &tail->full[stage], kc, vrow);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -136,10 +153,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     done:;
     }
   } else if (warp == 1) {
-    if (elect_one()) {
+    if (leader && elect_one()) {
       int stage = 0, acc = 0;
       uint32_t phase = 0, acc_phase = 0;
-      for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
+      for (int t = pair; t < p.ntiles; t += npairs) {
         const TileDesc td = p.tiles[t];
         const int nkb = p.ring_nkb[td.ring];
         if (!mbar_wait(&tail->tempty[acc], acc_phase ^ 1, p.err)) break;
@@ -155,16 +172,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const uint32_t a0 = smem_u32(sA + stage * A_BYTES), b0 = smem_u32(sB + stage * B_BYTES);
 #pragma unroll
           for (int k = 0; k < BK / 32; ++k)
-            mma_i8(tmem_d, sdesc_k128(a0 + k * 32), sdesc_k128(b0 + k * 32), idesc,
-                   (kb | k) != 0 ? 1u : 0u);
-          tc_commit(&tail->empty[stage]);
+            mma2_i8(tmem_d, sdesc_k128(a0 + k * 32), sdesc_k128(b0 + k * 32), idesc,
+                    (kb | k) != 0 ? 1u : 0u);
+          commit2(&tail->empty[stage]);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
         if (!ok) break;
-        tc_commit(&tail->tfull[acc]);
+        commit2(&tail->tfull[acc]);
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
@@ -176,13 +193,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int row = sub * 32 + lane;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
+    for (int t = pair; t < p.ntiles; t += npairs) {
       const TileDesc td = p.tiles[t];
       bool ok = mbar_wait(&tail->tfull[acc], acc_phase, p.err);
       ok = __all_sync(0xffffffffu, ok);
       if (!ok) break;
       tc_fence_after();
-      const int64_t frame = td.i0 + row;  // row of x; series frame p.t0 + frame
+      const int i0 = td.i0 + BM * static_cast<int>(rank);  // this CTA's 128 frames
+      const int64_t frame = i0 + row;  // row of x; series frame p.t0 + frame
       const bool live = frame < p.n_frames;
       const double inv =
           live ? p.inv[static_cast<int64_t>(td.ring) * p.inv_ld + p.t0 + frame] : 0.0;
@@ -243,7 +261,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         __syncwarp();
         if (p.planes && lane == 0) {
           const int row0 = static_cast<int>((static_cast<int64_t>(td.ring) * 3) * p.plane_rows +
-                                            p.t0) + td.i0 + 32 * sub;
+                                            p.t0) + i0 + 32 * sub;
 #pragma unroll
           for (int q = 0; q < 3; ++q)
             asm volatile(
@@ -259,7 +277,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll 4
         for (int it = 0; it < 16; ++it) {
           const int r = 2 * it + (lane >> 4);
-          const int64_t f = td.i0 + 32 * sub + r;
+          const int64_t f = i0 + 32 * sub + r;
           if (f < p.n_frames && j0 + c < p.k)
             p.y[(static_cast<int64_t>(td.ring) * p.y_ld + p.t0 + f) * p.k + j0 + c] = es->y[r * 17 + c];
         }
@@ -267,7 +285,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tail->tempty[acc]);
+      if (lane == 0) {
+        if (leader)
+          mbar_arrive(&tail->tempty[acc]);
+        else
+          arrive_leader(&tail->tempty[acc]);
+      }
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
@@ -276,10 +299,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   tc_fence_before();
-  __syncthreads();
+  cluster_sync();  // no remote arrivals in flight, both CTAs done with TMEM
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, TMEM_COLS);
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(TMEM_COLS)
+                 : "memory");
   }
 }
 
@@ -289,9 +314,9 @@ cudaError_t launch_project(const CUtensorMap& tmX, const CUtensorMap& tmV, const
   cudaError_t e =
       cudaFuncSetAttribute(k_project, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  const int grid = p.ntiles < num_sms ? p.ntiles : num_sms;
-  if (grid <= 0) return cudaSuccess;
-  k_project<<<grid, NUM_THREADS, smem, stream>>>(tmX, tmV, tmP, p);
+  const int pairs = p.ntiles < num_sms / 2 ? p.ntiles : num_sms / 2;
+  if (pairs <= 0) return cudaSuccess;
+  k_project<<<2 * pairs, NUM_THREADS, smem, stream>>>(tmX, tmV, tmP, p);
   return cudaGetLastError();
 }
 

@@ -1269,11 +1269,11 @@ static int compress_rows(xg_series* s, xg_basis* B, int64_t t0, int64_t n) {
   const int64_t key = n * 64 + B->ntiles_n;
   if (s->ptiles_key != key) {
     std::vector<TileDesc> tiles;
-    const int64_t nbi = (n + 127) / 128;
+    const int64_t nbi = (n + 255) / 256;  // 256-frame blocks: one CTA pair each
     for (int32_t r = 0; r < L->rings; ++r)
       for (int64_t ib = 0; ib < nbi; ++ib)
         for (int32_t nt = 0; nt < B->ntiles_n; ++nt)
-          tiles.push_back({r, (int32_t)(ib * 128), nt, 0});
+          tiles.push_back({r, (int32_t)(ib * 256), nt, 0});
     dfree(s->d_ptiles);
     XG_CUDA(c, dalloc(&s->d_ptiles, tiles.size()));
     XG_CUDA(c, cudaMemcpy(s->d_ptiles, tiles.data(), tiles.size() * sizeof(TileDesc),
@@ -1287,8 +1287,9 @@ static int compress_rows(xg_series* s, xg_basis* B, int64_t t0, int64_t n) {
   if (!rc)
     rc = make_map_bf16_box(c, &mp, s->d_planes, kp, (int64_t)L->rings * 3 * s->tp, 16, 32,
                            CU_TENSOR_MAP_SWIZZLE_NONE);
-  // one box = all S*kt digit rows of an N-tile (<= 256)
-  if (!rc) rc = make_map_u8(c, &mv, B->d_vd, L->ktot, B->vrows, L->ktot, 128, B->digits * B->kt);
+  // one box = this CTA's half of the S*kt digit rows of an N-tile
+  if (!rc)
+    rc = make_map_u8(c, &mv, B->d_vd, L->ktot, B->vrows, L->ktot, 128, B->digits * B->kt / 2);
   if (rc) return rc;
   ProjParams p;
   p.tiles = s->d_ptiles;
