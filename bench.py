@@ -227,19 +227,22 @@ def run_reference(args, rank, world):
 
 def run_compressed(args, torch, xg, ctx, stream, frames, series, ring, sizes, mine, world, dev):
     """Rank-k path on the same frames: basis per ring from a 256-frame
-    training prefix (untimed, host f64 Gram-trick SVD), then per step
+    training prefix (untimed, built on the device), then per step
     ingest (K1) -> int8-digit projection (K3) -> bf16x3 compressed Gram with
     fused g2 (K4)."""
     cfg = CFG
     T, k = cfg["T"], cfg["k"]
     t_train = 256
-    prior = frames[:t_train].cpu().numpy()
-    t0 = time.perf_counter()
-    vs = xg.build_ring_bases([prior[:, ring == r] for r in mine], k)
-    t_basis = time.perf_counter() - t0
+    # the basis is built on the device (K9, xg_series_build_basis: the
+    # reference's build_online_from_frames per ring) from a training series
     basis = xg.Basis(series.layout, k)
-    for i, v in enumerate(vs):
-        basis.set_ring(i, v)
+    train = xg.FrameSeries(series.layout, t_train).load(frames[:t_train])
+    ctx.synchronize()
+    t0 = time.perf_counter()
+    train.build_basis(k, basis=basis)
+    ctx.synchronize()
+    t_basis = time.perf_counter() - t0
+    del train
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 
     def step(rec=None):
@@ -294,7 +297,9 @@ def run_compressed(args, torch, xg, ctx, stream, frames, series, ring, sizes, mi
         "deviation_vs_raw": {"metric": "ttc_rel_error(raw C, compressed C~) per ring",
                              "median": float(np.median(rel)), "min": float(rel.min()),
                              "max": float(rel.max())},
-        "basis": f"per ring from the first {t_train} frames (host Gram-trick SVD, {t_basis:.1f} s, untimed)",
+        "basis": f"per ring from the first {t_train} frames, built on the device (K9 "
+                 f"xg_series_build_basis: Gram, Jacobi, W = Xn^T U, 2x Cholesky-QR), untimed",
+        "basis_build_ms": t_basis * 1e3,
         "projection": {"kernel": "k_project (K3)", "bound": "hbm", "ms": proj_ms,
                        "achieved": proj_bytes / (proj_ms / 1e3) / 1e9, "peak": peaks["hbm_gbs"],
                        "unit": "GB/s", "frac": proj_bytes / (proj_ms / 1e3) / 1e9 / peaks["hbm_gbs"],

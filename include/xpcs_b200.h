@@ -172,6 +172,20 @@ XG_API int xg_basis_create(xg_ctx* ctx, const xg_layout* layout, int32_t k, int3
                            xg_basis** out);
 XG_API void xg_basis_destroy(xg_basis* basis);
 XG_API int xg_basis_set_ring(xg_basis* basis, int32_t ring, const double* v);
+/* The same basis built ON THE DEVICE for every ring of a series, whose
+ * loaded frames are the training rows (replaces encoder_from_rows ->
+ * gram_svd, encoder.cpp:13-28 / linalg.cpp:279-439, per ring; T <= 2048):
+ * exact int32 Gram (K2) -> S = G/(|x_i||x_j|) -> parallel-order Jacobi ->
+ * W = Xn^T U (f64 GEMM) -> measured sigma, rank at 1e-12 sigma_max ->
+ * 2x Cholesky-QR (the k x k factor on the host) -> sign convention.
+ * k = 0: full numerical rank per ring (build_offline).  Outputs (each
+ * optional): v_out[ring] = m_ring x k_ring f64 in mask order (k_ring = k, or
+ * the ring's rank when k = 0); sigma_out[ring * sigma_ld + j] the spectrum;
+ * rank_out[ring] (required); basis (k > 0) gets every ring (set_ring).
+ * XG_ERR_RANK: k exceeds a ring's rank (payload = rank, ring);
+ * XG_ERR_NORMALIZATION: a zero training frame (payload = frame, ring). */
+XG_API int xg_series_build_basis(xg_series* s, int32_t k, double* const* v_out, double* sigma_out,
+                                 int64_t sigma_ld, int64_t* rank_out, xg_basis* basis);
 XG_API int xg_compress(xg_series* s, const xg_basis* basis, uint32_t flags);
 /* Append n frames (u8 raster) to a chunked series and compress them:
  * series rows [t, t + n) get norms, coefficients and bf16 planes; the frames

@@ -378,6 +378,27 @@ class FrameSeries:
         _check(self.ctx.h, lib.xg_series_rel_error(self.h, out.ctypes.data_as(_abi.PD)))
         return out
 
+    def build_basis(self, k: int, basis: "Basis | None" = None):
+        """Per-ring encoding basis from this series' frames, built on the
+        device (xg_series_build_basis; the reference's build_online_from_frames
+        per ring, k = 0 -> build_offline).  Returns (V per ring in mask order,
+        spectrum per ring, rank per ring); fills ``basis`` when given."""
+        q = self.layout.n_rings
+        n = self.n_frames
+        rank = np.zeros(q, np.int64)
+        sig = np.zeros((q, max(n, 1)), np.float64)
+        vs = [np.empty((self.layout.ring_pixels(r), k if k > 0 else n), np.float64)
+              for r in range(q)]
+        ptrs = (_abi.PD * q)(*[v.ctypes.data_as(_abi.PD) for v in vs])
+        _check(self.ctx.h, lib.xg_series_build_basis(
+            self.h, int(k), ptrs, sig.ctypes.data_as(_abi.PD), sig.shape[1],
+            rank.ctypes.data_as(_abi.PI64), basis.h if basis is not None else None))
+        if k == 0:  # full rank: V was written with the ring's own rank as row length
+            vs = [np.ascontiguousarray(v.ravel()[: v.shape[0] * int(rank[r])]
+                                       .reshape(v.shape[0], int(rank[r])))
+                  for r, v in enumerate(vs)]
+        return vs, [sig[r, : int(rank[r])].copy() for r in range(q)], rank
+
     def compress_chunk(self, basis: "Basis", frames, first: bool = False,
                        strict: bool = False) -> "FrameSeries":
         """Append a chunk of frames and compress it (xg_series_compress_chunk):

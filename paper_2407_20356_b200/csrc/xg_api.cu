@@ -8,12 +8,16 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 #include <climits>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <numeric>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/xpcs_b200.h"
@@ -1320,6 +1324,378 @@ static int check_basis(xg_series* s, const xg_basis* B) {
   if (B->L != s->L) return fail(c, XG_ERR_BINDING, "compress: basis built for another layout");
   for (int32_t r = 0; r < s->L->rings; ++r)
     if (!B->ring_set[r]) return fail(c, XG_ERR_CONTRACT, "compress: basis of ring %d not set", r);
+  return XG_OK;
+}
+
+// ------------------------------------------------------------ K9 basis on the device
+// build_online_from_frames / build_offline (encoder.cpp:13-60 -> gram_svd,
+// linalg.cpp:279-439) for every ring of a series at once; see k_basis.cu.
+}  // extern "C"
+namespace {
+
+struct DevBufs {  // frees every scratch buffer on any return path
+  std::vector<void*> p;
+  template <class T>
+  cudaError_t get(T** out, size_t count) {
+    cudaError_t e = dalloc(out, count);
+    if (e == cudaSuccess) p.push_back(*out);
+    return e;
+  }
+  ~DevBufs() {
+    for (void* q : p) cudaFree(q);
+  }
+};
+
+// Upper Cholesky G = R^T R of the leading m x m block (G upper, ld m) and the
+// transposed inverse: mt[j][i] = (R^-1)[i][j] (lower triangular, ld m).
+// Returns the first collapsed column or -1.
+int64_t chol_inv_t(const double* g, int64_t m, std::vector<double>& r, std::vector<double>& mt) {
+  r.assign(m * m, 0.0);
+  for (int64_t j = 0; j < m; ++j) {
+    double d = g[j * m + j];
+    for (int64_t i = 0; i < j; ++i) d -= r[i * m + j] * r[i * m + j];
+    if (!(d > 0.0)) return j;
+    const double rjj = std::sqrt(d);
+    r[j * m + j] = rjj;
+    for (int64_t l = j + 1; l < m; ++l) {
+      double v = g[j * m + l];
+      for (int64_t i = 0; i < j; ++i) v -= r[i * m + j] * r[i * m + l];
+      r[j * m + l] = v / rjj;
+    }
+  }
+  // X = R^-1 (upper) by back substitution, column by column
+  std::vector<double> x(m * m, 0.0);
+  for (int64_t c = 0; c < m; ++c) {
+    for (int64_t i = c; i >= 0; --i) {
+      double v = (i == c) ? 1.0 : 0.0;
+      for (int64_t l = i + 1; l <= c; ++l) v -= r[i * m + l] * x[l * m + c];
+      x[i * m + c] = v / r[i * m + i];
+    }
+  }
+  mt.assign(m * m, 0.0);
+  for (int64_t i = 0; i < m; ++i)
+    for (int64_t j = i; j < m; ++j) mt[j * m + i] = x[i * m + j];
+  return -1;
+}
+
+template <class F>
+void for_rings(int32_t n, F f) {
+  const int nt = std::max(1, std::min<int>(n, (int)std::thread::hardware_concurrency()));
+  std::vector<std::thread> pool;
+  for (int w = 0; w < nt; ++w)
+    pool.emplace_back([&, w] {
+      for (int32_t r = w; r < n; r += nt) f(r);
+    });
+  for (auto& t : pool) t.join();
+}
+
+}  // namespace
+extern "C" {
+
+int xg_series_build_basis(xg_series* s, int32_t k, double* const* v_out, double* sigma_out,
+                          int64_t sigma_ld, int64_t* rank_out, xg_basis* B) {
+  if (!s || !rank_out) return XG_ERR_INVALID;
+  xg_ctx* c = s->ctx;
+  const xg_layout* L = s->L;
+  const int32_t Q = L->rings;
+  const int64_t n = s->t;
+  if (k < 0) return fail(c, XG_ERR_CONTRACT, "build_online_from_frames: k must be >= 1");
+  if (n < 2) return fail(c, XG_ERR_CONTRACT, "build_online_from_frames: need at least 2 frames");
+  if (n > 2048) return fail(c, XG_ERR_CONTRACT, "build_basis: at most 2048 training frames");
+  if (s->x_row0 != 0 || n > s->xmax)
+    return fail(c, XG_ERR_CONTRACT, "build_basis: every training frame must be resident");
+  if (B && (B->L != L || B->k != k || k == 0))
+    return fail(c, XG_ERR_CONTRACT, "build_basis: basis of rank %d does not match k = %d",
+                B ? B->k : 0, k);
+  if (sigma_out && sigma_ld < n) return fail(c, XG_ERR_SHAPE, "build_basis: sigma_ld < frames");
+  int rc = strict_zero_check(s, "row_normalize");  // encoder_from_rows -> row_normalize
+  if (rc) return rc;
+  if (!(s->have_raw && s->raw_stored)) {
+    rc = xg_ttc_raw(s, 0);  // the exact Gram of the training frames (K2)
+    if (rc) return rc;
+  }
+  cudaStream_t st = c->stream;
+  const int np = static_cast<int>(n + (n & 1));
+  const int64_t rs = (int64_t)np * np;
+  static const bool timing = std::getenv("XG_BASIS_TIMING") != nullptr;
+  auto t_last = std::chrono::steady_clock::now();
+  auto phase = [&](const char* what) {
+    if (!timing) return;
+    cudaStreamSynchronize(st);
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[basis] %-10s %8.2f ms\n", what,
+            std::chrono::duration<double, std::milli>(now - t_last).count());
+    t_last = now;
+  };
+  DevBufs db;
+  double *d_a[2], *d_v[2];
+  JacState* d_state;
+  for (int b = 0; b < 2; ++b) {
+    XG_CUDA(c, db.get(&d_a[b], (size_t)Q * rs));
+    XG_CUDA(c, db.get(&d_v[b], (size_t)Q * rs));
+  }
+  XG_CUDA(c, db.get(&d_state, (size_t)Q));
+  BasisSParams sp{s->d_gram, static_cast<int32_t>(s->tp), s->d_inv, s->tp,
+                  static_cast<int32_t>(n), np, d_a[0], d_v[0]};
+  phase("gram");
+  XG_CUDA(c, launch_basis_s(sp, Q, st));
+  c->launches++;
+  // ---- Jacobi sweeps (sym_eig, linalg.cpp:234-276)
+  std::vector<JacState> hs(Q, JacState{1e-15, 1, 0});
+  std::vector<int> final_buf(Q, 0);
+  int64_t g = 0;
+  XG_CUDA(c, cudaMemcpyAsync(d_state, hs.data(), Q * sizeof(JacState), cudaMemcpyHostToDevice, st));
+  for (int sweep = 0; sweep < 100; ++sweep) {
+    for (int step = 0; step < np - 1; ++step, ++g) {
+      JacParams jp{d_a[g % 2], d_a[(g + 1) % 2], d_v[g % 2], d_v[(g + 1) % 2], d_state, np, step};
+      XG_CUDA(c, launch_jacobi_step(jp, Q, st));
+      c->launches++;
+    }
+    XG_CUDA(c, cudaMemcpyAsync(hs.data(), d_state, Q * sizeof(JacState), cudaMemcpyDeviceToHost, st));
+    XG_CUDA(c, cudaStreamSynchronize(st));
+    bool any = false;
+    for (int32_t r = 0; r < Q; ++r) {
+      if (!hs[r].active) continue;
+      final_buf[r] = static_cast<int>(g % 2);
+      if (!hs[r].rotated) {
+        hs[r].active = 0;
+        continue;
+      }
+      if (sweep >= 40 && sweep % 10 == 0) hs[r].tol *= 100.0;  // stall escape (linalg.cpp:255)
+      hs[r].rotated = 0;
+      any = true;
+    }
+    if (!any) break;
+    XG_CUDA(c, cudaMemcpyAsync(d_state, hs.data(), Q * sizeof(JacState), cudaMemcpyHostToDevice, st));
+  }
+  if (timing) fprintf(stderr, "[basis] %lld Jacobi steps (np %d, %d rings)\n", (long long)g, np, Q);
+  phase("jacobi");
+  // ---- eigenvalues (index order) and the accumulated rotations
+  std::vector<const double*> a_ptr(Q);
+  for (int32_t r = 0; r < Q; ++r) a_ptr[r] = d_a[final_buf[r]] + r * rs;
+  const double** d_aptr;
+  double* d_eig;
+  XG_CUDA(c, db.get(&d_aptr, (size_t)Q));
+  XG_CUDA(c, db.get(&d_eig, (size_t)Q * np));
+  XG_CUDA(c, cudaMemcpyAsync(d_aptr, a_ptr.data(), Q * sizeof(double*), cudaMemcpyHostToDevice, st));
+  XG_CUDA(c, launch_jacobi_diag(d_aptr, d_eig, np, Q, st));
+  c->launches++;
+  std::vector<double> eig((size_t)Q * np), hv((size_t)Q * rs), inv((size_t)Q * s->tp);
+  XG_CUDA(c, cudaMemcpyAsync(eig.data(), d_eig, eig.size() * 8, cudaMemcpyDeviceToHost, st));
+  for (int32_t r = 0; r < Q; ++r)
+    XG_CUDA(c, cudaMemcpyAsync(hv.data() + r * rs, d_v[final_buf[r]] + r * rs, rs * 8,
+                               cudaMemcpyDeviceToHost, st));
+  XG_CUDA(c, cudaMemcpyAsync(inv.data(), s->d_inv, inv.size() * 8, cudaMemcpyDeviceToHost, st));
+  XG_CUDA(c, cudaStreamSynchronize(st));
+  // Bt[j][t] = inv_t U[t][order_j]: eigenvectors in descending eigenvalue
+  // order (stable in the index, linalg.cpp:262-266), rows scaled by 1/|x_t|
+  std::vector<double> bt((size_t)Q * n * n);
+  for_rings(Q, [&](int32_t r) {
+    std::vector<int64_t> ord(n);
+    for (int64_t i = 0; i < n; ++i) ord[i] = i;
+    const double* e = eig.data() + (size_t)r * np;
+    std::stable_sort(ord.begin(), ord.end(), [&](int64_t a, int64_t b) { return e[a] > e[b]; });
+    const double* v = hv.data() + r * rs;
+    double* o = bt.data() + (size_t)r * n * n;
+    for (int64_t j = 0; j < n; ++j) {
+      const int sl = index_slot(static_cast<int>(ord[j]), 0, np);
+      for (int64_t t = 0; t < n; ++t) o[j * n + t] = inv[r * s->tp + t] * v[t * np + sl];
+    }
+  });
+  phase("eig+Bt");
+  double *d_bt, *d_w;
+  XG_CUDA(c, db.get(&d_bt, bt.size()));
+  XG_CUDA(c, db.get(&d_w, (size_t)n * L->ktot));
+  XG_CUDA(c, cudaMemcpyAsync(d_bt, bt.data(), bt.size() * 8, cudaMemcpyHostToDevice, st));
+  // ---- W_r = Bt_r X_r  (n x kpad_r), X = the ring-major u8 frames
+  int64_t kpad_max = 0;
+  std::vector<DGemmRing> gr(Q);
+  for (int32_t r = 0; r < Q; ++r) {
+    kpad_max = std::max(kpad_max, L->kpad[r]);
+    gr[r] = DGemmRing{d_bt + (size_t)r * n * n, n, s->d_x + L->koff[r], L->ktot,
+                      d_w + n * L->koff[r], L->kpad[r], (int32_t)n, (int32_t)L->kpad[r], (int32_t)n};
+  }
+  DGemmRing* d_gr;
+  XG_CUDA(c, db.get(&d_gr, (size_t)Q));
+  XG_CUDA(c, cudaMemcpyAsync(d_gr, gr.data(), Q * sizeof(DGemmRing), cudaMemcpyHostToDevice, st));
+  XG_CUDA(c, launch_dgemm_nn(d_gr, Q, (int)n, (int)kpad_max, true, st));
+  c->launches++;
+  // ---- measured singular values |W_j| (linalg.cpp:312-320)
+  double* d_nrm;
+  XG_CUDA(c, db.get(&d_nrm, (size_t)Q * n));
+  for (int32_t r = 0; r < Q; ++r) gr[r] = DGemmRing{d_w + n * L->koff[r], L->kpad[r], nullptr, 0,
+                                                    nullptr, 0, (int32_t)n, (int32_t)L->kpad[r], 0};
+  XG_CUDA(c, cudaMemcpyAsync(d_gr, gr.data(), Q * sizeof(DGemmRing), cudaMemcpyHostToDevice, st));
+  XG_CUDA(c, launch_row_norm2(d_gr, Q, (int)n, d_nrm, n, st));
+  c->launches++;
+  std::vector<double> nrm((size_t)Q * n);
+  XG_CUDA(c, cudaMemcpyAsync(nrm.data(), d_nrm, nrm.size() * 8, cudaMemcpyDeviceToHost, st));
+  XG_CUDA(c, cudaStreamSynchronize(st));
+  phase("W+norms");
+  std::vector<std::vector<int32_t>> ord2(Q);
+  std::vector<int64_t> rank(Q), kk(Q);
+  for (int32_t r = 0; r < Q; ++r) {
+    double* nr = nrm.data() + (size_t)r * n;
+    for (int64_t j = 0; j < n; ++j) nr[j] = std::sqrt(nr[j]);
+    auto& o = ord2[r];
+    o.resize(n);
+    for (int64_t j = 0; j < n; ++j) o[j] = static_cast<int32_t>(j);
+    std::stable_sort(o.begin(), o.end(), [&](int32_t a, int32_t b) { return nr[a] > nr[b]; });
+    const double smax = nr[o[0]];
+    int64_t rr = 0;
+    while (rr < n && nr[o[rr]] > 1e-12 * smax) ++rr;
+    rank[r] = rank_out[r] = rr;
+  }
+  for (int32_t r = 0; r < Q; ++r) {
+    if (rank[r] == 0) {
+      c->payload = 0;
+      c->payload_ring = r;
+      return fail(c, XG_ERR_RANK, "gram_svd: matrix is numerically zero, no spectrum");
+    }
+    if (k > rank[r]) {
+      c->payload = rank[r];
+      c->payload_ring = r;
+      return fail(c, XG_ERR_RANK, "requested k = %d exceeds the numerical rank %lld of the "
+                  "training rows (ring %d)", k, (long long)rank[r], r);
+    }
+    // columns that can reach the first k after the final sort (near-ties)
+    kk[r] = k == 0 ? rank[r] : std::min<int64_t>(rank[r], k + 8);
+  }
+  const int64_t kkmax = *std::max_element(kk.begin(), kk.end());
+  // ---- Q0 = kept columns of W (norm order) / |W_j|, then 2 x (Gram, Cholesky, Q R^-1)
+  std::vector<int32_t> hidx((size_t)Q * kkmax, 0);
+  std::vector<double> hsc((size_t)Q * kkmax, 0.0);
+  for (int32_t r = 0; r < Q; ++r)
+    for (int64_t j = 0; j < kk[r]; ++j) {
+      hidx[r * kkmax + j] = ord2[r][j];
+      hsc[r * kkmax + j] = 1.0 / nrm[(size_t)r * n + ord2[r][j]];
+    }
+  int32_t* d_idx;
+  double *d_sc, *d_q[2], *d_g, *d_part, *d_mt;
+  const int max_chunks = static_cast<int>((kpad_max + SYRK_CHUNK - 1) / SYRK_CHUNK);
+  const int64_t part_stride = (int64_t)max_chunks * kkmax * kkmax;
+  XG_CUDA(c, db.get(&d_idx, hidx.size()));
+  XG_CUDA(c, db.get(&d_sc, hsc.size()));
+  XG_CUDA(c, db.get(&d_q[0], (size_t)kkmax * L->ktot));
+  XG_CUDA(c, db.get(&d_q[1], (size_t)kkmax * L->ktot));
+  XG_CUDA(c, db.get(&d_g, (size_t)Q * kkmax * kkmax));
+  XG_CUDA(c, db.get(&d_part, (size_t)Q * part_stride));
+  XG_CUDA(c, db.get(&d_mt, (size_t)Q * kkmax * kkmax));
+  XG_CUDA(c, cudaMemcpyAsync(d_idx, hidx.data(), hidx.size() * 4, cudaMemcpyHostToDevice, st));
+  XG_CUDA(c, cudaMemcpyAsync(d_sc, hsc.data(), hsc.size() * 8, cudaMemcpyHostToDevice, st));
+  for (int32_t r = 0; r < Q; ++r)
+    gr[r] = DGemmRing{d_w + n * L->koff[r], L->kpad[r], nullptr, 0, d_q[0] + kkmax * L->koff[r],
+                      L->kpad[r], (int32_t)kk[r], (int32_t)L->kpad[r], 0};
+  XG_CUDA(c, cudaMemcpyAsync(d_gr, gr.data(), Q * sizeof(DGemmRing), cudaMemcpyHostToDevice, st));
+  XG_CUDA(c, launch_gather_rows(d_gr, d_idx, d_sc, kkmax, Q, (int)kkmax, (int)kpad_max, st));
+  c->launches++;
+  // r_total = R2 R1 D^-1 (linalg.cpp:352-373), D = diag(1 / |W_j|)
+  std::vector<std::vector<double>> rtot(Q);
+  for (int32_t r = 0; r < Q; ++r) rtot[r].assign(kk[r] * kk[r], 0.0);
+  for (int32_t r = 0; r < Q; ++r)
+    for (int64_t j = 0; j < kk[r]; ++j) rtot[r][j * kk[r] + j] = 1.0;
+  std::vector<double> hg((size_t)Q * kkmax * kkmax), hmt((size_t)Q * kkmax * kkmax, 0.0);
+  for (int pass = 0; pass < 2; ++pass) {
+    double* qin = d_q[pass];
+    double* qout = d_q[pass ^ 1];
+    for (int32_t r = 0; r < Q; ++r)
+      gr[r] = DGemmRing{qin + kkmax * L->koff[r], L->kpad[r], nullptr, 0,
+                        d_g + (size_t)r * kkmax * kkmax, kk[r], (int32_t)kk[r],
+                        (int32_t)L->kpad[r], 0};
+    XG_CUDA(c, cudaMemcpyAsync(d_gr, gr.data(), Q * sizeof(DGemmRing), cudaMemcpyHostToDevice, st));
+    XG_CUDA(c, launch_dsyrk(d_gr, Q, (int)kkmax, max_chunks, d_part, part_stride, st));
+    XG_CUDA(c, launch_dsyrk_sum(d_gr, Q, (int)kkmax, max_chunks, d_part, part_stride, st));
+    c->launches += 2;
+    XG_CUDA(c, cudaMemcpyAsync(hg.data(), d_g, hg.size() * 8, cudaMemcpyDeviceToHost, st));
+    XG_CUDA(c, cudaStreamSynchronize(st));
+    std::vector<int64_t> bad(Q, -1);
+    for_rings(Q, [&](int32_t r) {
+      const int64_t m = kk[r];
+      std::vector<double> rf, mt;
+      bad[r] = chol_inv_t(hg.data() + (size_t)r * kkmax * kkmax, m, rf, mt);
+      if (bad[r] >= 0) return;
+      std::copy(mt.begin(), mt.end(), hmt.begin() + (size_t)r * kkmax * kkmax);
+      std::vector<double> nt(m * m, 0.0);  // rtot = rf * rtot
+      for (int64_t i = 0; i < m; ++i)
+        for (int64_t l = i; l < m; ++l) {
+          double v = 0.0;
+          for (int64_t j = i; j <= l; ++j) v += rf[i * m + j] * rtot[r][j * m + l];
+          nt[i * m + l] = v;
+        }
+      rtot[r].swap(nt);
+    });
+    for (int32_t r = 0; r < Q; ++r)
+      if (bad[r] >= 0) {
+        c->payload = bad[r];
+        c->payload_ring = r;
+        return fail(c, XG_ERR_RANK, "gram_svd: column collapse during orthogonalization");
+      }
+    XG_CUDA(c, cudaMemcpyAsync(d_mt, hmt.data(), hmt.size() * 8, cudaMemcpyHostToDevice, st));
+    for (int32_t r = 0; r < Q; ++r)
+      gr[r] = DGemmRing{d_mt + (size_t)r * kkmax * kkmax, kk[r], qin + kkmax * L->koff[r],
+                        L->kpad[r], qout + kkmax * L->koff[r], L->kpad[r], (int32_t)kk[r],
+                        (int32_t)L->kpad[r], (int32_t)kk[r]};
+    XG_CUDA(c, cudaMemcpyAsync(d_gr, gr.data(), Q * sizeof(DGemmRing), cudaMemcpyHostToDevice, st));
+    XG_CUDA(c, launch_dgemm_nn(d_gr, Q, (int)kkmax, (int)kpad_max, false, st));
+    c->launches++;
+  }
+  phase("cholqr2");
+  // ---- orthonormal columns (d_q[0] after two passes) to the host
+  std::vector<double> hq((size_t)kkmax * L->ktot);
+  XG_CUDA(c, cudaMemcpyAsync(hq.data(), d_q[0], hq.size() * 8, cudaMemcpyDeviceToHost, st));
+  XG_CUDA(c, cudaStreamSynchronize(st));
+  std::vector<int> set_rc(Q, XG_OK);
+  for_rings(Q, [&](int32_t r) {
+    const int64_t m = kk[r], kout = k == 0 ? rank[r] : k, mq = L->ring_pixels[r];
+    // sigma_j = |a_j|, a = u_kept r_total^T with orthonormal u: the row norms
+    // of r_total times |W_j| (linalg.cpp:377-383); near-ties re-sorted (:387-391)
+    std::vector<double> sig(m);
+    for (int64_t j = 0; j < m; ++j) {
+      double acc = 0.0;
+      for (int64_t l = j; l < m; ++l) {
+        const double v = rtot[r][j * m + l] * nrm[(size_t)r * n + ord2[r][l]];
+        acc += v * v;
+      }
+      sig[j] = std::sqrt(acc);
+    }
+    std::vector<int64_t> perm(m);
+    for (int64_t j = 0; j < m; ++j) perm[j] = j;
+    std::stable_sort(perm.begin(), perm.end(), [&](int64_t a, int64_t b) { return sig[a] > sig[b]; });
+    if (sigma_out) {
+      double* so = sigma_out + (size_t)r * sigma_ld;
+      for (int64_t j = 0; j < n; ++j) so[j] = 0.0;
+      for (int64_t j = 0; j < m; ++j) so[j] = sig[perm[j]];
+      for (int64_t j = m; j < rank[r]; ++j) so[j] = nrm[(size_t)r * n + ord2[r][j]];
+    }
+    std::vector<double> vloc;
+    double* vo = v_out ? v_out[r] : nullptr;
+    if (!vo) {
+      if (!B) return;
+      vloc.resize(mq * kout);
+      vo = vloc.data();
+    }
+    const int64_t* col = L->colpos.data() + L->mask_off[r];
+    const double* qb = hq.data() + kkmax * L->koff[r];
+    for (int64_t j = 0; j < kout; ++j) {
+      const double* qrow = qb + perm[j] * L->kpad[r];
+      // sign: largest-magnitude entry positive, first in mask order (linalg.cpp:421-436)
+      int64_t arg = 0;
+      double best = -1.0;
+      for (int64_t i = 0; i < mq; ++i) {
+        const double mag = std::fabs(qrow[col[i] - L->koff[r]]);
+        if (mag > best) {
+          best = mag;
+          arg = i;
+        }
+      }
+      const double sg = qrow[col[arg] - L->koff[r]] < 0.0 ? -1.0 : 1.0;
+      for (int64_t i = 0; i < mq; ++i) vo[i * kout + j] = sg * qrow[col[i] - L->koff[r]];
+    }
+    if (B) set_rc[r] = xg_basis_set_ring(B, r, vo);
+  });
+  phase("V out");
+  for (int32_t r = 0; r < Q; ++r)
+    if (set_rc[r]) return set_rc[r];
   return XG_OK;
 }
 

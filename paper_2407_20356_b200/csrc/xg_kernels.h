@@ -329,4 +329,101 @@ struct SynthParams {
 };
 cudaError_t launch_synth(const SynthParams& p, cudaStream_t s);
 
+// ---------------------------------------------------------- K9 basis (gram_svd on the device)
+// Gram-trick SVD of every ring's training frames (linalg.cpp:279-439):
+// S = G_q / (|x_i||x_j|) from the exact int32 Gram, parallel-order Jacobi on
+// S, W = Xn^T U (f64 GEMM over the ring-major u8 frames), column norms,
+// Cholesky-QR x2 (the host factors the k x k Gram), K9.
+// Circle-method pairing of step s over np indices (np even, R = np - 1 fixed
+// point).  Pair 0 = (R, s); pair k >= 1 = (s + k, s - k) mod R.  Within a pair
+// the smaller original index takes the even slot (p < q, as the reference).
+__host__ __device__ inline int slot_index(int slot, int s, int np) {
+  const int R = np - 1, k = slot >> 1;
+  int x, y;
+  if (k == 0) {
+    x = R;
+    y = s;
+  } else {
+    x = (s + k) % R;
+    y = (s - k + R) % R;
+  }
+  const int lo = (x < y ? x : y), hi = (x < y ? y : x);
+  return (slot & 1) ? hi : lo;
+}
+
+__host__ __device__ inline int index_slot(int i, int s, int np) {
+  const int R = np - 1, half = np >> 1;
+  int k, partner;
+  if (i == R) {
+    k = 0;
+    partner = s;
+  } else {
+    const int d = (i - s + R) % R;
+    if (d == 0) {
+      k = 0;
+      partner = R;
+    } else if (d <= half - 1) {
+      k = d;
+      partner = (s - d + R) % R;
+    } else {
+      k = R - d;
+      partner = (s + k) % R;
+    }
+  }
+  return 2 * k + (i > partner ? 1 : 0);
+}
+
+struct JacState {
+  double tol;                // reference threshold, x100 per 10 sweeps after 40
+  int32_t active;            // 0 once a whole sweep rotated nothing
+  int32_t rotated;           // set by the step kernels of the current sweep
+};
+struct JacParams {
+  const double* a_in;        // [ring][np][np] slot layout of this step
+  double* a_out;             // [ring][np][np] slot layout of the next step
+  const double* v_in;        // [ring][np][np] rows: coordinates, cols: slots
+  double* v_out;
+  JacState* state;           // [ring]
+  int32_t np;                // padded (even) order
+  int32_t step;              // 0 .. np-2 within the sweep
+};
+cudaError_t launch_jacobi_step(const JacParams& p, int n_rings, cudaStream_t s);
+
+struct BasisSParams {
+  const int32_t* gram;       // [ring][ld][ld] upper tiles
+  int32_t ld;
+  const double* inv;         // [ring][inv_ld]
+  int64_t inv_ld;
+  int32_t n, np;
+  double* a;                 // [ring][np][np] slot layout of step 0
+  double* v;                 // [ring][np][np] identity in slot layout
+};
+cudaError_t launch_basis_s(const BasisSParams& p, int n_rings, cudaStream_t s);
+// diag of the converged A (slot layout of step 0) -> eig [ring][np]
+cudaError_t launch_jacobi_diag(const double* const* a_ring, double* eig, int np, int n_rings,
+                               cudaStream_t s);
+
+// One ring's operands of the f64 GEMMs: C[M x N] = A[M x K] * B[K x N]
+// (B u8 or f64, row-major), or the Gram C[M x M] = A A^T split over K.
+struct DGemmRing {
+  const double* a;  int64_t lda;
+  const void* b;    int64_t ldb;
+  double* c;        int64_t ldc;
+  int32_t m, n, k;
+};
+cudaError_t launch_dgemm_nn(const DGemmRing* d_rings, int n_rings, int max_m, int max_n,
+                            bool b_u8, cudaStream_t s);
+constexpr int SYRK_CHUNK = 2048;
+// partial [ring][chunk][m][m] (ring stride part_stride), then a fixed-order sum
+cudaError_t launch_dsyrk(const DGemmRing* d_rings, int n_rings, int max_m, int max_chunks,
+                         double* partial, int64_t part_stride, cudaStream_t s);
+cudaError_t launch_dsyrk_sum(const DGemmRing* d_rings, int n_rings, int max_m, int max_chunks,
+                             const double* partial, int64_t part_stride, cudaStream_t s);
+// row norms^2 of C rows [0, m) over n columns (fixed-order tree)
+cudaError_t launch_row_norm2(const DGemmRing* d_rings, int n_rings, int max_m, double* out,
+                             int64_t out_ld, cudaStream_t s);
+// dst row j = src row idx[j] * scale[j]  (idx/scale [ring][ld_idx])
+cudaError_t launch_gather_rows(const DGemmRing* d_rings, const int32_t* idx, const double* scale,
+                               int64_t ld_idx, int n_rings, int max_m, int max_n, cudaStream_t s);
+
 }  // namespace xg
