@@ -11,7 +11,7 @@ import os
 import re
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libxpcs_b200.so")
+LIB_PATH = os.environ.get("XG_LIB_OVERRIDE") or os.path.join(HERE, "libxpcs_b200.so")  # override: dev A/B probes only
 HEADER = os.path.join(os.path.dirname(HERE), "include", "xpcs_b200.h")
 
 if not os.path.exists(LIB_PATH):

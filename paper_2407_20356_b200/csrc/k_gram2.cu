@@ -67,7 +67,17 @@ struct __align__(1024) Tail2 {
   float2 inv_row2[BM];            // (hi, lo) float split of the same weights
   float2 inv_col2_ext[BN + 64];
   float2 acc[EPI_WARPS][NDIAG_PAD];  // per-diagonal (hi, lo) double-float sums
+  // K4: each epilogue warp's window sums of one tile (2 tiles in flight),
+  // folded by warp 3 (aliases acc: 2 x 8 x 160 <= 8 x 384 float2)
+  uint64_t accfull[2];
+  uint64_t accfree[2];
 };
+constexpr int WSLOTS = 160;  // 5 windows x 32 diagonals per K4 epilogue warp
+
+// K4 epilogue warp (sub, grp): windows [w_lo, w_lo + nwin) -- group 0 takes
+// windows 0..4, group 1 windows 5..8 (window 4 belongs to group 0).
+__device__ __forceinline__ int k4_wlo(int grp) { return grp ? 5 : 0; }
+__device__ __forceinline__ int k4_nwin(int grp) { return grp ? 4 : 5; }
 
 // f32 bits -> f64 with integer ops only (normal numbers; zero and
 // denormals -> +-0, far below the compressed path's 1e-5 tolerance)
@@ -135,6 +145,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tail->tfull[a], 1);
       mbar_init(&tail->tempty[a], 2 * EPI_WARPS);  // epilogue warps of both CTAs
+      mbar_init(&tail->accfull[a], EPI_WARPS);
+      mbar_init(&tail->accfree[a], 1);
     }
     fence_barrier_init();
     tma_prefetch(&tmX);
@@ -257,6 +269,38 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
         }
       }
     }
+  } else if (MODE == 1 && warp == 3) {
+    // K4 g2 fold: sums the 8 epilogue warps' window slots of each tile in a
+    // fixed warp order and writes the tile's diagonal sums, so the epilogue
+    // warps never meet at a barrier (they run up to 2 tiles ahead).
+    if (p.g2_partial) {
+      float2(*acc2)[EPI_WARPS][WSLOTS] = reinterpret_cast<float2(*)[EPI_WARPS][WSLOTS]>(&tail->acc[0][0]);
+      int it = 0;
+      for (int t = pair; t < p.ntiles; t += npairs, ++it) {
+        const int buf = it & 1;
+        if (!mbar_wait(&tail->accfull[buf], (it >> 1) & 1, p.err)) break;
+        const TileDesc td = p.tiles[t];
+        if (2 * (td.i0 / 256) + static_cast<int>(rank) < p.g2_nbi) {
+          const int64_t half = td.pad + static_cast<int64_t>(rank) * (p.g2_nbj - td.i0 / 256);
+          float2* out = p.g2_partial + half * NDIAG_PAD;
+          for (int e = lane; e < NDIAG; e += 32) {
+            float2 sum = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int w = 0; w < EPI_WARPS; ++w) {
+              const int sb = w & 3, gp = w >> 2;
+              const int off = e - 96 + 32 * sb - 32 * k4_wlo(gp);
+              if (off >= 0 && off < 32 * k4_nwin(gp)) {
+                const float2 v = acc2[buf][w][off];
+                sum = dd_add(sum, v.x, v.y);
+              }
+            }
+            out[e] = sum;
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tail->accfree[buf]);
+      }
+    }
   } else if (warp >= 4) {
     const int ew = warp - 4;        // epilogue warp 0..7
     const int sub = warp & 3;       // TMEM lane quarter this warp may access
@@ -267,13 +311,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
     uint32_t acc_phase = 0;
     bool ok = true;
     uint32_t* S = tail->stage[ew];
+    // K4 window walk: word offset (in the warp's two staging buffers, chunk
+    // c-1 in buffer 0 and chunk c in buffer 1) of this lane's element in row
+    // l; an even chunk c swaps the buffers (offset ^ 1024)
+    int wtab[MODE == 1 ? 32 : 1];
+    if (MODE == 1)
+#pragma unroll
+      for (int l = 0; l < 32; ++l) {
+        const int u = lane + 1 + l;
+        wtab[l] = (u >> 5) * 1024 + l * 32 + ((u & 31) ^ ((l & 7) << 2));
+      }
     for (int t = pair; t < p.ntiles; t += npairs) {
       const TileDesc td = p.tiles[t];
       const int i0 = td.i0 + 128 * static_cast<int>(rank);  // this CTA's half tile
       if (ok) ok = mbar_wait(&tail->tfull[acc], acc_phase, p.err);
       ok = __all_sync(0xffffffffu, ok);
       if (ok) tc_fence_after();
-      if (p.g2_partial) {
+      const int it = (t - pair) / npairs, buf = it & 1;
+      float2* slots = MODE == 1 ? reinterpret_cast<float2*>(&tail->acc[0][0]) +
+                                      (buf * EPI_WARPS + ew) * WSLOTS
+                                : nullptr;
+      if (MODE == 1 && p.g2_partial && it >= 2)  // warp 3 has folded this buffer's last tile
+        if (!mbar_wait(&tail->accfree[buf], ((it >> 1) - 1) & 1, p.err)) ok = false;
+      if (MODE == 0 && p.g2_partial) {
         epi_bar<EPI_WARPS>();
         const double* inv = MODE == 0 ? p.inv + static_cast<int64_t>(td.ring) * p.inv_ld : nullptr;
         const float2* inv2 = MODE == 0 ? p.inv2 + static_cast<int64_t>(td.ring) * p.inv_ld : nullptr;
@@ -319,7 +379,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
       const uint32_t tbase =
           tmem_base + static_cast<uint32_t>(acc * BN) + (static_cast<uint32_t>(sub * 32) << 16);
       const int out_row = td.ring * p.ld + i0 + 32 * sub;
-      const bool full_cols = td.j0 + BN <= p.n_frames;  // every tile column is a frame
       // Column chunks c (32 wide) go through staging buffer c & 1.  Group 0
       // stores chunks 0..3 and also loads chunk 4 (for window 4); group 1
       // stores 4..7.  Window w spans chunks w-1 and w (64 columns): lane L
@@ -358,6 +417,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
         const int w = c;  // window of chunks c-1, c
         if (p.g2_partial && !(EPI_WARPS == 8 && grp == 1 && w == 4)) {
           const int lagw = td.j0 - i0 + 32 * (w - 1 - sub) + lane + 1;  // this lane's lag
+          if (MODE == 1 && lagw < 0) slots[32 * (w - k4_wlo(grp)) + lane] = make_float2(0.f, 0.f);
           if (lagw >= 0) {
             const uint32_t* Sp = S + ((c - 1) & 1) * 1024;
             float wh, wl;  // this window's diagonal sum as (hi, lo)
@@ -368,18 +428,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
               const float2* ir2 = tail->inv_row2 + 32 * sub;
               const float2* ic2 = tail->inv_col2_ext + 32 * (w - 1) + 32 + lane + 1;
               float sh = 0.f, sl = 0.f;
-              if (MODE == 1 && full_cols) {
-                // every tile column is a frame: plain fp32 sum, no mask
+              if (MODE == 1 && w >= 1 && real && td.j0 + 32 * w + 32 <= p.n_frames) {
+                // both chunks hold frames only: plain fp32 sum over the
+                // precomputed walk, two interleaved partial sums
+                const int flip = (c & 1) ? 0 : 1024;
+                float s0 = 0.f, s1 = 0.f;
 #pragma unroll
-                for (int l = 0; l < 32; ++l) {
-                  const int cr = lane + 1 + l;
-                  const int kk = cr & 31;
-                  const uint32_t* B = cr < 32 ? Sp : Sc;
-                  const bool zero = cr < 32 ? (w == 0) : !real;
-                  const uint32_t wv =
-                      zero ? 0u : B[l * 32 + (((kk >> 2) ^ (l & 7)) << 2) + (kk & 3)];
-                  sh += __uint_as_float(wv);
+                for (int l = 0; l < 32; l += 2) {
+                  s0 += __uint_as_float(S[wtab[l] ^ flip]);
+                  s1 += __uint_as_float(S[wtab[l + 1] ^ flip]);
                 }
+                sh = s0 + s1;
               } else
 #pragma unroll
               for (int l = 0; l < 32; ++l) {
@@ -401,8 +460,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
                   ql = __fmaf_rn(g, pe, __fmaf_rn(g, ph, -qh));
                 } else {
                   // C~ is fp32 already (~1e-6): a plain fp32 sum of the 32
-                  // window terms adds < 2e-6 relative; windows add in fp64
-                  sh += ic2[l].x != 0.f ? __uint_as_float(wv) : 0.f;
+                  // window terms adds < 2e-6 relative; columns past the
+                  // last frame are masked
+                  sh += td.j0 + 32 * (w - 1) + cr < p.n_frames ? __uint_as_float(wv) : 0.f;
                   continue;
                 }
                 const float t = __fadd_rn(sh, qh);  // TwoSum(sh, qh)
@@ -436,11 +496,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
             }
             // double-float accumulation: the FP64 pipe stalls the tensor-core
             // pipeline on this part, FP32 does not
-            float2* ap = &tail->acc[ew][32 * (w - 1 - sub) + lane + 1 + 127];
-            *ap = dd_add(*ap, wh, wl);
+            if (MODE == 1) {
+              slots[32 * (w - k4_wlo(grp)) + lane] = make_float2(wh, wl);
+            } else {
+              float2* ap = &tail->acc[ew][32 * (w - 1 - sub) + lane + 1 + 127];
+              *ap = dd_add(*ap, wh, wl);
+            }
           }
           __syncwarp();
         }
+      }
+      if (MODE == 1 && p.g2_partial) {  // this warp's window slots of the tile are written
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tail->accfull[buf]);
       }
       if (ok) {
         tc_fence_before();
@@ -452,7 +520,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
             arrive_leader(&tail->tempty[acc]);
         }
       }
-      if (p.g2_partial) {
+      if (MODE == 0 && p.g2_partial) {
         epi_bar<EPI_WARPS>();
         // the 1-CTA enumeration index of this half tile (ib = 2I + rank); a
         // second half past the last 128-row block holds only rows >= T
