@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(256) k_stream_proj_acc(StreamParams p) {
 }
 
 // K6a': digit sums -> coefficients with the batch projection's expression
-// (bitwise-equal rows); resets pacc (and nz_n when this is the last pass).
+// (bitwise-equal rows); resets pacc.
 __global__ void __launch_bounds__(128) k_stream_proj_fin(StreamParams p) {
   const int r = blockIdx.x;
   int32_t* pa = p.pacc + static_cast<int64_t>(r) * 768;
@@ -140,7 +140,6 @@ __global__ void __launch_bounds__(128) k_stream_proj_fin(StreamParams p) {
   }
   __syncthreads();
   for (int j = threadIdx.x; j < p.n_digits * p.k; j += blockDim.x) pa[j] = 0;
-  if (threadIdx.x == 0 && p.nz_reset == 2) p.nz_n[r] = 0;
 }
 
 // K6b: grid (ceil((t+1)/SR_ROWS), rings); a warp per history row.
@@ -197,6 +196,11 @@ __global__ void __launch_bounds__(SR_THREADS) k_stream_cmp(StreamParams p) {
 // from one atomic per warp; any order, the column sums are integer) and
 // scattered into the pixel-major history.
 __global__ void __launch_bounds__(128) k_stream_ingest(StreamParams p) {
+  if (blockIdx.x == 0)  // the next push's counters
+    for (int r = threadIdx.x; r < p.n_rings; r += blockDim.x) {
+      if (p.nz_next) p.nz_next[r] = 0;
+      if (p.norm2_next) p.norm2_next[r] = 0ull;
+    }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t blk = static_cast<int64_t>(blockIdx.x) * 4 + warp;
   if (blk * 128 >= p.ktot) return;  // warp-uniform
@@ -236,72 +240,161 @@ __global__ void __launch_bounds__(128) k_stream_ingest(StreamParams p) {
   }
 }
 
-// K5s-b: grid (ceil((t+1)/2048), rings, SS_Z).  A thread owns 8 consecutive
-// history frames s and walks its z-slice of the ring's nonzeros: one
-// coalesced 64-bit load of hist[c][s..s+7] per nonzero; the slices' partial
-// integer sums meet in colbuf (integer atomics: exact, order-free).
-constexpr int SS_THREADS = 256;
-constexpr int SS_S = 8;             // history frames per thread
+// K1s (sparse mode): the new frame in pixel order, 1024 pixels per CTA (4
+// per thread, one 32-bit load).  Only nonzero pixels look up their packed
+// (ring << 22 | column) entry; the CTA counts them per ring in shared memory,
+// reserves each ring's run of the nonzero list with ONE global atomic, then
+// writes (column, value) and hist[column][t].  |x_t|^2 per ring likewise
+// meets in shared memory first (integer sums: exact, order-free).  Block 0
+// clears the next push's counters (nz_next, norm2 row t + 1).
+constexpr int SI_THREADS = 256;
+constexpr int SI_MAXQ = 1024;
+__global__ void __launch_bounds__(SI_THREADS) k_stream_ingest_sparse(StreamParams p) {
+  __shared__ uint32_t cnt[SI_MAXQ], sq[SI_MAXQ];
+  __shared__ int32_t base[SI_MAXQ];
+  if (blockIdx.x == 0)
+    for (int r = threadIdx.x; r < p.n_rings; r += blockDim.x) {
+      p.nz_next[r] = 0;
+      if (p.norm2_next) p.norm2_next[r] = 0ull;
+    }
+  for (int r = threadIdx.x; r < p.n_rings; r += blockDim.x) cnt[r] = sq[r] = 0;
+  const int64_t px0 = (static_cast<int64_t>(blockIdx.x) * SI_THREADS + threadIdx.x) * 4;
+  uint32_t w = 0;
+  if (px0 + 4 <= p.pixels) {
+    w = __ldcs(reinterpret_cast<const uint32_t*>(p.frame + px0));
+  } else {
+    for (int b = 0; b < 4; ++b)
+      if (px0 + b < p.pixels) w |= static_cast<uint32_t>(p.frame[px0 + b]) << (8 * b);
+  }
+  int ent[4], loc[4];
+  __syncthreads();
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    ent[b] = -1;
+    const uint32_t v = (w >> (8 * b)) & 0xFFu;
+    if (!v) continue;
+    const int e = p.pixcol[px0 + b];
+    if (e < 0) continue;
+    ent[b] = e;
+    const int r = e >> 22;
+    loc[b] = static_cast<int>(atomicAdd(&cnt[r], 1u));
+    atomicAdd(&sq[r], v * v);
+  }
+  __syncthreads();
+  for (int r = threadIdx.x; r < p.n_rings; r += blockDim.x) {
+    if (cnt[r]) {
+      base[r] = p.ring_koff[r] + atomicAdd(p.nz_n + r, static_cast<int>(cnt[r]));
+      atomicAdd(p.norm2 + p.t * p.n_rings + r, static_cast<unsigned long long>(sq[r]));
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    if (ent[b] < 0) continue;
+    const int r = ent[b] >> 22, col = ent[b] & 0x3FFFFF;
+    const uint8_t v = static_cast<uint8_t>((w >> (8 * b)) & 0xFFu);
+    const int64_t e = base[r] + loc[b];
+    p.nz_col[e] = col;
+    p.nz_val[e] = v;
+    if (p.hist) p.hist[static_cast<int64_t>(col) * p.hp + p.t] = v;
+  }
+}
+
+// K5s: grid (ceil((t+1)/SS_F), rings), 8 warps.  A CTA owns SS_F = 32 SS_V
+// history frames s: lane L of every warp holds SS_V consecutive s and warp w
+// walks the nonzeros i = w, w+8, ... of the ring, one coalesced SS_V-byte
+// load of hist[c_i][s..] per nonzero (SS_U of them in flight); the 8 warps'
+// integer partial sums meet in shared memory (exact, fixed order), and the
+// CTA finishes its column entries itself: C, g2 lag sums, optional stored
+// column -- the dense K5's expressions, so the results equal it bitwise.  No
+// atomics, no second pass.
 constexpr int SS_CHUNK = 1024;
-constexpr int SS_Z = 8;
-__global__ void __launch_bounds__(SS_THREADS) k_stream_sparse_col(StreamParams p) {
+#ifndef XG_SS_V
+#define XG_SS_V 8
+#endif
+#ifndef XG_SS_U
+#define XG_SS_U 8
+#endif
+constexpr int SS_V = XG_SS_V;  // history frames per lane (one 8- or 16-byte load)
+constexpr int SS_U = XG_SS_U;  // loads in flight per lane
+constexpr int SS_F = 32 * SS_V;  // history frames per CTA
+template <int V> struct SsVec;
+template <> struct SsVec<8> {
+  using T = uint2;
+  __device__ static void words(const T& v, uint32_t* w) { w[0] = v.x; w[1] = v.y; }
+  __device__ static T zero() { return make_uint2(0u, 0u); }
+};
+template <> struct SsVec<16> {
+  using T = uint4;
+  __device__ static void words(const T& v, uint32_t* w) { w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w; }
+  __device__ static T zero() { return make_uint4(0u, 0u, 0u, 0u); }
+};
+__global__ void __launch_bounds__(256) k_stream_sparse(StreamParams p) {
+  using VT = typename SsVec<SS_V>::T;
   __shared__ int32_t sc[SS_CHUNK];
   __shared__ uint32_t sv[SS_CHUNK];
+  __shared__ uint32_t red[8][SS_F + 1];
   const int r = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int koff = p.ring_koff[r];
   const int n = p.nz_n[r];
-  const int zb = static_cast<int>((static_cast<int64_t>(n) * blockIdx.z) / SS_Z);
-  const int ze = static_cast<int>((static_cast<int64_t>(n) * (blockIdx.z + 1)) / SS_Z);
-  const int64_t s0 = static_cast<int64_t>(blockIdx.x) * (SS_S * SS_THREADS) + SS_S * threadIdx.x;
-  uint32_t acc[SS_S];
+  const int64_t sb = static_cast<int64_t>(blockIdx.x) * SS_F;
+  const int64_t s0 = sb + SS_V * lane;
+  uint32_t acc[SS_V];
 #pragma unroll
-  for (int j = 0; j < SS_S; ++j) acc[j] = 0;
-  for (int c0 = zb; c0 < ze; c0 += SS_CHUNK) {
-    const int cn = ze - c0 < SS_CHUNK ? ze - c0 : SS_CHUNK;
+  for (int j = 0; j < SS_V; ++j) acc[j] = 0;
+  const uint8_t* h = p.hist + s0;
+  for (int c0 = 0; c0 < n; c0 += SS_CHUNK) {
+    const int cn = n - c0 < SS_CHUNK ? n - c0 : SS_CHUNK;
     __syncthreads();
-    for (int i = threadIdx.x; i < cn; i += SS_THREADS) {
+    for (int i = threadIdx.x; i < cn; i += 256) {
       sc[i] = p.nz_col[koff + c0 + i];
       sv[i] = p.nz_val[koff + c0 + i];
     }
     __syncthreads();
     if (s0 <= p.t) {
-      const uint8_t* h = p.hist + s0;
-      // latency-bound on the scattered history rows: keep 16 loads in flight
-#pragma unroll 16
-      for (int i = 0; i < cn; ++i) {
-        const uint2 w = __ldcs(reinterpret_cast<const uint2*>(h + static_cast<int64_t>(sc[i]) * p.hp));
-        const uint32_t v = sv[i];
+      // SS_U independent loads in flight per lane before any use
+      for (int i0 = warp; i0 < cn; i0 += 8 * SS_U) {
+        VT wv[SS_U];
+        uint32_t vv[SS_U];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          acc[j] += v * ((w.x >> (8 * j)) & 0xFFu);
-          acc[4 + j] += v * ((w.y >> (8 * j)) & 0xFFu);
+        for (int u = 0; u < SS_U; ++u) {
+          const int i = i0 + 8 * u;
+          const bool in = i < cn;
+          vv[u] = in ? sv[i] : 0u;
+          wv[u] = in ? __ldcs(reinterpret_cast<const VT*>(h + static_cast<int64_t>(sc[i]) * p.hp))
+                     : SsVec<SS_V>::zero();
+        }
+#pragma unroll
+        for (int u = 0; u < SS_U; ++u) {
+          uint32_t ww[SS_V / 4];
+          SsVec<SS_V>::words(wv[u], ww);
+#pragma unroll
+          for (int q = 0; q < SS_V / 4; ++q)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[4 * q + j] += vv[u] * ((ww[q] >> (8 * j)) & 0xFFu);
         }
       }
     }
   }
-  if (s0 > p.t) return;
-  int32_t* col = p.colbuf + static_cast<int64_t>(r) * p.hp + s0;
 #pragma unroll
-  for (int j = 0; j < SS_S; ++j)
-    if (acc[j] && s0 + j <= p.t) atomicAdd(col + j, static_cast<int>(acc[j]));
-}
-
-// K5s-c: the finished column -> C, g2 lag sums and the optional stored column
-// (the dense K5's expressions, so equal bitwise); resets colbuf and nz_n.
-__global__ void __launch_bounds__(256) k_stream_sparse_fin(StreamParams p) {
-  const int r = blockIdx.y;
-  const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (blockIdx.x == 0 && threadIdx.x == 0 && p.nz_reset == 1) p.nz_n[r] = 0;
-  if (s > p.t) return;
-  int32_t* col = p.colbuf + static_cast<int64_t>(r) * p.hp + s;
-  const int acc = *col;
-  *col = 0;
+  for (int j = 0; j < SS_V; ++j) red[warp][SS_V * lane + j] = acc[j];
+  __syncthreads();
   const double inv_t = p.inv[static_cast<int64_t>(r) * p.inv_ld + p.t];
-  const double inv_s = p.inv[static_cast<int64_t>(r) * p.inv_ld + s];
-  const int64_t gi = static_cast<int64_t>(r) * p.g2_ld + (p.t - s);
-  p.g2sum[gi] += static_cast<double>(acc) * (inv_s * inv_t);
-  p.g2cnt[gi] += (inv_s != 0.0 && inv_t != 0.0) ? 1 : 0;
-  if (p.gcol) p.gcol[static_cast<int64_t>(r) * p.col_ring_stride + s * p.col_ld + p.t] = acc;
+#pragma unroll
+  for (int f = threadIdx.x; f < SS_F; f += 256) {
+    const int64_t s = sb + f;
+    if (s > p.t) break;
+    uint32_t tot = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) tot += red[w][f];
+    const int accv = static_cast<int>(tot);
+    const double inv_s = p.inv[static_cast<int64_t>(r) * p.inv_ld + s];
+    const int64_t gi = static_cast<int64_t>(r) * p.g2_ld + (p.t - s);
+    p.g2sum[gi] += static_cast<double>(accv) * (inv_s * inv_t);
+    p.g2cnt[gi] += (inv_s != 0.0 && inv_t != 0.0) ? 1 : 0;
+    if (p.gcol) p.gcol[static_cast<int64_t>(r) * p.col_ring_stride + s * p.col_ld + p.t] = accv;
+  }
 }
 
 cudaError_t launch_stream_ingest(const StreamParams& p, cudaStream_t s) {
@@ -310,14 +403,16 @@ cudaError_t launch_stream_ingest(const StreamParams& p, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+cudaError_t launch_stream_ingest_sparse(const StreamParams& p, cudaStream_t s) {
+  if (p.n_rings > SI_MAXQ) return cudaErrorInvalidValue;
+  const unsigned blocks = static_cast<unsigned>((p.pixels + 4 * SI_THREADS - 1) / (4 * SI_THREADS));
+  k_stream_ingest_sparse<<<blocks, SI_THREADS, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_stream_sparse(const StreamParams& p, int32_t n_rings, cudaStream_t s) {
-  dim3 grid(static_cast<unsigned>((p.t + 1 + SS_S * SS_THREADS - 1) / (SS_S * SS_THREADS)),
-            n_rings, SS_Z);
-  k_stream_sparse_col<<<grid, SS_THREADS, 0, s>>>(p);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
-  dim3 g2(static_cast<unsigned>((p.t + 1 + 255) / 256), n_rings);
-  k_stream_sparse_fin<<<g2, 256, 0, s>>>(p);
+  dim3 grid(static_cast<unsigned>((p.t + 1 + SS_F - 1) / SS_F), n_rings);
+  k_stream_sparse<<<grid, 256, 0, s>>>(p);
   return cudaGetLastError();
 }
 

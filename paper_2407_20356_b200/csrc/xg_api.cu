@@ -1910,12 +1910,12 @@ struct xg_stream {
   uint8_t* d_hist = nullptr;  // sparse mode: pixel-major history [ktot][hp]
   int32_t* d_colpix = nullptr;  // [ktot] detector pixel of each column (-1 = padding)
   int32_t* d_blk_ring = nullptr;  // [ktot/128] ring of each 128-column block
-  int32_t* d_colbuf = nullptr;  // sparse mode: [ring][hp] partial column sums
+  int32_t* d_pixcol = nullptr;  // sparse mode: [pixels] ring << 22 | column (-1: no ring)
   int32_t* d_pacc = nullptr;    // with a basis: [ring][768] projection digit sums
   int64_t hp = 0;
   int32_t* d_nz_col = nullptr;
   uint8_t* d_nz_val = nullptr;
-  int32_t* d_nz_n = nullptr;
+  int32_t* d_nz_n = nullptr;     // [2][ring]: counts of even / odd pushes
 };
 
 extern "C" {
@@ -1941,7 +1941,9 @@ int xg_stream_create(xg_ctx* c, const xg_layout* L, const xg_basis* B, int64_t m
   cudaError_t e = cudaSuccess;
   const bool store = (flags & XG_STREAM_STORE_TTC) != 0;
   if ((e = dalloc(&s->d_frame, (size_t)L->pixels)) != cudaSuccess ||
-      (e = dalloc(&s->d_x, (size_t)max_frames * L->ktot)) != cudaSuccess ||
+      // the ring-major u8 history (dense K5); sparse mode keeps hist instead
+      (e = dalloc(&s->d_x, (flags & XG_STREAM_SPARSE) ? 1 : (size_t)max_frames * L->ktot)) !=
+          cudaSuccess ||
       (e = dalloc(&s->d_norm2, (size_t)max_frames * Q)) != cudaSuccess ||
       (e = dalloc(&s->d_zero, (size_t)Q)) != cudaSuccess ||
       (e = dalloc(&s->d_first_zero, (size_t)Q)) != cudaSuccess ||
@@ -1965,22 +1967,32 @@ int xg_stream_create(xg_ctx* c, const xg_layout* L, const xg_basis* B, int64_t m
       return cuda_fail(c, e, "stream sparse history alloc");
     }
     cudaMemsetAsync(s->d_hist, 0, (size_t)L->ktot * s->hp, c->stream);
-    if ((e = dalloc(&s->d_colbuf, (size_t)Q * s->hp)) != cudaSuccess) {
+    // packed (ring << 22 | column) of every pixel, -1 outside the rings
+    std::vector<int32_t> pc(static_cast<size_t>(L->pixels), -1);
+    if (L->ktot >= (1 << 22) || L->rings > 512) {
       xg_stream_destroy(s);
-      return cuda_fail(c, e, "stream sparse column alloc");
+      return fail(c, XG_ERR_CONTRACT, "sparse stream: at most 2^22 columns and 512 rings");
     }
-    cudaMemsetAsync(s->d_colbuf, 0, (size_t)Q * s->hp * 4, c->stream);
+    for (int32_t r = 0; r < L->rings; ++r)
+      for (int64_t col = L->koff[r]; col < L->koff[r] + L->kpad[r]; ++col)
+        if (L->colpix[col] >= 0) pc[L->colpix[col]] = (r << 22) | static_cast<int32_t>(col);
+    if ((e = dalloc(&s->d_pixcol, pc.size())) != cudaSuccess ||
+        (e = cudaMemcpy(s->d_pixcol, pc.data(), pc.size() * 4, cudaMemcpyHostToDevice)) !=
+            cudaSuccess) {
+      xg_stream_destroy(s);
+      return cuda_fail(c, e, "stream sparse pixel table");
+    }
   }
   if ((flags & XG_STREAM_SPARSE) || B) {
     // the new frame's nonzeros per ring (sparse raw column, sparse projection)
     if ((e = dalloc(&s->d_nz_col, (size_t)L->ktot)) != cudaSuccess ||
         (e = dalloc(&s->d_nz_val, (size_t)L->ktot)) != cudaSuccess ||
-        (e = dalloc(&s->d_nz_n, (size_t)Q)) != cudaSuccess ||
+        (e = dalloc(&s->d_nz_n, (size_t)2 * Q)) != cudaSuccess ||
         (B && (e = dalloc(&s->d_pacc, (size_t)Q * 768)) != cudaSuccess)) {
       xg_stream_destroy(s);
       return cuda_fail(c, e, "stream nonzero lists alloc");
     }
-    cudaMemsetAsync(s->d_nz_n, 0, (size_t)Q * 4, c->stream);
+    cudaMemsetAsync(s->d_nz_n, 0, (size_t)2 * Q * 4, c->stream);
     if (B) cudaMemsetAsync(s->d_pacc, 0, (size_t)Q * 768 * 4, c->stream);
   }
   {
@@ -1998,7 +2010,8 @@ int xg_stream_create(xg_ctx* c, const xg_layout* L, const xg_basis* B, int64_t m
       return cuda_fail(c, e, "stream ingest tables");
     }
   }
-  cudaMemsetAsync(s->d_x, 0, (size_t)max_frames * L->ktot, c->stream);
+  if (!(flags & XG_STREAM_SPARSE)) cudaMemsetAsync(s->d_x, 0, (size_t)max_frames * L->ktot, c->stream);
+  cudaMemsetAsync(s->d_norm2, 0, (size_t)max_frames * Q * 8, c->stream);
   cudaMemsetAsync(s->d_zero, 0, (size_t)Q * 8, c->stream);
   cudaMemsetAsync(s->d_first_zero, 0x7F, (size_t)Q * 8, c->stream);
   cudaMemsetAsync(s->d_nz_bits, 0, (size_t)Q * (s->tp / 32) * 4, c->stream);
@@ -2059,7 +2072,7 @@ void xg_stream_destroy(xg_stream* s) {
   dfree(s->d_hist);
   dfree(s->d_colpix);
   dfree(s->d_blk_ring);
-  dfree(s->d_colbuf);
+  dfree(s->d_pixcol);
   dfree(s->d_pacc);
   dfree(s->d_nz_col);
   dfree(s->d_nz_val);
@@ -2074,9 +2087,15 @@ int xg_stream_push(xg_stream* s, const uint8_t* frame, int on_device) {
   xg_ctx* c = s->ctx;
   const xg_layout* L = s->L;
   if (s->t >= s->tmax) return fail(c, XG_ERR_SHAPE, "stream: capacity %lld reached", (long long)s->tmax);
-  XG_CUDA(c, cudaMemcpyAsync(s->d_frame, frame, (size_t)L->pixels,
-                             on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
-                             c->stream));
+  // a device frame is read in place when 16-byte aligned (stream-ordered:
+  // the caller keeps it valid until the push's work has run)
+  const uint8_t* d_frame = s->d_frame;
+  if (on_device && (reinterpret_cast<uintptr_t>(frame) & 15u) == 0)
+    d_frame = frame;
+  else
+    XG_CUDA(c, cudaMemcpyAsync(s->d_frame, frame, (size_t)L->pixels,
+                               on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                               c->stream));
   StreamParams sp;
   sp.x = s->d_x;
   sp.ktot = L->ktot;
@@ -2106,17 +2125,23 @@ int xg_stream_push(xg_stream* s, const uint8_t* frame, int on_device) {
   sp.hp = s->hp;
   sp.nz_col = s->d_nz_col;
   sp.nz_val = s->d_nz_val;
-  sp.nz_n = s->d_nz_n;
-  sp.colbuf = s->d_colbuf;
+  sp.nz_n = s->d_nz_n ? s->d_nz_n + (s->t & 1) * L->rings : nullptr;
+  sp.nz_next = s->d_nz_n ? s->d_nz_n + ((s->t + 1) & 1) * L->rings : nullptr;
   sp.pacc = s->d_pacc;
-  sp.nz_reset = s->B ? 2 : 1;
-  sp.frame = s->d_frame;
+  sp.frame = d_frame;
+  sp.pixcol = s->d_pixcol;
+  sp.pixels = L->pixels;
   sp.colpix = s->d_colpix;
   sp.blk_ring = s->d_blk_ring;
   sp.n_rings = L->rings;
   sp.norm2 = reinterpret_cast<unsigned long long*>(s->d_norm2);
-  XG_CUDA(c, cudaMemsetAsync(s->d_norm2 + s->t * L->rings, 0, (size_t)L->rings * 8, c->stream));
-  XG_CUDA(c, launch_stream_ingest(sp, c->stream));
+  sp.norm2_next = s->t + 1 < s->tmax
+                      ? reinterpret_cast<unsigned long long*>(s->d_norm2 + (s->t + 1) * L->rings)
+                      : nullptr;
+  if (s->flags & XG_STREAM_SPARSE)
+    XG_CUDA(c, launch_stream_ingest_sparse(sp, c->stream));
+  else
+    XG_CUDA(c, launch_stream_ingest(sp, c->stream));
   NormParams np;
   np.t0 = s->t;
   np.norm2 = s->d_norm2;
@@ -2137,7 +2162,7 @@ int xg_stream_push(xg_stream* s, const uint8_t* frame, int on_device) {
   if (!(s->flags & XG_STREAM_NO_RAW)) {
     if (s->flags & XG_STREAM_SPARSE) {
       XG_CUDA(c, launch_stream_sparse(sp, L->rings, c->stream));
-      c->launches += 2;
+      c->launches++;
     } else {
       XG_CUDA(c, launch_stream_raw(sp, L->rings, s->max_kpad, c->stream));
       c->launches++;

@@ -221,21 +221,26 @@ struct StreamParams {
   int64_t hp;                // frames per pixel row (multiple of 16)
   int32_t* nz_col;           // [ktot]: ring r's nonzero columns at [koff_r, ...)
   uint8_t* nz_val;           // [ktot]
-  int32_t* nz_n;             // [ring] (zero on entry; reset by the column pass)
-  int32_t* colbuf;           // [ring][hp] partial column sums (zero on entry)
+  int32_t* nz_n;             // [ring] counts of this push (zero on entry)
+  int32_t* nz_next;          // [ring] counts of the next push: zeroed by the ingest
   int32_t* pacc;             // [ring][768] projection digit sums (zero on entry)
-  int32_t nz_reset;          // which pass resets nz_n: 1 sparse column, 2 projection
   // one-frame ingest
   const uint8_t* frame;      // raster of the new frame
   const int32_t* colpix;     // [ktot] detector pixel of each column (-1 = padding)
   const int32_t* blk_ring;   // [ktot / 128] ring of each 128-column block
+  const int32_t* pixcol;     // [pixels] ring << 22 | ring-major column (-1: no ring)
+  int64_t pixels;
   int32_t n_rings;
   unsigned long long* norm2; // [frame][ring] (row t zero on entry)
+  unsigned long long* norm2_next;  // row t + 1, zeroed by the ingest (or null)
 };
 // One-frame ingest for the streaming path: ring-major row t of the history,
 // |x_t|^2 per ring, and in sparse mode the frame's nonzeros per ring plus
 // their scatter into the pixel-major history.
 cudaError_t launch_stream_ingest(const StreamParams& p, cudaStream_t s);
+// Sparse mode: the same from the raster in pixel order (no ring-major row):
+// only the frame's nonzero pixels touch the tables.
+cudaError_t launch_stream_ingest_sparse(const StreamParams& p, cudaStream_t s);
 // Sparse raw streaming (photon-event data): the new column costs nnz * t
 // bytes instead of M * t; results equal the dense kernel's bitwise.
 cudaError_t launch_stream_sparse(const StreamParams& p, int32_t n_rings, cudaStream_t s);
