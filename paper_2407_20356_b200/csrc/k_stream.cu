@@ -87,40 +87,65 @@ __global__ void __launch_bounds__(SR_THREADS) k_stream_raw(StreamParams p) {
 // coefficient) pair from the pixel-major int8 digits; slices meet in pacc
 // (integer atomics: exact, order-free).
 constexpr int PZ = 8;
+constexpr int PA_MAXW = 6;  // 32-bit digit words per lane: 3 digits x k <= 768
+constexpr int PA_U = 4;     // pixels in flight per warp
 __global__ void __launch_bounds__(256) k_stream_proj_acc(StreamParams p) {
+  // warp w of the CTA takes nonzeros zb + w, zb + w + 8, ...; lane L holds
+  // the 32-bit digit words L, L + 32, ... of the pixel's row (4 digits per
+  // word), PA_U rows in flight; the 8 warps meet in shared memory, the PZ
+  // slices in pacc (integer atomics: exact, order-free)
+  __shared__ int32_t red[8][768];
   const int r = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int koff = p.ring_koff[r];
   const int n = p.nz_n[r];
   const int zb = static_cast<int>((static_cast<int64_t>(n) * blockIdx.y) / PZ);
   const int ze = static_cast<int>((static_cast<int64_t>(n) * (blockIdx.y + 1)) / PZ);
-  const int nacc = p.n_digits * p.k;  // <= 768
-  __shared__ int32_t sc[256];
-  __shared__ int32_t sv[256];
-  int32_t acc[3] = {0, 0, 0};
-  for (int c0 = zb; c0 < ze; c0 += 256) {
-    const int cn = ze - c0 < 256 ? ze - c0 : 256;
-    __syncthreads();
-    if (static_cast<int>(threadIdx.x) < cn) {
-      sc[threadIdx.x] = p.nz_col[koff + c0 + threadIdx.x];
-      sv[threadIdx.x] = p.nz_val[koff + c0 + threadIdx.x];
-    }
-    __syncthreads();
-#pragma unroll 8
-    for (int e = 0; e < cn; ++e) {
-      const int8_t* vd = p.vdt + static_cast<int64_t>(sc[e]) * p.vdt_ld;
-      const int xv = sv[e];
+  const int nw = p.vdt_ld >> 2;
+  int32_t acc[PA_MAXW][4];
 #pragma unroll
-      for (int m = 0; m < 3; ++m) {
-        const int j = threadIdx.x + 256 * m;
-        if (j < nacc) acc[m] += xv * vd[j];
+  for (int m = 0; m < PA_MAXW; ++m)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[m][q] = 0;
+  for (int e0 = zb + warp; e0 < ze; e0 += 8 * PA_U) {
+    uint32_t wv[PA_U][PA_MAXW];
+    int xv[PA_U];
+#pragma unroll
+    for (int u = 0; u < PA_U; ++u) {
+      const int e = e0 + 8 * u;
+      const bool in = e < ze;
+      const int col = in ? p.nz_col[koff + e] : 0;
+      xv[u] = in ? p.nz_val[koff + e] : 0;
+      const uint32_t* row = reinterpret_cast<const uint32_t*>(p.vdt + static_cast<int64_t>(col) * p.vdt_ld);
+#pragma unroll
+      for (int m = 0; m < PA_MAXW; ++m) {
+        const int wi = lane + 32 * m;
+        wv[u][m] = (in && wi < nw) ? __ldg(row + wi) : 0u;
       }
     }
-  }
-  int32_t* pa = p.pacc + static_cast<int64_t>(r) * 768;
 #pragma unroll
-  for (int m = 0; m < 3; ++m) {
-    const int j = threadIdx.x + 256 * m;
-    if (j < nacc && acc[m]) atomicAdd(pa + j, acc[m]);
+    for (int u = 0; u < PA_U; ++u)
+#pragma unroll
+      for (int m = 0; m < PA_MAXW; ++m)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          acc[m][q] += xv[u] * static_cast<int>(static_cast<int8_t>((wv[u][m] >> (8 * q)) & 0xFFu));
+  }
+#pragma unroll
+  for (int m = 0; m < PA_MAXW; ++m) {
+    const int wi = lane + 32 * m;
+    if (wi < nw && 4 * wi < 768)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) red[warp][4 * wi + q] = acc[m][q];
+  }
+  __syncthreads();
+  const int nacc = p.n_digits * p.k;  // <= 768
+  int32_t* pa = p.pacc + static_cast<int64_t>(r) * 768;
+  for (int j = threadIdx.x; j < nacc; j += 256) {
+    int32_t tot = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) tot += red[w][j];
+    if (tot) atomicAdd(pa + j, tot);
   }
 }
 
@@ -136,37 +161,52 @@ __global__ void __launch_bounds__(128) k_stream_proj_fin(StreamParams p) {
     const double y =
         combine_digits(a0, a1, a2, p.n_digits, p.scale[static_cast<int64_t>(r) * p.k + j], inv);
     p.y[(static_cast<int64_t>(r) * p.y_ld + p.t) * p.k + j] = y;
-    p.yf[(static_cast<int64_t>(r) * p.y_ld + p.t) * p.k + j] = static_cast<float>(y);
+    p.yf[(static_cast<int64_t>(r) * p.y_ld + p.t) * p.kq + j] = static_cast<float>(y);
   }
   __syncthreads();
   for (int j = threadIdx.x; j < p.n_digits * p.k; j += blockDim.x) pa[j] = 0;
 }
 
 // K6b: grid (ceil((t+1)/SR_ROWS), rings); a warp per history row.
-__global__ void __launch_bounds__(SR_THREADS) k_stream_cmp(StreamParams p) {
-  // fp32 coefficient history (C~ is fp32-accurate by contract): half the
-  // bytes of the f64 rows; products summed in fp32 over k, lags in f64
-  __shared__ float yt[1024];
+template <int MAXV>
+__global__ void __launch_bounds__(SR_THREADS, 4) k_stream_cmp(StreamParams p) {
+  // fp32 coefficient history (C~ is fp32-accurate by contract), rows padded
+  // to kq = k rounded up to 4 (zero pad): lane L holds float4 chunks L, L+32,
+  // ... of the new row; a warp's 8 history rows are loaded (16 B per lane per
+  // row) before any arithmetic; fp32 products summed over k, lags in f64
   const int r = blockIdx.y;
-  const float* ybase = p.yf + static_cast<int64_t>(r) * p.y_ld * p.k;
-  for (int j = threadIdx.x; j < p.k; j += blockDim.x) yt[j] = ybase[p.t * p.k + j];
-  __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kq = p.kq, nv = kq >> 2;
+  const float* ybase = p.yf + static_cast<int64_t>(r) * p.y_ld * kq;
+  float4 yn[MAXV];
+#pragma unroll
+  for (int m = 0; m < MAXV; ++m) {
+    const int v = lane + 32 * m;
+    yn[m] = v < nv ? *reinterpret_cast<const float4*>(ybase + p.t * kq + 4 * v)
+                   : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
   const double inv_t = p.inv[static_cast<int64_t>(r) * p.inv_ld + p.t];
-  // a warp's 8 rows are independent: all their loads go out before any
-  // reduction, and lanes 0..7 then update the 8 lags in parallel
   constexpr int RPW = SR_ROWS / (SR_THREADS / 32);
   const int64_t s_first = static_cast<int64_t>(blockIdx.x) * SR_ROWS + warp * RPW;
   float part[RPW];
 #pragma unroll
-  for (int q = 0; q < RPW; ++q) {
-    const int64_t s = s_first + q;
-    float a = 0.f;
-    if (s <= p.t) {
-      const float* ys = ybase + s * p.k;
-      for (int j = lane; j < p.k; j += 32) a = fmaf(__ldcs(ys + j), yt[j], a);
+  for (int q = 0; q < RPW; ++q) part[q] = 0.f;
+#pragma unroll
+  for (int m = 0; m < MAXV; ++m) {
+    if (32 * m >= nv) break;
+    const int v = lane + 32 * m;
+    float4 ld[RPW];
+#pragma unroll
+    for (int q = 0; q < RPW; ++q) {
+      const int64_t s = s_first + q;
+      ld[q] = (v < nv && s <= p.t)
+                  ? __ldcs(reinterpret_cast<const float4*>(ybase + s * kq + 4 * v))
+                  : make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    part[q] = a;
+#pragma unroll
+    for (int q = 0; q < RPW; ++q)
+      part[q] = fmaf(ld[q].x, yn[m].x,
+                     fmaf(ld[q].y, yn[m].y, fmaf(ld[q].z, yn[m].z, fmaf(ld[q].w, yn[m].w, part[q]))));
   }
   float mine = 0.f;
 #pragma unroll
@@ -437,7 +477,11 @@ cudaError_t launch_stream_cmp(const StreamParams& p, int32_t n_rings, cudaStream
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   dim3 grid(static_cast<unsigned>((p.t + 1 + SR_ROWS - 1) / SR_ROWS), n_rings);
-  k_stream_cmp<<<grid, SR_THREADS, 0, s>>>(p);
+  const int nv = p.kq / 4;  // float4 chunks per coefficient row (k <= 256)
+  if (nv <= 32)
+    k_stream_cmp<1><<<grid, SR_THREADS, 0, s>>>(p);
+  else
+    k_stream_cmp<2><<<grid, SR_THREADS, 0, s>>>(p);
   return cudaGetLastError();
 }
 

@@ -1894,6 +1894,10 @@ struct xg_stream {
   uint32_t flags = 0;
   int64_t tmax = 0, t = 0, tp = 0;
   int64_t max_kpad = 0;
+  // raw + compressed: the compressed column runs on a side stream, forked
+  // after the ingest and joined at the end of the push
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   uint8_t* d_frame = nullptr;
   uint8_t* d_x = nullptr;
   int64_t *d_norm2 = nullptr, *d_zero = nullptr, *d_first_zero = nullptr;
@@ -1926,6 +1930,9 @@ int xg_stream_create(xg_ctx* c, const xg_layout* L, const xg_basis* B, int64_t m
   *out = nullptr;
   if (max_frames < 1) return fail(c, XG_ERR_CONTRACT, "stream: max_frames must be >= 1");
   if (B && B->L != L) return fail(c, XG_ERR_BINDING, "stream: basis built for another layout");
+  if (B && B->digits * B->k > 768)
+    return fail(c, XG_ERR_CONTRACT, "stream: digits x k = %d exceeds 768 (k <= 256 at 3 digits)",
+                B->digits * B->k);
   if (B)
     for (int32_t r = 0; r < L->rings; ++r)
       if (!B->ring_set[r]) return fail(c, XG_ERR_CONTRACT, "stream: basis of ring %d not set", r);
@@ -2022,7 +2029,7 @@ int xg_stream_create(xg_ctx* c, const xg_layout* L, const xg_basis* B, int64_t m
   if (B) {
     // pixel-major copy of the basis digits: [ktot][digits * k], index s*k + j
     xg_basis* b = const_cast<xg_basis*>(B);
-    s->vdt_ld = b->digits * b->k;
+    s->vdt_ld = static_cast<int32_t>(round_up(b->digits * b->k, 16));  // 16-byte rows, zero pad
     std::vector<int8_t> vdt((size_t)L->ktot * s->vdt_ld, 0);
     for (int64_t row = 0; row < b->vrows; ++row) {
       const int64_t nt = row / (b->digits * b->kt), rem = row % (b->digits * b->kt);
@@ -2034,11 +2041,12 @@ int xg_stream_create(xg_ctx* c, const xg_layout* L, const xg_basis* B, int64_t m
     }
     if ((e = dalloc(&s->d_vdt, vdt.size())) != cudaSuccess ||
         (e = dalloc(&s->d_y, (size_t)Q * s->tp * b->k)) != cudaSuccess ||
-        (e = dalloc(&s->d_yf, (size_t)Q * s->tp * b->k)) != cudaSuccess ||
+        (e = dalloc(&s->d_yf, (size_t)Q * s->tp * ((b->k + 3) / 4 * 4))) != cudaSuccess ||
         (e = cudaMemcpy(s->d_vdt, vdt.data(), vdt.size(), cudaMemcpyHostToDevice)) != cudaSuccess) {
       xg_stream_destroy(s);
       return cuda_fail(c, e, "stream basis");
     }
+    cudaMemsetAsync(s->d_yf, 0, (size_t)Q * s->tp * ((b->k + 3) / 4 * 4) * 4, c->stream);
     if (b->dirty) {
       cudaMemcpy(b->d_vd, b->h_vd.data(), b->h_vd.size(), cudaMemcpyHostToDevice);
       cudaMemcpy(b->d_scale, b->h_scale.data(), b->h_scale.size() * 8, cudaMemcpyHostToDevice);
@@ -2051,6 +2059,12 @@ int xg_stream_create(xg_ctx* c, const xg_layout* L, const xg_basis* B, int64_t m
 
 void xg_stream_destroy(xg_stream* s) {
   if (!s) return;
+  if (s->side) {
+    cudaStreamSynchronize(s->side);
+    cudaStreamDestroy(s->side);
+  }
+  if (s->ev_fork) cudaEventDestroy(s->ev_fork);
+  if (s->ev_join) cudaEventDestroy(s->ev_join);
   dfree(s->d_frame);
   dfree(s->d_x);
   dfree(s->d_norm2);
@@ -2120,6 +2134,7 @@ int xg_stream_push(xg_stream* s, const uint8_t* frame, int on_device) {
   sp.scale = s->B ? s->B->d_scale : nullptr;
   sp.y = s->d_y;
   sp.yf = s->d_yf;
+  sp.kq = s->B ? (s->B->k + 3) / 4 * 4 : 0;
   sp.y_ld = s->tp;
   sp.hist = s->d_hist;
   sp.hp = s->hp;
@@ -2159,18 +2174,31 @@ int xg_stream_push(xg_stream* s, const uint8_t* frame, int on_device) {
   np.err = c->d_err;
   XG_CUDA(c, launch_norms(np, c->stream));
   c->launches += 2;
-  if (!(s->flags & XG_STREAM_NO_RAW)) {
-    if (s->flags & XG_STREAM_SPARSE) {
-      XG_CUDA(c, launch_stream_sparse(sp, L->rings, c->stream));
-      c->launches++;
-    } else {
-      XG_CUDA(c, launch_stream_raw(sp, L->rings, s->max_kpad, c->stream));
-      c->launches++;
+  const bool raw = !(s->flags & XG_STREAM_NO_RAW);
+  const bool fork = raw && s->B;  // compressed column on the side stream, overlapped
+  if (fork) {
+    if (!s->side) {
+      XG_CUDA(c, cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking));
+      XG_CUDA(c, cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming));
+      XG_CUDA(c, cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming));
     }
+    XG_CUDA(c, cudaEventRecord(s->ev_fork, c->stream));
+    XG_CUDA(c, cudaStreamWaitEvent(s->side, s->ev_fork, 0));
   }
   if (s->B) {
-    XG_CUDA(c, launch_stream_cmp(sp, L->rings, c->stream));
-    c->launches += 2;
+    XG_CUDA(c, launch_stream_cmp(sp, L->rings, fork ? s->side : c->stream));
+    c->launches += 3;
+  }
+  if (raw) {
+    if (s->flags & XG_STREAM_SPARSE)
+      XG_CUDA(c, launch_stream_sparse(sp, L->rings, c->stream));
+    else
+      XG_CUDA(c, launch_stream_raw(sp, L->rings, s->max_kpad, c->stream));
+    c->launches++;
+  }
+  if (fork) {
+    XG_CUDA(c, cudaEventRecord(s->ev_join, s->side));
+    XG_CUDA(c, cudaStreamWaitEvent(c->stream, s->ev_join, 0));
   }
   s->t++;
   return XG_OK;

@@ -213,7 +213,8 @@ struct StreamParams {
   int32_t k;
   const double* scale;       // [ring][k]
   double* y;                 // [ring][y_ld][k]
-  float* yf;                 // [ring][y_ld][k] fp32 copy: the compressed column's history
+  float* yf;                 // [ring][y_ld][kq] fp32 copy: the compressed column's history
+  int32_t kq;                // k rounded up to 4 (zero pad)
   int64_t y_ld;
   // sparse raw mode: pixel-major history hist[c][hp] (u8, column c of the
   // ring-major layout, frame s) and the new frame's nonzeros per ring
