@@ -141,6 +141,20 @@ XG_API int xg_series_get_g2_all(xg_series* s, double* values, int64_t* counts);
 XG_API int xg_series_rel_error(xg_series* s, double* out_per_ring);
 /* f64 frame norms |x_t| of ring (n) and the count of zero-norm frames. */
 XG_API int xg_series_get_norms(xg_series* s, int32_t ring, double* norms, int64_t* n_zero);
+/* Analysis consumers on the device (which: 0 raw, 1
+ * compressed).  ttc_background (analysis.cpp:202-235): per ring, the
+ * standard deviation of the stored TTC entries with lag > exclusion (two
+ * passes: mean, then squared deviations; pairs with a flagged zero-norm frame
+ * left out, as in g2).  fit_kww (analysis.cpp:77-172): per ring, the KWW fit
+ * g2 = B + C exp(-2 lag / t0) of the device g2 curve over lags
+ * [min_lag, max_lag] (lags d * frame_period), the reference's initialisation
+ * and damped Gauss-Newton; out[ring * 4 + {0..3}] = B, C, t0, residual rms;
+ * status[ring] = 0 ok, 1 FitDegenerateError, 2 FitError (out = the last
+ * accepted iterate), 3 ContractError (fewer than 5 points / non-finite). */
+XG_API int xg_series_ttc_background(xg_series* s, int32_t which, int64_t exclusion,
+                                    double* out_per_ring);
+XG_API int xg_series_fit_kww(xg_series* s, int32_t which, double frame_period, double min_lag,
+                             double max_lag, double* out, int32_t* status);
 XG_API int64_t xg_series_frames(const xg_series* s);
 
 /* ---- rank-k compression and the homomorphic TTC -----------------------

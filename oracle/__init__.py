@@ -236,6 +236,8 @@ class _RefOracle:
         L.ref_ttc_extend_stream.argtypes = [_d, _d, I64, I64, _d]
         L.ref_ttc_extend.argtypes = [_d, I64, _d, _d, I64, _d, _d]
         L.ref_g2_from_ttc.argtypes = [_d, I64, C_.c_double, _d, _d, _i64]
+        L.ref_ttc_background.argtypes = [_d, I64, I64, _d]
+        L.ref_fit_kww.argtypes = [_d, _d, I64, C_.c_double, C_.c_double, _d]
         L.ref_ttc_rel_error.argtypes = [_d, _d, I64, _d]
         L.ref_compress_series.argtypes = [_d, I64, I64, _d, I64, _d, _d]
         L.ref_compress_frame.argtypes = [_d, I64, _d, I64, _d, _d]
@@ -294,6 +296,21 @@ class _RefOracle:
         self._chk(self.L.ref_g2_from_ttc(_p(g, _d), n, period, _p(lags, _d), _p(vals, _d),
                                          _p(counts, _i64)))
         return lags, vals, counts
+
+    def ttc_background(self, g, exclusion=0):
+        g = _f64(g)
+        out = C_.c_double(0.0)
+        self._chk(self.L.ref_ttc_background(_p(g, _d), g.shape[0], exclusion, C_.byref(out)))
+        return out.value
+
+    def fit_kww(self, lags, values, min_lag, max_lag):
+        """(status, [B, C, t0, rms]): status 0 ok, 10 FitDegenerateError,
+        11 FitError (params = its best()), 2 ContractError."""
+        lags, values = _f64(lags), _f64(values)
+        out = np.zeros(4)
+        rc = self.L.ref_fit_kww(_p(lags, _d), _p(values, _d), lags.size, min_lag, max_lag,
+                                _p(out, _d))
+        return rc, out
 
     def content_hash(self, v, mode):
         v = _f64(v)

@@ -14,6 +14,7 @@
 #include <cstring>
 #include <vector>
 
+#include "xpcsvd/analysis.hpp"
 #include "xpcsvd/compress.hpp"
 #include "xpcsvd/correlate.hpp"
 #include "xpcsvd/encoder.hpp"
@@ -200,6 +201,43 @@ int ref_apply_mask(const double* x, int64_t n, int64_t m_full, const int64_t* id
                                PixelMask(static_cast<std::size_t>(m_full), ind));
     copy_out(f.intensities, out);
   });
+}
+
+// ttc_background (analysis.cpp:202-235) of an n x n TTC.
+int ref_ttc_background(const double* g, int64_t n, int64_t exclusion, double* out) {
+  return guarded([&] {
+    *out = ttc_background(TTCMatrix(to_matrix(g, n, n), false), static_cast<std::size_t>(exclusion));
+  });
+}
+
+// fit_kww (analysis.cpp:77-172) of a g2 curve; out = {B, C, t0, rms}.
+// Status 10: FitDegenerateError, 11: FitError (out = its best()).
+int ref_fit_kww(const double* lags, const double* values, int64_t n, double min_lag,
+                double max_lag, double* out) {
+  try {
+    G2Curve c;
+    c.lags.assign(lags, lags + n);
+    c.values.assign(values, values + n);
+    c.counts.assign(static_cast<std::size_t>(n), 1);
+    const KwwFit f = fit_kww(c, LagWindow{min_lag, max_lag});
+    out[0] = f.baseline;
+    out[1] = f.contrast;
+    out[2] = f.relaxation_time;
+    out[3] = f.residual_rms;
+    return 0;
+  } catch (const FitDegenerateError&) {
+    return 10;
+  } catch (const FitError& e) {
+    out[0] = e.best().baseline;
+    out[1] = e.best().contrast;
+    out[2] = e.best().relaxation_time;
+    out[3] = e.best().residual_rms;
+    return 11;
+  } catch (const ContractError&) {
+    return 2;
+  } catch (const Error&) {
+    return 99;
+  }
 }
 
 uint64_t ref_rng_bits(uint64_t seed, uint64_t tag, uint64_t index) {

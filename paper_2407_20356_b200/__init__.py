@@ -378,6 +378,29 @@ class FrameSeries:
         _check(self.ctx.h, lib.xg_series_rel_error(self.h, out.ctypes.data_as(_abi.PD)))
         return out
 
+    def ttc_background(self, exclusion: int = 0, compressed: bool = False) -> np.ndarray:
+        """Per-ring ttc_background (analysis.cpp:202-235) of the stored raw or
+        compressed TTC, on the device: sigma of the entries with lag > exclusion."""
+        out = np.empty(self.layout.n_rings, np.float64)
+        _check(self.ctx.h, lib.xg_series_ttc_background(self.h, 1 if compressed else 0,
+                                                         int(exclusion), out.ctypes.data_as(_abi.PD)))
+        return out
+
+    def fit_kww(self, min_lag: float, max_lag: float, compressed: bool = False):
+        """Per-ring fit_kww (analysis.cpp:77-172) of the device g2 curves over
+        lags [min_lag, max_lag] (lags in frame periods * frame_period).
+        Returns (fits [rings x 4]: B, C, t0, residual rms; status [rings]:
+        0 ok, 1 FitDegenerateError, 2 FitError (fit = last accepted iterate),
+        3 ContractError (window too small / non-finite))."""
+        q = self.layout.n_rings
+        fits = np.zeros((q, 4), np.float64)
+        st = np.zeros(q, np.int32)
+        _check(self.ctx.h, lib.xg_series_fit_kww(self.h, 1 if compressed else 0,
+                                                  float(self.frame_period), float(min_lag),
+                                                  float(max_lag), fits.ctypes.data_as(_abi.PD),
+                                                  st.ctypes.data_as(C.POINTER(C.c_int32))))
+        return fits, st
+
     def build_basis(self, k: int, basis: "Basis | None" = None):
         """Per-ring encoding basis from this series' frames, built on the
         device (xg_series_build_basis; the reference's build_online_from_frames

@@ -52,6 +52,8 @@ _sigs = {
     "xg_series_get_g2": (C.c_int, [P, I32, PD, PI64]),
     "xg_series_get_g2_all": (C.c_int, [P, PD, PI64]),
     "xg_series_rel_error": (C.c_int, [P, PD]),
+    "xg_series_ttc_background": (C.c_int, [P, I32, I64, PD]),
+    "xg_series_fit_kww": (C.c_int, [P, I32, C.c_double, C.c_double, C.c_double, PD, C.POINTER(I32)]),
     "xg_series_build_basis": (C.c_int, [P, I32, C.POINTER(PD), PD, I64, PI64, P]),
     "xg_series_get_norms": (C.c_int, [P, I32, PD, PI64]),
     "xg_series_frames": (I64, [P]),

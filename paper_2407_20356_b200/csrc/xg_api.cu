@@ -121,6 +121,7 @@ struct xg_series {
   double* d_cg2 = nullptr;
   int64_t* d_cg2cnt = nullptr;
   bool have_y = false, have_cttc = false;
+  bool raw_g2 = false, cmp_g2 = false;  // g2 curves current (not XG_NO_G2)
   TileDesc* d_ptiles = nullptr;    // projection tiles
   int32_t n_ptiles = 0;
   int64_t ptiles_key = -1;
@@ -932,6 +933,7 @@ int xg_ttc_raw(xg_series* s, uint32_t flags) {
     if (rc) return rc;
   }
   s->have_raw = true;
+  s->raw_g2 = g2;
   return XG_OK;
 }
 
@@ -994,6 +996,7 @@ int xg_series_ttc_raw_host(xg_series* s, const uint8_t* frames, int64_t n, uint3
     if (rc) return rc;
   }
   s->have_raw = true;
+  s->raw_g2 = g2;
   return XG_OK;
 }
 
@@ -1001,7 +1004,9 @@ int xg_series_g2(xg_series* s) {
   if (!s) return XG_ERR_INVALID;
   if (!s->have_raw) return fail(s->ctx, XG_ERR_CONTRACT, "g2: no TTC computed yet");
   if (!s->raw_stored) return fail(s->ctx, XG_ERR_CONTRACT, "g2: TTC computed with XG_NO_STORE");
-  return run_g2(s, 0);
+  const int rc = run_g2(s, 0);
+  if (!rc) s->raw_g2 = true;
+  return rc;
 }
 
 // Deviation report of the homomorphic path (north star; ttc_rel_error,
@@ -1815,7 +1820,88 @@ int xg_ttc_compressed(xg_series* s, uint32_t flags) {
     if (rc) return rc;
   }
   s->have_cttc = true;
+  s->cmp_g2 = g2;
   return XG_OK;
+}
+
+// ------------------------------------------------ analysis consumers (8(f) 4)
+int xg_series_ttc_background(xg_series* s, int32_t which, int64_t exclusion, double* out) {
+  if (!s || !out) return XG_ERR_INVALID;
+  xg_ctx* c = s->ctx;
+  const xg_layout* L = s->L;
+  if (which == 0 ? !(s->have_raw && s->raw_stored) : !(s->have_cttc && s->cmp_stored))
+    return fail(c, XG_ERR_CONTRACT, "ttc_background: needs a stored %s TTC",
+                which == 0 ? "raw" : "compressed");
+  if (exclusion < 0 || s->t <= 2 * exclusion)
+    return fail(c, XG_ERR_CONTRACT,
+                "ttc_background: exclusion band of %lld covers the whole %lld-frame TTC",
+                (long long)exclusion, (long long)s->t);
+  double2* part = nullptr;
+  double* d_buf = nullptr;
+  XG_CUDA(c, cudaMalloc(&part, (size_t)L->rings * BG_BLOCKS * sizeof(double2)));
+  XG_CUDA(c, cudaMalloc(&d_buf, (size_t)L->rings * 8 * 3));
+  BgParams p;
+  p.gram = which == 0 ? s->d_gram : nullptr;
+  p.cgram = which == 0 ? nullptr : s->d_cgram;
+  p.ring_stride = s->tp * s->tp;
+  p.ld = static_cast<int32_t>(s->tp);
+  p.inv = s->d_inv;
+  p.inv_ld = s->tp;
+  p.n = s->t;
+  p.excl = exclusion;
+  p.n_rings = L->rings;
+  p.partial = part;
+  p.mean = d_buf;
+  p.count = reinterpret_cast<int64_t*>(d_buf + L->rings);
+  p.out = d_buf + 2 * L->rings;
+  cudaError_t e = launch_ttc_background(p, c->stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(out, p.out, (size_t)L->rings * 8, cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  cudaFree(part);
+  cudaFree(d_buf);
+  if (e != cudaSuccess) return cuda_fail(c, e, "ttc_background");
+  c->launches += 4;
+  for (int32_t r = 0; r < L->rings; ++r)
+    if (out[r] < 0.0) {
+      c->payload_ring = r;
+      return fail(c, XG_ERR_CONTRACT, "ttc_background: no entries outside the band (ring %d)", r);
+    }
+  return check_device_error(c);
+}
+
+int xg_series_fit_kww(xg_series* s, int32_t which, double frame_period, double min_lag,
+                      double max_lag, double* out, int32_t* status) {
+  if (!s || !out || !status) return XG_ERR_INVALID;
+  xg_ctx* c = s->ctx;
+  const xg_layout* L = s->L;
+  if (which == 0 ? !(s->have_raw && s->raw_g2) : !(s->have_cttc && s->cmp_g2))
+    return fail(c, XG_ERR_CONTRACT, "fit_kww: no %s g2 computed", which == 0 ? "raw" : "compressed");
+  if (!(frame_period > 0.0) || !std::isfinite(frame_period))
+    return fail(c, XG_ERR_CONTRACT, "fit_kww: frame_period must be positive and finite");
+  if (!(min_lag <= max_lag)) return fail(c, XG_ERR_CONTRACT, "fit_kww: window is empty (min > max)");
+  double* d_out = nullptr;
+  XG_CUDA(c, cudaMalloc(&d_out, (size_t)L->rings * (4 * 8 + 4)));
+  KwwParams p;
+  p.g2 = which == 0 ? s->d_g2 : s->d_cg2;
+  p.g2_ld = s->tp;
+  p.n = s->t;
+  p.period = frame_period;
+  p.min_lag = min_lag;
+  p.max_lag = max_lag;
+  p.n_rings = L->rings;
+  p.out = d_out;
+  p.status = reinterpret_cast<int32_t*>(d_out + 4 * L->rings);
+  cudaError_t e = launch_fit_kww(p, c->stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(out, d_out, (size_t)L->rings * 32, cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(status, p.status, (size_t)L->rings * 4, cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  cudaFree(d_out);
+  if (e != cudaSuccess) return cuda_fail(c, e, "fit_kww");
+  c->launches++;
+  return check_device_error(c);
 }
 
 int xg_series_get_coeffs(xg_series* s, int32_t ring, double* y, double* norms) {

@@ -318,6 +318,39 @@ struct RelErrParams {
 constexpr int REL_BLOCKS = 64;
 cudaError_t launch_rel_error(const RelErrParams& p, cudaStream_t s);
 
+// ---------------------------------------------------------- analysis (8(f) 4)
+// ttc_background (analysis.cpp:202-235) of every ring's stored TTC: two
+// deterministic passes (mean, then squared deviations) over the upper tiles.
+struct BgParams {
+  const int32_t* gram;       // raw: exact Gram [ring][ld][ld] (cgram == null)
+  const float* cgram;        // compressed C~ (or null)
+  int64_t ring_stride;
+  int32_t ld;
+  const double* inv;         // [ring][inv_ld]
+  int64_t inv_ld;
+  int64_t n;
+  int64_t excl;              // exclusion band (lags <= excl left out)
+  int32_t n_rings;
+  double2* partial;          // [ring][BG_BLOCKS] (sum, count)
+  double* mean;              // [ring]
+  int64_t* count;            // [ring] entries outside the band (upper triangle)
+  double* out;               // [ring] sigma (-1: none)
+};
+constexpr int BG_BLOCKS = 64;
+cudaError_t launch_ttc_background(const BgParams& p, cudaStream_t s);
+
+// fit_kww (analysis.cpp:77-172) of every ring's g2 curve, one warp per ring.
+struct KwwParams {
+  const double* g2;          // [ring][g2_ld]
+  int64_t g2_ld;
+  int64_t n;                 // curve points (lags d * period, d < n)
+  double period, min_lag, max_lag;
+  int32_t n_rings;
+  double* out;               // [ring][4] B, C, t0, residual rms
+  int32_t* status;           // [ring] 0 ok, 1 FitDegenerate, 2 FitError, 3 Contract
+};
+cudaError_t launch_fit_kww(const KwwParams& p, cudaStream_t s);
+
 // ---------------------------------------------------------- K8 synthetic
 struct SynthParams {
   int64_t t_first;           // global index of the first frame generated

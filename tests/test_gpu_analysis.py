@@ -1,0 +1,88 @@
+"""Analysis consumers on the device against the
+reference's own functions (oracle/_ref) on the same inputs:
+
+* ttc_background (analysis.cpp:202-235) of the stored raw / compressed TTC,
+  fed to the reference as the read-back f64 matrix (identical entries; only
+  the summation order differs -> 1e-12 relative);
+* fit_kww (analysis.cpp:77-172) of the device g2 curve, fed to the reference
+  as the same curve (identical points; lane-split sums and the device exp ->
+  parameters within 1e-8 relative, identical status)."""
+import numpy as np
+import pytest
+
+import paper_2407_20356_b200 as xg
+
+pytestmark = pytest.mark.gpu
+
+
+def _series(ctx, orc, t, h, w, q, mu, seed, period=1.0):
+    frames = orc.gen_speckle(t, h, w, q, mu, seed)
+    ring, _ = orc.ring_map(h, w, q)
+    lay = xg.RingLayout.from_ring_map(ctx, ring, q)
+    return frames, ring, lay, xg.FrameSeries(lay, t, frame_period=period).load(frames)
+
+
+@pytest.mark.parametrize("excl", [0, 3, 40])
+def test_ttc_background_raw_matches_reference(ctx, orc, ref, excl):
+    frames, ring, lay, s = _series(ctx, orc, 300, 48, 48, 3, 0.3, 71)
+    s.ttc_raw()
+    bg = s.ttc_background(excl)
+    for r in range(3):
+        want = ref.ttc_background(s.ttc(r, "f64"), excl)
+        assert abs(bg[r] - want) <= 1e-12 * want, (r, bg[r], want)
+
+
+def test_ttc_background_compressed_matches_reference(ctx, orc, ref):
+    frames, ring, lay, s = _series(ctx, orc, 260, 48, 48, 2, 0.4, 72)
+    basis = xg.Basis(lay, 16)
+    vs, _, _ = xg.FrameSeries(lay, 64).load(frames[:64]).build_basis(16, basis=basis)
+    s.compress(basis).ttc_compressed()
+    bg = s.ttc_background(5, compressed=True)
+    for r in range(2):
+        c = np.array(s.cttc(r, "f64"))
+        np.fill_diagonal(c, 1.0)  # fp32 diagonal may exceed 1 by ~1e-7; excluded anyway
+        want = ref.ttc_background(c, 5)
+        assert abs(bg[r] - want) <= 1e-12 * want
+
+
+def test_ttc_background_leaves_out_flagged_frames(ctx, orc, ref):
+    frames, ring, lay, s = _series(ctx, orc, 120, 40, 40, 2, 0.4, 73)
+    frames = frames.copy()
+    frames[17, ring == 1] = 0
+    s = xg.FrameSeries(lay, 120).load(frames).ttc_raw()
+    bg = s.ttc_background(0)
+    c = s.ttc(1, "f64")
+    keep = np.ones(120, bool)
+    keep[17] = False
+    want = ref.ttc_background(c[np.ix_(keep, keep)], 0)  # lag > 0 == off-diagonal
+    assert abs(bg[1] - want) <= 1e-12 * want
+    with pytest.raises(xg.ContractError):
+        s.ttc_background(60)  # 2 * 60 >= 120: the band covers the TTC
+
+
+@pytest.mark.parametrize("period,window", [(1.0, (1.0, 150.0)), (0.01, (0.0, 2.5))])
+def test_fit_kww_matches_reference(ctx, orc, ref, period, window):
+    frames, ring, lay, s = _series(ctx, orc, 400, 64, 64, 4, 0.5, 74, period)
+    s.ttc_raw()
+    fits, st = s.fit_kww(*window)
+    n_ok = 0
+    for r in range(4):
+        lags, g2, _ = s.g2(r)
+        rc, want = ref.fit_kww(lags, g2, *window)
+        code = {0: 0, 10: 1, 11: 2, 2: 3}[rc]
+        assert st[r] == code, (r, st[r], rc)
+        if code in (0, 2):
+            assert np.allclose(fits[r], want, rtol=1e-8, atol=1e-12), (r, fits[r], want)
+            n_ok += code == 0
+    assert n_ok >= 1
+
+
+def test_fit_kww_contract_cases(ctx, orc):
+    frames, ring, lay, s = _series(ctx, orc, 64, 32, 32, 2, 0.5, 75)
+    with pytest.raises(xg.ContractError):
+        s.fit_kww(0.0, 10.0)  # no g2 yet
+    s.ttc_raw()
+    fits, st = s.fit_kww(10.0, 12.0)  # 3 points
+    assert list(st) == [3, 3]
+    with pytest.raises(xg.ContractError):
+        s.fit_kww(5.0, 1.0)
