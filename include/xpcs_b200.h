@@ -151,6 +151,31 @@ XG_API int xg_series_get_norms(xg_series* s, int32_t ring, double* norms, int64_
  * and damped Gauss-Newton; out[ring * 4 + {0..3}] = B, C, t0, residual rms;
  * status[ring] = 0 ok, 1 FitDegenerateError, 2 FitError (out = the last
  * accepted iterate), 3 ContractError (fewer than 5 points / non-finite). */
+/* On-disk formats next to the device buffers (the
+ * reference's io.cpp).  XCMP store (io.cpp:319-441): xg_series_write_xcmp
+ * writes one ring's compressed rows (norm + k f64 coefficients per frame),
+ * or with append != 0 extends an existing store like CompressedFileAppender
+ * (k mismatch -> XG_ERR_SHAPE, encoder hash -> XG_ERR_BINDING, corrupt
+ * file -> XG_ERR_FORMAT with the byte offset); xg_stream_append_xcmp appends
+ * the stream's rows [from_frame, t).  A flagged zero-norm frame cannot be
+ * stored (XG_ERR_NORMALIZATION, payload = frame).  XFSR frames (io.cpp:150-
+ * 225): dtype 0 u16 / 1 f32 / 2 f64 as the reference, dtype 3 = u8 photon
+ * counts (new); xg_series_load_xfsr reads any of them into the series
+ * (values must be integer counts in [0, 255]).  Host-only helpers report
+ * through xg_io_last_error / xg_io_last_payload. */
+XG_API int xg_series_write_xcmp(xg_series* s, int32_t ring, const char* path,
+                                uint64_t encoder_hash, int32_t append);
+XG_API int xg_stream_append_xcmp(xg_stream* s, int32_t ring, const char* path,
+                                 uint64_t encoder_hash, int64_t from_frame);
+XG_API int xg_series_load_xfsr(xg_series* s, const char* path, double* frame_period);
+XG_API const char* xg_io_last_error(void);
+XG_API int64_t xg_io_last_payload(void);
+XG_API int xg_io_write_xcmp(const char* path, int64_t k, uint64_t encoder_hash, int64_t n,
+                            const double* norms, const double* coeffs, int32_t append);
+XG_API int xg_io_write_xfsr_u8(const char* path, const uint8_t* frames, int64_t n, int64_t m,
+                               double frame_period);
+XG_API int xg_io_read_xfsr_u8(const char* path, uint8_t* out, int64_t out_cap, int64_t* n,
+                              int64_t* m, double* frame_period);
 XG_API int xg_series_ttc_background(xg_series* s, int32_t which, int64_t exclusion,
                                     double* out_per_ring);
 XG_API int xg_series_fit_kww(xg_series* s, int32_t which, double frame_period, double min_lag,

@@ -237,6 +237,9 @@ class _RefOracle:
         L.ref_ttc_extend.argtypes = [_d, I64, _d, _d, I64, _d, _d]
         L.ref_g2_from_ttc.argtypes = [_d, I64, C_.c_double, _d, _d, _i64]
         L.ref_ttc_background.argtypes = [_d, I64, I64, _d]
+        L.ref_read_compressed.argtypes = [C_.c_char_p, _i64, C_.POINTER(U64), _i64, _d, _d]
+        L.ref_write_frames.argtypes = [C_.c_char_p, _d, I64, I64, C_.c_double, C_.c_int]
+        L.ref_read_frames_status.argtypes = [C_.c_char_p, _i64, _i64]
         L.ref_fit_kww.argtypes = [_d, _d, I64, C_.c_double, C_.c_double, _d]
         L.ref_ttc_rel_error.argtypes = [_d, _d, I64, _d]
         L.ref_compress_series.argtypes = [_d, I64, I64, _d, I64, _d, _d]
@@ -296,6 +299,28 @@ class _RefOracle:
         self._chk(self.L.ref_g2_from_ttc(_p(g, _d), n, period, _p(lags, _d), _p(vals, _d),
                                          _p(counts, _i64)))
         return lags, vals, counts
+
+    def read_compressed(self, path):
+        """io::read_compressed -> (k, encoder hash, coefficients n x k, norms)."""
+        k, n, h = I64(0), I64(0), U64(0)
+        p = str(path).encode()
+        self._chk(self.L.ref_read_compressed(p, C_.byref(k), C_.byref(h), C_.byref(n), None, None))
+        y = np.empty((n.value, k.value))
+        nr = np.empty(n.value)
+        self._chk(self.L.ref_read_compressed(p, C_.byref(k), C_.byref(h), C_.byref(n), _p(y, _d),
+                                             _p(nr, _d)))
+        return k.value, h.value, y, nr
+
+    def write_frames(self, path, x, period, dtype):
+        x = _f64(x)
+        self._chk(self.L.ref_write_frames(str(path).encode(), _p(x, _d), x.shape[0], x.shape[1],
+                                          period, dtype))
+
+    def read_frames_status(self, path):
+        """(status, payload): 0 ok, 7 FormatError (payload = byte offset)."""
+        n, m = I64(0), I64(0)
+        rc = self.L.ref_read_frames_status(str(path).encode(), C_.byref(n), C_.byref(m))
+        return rc, self.L.ref_last_payload()
 
     def ttc_background(self, g, exclusion=0):
         g = _f64(g)

@@ -18,6 +18,7 @@
 #include "xpcsvd/compress.hpp"
 #include "xpcsvd/correlate.hpp"
 #include "xpcsvd/encoder.hpp"
+#include "xpcsvd/io.hpp"
 #include "xpcsvd/linalg.hpp"
 #include "xpcsvd/model.hpp"
 #include "xpcsvd/rng.hpp"
@@ -201,6 +202,51 @@ int ref_apply_mask(const double* x, int64_t n, int64_t m_full, const int64_t* id
                                PixelMask(static_cast<std::size_t>(m_full), ind));
     copy_out(f.intensities, out);
   });
+}
+
+// io::read_compressed (io.cpp:334-360): call with coeffs == null for the
+// dimensions, then with buffers.  FormatError -> 7 (payload = offset).
+int ref_read_compressed(const char* path, int64_t* k, uint64_t* hash, int64_t* n, double* coeffs,
+                        double* norms) {
+  try {
+    CompressedSeries cs = io::read_compressed(path);
+    auto snap = cs.snapshot();
+    *k = static_cast<int64_t>(snap.k);
+    *hash = snap.encoder_id;
+    *n = static_cast<int64_t>(snap.n_frames());
+    if (coeffs) std::memcpy(coeffs, snap.coefficients.data(), snap.coefficients.size() * 8);
+    if (norms) std::memcpy(norms, snap.norms.data(), snap.norms.size() * 8);
+    return 0;
+  } catch (const FormatError& e) {
+    g_payload = static_cast<int64_t>(e.offset());
+    return 7;
+  } catch (const Error&) {
+    return 99;
+  }
+}
+
+// io::write_frames (io.cpp:150-184) with dtype 0 u16, 1 f32, 2 f64.
+int ref_write_frames(const char* path, const double* x, int64_t n, int64_t m, double period,
+                     int dtype) {
+  return guarded([&] {
+    io::write_frames(path, FrameSeries(to_matrix(x, n, m), period),
+                     static_cast<io::FrameDtype>(dtype));
+  });
+}
+
+// io::read_frames status only (FormatError -> 7, payload = offset).
+int ref_read_frames_status(const char* path, int64_t* n, int64_t* m) {
+  try {
+    FrameSeries f = io::read_frames(path);
+    *n = static_cast<int64_t>(f.n_frames());
+    *m = static_cast<int64_t>(f.n_pixels());
+    return 0;
+  } catch (const FormatError& e) {
+    g_payload = static_cast<int64_t>(e.offset());
+    return 7;
+  } catch (const Error&) {
+    return 99;
+  }
 }
 
 // ttc_background (analysis.cpp:202-235) of an n x n TTC.

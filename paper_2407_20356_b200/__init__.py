@@ -54,7 +54,11 @@ class BindingError(Error):
 
 
 class FormatError(Error):
-    pass
+    """xpcs::FormatError; ``offset`` = byte offset of the first inconsistency."""
+
+    def __init__(self, msg: str, offset: int = -1):
+        super().__init__(msg)
+        self.offset = offset
 
 
 class DeviceError(Error):
@@ -80,6 +84,8 @@ def _check(ctx_handle, rc: int) -> None:
         raise NormalizationError(msg, int(frame), int(ring.value))
     if rc == _abi.ERR_RANK:
         raise RankError(msg, int(lib.xg_last_error_payload(ctx_handle, None)))
+    if rc == _abi.ERR_FORMAT:
+        raise FormatError(msg, int(lib.xg_last_error_payload(ctx_handle, None)))
     raise _ERRS.get(rc, DeviceError)(msg or f"status {rc}")
 
 
@@ -103,6 +109,54 @@ def _as_counts_u8(frames) -> np.ndarray:
 
 def _ptr(a: np.ndarray) -> C.c_void_p:
     return C.c_void_p(a.ctypes.data)
+
+
+# ---------------------------------------------------------------- formats
+def _io_check(rc: int) -> None:
+    """Errors of the host format helpers (xg_io_*)."""
+    if rc == _abi.OK:
+        return
+    msg = lib.xg_io_last_error().decode()
+    payload = int(lib.xg_io_last_payload())
+    if rc == _abi.ERR_FORMAT:
+        raise FormatError(msg, payload)
+    if rc == _abi.ERR_NORMALIZATION:
+        raise NormalizationError(msg, payload)
+    raise _ERRS.get(rc, DeviceError)(msg or f"status {rc}")
+
+
+def write_xfsr(path, frames, frame_period: float = 1.0) -> None:
+    """XFSR frames file with dtype 3 = u8 photon counts (new; the reference's
+    io.cpp:150-184 writes u16/f32/f64)."""
+    a = _as_counts_u8(frames)
+    if a.ndim != 2:
+        raise ShapeError("frames must be N x M")
+    _io_check(lib.xg_io_write_xfsr_u8(str(path).encode(), _ptr(a), a.shape[0], a.shape[1],
+                                      float(frame_period)))
+
+
+def read_xfsr(path):
+    """Any XFSR frames file (dtype u16/f32/f64 as the reference, or u8) as
+    u8 photon counts + frame period; read_frames' checks (io.cpp:187-225)."""
+    n, m, per = C.c_int64(0), C.c_int64(0), C.c_double(0.0)
+    p = str(path).encode()
+    _io_check(lib.xg_io_read_xfsr_u8(p, None, 0, C.byref(n), C.byref(m), C.byref(per)))
+    out = np.empty((n.value, m.value), np.uint8)
+    _io_check(lib.xg_io_read_xfsr_u8(p, _ptr(out), out.size, C.byref(n), C.byref(m),
+                                     C.byref(per)))
+    return out, per.value
+
+
+def write_xcmp(path, coefficients, norms, encoder_hash: int, append: bool = False) -> None:
+    """XCMP compressed store from host rows (io.cpp:319-441; append like
+    CompressedFileAppender)."""
+    y = np.ascontiguousarray(coefficients, dtype=np.float64)
+    nr = np.ascontiguousarray(norms, dtype=np.float64)
+    if y.ndim != 2 or nr.shape != (y.shape[0],):
+        raise ShapeError("coefficients must be N x k with N norms")
+    _io_check(lib.xg_io_write_xcmp(str(path).encode(), y.shape[1], int(encoder_hash), y.shape[0],
+                                   nr.ctypes.data_as(_abi.PD), y.ctypes.data_as(_abi.PD),
+                                   1 if append else 0))
 
 
 # ---------------------------------------------------------------- context
@@ -378,6 +432,19 @@ class FrameSeries:
         _check(self.ctx.h, lib.xg_series_rel_error(self.h, out.ctypes.data_as(_abi.PD)))
         return out
 
+    def write_xcmp(self, ring: int, path, encoder_hash: int, append: bool = False) -> None:
+        """This ring's compressed rows as an XCMP store (io.cpp:319-441)."""
+        _check(self.ctx.h, lib.xg_series_write_xcmp(self.h, ring, str(path).encode(),
+                                                     int(encoder_hash), 1 if append else 0))
+
+    def load_xfsr(self, path) -> "FrameSeries":
+        """Load an XFSR frames file (u16/f32/f64 as the reference, or u8) of
+        photon counts; the series takes the file's frame period."""
+        per = C.c_double(0.0)
+        _check(self.ctx.h, lib.xg_series_load_xfsr(self.h, str(path).encode(), C.byref(per)))
+        self.frame_period = per.value
+        return self
+
     def ttc_background(self, exclusion: int = 0, compressed: bool = False) -> np.ndarray:
         """Per-ring ttc_background (analysis.cpp:202-235) of the stored raw or
         compressed TTC, on the device: sigma of the entries with lag > exclusion."""
@@ -487,7 +554,8 @@ class FrameSeries:
 
 
 __all__ = [
-    "Context", "RingLayout", "FrameSeries", "Error", "ShapeError", "ContractError", "MaskError",
+    "Context", "RingLayout", "FrameSeries", "FrameStream", "Basis", "write_xfsr", "read_xfsr",
+    "write_xcmp", "Error", "ShapeError", "ContractError", "MaskError",
     "NormalizationError", "RankError", "BindingError", "FormatError", "DeviceError",
 ]
 
@@ -522,6 +590,12 @@ class FrameStream:
     @property
     def n_frames(self) -> int:
         return int(lib.xg_stream_frames(self.h))
+
+    def append_xcmp(self, ring: int, path, encoder_hash: int, from_frame: int = 0) -> None:
+        """Append this ring's compressed rows [from_frame, t) to an XCMP store
+        (CompressedFileAppender, io.cpp:368-441; created if missing)."""
+        _check(self.ctx.h, lib.xg_stream_append_xcmp(self.h, ring, str(path).encode(),
+                                                      int(encoder_hash), int(from_frame)))
 
     def push(self, frame) -> None:
         if hasattr(frame, "data_ptr"):

@@ -52,6 +52,14 @@ _sigs = {
     "xg_series_get_g2": (C.c_int, [P, I32, PD, PI64]),
     "xg_series_get_g2_all": (C.c_int, [P, PD, PI64]),
     "xg_series_rel_error": (C.c_int, [P, PD]),
+    "xg_series_write_xcmp": (C.c_int, [P, I32, C.c_char_p, C.c_uint64, I32]),
+    "xg_stream_append_xcmp": (C.c_int, [P, I32, C.c_char_p, C.c_uint64, I64]),
+    "xg_series_load_xfsr": (C.c_int, [P, C.c_char_p, PD]),
+    "xg_io_last_error": (C.c_char_p, []),
+    "xg_io_last_payload": (I64, []),
+    "xg_io_write_xcmp": (C.c_int, [C.c_char_p, I64, C.c_uint64, I64, PD, PD, I32]),
+    "xg_io_write_xfsr_u8": (C.c_int, [C.c_char_p, P, I64, I64, C.c_double]),
+    "xg_io_read_xfsr_u8": (C.c_int, [C.c_char_p, P, I64, PI64, PI64, PD]),
     "xg_series_ttc_background": (C.c_int, [P, I32, I64, PD]),
     "xg_series_fit_kww": (C.c_int, [P, I32, C.c_double, C.c_double, C.c_double, PD, C.POINTER(I32)]),
     "xg_series_build_basis": (C.c_int, [P, I32, C.POINTER(PD), PD, I64, PI64, P]),

@@ -2325,6 +2325,77 @@ int xg_stream_get_coeffs(xg_stream* s, int32_t ring, double* y, double* norms) {
   return check_device_error(c);
 }
 
+// ------------------------------------------------ formats
+// rows [t0, t1) of one ring (coefficients [ring][tp][k], norms [ring][tp])
+// to an XCMP store through the host writer (xg_io.cpp)
+static int write_xcmp_rows(xg_ctx* c, const double* d_y, const double* d_norms, int64_t tp,
+                           int64_t k, int32_t ring, int64_t t0, int64_t t1, const char* path,
+                           uint64_t hash, int32_t append) {
+  const int64_t n = t1 - t0;
+  std::vector<double> y((size_t)std::max<int64_t>(n, 0) * k), nr((size_t)std::max<int64_t>(n, 0));
+  if (n > 0) {
+    XG_CUDA(c, cudaMemcpyAsync(y.data(), d_y + ((int64_t)ring * tp + t0) * k, (size_t)n * k * 8,
+                               cudaMemcpyDeviceToHost, c->stream));
+    XG_CUDA(c, cudaMemcpyAsync(nr.data(), d_norms + (int64_t)ring * tp + t0, (size_t)n * 8,
+                               cudaMemcpyDeviceToHost, c->stream));
+    XG_CUDA(c, cudaStreamSynchronize(c->stream));
+  }
+  const int rc = xg_io_write_xcmp(path, k, hash, n, nr.data(), y.data(), append);
+  if (rc == XG_OK) return check_device_error(c);
+  if (rc == XG_ERR_NORMALIZATION) {
+    c->payload = t0 + xg_io_last_payload();
+    c->payload_ring = ring;
+    return fail(c, rc, "write_xcmp: frame %lld of ring %d has zero norm", (long long)c->payload, ring);
+  }
+  if (rc == XG_ERR_FORMAT) c->payload = xg_io_last_payload();
+  return fail(c, rc, "%s", xg_io_last_error());
+}
+
+int xg_series_write_xcmp(xg_series* s, int32_t ring, const char* path, uint64_t hash,
+                         int32_t append) {
+  if (!s || !path) return XG_ERR_INVALID;
+  xg_ctx* c = s->ctx;
+  if (ring < 0 || ring >= s->L->rings) return fail(c, XG_ERR_SHAPE, "ring %d out of range", ring);
+  if (!s->have_y) return fail(c, XG_ERR_CONTRACT, "write_xcmp: compress first");
+  return write_xcmp_rows(c, s->d_y, s->d_norms, s->tp, s->ck, ring, 0, s->t, path, hash, append);
+}
+
+int xg_stream_append_xcmp(xg_stream* s, int32_t ring, const char* path, uint64_t hash,
+                          int64_t from_frame) {
+  if (!s || !path) return XG_ERR_INVALID;
+  xg_ctx* c = s->ctx;
+  if (ring < 0 || ring >= s->L->rings) return fail(c, XG_ERR_SHAPE, "ring %d out of range", ring);
+  if (!s->B) return fail(c, XG_ERR_CONTRACT, "stream has no basis");
+  if (from_frame < 0 || from_frame > s->t)
+    return fail(c, XG_ERR_SHAPE, "append_xcmp: from_frame %lld outside [0, %lld]",
+                (long long)from_frame, (long long)s->t);
+  return write_xcmp_rows(c, s->d_y, s->d_norms, s->tp, s->B->k, ring, from_frame, s->t, path, hash, 1);
+}
+
+int xg_series_load_xfsr(xg_series* s, const char* path, double* period) {
+  if (!s || !path) return XG_ERR_INVALID;
+  xg_ctx* c = s->ctx;
+  int64_t n = 0, m = 0;
+  double per = 0.0;
+  int rc = xg_io_read_xfsr_u8(path, nullptr, 0, &n, &m, &per);
+  if (rc == XG_OK) {
+    if (m != s->L->pixels)
+      return fail(c, XG_ERR_SHAPE, "load_xfsr: file frames have %lld pixels, layout %lld",
+                  (long long)m, (long long)s->L->pixels);
+    if (n > s->xmax)
+      return fail(c, XG_ERR_SHAPE, "load_xfsr: %lld frames, capacity %lld", (long long)n,
+                  (long long)s->xmax);
+    std::vector<uint8_t> buf((size_t)n * m);
+    rc = xg_io_read_xfsr_u8(path, buf.data(), (int64_t)buf.size(), &n, &m, &per);
+    if (rc == XG_OK) {
+      if (period) *period = per;
+      return xg_series_load_frames(s, buf.data(), n, 0);
+    }
+  }
+  if (rc == XG_ERR_FORMAT || rc == XG_ERR_CONTRACT) c->payload = xg_io_last_payload();
+  return fail(c, rc, "%s", xg_io_last_error());
+}
+
 // Full n x n TTC of a ring from the stored columns (XG_STREAM_STORE_TTC).
 int xg_stream_get_ttc(xg_stream* s, int32_t ring, int32_t which, int32_t dtype, void* out,
                       int64_t ld) {
