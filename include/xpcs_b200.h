@@ -168,6 +168,13 @@ XG_API int xg_series_write_xcmp(xg_series* s, int32_t ring, const char* path,
 XG_API int xg_stream_append_xcmp(xg_stream* s, int32_t ring, const char* path,
                                  uint64_t encoder_hash, int64_t from_frame);
 XG_API int xg_series_load_xfsr(xg_series* s, const char* path, double* frame_period);
+/* TTC tile sink (new format; CSV export, io.cpp:465-478, does not scale to
+ * C4/C5): "XTTC", u32 1, u32 dtype (0 f64 C, 1 f32 C~, 2 i32 exact Gram),
+ * u64 n, then the upper triangle row after row (row i: columns i..n-1),
+ * streamed from the stored tiles; which 0 raw (XG_F64 or XG_I32_GRAM),
+ * 1 compressed (XG_F32). */
+XG_API int xg_series_write_ttc(xg_series* s, int32_t ring, int32_t which, int32_t dtype,
+                               const char* path);
 XG_API const char* xg_io_last_error(void);
 XG_API int64_t xg_io_last_payload(void);
 XG_API int xg_io_write_xcmp(const char* path, int64_t k, uint64_t encoder_hash, int64_t n,

@@ -147,6 +147,26 @@ def read_xfsr(path):
     return out, per.value
 
 
+def read_xttc(path) -> np.ndarray:
+    """An XTTC tile file (FrameSeries.write_ttc) as the full symmetric matrix."""
+    raw = open(path, "rb").read()
+    if len(raw) < 20 or raw[:4] != b"XTTC":
+        raise FormatError("bad magic, expected \"XTTC\"", 0)
+    ver, code = np.frombuffer(raw[4:12], "<u4")
+    n = int(np.frombuffer(raw[12:20], "<u8")[0])
+    if ver != 1 or code > 2:
+        raise FormatError(f"unsupported XTTC version {ver} / dtype {code}", 4)
+    dt = {0: "<f8", 1: "<f4", 2: "<i4"}[int(code)]
+    tri = np.frombuffer(raw[20:], dt)
+    if tri.size != n * (n + 1) // 2:
+        raise FormatError("XTTC payload length does not match n", 20)
+    out = np.zeros((n, n), tri.dtype)
+    iu = np.triu_indices(n)
+    out[iu] = tri
+    out.T[iu] = tri
+    return out
+
+
 def write_xcmp(path, coefficients, norms, encoder_hash: int, append: bool = False) -> None:
     """XCMP compressed store from host rows (io.cpp:319-441; append like
     CompressedFileAppender)."""
@@ -437,6 +457,14 @@ class FrameSeries:
         _check(self.ctx.h, lib.xg_series_write_xcmp(self.h, ring, str(path).encode(),
                                                      int(encoder_hash), 1 if append else 0))
 
+    def write_ttc(self, ring: int, path, dtype: str = "f64", compressed: bool = False) -> None:
+        """Stream one ring's stored TTC to an XTTC tile file (upper triangle,
+        row after row): raw as "f64" C or exact "gram" (int32); compressed as
+        "f32" C~.  read_xttc() loads it back."""
+        code = {"f64": 0, "f32": 1, "gram": 2}[dtype]
+        _check(self.ctx.h, lib.xg_series_write_ttc(self.h, ring, 1 if compressed else 0, code,
+                                                    str(path).encode()))
+
     def load_xfsr(self, path) -> "FrameSeries":
         """Load an XFSR frames file (u16/f32/f64 as the reference, or u8) of
         photon counts; the series takes the file's frame period."""
@@ -555,7 +583,7 @@ class FrameSeries:
 
 __all__ = [
     "Context", "RingLayout", "FrameSeries", "FrameStream", "Basis", "write_xfsr", "read_xfsr",
-    "write_xcmp", "Error", "ShapeError", "ContractError", "MaskError",
+    "write_xcmp", "read_xttc", "Error", "ShapeError", "ContractError", "MaskError",
     "NormalizationError", "RankError", "BindingError", "FormatError", "DeviceError",
 ]
 

@@ -55,6 +55,7 @@ _sigs = {
     "xg_series_write_xcmp": (C.c_int, [P, I32, C.c_char_p, C.c_uint64, I32]),
     "xg_stream_append_xcmp": (C.c_int, [P, I32, C.c_char_p, C.c_uint64, I64]),
     "xg_series_load_xfsr": (C.c_int, [P, C.c_char_p, PD]),
+    "xg_series_write_ttc": (C.c_int, [P, I32, I32, I32, C.c_char_p]),
     "xg_io_last_error": (C.c_char_p, []),
     "xg_io_last_payload": (I64, []),
     "xg_io_write_xcmp": (C.c_int, [C.c_char_p, I64, C.c_uint64, I64, PD, PD, I32]),

@@ -248,6 +248,33 @@ cudaError_t launch_g2(const G2Params& p, int mode, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// Upper-triangle rows [row0, row1) of one ring packed row after row (row i
+// holds columns i .. n-1): the TTC tile sink's staging.  Same entry
+// expressions as k_expand.
+__global__ void k_pack_upper(ExpandParams p, int src_mode, int64_t row0) {
+  const int64_t i = row0 + blockIdx.x;
+  if (i >= p.n) return;
+  const int64_t off = (i - row0) * p.n - ((i * (i - 1)) / 2 - (row0 * (row0 - 1)) / 2);
+  for (int64_t j = i + threadIdx.x; j < p.n; j += blockDim.x) {
+    const int64_t o = off + (j - i);
+    if (src_mode == 0) {
+      const int32_t g = p.gram[i * p.ld + j];
+      if (p.out_dtype == 2)
+        static_cast<int32_t*>(p.out)[o] = g;
+      else
+        static_cast<double*>(p.out)[o] = static_cast<double>(g) * (p.inv[i] * p.inv[j]);
+    } else {
+      static_cast<float*>(p.out)[o] = p.cf32[i * p.ld + j];
+    }
+  }
+}
+
+cudaError_t launch_pack_upper(const ExpandParams& p, int src_mode, int64_t row0, int64_t rows,
+                              cudaStream_t s) {
+  k_pack_upper<<<static_cast<unsigned>(rows), 256, 0, s>>>(p, src_mode, row0);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_expand(const ExpandParams& p, int src_mode, cudaStream_t s) {
   const unsigned nt = static_cast<unsigned>((p.n + 31) / 32);
   dim3 grid(nt, nt);

@@ -2372,6 +2372,77 @@ int xg_stream_append_xcmp(xg_stream* s, int32_t ring, const char* path, uint64_t
   return write_xcmp_rows(c, s->d_y, s->d_norms, s->tp, s->B->k, ring, from_frame, s->t, path, hash, 1);
 }
 
+// TTC tile sink: "XTTC", u32 version 1, u32 dtype (0 f64 C, 1 f32 C~, 2 i32
+// exact Gram), u64 n, then the upper triangle row after row (row i: columns
+// i .. n-1), little-endian; size 20 + n (n + 1) / 2 * elem.  Streamed from
+// the stored tiles in blocks of 256 rows (CSV export, io.cpp:465-478, does
+// not scale to C4/C5 TTCs).
+int xg_series_write_ttc(xg_series* s, int32_t ring, int32_t which, int32_t dtype,
+                        const char* path) {
+  if (!s || !path) return XG_ERR_INVALID;
+  xg_ctx* c = s->ctx;
+  if (ring < 0 || ring >= s->L->rings) return fail(c, XG_ERR_SHAPE, "ring %d out of range", ring);
+  if (which == 0 ? !(s->have_raw && s->raw_stored) : !(s->have_cttc && s->cmp_stored))
+    return fail(c, XG_ERR_CONTRACT, "write_ttc: needs a stored %s TTC", which == 0 ? "raw" : "compressed");
+  if (which == 0 ? (dtype != XG_F64 && dtype != XG_I32_GRAM) : dtype != XG_F32)
+    return fail(c, XG_ERR_CONTRACT, "write_ttc: dtype %d not available for this TTC", dtype);
+  const int64_t n = s->t;
+  const int elem = dtype == XG_F64 ? 8 : 4;
+  const uint32_t code = dtype == XG_F64 ? 0u : dtype == XG_F32 ? 1u : 2u;
+  FILE* f = fopen(path, "wb");
+  if (!f) return fail(c, XG_ERR_FORMAT, "cannot create TTC file %s", path);
+  struct Closer {
+    FILE* f;
+    ~Closer() {
+      if (f) fclose(f);
+    }
+  } closer{f};
+  uint8_t head[20];
+  std::memcpy(head, "XTTC", 4);
+  const uint32_t ver = 1;
+  const uint64_t nn = static_cast<uint64_t>(n);
+  for (int i = 0; i < 4; ++i) head[4 + i] = static_cast<uint8_t>(ver >> (8 * i));
+  for (int i = 0; i < 4; ++i) head[8 + i] = static_cast<uint8_t>(code >> (8 * i));
+  for (int i = 0; i < 8; ++i) head[12 + i] = static_cast<uint8_t>(nn >> (8 * i));
+  if (fwrite(head, 1, 20, f) != 20) return fail(c, XG_ERR_FORMAT, "failed writing TTC file %s", path);
+  constexpr int64_t RB = 256;
+  const size_t cap = static_cast<size_t>(RB) * n * elem;
+  void* d_stage = nullptr;
+  XG_CUDA(c, cudaMalloc(&d_stage, cap));
+  std::vector<uint8_t> h(cap);
+  ExpandParams p;
+  p.gram = which == 0 ? s->d_gram + (int64_t)ring * s->tp * s->tp : nullptr;
+  p.cf32 = which == 0 ? nullptr : s->d_cgram + (int64_t)ring * s->tp * s->tp;
+  p.ring_stride = 0;
+  p.ld = static_cast<int32_t>(s->tp);
+  p.inv = s->d_inv + (int64_t)ring * s->tp;
+  p.n = n;
+  p.out = d_stage;
+  p.out_ld = 0;
+  p.out_dtype = dtype;
+  int rc = XG_OK;
+  for (int64_t r0 = 0; r0 < n && rc == XG_OK; r0 += RB) {
+    const int64_t rows = std::min(RB, n - r0);
+    const int64_t cnt = rows * n - ((r0 + rows) * (r0 + rows - 1) / 2 - r0 * (r0 - 1) / 2);
+    cudaError_t e = launch_pack_upper(p, which, r0, rows, c->stream);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(h.data(), d_stage, (size_t)cnt * elem, cudaMemcpyDeviceToHost, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) {
+      rc = cuda_fail(c, e, "write_ttc");
+      break;
+    }
+    c->launches++;
+    if (fwrite(h.data(), 1, (size_t)cnt * elem, f) != (size_t)cnt * elem)
+      rc = fail(c, XG_ERR_FORMAT, "failed writing TTC file %s", path);
+  }
+  cudaFree(d_stage);
+  if (rc) return rc;
+  closer.f = nullptr;
+  if (fclose(f) != 0) return fail(c, XG_ERR_FORMAT, "failed writing TTC file %s", path);
+  return check_device_error(c);
+}
+
 int xg_series_load_xfsr(xg_series* s, const char* path, double* period) {
   if (!s || !path) return XG_ERR_INVALID;
   xg_ctx* c = s->ctx;

@@ -299,6 +299,9 @@ struct ExpandParams {
   int32_t out_dtype;         // 0 f64, 1 f32, 2 i32 (raw Gram)
 };
 cudaError_t launch_expand(const ExpandParams& p, int src_mode, cudaStream_t s);
+// rows [row0, row0 + rows) of the upper triangle, packed (row i: columns i..n-1)
+cudaError_t launch_pack_upper(const ExpandParams& p, int src_mode, int64_t row0, int64_t rows,
+                              cudaStream_t s);
 
 // ttc_rel_error (correlate.cpp:87-108) of every ring between the stored raw
 // TTC (exact Gram * 1/|x_i| 1/|x_j|) and the stored compressed C~, over the

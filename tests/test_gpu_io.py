@@ -64,3 +64,23 @@ def test_load_xfsr_equals_direct_load(ctx, orc, ref, tmp_path, dtype):
         assert np.array_equal(a.ttc(r, "gram"), b.ttc(r, "gram"))
     with pytest.raises(xg.ShapeError):
         xg.FrameSeries(xg.RingLayout(ctx, 100, [np.arange(10)]), 90).load_xfsr(p)
+
+
+def test_ttc_tile_sink_round_trip(ctx, orc, tmp_path):
+    """XTTC tile files stream the stored TTC (upper triangle, 256-row blocks)
+    and read back to exactly the readback matrices."""
+    frames, ring, lay = _setup(ctx, orc, 300, 40, 40, 2, 0.5, 84)
+    basis = xg.Basis(lay, 8)
+    xg.FrameSeries(lay, 40).load(frames[:40]).build_basis(8, basis=basis)
+    s = xg.FrameSeries(lay, 300).load(frames).ttc_raw()
+    s.compress(basis).ttc_compressed()
+    for r in range(2):
+        s.write_ttc(r, tmp_path / "g.xttc", "gram")
+        assert np.array_equal(xg.read_xttc(tmp_path / "g.xttc"), s.ttc(r, "gram"))
+        s.write_ttc(r, tmp_path / "c.xttc", "f64")
+        assert np.array_equal(xg.read_xttc(tmp_path / "c.xttc"), s.ttc(r, "f64"))
+        s.write_ttc(r, tmp_path / "k.xttc", "f32", compressed=True)
+        assert np.array_equal(xg.read_xttc(tmp_path / "k.xttc"), s.cttc(r, "f32"))
+    assert (tmp_path / "g.xttc").stat().st_size == 20 + 300 * 301 // 2 * 4
+    with pytest.raises(xg.ContractError):
+        s.write_ttc(0, tmp_path / "x.xttc", "f32")  # raw TTC has no f32 sink
