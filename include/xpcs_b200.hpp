@@ -151,16 +151,19 @@ class RingLayout {
     }
     ctx.check(xg_layout_create(ctx.get(), full_pixels, static_cast<int32_t>(masks.size()),
                                off.data(), idx.data(), &h_));
+    rings_ = static_cast<int32_t>(masks.size());
   }
   ~RingLayout() { xg_layout_destroy(h_); }
   RingLayout(const RingLayout&) = delete;
   RingLayout& operator=(const RingLayout&) = delete;
   xg_layout* get() const { return h_; }
   const Context& ctx() const { return ctx_; }
+  int32_t rings() const { return rings_; }
 
  private:
   const Context& ctx_;
   xg_layout* h_ = nullptr;
+  int32_t rings_ = 0;
 };
 
 class Basis {
@@ -228,6 +231,51 @@ class Series {
     if (counts) *counts = std::move(c);
     return v;
   }
+  // build_online_from_frames per ring on the device (k = 0: build_offline);
+  // fills b (k > 0) and returns each ring's numerical rank
+  std::vector<int64_t> build_basis(int32_t k, Basis* b = nullptr) {
+    std::vector<int64_t> rank(static_cast<size_t>(rings()));
+    L_.ctx().check(xg_series_build_basis(h_, k, nullptr, nullptr, 0, rank.data(),
+                                         b ? b->get() : nullptr));
+    return rank;
+  }
+  // analysis.cpp on the device: ttc_background per ring; fit_kww per ring
+  // (KwwFit fields B, C, t0, rms + status 0 ok / 1 degenerate / 2 no
+  // convergence / 3 contract)
+  std::vector<double> ttc_background(int64_t exclusion = 0, bool compressed = false) {
+    std::vector<double> out(static_cast<size_t>(rings()));
+    L_.ctx().check(xg_series_ttc_background(h_, compressed ? 1 : 0, exclusion, out.data()));
+    return out;
+  }
+  struct KwwFit {
+    double baseline, contrast, relaxation_time, residual_rms;
+    int32_t status;
+  };
+  std::vector<KwwFit> fit_kww(double frame_period, double min_lag, double max_lag,
+                              bool compressed = false) {
+    const int32_t q = rings();
+    std::vector<double> o(static_cast<size_t>(4 * q));
+    std::vector<int32_t> st(static_cast<size_t>(q));
+    L_.ctx().check(xg_series_fit_kww(h_, compressed ? 1 : 0, frame_period, min_lag, max_lag,
+                                     o.data(), st.data()));
+    std::vector<KwwFit> out;
+    for (int32_t r = 0; r < q; ++r) out.push_back({o[4 * r], o[4 * r + 1], o[4 * r + 2], o[4 * r + 3], st[r]});
+    return out;
+  }
+  // io.cpp formats next to the device buffers
+  void write_xcmp(int32_t ring, const std::string& path, uint64_t encoder_hash, bool append = false) {
+    L_.ctx().check(xg_series_write_xcmp(h_, ring, path.c_str(), encoder_hash, append ? 1 : 0));
+  }
+  double load_xfsr(const std::string& path) {
+    double period = 0.0;
+    L_.ctx().check(xg_series_load_xfsr(h_, path.c_str(), &period));
+    return period;
+  }
+  void write_ttc(int32_t ring, const std::string& path, xg_dtype dtype = XG_F64,
+                 bool compressed = false) {
+    L_.ctx().check(xg_series_write_ttc(h_, ring, compressed ? 1 : 0, dtype, path.c_str()));
+  }
+  int32_t rings() const { return L_.rings(); }
   xg_series* get() const { return h_; }
 
  private:

@@ -4,6 +4,7 @@
 // Gram diagonal checksum, the f64 TTC checksum and g2[0..2] of every ring.
 #include <cstdio>
 #include <fstream>
+#include <string>
 #include <vector>
 
 #include "xpcs_b200.hpp"
@@ -33,6 +34,22 @@ int main(int argc, char** argv) {
       for (double v : c) sum += v;
       const auto g2 = s.g2(r);
       std::printf("ring %d sum %.17g g2 %.17g %.17g %.17g\n", r, sum, g2[0], g2[1], g2[2]);
+    }
+    // device basis, compressed TTC, analysis and formats through the facade
+    {
+      xpcs_b200::Basis b(layout, 4);
+      const auto rank = s.build_basis(4, &b);
+      s.compress(b);
+      s.ttc_compressed();
+      const auto bg = s.ttc_background(2);
+      const auto fits = s.fit_kww(1.0, 1.0, static_cast<double>(n / 2));
+      std::printf("basis rank %lld bg %.6g fit status %d\n", (long long)rank[0], bg[0], fits[0].status);
+      s.write_xcmp(0, "/tmp/facade_r0.xcmp", 42);
+      s.write_ttc(0, "/tmp/facade_r0.xttc", XG_I32_GRAM);
+      xpcs_b200::Series s3(layout, n);
+      s3.load_xfsr("/tmp/facade_frames.xfsr");  // written by the test (u8 XFSR)
+      s3.ttc_raw();
+      std::printf("xfsr load %s\n", s3.ttc(0) == s.ttc(0) ? "equal" : "DIFFERENT");
     }
     // reference-facing exact entry on the same ring 0 data
     std::vector<double> x0;

@@ -20,6 +20,8 @@ def test_cpp_facade(tmp_path, orc):
     frames = orc.gen_speckle(n, h, w, q, 0.4, 3)
     ring, _ = orc.ring_map(h, w, q)
     frames.tofile(tmp_path / "f.u8")
+    import paper_2407_20356_b200 as xg
+    xg.write_xfsr("/tmp/facade_frames.xfsr", frames, 1.0)
     ring.astype(np.int32).tofile(tmp_path / "r.i32")
     out = subprocess.run([EXE, str(tmp_path / "f.u8"), str(tmp_path / "r.i32"), str(n),
                           str(h * w), str(q)], capture_output=True, text=True, timeout=120)
@@ -32,8 +34,12 @@ def test_cpp_facade(tmp_path, orc):
         g2 = orc.g2_from_ttc(c)[1]
         assert np.allclose([float(x) for x in parts[5:8]], g2[:3], atol=1e-12, rtol=0)
     c0 = orc.ttc_raw(frames[:, ring == 0].astype(np.float64))
+    basis = lines[q].split()  # device basis + compressed TTC + analysis + formats
+    assert basis[:3] == ["basis", "rank", "4"] or int(basis[2]) >= 4
+    assert float(basis[4]) > 0.0 and basis[7] in ("0", "1", "2")
+    assert lines[q + 1] == "xfsr load equal"
     # the exact entry returns the reference's bits: same sum up to summation order
-    assert abs(float(lines[q].split()[-1]) - float(c0.sum())) <= 1e-12 * c0.size
-    assert lines[q + 1] == "f64 load equal"
-    assert lines[q + 2] == "ContractError non-integer"
-    assert lines[q + 3] == "NormalizationError frame 1"
+    assert abs(float(lines[q + 2].split()[-1]) - float(c0.sum())) <= 1e-12 * c0.size
+    assert lines[q + 3] == "f64 load equal"
+    assert lines[q + 4] == "ContractError non-integer"
+    assert lines[q + 5] == "NormalizationError frame 1"
