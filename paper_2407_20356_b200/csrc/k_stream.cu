@@ -338,6 +338,31 @@ __global__ void __launch_bounds__(SI_THREADS) k_stream_ingest_sparse(StreamParam
     p.nz_val[e] = v;
     if (p.hist) p.hist[static_cast<int64_t>(col) * p.hp + p.t] = v;
   }
+  // the last CTA to finish computes frame t's norms, 1/|x|, nonzero bit and
+  // zero-frame bookkeeping (k_norms' expressions) -- no separate launch
+  __shared__ bool last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(p.done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int r = threadIdx.x; r < p.n_rings; r += blockDim.x) {
+    const long long n2 = static_cast<long long>(atomicAdd(p.norm2 + p.t * p.n_rings + r, 0ull));
+    const double nrm = sqrt(static_cast<double>(n2));
+    p.norms_w[r * p.inv_ld + p.t] = nrm;
+    p.inv_w[r * p.inv_ld + p.t] = n2 > 0 ? 1.0 / nrm : 0.0;
+    if (n2 > 0) {
+      atomicOr(p.nz_bits + static_cast<int64_t>(r) * p.nz_words + (p.t >> 5), 1u << (p.t & 31));
+    } else {
+      atomicAdd(reinterpret_cast<unsigned long long*>(p.zero_count + r), 1ull);
+      atomicMin(reinterpret_cast<long long*>(p.first_zero + r), static_cast<long long>(p.t));
+    }
+    if (n2 >= (1ll << 31)) atomicOr(p.err, 4);
+  }
+  if (threadIdx.x == 0) *p.done = 0u;
 }
 
 // K5s: grid (ceil((t+1)/SS_F), rings), 8 warps.  A CTA owns SS_F = 32 SS_V

@@ -2006,6 +2006,7 @@ struct xg_stream {
   int32_t* d_nz_col = nullptr;
   uint8_t* d_nz_val = nullptr;
   int32_t* d_nz_n = nullptr;     // [2][ring]: counts of even / odd pushes
+  unsigned int* d_done = nullptr;  // sparse ingest's CTA counter
 };
 
 extern "C" {
@@ -2069,7 +2070,9 @@ int xg_stream_create(xg_ctx* c, const xg_layout* L, const xg_basis* B, int64_t m
     for (int32_t r = 0; r < L->rings; ++r)
       for (int64_t col = L->koff[r]; col < L->koff[r] + L->kpad[r]; ++col)
         if (L->colpix[col] >= 0) pc[L->colpix[col]] = (r << 22) | static_cast<int32_t>(col);
-    if ((e = dalloc(&s->d_pixcol, pc.size())) != cudaSuccess ||
+    if ((e = dalloc(&s->d_done, 1)) != cudaSuccess ||
+        (e = cudaMemset(s->d_done, 0, 4)) != cudaSuccess ||
+        (e = dalloc(&s->d_pixcol, pc.size())) != cudaSuccess ||
         (e = cudaMemcpy(s->d_pixcol, pc.data(), pc.size() * 4, cudaMemcpyHostToDevice)) !=
             cudaSuccess) {
       xg_stream_destroy(s);
@@ -2173,6 +2176,7 @@ void xg_stream_destroy(xg_stream* s) {
   dfree(s->d_colpix);
   dfree(s->d_blk_ring);
   dfree(s->d_pixcol);
+  dfree(s->d_done);
   dfree(s->d_pacc);
   dfree(s->d_nz_col);
   dfree(s->d_nz_val);
@@ -2239,7 +2243,16 @@ int xg_stream_push(xg_stream* s, const uint8_t* frame, int on_device) {
   sp.norm2_next = s->t + 1 < s->tmax
                       ? reinterpret_cast<unsigned long long*>(s->d_norm2 + (s->t + 1) * L->rings)
                       : nullptr;
-  if (s->flags & XG_STREAM_SPARSE)
+  sp.norms_w = s->d_norms;
+  sp.inv_w = s->d_inv;
+  sp.zero_count = s->d_zero;
+  sp.first_zero = s->d_first_zero;
+  sp.nz_bits = s->d_nz_bits;
+  sp.nz_words = static_cast<int32_t>(s->tp / 32);
+  sp.err = c->d_err;
+  sp.done = s->d_done;
+  const bool sparse = (s->flags & XG_STREAM_SPARSE) != 0;
+  if (sparse)  // its last CTA also finishes the frame's norms
     XG_CUDA(c, launch_stream_ingest_sparse(sp, c->stream));
   else
     XG_CUDA(c, launch_stream_ingest(sp, c->stream));
@@ -2258,8 +2271,8 @@ int xg_stream_push(xg_stream* s, const uint8_t* frame, int on_device) {
   np.nz_words = static_cast<int32_t>(s->tp / 32);
   np.max_norm2 = nullptr;
   np.err = c->d_err;
-  XG_CUDA(c, launch_norms(np, c->stream));
-  c->launches += 2;
+  if (!sparse) XG_CUDA(c, launch_norms(np, c->stream));
+  c->launches += sparse ? 1 : 2;
   const bool raw = !(s->flags & XG_STREAM_NO_RAW);
   const bool fork = raw && s->B;  // compressed column on the side stream, overlapped
   if (fork) {

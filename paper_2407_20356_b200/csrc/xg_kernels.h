@@ -234,6 +234,15 @@ struct StreamParams {
   int32_t n_rings;
   unsigned long long* norm2; // [frame][ring] (row t zero on entry)
   unsigned long long* norm2_next;  // row t + 1, zeroed by the ingest (or null)
+  // sparse ingest: its last CTA finishes frame t's norms (k_norms' work)
+  double* norms_w;           // [ring][inv_ld]
+  double* inv_w;             // [ring][inv_ld]
+  int64_t* zero_count;       // [ring]
+  int64_t* first_zero;       // [ring]
+  uint32_t* nz_bits;         // [ring][nz_words]
+  int32_t nz_words;
+  int* err;
+  unsigned int* done;        // CTA counter (zero on entry, reset by the last CTA)
 };
 // One-frame ingest for the streaming path: ring-major row t of the history,
 // |x_t|^2 per ring, and in sparse mode the frame's nonzeros per ring plus
