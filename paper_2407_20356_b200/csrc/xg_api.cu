@@ -2055,7 +2055,7 @@ int xg_stream_create(xg_ctx* c, const xg_layout* L, const xg_basis* B, int64_t m
     return cuda_fail(c, e, "stream alloc");
   }
   if (flags & XG_STREAM_SPARSE) {
-    s->hp = round_up(max_frames, 16);
+    s->hp = round_up(max_frames, 128);  // whole 32-frame lane loads stay inside a row
     if ((e = dalloc(&s->d_hist, (size_t)L->ktot * s->hp)) != cudaSuccess) {
       xg_stream_destroy(s);
       return cuda_fail(c, e, "stream sparse history alloc");
