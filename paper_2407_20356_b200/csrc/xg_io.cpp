@@ -200,52 +200,67 @@ XG_API int xg_io_write_xfsr_u8(const char* path, const uint8_t* frames, int64_t 
 XG_API int xg_io_read_xfsr_u8(const char* path, uint8_t* out, int64_t out_cap, int64_t* n_out,
                               int64_t* m_out, double* period_out) {
   if (!path || !n_out || !m_out) return XG_ERR_INVALID;
-  std::vector<uint8_t> b;
-  if (!read_all(path, b)) return io_fail(XG_ERR_FORMAT, -1, "cannot open frames file %s", path);
-  if (b.size() < 4 || std::memcmp(b.data(), "XFSR", 4) != 0)
+  // header + size checks first, then the payload in 16 MB pieces (the file
+  // is never held in memory whole)
+  File fh;
+  fh.f = fopen(path, "rb");
+  if (!fh.f) return io_fail(XG_ERR_FORMAT, -1, "cannot open frames file %s", path);
+  if (fseeko(fh.f, 0, SEEK_END) != 0) return io_fail(XG_ERR_FORMAT, -1, "cannot read frames file %s", path);
+  const uint64_t size = static_cast<uint64_t>(ftello(fh.f));
+  rewind(fh.f);
+  uint8_t h[36];
+  const size_t got = fread(h, 1, sizeof h, fh.f);
+  if (got < 4 || std::memcmp(h, "XFSR", 4) != 0)
     return io_fail(XG_ERR_FORMAT, 0, "bad magic, expected \"XFSR\" for frames");
-  if (b.size() < 8) return io_fail(XG_ERR_FORMAT, (int64_t)b.size(), "frames file truncated, need 4 more bytes");
-  if (get_u32(b.data() + 4) != 1)
-    return io_fail(XG_ERR_FORMAT, 4, "unsupported frames version %u", get_u32(b.data() + 4));
-  if (b.size() < 36) return io_fail(XG_ERR_FORMAT, (int64_t)b.size(), "frames file truncated");
-  const uint32_t dtype = get_u32(b.data() + 8);
+  if (got < 8) return io_fail(XG_ERR_FORMAT, (int64_t)got, "frames file truncated, need 4 more bytes");
+  if (get_u32(h + 4) != 1) return io_fail(XG_ERR_FORMAT, 4, "unsupported frames version %u", get_u32(h + 4));
+  if (got < 36) return io_fail(XG_ERR_FORMAT, (int64_t)got, "frames file truncated");
+  const uint32_t dtype = get_u32(h + 8);
   if (dtype > 3) return io_fail(XG_ERR_FORMAT, 8, "unknown frames dtype %u", dtype);
-  const uint64_t n = get_u64(b.data() + 12), m = get_u64(b.data() + 20);
+  const uint64_t n = get_u64(h + 12), m = get_u64(h + 20);
   if (n < 1 || m < 1 || m > (1ull << 40) / n)
     return io_fail(XG_ERR_FORMAT, 12, "implausible frame dimensions %llux%llu", (unsigned long long)n,
                    (unsigned long long)m);
-  const double period = get_f64(b.data() + 28);
+  const double period = get_f64(h + 28);
   if (!(period > 0.0) || !std::isfinite(period))
     return io_fail(XG_ERR_FORMAT, 28, "frame period must be positive");
   const uint64_t elem = dtype == 0 ? 2 : dtype == 1 ? 4 : dtype == 2 ? 8 : 1;
   const uint64_t want = 36 + n * m * elem;
-  if (b.size() != want)
-    return io_fail(XG_ERR_FORMAT, (int64_t)std::min<uint64_t>(b.size(), want),
-                   "frames file length %zu, expected %llu", b.size(), (unsigned long long)want);
+  if (size != want)
+    return io_fail(XG_ERR_FORMAT, (int64_t)std::min<uint64_t>(size, want),
+                   "frames file length %llu, expected %llu", (unsigned long long)size,
+                   (unsigned long long)want);
   *n_out = static_cast<int64_t>(n);
   *m_out = static_cast<int64_t>(m);
   if (period_out) *period_out = period;
   if (!out) return XG_OK;
   if (out_cap < static_cast<int64_t>(n * m)) return XG_ERR_INVALID;
-  const uint8_t* p = b.data() + 36;
-  for (uint64_t i = 0; i < n * m; ++i) {
-    double v;
-    switch (dtype) {
-      case 0: v = static_cast<double>(p[2 * i] | (uint32_t(p[2 * i + 1]) << 8)); break;
-      case 1: {
-        const uint32_t u = get_u32(p + 4 * i);
-        float f;
-        std::memcpy(&f, &u, 4);
-        v = f;
-        break;
+  const uint64_t total = n * m, per = (16u << 20) / elem;
+  std::vector<uint8_t> buf(static_cast<size_t>(std::min<uint64_t>(total, per) * elem));
+  for (uint64_t i0 = 0; i0 < total; i0 += per) {
+    const uint64_t cnt = std::min<uint64_t>(per, total - i0);
+    if (fread(buf.data(), 1, cnt * elem, fh.f) != cnt * elem)
+      return io_fail(XG_ERR_FORMAT, (int64_t)(36 + i0 * elem), "cannot read frames file %s", path);
+    const uint8_t* p = buf.data();
+    for (uint64_t j = 0; j < cnt; ++j) {
+      double v;
+      switch (dtype) {
+        case 0: v = static_cast<double>(p[2 * j] | (uint32_t(p[2 * j + 1]) << 8)); break;
+        case 1: {
+          const uint32_t u = get_u32(p + 4 * j);
+          float f;
+          std::memcpy(&f, &u, 4);
+          v = f;
+          break;
+        }
+        case 2: v = get_f64(p + 8 * j); break;
+        default: v = p[j];
       }
-      case 2: v = get_f64(p + 8 * i); break;
-      default: v = p[i];
+      if (!(v >= 0.0 && v <= 255.0) || v != std::floor(v))
+        return io_fail(XG_ERR_CONTRACT, static_cast<int64_t>(36 + (i0 + j) * elem),
+                       "frame value %g is not a photon count in [0, 255]", v);
+      out[i0 + j] = static_cast<uint8_t>(v);
     }
-    if (!(v >= 0.0 && v <= 255.0) || v != std::floor(v))
-      return io_fail(XG_ERR_CONTRACT, static_cast<int64_t>(36 + i * elem),
-                     "frame value %g is not a photon count in [0, 255]", v);
-    out[i] = static_cast<uint8_t>(v);
   }
   return XG_OK;
 }

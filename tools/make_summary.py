@@ -22,7 +22,8 @@ def main():
              "(cold, serialised; compare SHARES)",
              "# command: python bench.py --steps 3 --warmup 3 --no-cpu-baseline",
              run("tools/launches.py", os.path.join(PROF, f"{rnd}_launches.csv")).rstrip(), ""]
-    for name in ("ingest", "gram_raw", "project", "gram_cmp", "stream_dense", "stream_sparse"):
+    for name in ("ingest", "gram_raw", "project", "gram_cmp", "stream_dense", "stream_sparse",
+                 "stream_cmp"):
         rep = os.path.join(PROF, f"{rnd}_{name}.ncu-rep")
         if not os.path.exists(rep):
             continue
