@@ -63,6 +63,8 @@ typedef enum xg_dtype { XG_F64 = 0, XG_F32 = 1, XG_I32_GRAM = 2 } xg_dtype;
                               (one product; ~1e-2 relative) instead of the
                               bf16x3 split (6 products; ~1e-6 relative) */
 #define XG_CHUNK_FIRST 0x10u /* xg_series_compress_chunk: first chunk of a series */
+#define XG_G2_SPECTRAL 0x20u /* xg_ttc_compressed: g2 only, from the coefficient series'
+                              autocorrelations by FFT (no C~ tile is formed; f64) */
 #define XG_NO_STORE 0x8u    /* g2 only: the TTC tiles never leave the chip (no
                               Q x T x T buffer is allocated or written; TTC
                               readback then fails) -- series whose TTC outgrows

@@ -540,12 +540,14 @@ class FrameSeries:
         return self
 
     def ttc_compressed(self, mode: str = "f32", g2: bool = True,
-                       store: bool = True) -> "FrameSeries":
+                       store: bool = True, spectral: bool = False) -> "FrameSeries":
         """Homomorphic TTC C~ = Y Y^T of every ring (ttc_compressed,
         correlate.cpp:27-35). mode 'f32' (bf16x3 split, ~1e-6) or 'bf16';
-        store=False keeps only g2."""
+        store=False keeps only g2.  spectral=True (with store=False): g2 from
+        the coefficient series' autocorrelations by FFT, in f64, without
+        forming any C~ tile (O(k T log T) instead of O(k T^2))."""
         flags = ((_abi.CMP_BF16 if mode == "bf16" else 0) | (0 if g2 else _abi.NO_G2)
-                 | (0 if store else _abi.NO_STORE))
+                 | (0 if store else _abi.NO_STORE) | (_abi.G2_SPECTRAL if spectral else 0))
         _check(self.ctx.h, lib.xg_ttc_compressed(self.h, flags))
         return self
 

@@ -130,6 +130,7 @@ NO_G2 = 0x2
 CMP_BF16 = 0x4
 NO_STORE = 0x8
 CHUNK_FIRST = 0x10
+G2_SPECTRAL = 0x20
 STREAM_STORE_TTC = 0x1
 STREAM_NO_RAW = 0x2
 STREAM_SPARSE = 0x4

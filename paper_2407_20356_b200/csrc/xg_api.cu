@@ -122,6 +122,8 @@ struct xg_series {
   int64_t* d_cg2cnt = nullptr;
   bool have_y = false, have_cttc = false;
   bool raw_g2 = false, cmp_g2 = false;  // g2 curves current (not XG_NO_G2)
+  void* d_spec = nullptr;           // XG_G2_SPECTRAL scratch (kept for the next call)
+  size_t spec_cap = 0;
   TileDesc* d_ptiles = nullptr;    // projection tiles
   int32_t n_ptiles = 0;
   int64_t ptiles_key = -1;
@@ -626,6 +628,7 @@ void xg_series_destroy(xg_series* s) {
   dfree(s->d_planes);
   dfree(s->d_cgram);
   dfree(s->d_cg2);
+  dfree(s->d_spec);
   dfree(s->d_cg2cnt);
   dfree(s->d_ptiles);
   delete s;
@@ -1773,6 +1776,38 @@ int xg_ttc_compressed(xg_series* s, uint32_t flags) {
   if (!s->d_cg2) {
     XG_CUDA(c, dalloc(&s->d_cg2, (size_t)L->rings * s->tp));
     XG_CUDA(c, dalloc(&s->d_cg2cnt, (size_t)L->rings * s->tp));
+  }
+  if (flags & XG_G2_SPECTRAL) {
+    // g2 only, in the Fourier domain (k_spectral.cu): no C~ tile at all
+    if (store || (flags & XG_NO_G2))
+      return fail(c, XG_ERR_CONTRACT, "ttc_compressed: XG_G2_SPECTRAL computes g2 only "
+                                      "(needs XG_NO_STORE, not XG_NO_G2)");
+    const size_t need = spectral_scratch_bytes(L->rings, s->t, s->ck);
+    if (need > s->spec_cap) {
+      dfree(s->d_spec);
+      s->spec_cap = 0;
+      XG_CUDA(c, cudaMalloc(&s->d_spec, need));
+      s->spec_cap = need;
+    }
+    SpecParams sp{};
+    sp.y = s->d_y;
+    sp.y_ld = s->tp;
+    sp.k = s->ck;
+    sp.n = s->t;
+    sp.n_rings = L->rings;
+    sp.nz_bits = s->d_nz_bits;
+    sp.nz_words = s->nz_words;
+    sp.zero_count = s->d_zero;
+    sp.g2 = s->d_cg2;
+    sp.counts = s->d_cg2cnt;
+    sp.g2_ld = s->tp;
+    const cudaError_t e = launch_spectral_g2(sp, s->d_spec, c->stream);
+    if (e != cudaSuccess) return cuda_fail(c, e, "spectral g2");
+    c->launches += 4;
+    s->cmp_stored = false;
+    s->have_cttc = true;
+    s->cmp_g2 = true;
+    return check_device_error(c);
   }
   if (store && !s->d_cgram) XG_CUDA(c, dalloc(&s->d_cgram, (size_t)L->rings * s->tp * s->tp));
   int rc = build_tiles(s);

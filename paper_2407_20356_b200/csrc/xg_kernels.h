@@ -363,6 +363,32 @@ struct KwwParams {
 };
 cudaError_t launch_fit_kww(const KwwParams& p, cudaStream_t s);
 
+// ---------------------------------------------------------- spectral g2 (compressed, g2 only)
+// g2 of C~ = Y Y^T from the coefficient series' autocorrelations by FFT
+// (k_spectral.cu): no T x T tile is formed.
+constexpr int SPEC_B = 4096;  // frames per time block
+constexpr int SPEC_L = 8192;  // FFT length (2 B: linear correlation)
+struct SpecParams {
+  const double* y;           // [ring][y_ld][k] coefficients (f64)
+  int64_t y_ld;
+  int32_t k;
+  int64_t n;
+  int32_t n_rings;
+  const uint32_t* nz_bits;   // [ring][nz_words]
+  int32_t nz_words;
+  const int64_t* zero_count; // [ring]
+  double* g2;                // [ring][g2_ld]
+  int64_t* counts;
+  int64_t g2_ld;
+  // set by the launcher inside the scratch buffer
+  int32_t nb, nm, npairs;
+  const double2* tw;
+  double2* spec;
+  double* corr;
+};
+size_t spectral_scratch_bytes(int n_rings, int64_t n, int k);
+cudaError_t launch_spectral_g2(SpecParams p, void* scratch, cudaStream_t s);
+
 // ---------------------------------------------------------- K8 synthetic
 struct SynthParams {
   int64_t t_first;           // global index of the first frame generated

@@ -163,3 +163,46 @@ def test_rel_error_report_matches_oracle(ctx, orc):
         ref = orc.ttc_rel_error(s.ttc(r, "f64"), s.cttc(r).astype(np.float64))
         assert abs(rel[r] - ref) <= 1e-12 * ref + 1e-15, (r, rel[r], ref)
         assert 0.0 < rel[r] < 1.0
+
+
+def _g2_exact(y, nr):
+    """f64 g2 of C~ = Y Y^T over the nonzero frames (per-lag dot products)."""
+    n = y.shape[0]
+    ok = nr > 0
+    sums = np.zeros(n)
+    cnt = np.zeros(n, np.int64)
+    for d in range(n):
+        sums[d] = float(np.einsum("ij,ij->", y[: n - d], y[d:]))
+        cnt[d] = int(np.sum(ok[: n - d] & ok[d:]))
+    return np.where(cnt > 0, sums / np.maximum(cnt, 1), 0.0), cnt
+
+
+@pytest.mark.parametrize("t,k,zero", [(1500, 16, False), (4100, 8, False), (9000, 5, True)])
+def test_spectral_g2_matches_exact_and_fused(ctx, orc, t, k, zero):
+    """XG_G2_SPECTRAL: g2 from the FFT of the coefficient series (one and
+    several 4096-frame blocks, odd k, a flagged frame) equals the f64 g2 of
+    Y Y^T to 1e-11 and the fused-epilogue g2 to its fp32 accuracy."""
+    h = w = 32
+    q = 2
+    frames = orc.gen_speckle(t, h, w, q, 0.5, 90 + k)
+    ring, _ = orc.ring_map(h, w, q)
+    if zero:
+        frames = frames.copy()
+        frames[4500, ring == 1] = 0
+    lay = xg.RingLayout.from_ring_map(ctx, ring, q)
+    basis = xg.Basis(lay, k)
+    xg.FrameSeries(lay, 64).load(frames[:64]).build_basis(k, basis=basis)
+    s = xg.FrameSeries(lay, t).load(frames).compress(basis)
+    s.ttc_compressed(store=False, spectral=True)
+    spec = [s.cg2(r) for r in range(q)]
+    s.ttc_compressed(store=False)
+    for r in range(q):
+        y, nr = s.coeffs(r)
+        g_ex, c_ex = _g2_exact(y, nr)
+        _, g_sp, c_sp = spec[r]
+        _, g_fu, c_fu = s.cg2(r)
+        assert np.array_equal(c_sp, c_ex) and np.array_equal(c_sp, c_fu)
+        assert np.abs(g_sp - g_ex).max() <= 1e-11 * np.abs(g_ex).max()
+        assert np.abs(g_sp - g_fu).max() <= 1e-5 * np.abs(g_ex).max()
+    with pytest.raises(xg.ContractError):
+        s.ttc_compressed(store=True, spectral=True)

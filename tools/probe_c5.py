@@ -53,8 +53,18 @@ def main():
     b.record(st)
     torch.cuda.synchronize()
     t_g2 = a.elapsed_time(b) / 1e3
+    ref_g2 = [s.cg2(r)[1] for r in (0, 64, 127)]
+    s.ttc_compressed(store=False, spectral=True)  # warm
+    a, b = ev(), ev()
+    a.record(st)
+    s.ttc_compressed(store=False, spectral=True)
+    b.record(st)
+    torch.cuda.synchronize()
+    t_sp = a.elapsed_time(b) / 1e3
+    dev = max(float(np.abs(s.cg2(r)[1] - g).max()) for r, g in zip((0, 64, 127), ref_g2))
     print(f"C5 T={T} {H}x{W} Q={Q} k={k}: ingest+project {t_cmp:.2f} s "
-          f"({T / t_cmp:.0f} frames/s), homomorphic g2 (no C~ store) {t_g2:.2f} s; "
+          f"({T / t_cmp:.0f} frames/s), homomorphic g2 (no C~ store) {t_g2:.2f} s, "
+          f"spectral g2 {t_sp:.3f} s (max |dg2| vs tiles {dev:.1e}); "
           f"synthetic generation {t_gen:.2f} s (untimed)")
     for r in (0, 64, 127):
         lags, g2, cnt = s.cg2(r)
