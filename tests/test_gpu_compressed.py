@@ -206,3 +206,45 @@ def test_spectral_g2_matches_exact_and_fused(ctx, orc, t, k, zero):
         assert np.abs(g_sp - g_fu).max() <= 1e-5 * np.abs(g_ex).max()
     with pytest.raises(xg.ContractError):
         s.ttc_compressed(store=True, spectral=True)
+
+
+def test_lossy_error_non_increasing_in_k(ctx, orc):
+    """Reference test_correlate.cpp:80-93 on the device path: with the
+    device-built offline basis truncated to k = 1 .. rank, ttc_rel_error(raw,
+    compressed) (device) does not increase with k (to the F32 mode's noise)
+    and full rank reaches the homomorphic identity."""
+    t, h, w, q = 24, 32, 32, 1
+    frames = orc.gen_speckle(t, h, w, q, 1.0, 95)
+    ring = np.zeros(h * w, np.int32)
+    lay = xg.RingLayout.from_ring_map(ctx, ring, q)
+    s = xg.FrameSeries(lay, t).load(frames).ttc_raw()
+    vs, _, rank = xg.FrameSeries(lay, t).load(frames).build_basis(0)
+    prev = 1e300
+    for k in range(1, int(rank[0]) + 1):
+        basis = xg.Basis(lay, k).set_ring(0, np.ascontiguousarray(vs[0][:, :k]))
+        s.compress(basis).ttc_compressed()
+        err = float(s.rel_error()[0])
+        assert err <= prev + 2e-6, (k, err, prev)
+        prev = err
+    assert prev <= 1e-5  # full rank: C~ == C to the F32 mode's accuracy
+
+
+def test_compressed_ttc_psd_and_unit_bounded(ctx, orc):
+    """Reference test_correlate.cpp:95-106: C~ of a truncated basis is
+    positive semidefinite and its diagonal <= 1 (here within the F32 mode's
+    1e-5 contract; C~ = Y Y^T with |y_t| <= 1)."""
+    t, h, w, q, k = 64, 32, 32, 2, 3
+    frames = orc.gen_speckle(t, h, w, q, 0.8, 96)
+    ring, _ = orc.ring_map(h, w, q)
+    lay = xg.RingLayout.from_ring_map(ctx, ring, q)
+    s = xg.FrameSeries(lay, t).load(frames)
+    basis = xg.Basis(lay, k)
+    xg.FrameSeries(lay, t).load(frames).build_basis(k, basis=basis)
+    s.compress(basis).ttc_compressed()
+    for r in range(q):
+        c = s.cttc(r)
+        lam = np.linalg.eigvalsh(c)
+        assert lam.min() >= -1e-5 * lam.max()
+        assert np.diag(c).max() <= 1.0 + 1e-5
+        y, _ = s.coeffs(r)
+        assert np.linalg.norm(y, axis=1).max() <= 1.0 + 1e-12
