@@ -40,8 +40,11 @@ constexpr int TMEM_COLS = 512;
 // dominates, so 4 stages and 8 epilogue warps (two per lane quarter, each
 // taking half the columns).
 template <int MODE> struct Cfg2 {
+#ifndef XG_K2_EPI
+#define XG_K2_EPI 8
+#endif
   static constexpr int STAGES = MODE == 0 ? 5 : 4;
-  static constexpr int EPI_WARPS = MODE == 0 ? 4 : 8;
+  static constexpr int EPI_WARPS = MODE == 0 ? XG_K2_EPI : 8;
   static constexpr int NUM_THREADS = 128 + 32 * EPI_WARPS;
 };
 constexpr int NDIAG = BM + BN - 1;
@@ -53,9 +56,10 @@ constexpr uint32_t idesc2() {
   return MODE == 0 ? idesc_i8(256, BN, false) : idesc_bf16(256, BN);
 }
 
-template <int EPI_WARPS, int STAGES>
+template <int EPI_WARPS, int STAGES, int NSTAGE_BUF>
 struct __align__(1024) Tail2 {
-  uint32_t stage[EPI_WARPS][2 * 32 * 32];  // two 32x32 chunks per warp, 128B-swizzled
+  // K2: one 32x32 chunk per warp; K4: two (its windows read both)
+  uint32_t stage[EPI_WARPS][NSTAGE_BUF * 32 * 32];  // 128B-swizzled
   uint64_t full[STAGES];
   uint64_t empty[STAGES];
   uint64_t tfull[2];
@@ -110,7 +114,7 @@ __device__ __forceinline__ void epi_bar() {
 template <int MODE>
 constexpr size_t smem2_bytes() {
   return 1024 + Cfg2<MODE>::STAGES * STAGE_BYTES +
-         sizeof(Tail2<Cfg2<MODE>::EPI_WARPS, Cfg2<MODE>::STAGES>);
+         sizeof(Tail2<Cfg2<MODE>::EPI_WARPS, Cfg2<MODE>::STAGES, MODE == 1 ? 2 : 1>);
 }
 size_t gram2_smem_bytes(int mode) { return mode == 0 ? smem2_bytes<0>() : smem2_bytes<1>(); }
 
@@ -120,7 +124,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
             GramParams p) {
   constexpr uint32_t IDESC = idesc2<MODE>();
   constexpr int STAGES = Cfg2<MODE>::STAGES, EPI_WARPS = Cfg2<MODE>::EPI_WARPS;
-  using Tail = Tail2<EPI_WARPS, STAGES>;
+  using Tail = Tail2<EPI_WARPS, STAGES, MODE == 1 ? 2 : 1>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
@@ -376,6 +380,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
         for (int e = lane; e < NDIAG_PAD; e += 32) tail->acc[ew][e] = make_float2(0.f, 0.f);
         epi_bar<EPI_WARPS>();
       }
+      if constexpr (MODE == 1) {
+      // K4: two staging buffers per warp, windows over a precomputed walk
       const uint32_t tbase =
           tmem_base + static_cast<uint32_t>(acc * BN) + (static_cast<uint32_t>(sub * 32) << 16);
       const int out_row = td.ring * p.ld + i0 + 32 * sub;
@@ -505,6 +511,122 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
           }
           __syncwarp();
         }
+      }
+      } else {
+      const uint32_t tbase =
+          tmem_base + static_cast<uint32_t>(acc * BN) + (static_cast<uint32_t>(sub * 32) << 16);
+      const int out_row = td.ring * p.ld + i0 + 32 * sub;
+      // Column chunks c (32 wide) are staged one at a time in this warp's
+      // buffer, stored by TMA and read by the g2 window sums.  Window w
+      // (lane L sums the diagonal elements (l, 32(w-1) + L + 1 + l), l =
+      // 0..31) spans chunks w-1 and w: element (l, kk = (L+1+l) & 31) of chunk
+      // c finishes window c when L+1+l >= 32 and starts window c+1 otherwise.
+      // Both sums advance in ascending l, so every window keeps its
+      // one-pass order with a single staged chunk.  With 8 epilogue warps
+      // group 0 stores chunks 0..3 and also reads chunk 4 (to finish window
+      // 4); group 1 stores 4..7 and owns windows 5..8.
+      const int grp = EPI_WARPS == 8 ? (ew >> 2) : 0;
+      const int c_first = grp ? 4 : 0;
+      const int c_last = EPI_WARPS == 8 ? (grp ? 7 : 4) : 7;
+      const int w_lo = EPI_WARPS == 8 ? (grp ? 5 : 0) : 0;
+      const int w_hi = EPI_WARPS == 8 ? (grp ? 8 : 4) : 8;
+      const bool fp32 = MODE == 1 || dd_ok;  // FP32 (double-float) sums, else FP64
+      float cur_h = 0.f, cur_l = 0.f, nxt_h = 0.f, nxt_l = 0.f;
+      double cur_d = 0.0, nxt_d = 0.0;
+      auto finish = [&](int w, float wh, float wl) {
+        if (w < w_lo || w > w_hi) return;
+        const int lagw = td.j0 - i0 + 32 * (w - 1 - sub) + lane + 1;  // this lane's lag
+        if (MODE == 1) {
+          slots[32 * (w - w_lo) + lane] = lagw >= 0 ? make_float2(wh, wl) : make_float2(0.f, 0.f);
+        } else if (lagw >= 0) {
+          float2* ap = &tail->acc[ew][32 * (w - 1 - sub) + lane + 1 + 127];
+          *ap = dd_add(*ap, wh, wl);
+        }
+      };
+#pragma unroll 1
+      for (int c = c_first; ok && c <= c_last; ++c) {
+        uint32_t r[32];
+        tmem_ld32(tbase + c * 32, r);
+        tmem_ld_wait();
+        // the TMA store of the previous chunk has read the buffer
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          *reinterpret_cast<uint4*>(S + lane * 32 + ((q ^ (lane & 7)) << 2)) =
+              make_uint4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0 && p.store && (EPI_WARPS == 4 || (grp ? c >= 4 : c < 4))) {
+          asm volatile(
+              "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                  reinterpret_cast<uint64_t>(&tmOut)),
+              "r"(smem_u32(S)), "r"(td.j0 + 32 * c), "r"(out_row)
+              : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        if (p.g2_partial) {
+          const int col0 = td.j0 + 32 * c;  // first frame of this chunk's columns
+          const float2* ir2 = tail->inv_row2 + 32 * sub;
+          const float2* ic2 = tail->inv_col2_ext + 32 + 32 * c;  // + kk
+          const double* ir = tail->inv_row + 32 * sub;
+          const double* ic = tail->inv_col_ext + 32 + 32 * c;
+#pragma unroll
+          for (int l = 0; l < 32; ++l) {
+            const int u = lane + 1 + l;
+            const bool fin = u >= 32;  // finishes window c, else starts window c + 1
+            const int kk = u & 31;
+            const uint32_t wv = S[l * 32 + (kk ^ ((l & 7) << 2))];
+            if (MODE == 1) {
+              const float v = col0 + kk < p.n_frames ? __uint_as_float(wv) : 0.f;
+              if (fin) cur_h += v; else nxt_h += v;
+            } else if (fp32) {
+              // exact float G (< 2^23), error-free two-product of the (hi, lo)
+              // weights, TwoSum accumulation
+              const float g = __fsub_rn(__int_as_float(0x4B000000 | static_cast<int>(wv)), 8388608.f);
+              const float2 a = ir2[l], b = ic2[kk];
+              const float ph = __fmul_rn(a.x, b.x);
+              float pe = __fmaf_rn(a.x, b.x, -ph);
+              pe = __fmaf_rn(a.x, b.y, pe);
+              pe = __fmaf_rn(a.y, b.x, pe);
+              const float qh = __fmul_rn(g, ph);
+              const float ql = __fmaf_rn(g, pe, __fmaf_rn(g, ph, -qh));
+              const float sh = fin ? cur_h : nxt_h, sl = fin ? cur_l : nxt_l;
+              const float t = __fadd_rn(sh, qh);  // TwoSum(sh, qh)
+              const float z = __fsub_rn(t, sh);
+              const float er = __fadd_rn(__fsub_rn(sh, __fsub_rn(t, z)), __fsub_rn(qh, z));
+              const float nl = __fadd_rn(sl, __fadd_rn(er, ql));
+              if (fin) { cur_h = t; cur_l = nl; } else { nxt_h = t; nxt_l = nl; }
+            } else {
+              // FP64 path (a frame with |x|^2 >= 2^23 in this series)
+              const double v =
+                  (__hiloint2double(0x43300000, static_cast<int>(wv)) - 4503599627370496.0) *
+                  (ir[l] * ic[kk]);
+              if (fin) cur_d += v; else nxt_d += v;
+            }
+          }
+          if (MODE == 0 && !fp32) {
+            const float wh = static_cast<float>(cur_d);
+            finish(c, wh, static_cast<float>(cur_d - static_cast<double>(wh)));
+          } else {
+            finish(c, cur_h, cur_l);
+          }
+          cur_h = nxt_h;
+          cur_l = nxt_l;
+          cur_d = nxt_d;
+          nxt_h = nxt_l = 0.f;
+          nxt_d = 0.0;
+        }
+        __syncwarp();
+      }
+      if (ok && p.g2_partial) {  // the last window: its second chunk is past the tile
+        if (MODE == 0 && !fp32) {
+          const float wh = static_cast<float>(cur_d);
+          finish(c_last + 1, wh, static_cast<float>(cur_d - static_cast<double>(wh)));
+        } else {
+          finish(c_last + 1, cur_h, cur_l);
+        }
+      }
       }
       if (MODE == 1 && p.g2_partial) {  // this warp's window slots of the tile are written
         __syncwarp();
