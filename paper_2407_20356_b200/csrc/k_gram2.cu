@@ -43,7 +43,7 @@ template <int MODE> struct Cfg2 {
 #ifndef XG_K2_EPI
 #define XG_K2_EPI 8
 #endif
-  static constexpr int STAGES = MODE == 0 ? 5 : 4;
+  static constexpr int STAGES = 5;
   static constexpr int EPI_WARPS = MODE == 0 ? XG_K2_EPI : 8;
   static constexpr int NUM_THREADS = 128 + 32 * EPI_WARPS;
 };
@@ -56,10 +56,9 @@ constexpr uint32_t idesc2() {
   return MODE == 0 ? idesc_i8(256, BN, false) : idesc_bf16(256, BN);
 }
 
-template <int EPI_WARPS, int STAGES, int NSTAGE_BUF>
+template <int EPI_WARPS, int STAGES>
 struct __align__(1024) Tail2 {
-  // K2: one 32x32 chunk per warp; K4: two (its windows read both)
-  uint32_t stage[EPI_WARPS][NSTAGE_BUF * 32 * 32];  // 128B-swizzled
+  uint32_t stage[EPI_WARPS][32 * 32];  // one 32x32 chunk per warp, 128B-swizzled
   uint64_t full[STAGES];
   uint64_t empty[STAGES];
   uint64_t tfull[2];
@@ -114,7 +113,7 @@ __device__ __forceinline__ void epi_bar() {
 template <int MODE>
 constexpr size_t smem2_bytes() {
   return 1024 + Cfg2<MODE>::STAGES * STAGE_BYTES +
-         sizeof(Tail2<Cfg2<MODE>::EPI_WARPS, Cfg2<MODE>::STAGES, MODE == 1 ? 2 : 1>);
+         sizeof(Tail2<Cfg2<MODE>::EPI_WARPS, Cfg2<MODE>::STAGES>);
 }
 size_t gram2_smem_bytes(int mode) { return mode == 0 ? smem2_bytes<0>() : smem2_bytes<1>(); }
 
@@ -124,7 +123,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
             GramParams p) {
   constexpr uint32_t IDESC = idesc2<MODE>();
   constexpr int STAGES = Cfg2<MODE>::STAGES, EPI_WARPS = Cfg2<MODE>::EPI_WARPS;
-  using Tail = Tail2<EPI_WARPS, STAGES, MODE == 1 ? 2 : 1>;
+  using Tail = Tail2<EPI_WARPS, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
@@ -315,15 +314,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
     uint32_t acc_phase = 0;
     bool ok = true;
     uint32_t* S = tail->stage[ew];
-    // K4 window walk: word offset (in the warp's two staging buffers, chunk
-    // c-1 in buffer 0 and chunk c in buffer 1) of this lane's element in row
-    // l; an even chunk c swaps the buffers (offset ^ 1024)
+    // K4 window walk: word offset in the staged (swizzled) chunk of this
+    // lane's element in row l, column (lane + 1 + l) mod 32
     int wtab[MODE == 1 ? 32 : 1];
     if (MODE == 1)
 #pragma unroll
       for (int l = 0; l < 32; ++l) {
         const int u = lane + 1 + l;
-        wtab[l] = (u >> 5) * 1024 + l * 32 + ((u & 31) ^ ((l & 7) << 2));
+        wtab[l] = l * 32 + ((u & 31) ^ ((l & 7) << 2));
       }
     for (int t = pair; t < p.ntiles; t += npairs) {
       const TileDesc td = p.tiles[t];
@@ -380,139 +378,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
         for (int e = lane; e < NDIAG_PAD; e += 32) tail->acc[ew][e] = make_float2(0.f, 0.f);
         epi_bar<EPI_WARPS>();
       }
-      if constexpr (MODE == 1) {
-      // K4: two staging buffers per warp, windows over a precomputed walk
-      const uint32_t tbase =
-          tmem_base + static_cast<uint32_t>(acc * BN) + (static_cast<uint32_t>(sub * 32) << 16);
-      const int out_row = td.ring * p.ld + i0 + 32 * sub;
-      // Column chunks c (32 wide) go through staging buffer c & 1.  Group 0
-      // stores chunks 0..3 and also loads chunk 4 (for window 4); group 1
-      // stores 4..7.  Window w spans chunks w-1 and w (64 columns): lane L
-      // sums the elements (l, 32(w-1) + L + 1 + l), l = 0..31 -- one full
-      // diagonal per lane per window, no wrap, 3 FP64 ops per element.
-      // (with 4 epilogue warps one warp takes chunks 0..7 and windows 0..8)
-      const int grp = EPI_WARPS == 8 ? (ew >> 2) : 0;
-      const int c_first = grp ? 4 : 0;
-      const int c_end = EPI_WARPS == 8 ? (grp ? 9 : 5) : 9;  // chunk 8 = virtual zeros
-#pragma unroll 1
-      for (int c = c_first; ok && c < c_end; ++c) {
-        uint32_t* Sc = S + (c & 1) * 1024;
-        const bool real = c < BN / 32;
-        if (real) {
-          uint32_t r[32];
-          tmem_ld32(tbase + c * 32, r);
-          tmem_ld_wait();
-          // the TMA store issued two chunks ago from this buffer has read it
-          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-          __syncwarp();
-#pragma unroll
-          for (int q = 0; q < 8; ++q)
-            *reinterpret_cast<uint4*>(Sc + lane * 32 + ((q ^ (lane & 7)) << 2)) =
-                make_uint4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
-          fence_proxy_async();
-          __syncwarp();
-          if (lane == 0 && p.store && (EPI_WARPS == 4 || (grp ? c >= 4 : c < 4))) {
-            asm volatile(
-                "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
-                    reinterpret_cast<uint64_t>(&tmOut)),
-                "r"(smem_u32(Sc)), "r"(td.j0 + 32 * c), "r"(out_row)
-                : "memory");
-            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-          }
-        }
-        const int w = c;  // window of chunks c-1, c
-        if (p.g2_partial && !(EPI_WARPS == 8 && grp == 1 && w == 4)) {
-          const int lagw = td.j0 - i0 + 32 * (w - 1 - sub) + lane + 1;  // this lane's lag
-          if (MODE == 1 && lagw < 0) slots[32 * (w - k4_wlo(grp)) + lane] = make_float2(0.f, 0.f);
-          if (lagw >= 0) {
-            const uint32_t* Sp = S + ((c - 1) & 1) * 1024;
-            float wh, wl;  // this window's diagonal sum as (hi, lo)
-            if (MODE == 1 || dd_ok) {
-              // FP32 double-float (~48 bits): exact float G (< 2^23), error-free
-              // two-product of the (hi, lo) weights, TwoSum accumulation; the
-              // B200's FP32 pipe is far wider than its FP64 pipe.
-              const float2* ir2 = tail->inv_row2 + 32 * sub;
-              const float2* ic2 = tail->inv_col2_ext + 32 * (w - 1) + 32 + lane + 1;
-              float sh = 0.f, sl = 0.f;
-              if (MODE == 1 && w >= 1 && real && td.j0 + 32 * w + 32 <= p.n_frames) {
-                // both chunks hold frames only: plain fp32 sum over the
-                // precomputed walk, two interleaved partial sums
-                const int flip = (c & 1) ? 0 : 1024;
-                float s0 = 0.f, s1 = 0.f;
-#pragma unroll
-                for (int l = 0; l < 32; l += 2) {
-                  s0 += __uint_as_float(S[wtab[l] ^ flip]);
-                  s1 += __uint_as_float(S[wtab[l + 1] ^ flip]);
-                }
-                sh = s0 + s1;
-              } else
-#pragma unroll
-              for (int l = 0; l < 32; ++l) {
-                const int cr = lane + 1 + l;  // column within the 64-wide window
-                const int kk = cr & 31;
-                const uint32_t* B = cr < 32 ? Sp : Sc;
-                const bool zero = cr < 32 ? (w == 0) : !real;
-                const uint32_t wv = zero ? 0u : B[l * 32 + (((kk >> 2) ^ (l & 7)) << 2) + (kk & 3)];
-                float qh, ql;
-                if (MODE == 0) {
-                  const float g = __fsub_rn(__int_as_float(0x4B000000 | static_cast<int>(wv)),
-                                            8388608.f);  // exact for wv < 2^23
-                  const float2 a = ir2[l], b = ic2[l];
-                  const float ph = __fmul_rn(a.x, b.x);
-                  float pe = __fmaf_rn(a.x, b.x, -ph);
-                  pe = __fmaf_rn(a.x, b.y, pe);
-                  pe = __fmaf_rn(a.y, b.x, pe);
-                  qh = __fmul_rn(g, ph);
-                  ql = __fmaf_rn(g, pe, __fmaf_rn(g, ph, -qh));
-                } else {
-                  // C~ is fp32 already (~1e-6): a plain fp32 sum of the 32
-                  // window terms adds < 2e-6 relative; columns past the
-                  // last frame are masked
-                  sh += td.j0 + 32 * (w - 1) + cr < p.n_frames ? __uint_as_float(wv) : 0.f;
-                  continue;
-                }
-                const float t = __fadd_rn(sh, qh);  // TwoSum(sh, qh)
-                const float z = __fsub_rn(t, sh);
-                const float er = __fadd_rn(__fsub_rn(sh, __fsub_rn(t, z)), __fsub_rn(qh, z));
-                sh = t;
-                sl = __fadd_rn(sl, __fadd_rn(er, ql));
-              }
-              wh = sh;
-              wl = sl;
-            } else {
-              // FP64 path (a frame with |x|^2 >= 2^23 in this series)
-              const double* ir = tail->inv_row + 32 * sub;
-              const double* ic = tail->inv_col_ext + 32 * (w - 1) + 32 + lane + 1;  // col + 32 pad
-              double r0 = 0.0, r1 = 0.0;
-#pragma unroll 4
-              for (int l = 0; l < 32; ++l) {
-                const int cr = lane + 1 + l;
-                const int kk = cr & 31;
-                const uint32_t* B = cr < 32 ? Sp : Sc;
-                const bool zero = cr < 32 ? (w == 0) : !real;
-                const uint32_t wv = zero ? 0u : B[l * 32 + (((kk >> 2) ^ (l & 7)) << 2) + (kk & 3)];
-                const double v =
-                    (__hiloint2double(0x43300000, static_cast<int>(wv)) - 4503599627370496.0) *
-                    (ir[l] * ic[l]);
-                if (l & 1) r1 += v; else r0 += v;
-              }
-              const double ws = r0 + r1;
-              wh = static_cast<float>(ws);
-              wl = static_cast<float>(ws - static_cast<double>(wh));
-            }
-            // double-float accumulation: the FP64 pipe stalls the tensor-core
-            // pipeline on this part, FP32 does not
-            if (MODE == 1) {
-              slots[32 * (w - k4_wlo(grp)) + lane] = make_float2(wh, wl);
-            } else {
-              float2* ap = &tail->acc[ew][32 * (w - 1 - sub) + lane + 1 + 127];
-              *ap = dd_add(*ap, wh, wl);
-            }
-          }
-          __syncwarp();
-        }
-      }
-      } else {
       const uint32_t tbase =
           tmem_base + static_cast<uint32_t>(acc * BN) + (static_cast<uint32_t>(sub * 32) << 16);
       const int out_row = td.ring * p.ld + i0 + 32 * sub;
@@ -571,6 +436,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
           const float2* ic2 = tail->inv_col2_ext + 32 + 32 * c;  // + kk
           const double* ir = tail->inv_row + 32 * sub;
           const double* ic = tail->inv_col_ext + 32 + 32 * c;
+          if (MODE == 1 && col0 + 32 <= p.n_frames) {
+            // every column is a frame: the precomputed walk, no mask
+#pragma unroll
+            for (int l = 0; l < 32; ++l) {
+              const float v = __uint_as_float(S[wtab[l]]);
+              if (lane + 1 + l >= 32) cur_h += v; else nxt_h += v;
+            }
+          } else
 #pragma unroll
           for (int l = 0; l < 32; ++l) {
             const int u = lane + 1 + l;
@@ -626,7 +499,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
         } else {
           finish(c_last + 1, cur_h, cur_l);
         }
-      }
       }
       if (MODE == 1 && p.g2_partial) {  // this warp's window slots of the tile are written
         __syncwarp();
