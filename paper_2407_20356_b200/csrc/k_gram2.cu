@@ -65,15 +65,17 @@ struct __align__(1024) Tail2 {
   uint64_t tempty[2];
   uint32_t tmem_base;
   uint32_t pad_;
-  double inv_row[BM];
-  double inv_col_ext[BN + 64];
-  float2 inv_row2[BM];            // (hi, lo) float split of the same weights
-  float2 inv_col2_ext[BN + 64];
-  float2 acc[EPI_WARPS][NDIAG_PAD];  // per-diagonal (hi, lo) double-float sums
-  // K4: each epilogue warp's window sums of one tile (2 tiles in flight),
-  // folded by warp 3 (aliases acc: 2 x 8 x 160 <= 8 x 384 float2)
+  // 1/|x| of the tile's rows and columns as (hi, lo) floats, staged by warp 2
+  // one tile ahead (two buffers); the columns reach 32 past either side
+  float2 inv_row2[2][BM];
+  float2 inv_col2_ext[2][BN + 64];
+  // each epilogue warp's window sums of one tile (2 tiles in flight),
+  // folded by warp 3
+  float2 slot[2][EPI_WARPS][160];
   uint64_t accfull[2];
   uint64_t accfree[2];
+  uint64_t invfull[2];
+  uint64_t invfree[2];
 };
 constexpr int WSLOTS = 160;  // 5 windows x 32 diagonals per K4 epilogue warp
 
@@ -150,6 +152,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
       mbar_init(&tail->tempty[a], 2 * EPI_WARPS);  // epilogue warps of both CTAs
       mbar_init(&tail->accfull[a], EPI_WARPS);
       mbar_init(&tail->accfree[a], 1);
+      mbar_init(&tail->invfull[a], 1);
+      mbar_init(&tail->invfree[a], EPI_WARPS);
     }
     fence_barrier_init();
     tma_prefetch(&tmX);
@@ -272,12 +276,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
         }
       }
     }
-  } else if (MODE == 1 && warp == 3) {
-    // K4 g2 fold: sums the 8 epilogue warps' window slots of each tile in a
+  } else if (warp == 2) {
+    // K2 g2 weights: 1/|x| of the next tile's rows and columns staged one
+    // tile ahead, so the epilogue warps never stop to load them
+    if (MODE == 0 && p.g2_partial) {
+      int it = 0;
+      for (int t = pair; t < p.ntiles; t += npairs, ++it) {
+        const int buf = it & 1;
+        if (it >= 2 && !mbar_wait(&tail->invfree[buf], ((it >> 1) - 1) & 1, p.err)) break;
+        const TileDesc td = p.tiles[t];
+        const int i0 = td.i0 + 128 * static_cast<int>(rank);
+        const float2* inv2 = p.inv2 + static_cast<int64_t>(td.ring) * p.inv_ld;
+        for (int e = lane; e < BM + BN + 64; e += 32) {
+          const int j = e - BM - 32;
+          const int idx = e < BM ? i0 + e : td.j0 + j;
+          const bool in = idx < p.n_frames && (e < BM || (j >= 0 && j < BN));
+          const float2 hl = in ? inv2[idx] : make_float2(0.f, 0.f);
+          if (e < BM)
+            tail->inv_row2[buf][e] = hl;
+          else
+            tail->inv_col2_ext[buf][e - BM] = hl;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tail->invfull[buf]);
+      }
+    }
+  } else if (warp == 3) {
+    // g2 fold: sums the 8 epilogue warps' window slots of each tile in a
     // fixed warp order and writes the tile's diagonal sums, so the epilogue
     // warps never meet at a barrier (they run up to 2 tiles ahead).
     if (p.g2_partial) {
-      float2(*acc2)[EPI_WARPS][WSLOTS] = reinterpret_cast<float2(*)[EPI_WARPS][WSLOTS]>(&tail->acc[0][0]);
+      float2(*acc2)[EPI_WARPS][WSLOTS] = tail->slot;
       int it = 0;
       for (int t = pair; t < p.ntiles; t += npairs, ++it) {
         const int buf = it & 1;
@@ -330,54 +359,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
       ok = __all_sync(0xffffffffu, ok);
       if (ok) tc_fence_after();
       const int it = (t - pair) / npairs, buf = it & 1;
-      float2* slots = MODE == 1 ? reinterpret_cast<float2*>(&tail->acc[0][0]) +
-                                      (buf * EPI_WARPS + ew) * WSLOTS
-                                : nullptr;
-      if (MODE == 1 && p.g2_partial && it >= 2)  // warp 3 has folded this buffer's last tile
+      float2* slots = &tail->slot[buf][ew][0];
+      if (p.g2_partial && it >= 2)  // warp 3 has folded this buffer's last tile
         if (!mbar_wait(&tail->accfree[buf], ((it >> 1) - 1) & 1, p.err)) ok = false;
-      if (MODE == 0 && p.g2_partial) {
-        epi_bar<EPI_WARPS>();
-        const double* inv = MODE == 0 ? p.inv + static_cast<int64_t>(td.ring) * p.inv_ld : nullptr;
-        const float2* inv2 = MODE == 0 ? p.inv2 + static_cast<int64_t>(td.ring) * p.inv_ld : nullptr;
-        // inv_col_ext[32 + j] = 1/|x_{j0+j}| for j in [0, 256), zero for the 32
-        // columns either side (the windows reach one chunk past the tile).
-        // The double-float path takes the precomputed (hi, lo) split: no FP64
-        // here (FP64 work in this kernel stalls the tensor-core pipeline).
-        if (MODE == 1 || dd_ok) {
-          for (int e = etid; e < BM + BN + 64; e += 32 * EPI_WARPS) {
-            const int j = e - BM - 32;
-            const int idx = e < BM ? i0 + e : td.j0 + j;
-            const bool in = idx < p.n_frames && (e < BM || (j >= 0 && j < BN));
-            const float2 hl = in ? (MODE == 0 ? inv2[idx] : make_float2(1.f, 0.f))
-                                 : make_float2(0.f, 0.f);
-            if (e < BM)
-              tail->inv_row2[e] = hl;
-            else
-              tail->inv_col2_ext[e - BM] = hl;
-          }
-        } else
-        for (int e = etid; e < BM + BN + 64; e += 32 * EPI_WARPS) {
-          double v;
-          if (e < BM) {
-            const int idx = i0 + e;
-            v = idx < p.n_frames ? (MODE == 0 ? inv[idx] : 1.0) : 0.0;
-            tail->inv_row[e] = v;
-          } else {
-            const int j = e - BM - 32;
-            const int idx = td.j0 + j;
-            v = (j >= 0 && j < BN && idx < p.n_frames) ? (MODE == 0 ? inv[idx] : 1.0) : 0.0;
-            tail->inv_col_ext[e - BM] = v;
-          }
-          const float hi = static_cast<float>(v);
-          const float2 hl = make_float2(hi, static_cast<float>(v - static_cast<double>(hi)));
-          if (e < BM)
-            tail->inv_row2[e] = hl;
-          else
-            tail->inv_col2_ext[e - BM] = hl;
-        }
-        for (int e = lane; e < NDIAG_PAD; e += 32) tail->acc[ew][e] = make_float2(0.f, 0.f);
-        epi_bar<EPI_WARPS>();
-      }
+      if (MODE == 0 && p.g2_partial)  // warp 2 has staged this tile's 1/|x|
+        if (!mbar_wait(&tail->invfull[buf], (it >> 1) & 1, p.err)) ok = false;
       const uint32_t tbase =
           tmem_base + static_cast<uint32_t>(acc * BN) + (static_cast<uint32_t>(sub * 32) << 16);
       const int out_row = td.ring * p.ld + i0 + 32 * sub;
@@ -401,12 +387,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
       auto finish = [&](int w, float wh, float wl) {
         if (w < w_lo || w > w_hi) return;
         const int lagw = td.j0 - i0 + 32 * (w - 1 - sub) + lane + 1;  // this lane's lag
-        if (MODE == 1) {
-          slots[32 * (w - w_lo) + lane] = lagw >= 0 ? make_float2(wh, wl) : make_float2(0.f, 0.f);
-        } else if (lagw >= 0) {
-          float2* ap = &tail->acc[ew][32 * (w - 1 - sub) + lane + 1 + 127];
-          *ap = dd_add(*ap, wh, wl);
-        }
+        slots[32 * (w - w_lo) + lane] = lagw >= 0 ? make_float2(wh, wl) : make_float2(0.f, 0.f);
       };
 #pragma unroll 1
       for (int c = c_first; ok && c <= c_last; ++c) {
@@ -432,10 +413,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
         }
         if (p.g2_partial) {
           const int col0 = td.j0 + 32 * c;  // first frame of this chunk's columns
-          const float2* ir2 = tail->inv_row2 + 32 * sub;
-          const float2* ic2 = tail->inv_col2_ext + 32 + 32 * c;  // + kk
-          const double* ir = tail->inv_row + 32 * sub;
-          const double* ic = tail->inv_col_ext + 32 + 32 * c;
+          const float2* ir2 = tail->inv_row2[buf] + 32 * sub;
+          const float2* ic2 = tail->inv_col2_ext[buf] + 32 + 32 * c;  // + kk
           if (MODE == 1 && col0 + 32 <= p.n_frames) {
             // every column is a frame: the precomputed walk, no mask
 #pragma unroll
@@ -472,9 +451,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
               if (fin) { cur_h = t; cur_l = nl; } else { nxt_h = t; nxt_l = nl; }
             } else {
               // FP64 path (a frame with |x|^2 >= 2^23 in this series)
+              const double ia = static_cast<double>(ir2[l].x) + ir2[l].y;
+              const double ib = static_cast<double>(ic2[kk].x) + ic2[kk].y;
               const double v =
-                  (__hiloint2double(0x43300000, static_cast<int>(wv)) - 4503599627370496.0) *
-                  (ir[l] * ic[kk]);
+                  (__hiloint2double(0x43300000, static_cast<int>(wv)) - 4503599627370496.0) * (ia * ib);
               if (fin) cur_d += v; else nxt_d += v;
             }
           }
@@ -500,9 +480,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
           finish(c_last + 1, cur_h, cur_l);
         }
       }
-      if (MODE == 1 && p.g2_partial) {  // this warp's window slots of the tile are written
+      if (p.g2_partial) {  // this warp's window slots are written, the weights read
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tail->accfull[buf]);
+        if (lane == 0) {
+          mbar_arrive(&tail->accfull[buf]);
+          if (MODE == 0) mbar_arrive(&tail->invfree[buf]);
+        }
       }
       if (ok) {
         tc_fence_before();
@@ -512,21 +495,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
             mbar_arrive(&tail->tempty[acc]);
           else
             arrive_leader(&tail->tempty[acc]);
-        }
-      }
-      if (MODE == 0 && p.g2_partial) {
-        epi_bar<EPI_WARPS>();
-        // the 1-CTA enumeration index of this half tile (ib = 2I + rank); a
-        // second half past the last 128-row block holds only rows >= T
-        if (ok && 2 * (td.i0 / 256) + static_cast<int>(rank) < p.g2_nbi) {
-          const int64_t half = td.pad + static_cast<int64_t>(rank) * (p.g2_nbj - td.i0 / 256);
-          float2* out = p.g2_partial + half * NDIAG_PAD;
-          for (int e = etid; e < NDIAG; e += 32 * EPI_WARPS) {
-            float2 sum = tail->acc[0][e];  // fixed warp order
-#pragma unroll
-            for (int w = 1; w < EPI_WARPS; ++w) sum = dd_add(sum, tail->acc[w][e].x, tail->acc[w][e].y);
-            out[e] = sum;
-          }
         }
       }
       if (++acc == 2) {
