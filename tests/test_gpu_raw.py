@@ -204,3 +204,22 @@ def test_g2_only_mode_equals_stored_mode(ctx, orc):
         assert np.array_equal(ga, gb) and np.array_equal(ca, cb)
     with pytest.raises(xg.ContractError):
         b.ttc(0)
+
+
+def test_bright_frames_take_the_fp64_g2_path(ctx, orc):
+    """|x|^2 >= 2^23 (bright rings): the Gram entries are no longer exact in
+    fp32, so the fused g2 runs its FP64 branch (weights from the staged
+    (hi, lo) split of 1/|x|).  g2 still within 1e-12 of the oracle."""
+    t, m = 300, 4000
+    rng = np.random.default_rng(77)
+    frames = rng.integers(100, 256, size=(t, m), dtype=np.uint8)  # |x|^2 ~ 1e8 > 2^23
+    lay = xg.RingLayout(ctx, m, [np.arange(0, m, 2), np.arange(1, m, 2)])
+    s = xg.FrameSeries(lay, t).load(frames).ttc_raw()
+    for r, idx in enumerate([np.arange(0, m, 2), np.arange(1, m, 2)]):
+        xq = frames[:, idx].astype(np.float64)
+        assert (xq ** 2).sum(1).max() >= 2 ** 23
+        c_ref = orc.ttc_raw(xq)
+        _, g2_ref, cnt_ref = orc.g2_from_ttc(c_ref)
+        _, g2, cnt = s.g2(r)
+        assert np.array_equal(cnt, cnt_ref)
+        assert np.abs(g2 - g2_ref).max() <= 1e-12
