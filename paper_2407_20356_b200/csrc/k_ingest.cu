@@ -8,7 +8,7 @@
 // (hi, lo) float split for the FP32 fused g2) and the zero-frame bookkeeping.
 //
 // HBM-bound (reads M bytes, writes ~M bytes per frame).  A CTA owns one
-// detector band (8192 pixels) and a run of frames.  Warp 8 streams band
+// detector band (16384 pixels) and a run of frames.  Warp 8 streams band
 // bytes into a 4-deep ring of shared-memory buffers with TMA bulk copies
 // (cp.async.bulk + full/empty mbarriers); 512-byte pieces sit at a 528-byte
 // pitch so consecutive detector rows land 4 banks apart.  The band's output
