@@ -30,7 +30,7 @@ namespace xg {
 
 namespace {
 
-constexpr int INGEST_THREADS = 256;
+constexpr int INGEST_THREADS = 32 * INGEST_CONSUMERS;
 constexpr int NBUF = 4;  // frames in flight per CTA
 constexpr int FR = 2;    // frames per consumer pass (divides NBUF)
 static_assert(NBUF % FR == 0, "NBUF must be a multiple of FR");
@@ -75,7 +75,7 @@ __device__ __forceinline__ void red_add_u64(unsigned long long* p, unsigned long
 // pieces, cut on the host), warp 8 produces (one lane issues the TMA bulk
 // copies).  full/empty mbarriers per ring slot let the consumer warps run up
 // to NBUF frames apart.
-constexpr int CONSUMERS = 8;
+constexpr int CONSUMERS = INGEST_CONSUMERS;
 
 __global__ void __launch_bounds__(INGEST_THREADS + 32)
     k_ingest(IngestParams p) {

@@ -396,7 +396,7 @@ int xg_layout_create(xg_ctx* c, int64_t full_pixels, int32_t n_rings,
   std::vector<int32_t> band_word(nb + 1, 0), band_byte(nb + 1, 0);
   std::vector<uint16_t> words, bytes;
   std::vector<Piece> pieces;
-  constexpr int kWarps = 8;
+  constexpr int kWarps = INGEST_CONSUMERS;
   std::vector<int32_t> band_piece((size_t)nb * (kWarps + 1) + 1, 0);
   std::vector<int64_t> cursor(static_cast<size_t>(n_rings), 0);
   for (int32_t r = 0; r < n_rings; ++r) cursor[r] = offsets[r];

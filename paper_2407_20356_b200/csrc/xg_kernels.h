@@ -15,6 +15,10 @@ namespace xg {
 // at a 528-byte pitch (+16 zero bytes that padding entries point to).
 constexpr int INGEST_PIECE = 512;
 constexpr int INGEST_PITCH = 528;
+#ifndef XG_INGEST_CONSUMERS
+#define XG_INGEST_CONSUMERS 8
+#endif
+constexpr int INGEST_CONSUMERS = XG_INGEST_CONSUMERS;  // consumer warps per K1 CTA
 __host__ __device__ constexpr int ingest_band_stride(int band) {
   return ((band + INGEST_PIECE - 1) / INGEST_PIECE) * INGEST_PITCH + 16;
 }
