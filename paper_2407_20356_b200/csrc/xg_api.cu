@@ -1028,7 +1028,10 @@ int xg_series_rel_error(xg_series* s, double* out) {
   double2* part = nullptr;
   double* d_out = nullptr;
   XG_CUDA(c, cudaMalloc(&part, (size_t)L->rings * REL_BLOCKS * sizeof(double2)));
-  XG_CUDA(c, cudaMalloc(&d_out, (size_t)L->rings * 8));
+  if (cudaError_t e0 = cudaMalloc(&d_out, (size_t)L->rings * 8); e0 != cudaSuccess) {
+    cudaFree(part);
+    return cuda_fail(c, e0, "rel_error");
+  }
   RelErrParams p;
   p.gram = s->d_gram;
   p.cgram = s->d_cgram;
@@ -1877,7 +1880,10 @@ int xg_series_ttc_background(xg_series* s, int32_t which, int64_t exclusion, dou
   double2* part = nullptr;
   double* d_buf = nullptr;
   XG_CUDA(c, cudaMalloc(&part, (size_t)L->rings * BG_BLOCKS * sizeof(double2)));
-  XG_CUDA(c, cudaMalloc(&d_buf, (size_t)L->rings * 8 * 3));
+  if (cudaError_t e0 = cudaMalloc(&d_buf, (size_t)L->rings * 8 * 3); e0 != cudaSuccess) {
+    cudaFree(part);
+    return cuda_fail(c, e0, "ttc_background");
+  }
   BgParams p;
   p.gram = which == 0 ? s->d_gram : nullptr;
   p.cgram = which == 0 ? nullptr : s->d_cgram;
