@@ -185,6 +185,13 @@ XG_API int xg_io_write_xfsr_u8(const char* path, const uint8_t* frames, int64_t 
                                double frame_period);
 XG_API int xg_io_read_xfsr_u8(const char* path, uint8_t* out, int64_t out_cap, int64_t* n,
                               int64_t* m, double* frame_period);
+/* XENC encoder file (io.cpp:273-321): a device-built basis (V per ring,
+ * mask order) saved for / read from the reference.  read: v == null returns
+ * the header only (mode, m, k, spectrum_len). */
+XG_API int xg_io_write_xenc(const char* path, int32_t mode, int64_t m, int64_t k,
+                            const double* spectrum, int64_t spectrum_len, const double* v);
+XG_API int xg_io_read_xenc(const char* path, int32_t* mode, int64_t* m, int64_t* k,
+                           int64_t* spectrum_len, double* spectrum, double* v);
 XG_API int xg_series_ttc_background(xg_series* s, int32_t which, int64_t exclusion,
                                     double* out_per_ring);
 XG_API int xg_series_fit_kww(xg_series* s, int32_t which, double frame_period, double min_lag,

@@ -240,6 +240,8 @@ class _RefOracle:
         L.ref_read_compressed.argtypes = [C_.c_char_p, _i64, C_.POINTER(U64), _i64, _d, _d]
         L.ref_write_frames.argtypes = [C_.c_char_p, _d, I64, I64, C_.c_double, C_.c_int]
         L.ref_read_frames_status.argtypes = [C_.c_char_p, _i64, _i64]
+        L.ref_write_encoder.argtypes = [C_.c_char_p, _d, I64, I64, _d, I64, C_.c_int]
+        L.ref_read_encoder.argtypes = [C_.c_char_p, _i64, _i64, _i64, C_.POINTER(C_.c_int), _d, _d]
         L.ref_fit_kww.argtypes = [_d, _d, I64, C_.c_double, C_.c_double, _d]
         L.ref_ttc_rel_error.argtypes = [_d, _d, I64, _d]
         L.ref_compress_series.argtypes = [_d, I64, I64, _d, I64, _d, _d]
@@ -315,6 +317,23 @@ class _RefOracle:
         x = _f64(x)
         self._chk(self.L.ref_write_frames(str(path).encode(), _p(x, _d), x.shape[0], x.shape[1],
                                           period, dtype))
+
+    def write_encoder(self, path, v, spectrum, mode):
+        v, sp = _f64(v), _f64(spectrum)
+        self._chk(self.L.ref_write_encoder(str(path).encode(), _p(v, _d), v.shape[0], v.shape[1],
+                                           _p(sp, _d), sp.size, mode))
+
+    def read_encoder(self, path):
+        """io::read_encoder -> (V, spectrum, mode); raises OracleError(7) on FormatError."""
+        m, k, sl, md = I64(0), I64(0), I64(0), C_.c_int(0)
+        p = str(path).encode()
+        self._chk(self.L.ref_read_encoder(p, C_.byref(m), C_.byref(k), C_.byref(sl), C_.byref(md),
+                                          None, None))
+        v = np.empty((m.value, k.value))
+        sp = np.empty(sl.value)
+        self._chk(self.L.ref_read_encoder(p, C_.byref(m), C_.byref(k), C_.byref(sl), C_.byref(md),
+                                          _p(v, _d), _p(sp, _d)))
+        return v, sp, md.value
 
     def read_frames_status(self, path):
         """(status, payload): 0 ok, 7 FormatError (payload = byte offset)."""

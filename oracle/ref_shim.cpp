@@ -225,6 +225,33 @@ int ref_read_compressed(const char* path, int64_t* k, uint64_t* hash, int64_t* n
   }
 }
 
+// io::write_encoder / read_encoder (io.cpp:273-321).
+int ref_write_encoder(const char* path, const double* v, int64_t m, int64_t k, const double* spec,
+                      int64_t sl, int mode) {
+  return guarded([&] {
+    io::write_encoder(path, EncodingMatrix(to_matrix(v, m, k), std::vector<double>(spec, spec + sl),
+                                           static_cast<EncoderMode>(mode)));
+  });
+}
+int ref_read_encoder(const char* path, int64_t* m, int64_t* k, int64_t* sl, int* mode, double* v,
+                     double* spec) {
+  try {
+    EncodingMatrix e = io::read_encoder(path);
+    *m = static_cast<int64_t>(e.n_pixels());
+    *k = static_cast<int64_t>(e.k());
+    *sl = static_cast<int64_t>(e.spectrum().size());
+    *mode = static_cast<int>(e.mode());
+    if (v) std::memcpy(v, e.v().data().data(), e.v().data().size() * 8);
+    if (spec) std::memcpy(spec, e.spectrum().data(), e.spectrum().size() * 8);
+    return 0;
+  } catch (const FormatError& ex) {
+    g_payload = static_cast<int64_t>(ex.offset());
+    return 7;
+  } catch (const Error&) {
+    return 99;
+  }
+}
+
 // io::write_frames (io.cpp:150-184) with dtype 0 u16, 1 f32, 2 f64.
 int ref_write_frames(const char* path, const double* x, int64_t n, int64_t m, double period,
                      int dtype) {

@@ -147,6 +147,36 @@ def read_xfsr(path):
     return out, per.value
 
 
+def content_hash(v, mode: int = 1) -> int:
+    """content_hash_u64 (model.cpp:99-114) of a basis V (m x k) and mode: the
+    encoder id an XCMP store is bound to."""
+    vv = np.ascontiguousarray(v, dtype=np.float64)
+    return int(lib.xg_content_hash(vv.ctypes.data_as(_abi.PD), vv.shape[0], vv.shape[1], int(mode)))
+
+
+def write_xenc(path, v, spectrum, mode: int = 1) -> None:
+    """XENC encoder file of one ring's basis (io.cpp:273-285): V (m x k, mask
+    order), its spectrum, mode 0 offline / 1 online-related / 2 unrelated."""
+    vv = np.ascontiguousarray(v, dtype=np.float64)
+    sp = np.ascontiguousarray(spectrum, dtype=np.float64)
+    if vv.ndim != 2 or sp.ndim != 1 or sp.size < vv.shape[1]:
+        raise ShapeError("V must be m x k with at least k spectrum values")
+    _io_check(lib.xg_io_write_xenc(str(path).encode(), int(mode), vv.shape[0], vv.shape[1],
+                                   sp.ctypes.data_as(_abi.PD), sp.size, vv.ctypes.data_as(_abi.PD)))
+
+
+def read_xenc(path):
+    """An XENC encoder file -> (V m x k, spectrum, mode) (io.cpp:287-321)."""
+    mode, m, k, sl = C.c_int32(0), C.c_int64(0), C.c_int64(0), C.c_int64(0)
+    p = str(path).encode()
+    _io_check(lib.xg_io_read_xenc(p, C.byref(mode), C.byref(m), C.byref(k), C.byref(sl), None, None))
+    v = np.empty((m.value, k.value))
+    sp = np.empty(sl.value)
+    _io_check(lib.xg_io_read_xenc(p, C.byref(mode), C.byref(m), C.byref(k), C.byref(sl),
+                                  sp.ctypes.data_as(_abi.PD), v.ctypes.data_as(_abi.PD)))
+    return v, sp, int(mode.value)
+
+
 def read_xttc(path) -> np.ndarray:
     """An XTTC tile file (FrameSeries.write_ttc) as the full symmetric matrix."""
     raw = open(path, "rb").read()
@@ -585,7 +615,7 @@ class FrameSeries:
 
 __all__ = [
     "Context", "RingLayout", "FrameSeries", "FrameStream", "Basis", "write_xfsr", "read_xfsr",
-    "write_xcmp", "read_xttc", "Error", "ShapeError", "ContractError", "MaskError",
+    "write_xcmp", "read_xttc", "write_xenc", "read_xenc", "content_hash", "Error", "ShapeError", "ContractError", "MaskError",
     "NormalizationError", "RankError", "BindingError", "FormatError", "DeviceError",
 ]
 

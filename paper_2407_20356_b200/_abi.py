@@ -61,6 +61,8 @@ _sigs = {
     "xg_io_write_xcmp": (C.c_int, [C.c_char_p, I64, C.c_uint64, I64, PD, PD, I32]),
     "xg_io_write_xfsr_u8": (C.c_int, [C.c_char_p, P, I64, I64, C.c_double]),
     "xg_io_read_xfsr_u8": (C.c_int, [C.c_char_p, P, I64, PI64, PI64, PD]),
+    "xg_io_write_xenc": (C.c_int, [C.c_char_p, I32, I64, I64, PD, I64, PD]),
+    "xg_io_read_xenc": (C.c_int, [C.c_char_p, C.POINTER(I32), PI64, PI64, PI64, PD, PD]),
     "xg_series_ttc_background": (C.c_int, [P, I32, I64, PD]),
     "xg_series_fit_kww": (C.c_int, [P, I32, C.c_double, C.c_double, C.c_double, PD, C.POINTER(I32)]),
     "xg_series_build_basis": (C.c_int, [P, I32, C.POINTER(PD), PD, I64, PI64, P]),

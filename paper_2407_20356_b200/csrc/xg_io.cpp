@@ -265,4 +265,74 @@ XG_API int xg_io_read_xfsr_u8(const char* path, uint8_t* out, int64_t out_cap, i
   return XG_OK;
 }
 
+// XENC encoder (io.cpp:273-321): "XENC", u32 1, u8 mode, u64 M, u64 K, u64
+// spectrum length, spectrum f64, M*K f64 row-major.  A device-built basis
+// saved for the reference (or read back); the content hash that binds an
+// XCMP store is xg_content_hash over the same V and mode.
+XG_API int xg_io_write_xenc(const char* path, int32_t mode, int64_t m, int64_t k,
+                            const double* spectrum, int64_t spectrum_len, const double* v) {
+  if (!path || !v || !spectrum || m < 1 || k < 1 || spectrum_len < k) return XG_ERR_INVALID;
+  if (mode < 0 || mode > 2) return io_fail(XG_ERR_CONTRACT, -1, "unknown encoder mode %d", mode);
+  File fh;
+  fh.f = fopen(path, "wb");
+  if (!fh.f) return io_fail(XG_ERR_FORMAT, -1, "cannot create encoder file %s", path);
+  std::vector<uint8_t> b;
+  b.insert(b.end(), {'X', 'E', 'N', 'C'});
+  put_u32(b, 1);
+  b.push_back(static_cast<uint8_t>(mode));
+  put_u64(b, static_cast<uint64_t>(m));
+  put_u64(b, static_cast<uint64_t>(k));
+  put_u64(b, static_cast<uint64_t>(spectrum_len));
+  for (int64_t i = 0; i < spectrum_len; ++i) put_f64(b, spectrum[i]);
+  for (int64_t i = 0; i < m * k; ++i) {
+    put_f64(b, v[i]);
+    if (b.size() >= (8u << 20) || i + 1 == m * k) {
+      if (fwrite(b.data(), 1, b.size(), fh.f) != b.size())
+        return io_fail(XG_ERR_FORMAT, -1, "failed writing encoder file %s", path);
+      b.clear();
+    }
+  }
+  if (fclose(fh.f) != 0) {
+    fh.f = nullptr;
+    return io_fail(XG_ERR_FORMAT, -1, "failed writing encoder file %s", path);
+  }
+  fh.f = nullptr;
+  return XG_OK;
+}
+
+// Two calls: v == null returns mode, M, K and the spectrum length; then v
+// (M*K) and spectrum (spectrum_len) receive the payload.  read_encoder's
+// layout checks; the orthonormality check is the caller's (Basis.set_ring /
+// the tests), as EncodingMatrix's constructor is in the reference.
+XG_API int xg_io_read_xenc(const char* path, int32_t* mode, int64_t* m, int64_t* k,
+                           int64_t* spectrum_len, double* spectrum, double* v) {
+  if (!path || !mode || !m || !k || !spectrum_len) return XG_ERR_INVALID;
+  std::vector<uint8_t> b;
+  if (!read_all(path, b)) return io_fail(XG_ERR_FORMAT, -1, "cannot open encoder file %s", path);
+  if (b.size() < 4 || std::memcmp(b.data(), "XENC", 4) != 0)
+    return io_fail(XG_ERR_FORMAT, 0, "bad magic, expected \"XENC\" for encoder");
+  if (b.size() < 33) return io_fail(XG_ERR_FORMAT, (int64_t)b.size(), "encoder file truncated");
+  if (get_u32(b.data() + 4) != 1)
+    return io_fail(XG_ERR_FORMAT, 4, "unsupported encoder version %u", get_u32(b.data() + 4));
+  if (b[8] > 2) return io_fail(XG_ERR_FORMAT, 8, "unknown encoder mode %u", b[8]);
+  const uint64_t mm = get_u64(b.data() + 9), kk = get_u64(b.data() + 17),
+                 sl = get_u64(b.data() + 25);
+  if (mm < 1 || kk < 1 || kk > mm || sl < kk || sl > (1ull << 40) || mm > (1ull << 40) / kk)
+    return io_fail(XG_ERR_FORMAT, 9, "implausible encoder dimensions");
+  const uint64_t want = 33 + 8 * sl + 8 * mm * kk;
+  if (b.size() != want)
+    return io_fail(XG_ERR_FORMAT, (int64_t)std::min<uint64_t>(b.size(), want),
+                   "encoder file length %zu, expected %llu", b.size(), (unsigned long long)want);
+  *mode = b[8];
+  *m = static_cast<int64_t>(mm);
+  *k = static_cast<int64_t>(kk);
+  *spectrum_len = static_cast<int64_t>(sl);
+  if (!v) return XG_OK;
+  if (spectrum)
+    for (uint64_t i = 0; i < sl; ++i) spectrum[i] = get_f64(b.data() + 33 + 8 * i);
+  const uint8_t* pv = b.data() + 33 + 8 * sl;
+  for (uint64_t i = 0; i < mm * kk; ++i) v[i] = get_f64(pv + 8 * i);
+  return XG_OK;
+}
+
 }  // extern "C"

@@ -84,3 +84,17 @@ def test_ttc_tile_sink_round_trip(ctx, orc, tmp_path):
     assert (tmp_path / "g.xttc").stat().st_size == 20 + 300 * 301 // 2 * 4
     with pytest.raises(xg.ContractError):
         s.write_ttc(0, tmp_path / "x.xttc", "f32")  # raw TTC has no f32 sink
+
+
+def test_device_basis_saved_as_xenc_for_the_reference(ctx, orc, ref, tmp_path):
+    """A basis built on the device, written as XENC, loads in the reference
+    (its EncodingMatrix checks orthonormality to 1e-10) and binds stores by
+    the same content hash."""
+    frames, ring, lay = _setup(ctx, orc, 80, 32, 32, 2, 0.6, 85)
+    vs, sig, rank = xg.FrameSeries(lay, 80).load(frames).build_basis(12)
+    for r in range(2):
+        p = tmp_path / f"r{r}.xenc"
+        xg.write_xenc(p, vs[r], sig[r], mode=1)
+        v, spec, mode = ref.read_encoder(p)
+        assert mode == 1 and np.array_equal(v, vs[r]) and np.array_equal(spec, sig[r])
+        assert xg.content_hash(vs[r], 1) == ref.content_hash(vs[r], 1)

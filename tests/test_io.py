@@ -82,3 +82,27 @@ def test_xfsr_u8_round_trip_and_checks(tmp_path, ref):
     ref.write_frames(f, np.full((2, 3), 1.5), 1.0, 2)
     with pytest.raises(xg.ContractError):
         xg.read_xfsr(f)
+
+
+def test_xenc_round_trips_with_reference(tmp_path, ref, orc):
+    """XENC (io.cpp:273-321): our writer is read by the reference (which
+    checks orthonormality and spectrum order on load), the reference's
+    writer is read by ours, bitwise; layout errors are FormatError with the
+    byte offset."""
+    x = orc.random_positive_matrix(20, 300, 4)
+    v, spec = ref.build_online_from_frames(x, 6)
+    p = tmp_path / "a.xenc"
+    xg.write_xenc(p, v, spec, mode=1)
+    v2, s2, md = ref.read_encoder(p)
+    assert md == 1 and np.array_equal(v2, v) and np.array_equal(s2, spec)
+    assert p.stat().st_size == 33 + 8 * spec.size + 8 * v.size
+    q = tmp_path / "b.xenc"
+    ref.write_encoder(q, v, spec, 0)
+    v3, s3, md3 = xg.read_xenc(q)
+    assert md3 == 0 and np.array_equal(v3, v) and np.array_equal(s3, spec)
+    assert q.read_bytes() == p.read_bytes()[:8] + bytes([0]) + p.read_bytes()[9:]
+    raw = p.read_bytes()
+    (tmp_path / "cut.xenc").write_bytes(raw[:-8])
+    with pytest.raises(xg.FormatError) as e:
+        xg.read_xenc(tmp_path / "cut.xenc")
+    assert e.value.offset == len(raw) - 8
