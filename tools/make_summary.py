@@ -20,7 +20,8 @@ def main():
     rnd = sys.argv[1] if len(sys.argv) > 1 else "r1"
     lines = [f"# {rnd} launch list: ncu --metrics gpu__time_duration.sum --clock-control none "
              "(cold, serialised; compare SHARES)",
-             "# command: python bench.py --steps 3 --warmup 3 --no-cpu-baseline",
+             "# command: python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-stream "
+             "(tools/capture_profiles.sh)",
              run("tools/launches.py", os.path.join(PROF, f"{rnd}_launches.csv")).rstrip(), ""]
     for name in ("ingest", "gram_raw", "project", "gram_cmp", "stream_dense", "stream_sparse",
                  "stream_cmp"):
