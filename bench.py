@@ -392,6 +392,7 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--no-compressed", action="store_true")
     ap.add_argument("--no-stream", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--stream-depth", type=int, default=8192)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -484,32 +485,35 @@ def main():
     value = world * T / (ms / 1e3)  # frames of all partitions / max-over-ranks time
 
     # ---------------------------------------------------------- end to end
-    host = torch.empty((T, P), dtype=torch.uint8, pin_memory=True)
-    host.copy_(frames)
-    g2_out = np.empty(T)
+    if args.no_e2e:  # profiling runs only (tools/capture_profiles.sh launch list)
+        e2e = {"skipped": "--no-e2e (profiling run)"}
+    else:
+        host = torch.empty((T, P), dtype=torch.uint8, pin_memory=True)
+        host.copy_(frames)
+        g2_out = np.empty(T)
 
-    def step_e2e():
-        # pinned H2D in chunks, overlapped with ingest + Gram (one public call)
-        series.ttc_raw_host(host)
-        series.g2_all()  # D2H of every ring's g2 values + counts
+        def step_e2e():
+            # pinned H2D in chunks, overlapped with ingest + Gram (one public call)
+            series.ttc_raw_host(host)
+            series.g2_all()  # D2H of every ring's g2 values + counts
 
-    for _ in range(2):
-        step_e2e()
-    barrier()
-    torch.cuda.synchronize()
-    e2e_steps = max(3, min(args.steps, 10))
-    tw0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        step_e2e()
-    torch.cuda.synchronize()
-    e2e_s = (time.perf_counter() - tw0) / e2e_steps
-    if world > 1:
-        tt = torch.tensor([e2e_s], device=dev)
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        e2e_s = float(tt[0])
-    e2e = {"value": world * T / e2e_s, "unit": "frames/s", "h2d_bytes_per_step": T * P,
-           "d2h_bytes_per_step": len(mine) * T * 16, "ms_per_step": e2e_s * 1e3,
-           "timing": "host wall clock around synchronous API calls"}
+        for _ in range(2):
+            step_e2e()
+        barrier()
+        torch.cuda.synchronize()
+        e2e_steps = max(3, min(args.steps, 10))
+        tw0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            step_e2e()
+        torch.cuda.synchronize()
+        e2e_s = (time.perf_counter() - tw0) / e2e_steps
+        if world > 1:
+            tt = torch.tensor([e2e_s], device=dev)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            e2e_s = float(tt[0])
+        e2e = {"value": world * T / e2e_s, "unit": "frames/s", "h2d_bytes_per_step": T * P,
+               "d2h_bytes_per_step": len(mine) * T * 16, "ms_per_step": e2e_s * 1e3,
+               "timing": "host wall clock around synchronous API calls"}
 
     # ---------------------------------------------------------- roofline
     peak, peak_src = measure_int8_peak(torch, dev)

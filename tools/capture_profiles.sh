@@ -12,7 +12,8 @@ python tools/time_gram.py > $O/time_gram.log 2>&1 || exit 1
 python tools/time_cmp.py > $O/time_cmp.log 2>&1 || exit 1
 DEPTH=8192 K=128 python tools/time_stream.py > $O/time_stream.log 2>&1 || exit 1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/${R}_launches.csv \
-    python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-stream > /dev/null 2>&1
+    python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-stream --no-compressed --no-e2e \
+    > /dev/null 2>&1
 $NCU -k regex:"k_ingest" -s 2 -c 1 -o $O/${R}_ingest python tools/time_gram.py > /dev/null 2>&1
 $NCU -k regex:"k_gram2" -c 1 -o $O/${R}_gram_raw python tools/time_gram.py > /dev/null 2>&1
 $NCU -k regex:"k_project" -c 1 -o $O/${R}_project python tools/time_cmp.py > /dev/null 2>&1

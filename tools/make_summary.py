@@ -21,7 +21,7 @@ def main():
     lines = [f"# {rnd} launch list: ncu --metrics gpu__time_duration.sum --clock-control none "
              "(cold, serialised; compare SHARES)",
              "# command: python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-stream "
-             "(tools/capture_profiles.sh)",
+             "--no-compressed --no-e2e (tools/capture_profiles.sh): the device-resident raw step",
              run("tools/launches.py", os.path.join(PROF, f"{rnd}_launches.csv")).rstrip(), ""]
     for name in ("ingest", "gram_raw", "project", "gram_cmp", "stream_dense", "stream_sparse",
                  "stream_cmp"):
