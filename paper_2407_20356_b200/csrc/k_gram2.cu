@@ -404,11 +404,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
         fence_proxy_async();
         __syncwarp();
         if (lane == 0 && p.store && (EPI_WARPS == 4 || (grp ? c >= 4 : c < 4))) {
+          // the TTC streams out once: evict-first in L2, so it does not push
+          // the ring's frame rows (re-read by later tiles) out of L2
+          uint64_t pol;
+          asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
           asm volatile(
-              "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+              "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3}], [%1], %4;" ::"l"(
                   reinterpret_cast<uint64_t>(&tmOut)),
-              "r"(smem_u32(S)), "r"(td.j0 + 32 * c), "r"(out_row)
+              "r"(smem_u32(S)), "r"(td.j0 + 32 * c), "r"(out_row), "l"(pol)
               : "memory");
+
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
         if (p.g2_partial) {
