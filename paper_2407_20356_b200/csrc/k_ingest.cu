@@ -151,19 +151,20 @@ __global__ void __launch_bounds__(INGEST_THREADS + 32)
       uint8_t* dst = bufs + slot * bstride;
       const uint8_t* src = p.raster + (f_begin + i) * p.pixels + pix0;
       if (bulk) {
-        if (lane == 0) {
+        if (lane == 0)
           asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
                            smem_addr(&full[slot])),
                        "r"(blen)
                        : "memory");
-          for (int o = 0; o < blen; o += PIECE) {
-            const int len = blen - o < PIECE ? blen - o : PIECE;
-            asm volatile(
-                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], "
-                "%2, [%3];" ::"r"(smem_addr(dst + (o / PIECE) * PITCH)),
-                "l"(src + o), "r"(len), "r"(smem_addr(&full[slot]))
-                : "memory");
-          }
+        __syncwarp();
+        // one piece per lane: the band's bulk copies are issued in parallel
+        for (int o = lane * PIECE; o < blen; o += 32 * PIECE) {
+          const int len = blen - o < PIECE ? blen - o : PIECE;
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], "
+              "%2, [%3];" ::"r"(smem_addr(dst + (o / PIECE) * PITCH)),
+              "l"(src + o), "r"(len), "r"(smem_addr(&full[slot]))
+              : "memory");
         }
       } else {
         for (int k = lane; k < blen; k += 32) dst[ingest_smem_offset(k)] = src[k];
