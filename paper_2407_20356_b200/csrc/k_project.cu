@@ -31,6 +31,10 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 128;
+#ifndef XG_K3_KPS
+#define XG_K3_KPS 2
+#endif
+constexpr int KPS = XG_K3_KPS;  // 128-byte K blocks per pipeline stage (one wait/commit each)
 constexpr int MAX_STAGES = 6;
 constexpr int A_BYTES = BM * BK;    // 16 KB
 constexpr int TMEM_COLS = 512;
@@ -56,7 +60,7 @@ struct __align__(8) ProjTail {
 
 // per CTA: its 128 frame rows + half of the digit rows (the pair's MMA
 // reads the other half from the peer CTA)
-__host__ __device__ inline int proj_stage_bytes(int nt_rows) { return A_BYTES + nt_rows / 2 * BK; }
+__host__ __device__ inline int proj_stage_bytes(int nt_rows) { return KPS * (A_BYTES + nt_rows / 2 * BK); }
 __host__ __device__ inline int proj_stages(int nt_rows) {
   const int fixed = 1024 + 4 * static_cast<int>(sizeof(EpiStage)) + static_cast<int>(sizeof(ProjTail));
   const int st = (SMEM_LIMIT - fixed) / proj_stage_bytes(nt_rows);
@@ -93,16 +97,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   const int half_rows = nt_rows / 2;                   // digit rows staged by this CTA
   const int STAGES = proj_stages(nt_rows);
   const int B_BYTES = half_rows * BK;                  // multiple of 1 KB
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + STAGES * A_BYTES;
-  EpiStage* epi = reinterpret_cast<EpiStage*>(sB + STAGES * B_BYTES);
+  uint8_t* sA = smem;                                   // [stage][KPS] A sub-tiles
+  uint8_t* sB = smem + STAGES * KPS * A_BYTES;          // [stage][KPS] B sub-tiles
+  EpiStage* epi = reinterpret_cast<EpiStage*>(sB + STAGES * KPS * B_BYTES);
   ProjTail* tail = reinterpret_cast<ProjTail*>(epi + 4);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cta_rank();
   const bool leader = rank == 0;
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
   const uint32_t idesc = idesc_i8(2 * BM, static_cast<uint32_t>(nt_rows), true);
-  const uint32_t stage_tx = 2 * (A_BYTES + B_BYTES);  // both CTAs' bytes, on the leader
+  const uint32_t sub_tx = 2 * (A_BYTES + B_BYTES);  // both CTAs' bytes of one K block
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -137,13 +141,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         const TileDesc td = p.tiles[t];
         const int koff = p.ring_koff[td.ring], nkb = p.ring_nkb[td.ring];
         const int vrow = td.j0 * nt_rows + static_cast<int>(rank) * half_rows;
-        for (int kb = 0; kb < nkb; ++kb) {
+        for (int kb = 0; kb < nkb; kb += KPS) {
           if (!mbar_wait(&tail->empty[stage], phase ^ 1, p.err)) goto done;
-          if (leader) mbar_arrive_expect_tx(&tail->full[stage], stage_tx);
-          const int kc = koff + kb * BK;
-          tma_load_2sm(sA + stage * A_BYTES, &tmX, &tail->full[stage], kc,
-                       td.i0 + BM * static_cast<int>(rank));
-          tma_load_2sm(sB + stage * B_BYTES, &tmV, &tail->full[stage], kc, vrow);
+          const int nsub = nkb - kb < KPS ? nkb - kb : KPS;
+          if (leader) mbar_arrive_expect_tx(&tail->full[stage], nsub * sub_tx);
+          for (int sub = 0; sub < nsub; ++sub) {
+            const int kc = koff + (kb + sub) * BK;
+            tma_load_2sm(sA + (stage * KPS + sub) * A_BYTES, &tmX, &tail->full[stage], kc,
+                         td.i0 + BM * static_cast<int>(rank));
+            tma_load_2sm(sB + (stage * KPS + sub) * B_BYTES, &tmV, &tail->full[stage], kc, vrow);
+          }
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -163,17 +170,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + static_cast<uint32_t>(acc * 256);
         bool ok = true;
-        for (int kb = 0; kb < nkb; ++kb) {
+        for (int kb = 0; kb < nkb; kb += KPS) {
           if (!mbar_wait(&tail->full[stage], phase, p.err)) {
             ok = false;
             break;
           }
           tc_fence_after();
-          const uint32_t a0 = smem_u32(sA + stage * A_BYTES), b0 = smem_u32(sB + stage * B_BYTES);
+          const int nsub = nkb - kb < KPS ? nkb - kb : KPS;
+          for (int sub = 0; sub < nsub; ++sub) {
+            const uint32_t a0 = smem_u32(sA + (stage * KPS + sub) * A_BYTES);
+            const uint32_t b0 = smem_u32(sB + (stage * KPS + sub) * B_BYTES);
 #pragma unroll
-          for (int k = 0; k < BK / 32; ++k)
-            mma2_i8(tmem_d, sdesc_k128(a0 + k * 32), sdesc_k128(b0 + k * 32), idesc,
-                    (kb | k) != 0 ? 1u : 0u);
+            for (int k = 0; k < BK / 32; ++k)
+              mma2_i8(tmem_d, sdesc_k128(a0 + k * 32), sdesc_k128(b0 + k * 32), idesc,
+                      (kb | sub | k) != 0 ? 1u : 0u);
+          }
           commit2(&tail->empty[stage]);
           if (++stage == STAGES) {
             stage = 0;
