@@ -383,6 +383,10 @@ constexpr int SS_CHUNK = 1024;
 constexpr int SS_V = XG_SS_V;  // history frames per lane (one 8- or 16-byte load)
 constexpr int SS_U = XG_SS_U;  // loads in flight per lane
 constexpr int SS_F = 32 * SS_V;  // history frames per CTA
+#ifndef XG_SS_W
+#define XG_SS_W 8
+#endif
+constexpr int SS_W = XG_SS_W;  // warps per CTA, splitting the ring's nonzeros
 template <int V> struct SsVec;
 template <> struct SsVec<8> {
   using T = uint2;
@@ -394,11 +398,11 @@ template <> struct SsVec<16> {
   __device__ static void words(const T& v, uint32_t* w) { w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w; }
   __device__ static T zero() { return make_uint4(0u, 0u, 0u, 0u); }
 };
-__global__ void __launch_bounds__(256) k_stream_sparse(StreamParams p) {
+__global__ void __launch_bounds__(32 * SS_W) k_stream_sparse(StreamParams p) {
   using VT = typename SsVec<SS_V>::T;
   __shared__ int32_t sc[SS_CHUNK];
   __shared__ uint32_t sv[SS_CHUNK];
-  __shared__ uint32_t red[8][SS_F + 1];
+  __shared__ uint32_t red[SS_W][SS_F + 1];
   const int r = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int koff = p.ring_koff[r];
@@ -412,19 +416,19 @@ __global__ void __launch_bounds__(256) k_stream_sparse(StreamParams p) {
   for (int c0 = 0; c0 < n; c0 += SS_CHUNK) {
     const int cn = n - c0 < SS_CHUNK ? n - c0 : SS_CHUNK;
     __syncthreads();
-    for (int i = threadIdx.x; i < cn; i += 256) {
+    for (int i = threadIdx.x; i < cn; i += 32 * SS_W) {
       sc[i] = p.nz_col[koff + c0 + i];
       sv[i] = p.nz_val[koff + c0 + i];
     }
     __syncthreads();
     if (s0 <= p.t) {
       // SS_U independent loads in flight per lane before any use
-      for (int i0 = warp; i0 < cn; i0 += 8 * SS_U) {
+      for (int i0 = warp; i0 < cn; i0 += SS_W * SS_U) {
         VT wv[SS_U];
         uint32_t vv[SS_U];
 #pragma unroll
         for (int u = 0; u < SS_U; ++u) {
-          const int i = i0 + 8 * u;
+          const int i = i0 + SS_W * u;
           const bool in = i < cn;
           vv[u] = in ? sv[i] : 0u;
           wv[u] = in ? __ldcs(reinterpret_cast<const VT*>(h + static_cast<int64_t>(sc[i]) * p.hp))
@@ -447,12 +451,12 @@ __global__ void __launch_bounds__(256) k_stream_sparse(StreamParams p) {
   __syncthreads();
   const double inv_t = p.inv[static_cast<int64_t>(r) * p.inv_ld + p.t];
 #pragma unroll
-  for (int f = threadIdx.x; f < SS_F; f += 256) {
+  for (int f = threadIdx.x; f < SS_F; f += 32 * SS_W) {
     const int64_t s = sb + f;
     if (s > p.t) break;
     uint32_t tot = 0;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) tot += red[w][f];
+    for (int w = 0; w < SS_W; ++w) tot += red[w][f];
     const int accv = static_cast<int>(tot);
     const double inv_s = p.inv[static_cast<int64_t>(r) * p.inv_ld + s];
     const int64_t gi = static_cast<int64_t>(r) * p.g2_ld + (p.t - s);
@@ -477,7 +481,7 @@ cudaError_t launch_stream_ingest_sparse(const StreamParams& p, cudaStream_t s) {
 
 cudaError_t launch_stream_sparse(const StreamParams& p, int32_t n_rings, cudaStream_t s) {
   dim3 grid(static_cast<unsigned>((p.t + 1 + SS_F - 1) / SS_F), n_rings);
-  k_stream_sparse<<<grid, 256, 0, s>>>(p);
+  k_stream_sparse<<<grid, 32 * SS_W, 0, s>>>(p);
   return cudaGetLastError();
 }
 
