@@ -223,3 +223,20 @@ def test_bright_frames_take_the_fp64_g2_path(ctx, orc):
         _, g2, cnt = s.g2(r)
         assert np.array_equal(cnt, cnt_ref)
         assert np.abs(g2 - g2_ref).max() <= 1e-12
+
+
+def test_megapixel_detector_many_bands(ctx, orc):
+    """C3/C4 geometry (1024 x 1024, 50 rings: 64 ingest bands of 16384
+    pixels, rings crossing band edges, many pieces per band): exact Gram and
+    norms of sampled rings against the oracle."""
+    t, h, w, q = 160, 1024, 1024, 50
+    rng = np.random.default_rng(88)
+    frames = rng.poisson(0.05, size=(t, h * w)).clip(0, 255).astype(np.uint8)
+    ring, _ = orc.ring_map(h, w, q)
+    lay = xg.RingLayout.from_ring_map(ctx, ring, q)
+    s = xg.FrameSeries(lay, t).load(frames).ttc_raw()
+    for r in (0, 7, 24, 49):
+        xq = frames[:, ring == r]
+        assert np.array_equal(s.ttc(r, "gram").astype(np.int64), orc.gram_u8(xq)), f"ring {r}"
+        norms, _ = s.norms(r)
+        assert np.array_equal(norms, np.sqrt((xq.astype(np.float64) ** 2).sum(1)))
