@@ -145,6 +145,14 @@ def test_chunked_compress_equals_one_shot(ctx, orc):
         assert np.array_equal(one.cg2(r)[2], ch.cg2(r)[2])
     with pytest.raises(xg.ContractError):
         ch.ttc_raw()
+    # the chunked series' g2 by FFT of its coefficients (no C~), zero frame
+    # included: same counts, same values to the fused path's fp32 accuracy
+    fused = [ch.cg2(r) for r in range(q)]
+    ch.ttc_compressed(store=False, spectral=True)
+    for r in range(q):
+        _, g_sp, c_sp = ch.cg2(r)
+        assert np.array_equal(c_sp, fused[r][2])
+        assert np.abs(g_sp - fused[r][1]).max() <= 1e-5 * np.abs(fused[r][1]).max()
 
 
 def test_rel_error_report_matches_oracle(ctx, orc):
