@@ -531,7 +531,12 @@ def main():
                 "peak_source": peak_src, "traffic": traffic,
                 "traffic_source": "profiles/r1_traffic.json (ncu dram__bytes_read+write, one launch)",
                 "work_per_launch": f"sum_q T(T+1) M_q = {ops:.4g} int8 ops",
-                "kernel_ms": gram_ms, "share_of_step": gram_ms / ms}
+                "kernel_ms": gram_ms, "share_of_step": gram_ms / ms,
+                # the denominator is "of measured" (an in-run cuBLAS int8 GEMM, the
+                # method MEASURED_PEAKS.json uses for bf16, which has no int8 entry);
+                # the nominal dense int8 rate for context
+                "of": "measured", "nominal": {"peak": 4500.0, "frac": achieved / 4500.0,
+                                              "note": "B200 dense int8 nominal, context only"}}
 
     line = {
         "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world,
