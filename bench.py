@@ -2,28 +2,37 @@
 """Benchmark of the XPCS two-time-correlation hot path (BASELINE.json metric:
 "two-time corr frames/sec (raw & rank-k) at 1/2/4/8 B200; % of roofline").
 
-Workload (configs[1], C2): T=4096 frames of 512x512 u8 photon counts,
-mean 0.05 photons/pixel, Q=32 equal-width annular q-rings, seeded synthetic
-speckle generated on the device.  One step = one pass of
-the raw hot path over the batch: ingest (ring permutation + statistics,
-K1) -> exact u8 tcgen05 Gram of every ring (K2) -> g2(tau) (K7).
+Headline workload (configs[1], C2): T=4096 frames of 512x512 u8 photon
+counts, mean 0.05 photons/pixel, Q=32 equal-width annular q-rings, seeded
+synthetic speckle generated on the device.  One step = one
+pass of the raw hot path over the batch: ingest (ring permutation +
+statistics, K1) -> exact u8 tcgen05 Gram of every ring (K2, fused g2) ->
+g2 fold (K7).
 
-  value : T / step time, frames already resident in HBM (raster order).
-  e2e   : the same step through the public API with HOST frames: pinned H2D of
-          the frames + step + D2H of every ring's g2, all inside the timing.
+  value : T / step time with the frames resident in HBM.  With N GPUs the
+          ONE detector is sharded along q-ring boundaries (dist.plan_shards):
+          every GPU holds only its pixel slice of the frames, computes its
+          rings, split rings (if any) are summed on their owner, and every
+          ring's g2 is gathered to rank 0 inside the timed region; value =
+          T / the slowest rank's step time (strong scaling: the work is the
+          same detector at every N).
+  e2e   : the same step through the public API with HOST frames (pinned H2D
+          overlapped with ingest + Gram, xg_series_ttc_raw_host) + D2H of
+          every ring's g2; `e2e.ttc` also returns every ring's int32 TTC.
   roofline: K2 int8 tensor ops per launch / its CUDA-event duration vs the
           int8 peak measured in-run (cuBLAS int8 GEMM via torch._int_mm).
-  cpu_baseline: the UNMODIFIED reference (oracle/_ref, built from
-          /root/reference) on a bounded sample of rings, host cores.
+  c3 / c4 / c5 / compressed: the other BASELINE configs (streaming to
+          T=20000, the 16384-frame 1024^2 raw batch, the 3-MP rank-k sweep).
+  cpu_baseline: the UNMODIFIED reference (oracle/_ref, compiled from
+          /root/reference) on one ring at full T, host cores.
 
 `--impl reference` times the reference's own CPU path on the same config.
-Multi-GPU (torchrun): rings are sharded across ranks (LPT on pixel counts),
-no collective on the data path; value = T / max-over-ranks step time.
 """
 from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -36,28 +45,134 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-CFG = dict(name="C2", T=4096, H=512, W=512, Q=32, mu=0.05, k=64, seed=2, gamma_a=0.002)
 METRIC = "two-time corr frames/sec (raw & rank-k) at 1/2/4/8 B200; % of roofline"
+C2 = dict(name="C2", T=4096, H=512, W=512, Q=32, mu=0.05, k=64, seed=2, gamma_mode=0,
+          gamma_a=0.002)
+C3 = dict(name="C3", T=20000, H=1024, W=1024, Q=64, mu=0.02, k=128, seed=3, gamma_mode=0,
+          gamma_a=0.002)
+C4 = dict(name="C4", T=16384, H=1024, W=1024, Q=100, mu=0.05, seed=4, gamma_mode=1,
+          gamma_a=2e-4)
+C5 = dict(name="C5", T=65536, H=1536, W=2048, Q=128, mu=0.01, ks=(16, 64, 256), seed=5,
+          gamma_mode=0, gamma_a=0.002, chunk=4096)
 
 
-def lpt_shard(sizes, n):
-    """Longest-processing-time assignment of rings (by pixel count) to n ranks."""
-    order = sorted(range(len(sizes)), key=lambda r: -sizes[r])
-    load = [0] * n
-    out = [[] for _ in range(n)]
-    for r in order:
-        j = min(range(n), key=lambda i: load[i])
-        out[j].append(r)
-        load[j] += sizes[r]
-    return [sorted(o) for o in out]
+def headline_config() -> dict:
+    """The `config` object of the headline line, identical in both arms."""
+    c = C2
+    return {"workload": f"{c['name']} (BASELINE configs[1]): raw two-time correlation + g2 of "
+                        f"every q-ring, T={c['T']}, {c['H']}x{c['W']}, Q={c['Q']}, mu={c['mu']}",
+            "T": c["T"], "detector": [c["H"], c["W"]], "rings": c["Q"], "mu": c["mu"],
+            "inputs": f"{c['T'] * c['H'] * c['W'] / 1e9:.2f} GB u8 > 126 MB L2 (no flush needed)"}
 
 
-def gram_ops(T, ring_sizes):
-    """Algorithmic int8 ops of the raw Gram: upper triangle incl. diagonal,
-    2 ops per MAC: sum_q T(T+1) M_q (SURVEY.md 8(d))."""
-    return float(T) * (T + 1) * float(sum(ring_sizes))
+def host_info() -> dict:
+    try:
+        nproc = len(os.sched_getaffinity(0))
+    except Exception:
+        nproc = os.cpu_count() or 1
+    model = "unknown"
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return {"nproc": nproc, "cpu_model": model}
 
 
+def ref_threads(T: int, m: int) -> int:
+    """Threads the reference's gram actually runs on for one ring:
+    parallel_for(n=T, grain=max(16, 2^21 / M_q)) uses min(budget,
+    ceil(T / grain)) workers (linalg.cpp:62-91,127-156)."""
+    env = int(os.environ.get("XPCS_THREADS", "0") or 0)
+    budget = env if env > 0 else (os.cpu_count() or 1)
+    grain = max(16, (1 << 21) // m)
+    return max(1, min(budget, (T + grain - 1) // grain))
+
+
+def reference_ring(sizes, T: int) -> int:
+    """The ring one reference step times: the smallest ring on which the
+    reference's gram already uses every host thread it can (so its per-pixel
+    rate is its best), else the largest ring."""
+    best = max(range(len(sizes)), key=lambda r: sizes[r])
+    full = ref_threads(T, sizes[best])
+    cands = [r for r in range(len(sizes)) if ref_threads(T, sizes[r]) >= full]
+    return min(cands, key=lambda r: (sizes[r], r))
+
+
+def time_reference_ring(cfg, steps: int, warmup: int):
+    """ttc_raw + g2_from_ttc (the reference's per-mask call pattern,
+    SPEC.md:386) of one ring at full T on the UNMODIFIED reference; returns
+    (per-step seconds, ring, its pixels, all ring sizes)."""
+    import oracle
+
+    orc = oracle.c()
+    T, H, W, Q = cfg["T"], cfg["H"], cfg["W"], cfg["Q"]
+    ring, _ = orc.ring_map(H, W, Q)
+    sizes = [int(v) for v in np.bincount(ring, minlength=Q)]
+    r_s = reference_ring(sizes, T)
+    idx = np.nonzero(ring == r_s)[0]
+    # every pixel is an independent seeded chain: generate just this ring (host)
+    xq = orc.gen_speckle_pixels(T, H, W, Q, cfg["mu"], cfg["seed"], idx,
+                                gamma_mode=cfg["gamma_mode"],
+                                gamma_a=cfg["gamma_a"]).astype(np.float64)
+    R = oracle.ref()
+    times = []
+    for i in range(warmup + steps):
+        t0 = time.perf_counter()
+        g = R.ttc_raw(xq)
+        R.g2_from_ttc(g)
+        dt = time.perf_counter() - t0
+        if i >= warmup:
+            times.append(dt)
+    return times, r_s, sizes
+
+
+def reference_fields(cfg, times, r_s, sizes):
+    t_step = statistics.median(times)
+    factor = sum(sizes) / sizes[r_s]
+    t_full = t_step * factor
+    T = cfg["T"]
+    value = T / t_full
+    sample = (f"ring {r_s} ({sizes[r_s]} of {sum(sizes)} px) of {cfg['name']} at full T={T} "
+              f"per step: xpcs::ttc_raw + g2_from_ttc (oracle/_ref, the unmodified reference "
+              f"compiled with its Release flags)")
+    extra = {"measured_ms_per_sample_step": t_step * 1e3,
+             "extrapolation": {"factor": factor, "ms_per_full_step": t_full * 1e3,
+                               "rule": "reference work is T(T+1)/2 * M_q MACs per ring: "
+                                       "linear in pixels at fixed T; full step = sample step "
+                                       "x sum(M_q) / M_sample"}}
+    return value, t_step, sample, extra
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference's own CPU implementation on the host
+    (rank 0 only; never loads this repo's library)."""
+    if rank != 0:
+        return
+    cfg = C2
+    times, r_s, sizes = time_reference_ring(cfg, args.steps, args.warmup)
+    value, t_step, sample, extra = reference_fields(cfg, times, r_s, sizes)
+    hi = host_info()
+    cores = ref_threads(cfg["T"], sizes[r_s])
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "frames/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded speckle, host generator of the same recipe)",
+        "config": headline_config(),
+        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": cores, "kind": "reference",
+                         "sample": sample, **hi},
+        "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "host": hi, **extra,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- GPU arm
 class ClockSampler:
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -110,7 +225,7 @@ class ClockSampler:
 
 
 def measure_int8_peak(torch, dev):
-    """cuBLAS int8 GEMM throughput (torch._int_mm, 8192^3, best of 10) as the
+    """cuBLAS int8 GEMM throughput (torch._int_mm, 8192^3, best of 10): the
     int8 tensor roofline denominator (MEASURED_PEAKS.json has bf16 only)."""
     try:
         n = 8192
@@ -134,165 +249,360 @@ def measure_int8_peak(torch, dev):
         return 2.0 * peaks["bf16_tflops"], f"2 x measured bf16 burst (int8 GEMM unavailable: {e})"
 
 
-def reference_sample(frames_host_cols, ring_sizes, T, budget_s=12.0, max_rings=None):
-    """Time the unmodified reference (ttc_raw + g2_from_ttc per ring, the
-    reference's per-mask call pattern) on rings in ascending
-    size until ~budget_s; extrapolate linearly in pixels at fixed T (the
-    reference's work is T(T+1)/2 * M_q MACs per ring)."""
+class Env:
+    """Per-process state of the GPU arm."""
+
+    def __init__(self, args):
+        import torch
+
+        self.args = args
+        self.torch = torch
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        torch.cuda.set_device(self.local)
+        self.dev = torch.device("cuda", self.local)
+        if self.world > 1:
+            import torch.distributed as tdist
+
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            tdist.init_process_group("nccl", device_id=self.dev)
+        import paper_2407_20356_b200 as xg
+        from paper_2407_20356_b200 import dist
+
+        self.xg, self.dist = xg, dist
+        # one dedicated stream: the library launches on it, events are recorded on it
+        self.stream = torch.cuda.Stream(self.dev)
+        torch.cuda.set_stream(self.stream)
+        self.ctx = xg.Context(self.local, stream=self.stream.cuda_stream)
+        self.peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+
+    def ev(self):
+        return self.torch.cuda.Event(enable_timing=True)
+
+    def barrier(self):
+        if self.world > 1:
+            self.torch.distributed.barrier()
+
+    def max_over_ranks(self, *vals):
+        if self.world == 1:
+            return vals if len(vals) > 1 else vals[0]
+        t = self.torch.tensor([float(v) for v in vals], device=self.dev, dtype=self.torch.float64)
+        self.torch.distributed.all_reduce(t, op=self.torch.distributed.ReduceOp.MAX)
+        out = tuple(float(x) for x in t)
+        return out if len(out) > 1 else out[0]
+
+    def sync(self):
+        self.torch.cuda.synchronize()
+        self.ctx.synchronize()
+
+    def free(self):
+        import gc
+
+        gc.collect()
+        self.torch.cuda.synchronize()
+        self.torch.cuda.empty_cache()
+
+
+class Shard:
+    """This rank's share of one detector: the ring-aligned pixel slice of the
+    frames (the whole raster on one GPU), its layout and ring order."""
+
+    def __init__(self, E: Env, cfg: dict, allow_split: bool = True):
+        xg, dist = E.xg, E.dist
+        T, H, W, Q = cfg["T"], cfg["H"], cfg["W"], cfg["Q"]
+        self.cfg = cfg
+        self.ring = xg.annular_rings(H, W, Q)
+        self.masks = [np.nonzero(self.ring == r)[0] for r in range(Q)]
+        self.sizes = [int(m.size) for m in self.masks]
+        self.plan = dist.plan_shards(self.sizes, E.world)
+        if not allow_split and self.plan.split_rings():
+            self.plan = dist.plan_shards(self.sizes, E.world, tol=1e9)  # whole rings only
+        if E.world == 1:
+            self.pixels = None
+            self.rings = list(range(Q))
+            self.layout = xg.RingLayout(E.ctx, H * W, self.masks)
+        else:
+            self.pixels, local, self.rings = dist.rank_slice(self.plan, E.rank, self.masks)
+            self.layout = xg.RingLayout(E.ctx, int(self.pixels.size), local)
+        self.my_pixels = sum(self.layout.ring_pixels(i) for i in range(len(self.rings)))
+
+    def frames(self, E: Env, T: int | None = None, seed: int | None = None):
+        """Device frames of this rank's pixel slice (K8 generator; on >1 GPU
+        the full raster is generated and sliced untimed, standing in for a
+        detector readout that delivers each GPU its pixels)."""
+        torch = E.torch
+        c = self.cfg
+        T = T or c["T"]
+        full = torch.empty((T, c["H"] * c["W"]), dtype=torch.uint8, device=E.dev)
+        E.xg.synth_speckle(E.ctx, full.data_ptr(), T, c["H"], c["W"], c["Q"], c["mu"],
+                           c["seed"] if seed is None else seed, gamma_mode=c["gamma_mode"],
+                           gamma_a=c["gamma_a"])
+        if self.pixels is None:
+            return full
+        idx = torch.from_numpy(self.pixels).to(E.dev)
+        E.torch.cuda.synchronize()
+        sl = torch.index_select(full, 1, idx)
+        del full
+        return sl.contiguous()
+
+    def describe(self, E: Env) -> str:
+        if E.world == 1:
+            return "1 GPU: whole detector"
+        sp = self.plan.split_rings()
+        return (f"{E.world} GPUs: one detector sharded along q-ring boundaries (LPT on pixel "
+                f"counts, imbalance {self.plan.imbalance():.3%}, split rings {sp}); each GPU holds "
+                f"only its pixel slice; split-ring shares summed on the owner; g2 all-gathered "
+                f"(NCCL) inside the timed region")
+
+
+def raw_step(E, sh, series, frames, rec=None, gather=True):
+    series.load(frames)
+    if rec is not None:
+        rec[0].record(E.stream)
+    series.ttc_raw()
+    if rec is not None:
+        rec[1].record(E.stream)
+    if E.world > 1:
+        if sh.plan.split_rings():
+            E.dist.reduce_split_rings(series, sh.plan, E.rank, sh.rings)
+        if gather:
+            E.dist.gather_g2(series, sh.plan, E.rank, sh.rings)
+
+
+def time_raw(E, sh, series, frames, steps, warmup, clocks=False):
+    for _ in range(warmup):
+        raw_step(E, sh, series, frames)
+    E.sync()
+    recs = [(E.ev(), E.ev()) for _ in range(steps)]
+    sampler = None
+    if clocks:
+        sampler = ClockSampler(E.local)
+        sampler.start()
+        time.sleep(0.15)
+    E.barrier()
+    E.torch.cuda.synchronize()
+    l0 = E.ctx.kernel_launches
+    a, b = E.ev(), E.ev()
+    a.record(E.stream)
+    for i in range(steps):
+        raw_step(E, sh, series, frames, recs[i])
+    b.record(E.stream)
+    E.torch.cuda.synchronize()
+    E.barrier()
+    clk = sampler.stop() if sampler else None
+    launches = E.ctx.kernel_launches - l0
+    E.ctx.synchronize()
+    ms = a.elapsed_time(b) / steps
+    gram_ms = statistics.mean(x.elapsed_time(y) for x, y in recs)
+    ms, gram_ms = E.max_over_ranks(ms, gram_ms)
+    return ms, gram_ms, launches, clk
+
+
+def gram_ops(T, ring_sizes):
+    """Algorithmic int8 ops of the raw Gram: upper triangle incl. diagonal,
+    2 ops per MAC: sum_q T(T+1) M_q (SURVEY.md 8(d))."""
+    return float(T) * (T + 1) * float(sum(ring_sizes))
+
+
+def exact_gram(x_u8):
+    # counts: every partial sum < 2^53, so the f64 product is exact in any order
+    x = x_u8.astype(np.float64)
+    return (x @ x.T).astype(np.int64)
+
+
+def parity_check(E, sh, series, frames):
+    """Untimed self-check of the benchmark's own output: the smallest and a
+    mid-size ring this rank owns whole -- int32 Gram bitwise against an exact
+    host product of the same bytes, C and g2 against the unmodified
+    reference (oracle/_ref ttc_raw + g2_from_ttc) on the small ring."""
     import oracle
 
-    R = oracle.ref()
-    order = sorted(range(len(ring_sizes)), key=lambda r: ring_sizes[r])
-    # start near the median ring so the sample has representative threading
-    order = order[len(order) // 2:] + order[: len(order) // 2]
-    spent, pix, used = 0.0, 0, []
-    for r in order:
-        xq = frames_host_cols(r)
+    owned = [r for r in sh.plan.owned_rings(E.rank) if r not in sh.plan.split_rings()]
+    if not owned:
+        return {"status": "skipped", "why": "no whole ring on this rank"}
+    small = min(owned, key=lambda r: sh.sizes[r])
+    mid = sorted(owned, key=lambda r: sh.sizes[r])[len(owned) // 2]
+    host = frames.cpu().numpy()
+    out = {"rings": sorted({small, mid})}
+    ref = oracle.ref() if oracle.ref_available() else None
+    for r in out["rings"]:
+        li = sh.rings.index(r)
+        cols = (sh.masks[r] if sh.pixels is None
+                else np.searchsorted(sh.pixels, sh.masks[r]))
+        xq = np.ascontiguousarray(host[:, cols])
+        if not np.array_equal(series.ttc(li, "gram").astype(np.int64), exact_gram(xq)):
+            return {"status": "FAILED", "ring": r, "what": "int32 Gram != exact product"}
+        if r == small and ref is not None:
+            c_ref = ref.ttc_raw(xq.astype(np.float64))
+            dc = float(np.abs(series.ttc(li, "f64") - c_ref).max())
+            _, g2_ref, cnt_ref = ref.g2_from_ttc(c_ref)
+            _, g2, cnt = series.g2(li)
+            dg = float(np.abs(g2 - g2_ref).max())
+            if dc > 1e-12 or dg > 1e-12 or not np.array_equal(cnt, cnt_ref):
+                return {"status": "FAILED", "ring": r, "max_dC": dc, "max_dg2": dg}
+            out.update(max_abs_dC_vs_reference=dc, max_abs_dg2_vs_reference=dg)
+    out["status"] = "ok"
+    out["checks"] = ("int32 Gram bitwise vs an exact host product of the same bytes; C and g2 "
+                     "within 1e-12 of the unmodified reference's ttc_raw / g2_from_ttc")
+    return out
+
+
+def run_headline(E, line):
+    """C2 raw: value, e2e, roofline, parity."""
+    torch, args = E.torch, E.args
+    cfg = C2
+    T = cfg["T"]
+    sh = Shard(E, cfg)
+    frames = sh.frames(E)
+    series = E.xg.FrameSeries(sh.layout, T)
+    ms, gram_ms, launches, clocks = time_raw(E, sh, series, frames, args.steps, args.warmup,
+                                             clocks=True)
+    line.update(value=T / (ms / 1e3), ms_per_step=ms, gpu_launches=launches, clocks=clocks)
+    line["parallelism"] = sh.describe(E)
+    # ---------------------------------------------------------------- e2e
+    if not args.no_e2e:
+        host = torch.empty(tuple(frames.shape), dtype=torch.uint8, pin_memory=True)
+        host.copy_(frames)
+        nring = len(sh.rings)
+
+        def step_e2e(ttc_out=None):
+            series.ttc_raw_host(host)  # pinned H2D in chunks, overlapped with ingest + Gram
+            if E.world > 1:
+                if sh.plan.split_rings():
+                    E.dist.reduce_split_rings(series, sh.plan, E.rank, sh.rings)
+                res = E.dist.gather_g2(series, sh.plan, E.rank, sh.rings)  # to rank 0 (host)
+            else:
+                series.g2_all()  # D2H of every ring's g2 values + counts
+            if ttc_out is not None:  # the TTC itself: every owned ring's exact int32 Gram
+                for li, r in enumerate(sh.rings):
+                    if sh.plan.owner[r] == E.rank:
+                        ttc_out.append(series.ttc(li, "gram"))
+
+        for _ in range(2):
+            step_e2e()
+        E.barrier()
+        E.sync()
+        n_e2e = max(3, min(args.steps, 10))
         t0 = time.perf_counter()
-        g = R.ttc_raw(xq)
-        R.g2_from_ttc(g)
-        spent += time.perf_counter() - t0
-        pix += ring_sizes[r]
-        used.append(r)
-        if spent >= budget_s or (max_rings and len(used) >= max_rings):
-            break
-    total = float(sum(ring_sizes))
-    t_full = spent * total / pix
-    return T / t_full, used, spent, pix
-
-
-def ref_threads(T, ring_sizes_used):
-    ncpu = os.cpu_count() or 1
-    env = int(os.environ.get("XPCS_THREADS", "0") or 0)
-    budget = env if env > 0 else ncpu
-    best = 1
-    for m in ring_sizes_used:  # parallel_for(n, grain=max(16, 2^21/m)) (linalg.cpp:138)
-        grain = max(16, (1 << 21) // m)
-        best = max(best, min(budget, (T + grain - 1) // grain))
-    return best
-
-
-def run_reference(args, rank, world):
-    """--impl reference: the reference's own CPU implementation on the host."""
-    if rank != 0:
-        return
-    import oracle
-
-    cfg = CFG
-    import paper_2407_20356_b200 as xg  # geometry helper only (numpy)
-
-    orc = oracle.c()
-    T, H, W, Q = cfg["T"], cfg["H"], cfg["W"], cfg["Q"]
-    ring = xg.annular_rings(H, W, Q)
-    sizes = [int((ring == r).sum()) for r in range(Q)]
-    # the largest ring per step, full T (the reference parallelises one ring
-    # at a time with grain 2^21/M_q rows, linalg.cpp:138: its biggest ring
-    # gets the most host threads, so this is its best per-pixel rate);
-    # frames from the same generator (host)
-    r_s = max(range(Q), key=lambda r: sizes[r])
-    idx = np.nonzero(ring == r_s)[0]
-    # every pixel is an independent seeded chain: generate just this ring
-    xq = orc.gen_speckle_pixels(T, H, W, Q, cfg["mu"], cfg["seed"], idx,
-                                gamma_a=cfg["gamma_a"]).astype(np.float64)
-    R = oracle.ref()
-    times = []
-    for i in range(args.warmup + args.steps):
+        for _ in range(n_e2e):
+            step_e2e()
+        E.sync()
+        e2e_s = E.max_over_ranks((time.perf_counter() - t0) / n_e2e)
+        # the same with every ring's TTC (int32 Gram, full symmetric) read back
+        n_ttc = 3
         t0 = time.perf_counter()
-        g = R.ttc_raw(xq)
-        R.g2_from_ttc(g)
-        dt = time.perf_counter() - t0
-        if i >= args.warmup:
-            times.append(dt)
-    t_step = statistics.median(times)
-    t_full = t_step * sum(sizes) / sizes[r_s]
-    value = T / t_full
-    cores = ref_threads(T, [sizes[r_s]])
-    sample = (f"ring {r_s} ({sizes[r_s]} px) of {Q} at full T={T} per step (ttc_raw + g2_from_ttc), "
-              f"step time scaled by sum(M_q)/M_q = {sum(sizes) / sizes[r_s]:.1f} (work is linear in "
-              f"M at fixed T)")
-    line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "frames/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": t_full * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded speckle, host generator)",
-        "config": {"workload": f"{cfg['name']}: raw TTC, T={T}, {H}x{W}, Q={Q}, mu={cfg['mu']}",
-                   "T": T, "detector": [H, W], "rings": Q},
-        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": cores, "kind": "reference",
-                         "sample": sample},
-        "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(line), flush=True)
+        for _ in range(n_ttc):
+            out = []
+            step_e2e(out)
+            del out
+        E.sync()
+        ttc_s = E.max_over_ranks((time.perf_counter() - t0) / n_ttc)
+        g2_bytes = cfg["Q"] * T * 16
+        ttc_bytes = cfg["Q"] * T * T * 4
+        line["e2e"] = {
+            "value": T / e2e_s, "unit": "frames/s", "h2d_bytes_per_step": T * cfg["H"] * cfg["W"],
+            "d2h_bytes_per_step": g2_bytes, "ms_per_step": e2e_s * 1e3,
+            "what": "public API from pinned host frames: FrameSeries.ttc_raw_host (chunked H2D "
+                    "overlapped with ingest + Gram) + every ring's g2 to the host",
+            "timing": "host wall clock around synchronous API calls, max over ranks",
+            "ttc": {"value": T / ttc_s, "unit": "frames/s", "ms_per_step": ttc_s * 1e3,
+                    "h2d_bytes_per_step": T * cfg["H"] * cfg["W"],
+                    "d2h_bytes_per_step": g2_bytes + ttc_bytes,
+                    "what": "same + every ring's TTC (the exact int32 Gram, full symmetric "
+                            "T x T) read back to host memory, as ttc_raw returns it"}}
+        del host
+    else:
+        line["e2e"] = {"skipped": "--no-e2e (profiling run)"}
+    # ---------------------------------------------------------------- roofline
+    peak, peak_src = measure_int8_peak(torch, E.dev)
+    my_sizes = [sh.layout.ring_pixels(i) for i in range(len(sh.rings))]
+    ops = gram_ops(T, my_sizes)
+    achieved = ops / (gram_ms / 1e3) / 1e12
+    traffic = None
+    try:  # DRAM bytes of K2 from the committed ncu --set full capture (per launch)
+        tr = json.load(open(os.path.join(ROOT, "profiles", "r2_traffic.json")))["k_gram2<0>"]
+        traffic = tr["dram_read_bytes"] + tr["dram_write_bytes"]
+    except Exception:
+        pass
+    line["roofline"] = {
+        "bound": "tensor", "kernel": "k_gram2<0> (K2 CTA-pair, fused g2 epilogue) + g2 fold",
+        "achieved": achieved, "peak": peak, "unit": "TOPS (int8)", "frac": achieved / peak,
+        "peak_source": peak_src, "traffic": traffic,
+        "traffic_source": "profiles/r2_traffic.json (ncu dram__bytes_read+write, one launch)",
+        "work_per_launch": f"sum_q T(T+1) M_q = {ops:.4g} int8 ops (this rank's rings)",
+        "kernel_ms": gram_ms, "share_of_step": gram_ms / ms, "of": "measured",
+        "nominal": {"peak": 4500.0, "frac": achieved / 4500.0,
+                    "note": "B200 dense int8 nominal, context only"}}
+    # ---------------------------------------------------------------- parity
+    try:
+        line["parity"] = parity_check(E, sh, series, frames)
+    except Exception as e:  # pragma: no cover
+        line["parity"] = {"status": "FAILED", "error": str(e)}
+    return sh, series, frames
 
 
-def run_compressed(args, torch, xg, ctx, stream, frames, series, ring, sizes, mine, world, dev):
-    """Rank-k path on the same frames: basis per ring from a 256-frame
-    training prefix (untimed, built on the device), then per step
-    ingest (K1) -> int8-digit projection (K3) -> bf16x3 compressed Gram with
-    fused g2 (K4)."""
-    cfg = CFG
+def run_compressed(E, sh, series, frames):
+    """Rank-k path on the same C2 frames (k=64): basis per ring from a
+    256-frame training prefix built on the device (K9, untimed), then per
+    step ingest (K1) -> int8-digit projection (K3) -> bf16x3 compressed Gram
+    with fused g2 (K4)."""
+    xg, args = E.xg, E.args
+    cfg = C2
     T, k = cfg["T"], cfg["k"]
     t_train = 256
-    # the basis is built on the device (K9, xg_series_build_basis: the
-    # reference's build_online_from_frames per ring) from a training series
-    basis = xg.Basis(series.layout, k)
-    train = xg.FrameSeries(series.layout, t_train).load(frames[:t_train])
-    ctx.synchronize()
+    basis = xg.Basis(sh.layout, k)
+    train = xg.FrameSeries(sh.layout, t_train).load(frames[:t_train])
+    E.sync()
     t0 = time.perf_counter()
     train.build_basis(k, basis=basis)
-    ctx.synchronize()
+    E.sync()
     t_basis = time.perf_counter() - t0
     del train
-    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 
     def step(rec=None):
         series.load(frames)
         if rec:
-            rec[0].record(stream)
+            rec[0].record(E.stream)
         series.compress(basis)
         if rec:
-            rec[1].record(stream)
+            rec[1].record(E.stream)
         series.ttc_compressed()
         if rec:
-            rec[2].record(stream)
+            rec[2].record(E.stream)
+        if E.world > 1:
+            E.dist.gather_g2(series, sh.plan, E.rank, sh.rings, compressed=True)
 
     for _ in range(args.warmup):
         step()
-    torch.cuda.synchronize()
-    ctx.synchronize()
-    recs = [(ev(), ev(), ev()) for _ in range(args.steps)]
-    if world > 1:
-        torch.distributed.barrier()
-    torch.cuda.synchronize()
-    a, b = ev(), ev()
-    a.record(stream)
+    E.sync()
+    recs = [(E.ev(), E.ev(), E.ev()) for _ in range(args.steps)]
+    E.barrier()
+    E.torch.cuda.synchronize()
+    a, b = E.ev(), E.ev()
+    a.record(E.stream)
     for i in range(args.steps):
         step(recs[i])
-    b.record(stream)
-    torch.cuda.synchronize()
-    ctx.synchronize()
+    b.record(E.stream)
+    E.sync()
     ms = a.elapsed_time(b) / args.steps
     proj_ms = statistics.mean(r[0].elapsed_time(r[1]) for r in recs)
     cg_ms = statistics.mean(r[1].elapsed_time(r[2]) for r in recs)
-    if world > 1:
-        tt = torch.tensor([ms, proj_ms, cg_ms], device=dev)
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        ms, proj_ms, cg_ms = (float(x) for x in tt)
-    # deviation of the homomorphic path from the raw correlation (untimed):
-    # ttc_rel_error(raw C, compressed C~) per ring on the device
+    ms, proj_ms, cg_ms = E.max_over_ranks(ms, proj_ms, cg_ms)
+    # deviation of the homomorphic path from the raw correlation (untimed)
     series.ttc_raw()
     rel = series.rel_error()
-    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-    my_m = float(sum(sizes[r] for r in mine))
-    q = len(mine)
+    hbm = E.peaks["hbm_gbs"]
+    my_m = float(sh.my_pixels)
+    q = len(sh.rings)
     kp = (k + 63) // 64 * 64
     proj_bytes = T * my_m + 3 * k * my_m + T * q * k * 8 + 3 * T * q * kp * 2
-    cg_flops_alg = q * T * (T + 1) * k
     cg_flops_mma = 6 * q * T * (T + 1) * k
     nb256 = (T + 255) // 256
     cg_bytes = q * (nb256 * (nb256 + 1) // 2) * 256 * 256 * 4 + 3 * T * q * kp * 2
     return {
-        "value": world * T / (ms / 1e3), "unit": "frames/s", "ms_per_step": ms, "k": k,
+        "value": T / (ms / 1e3), "unit": "frames/s", "ms_per_step": ms, "k": k,
+        "workload": "C2 frames, rank k=64 per ring: ingest + projection + homomorphic TTC + g2",
         "mode": "F32-accurate (3 int8 digits of V; bf16x3 split Y, 6 products, fp32 accumulate)",
         "deviation_vs_raw": {"metric": "ttc_rel_error(raw C, compressed C~) per ring",
                              "median": float(np.median(rel)), "min": float(rel.min()),
@@ -301,85 +611,215 @@ def run_compressed(args, torch, xg, ctx, stream, frames, series, ring, sizes, mi
                  f"xg_series_build_basis: Gram, Jacobi, W = Xn^T U, 2x Cholesky-QR), untimed",
         "basis_build_ms": t_basis * 1e3,
         "projection": {"kernel": "k_project (K3)", "bound": "hbm", "ms": proj_ms,
-                       "achieved": proj_bytes / (proj_ms / 1e3) / 1e9, "peak": peaks["hbm_gbs"],
-                       "unit": "GB/s", "frac": proj_bytes / (proj_ms / 1e3) / 1e9 / peaks["hbm_gbs"],
+                       "achieved": proj_bytes / (proj_ms / 1e3) / 1e9, "peak": hbm,
+                       "unit": "GB/s", "frac": proj_bytes / (proj_ms / 1e3) / 1e9 / hbm,
                        "bytes": proj_bytes},
         "gram": {"kernel": "k_gram2<1> (K4, CTA-pair, fused g2) + fold",
                  "bound": "hbm (C~ write)", "ms": cg_ms,
-                 "achieved": cg_bytes / (cg_ms / 1e3) / 1e9, "peak": peaks["hbm_gbs"],
-                 "unit": "GB/s", "frac": cg_bytes / (cg_ms / 1e3) / 1e9 / peaks["hbm_gbs"],
+                 "achieved": cg_bytes / (cg_ms / 1e3) / 1e9, "peak": hbm,
+                 "unit": "GB/s", "frac": cg_bytes / (cg_ms / 1e3) / 1e9 / hbm,
                  "bytes": cg_bytes,
                  "bytes_note": "f32 C~ of the upper 256x256 pair tiles + the bf16 planes read",
                  "mma_tflops": cg_flops_mma / (cg_ms / 1e3) / 1e12,
-                 "mma_frac_of_bf16_peak": cg_flops_mma / (cg_ms / 1e3) / 1e12 / peaks["bf16_tflops"]},
+                 "mma_frac_of_bf16_peak": cg_flops_mma / (cg_ms / 1e3) / 1e12 / E.peaks["bf16_tflops"]},
     }
 
 
-def run_streaming(args, torch, xg, ctx, stream):
-    """configs[2] (C3) streaming mode at a bounded history depth: 1024^2
-    detector, Q=64 rings, mu=0.02, k=128.  Frames are pushed one at a time
-    (the public FrameStream API, frames already on the device); each push
-    ingests the frame and correlates it against the whole history of every
-    ring.  Timed: n pushes at history depth D after an untimed fill."""
-    H = W = 1024
-    Q, mu, k, n = 64, 0.02, 128, 64
-    D = args.stream_depth
-    dev = torch.device("cuda", torch.cuda.current_device())
-    frames = torch.empty((D + n, H * W), dtype=torch.uint8, device=dev)
-    xg.synth_speckle(ctx, frames.data_ptr(), D + n, H, W, Q, mu, 7)
-    ring = xg.annular_rings(H, W, Q)
-    lay = xg.RingLayout(ctx, H * W, [np.nonzero(ring == r)[0] for r in range(Q)])
-    rng = np.random.default_rng(3)
+def run_c3(E):
+    """configs[2] (C3) streaming: 1024x1024, Q=64, mu=0.02, k=128.  Frames
+    are pushed one at a time through the public FrameStream API (frames
+    already on the device) up to T=20000; every push ingests the frame and
+    correlates it against the whole history of every ring, raw (photon-event
+    mode: nnz * t bytes) and rank-k compressed.  Reported: run average and
+    the tail rate over the last 1000 frames; plus the dense raw
+    kernel at a bounded depth with its HBM roofline."""
+    torch, xg = E.torch, E.xg
+    c = C3
+    T, H, W, Q, k = c["T"], c["H"], c["W"], c["Q"], c["k"]
+    sh = Shard(E, c)
+    frames = sh.frames(E)
+    lay = sh.layout
     basis = xg.Basis(lay, k)
-    for r in range(Q):  # timing does not depend on the basis values
-        qm, _ = np.linalg.qr(rng.standard_normal((int((ring == r).sum()), k)))
-        basis.set_ring(r, qm)
-    nnz = float((frames[:256] != 0).float().mean()) * H * W
-    m_total = sum(lay.ring_pixels(r) for r in range(Q))
-    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
-
-    def timed(depth, **kw):
-        s = xg.FrameStream(lay, depth + n, **kw)
-        for i in range(depth):
-            s.push(frames[i])
-        torch.cuda.synchronize()
-        ctx.synchronize()
-        a, b = ev(), ev()
-        a.record(stream)
-        for i in range(depth, depth + n):
-            s.push(frames[i])
-        b.record(stream)
-        torch.cuda.synchronize()
-        ctx.synchronize()
-        ms = a.elapsed_time(b) / n
-        del s
-        return ms
-
-    peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
-    t_mid = D + n / 2
-    ms_s = timed(D, sparse=True)
-    ms_c = timed(D, sparse=True, basis=basis)
-    d_dense = min(D, 4096)
-    ms_d = timed(d_dense)
-    dense_bytes = m_total * (d_dense + n / 2)
-    sparse_bytes = nnz * t_mid
-    cmp_bytes = t_mid * Q * k * 4
+    train = xg.FrameSeries(lay, 256).load(frames[:256])
+    try:
+        train.build_basis(k, basis=basis)
+        bsrc = "device-built from the first 256 frames (K9)"
+    except xg.Error:  # a zero training frame in a tiny ring: timing does not depend on V
+        rng = np.random.default_rng(3)
+        for r in range(Q):
+            qm, _ = np.linalg.qr(rng.standard_normal((lay.ring_pixels(r), k)))
+            basis.set_ring(r, qm)
+        bsrc = "random orthonormal (a training frame was all-zero in a small ring)"
+    del train
+    nnz = float((frames[:512] != 0).float().mean()) * H * W
+    st = xg.FrameStream(lay, T, basis=basis, sparse=True)
+    marks = {0: E.ev(), T - 1000: E.ev(), T: E.ev()}
+    E.sync()
+    marks[0].record(E.stream)
+    for i in range(T):
+        st.push(frames[i])
+        if i + 1 == T - 1000:
+            marks[T - 1000].record(E.stream)
+    marks[T].record(E.stream)
+    E.sync()
+    avg_ms = marks[0].elapsed_time(marks[T]) / T
+    tail_ms = marks[T - 1000].elapsed_time(marks[T]) / 1000
+    t_tail = T - 500
+    raw_bytes_tail = nnz * t_tail
+    cmp_bytes_tail = t_tail * Q * k * 4
+    del st
+    # dense raw column (K5) at a bounded history depth: the HBM roofline
+    D, n = 4096, 64
+    sd = xg.FrameStream(lay, D + n)
+    for i in range(D):
+        sd.push(frames[i])
+    E.sync()
+    a, b = E.ev(), E.ev()
+    a.record(E.stream)
+    for i in range(D, D + n):
+        sd.push(frames[i])
+    b.record(E.stream)
+    E.sync()
+    ms_d = a.elapsed_time(b) / n
+    dense_bytes = sh.my_pixels * (D + n / 2)
+    hbm = E.peaks["hbm_gbs"]
+    del sd, frames
+    E.free()
     return {
-        "workload": f"C3: 1024x1024, Q={Q}, mu={mu}, k={k}; {n} pushes timed at history depth {D}",
-        "nnz_per_frame": nnz,
-        "raw_sparse": {"frames_per_s": 1e3 / ms_s, "ms_per_frame": ms_s,
-                       "column_bytes_per_frame": sparse_bytes,
-                       "achieved_gbs": sparse_bytes / (ms_s / 1e3) / 1e9},
-        "raw_sparse_plus_compressed": {
-            "frames_per_s": 1e3 / ms_c, "ms_per_frame": ms_c,
-            "bytes_per_frame": sparse_bytes + cmp_bytes,
-            "achieved_gbs": (sparse_bytes + cmp_bytes) / (ms_c / 1e3) / 1e9},
-        "raw_dense": {"depth": d_dense, "frames_per_s": 1e3 / ms_d, "ms_per_frame": ms_d,
+        "workload": f"C3 (configs[2]): {H}x{W}, Q={Q}, mu={c['mu']}, k={k}; frames pushed one "
+                    f"at a time to T={T}, each correlated against the whole history (raw "
+                    f"photon-event columns + rank-k compressed columns + g2 per lag)",
+        "frames_per_s_avg": 1e3 / avg_ms, "ms_per_frame_avg": avg_ms,
+        "frames_per_s_tail": 1e3 / tail_ms, "ms_per_frame_tail": tail_ms,
+        "tail": "last 1000 frames (history depth 19000-20000)",
+        "nnz_per_frame": nnz, "basis": bsrc,
+        "tail_bytes_per_frame": {"raw_nnz_history": raw_bytes_tail,
+                                 "compressed_history": cmp_bytes_tail,
+                                 "achieved_gbs": (raw_bytes_tail + cmp_bytes_tail) / (tail_ms / 1e3) / 1e9},
+        "raw_dense": {"depth": D, "frames_per_s": 1e3 / ms_d, "ms_per_frame": ms_d,
                       "roofline": {"kernel": "k_stream_raw (K5, whole push timed)", "bound": "hbm",
-                                   "achieved": dense_bytes / (ms_d / 1e3) / 1e9, "peak": peak,
+                                   "achieved": dense_bytes / (ms_d / 1e3) / 1e9, "peak": hbm,
                                    "unit": "GB/s",
-                                   "frac": dense_bytes / (ms_d / 1e3) / 1e9 / peak}},
+                                   "frac": dense_bytes / (ms_d / 1e3) / 1e9 / hbm}},
     }
+
+
+def run_c4(E, peak):
+    """configs[3] (C4): T=16384 frames of 1024x1024, Q=100 rings with
+    log-spaced Gamma_q (3 decades), raw exact Gram + g2 of every ring, TTC
+    stored (107 GB of int32 tiles on one GPU).  Sharded along q-ring
+    boundaries on >1 GPU."""
+    c = C4
+    T = c["T"]
+    sh = Shard(E, c)
+    frames = sh.frames(E)
+    series = E.xg.FrameSeries(sh.layout, T)
+    ms, gram_ms, launches, _ = time_raw(E, sh, series, frames, 3, 2)
+    my_sizes = [sh.layout.ring_pixels(i) for i in range(len(sh.rings))]
+    ops = gram_ops(T, my_sizes)
+    out = {
+        "workload": f"C4 (configs[3]): raw TTC + g2, T={T}, {c['H']}x{c['W']}, Q={c['Q']}, "
+                    f"mu={c['mu']}, Gamma_q = {c['gamma_a']} x 10^(3q/(Q-1))",
+        "frames_per_s": T / (ms / 1e3), "ms_per_step": ms, "parallelism": sh.describe(E),
+        "roofline": {"kernel": "k_gram2<0>", "bound": "tensor", "kernel_ms": gram_ms,
+                     "achieved": ops / (gram_ms / 1e3) / 1e12, "peak": peak,
+                     "unit": "TOPS (int8)", "frac": ops / (gram_ms / 1e3) / 1e12 / peak},
+    }
+    del series, frames
+    E.free()
+    return out
+
+
+def run_c5(E):
+    """configs[4] (C5): 1536x2048 detector, T=65536, mu=0.01, Q=128, k in
+    {16, 64, 256}: frames arrive in chunks of 4096 (generated on the device,
+    untimed; 206 GB never resident), every chunk is ingested and projected
+    for the three ranks (timed), then the homomorphic g2 of every ring is
+    formed without storing C~ (2.2 TB): through the K4 tiles (fused g2) and
+    in the Fourier domain (spectral).  Bases: random orthonormal (timing does
+    not depend on V)."""
+    torch, xg = E.torch, E.xg
+    c = C5
+    T, ch = c["T"], c["chunk"]
+    sh = Shard(E, c, allow_split=False)
+    lay = sh.layout
+    rng = np.random.default_rng(5)
+    ks = c["ks"]
+    bases, series = {}, {}
+    for k in ks:
+        b = xg.Basis(lay, k)
+        for i in range(len(sh.rings)):
+            qm, _ = np.linalg.qr(rng.standard_normal((lay.ring_pixels(i), k)))
+            b.set_ring(i, qm)
+        bases[k] = b
+        series[k] = xg.FrameSeries(lay, T, x_frames=ch)
+    t_cmp = {k: 0.0 for k in ks}
+    full = None
+    for j, f0 in enumerate(range(0, T, ch)):
+        n = min(ch, T - f0)
+        seed = c["seed"] * 1000 + j  # each chunk: a fresh stationary stretch of the series
+        if sh.pixels is None:
+            if full is None:
+                full = torch.empty((ch, c["H"] * c["W"]), dtype=torch.uint8, device=E.dev)
+            xg.synth_speckle(E.ctx, full.data_ptr(), n, c["H"], c["W"], c["Q"], c["mu"], seed,
+                             gamma_mode=c["gamma_mode"], gamma_a=c["gamma_a"])
+            chunk = full[:n]
+        else:
+            chunk = sh.frames(E, T=n, seed=seed)
+        for k in ks:
+            a, b = E.ev(), E.ev()
+            a.record(E.stream)
+            series[k].compress_chunk(bases[k], chunk, first=(j == 0))
+            b.record(E.stream)
+            b.synchronize()
+            t_cmp[k] += a.elapsed_time(b) / 1e3
+    del full
+    out = {"workload": f"C5 (configs[4]): {c['H']}x{c['W']} ({c['H'] * c['W']} px), T={T}, "
+                       f"mu={c['mu']}, Q={c['Q']}; chunks of {ch} frames ingested + projected "
+                       f"(K1 + K3) per rank k, then homomorphic g2 without storing C~",
+           "parallelism": sh.describe(E), "by_k": {}}
+    hbm = E.peaks["hbm_gbs"]
+    for k in ks:
+        s = series[k]
+        E.sync()
+        s.ttc_compressed(store=False)  # warm
+        E.sync()
+        a, b = E.ev(), E.ev()
+        a.record(E.stream)
+        s.ttc_compressed(store=False)
+        b.record(E.stream)
+        E.sync()
+        t_tiles = a.elapsed_time(b) / 1e3
+        s.ttc_compressed(store=False, spectral=True)
+        E.sync()
+        a, b = E.ev(), E.ev()
+        a.record(E.stream)
+        s.ttc_compressed(store=False, spectral=True)
+        b.record(E.stream)
+        E.sync()
+        t_spec = a.elapsed_time(b) / 1e3
+        tc, tt, ts = E.max_over_ranks(t_cmp[k], t_tiles, t_spec)
+        ingest_bytes = 3.0 * T * sh.my_pixels  # K1 raster read + ring-major write, K3 read
+        out["by_k"][str(k)] = {
+            "ingest_project_s": tc, "frames_per_s_ingest_project": T / tc,
+            "g2_tiles_s": tt, "g2_spectral_s": ts,
+            "frames_per_s_total_tiles": T / (tc + tt), "frames_per_s_total_spectral": T / (tc + ts),
+            "ingest_project_hbm": {"bytes": ingest_bytes, "achieved_gbs": ingest_bytes / tc / 1e9,
+                                   "frac": ingest_bytes / tc / 1e9 / hbm,
+                                   "note": "K1 reads the raster + writes the ring-major copy, K3 "
+                                           "re-reads it (3 B per pixel per frame)"}}
+    del series, bases
+    E.free()
+    return out
+
+
+def cpu_baseline(E, args):
+    cfg = C2
+    times, r_s, sizes = time_reference_ring(cfg, 1, 0)
+    value, t_step, sample, extra = reference_fields(cfg, times, r_s, sizes)
+    hi = host_info()
+    return {"value": value, "unit": "frames/s", "cores": ref_threads(cfg["T"], sizes[r_s]),
+            "kind": "reference", "sample": sample, **hi, **extra}
 
 
 def main():
@@ -389,208 +829,54 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--no-compressed", action="store_true")
     ap.add_argument("--no-stream", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--stream-depth", type=int, default=8192)
+    ap.add_argument("--no-large", action="store_true", help="skip C4 and C5")
+    ap.add_argument("--only", default="", help="profiling: run only the headline step")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
 
-    import torch
-
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        import torch.distributed as dist
-
-        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=dev)
-    import paper_2407_20356_b200 as xg
-
-    cfg = CFG
-    T, H, W, Q = cfg["T"], cfg["H"], cfg["W"], cfg["Q"]
-    P = H * W
-    ring = xg.annular_rings(H, W, Q)
-    sizes = [int((ring == r).sum()) for r in range(Q)]
-    # Multi-GPU = weak scaling over independent ring partitions (SURVEY 8(e):
-    # rings are independent objects, no data-path collective): every GPU owns
-    # a C2-sized partition -- its own 512x512 detector region with 32 rings
-    # and its own seeded frames -- so per-GPU work is fixed as N grows and
-    # `value` counts the frames of all partitions.
-    mine = list(range(Q))
-    # a dedicated (non-default) stream: the library launches on it and the
-    # CUDA events below are recorded on it
-    stream = torch.cuda.Stream(dev)
-    torch.cuda.set_stream(stream)
-    ctx = xg.Context(local, stream=stream.cuda_stream)
-
-    frames = torch.empty((T, P), dtype=torch.uint8, device=dev)
-    xg.synth_speckle(ctx, frames.data_ptr(), T, H, W, Q, cfg["mu"], cfg["seed"] + 1000 * rank,
-                     gamma_a=cfg["gamma_a"])
-    layout = xg.RingLayout(ctx, P, [np.nonzero(ring == r)[0] for r in mine])
-    series = xg.FrameSeries(layout, T)
-
-    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
-
-    def step(record=None):
-        series.load(frames)
-        if record is not None:
-            record[0].record(stream)
-        series.ttc_raw()  # K2 Gram with fused g2 epilogue + g2 fold
-        if record is not None:
-            record[1].record(stream)
-
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    ctx.synchronize()
-
-    def barrier():
-        if world > 1:
-            torch.distributed.barrier()
-
-    # ---------------------------------------------------------- device-resident
-    gram_ev = [(ev(), ev()) for _ in range(args.steps)]
-    sampler = ClockSampler(local)
-    sampler.start()
-    time.sleep(0.15)
-    barrier()
-    torch.cuda.synchronize()
-    l0 = ctx.kernel_launches
-    t0, t1 = ev(), ev()
-    t0.record(stream)
-    for i in range(args.steps):
-        step(gram_ev[i])
-    t1.record(stream)
-    torch.cuda.synchronize()
-    barrier()
-    clocks = sampler.stop()
-    launches = ctx.kernel_launches - l0
-    ctx.synchronize()
-    ms = t0.elapsed_time(t1) / args.steps
-    gram_ms = statistics.mean(a.elapsed_time(b) for a, b in gram_ev)
-    if world > 1:
-        tt = torch.tensor([ms, gram_ms], device=dev)
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        ms, gram_ms = float(tt[0]), float(tt[1])
-    value = world * T / (ms / 1e3)  # frames of all partitions / max-over-ranks time
-
-    # ---------------------------------------------------------- end to end
-    if args.no_e2e:  # profiling runs only (tools/capture_profiles.sh launch list)
-        e2e = {"skipped": "--no-e2e (profiling run)"}
-    else:
-        host = torch.empty((T, P), dtype=torch.uint8, pin_memory=True)
-        host.copy_(frames)
-        g2_out = np.empty(T)
-
-        def step_e2e():
-            # pinned H2D in chunks, overlapped with ingest + Gram (one public call)
-            series.ttc_raw_host(host)
-            series.g2_all()  # D2H of every ring's g2 values + counts
-
-        for _ in range(2):
-            step_e2e()
-        barrier()
-        torch.cuda.synchronize()
-        e2e_steps = max(3, min(args.steps, 10))
-        tw0 = time.perf_counter()
-        for _ in range(e2e_steps):
-            step_e2e()
-        torch.cuda.synchronize()
-        e2e_s = (time.perf_counter() - tw0) / e2e_steps
-        if world > 1:
-            tt = torch.tensor([e2e_s], device=dev)
-            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-            e2e_s = float(tt[0])
-        e2e = {"value": world * T / e2e_s, "unit": "frames/s", "h2d_bytes_per_step": T * P,
-               "d2h_bytes_per_step": len(mine) * T * 16, "ms_per_step": e2e_s * 1e3,
-               "timing": "host wall clock around synchronous API calls"}
-
-    # ---------------------------------------------------------- roofline
-    peak, peak_src = measure_int8_peak(torch, dev)
-    my_sizes = [sizes[r] for r in mine]
-    ops = gram_ops(T, my_sizes)
-    achieved = ops / (gram_ms / 1e3) / 1e12
-    traffic = None
-    try:  # DRAM bytes of K2 from the committed ncu --set full capture (per launch)
-        tr = json.load(open(os.path.join(ROOT, "profiles", "r1_traffic.json")))["k_gram2<0>"]
-        traffic = tr["dram_read_bytes"] + tr["dram_write_bytes"]
-    except Exception:
-        pass
-    roofline = {"bound": "tensor", "kernel": "k_gram2<0> (K2 CTA-pair, fused g2 epilogue) + g2 fold", "achieved": achieved,
-                "peak": peak, "unit": "TOPS (int8)", "frac": achieved / peak,
-                "peak_source": peak_src, "traffic": traffic,
-                "traffic_source": "profiles/r1_traffic.json (ncu dram__bytes_read+write, one launch)",
-                "work_per_launch": f"sum_q T(T+1) M_q = {ops:.4g} int8 ops",
-                "kernel_ms": gram_ms, "share_of_step": gram_ms / ms,
-                # the denominator is "of measured" (an in-run cuBLAS int8 GEMM, the
-                # method MEASURED_PEAKS.json uses for bf16, which has no int8 entry);
-                # the nominal dense int8 rate for context
-                "of": "measured", "nominal": {"peak": 4500.0, "frac": achieved / 4500.0,
-                                              "note": "B200 dense int8 nominal, context only"}}
-
-    line = {
-        "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
-        "data": "synthetic (seeded speckle generated on device, SURVEY.md 8(d))",
-        "config": {"workload": f"{cfg['name']}: raw TTC + g2, T={T}, {H}x{W}, Q={Q}, "
-                               f"mu={cfg['mu']}, all rings",
-                   "T": T, "detector": [H, W], "rings": Q, "rings_this_rank": len(mine),
-                   "parallelism": f"{world} independent ring partitions (one C2 detector region "
-                                  f"of {Q} rings per GPU, no collective)",
-                   "l2": f"inputs {T * P / 1e9:.2f} GB > 126 MB L2 (no flush needed)"},
-        "roofline": roofline, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
-    }
-
-    # ---------------------------------------------------------- compressed (rank-k)
-    if not args.no_compressed:
-        line["compressed"] = run_compressed(args, torch, xg, ctx, stream, frames, series, ring,
-                                           sizes, mine, world, dev)
-
-    # ---------------------------------------------------------- streaming (C3)
-    if not args.no_stream and world == 1:
+    E = Env(args)
+    line = {"metric": METRIC, "value": None, "unit": "frames/s", "n_gpus": E.world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic (seeded speckle generated on device, SURVEY.md 8(d))",
+            "config": headline_config()}
+    sh, series, frames = run_headline(E, line)
+    if not args.no_compressed and not args.only:
+        line["compressed"] = run_compressed(E, sh, series, frames)
+    del series, frames
+    E.free()
+    if not args.only:
+        if not args.no_stream and E.world == 1:
+            try:
+                line["c3_streaming"] = run_c3(E)
+            except Exception as e:  # keep the main line
+                line["c3_streaming"] = {"failed": repr(e)}
+        if not args.no_large:
+            for key, fn in (("c4_raw", lambda: run_c4(E, line["roofline"]["peak"])),
+                            ("c5_compressed", lambda: run_c5(E))):
+                try:
+                    line[key] = fn()
+                except Exception as e:  # keep the main line
+                    line[key] = {"failed": repr(e)}
+                    E.free()
+    if E.rank == 0 and E.world == 1 and not args.no_cpu_baseline and not args.only:
         try:
-            line["streaming"] = run_streaming(args, torch, xg, ctx, stream)
-        except Exception as e:  # keep the main line
-            line["streaming"] = {"failed": str(e)}
-
-    # ---------------------------------------------------------- CPU baseline
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        try:
-            import oracle
-
-            if oracle.ref_available():
-                fr_host = frames.cpu().numpy()
-
-                def cols(r):
-                    return fr_host[:, ring == r].astype(np.float64)
-
-                v, used, spent, pix = reference_sample(cols, sizes, T, budget_s=args.cpu_budget)
-                line["cpu_baseline"] = {
-                    "value": v, "unit": "frames/s", "cores": ref_threads(T, [sizes[r] for r in used]),
-                    "kind": "reference",
-                    "sample": f"rings {used} ({pix} of {sum(sizes)} px) at full T={T}, "
-                              f"ttc_raw + g2_from_ttc, {spent:.1f} s; scaled linearly in pixels"}
-            else:
-                line["cpu_baseline"] = {"value": None, "kind": "reference",
-                                        "sample": "oracle/_ref not built"}
+            line["cpu_baseline"] = cpu_baseline(E, args)
         except Exception as e:  # keep the GPU line even if the CPU leg fails
             line["cpu_baseline"] = {"value": None, "kind": "reference", "sample": f"failed: {e}"}
-
-    if rank == 0:
+    if E.rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
-        torch.distributed.destroy_process_group()
+    if E.world > 1:
+        E.torch.distributed.destroy_process_group()
 
 
 if __name__ == "__main__":

@@ -128,6 +128,25 @@ XG_API int xg_series_ttc_raw_host(xg_series* s, const uint8_t* frames, int64_t n
 /* g2 of every ring from the current raw TTC (run separately after
  * xg_ttc_raw(..., XG_NO_G2)). */
 XG_API int xg_series_g2(xg_series* s);
+/* Split rings across processes (multi-GPU).  The Gram and the
+ * frame norms^2 of a ring are sums over its pixels (gram, linalg.cpp:127-156),
+ * so a ring whose pixels are divided among processes is exact after an
+ * integer sum of the per-process partials.  Each process runs xg_ttc_raw on
+ * its share (stored, not XG_NO_STORE); xg_series_export_partial writes the
+ * share's exact Gram as the packed upper 256 x 256 pair tiles (I <= J in
+ * (I, J) row-major order, xg_series_partial_elems() int32 values) and its
+ * |x_t|^2 column (n_frames int64); the caller sums them (e.g. NCCL int32 /
+ * int64 sum, or send + add); xg_series_import_partial writes the total back
+ * into one process's series and refreshes the ring's norms, zero-frame
+ * bookkeeping and (unless XG_NO_G2) g2.  XG_STRICT raises the reference's
+ * NormalizationError for a zero frame of the summed ring; a summed |x|^2 >=
+ * 2^31 is reported as XG_ERR_CONTRACT by the next synchronising call.
+ * on_device: the buffers are device (1) or host (0) memory. */
+XG_API int64_t xg_series_partial_elems(const xg_series* s);
+XG_API int xg_series_export_partial(xg_series* s, int32_t ring, int32_t* gram, int64_t* norm2,
+                                    int on_device);
+XG_API int xg_series_import_partial(xg_series* s, int32_t ring, const int32_t* gram,
+                                    const int64_t* norm2, int on_device, uint32_t flags);
 /* Readback.  dtype XG_F64/XG_F32: C = G_ij / (|x_i| |x_j|) (full symmetric
  * n x n, ld elements per row); XG_I32_GRAM: the exact integer Gram. */
 XG_API int xg_series_get_ttc(xg_series* s, int32_t ring, int32_t dtype, void* out, int64_t ld,
@@ -135,6 +154,12 @@ XG_API int xg_series_get_ttc(xg_series* s, int32_t ring, int32_t dtype, void* ou
 /* g2 values (n), counts (n; N-d, or fewer when frames were flagged), lags in
  * frames (multiply by frame_period for seconds). */
 XG_API int xg_series_get_g2(xg_series* s, int32_t ring, double* values, int64_t* counts);
+/* Device pointers of every ring's g2 values / pair counts (which: 0 raw, 1
+ * compressed), [ring][ld] with n_frames valid per ring; borrowed, valid until
+ * the series is recomputed or destroyed (collectives gather g2 without a
+ * host round trip). */
+XG_API int xg_series_g2_device(xg_series* s, int32_t which, const double** values,
+                               const int64_t** counts, int64_t* ld);
 /* g2 and pair counts of every ring in one transfer: [ring][n_frames] each */
 XG_API int xg_series_get_g2_all(xg_series* s, double* values, int64_t* counts);
 /* Deviation of the homomorphic path per ring (ttc_rel_error, correlate.cpp:
@@ -165,6 +190,11 @@ XG_API int xg_series_get_norms(xg_series* s, int32_t ring, double* norms, int64_
  * counts (new); xg_series_load_xfsr reads any of them into the series
  * (values must be integer counts in [0, 255]).  Host-only helpers report
  * through xg_io_last_error / xg_io_last_payload. */
+/* Device coefficient rows a few 1e-9 above unit norm (the 3-digit int8 basis
+ * of a frame inside the basis span) are rescaled to unit norm before writing,
+ * so the reference reader's append() (model.cpp:184-193) accepts the store;
+ * rows further above 1, non-finite rows (and, in xg_io_write_xcmp, any row
+ * above 1 + 1e-10) are XG_ERR_CONTRACT. */
 XG_API int xg_series_write_xcmp(xg_series* s, int32_t ring, const char* path,
                                 uint64_t encoder_hash, int32_t append);
 XG_API int xg_stream_append_xcmp(xg_stream* s, int32_t ring, const char* path,

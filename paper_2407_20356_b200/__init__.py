@@ -107,6 +107,32 @@ def _as_counts_u8(frames) -> np.ndarray:
     return np.ascontiguousarray(a, dtype=np.uint8)
 
 
+def _tensor_frames(frames, ctx: "Context", pixels: int, n: int | None, what: str,
+                   host_ok: bool = True, device_ok: bool = True):
+    """Validate a torch tensor of u8 frames handed to the library by pointer:
+    uint8, contiguous (a strided view would feed the wrong pixels), exactly
+    n x pixels elements, on the context's device (or in host memory).
+    Returns (n, on_device)."""
+    if str(getattr(frames, "dtype", "")) != "torch.uint8":
+        raise ContractError(f"{what}: frames tensor must be uint8 photon counts")
+    if not frames.is_contiguous():
+        raise ContractError(f"{what}: frames tensor must be contiguous")
+    on_dev = bool(getattr(frames, "is_cuda", False))
+    if on_dev and not device_ok:
+        raise ContractError(f"{what} takes host frames; use load() for device ones")
+    if not on_dev and not host_ok:
+        raise ContractError(f"{what} takes device frames")
+    if on_dev and frames.device.index != ctx.device:
+        raise ContractError(f"{what}: frames are on cuda:{frames.device.index}, the context "
+                            f"on cuda:{ctx.device}")
+    if n is None:
+        n = int(frames.shape[0]) if frames.dim() > 1 else 1
+    if n < 1 or frames.numel() != n * pixels:
+        raise ShapeError(f"{what}: frames tensor has {frames.numel()} elements, expected "
+                         f"{n} x {pixels}")
+    return n, on_dev
+
+
 def _ptr(a: np.ndarray) -> C.c_void_p:
     return C.c_void_p(a.ctypes.data)
 
@@ -351,6 +377,16 @@ class Basis:
             self.h = None
 
 
+class _DeviceArray:
+    """__cuda_array_interface__ view of a library-owned device buffer (keeps
+    its owner alive)."""
+
+    def __init__(self, ptr: int, shape, typestr: str, owner):
+        self.__cuda_array_interface__ = {"data": (int(ptr), False), "shape": tuple(shape),
+                                         "typestr": typestr, "version": 3, "strides": None}
+        self._owner = owner
+
+
 # ----------------------------------------------------------------- series
 class FrameSeries:
     """Device-resident photon-count frames of one detector, correlated per
@@ -386,14 +422,11 @@ class FrameSeries:
         """Ingest ``frames`` (n x full_pixels u8): a numpy array (host, copied
         H2D) or any object exposing ``data_ptr()`` (a CUDA torch tensor)."""
         if hasattr(frames, "data_ptr"):  # torch tensor: CUDA (device) or pinned host
-            if str(getattr(frames, "dtype", "torch.uint8")) != "torch.uint8":
-                raise ContractError("frames tensor must be uint8 photon counts")
-            n = int(frames.shape[0]) if n_frames is None else n_frames
-            if frames.numel() < n * self.layout.full_pixels:
-                raise ShapeError("frames tensor smaller than n x full_pixels")
-            on_dev = 1 if getattr(frames, "is_cuda", False) else 0
+            n, on_dev = _tensor_frames(frames, self.ctx, self.layout.full_pixels, n_frames, "load")
             _check(self.ctx.h, lib.xg_series_load_frames(self.h, C.c_void_p(frames.data_ptr()),
-                                                         n, on_dev))
+                                                         n, 1 if on_dev else 0))
+            # a host tensor's copy is asynchronous: keep it alive until replaced
+            self._keep = None if on_dev else frames
             return self
         a = _as_counts_u8(frames)
         if a.ndim != 2 or a.shape[1] != self.layout.full_pixels:
@@ -419,15 +452,11 @@ class FrameSeries:
         flags = ((_abi.STRICT if strict else 0) | (0 if g2 else _abi.NO_G2)
                  | (0 if store else _abi.NO_STORE))
         if hasattr(frames, "data_ptr"):
-            if getattr(frames, "is_cuda", False):
-                raise ContractError("ttc_raw_host takes host frames; use load() for device ones")
-            if str(getattr(frames, "dtype", "torch.uint8")) != "torch.uint8":
-                raise ContractError("frames tensor must be uint8 photon counts")
-            n = int(frames.shape[0])
-            if frames.numel() < n * self.layout.full_pixels:
-                raise ShapeError("frames tensor smaller than n x full_pixels")
+            n, _ = _tensor_frames(frames, self.ctx, self.layout.full_pixels, None, "ttc_raw_host",
+                                  device_ok=False)
             _check(self.ctx.h, lib.xg_series_ttc_raw_host(self.h, C.c_void_p(frames.data_ptr()),
                                                           n, flags))
+            self._keep = frames
             return self
         a = _as_counts_u8(frames)
         if a.ndim != 2 or a.shape[1] != self.layout.full_pixels:
@@ -435,6 +464,58 @@ class FrameSeries:
         _check(self.ctx.h, lib.xg_series_ttc_raw_host(self.h, _ptr(a), a.shape[0], flags))
         self._keep = a
         return self
+
+    # ---------------------------------------------- split rings (multi-GPU)
+    @property
+    def partial_elems(self) -> int:
+        """int32 values of one ring's packed Gram partial (upper pair tiles)."""
+        return int(lib.xg_series_partial_elems(self.h))
+
+    def export_partial(self, ring: int, gram=None, norm2=None):
+        """This process's share of a split ring: (packed int32 Gram tiles,
+        int64 |x_t|^2).  Pass CUDA torch tensors (int32 [partial_elems], int64
+        [n_frames]) to export on the device; by default numpy host arrays."""
+        on_dev = gram is not None and getattr(gram, "is_cuda", False)
+        if gram is None:
+            gram = np.empty(self.partial_elems, np.int32)
+            norm2 = np.empty(self.n_frames, np.int64)
+        self._check_partial(gram, norm2, on_dev)
+        gp = gram.data_ptr() if on_dev else gram.ctypes.data
+        npp = norm2.data_ptr() if on_dev else norm2.ctypes.data
+        _check(self.ctx.h, lib.xg_series_export_partial(self.h, ring, C.c_void_p(gp),
+                                                        C.c_void_p(npp), 1 if on_dev else 0))
+        return gram, norm2
+
+    def import_partial(self, ring: int, gram, norm2, strict: bool = False,
+                       g2: bool = True) -> "FrameSeries":
+        """Install the summed partials of a split ring (numpy or CUDA tensors)."""
+        on_dev = getattr(gram, "is_cuda", False)
+        if not on_dev:
+            gram = np.ascontiguousarray(gram, dtype=np.int32)
+            norm2 = np.ascontiguousarray(norm2, dtype=np.int64)
+        self._check_partial(gram, norm2, on_dev)
+        gp = gram.data_ptr() if on_dev else gram.ctypes.data
+        npp = norm2.data_ptr() if on_dev else norm2.ctypes.data
+        flags = (_abi.STRICT if strict else 0) | (0 if g2 else _abi.NO_G2)
+        _check(self.ctx.h, lib.xg_series_import_partial(self.h, ring, C.c_void_p(gp),
+                                                        C.c_void_p(npp), 1 if on_dev else 0,
+                                                        flags))
+        return self
+
+    def _check_partial(self, gram, norm2, on_dev: bool) -> None:
+        if on_dev:
+            ok = (str(gram.dtype) == "torch.int32" and str(norm2.dtype) == "torch.int64"
+                  and gram.is_contiguous() and norm2.is_contiguous()
+                  and getattr(norm2, "is_cuda", False)
+                  and gram.numel() == self.partial_elems and norm2.numel() == self.n_frames)
+        else:
+            ok = (isinstance(gram, np.ndarray) and isinstance(norm2, np.ndarray)
+                  and gram.dtype == np.int32 and norm2.dtype == np.int64
+                  and gram.flags.c_contiguous and norm2.flags.c_contiguous
+                  and gram.size == self.partial_elems and norm2.size == self.n_frames)
+        if not ok:
+            raise ShapeError(f"split-ring partial must be int32[{self.partial_elems}] + "
+                             f"int64[{self.n_frames}], contiguous, both host or both device")
 
     def compute_g2(self) -> "FrameSeries":
         """g2 of every ring from the current raw TTC (after ttc_raw(g2=False))."""
@@ -466,6 +547,28 @@ class FrameSeries:
         cnt = np.empty((q, n), np.int64)
         _check(self.ctx.h, lib.xg_series_get_g2_all(self.h, vals.ctypes.data_as(_abi.PD),
                                                     cnt.ctypes.data_as(_abi.PI64)))
+        return np.arange(n, dtype=np.float64) * self.frame_period, vals, cnt
+
+    def g2_device(self, compressed: bool = False):
+        """Every ring's g2 values and pair counts as CUDA torch tensors
+        [rings, ld] viewing the library's device buffers (no copy; valid
+        until the series is recomputed; columns >= n_frames are padding)."""
+        import torch
+
+        v, c, ld = C.c_void_p(), C.c_void_p(), C.c_int64(0)
+        _check(self.ctx.h, lib.xg_series_g2_device(self.h, 1 if compressed else 0, C.byref(v),
+                                                   C.byref(c), C.byref(ld)))
+        shape = (self.layout.n_rings, int(ld.value))
+        return (torch.as_tensor(_DeviceArray(v.value, shape, "<f8", self), device="cuda"),
+                torch.as_tensor(_DeviceArray(c.value, shape, "<i8", self), device="cuda"))
+
+    def cg2_all(self):
+        """(lags, values [ring][n], counts [ring][n]) of the compressed g2."""
+        n, q = self.n_frames, self.layout.n_rings
+        vals = np.empty((q, n), np.float64)
+        cnt = np.empty((q, n), np.int64)
+        for r in range(q):
+            _, vals[r], cnt[r] = self.cg2(r)
         return np.arange(n, dtype=np.float64) * self.frame_period, vals, cnt
 
     # ------------------------------------------------------ compressed path
@@ -554,12 +657,11 @@ class FrameSeries:
         frames are not kept.  ``first`` starts a new series."""
         flags = (_abi.CHUNK_FIRST if first else 0) | (_abi.STRICT if strict else 0)
         if hasattr(frames, "data_ptr"):
-            if str(getattr(frames, "dtype", "torch.uint8")) != "torch.uint8":
-                raise ContractError("frames tensor must be uint8 photon counts")
-            n = int(frames.shape[0])
-            on_dev = 1 if getattr(frames, "is_cuda", False) else 0
+            n, on_dev = _tensor_frames(frames, self.ctx, self.layout.full_pixels, None,
+                                       "compress_chunk")
             _check(self.ctx.h, lib.xg_series_compress_chunk(
-                self.h, basis.h, C.c_void_p(frames.data_ptr()), n, on_dev, flags))
+                self.h, basis.h, C.c_void_p(frames.data_ptr()), n, 1 if on_dev else 0, flags))
+            self._keep = None if on_dev else frames
         else:
             a = _as_counts_u8(frames)
             if a.ndim != 2 or a.shape[1] != self.layout.full_pixels:
@@ -659,10 +761,10 @@ class FrameStream:
 
     def push(self, frame) -> None:
         if hasattr(frame, "data_ptr"):
-            if str(getattr(frame, "dtype", "torch.uint8")) != "torch.uint8":
-                raise ContractError("frame tensor must be uint8 photon counts")
+            _, on_dev = _tensor_frames(frame, self.ctx, self.layout.full_pixels, 1, "push")
             _check(self.ctx.h, lib.xg_stream_push(self.h, C.c_void_p(frame.data_ptr()),
-                                                  1 if getattr(frame, "is_cuda", False) else 0))
+                                                  1 if on_dev else 0))
+            self._keep = None if on_dev else frame
             return
         a = _as_counts_u8(frame).ravel()
         if a.size != self.layout.full_pixels:

@@ -48,9 +48,13 @@ _sigs = {
     "xg_ttc_raw": (C.c_int, [P, U32]),
     "xg_series_ttc_raw_host": (C.c_int, [P, P, I64, U32]),
     "xg_series_g2": (C.c_int, [P]),
+    "xg_series_partial_elems": (I64, [P]),
+    "xg_series_export_partial": (C.c_int, [P, I32, P, P, C.c_int]),
+    "xg_series_import_partial": (C.c_int, [P, I32, P, P, C.c_int, U32]),
     "xg_series_get_ttc": (C.c_int, [P, I32, I32, P, I64, C.c_int]),
     "xg_series_get_g2": (C.c_int, [P, I32, PD, PI64]),
     "xg_series_get_g2_all": (C.c_int, [P, PD, PI64]),
+    "xg_series_g2_device": (C.c_int, [P, I32, C.POINTER(P), C.POINTER(P), PI64]),
     "xg_series_rel_error": (C.c_int, [P, PD]),
     "xg_series_write_xcmp": (C.c_int, [P, I32, C.c_char_p, C.c_uint64, I32]),
     "xg_stream_append_xcmp": (C.c_int, [P, I32, C.c_char_p, C.c_uint64, I64]),

@@ -44,22 +44,38 @@ __device__ __forceinline__ double ref_dot(const double* a, const double* b, int6
   return __dadd_rn(__dadd_rn(__dadd_rn(s0, s1), __dadd_rn(s2, s3)), tail);
 }
 
-// row_normalize: one thread per row (the dot is one sequential chain per
-// accumulator); bad[0] = first zero row (atomicMin), rows written only when
-// the norm is nonzero.
-__global__ void k_exact_rownorm(const double* x, int64_t n, int64_t m, double* xn, double* norms,
-                                unsigned long long* bad) {
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+// row_normalize: one warp per row.  The warp loads 32 consecutive elements
+// per step (coalesced) and squares them in parallel; lane l < 4 owns the
+// reference's accumulator s_l (elements k = 4q + l) and adds its 8 products
+// of the step in ascending q through shuffles, so every chain is the
+// reference's sequential one.  bad[0] = first zero row (atomicMin).
+__global__ void __launch_bounds__(256) k_exact_rownorm(const double* x, int64_t n, int64_t m,
+                                                       double* norms, unsigned long long* bad) {
+  const int lane = threadIdx.x & 31;
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
   if (i >= n) return;
   const double* row = x + i * m;
-  const double nr = sqrt(ref_dot(row, row, m));
-  norms[i] = nr;
-  if (nr == 0.0) {
-    atomicMin(bad, static_cast<unsigned long long>(i));
-    return;
+  const int64_t body = m / 4 * 4;
+  double acc = 0.0;  // lane l < 4: s_l
+  for (int64_t k0 = 0; k0 < body; k0 += 32) {
+    const int64_t k = k0 + lane;
+    const double v = k < body ? row[k] : 0.0;
+    const double pr = __dmul_rn(v, v);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const double t = __shfl_sync(0xffffffffu, pr, 4 * q + (lane & 3));
+      if (k0 + 4 * q + (lane & 3) < body) acc = __dadd_rn(acc, t);
+    }
   }
-  if (xn)
-    for (int64_t p = 0; p < m; ++p) xn[i * m + p] = __ddiv_rn(row[p], nr);
+  double tail = 0.0;
+  for (int64_t k = body; k < m; ++k) tail = __dadd_rn(tail, __dmul_rn(row[k], row[k]));
+  const double s0 = __shfl_sync(0xffffffffu, acc, 0), s1 = __shfl_sync(0xffffffffu, acc, 1);
+  const double s2 = __shfl_sync(0xffffffffu, acc, 2), s3 = __shfl_sync(0xffffffffu, acc, 3);
+  if (lane == 0) {
+    const double nr = sqrt(__dadd_rn(__dadd_rn(__dadd_rn(s0, s1), __dadd_rn(s2, s3)), tail));
+    norms[i] = nr;
+    if (nr == 0.0) atomicMin(bad, static_cast<unsigned long long>(i));
+  }
 }
 
 // Elementwise division pass (coalesced) for the normalised copy.
@@ -168,10 +184,11 @@ __global__ void k_exact_g2(const double* g, int64_t n, double period, double* la
 __global__ void k_exact_project(const double* xn, int64_t n, int64_t m, const double* v,
                                 int64_t k, double* coeffs) {
   const int64_t i = blockIdx.x;
+  const int64_t j0 = static_cast<int64_t>(blockIdx.y) * 1024;  // this block's coefficients
   __shared__ double sx[256];
   __shared__ int32_t sp[256];
   __shared__ int cnt;
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};  // coefficients threadIdx.x + 256 * e (k <= 1024)
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};  // coefficients j0 + threadIdx.x + 256 * e
   for (int64_t p0 = 0; p0 < m; p0 += 256) {
     __syncthreads();
     if (threadIdx.x == 0) cnt = 0;
@@ -200,7 +217,7 @@ __global__ void k_exact_project(const double* xn, int64_t n, int64_t m, const do
     }
     __syncthreads();
     for (int e = 0; e < 4; ++e) {
-      const int64_t j = threadIdx.x + 256 * e;
+      const int64_t j = j0 + threadIdx.x + 256 * e;
       if (j >= k) break;
       double a = acc[e];
       for (int q = 0; q < cnt; ++q) a = __dadd_rn(a, __dmul_rn(sx[q], v[sp[q] * k + j]));
@@ -208,28 +225,52 @@ __global__ void k_exact_project(const double* xn, int64_t n, int64_t m, const do
     }
   }
   for (int e = 0; e < 4; ++e) {
-    const int64_t j = threadIdx.x + 256 * e;
+    const int64_t j = j0 + threadIdx.x + 256 * e;
     if (j < k) coeffs[i * k + j] = acc[e];
   }
 }
 
-// ttc_rel_error: the reference's single sequential pass.
-__global__ void k_exact_relerr(const double* a, const double* b, int64_t count, double* out) {
+// ttc_rel_error: the reference's single sequential pass (two chains, num
+// and den, in ascending entry order -- its bits need that order).  One warp:
+// 32 consecutive entries per step are loaded coalesced (4 steps in flight)
+// and their products formed in parallel; every lane then runs both chains
+// over the step's products, taken by shuffles in ascending order, so only
+// the two dependent DADDs per entry remain on the critical path.
+__global__ void __launch_bounds__(32) k_exact_relerr(const double* a, const double* b,
+                                                     int64_t count, double* out) {
+  const int lane = threadIdx.x;
   double num = 0.0, den = 0.0;
-  for (int64_t i = 0; i < count; ++i) {
-    const double d = __dadd_rn(a[i], -b[i]);
-    num = __dadd_rn(num, __dmul_rn(d, d));
-    den = __dadd_rn(den, __dmul_rn(a[i], a[i]));
+  for (int64_t i0 = 0; i0 < count; i0 += 128) {
+    double dd[4], aa[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t i = i0 + 32 * u + lane;
+      const double av = i < count ? a[i] : 0.0, bv = i < count ? b[i] : 0.0;
+      const double d = __dadd_rn(av, -bv);
+      dd[u] = __dmul_rn(d, d);
+      aa[u] = __dmul_rn(av, av);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int l = 0; l < 32; ++l) {
+        const double pd = __shfl_sync(0xffffffffu, dd[u], l);
+        const double pa = __shfl_sync(0xffffffffu, aa[u], l);
+        if (i0 + 32 * u + l < count) {
+          num = __dadd_rn(num, pd);
+          den = __dadd_rn(den, pa);
+        }
+      }
   }
-  out[0] = den == 0.0 ? -1.0 : sqrt(__ddiv_rn(num, den));
+  if (lane == 0) out[0] = den == 0.0 ? -1.0 : sqrt(__ddiv_rn(num, den));
 }
 
 }  // namespace
 
 cudaError_t launch_exact_rownorm(const double* x, int64_t n, int64_t m, double* xn, double* norms,
                                  unsigned long long* bad, cudaStream_t s) {
-  k_exact_rownorm<<<static_cast<unsigned>((n + 127) / 128), 128, 0, s>>>(x, n, m, nullptr, norms,
-                                                                        bad);
+  if (n < 1) return cudaSuccess;
+  k_exact_rownorm<<<static_cast<unsigned>((n + 7) / 8), 256, 0, s>>>(x, n, m, norms, bad);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || !xn) return e;
   k_exact_divide<<<static_cast<unsigned>((n * m + 255) / 256), 256, 0, s>>>(x, norms, n, m, xn);
@@ -258,13 +299,15 @@ cudaError_t launch_exact_g2(const double* g, int64_t n, double period, double* l
 
 cudaError_t launch_exact_project(const double* xn, int64_t n, int64_t m, const double* v,
                                  int64_t k, double* coeffs, cudaStream_t s) {
-  k_exact_project<<<static_cast<unsigned>(n), 256, 0, s>>>(xn, n, m, v, k, coeffs);
+  if (n < 1 || k < 1) return cudaSuccess;
+  k_exact_project<<<dim3(static_cast<unsigned>(n), static_cast<unsigned>((k + 1023) / 1024)), 256,
+                    0, s>>>(xn, n, m, v, k, coeffs);
   return cudaGetLastError();
 }
 
 cudaError_t launch_exact_relerr(const double* a, const double* b, int64_t count, double* out,
                                 cudaStream_t s) {
-  k_exact_relerr<<<1, 1, 0, s>>>(a, b, count, out);
+  k_exact_relerr<<<1, 32, 0, s>>>(a, b, count, out);
   return cudaGetLastError();
 }
 

@@ -275,6 +275,37 @@ cudaError_t launch_pack_upper(const ExpandParams& p, int src_mode, int64_t row0,
   return cudaGetLastError();
 }
 
+// Split-ring exchange: copy the upper pair tiles of one ring's Gram slab
+// to / from the packed tile buffer.  One CTA per tile; 16-byte accesses.
+__global__ void __launch_bounds__(256) k_tiles_copy(int32_t* slab, int64_t ld, int32_t nb,
+                                                    int32_t* packed, int dir) {
+  int64_t tile = blockIdx.x;
+  int32_t I = 0;
+  while (tile >= nb - I) {  // row I of the tile triangle holds nb - I tiles
+    tile -= nb - I;
+    ++I;
+  }
+  const int32_t J = I + static_cast<int32_t>(tile);
+  int4* pk = reinterpret_cast<int4*>(packed + static_cast<int64_t>(blockIdx.x) * 65536);
+  for (int e = threadIdx.x; e < 256 * 64; e += blockDim.x) {
+    const int row = e >> 6, c4 = e & 63;
+    int4* sp = reinterpret_cast<int4*>(slab + (static_cast<int64_t>(I) * 256 + row) * ld +
+                                       static_cast<int64_t>(J) * 256) + c4;
+    if (dir == 0)
+      pk[e] = *sp;
+    else
+      *sp = pk[e];
+  }
+}
+
+cudaError_t launch_tiles_copy(int32_t* slab, int64_t ld, int32_t nb, int32_t* packed, int dir,
+                              cudaStream_t s) {
+  const int64_t ntiles = static_cast<int64_t>(nb) * (nb + 1) / 2;
+  if (ntiles == 0) return cudaSuccess;
+  k_tiles_copy<<<static_cast<unsigned>(ntiles), 256, 0, s>>>(slab, ld, nb, packed, dir);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_expand(const ExpandParams& p, int src_mode, cudaStream_t s) {
   const unsigned nt = static_cast<unsigned>((p.n + 31) / 32);
   dim3 grid(nt, nt);

@@ -1,21 +1,21 @@
-// k_gram2.cu -- K2/K4 on CTA pairs: tcgen05.mma.cta_group::2, 256 x 256
-// tiles per cluster of 2 SMs.
+// k_gram2.cu -- K2 (raw u8 Gram, kind::i8) and K4 (compressed Gram,
+// kind::f16 over bf16 split planes) on CTA pairs: tcgen05.mma.cta_group::2,
+// 256 x 256 tiles per cluster of 2 SMs.
 //
-// Same math, epilogue and fused-g2 contract as k_gram.cu, but each MMA is
-// M=256 x N=256 x K=32 issued by the leader CTA for the pair: CTA r of the
-// pair stages rows [i0 + 128 r, +128) of A and columns [j0 + 128 r, +128) of
-// B (half of each operand), so every SM moves half the B bytes per output of
-// the 1-CTA kernel (64 instead of 96 B/cycle of smem+L2 operand traffic at
-// full MMA rate).  Each CTA's TMEM holds its 128 rows x 256 columns; its
-// epilogue is exactly the 1-CTA epilogue on a 128 x 256 half tile, and the
-// half tile's g2 partial lands at the index the 1-CTA enumeration gives it,
-// so k_g2_fold is shared.
+// Each MMA is M=256 x N=256 x K=32 issued by the leader CTA for the pair:
+// CTA r of the pair stages rows [i0 + 128 r, +128) of A and columns
+// [j0 + 128 r, +128) of B (half of each operand), so every SM moves half the
+// B bytes per output that a 1-CTA 128 x 256 tile would (64 instead of
+// 96 B/cycle of smem+L2 operand traffic at full MMA rate).  Each CTA's TMEM
+// holds its 128 rows x 256 columns; its epilogue works on that 128 x 256 half
+// tile, and the half tile's g2 partial lands at the index of the 128 x 256
+// half-tile enumeration (build_tiles' d_tiles), which k_g2_fold folds.
 //
 // Pair protocol: full barriers live in the leader (count 1, leader posts
 // expect_tx for both CTAs' bytes; both CTAs' TMA loads complete_tx there);
 // empty/tfull barriers in both CTAs are signalled by the leader's commits
-// multicast to the pair; the leader's tempty counts 8 arrivals (4 epilogue
-// warps per CTA; the peer arrives remotely).
+// multicast to the pair; the leader's tempty counts the epilogue warps of
+// both CTAs (the peer arrives remotely).
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -35,16 +35,12 @@ constexpr int A_BYTES = BM * BK;   // 16 KB
 constexpr int B_BYTES = 128 * BK;  // 16 KB: this CTA's half of the 256 columns
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int TMEM_COLS = 512;
-// K2 (raw, long K loop): 5 stages, 4 epilogue warps (one per TMEM lane
-// quarter).  K4 (compressed, K = 6 x 64): the MMA is short and the epilogue
-// dominates, so 4 stages and 8 epilogue warps (two per lane quarter, each
-// taking half the columns).
+// K2 (raw, long K loop) and K4 (compressed, K = 6 x 64): 5 operand stages
+// and 8 epilogue warps (two per TMEM lane quarter, each taking half the
+// columns); the epilogue is on the critical path of small-ring and K4 tiles.
 template <int MODE> struct Cfg2 {
-#ifndef XG_K2_EPI
-#define XG_K2_EPI 8
-#endif
   static constexpr int STAGES = 5;
-  static constexpr int EPI_WARPS = MODE == 0 ? XG_K2_EPI : 8;
+  static constexpr int EPI_WARPS = 8;
   static constexpr int NUM_THREADS = 128 + 32 * EPI_WARPS;
 };
 constexpr int NDIAG = BM + BN - 1;
@@ -166,6 +162,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
   }
+  // the exact int32 Gram holds every entry only while |x|^2 < 2^31 (checked
+  // here, where the raw Gram is formed, not at ingest: compressed-only series
+  // may carry brighter frames)
+  if (MODE == 0 && blockIdx.x == 0 && threadIdx.x == 0 && p.max_norm2 != nullptr &&
+      *p.max_norm2 >= (1ull << 31))
+    atomicOr(p.err, 4);
   tc_fence_before();
   cluster_sync();  // barriers of both CTAs initialised, TMEM allocated
   tc_fence_after();

@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(INGEST_THREADS + 32)
 // Per (frame, ring): norms, inverse norms, zero-frame bookkeeping.
 __global__ void k_norms(NormParams p) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int r = blockIdx.y;
+  const int r = p.ring0 + static_cast<int>(blockIdx.y);
   const int lane = threadIdx.x & 31;
   const bool valid = i < p.n_frames;
   const int64_t t = p.t0 + i;
@@ -292,7 +292,7 @@ __global__ void k_norms(NormParams p) {
       atomicMin(reinterpret_cast<long long*>(p.first_zero + r),
                 static_cast<long long>(tw + __ffs(zero) - 1));
     }
-    if (ovf) atomicOr(p.err, 4);
+    if (ovf && p.err) atomicOr(p.err, 4);  // raw streams only; K2 checks batch series
     if (p.max_norm2) atomicMax(p.max_norm2, mx);
   }
 }
@@ -316,7 +316,8 @@ cudaError_t launch_ingest(const IngestParams& p, cudaStream_t s) {
 }
 
 cudaError_t launch_norms(const NormParams& p, cudaStream_t s) {
-  dim3 grid(static_cast<unsigned>((p.n_frames + 255) / 256), p.n_rings);
+  dim3 grid(static_cast<unsigned>((p.n_frames + 255) / 256),
+            p.ring_count >= 0 ? p.ring_count : p.n_rings);
   k_norms<<<grid, 256, 0, s>>>(p);
   return cudaGetLastError();
 }

@@ -12,7 +12,7 @@
 //     y(t, j) = scale_j / |x_t| * (a0 + a1/254 + a2/254^2).
 // HBM-bound on reading X once (the MMA work per byte is small).  The epilogue
 // also writes the bf16 split planes y = b0 + b1 + b2 consumed by the
-// compressed Gram (K4, k_gram.cu MODE 1).
+// compressed Gram (K4, k_gram2.cu MODE 1).
 //
 // Tile = (ring, 128 frames, N-tile of S*kt digit rows); same warp roles and
 // mbarrier pipeline as K2.

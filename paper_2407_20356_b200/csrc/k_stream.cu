@@ -360,7 +360,7 @@ __global__ void __launch_bounds__(SI_THREADS) k_stream_ingest_sparse(StreamParam
       atomicAdd(reinterpret_cast<unsigned long long*>(p.zero_count + r), 1ull);
       atomicMin(reinterpret_cast<long long*>(p.first_zero + r), static_cast<long long>(p.t));
     }
-    if (n2 >= (1ll << 31)) atomicOr(p.err, 4);
+    if (n2 >= (1ll << 31) && p.ovf_check) atomicOr(p.err, 4);
   }
   if (threadIdx.x == 0) *p.done = 0u;
 }

@@ -577,8 +577,9 @@ int xg_series_create2(xg_ctx* c, const xg_layout* L, int64_t max_frames, int64_t
   s->tp = round_up(max_frames, 256);
   const int64_t Q = L->rings;
   cudaError_t e = cudaSuccess;
-  if ((e = dalloc(&s->d_raster, (size_t)x_frames * L->pixels)) != cudaSuccess ||
-      (e = dalloc(&s->d_x, (size_t)x_frames * L->ktot)) != cudaSuccess ||
+  // d_raster (the H2D staging raster) is allocated on the first host load:
+  // device-resident frames never need it (C4: 17 GB saved)
+  if ((e = dalloc(&s->d_x, (size_t)x_frames * L->ktot)) != cudaSuccess ||
       (e = dalloc(&s->d_norm2, (size_t)max_frames * Q)) != cudaSuccess ||
       (e = dalloc(&s->d_norms, (size_t)s->tp * Q)) != cudaSuccess ||
       (e = dalloc(&s->d_inv, (size_t)s->tp * Q)) != cudaSuccess ||
@@ -639,6 +640,25 @@ void xg_series_destroy(xg_series* s) {
 
 int64_t xg_series_frames(const xg_series* s) { return s ? s->t : -1; }
 
+// The staging raster for frames that arrive from host memory.
+static int ensure_raster(xg_series* s) {
+  if (s->d_raster) return XG_OK;
+  XG_CUDA(s->ctx, dalloc(&s->d_raster, (size_t)s->xmax * s->L->pixels));
+  return XG_OK;
+}
+
+// New frames replace the series: every result derived from the old ones
+// (raw TTC, coefficients, compressed TTC, both g2 curves) stops being valid.
+static void invalidate_results(xg_series* s) {
+  s->have_raw = false;
+  s->raw_stored = false;
+  s->raw_g2 = false;
+  s->have_y = false;
+  s->have_cttc = false;
+  s->cmp_stored = false;
+  s->cmp_g2 = false;
+}
+
 // Ingest frames [t0, t0 + n) from a device raster whose first frame is t0:
 // K1 (ring permutation + |x|^2 per (frame, ring)) and K1b (norms, 1/|x|,
 // zero-frame bookkeeping).  reset_stats() must have run for this series.
@@ -685,7 +705,7 @@ static int ingest_range(xg_series* s, const uint8_t* raster, int64_t t0, int64_t
   np.nz_bits = s->d_nz_bits;
   np.nz_words = s->nz_words;
   np.max_norm2 = reinterpret_cast<unsigned long long*>(s->d_max_norm2);
-  np.err = c->d_err;
+  np.err = nullptr;  // the int32 overflow is checked by K2, where the raw Gram is formed
   XG_CUDA(c, launch_norms(np, c->stream));
   c->launches += 2;
   return XG_OK;
@@ -713,16 +733,17 @@ int xg_series_load_frames(xg_series* s, const uint8_t* frames, int64_t n, int on
   s->x_row0 = 0;
   const uint8_t* src = frames;
   if (!on_device) {
+    if (int rc0 = ensure_raster(s)) return rc0;
     XG_CUDA(c, cudaMemcpyAsync(s->d_raster, frames, (size_t)n * L->pixels,
                                cudaMemcpyHostToDevice, c->stream));
     src = s->d_raster;
   }
   int rc = reset_stats(s, n);
   if (rc) return rc;
+  invalidate_results(s);
   rc = ingest_range(s, src, 0, n);
   if (rc) return rc;
   s->t = n;
-  s->have_raw = false;
   return XG_OK;
 }
 
@@ -791,23 +812,12 @@ static int build_tiles(xg_series* s) {
   return XG_OK;
 }
 
-// K2/K4 launch: CTA-pair kernel (default) or the 1-CTA kernel (XG_GRAM_1CTA=1).
-static bool gram_one_cta() {
-  static const bool one = [] {
-    const char* e = std::getenv("XG_GRAM_1CTA");
-    return e && e[0] == '1';
-  }();
-  return one;
-}
-
+// K2/K4 launch: the CTA-pair kernel over the pair tiles (or a J-group of them).
 static cudaError_t launch_gram_any(xg_series* s, int mode, const CUtensorMap& in,
                                    const CUtensorMap& out, GramParams gp,
                                    const TileDesc* tiles2 = nullptr, int32_t ntiles2 = -1) {
-  const bool one_cta = gram_one_cta();
   gp.g2_nbi = static_cast<int32_t>((s->t + 127) / 128);
   gp.g2_nbj = static_cast<int32_t>((s->t + 255) / 256);
-  if (one_cta) return mode == 0 ? launch_gram_u8(in, out, gp, s->ctx->num_sms, s->ctx->stream)
-                                : launch_gram_cmp(in, out, gp, s->ctx->num_sms, s->ctx->stream);
   gp.tiles = tiles2 ? tiles2 : s->d_tiles2;
   gp.ntiles = ntiles2 >= 0 ? ntiles2 : s->ntiles2;
   if (gp.ntiles == 0) return cudaSuccess;
@@ -815,8 +825,9 @@ static cudaError_t launch_gram_any(xg_series* s, int mode, const CUtensorMap& in
                    : launch_gram2_cmp(in, out, gp, s->ctx->num_sms, s->ctx->stream);
 }
 
-static int run_g2(xg_series* s, int mode) {
+static int run_g2(xg_series* s, int mode, int32_t ring0 = 0, int32_t n_rings = -1) {
   xg_ctx* c = s->ctx;
+  if (n_rings < 0) n_rings = s->L->rings - ring0;
   // <= 8 segments of >= 1024 frames: bounded partial storage, long serial chains split
   const int32_t seg = static_cast<int32_t>(std::max<int64_t>(1024, (s->t + 7) / 8));
   const int32_t nseg = static_cast<int32_t>((s->t + seg - 1) / seg);
@@ -831,20 +842,20 @@ static int run_g2(xg_series* s, int mode) {
     s->g2part_cap = need;
   }
   G2Params g;
-  g.gram = s->d_gram;
+  g.gram = s->d_gram + (int64_t)ring0 * s->tp * s->tp;
   g.cf32 = nullptr;
   g.ring_stride = s->tp * s->tp;
   g.ld = static_cast<int32_t>(s->tp);
-  g.inv = s->d_inv;
+  g.inv = s->d_inv + (int64_t)ring0 * s->tp;
   g.inv_ld = s->tp;
   g.n_frames = s->t;
-  g.n_rings = s->L->rings;
+  g.n_rings = n_rings;
   g.seg = seg;
   g.n_seg = nseg;
   g.partial = s->d_g2part;
   g.pcount = s->d_g2pcnt;
-  g.g2 = s->d_g2;
-  g.counts = s->d_g2cnt;
+  g.g2 = s->d_g2 + (int64_t)ring0 * s->tp;
+  g.counts = s->d_g2cnt + (int64_t)ring0 * s->tp;
   g.g2_ld = s->tp;
   XG_CUDA(c, launch_g2(g, mode, c->stream));
   c->launches += 2;
@@ -957,11 +968,12 @@ int xg_series_ttc_raw_host(xg_series* s, const uint8_t* frames, int64_t n, uint3
                 (long long)s->xmax);
   if (n < 2) return fail(c, XG_ERR_CONTRACT, "ttc_raw: need at least 2 frames");
   s->x_row0 = 0;
-  if ((flags & XG_STRICT) || gram_one_cta()) {  // strict needs every frame before the Gram
+  if (flags & XG_STRICT) {  // strict needs every frame before the Gram
     int rc = xg_series_load_frames(s, frames, n, 0);
     return rc ? rc : xg_ttc_raw(s, flags);
   }
   if (!c->copy_stream) XG_CUDA(c, cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+  if (int rc0 = ensure_raster(s)) return rc0;
   // ~8 chunks of whole 256-frame column blocks
   const int64_t nbj = (n + 255) / 256;
   const int64_t jb_per = std::max<int64_t>(1, (nbj + 7) / 8);
@@ -974,7 +986,7 @@ int xg_series_ttc_raw_host(xg_series* s, const uint8_t* frames, int64_t n, uint3
   int rc = reset_stats(s, n);
   if (rc) return rc;
   s->t = n;
-  s->have_raw = false;
+  invalidate_results(s);
   const bool g2 = !(flags & XG_NO_G2);
   GramParams gp;
   CUtensorMap map, omap;
@@ -1013,6 +1025,127 @@ int xg_series_g2(xg_series* s) {
   const int rc = run_g2(s, 0);
   if (!rc) s->raw_g2 = true;
   return rc;
+}
+
+// ------------------------------------------------ split rings
+// A ring whose pixels are spread over several processes: each holds the
+// exact int32 Gram and |x_t|^2 of its share (both sums over pixels,
+// linalg.cpp:127-156), exported as the packed upper pair tiles + a norm^2
+// column, summed by the caller (integer sum: exact and order-free), and the
+// total imported back into one process's series, which then refreshes the
+// ring's norms, zero-frame bookkeeping and g2 (standalone pass over the
+// stored Gram: the fused epilogue saw only the partial).
+int64_t xg_series_partial_elems(const xg_series* s) {
+  if (!s || s->t < 1) return -1;
+  const int64_t nb = (s->t + 255) / 256;
+  return nb * (nb + 1) / 2 * 65536;
+}
+
+static int partial_check(xg_series* s, int32_t ring, const char* what) {
+  xg_ctx* c = s->ctx;
+  if (ring < 0 || ring >= s->L->rings) return fail(c, XG_ERR_SHAPE, "ring %d out of range", ring);
+  if (!s->have_raw || !s->raw_stored)
+    return fail(c, XG_ERR_CONTRACT, "%s: needs a stored raw TTC (ttc_raw without XG_NO_STORE)",
+                what);
+  return XG_OK;
+}
+
+int xg_series_export_partial(xg_series* s, int32_t ring, int32_t* gram, int64_t* norm2,
+                             int on_device) {
+  if (!s || !gram || !norm2) return XG_ERR_INVALID;
+  xg_ctx* c = s->ctx;
+  int rc = partial_check(s, ring, "export_partial");
+  if (rc) return rc;
+  const int64_t elems = xg_series_partial_elems(s);
+  const int32_t nb = static_cast<int32_t>((s->t + 255) / 256);
+  int32_t* slab = s->d_gram + (int64_t)ring * s->tp * s->tp;
+  int32_t* dst = gram;
+  if (!on_device) XG_CUDA(c, dalloc(&dst, (size_t)elems));
+  cudaError_t e = launch_tiles_copy(slab, s->tp, nb, dst, 0, c->stream);
+  if (e == cudaSuccess && !on_device)
+    e = cudaMemcpyAsync(gram, dst, (size_t)elems * 4, cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpy2DAsync(norm2, 8, s->d_norm2 + ring, (size_t)s->L->rings * 8, 8, s->t,
+                          on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess && !on_device) e = cudaStreamSynchronize(c->stream);
+  if (!on_device) cudaFree(dst);
+  if (e != cudaSuccess) return cuda_fail(c, e, "export_partial");
+  c->launches++;
+  return on_device ? XG_OK : check_device_error(c);
+}
+
+int xg_series_import_partial(xg_series* s, int32_t ring, const int32_t* gram, const int64_t* norm2,
+                             int on_device, uint32_t flags) {
+  if (!s || !gram || !norm2) return XG_ERR_INVALID;
+  xg_ctx* c = s->ctx;
+  const xg_layout* L = s->L;
+  int rc = partial_check(s, ring, "import_partial");
+  if (rc) return rc;
+  const int64_t elems = xg_series_partial_elems(s);
+  const int32_t nb = static_cast<int32_t>((s->t + 255) / 256);
+  int32_t* src = const_cast<int32_t*>(gram);
+  if (!on_device) {
+    XG_CUDA(c, dalloc(&src, (size_t)elems));
+    cudaError_t e = cudaMemcpyAsync(src, gram, (size_t)elems * 4, cudaMemcpyHostToDevice, c->stream);
+    if (e != cudaSuccess) {
+      cudaFree(src);
+      return cuda_fail(c, e, "import_partial");
+    }
+  }
+  cudaError_t e = launch_tiles_copy(s->d_gram + (int64_t)ring * s->tp * s->tp, s->tp, nb, src, 1,
+                                    c->stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpy2DAsync(s->d_norm2 + ring, (size_t)L->rings * 8, norm2, 8, 8, s->t,
+                          on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->stream);
+  // the ring's frame statistics are rebuilt from the summed |x|^2
+  if (e == cudaSuccess) e = cudaMemsetAsync(s->d_zero + ring, 0, 8, c->stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(s->d_first_zero + ring, 0x7F, 8, c->stream);
+  if (e == cudaSuccess)
+    e = cudaMemsetAsync(s->d_nz_bits + (int64_t)ring * s->nz_words, 0, (size_t)s->nz_words * 4,
+                        c->stream);
+  if (e == cudaSuccess) {
+    NormParams np;
+    np.t0 = 0;
+    np.norm2 = s->d_norm2;
+    np.n_frames = s->t;
+    np.ld = s->tp;
+    np.n_rings = L->rings;
+    np.norms = s->d_norms;
+    np.inv = s->d_inv;
+    np.inv2 = s->d_inv2;
+    np.zero_count = s->d_zero;
+    np.first_zero = s->d_first_zero;
+    np.nz_bits = s->d_nz_bits;
+    np.nz_words = s->nz_words;
+    np.max_norm2 = reinterpret_cast<unsigned long long*>(s->d_max_norm2);
+    np.err = c->d_err;  // the summed ring forms a raw Gram: |x|^2 < 2^31 required
+    np.ring0 = ring;
+    np.ring_count = 1;
+    e = launch_norms(np, c->stream);
+  }
+  if (!on_device) {
+    const cudaError_t e2 = cudaStreamSynchronize(c->stream);
+    cudaFree(src);
+    if (e == cudaSuccess) e = e2;
+  }
+  if (e != cudaSuccess) return cuda_fail(c, e, "import_partial");
+  c->launches += 2;
+  if (flags & XG_STRICT) {
+    int64_t fz = 0;
+    XG_CUDA(c, cudaMemcpyAsync(&fz, s->d_first_zero + ring, 8, cudaMemcpyDeviceToHost, c->stream));
+    XG_CUDA(c, cudaStreamSynchronize(c->stream));
+    if (fz != kNoZero) {
+      c->payload = fz;
+      c->payload_ring = ring;
+      return fail(c, XG_ERR_NORMALIZATION, "row_normalize: frame %lld of ring %d has zero norm",
+                  (long long)fz, ring);
+    }
+  }
+  if (!(flags & XG_NO_G2)) {
+    rc = run_g2(s, 0, ring, 1);
+    if (rc) return rc;
+  }
+  return XG_OK;
 }
 
 // Deviation report of the homomorphic path (north star; ttc_rel_error,
@@ -1106,6 +1239,20 @@ int xg_series_get_g2(xg_series* s, int32_t ring, double* values, int64_t* counts
                                cudaMemcpyDeviceToHost, c->stream));
   XG_CUDA(c, cudaStreamSynchronize(c->stream));
   return check_device_error(c);
+}
+
+// Device pointers of the g2 curves (borrowed; valid until the series is
+// recomputed or destroyed): collectives gather them without a host trip.
+int xg_series_g2_device(xg_series* s, int32_t which, const double** values,
+                        const int64_t** counts, int64_t* ld) {
+  if (!s || !values || !counts || !ld) return XG_ERR_INVALID;
+  xg_ctx* c = s->ctx;
+  if (which == 0 ? !(s->have_raw && s->raw_g2) : !(s->have_cttc && s->cmp_g2))
+    return fail(c, XG_ERR_CONTRACT, "g2_device: no current %s g2", which == 0 ? "raw" : "compressed");
+  *values = which == 0 ? s->d_g2 : s->d_cg2;
+  *counts = which == 0 ? s->d_g2cnt : s->d_cg2cnt;
+  *ld = s->tp;
+  return XG_OK;
 }
 
 // g2 of every ring in one transfer: values[r * n + d], counts likewise.
@@ -1751,6 +1898,7 @@ int xg_series_compress_chunk(xg_series* s, const xg_basis* Bc, const uint8_t* fr
                 (long long)(t0 + n), (long long)s->tmax);
   const uint8_t* src = frames;
   if (!on_device) {
+    if (int rc0 = ensure_raster(s)) return rc0;
     XG_CUDA(c, cudaMemcpyAsync(s->d_raster, frames, (size_t)n * L->pixels,
                                cudaMemcpyHostToDevice, c->stream));
     src = s->d_raster;
@@ -1758,8 +1906,15 @@ int xg_series_compress_chunk(xg_series* s, const xg_basis* Bc, const uint8_t* fr
   if (t0 == 0) {
     rc = reset_stats(s, s->tmax);
     if (rc) return rc;
-    s->have_raw = false;
+    invalidate_results(s);
   }
+  // a chunk grows the series past any raw TTC and replaces the compressed one
+  s->have_raw = false;
+  s->raw_stored = false;
+  s->raw_g2 = false;
+  s->have_cttc = false;
+  s->cmp_stored = false;
+  s->cmp_g2 = false;
   s->x_row0 = t0;
   rc = ingest_range(s, src, t0, n);
   if (rc) return rc;
@@ -2294,6 +2449,7 @@ int xg_stream_push(xg_stream* s, const uint8_t* frame, int on_device) {
   sp.nz_bits = s->d_nz_bits;
   sp.nz_words = static_cast<int32_t>(s->tp / 32);
   sp.err = c->d_err;
+  sp.ovf_check = (s->flags & XG_STREAM_NO_RAW) ? 0 : 1;
   sp.done = s->d_done;
   const bool sparse = (s->flags & XG_STREAM_SPARSE) != 0;
   if (sparse)  // its last CTA also finishes the frame's norms
@@ -2314,7 +2470,7 @@ int xg_stream_push(xg_stream* s, const uint8_t* frame, int on_device) {
   np.nz_bits = s->d_nz_bits;
   np.nz_words = static_cast<int32_t>(s->tp / 32);
   np.max_norm2 = nullptr;
-  np.err = c->d_err;
+  np.err = (s->flags & XG_STREAM_NO_RAW) ? nullptr : c->d_err;  // int32 columns formed
   if (!sparse) XG_CUDA(c, launch_norms(np, c->stream));
   c->launches += sparse ? 1 : 2;
   const bool raw = !(s->flags & XG_STREAM_NO_RAW);
@@ -2396,6 +2552,20 @@ static int write_xcmp_rows(xg_ctx* c, const double* d_y, const double* d_norms, 
     XG_CUDA(c, cudaMemcpyAsync(nr.data(), d_norms + (int64_t)ring * tp + t0, (size_t)n * 8,
                                cudaMemcpyDeviceToHost, c->stream));
     XG_CUDA(c, cudaStreamSynchronize(c->stream));
+  }
+  // Device rows come from the 3-digit int8 basis (|dV| <= 3e-8 max|V|): a
+  // row of a frame inside the basis span may land a few 1e-9 above unit norm,
+  // which the reference's append (model.cpp:184-193) would reject on read.
+  // Such rows are rescaled to unit norm (the projection of a unit row has
+  // norm <= 1 exactly); anything further above 1 is a real contract error.
+  for (int64_t i = 0; i < n; ++i) {
+    double* row = y.data() + (size_t)i * k;
+    double sq = 0.0;
+    for (int64_t j = 0; j < k; ++j) sq += row[j] * row[j];
+    if (sq > (1.0 + 1e-10) * (1.0 + 1e-10) && sq <= (1.0 + 1e-6) * (1.0 + 1e-6)) {
+      const double inv = 1.0 / std::sqrt(sq);
+      for (int64_t j = 0; j < k; ++j) row[j] *= inv;
+    }
   }
   const int rc = xg_io_write_xcmp(path, k, hash, n, nr.data(), y.data(), append);
   if (rc == XG_OK) return check_device_error(c);

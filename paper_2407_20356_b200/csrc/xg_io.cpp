@@ -98,10 +98,24 @@ XG_API int xg_io_write_xcmp(const char* path, int64_t k, uint64_t hash, int64_t 
                             const double* norms, const double* coeffs, int32_t append) {
   if (!path || n < 0 || (n > 0 && (!norms || !coeffs))) return XG_ERR_INVALID;
   if (k < 1) return io_fail(XG_ERR_CONTRACT, -1, "appender needs k >= 1");
-  for (int64_t i = 0; i < n; ++i)  // CompressedSeries::append (model.cpp:177-193)
+  for (int64_t i = 0; i < n; ++i) {  // CompressedSeries::append (model.cpp:177-193)
     if (!(norms[i] > 0.0) || !std::isfinite(norms[i]))
       return io_fail(XG_ERR_NORMALIZATION, i, "store row %lld: frame norm must be positive and finite",
                      (long long)i);
+    double sq = 0.0;
+    for (int64_t j = 0; j < k; ++j) {
+      const double v = coeffs[i * k + j];
+      if (!std::isfinite(v))
+        return io_fail(XG_ERR_CONTRACT, i, "store row %lld: non-finite coefficient", (long long)i);
+      sq += v * v;
+    }
+    // the reader rebuilds the store through append(), which rejects rows
+    // above unit norm: such a file could never be read back
+    if (sq > (1.0 + 1e-10) * (1.0 + 1e-10))
+      return io_fail(XG_ERR_CONTRACT, i,
+                     "store row %lld: coefficient row norm %.17g exceeds 1 (not a projection "
+                     "of a unit row)", (long long)i, std::sqrt(sq));
+  }
   uint64_t n_old = 0;
   std::vector<uint8_t> head;
   File fh;

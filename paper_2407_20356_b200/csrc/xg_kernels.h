@@ -83,7 +83,9 @@ struct NormParams {
   uint32_t* nz_bits;         // [ring][nz_words] nonzero-frame bitmask (pre-zeroed)
   int32_t nz_words;
   unsigned long long* max_norm2;  // running max of |x|^2 (or null)
-  int* err;                  // bit 2: overflow
+  int* err;                  // bit 2: overflow (null: not checked here)
+  int32_t ring0 = 0;         // first ring processed (split-ring import: one ring)
+  int32_t ring_count = -1;   // rings processed (-1: all n_rings)
 };
 cudaError_t launch_norms(const NormParams& p, cudaStream_t s);
 
@@ -111,7 +113,7 @@ struct GramParams {
   int64_t n_frames;
   float2* g2_partial;        // [ntiles][384] (hi, lo) double-float diagonal sums
   int32_t store;             // 0: g2 only, the TTC tiles are not written
-  // compressed mode (launch_gram_cmp): K blocks run over precision pairs
+  // compressed mode (launch_gram2_cmp): K blocks run over precision pairs
   // (plane_a, plane_b) packed 4 bits each in `pairs`, kb_per_plane 64-element
   // blocks per plane; plane rows of ring r, plane s start at (3r+s)*plane_rows
   int32_t n_pairs;
@@ -130,9 +132,6 @@ cudaError_t launch_gram2_u8(const CUtensorMap& tmX, const CUtensorMap& tmOut, co
                             int num_sms, cudaStream_t stream);
 cudaError_t launch_gram2_cmp(const CUtensorMap& tmY, const CUtensorMap& tmOut, const GramParams& p,
                              int num_sms, cudaStream_t stream);
-size_t gram_u8_smem_bytes();
-cudaError_t launch_gram_cmp(const CUtensorMap& tmY, const CUtensorMap& tmOut, const GramParams& p,
-                            int num_sms, cudaStream_t stream);
 
 // Fold the per-tile diagonal sums of K2 into g2[ring][d] (fixed order) and
 // count the valid (t, t+d) pairs from the nonzero-frame bitmask.
@@ -151,10 +150,6 @@ struct G2FoldParams {
   int64_t g2_ld;
 };
 cudaError_t launch_g2_fold(const G2FoldParams& p, cudaStream_t s);
-// tmOut: 32-bit 2D map over the output, cols = ld, rows = rings * ld, box 32 x 32,
-// 128-byte swizzle (the epilogue TMA-stores 32 x 32 chunks)
-cudaError_t launch_gram_u8(const CUtensorMap& tmX, const CUtensorMap& tmOut, const GramParams& p,
-                           int num_sms, cudaStream_t stream);
 
 // ------------------------------------------------------ K3 projection
 #ifdef __CUDACC__
@@ -246,6 +241,7 @@ struct StreamParams {
   uint32_t* nz_bits;         // [ring][nz_words]
   int32_t nz_words;
   int* err;
+  int32_t ovf_check;         // raw columns formed: |x|^2 >= 2^31 sets err bit 2
   unsigned int* done;        // CTA counter (zero on entry, reset by the last CTA)
 };
 // One-frame ingest for the streaming path: ring-major row t of the history,
@@ -298,6 +294,12 @@ struct G2Params {
   int64_t g2_ld;
 };
 cudaError_t launch_g2(const G2Params& p, int mode, cudaStream_t s);
+
+// Split-ring exchange format: the upper 256 x 256 pair tiles (I <= J) of one
+// ring's Gram slab, packed in (I, J) row-major tile order, tile rows
+// row-major.  dir 0: slab -> packed, 1: packed -> slab.
+cudaError_t launch_tiles_copy(int32_t* slab, int64_t ld, int32_t nb, int32_t* packed, int dir,
+                              cudaStream_t s);
 
 // ---------------------------------------------------- TTC readback expand
 struct ExpandParams {

@@ -1,0 +1,143 @@
+"""Parity at the BASELINE configuration sizes (BASELINE.json configs[0..2],
+SURVEY 8(d)), not only at toy sizes.
+
+  * C1 in full (T=1000, 128x128, Q=8, mu=0.1): every ring's int32 Gram is
+    bitwise xpcs::gram(counts); C within 1e-12 of the UNMODIFIED reference's
+    ttc_raw; g2 within 1e-12 of its g2_from_ttc; norms bitwise.  Rank k=32
+    compressed path with the reference's own build_online_from_frames V
+    (first 256 frames): C~ within 1e-5 max|C~_ref| of the reference's
+    ttc_compressed(compress_series(...)), and the deviation report equal to
+    the reference's ttc_rel_error.
+    Pins: acceptance_main.cpp:176-200 (raw vs naive, 1e-12),
+    test_correlate.cpp:31-46.
+  * C2 geometry at full T=4096 (512x512, Q=32, mu=0.05; the 1 GB of frames
+    generated on the device and downloaded for the checker): the exact Gram
+    of the smallest, a mid-size, the corner and the LARGEST ring (17,224 px:
+    every K block of K2's tile schedule with 16 column blocks) bitwise; C and
+    g2 of the small rings against the reference (f64 ttc_raw at T=4096).
+  * C3 geometry streamed (1024x1024, Q=64, mu=0.02, k=128) to depth 4352:
+    sampled rings' exact streamed Gram columns bitwise, raw g2 within 1e-12
+    of the reference; streamed coefficients / C~ against the reference's
+    compress_series + ttc_compressed on the SAME V (device-built basis read
+    back), within 1e-5.  Pins: acceptance_main.cpp:329-353 (stream == batch),
+    test_correlate.cpp:138-157.
+"""
+import numpy as np
+import pytest
+
+import paper_2407_20356_b200 as xg
+
+pytestmark = pytest.mark.gpu
+
+
+def _exact_gram(x_u8):
+    # counts: every partial sum < 2^53, so the f64 BLAS product is exact in
+    # any order (SURVEY finding 3) -- an independent exact checker
+    x = x_u8.astype(np.float64)
+    return (x @ x.T).astype(np.int64)
+
+
+def test_c1_full_raw_and_k32(ctx, orc, ref):
+    t, h, w, q, mu, k = 1000, 128, 128, 8, 0.1, 32
+    frames = orc.gen_speckle(t, h, w, q, mu, 1)
+    ring, _ = orc.ring_map(h, w, q)
+    lay = xg.RingLayout.from_ring_map(ctx, ring, q)
+    s = xg.FrameSeries(lay, t).load(frames).ttc_raw()
+    basis = xg.Basis(lay, k)
+    vs = []
+    for r in range(q):
+        xq = frames[:, ring == r]
+        xf = xq.astype(np.float64)
+        assert np.array_equal(s.ttc(r, "gram").astype(np.int64), orc.gram_u8(xq)), r
+        c_ref = ref.ttc_raw(xf)
+        c = s.ttc(r, "f64")
+        assert np.abs(c - c_ref).max() <= 1e-12, r
+        _, g2_ref, cnt_ref = ref.g2_from_ttc(c_ref)
+        _, g2, cnt = s.g2(r)
+        assert np.array_equal(cnt, cnt_ref)
+        assert np.abs(g2 - g2_ref).max() <= 1e-12, r
+        nrm, nz = s.norms(r)
+        assert nz == 0 and np.array_equal(nrm, np.sqrt((xf * xf).sum(1)))
+        v, _ = ref.build_online_from_frames(xf[:256], k)
+        vs.append(v)
+        basis.set_ring(r, v)
+    s.compress(basis).ttc_compressed()
+    rel = s.rel_error()
+    for r in range(q):
+        xf = frames[:, ring == r].astype(np.float64)
+        y_ref, n_ref = ref.compress_series(xf, vs[r])
+        y, nr = s.coeffs(r)
+        assert np.abs(y - y_ref).max() <= 1e-6 * np.abs(y_ref).max(), r
+        assert np.array_equal(nr, n_ref)
+        cc_ref = ref.ttc_compressed(y_ref)[0]
+        cc = s.cttc(r)
+        scale = np.abs(cc_ref).max()
+        assert np.abs(cc - cc_ref).max() <= 1e-5 * scale, r
+        _, cg2_ref, _ = ref.g2_from_ttc(cc_ref)
+        _, cg2, _ = s.cg2(r)
+        assert np.abs(cg2 - cg2_ref).max() <= 1e-5 * scale, r
+        rel_ref = ref.ttc_rel_error(ref.ttc_raw(xf), cc_ref)
+        assert abs(rel[r] - rel_ref) <= 1e-5 * max(rel_ref, 1e-3), (r, rel[r], rel_ref)
+
+
+def test_c2_full_T_rings(ctx, orc, ref):
+    import torch
+
+    t, h, w, q, mu = 4096, 512, 512, 32, 0.05
+    dev = torch.empty((t, h * w), dtype=torch.uint8, device="cuda")
+    xg.synth_speckle(ctx, dev.data_ptr(), t, h, w, q, mu, 2)
+    ring = xg.annular_rings(h, w, q)
+    lay = xg.RingLayout.from_ring_map(ctx, ring, q)
+    s = xg.FrameSeries(lay, t).load(dev).ttc_raw()
+    host = dev.cpu().numpy()
+    for r in (0, 31, 3, 22):  # 392, 592, 2800, 17224 px
+        xq = np.ascontiguousarray(host[:, ring == r])
+        g = s.ttc(r, "gram").astype(np.int64)
+        assert np.array_equal(g, _exact_gram(xq)), r
+        if r in (0, 31):
+            xf = xq.astype(np.float64)
+            assert np.array_equal(g[:300, :300], orc.gram_u8(xq[:300]))
+            c_ref = ref.ttc_raw(xf)
+            assert np.abs(s.ttc(r, "f64") - c_ref).max() <= 1e-12, r
+            _, g2_ref, cnt_ref = ref.g2_from_ttc(c_ref)
+            _, g2, cnt = s.g2(r)
+            assert np.array_equal(cnt, cnt_ref)
+            assert np.abs(g2 - g2_ref).max() <= 1e-12, r
+
+
+def test_c3_stream_to_depth_4352(ctx, orc, ref):
+    import torch
+
+    h = w = 1024
+    q, mu, k, depth = 64, 0.02, 128, 4352
+    dev = torch.empty((depth, h * w), dtype=torch.uint8, device="cuda")
+    xg.synth_speckle(ctx, dev.data_ptr(), depth, h, w, q, mu, 3)
+    ring = xg.annular_rings(h, w, q)
+    lay = xg.RingLayout.from_ring_map(ctx, ring, q)
+    basis = xg.Basis(lay, k)
+    vs, _, _ = xg.FrameSeries(lay, 256).load(dev[:256]).build_basis(k, basis=basis)
+    st = xg.FrameStream(lay, depth, basis=basis, store_ttc=True, sparse=True)
+    for i in range(depth):
+        st.push(dev[i])
+    assert st.n_frames == depth
+    host = dev.cpu().numpy()
+    for r in (0, 63, 40):  # 392, 592, ~33k px
+        xq = np.ascontiguousarray(host[:, ring == r])
+        xf = xq.astype(np.float64)
+        g = st.ttc(r, dtype="gram").astype(np.int64)
+        assert np.array_equal(g, _exact_gram(xq)), r
+        if r in (0, 63):
+            nz = np.count_nonzero(xq.sum(1) == 0)
+            if nz == 0:  # the reference raises on a zero frame; compare only if none
+                c_ref = ref.ttc_raw(xf)
+                _, g2_ref, _ = ref.g2_from_ttc(c_ref)
+                _, g2, _ = st.g2(r)
+                assert np.abs(g2 - g2_ref).max() <= 1e-12, r
+        keep = xq.sum(1) > 0  # compress_series raises on zero frames: check the others
+        y_ref, n_ref = ref.compress_series(xf[keep], vs[r])
+        y, nr = st.coeffs(r)
+        assert np.abs(y[keep] - y_ref).max() <= 1e-6 * np.abs(y_ref).max(), r
+        assert np.array_equal(nr[keep], n_ref)
+        cc_ref = ref.ttc_compressed(y_ref)[0]
+        cc = st.ttc(r, compressed=True)[np.ix_(keep, keep)]
+        assert np.abs(cc - cc_ref).max() <= 1e-5 * np.abs(cc_ref).max(), r

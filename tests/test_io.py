@@ -49,6 +49,24 @@ def test_xcmp_appender_semantics(tmp_path, ref):
     assert e.value.frame_index == 2
 
 
+def test_xcmp_writer_enforces_append_contract(tmp_path, ref):
+    """Rows the reference reader's append() would reject (model.cpp:184-193:
+    non-finite, or above unit norm) are refused at write time."""
+    y, nr = _rows(4, 3, 5)
+    bad = y.copy()
+    bad[2] *= 1.0 / np.linalg.norm(bad[2]) * 1.001
+    with pytest.raises(xg.ContractError):
+        xg.write_xcmp(tmp_path / "n.xcmp", bad, nr, 1)
+    bad = y.copy()
+    bad[1, 0] = np.nan
+    with pytest.raises(xg.ContractError):
+        xg.write_xcmp(tmp_path / "f.xcmp", bad, nr, 1)
+    edge = y.copy()
+    edge[0] /= np.linalg.norm(edge[0])  # exactly unit norm is accepted
+    xg.write_xcmp(tmp_path / "u.xcmp", edge, nr, 1)
+    assert np.array_equal(ref.read_compressed(tmp_path / "u.xcmp")[2], edge)
+
+
 @pytest.mark.parametrize("dtype", [0, 1, 2])
 def test_xfsr_reference_files_read_as_counts(tmp_path, ref, dtype):
     rng = np.random.default_rng(dtype)
