@@ -466,6 +466,9 @@ def run_headline(E, line):
         host.copy_(frames)
         nring = len(sh.rings)
 
+        owned_li = [li for li, r in enumerate(sh.rings) if sh.plan.owner[r] == E.rank]
+        ttc_host = torch.empty((len(owned_li), T, T), dtype=torch.int32, pin_memory=True)
+
         def step_e2e(ttc_out=None):
             series.ttc_raw_host(host)  # pinned H2D in chunks, overlapped with ingest + Gram
             if E.world > 1:
@@ -475,9 +478,8 @@ def run_headline(E, line):
             else:
                 series.g2_all()  # D2H of every ring's g2 values + counts
             if ttc_out is not None:  # the TTC itself: every owned ring's exact int32 Gram
-                for li, r in enumerate(sh.rings):
-                    if sh.plan.owner[r] == E.rank:
-                        ttc_out.append(series.ttc(li, "gram"))
+                for j, li in enumerate(owned_li):
+                    series.ttc(li, "gram", out=ttc_out[j])
 
         for _ in range(2):
             step_e2e()
@@ -493,9 +495,7 @@ def run_headline(E, line):
         n_ttc = 3
         t0 = time.perf_counter()
         for _ in range(n_ttc):
-            out = []
-            step_e2e(out)
-            del out
+            step_e2e(ttc_host)
         E.sync()
         ttc_s = E.max_over_ranks((time.perf_counter() - t0) / n_ttc)
         g2_bytes = cfg["Q"] * T * 16
@@ -510,8 +510,8 @@ def run_headline(E, line):
                     "h2d_bytes_per_step": T * cfg["H"] * cfg["W"],
                     "d2h_bytes_per_step": g2_bytes + ttc_bytes,
                     "what": "same + every ring's TTC (the exact int32 Gram, full symmetric "
-                            "T x T) read back to host memory, as ttc_raw returns it"}}
-        del host
+                            "T x T) read back into pinned host memory, as ttc_raw returns it"}}
+        del host, ttc_host
     else:
         line["e2e"] = {"skipped": "--no-e2e (profiling run)"}
     # ---------------------------------------------------------------- roofline
@@ -767,6 +767,9 @@ def run_c5(E):
         else:
             chunk = sh.frames(E, T=n, seed=seed)
         for k in ks:
+            if j == 0:  # untimed warm-up: the basis' one-time digit upload and tile lists
+                series[k].compress_chunk(bases[k], chunk, first=True)
+                E.sync()
             a, b = E.ev(), E.ev()
             a.record(E.stream)
             series[k].compress_chunk(bases[k], chunk, first=(j == 0))
@@ -780,7 +783,7 @@ def run_c5(E):
            "parallelism": sh.describe(E), "by_k": {}}
     hbm = E.peaks["hbm_gbs"]
     for k in ks:
-        s = series[k]
+        s = series.pop(k)  # one k at a time: the g2 tile partials of T=65536 are 26 GB
         E.sync()
         s.ttc_compressed(store=False)  # warm
         E.sync()
@@ -808,6 +811,8 @@ def run_c5(E):
                                    "frac": ingest_bytes / tc / 1e9 / hbm,
                                    "note": "K1 reads the raster + writes the ring-major copy, K3 "
                                            "re-reads it (3 B per pixel per frame)"}}
+        del s
+        E.free()
     del series, bases
     E.free()
     return out

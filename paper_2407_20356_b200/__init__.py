@@ -286,9 +286,10 @@ class RingLayout:
 
     @classmethod
     def from_ring_map(cls, ctx: Context, ring_of_pixel: np.ndarray, n_rings: int):
-        ring_of_pixel = np.asarray(ring_of_pixel).ravel()
-        masks = [np.nonzero(ring_of_pixel == r)[0] for r in range(n_rings)]
-        return cls(ctx, ring_of_pixel.size, masks)
+        """Masks from a per-pixel ring index (-1 = no ring)."""
+        rp = np.asarray(ring_of_pixel).ravel()
+        masks = [np.nonzero(rp == r)[0] for r in range(n_rings)]
+        return cls(ctx, rp.size, masks)
 
     @property
     def n_rings(self) -> int:
@@ -522,11 +523,26 @@ class FrameSeries:
         _check(self.ctx.h, lib.xg_series_g2(self.h))
         return self
 
-    def ttc(self, ring: int, dtype: str = "f64") -> np.ndarray:
+    def ttc(self, ring: int, dtype: str = "f64", out=None):
+        """Full symmetric n x n TTC of one ring: "f64" C, "f32", or the exact
+        int32 "gram".  ``out``: an optional preallocated n x n destination (a
+        numpy array, or a torch tensor -- pinned host memory reads back at
+        PCIe speed, a CUDA tensor is filled on the device)."""
         code = {"f64": _abi.F64, "f32": _abi.F32, "gram": _abi.I32_GRAM}[dtype]
         n = self.n_frames
         npd = {"f64": np.float64, "f32": np.float32, "gram": np.int32}[dtype]
-        out = np.empty((n, n), npd)
+        if out is None:
+            out = np.empty((n, n), npd)
+        if hasattr(out, "data_ptr"):
+            tdt = {"f64": "torch.float64", "f32": "torch.float32", "gram": "torch.int32"}[dtype]
+            if str(out.dtype) != tdt or not out.is_contiguous() or out.numel() != n * n:
+                raise ShapeError(f"ttc out must be a contiguous {n} x {n} {tdt} tensor")
+            on_dev = 1 if getattr(out, "is_cuda", False) else 0
+            _check(self.ctx.h, lib.xg_series_get_ttc(self.h, ring, code, C.c_void_p(out.data_ptr()),
+                                                     n, on_dev))
+            return out
+        if out.dtype != npd or out.shape != (n, n) or not out.flags.c_contiguous:
+            raise ShapeError(f"ttc out must be a contiguous {n} x {n} {np.dtype(npd)} array")
         _check(self.ctx.h, lib.xg_series_get_ttc(self.h, ring, code, _ptr(out), n, 0))
         return out
 

@@ -177,7 +177,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
     if (elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = pair; t < p.ntiles; t += npairs) {
+      int wave = 0;
+      for (int t = pair; t < p.ntiles; t += npairs, ++wave) {
+        if (MODE == 0 && leader && p.wave_ctr) {
+          // wave gate: every pair has started wave - gate_lag (bounded wait)
+          const unsigned need = static_cast<unsigned>((wave - p.gate_lag + 1) * npairs);
+          if (wave >= p.gate_lag) {
+            uint32_t spins = 0;
+            while (ld_acquire_u32(p.wave_ctr) < need) {
+              __nanosleep(64);
+              if (++spins == (1u << 26)) {
+                atomicExch(p.err, 1);
+                goto producer_done;
+              }
+            }
+          }
+          atomicAdd(p.wave_ctr, 1u);
+        }
         const TileDesc td = p.tiles[t];
         const int koff = MODE == 0 ? p.ring_koff[td.ring] : 0;
         // K4: per 64-coefficient block, one stage per bf16 plane (A and B

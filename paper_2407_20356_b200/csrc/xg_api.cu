@@ -52,6 +52,8 @@ struct xg_ctx {
   PFN_encodeTiled encode = nullptr;
   cudaStream_t copy_stream = nullptr;    // host -> device copies overlapped with compute
   std::vector<cudaEvent_t> events;       // chunk-arrival events (reused)
+  void* scratch = nullptr;               // readback staging (grown, reused: no malloc/free
+  size_t scratch_cap = 0;                // per call, so pinned readbacks run at PCIe speed)
 };
 
 struct xg_layout {
@@ -127,6 +129,7 @@ struct xg_series {
   TileDesc* d_ptiles = nullptr;    // projection tiles
   int32_t n_ptiles = 0;
   int64_t ptiles_key = -1;
+  unsigned int* d_wave = nullptr;  // K2 wave-gate counter (zeroed before each launch)
 };
 
 struct xg_basis {
@@ -241,6 +244,23 @@ int make_map_u8(xg_ctx* c, CUtensorMap* map, const void* base, int64_t cols, int
   return XG_OK;
 }
 
+// The context's readback staging buffer, at least `bytes` large.
+cudaError_t ctx_scratch(xg_ctx* c, size_t bytes, void** out) {
+  if (bytes > c->scratch_cap) {
+    if (c->scratch) {
+      cudaStreamSynchronize(c->stream);
+      cudaFree(c->scratch);
+      c->scratch = nullptr;
+      c->scratch_cap = 0;
+    }
+    const cudaError_t e = cudaMalloc(&c->scratch, bytes);
+    if (e != cudaSuccess) return e;
+    c->scratch_cap = bytes;
+  }
+  *out = c->scratch;
+  return cudaSuccess;
+}
+
 // Device error word: bit0 pipeline timeout, bit2 int32 Gram overflow.
 int check_device_error(xg_ctx* c) {
   int h = 0;
@@ -308,6 +328,7 @@ void xg_ctx_destroy(xg_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->d_err) cudaFree(c->d_err);
+  if (c->scratch) cudaFree(c->scratch);
   if (c->own_stream) cudaStreamDestroy(c->stream);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   for (cudaEvent_t ev : c->events) cudaEventDestroy(ev);
@@ -331,8 +352,8 @@ int xg_synchronize(xg_ctx* c) {
 int64_t xg_kernel_launches(const xg_ctx* c) { return c ? c->launches : -1; }
 
 // ------------------------------------------------------------------ layout
-int xg_layout_create(xg_ctx* c, int64_t full_pixels, int32_t n_rings,
-                     const int64_t* offsets, const int64_t* indices, xg_layout** out) {
+int xg_layout_create(xg_ctx* c, int64_t full_pixels, int32_t n_rings, const int64_t* offsets,
+                     const int64_t* indices, xg_layout** out) {
   if (!c || !out || !offsets || !indices) return XG_ERR_INVALID;
   *out = nullptr;
   if (full_pixels < 1) return fail(c, XG_ERR_CONTRACT, "layout: full_pixels must be >= 1");
@@ -354,16 +375,34 @@ int xg_layout_create(xg_ctx* c, int64_t full_pixels, int32_t n_rings,
   L->ctx = c;
   L->pixels = full_pixels;
   L->rings = n_rings;
-  // 16384-pixel bands: a consumer pass moves twice the bytes of an 8192
+  // 16384-pixel row strips: a consumer pass moves twice the bytes of an 8192
   // band for the same bookkeeping (measured: K1 0.475 -> 0.441 ms at C2;
-  // 4096 and >= 24576 are slower: fewer passes vs fewer CTAs per SM)
+  // 4096 and >= 24576 are slower: fewer passes vs fewer CTAs per SM).  128 x
+  // 128-pixel 2D blocks were tried and are slower (C2 0.40 -> 0.90 ms, C5
+  // 8.8 -> 10.8 ms per 4096 frames): an annulus crosses a square block in
+  // short row runs, so far fewer of its pixels form whole aligned words.
   L->band = static_cast<int32_t>(std::min<int64_t>(16384, round_up(full_pixels, 16)));
   L->n_bands = static_cast<int32_t>((full_pixels + L->band - 1) / L->band);
   const int32_t nb = L->n_bands;
-  // count[r][b] pixels of ring r in band b (indices ascending -> bands ascending)
+  auto band_of = [&](int64_t px) -> int32_t { return static_cast<int32_t>(px / L->band); };
+  auto e_of = [&](int64_t px) -> int32_t { return static_cast<int32_t>(px % L->band); };
+  auto smem_of = [&](int32_t e) -> int32_t { return ingest_smem_offset(e); };
+  // mask entries bucketed by band: ring order, ascending inside a ring
   std::vector<int64_t> cnt(static_cast<size_t>(n_rings) * nb, 0);
+  std::vector<int64_t> bstart(static_cast<size_t>(nb) + 1, 0);
   for (int32_t r = 0; r < n_rings; ++r)
-    for (int64_t i = offsets[r]; i < offsets[r + 1]; ++i) cnt[(size_t)r * nb + indices[i] / L->band]++;
+    for (int64_t i = offsets[r]; i < offsets[r + 1]; ++i) {
+      const int32_t b = band_of(indices[i]);
+      cnt[(size_t)r * nb + b]++;
+      bstart[b + 1]++;
+    }
+  for (int32_t b = 0; b < nb; ++b) bstart[b + 1] += bstart[b];
+  std::vector<int64_t> bucket(static_cast<size_t>(offsets[n_rings]));
+  {
+    std::vector<int64_t> fill(bstart.begin(), bstart.end() - 1);
+    for (int32_t r = 0; r < n_rings; ++r)
+      for (int64_t i = offsets[r]; i < offsets[r + 1]; ++i) bucket[fill[band_of(indices[i])]++] = i;
+  }
   L->ring_pixels.resize(n_rings);
   L->mask_off.assign(offsets, offsets + n_rings + 1);
   L->colpos.assign(static_cast<size_t>(offsets[n_rings]), 0);
@@ -398,25 +437,27 @@ int xg_layout_create(xg_ctx* c, int64_t full_pixels, int32_t n_rings,
   std::vector<Piece> pieces;
   constexpr int kWarps = INGEST_CONSUMERS;
   std::vector<int32_t> band_piece((size_t)nb * (kWarps + 1) + 1, 0);
-  std::vector<int64_t> cursor(static_cast<size_t>(n_rings), 0);
-  for (int32_t r = 0; r < n_rings; ++r) cursor[r] = offsets[r];
   std::vector<int64_t> pos(static_cast<size_t>(L->band), -1);  // band pixel -> mask entry
   struct Seg { int32_t ring, dst, nw, woff, nb, boff; };
   for (int32_t b = 0; b < nb; ++b) {
     band_word[b] = static_cast<int32_t>(words.size());
     band_byte[b] = static_cast<int32_t>(bytes.size() / 4);
-    const int64_t base = (int64_t)b * L->band;
     std::vector<Seg> sg;
+    int64_t cur = bstart[b];
     for (int32_t r = 0; r < n_rings; ++r) {
       const int64_t n = cnt[(size_t)r * nb + b];
       if (n == 0) continue;
-      const int64_t* ix = indices + cursor[r];
-      for (int64_t i = 0; i < n; ++i) pos[ix[i] - base] = cursor[r] + i;
+      const int64_t* ent = bucket.data() + cur;  // this ring's mask entries in the band
+      std::vector<int32_t> ex(static_cast<size_t>(n));
+      for (int64_t i = 0; i < n; ++i) {
+        ex[i] = e_of(indices[ent[i]]);
+        pos[ex[i]] = ent[i];
+      }
       std::vector<int32_t> bank_words[32], left;
       for (int64_t i = 0; i < n; ++i) {
-        const int32_t e = static_cast<int32_t>(ix[i] - base);
-        if ((e & 3) == 0 && i + 3 < n && ix[i + 3] - base == e + 3) {  // ascending => all 4 in ring
-          bank_words[(ingest_smem_offset(e) / 4) & 31].push_back(e);
+        const int32_t e = ex[i];
+        if ((e & 3) == 0 && i + 3 < n && ex[i + 3] == e + 3) {  // ascending => all 4 in ring
+          bank_words[(smem_of(e) / 4) & 31].push_back(e);
           i += 3;
         } else {
           left.push_back(e);
@@ -435,7 +476,7 @@ int xg_layout_create(xg_ctx* c, int64_t full_pixels, int32_t n_rings,
           if (next[k] == bank_words[k].size()) continue;
           const int32_t e = bank_words[k][next[k]++];
           any = true;
-          words.push_back(static_cast<uint16_t>(ingest_smem_offset(e) / 4));
+          words.push_back(static_cast<uint16_t>(smem_of(e) / 4));
           for (int j = 0; j < 4; ++j) L->colpos[pos[e + j]] = s.dst + 4 * g + j;
           ++g;
         }
@@ -444,7 +485,7 @@ int xg_layout_create(xg_ctx* c, int64_t full_pixels, int32_t n_rings,
       const size_t nl = left.size(), nlp = static_cast<size_t>(round_up((int64_t)nl, 4));
       for (size_t q = 0; q < nlp; ++q) {
         if (q < nl) {
-          bytes.push_back(static_cast<uint16_t>(ingest_smem_offset(left[q])));
+          bytes.push_back(static_cast<uint16_t>(smem_of(left[q])));
           L->colpos[pos[left[q]]] = s.dst + 4 * g + static_cast<int64_t>(q);
         } else {
           bytes.push_back(zero_at);
@@ -452,7 +493,7 @@ int xg_layout_create(xg_ctx* c, int64_t full_pixels, int32_t n_rings,
       }
       s.nb = static_cast<int32_t>(nlp / 4);
       sg.push_back(s);
-      cursor[r] += n;
+      cur += n;
     }
     // Split the band's groups over the consumer warps by estimated cost
     // (a word group ~2 shared-memory wavefronts, a byte group ~5).
@@ -635,6 +676,7 @@ void xg_series_destroy(xg_series* s) {
   dfree(s->d_spec);
   dfree(s->d_cg2cnt);
   dfree(s->d_ptiles);
+  dfree(s->d_wave);
   delete s;
 }
 
@@ -776,19 +818,28 @@ static int build_tiles(xg_series* s) {
                         cudaMemcpyHostToDevice));
   XG_CUDA(c, cudaMemcpy(s->d_ib_tile_off, iboff.data(), iboff.size() * 4, cudaMemcpyHostToDevice));
   s->ntiles = static_cast<int32_t>(tiles.size());
-  // 256 x 256 pair tiles (k_gram2): pad = 1-CTA index of the upper half tile
+  // 256 x 256 pair tiles (k_gram2): pad = 1-CTA index of the upper half tile.
+  // The persistent kernel deals consecutive tiles to the CTA pairs, so ~one
+  // wave of (SMs / 2) consecutive tiles is in flight at once.  Tiles are
+  // listed ring by ring in 8 x 8 super-tiles (row-major inside): a wave then
+  // reads ~16 row/column blocks of the ring's frames instead of ~75 column
+  // blocks, so the operands stay in L2 even when a ring's frames do not fit
+  // (C4: 172 MB per ring); the order does not change any result.
   std::vector<TileDesc> tiles2;
   const int64_t nbi2 = (s->t + 255) / 256;
+  constexpr int64_t SUPER = 8;  // C4 ncu: DRAM reads 425 GB (row-major) -> 294 GB
   for (int32_t r = 0; r < s->L->rings; ++r)
-    for (int64_t I = 0; I < nbi2; ++I)
-      for (int64_t J = I; J < nbj; ++J) {
-        TileDesc d;
-        d.ring = r;
-        d.i0 = static_cast<int32_t>(I * 256);
-        d.j0 = static_cast<int32_t>(J * 256);
-        d.pad = static_cast<int32_t>((int64_t)r * s->tiles_per_ring + iboff[2 * I] + (J - I));
-        tiles2.push_back(d);
-      }
+    for (int64_t SI = 0; SI < nbi2; SI += SUPER)
+      for (int64_t SJ = SI; SJ < nbj; SJ += SUPER)
+        for (int64_t I = SI; I < std::min(nbi2, SI + SUPER); ++I)
+          for (int64_t J = std::max(I, SJ); J < std::min(nbj, SJ + SUPER); ++J) {
+            TileDesc d;
+            d.ring = r;
+            d.i0 = static_cast<int32_t>(I * 256);
+            d.j0 = static_cast<int32_t>(J * 256);
+            d.pad = static_cast<int32_t>((int64_t)r * s->tiles_per_ring + iboff[2 * I] + (J - I));
+            tiles2.push_back(d);
+          }
   dfree(s->d_tiles2);
   XG_CUDA(c, dalloc(&s->d_tiles2, tiles2.size()));
   XG_CUDA(c, cudaMemcpy(s->d_tiles2, tiles2.data(), tiles2.size() * sizeof(TileDesc),
@@ -821,6 +872,18 @@ static cudaError_t launch_gram_any(xg_series* s, int mode, const CUtensorMap& in
   gp.tiles = tiles2 ? tiles2 : s->d_tiles2;
   gp.ntiles = ntiles2 >= 0 ? ntiles2 : s->ntiles2;
   if (gp.ntiles == 0) return cudaSuccess;
+  if (gp.wave_ctr) {
+    // the wave gate pays where a ring's frames overflow L2 (C4: 172 MB per
+    // ring, 109.6 -> 105.5 ms); where they fit (C2: 33 MB) it only costs
+    const double ring_bytes = (double)s->t * (double)s->L->ktot / std::max(1, s->L->rings);
+    if (ring_bytes <= 64e6) {
+      gp.wave_ctr = nullptr;
+    } else {
+      gp.gate_lag = 2;
+      const cudaError_t e = cudaMemsetAsync(gp.wave_ctr, 0, sizeof(unsigned int), s->ctx->stream);
+      if (e != cudaSuccess) return e;
+    }
+  }
   return mode == 0 ? launch_gram2_u8(in, out, gp, s->ctx->num_sms, s->ctx->stream)
                    : launch_gram2_cmp(in, out, gp, s->ctx->num_sms, s->ctx->stream);
 }
@@ -910,6 +973,8 @@ static int raw_gram_setup(xg_series* s, bool g2, bool store, GramParams& gp, CUt
   gp.n_frames = s->t;
   gp.g2_partial = g2 ? s->d_g2tile : nullptr;
   gp.store = store ? 1 : 0;
+  if (!s->d_wave) XG_CUDA(c, dalloc(&s->d_wave, 1));
+  gp.wave_ctr = s->d_wave;
   s->raw_stored = store;
   if (!store)  // a valid (never written) map over the frames buffer
     return make_map_out32(c, &omap, s->d_x, 32, 32);
@@ -1203,7 +1268,7 @@ int xg_series_get_ttc(xg_series* s, int32_t ring, int32_t dtype, void* out, int6
   void* dst = out;
   void* tmp = nullptr;
   if (!out_on_device) {
-    XG_CUDA(c, cudaMalloc(&tmp, bytes));
+    XG_CUDA(c, ctx_scratch(c, bytes, &tmp));
     dst = tmp;
   }
   ExpandParams p;
@@ -1222,7 +1287,6 @@ int xg_series_get_ttc(xg_series* s, int32_t ring, int32_t dtype, void* out, int6
     e = cudaMemcpyAsync(out, tmp, bytes, cudaMemcpyDeviceToHost, c->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
   }
-  if (tmp) cudaFree(tmp);
   if (e != cudaSuccess) return cuda_fail(c, e, "get_ttc");
   return check_device_error(c);
 }
@@ -2131,7 +2195,7 @@ int xg_series_get_cttc(xg_series* s, int32_t ring, int32_t dtype, void* out, int
   void* dst = out;
   void* tmp = nullptr;
   if (!out_on_device) {
-    XG_CUDA(c, cudaMalloc(&tmp, bytes));
+    XG_CUDA(c, ctx_scratch(c, bytes, &tmp));
     dst = tmp;
   }
   ExpandParams p;
@@ -2150,7 +2214,6 @@ int xg_series_get_cttc(xg_series* s, int32_t ring, int32_t dtype, void* out, int
     e = cudaMemcpyAsync(out, tmp, bytes, cudaMemcpyDeviceToHost, c->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
   }
-  if (tmp) cudaFree(tmp);
   if (e != cudaSuccess) return cuda_fail(c, e, "get_cttc");
   return check_device_error(c);
 }
@@ -2706,7 +2769,7 @@ int xg_stream_get_ttc(xg_stream* s, int32_t ring, int32_t which, int32_t dtype, 
   if (which == 1 && dtype == XG_I32_GRAM) return fail(c, XG_ERR_CONTRACT, "bad dtype");
   const size_t bytes = (size_t)s->t * ld * (dtype == XG_F64 ? 8 : 4);
   void* tmp = nullptr;
-  XG_CUDA(c, cudaMalloc(&tmp, bytes));
+  XG_CUDA(c, ctx_scratch(c, bytes, &tmp));
   ExpandParams p;
   p.gram = which == 0 ? s->d_gcol + (int64_t)ring * s->tp * s->tp : nullptr;
   p.cf32 = which == 1 ? s->d_ccol + (int64_t)ring * s->tp * s->tp : nullptr;
@@ -2721,7 +2784,6 @@ int xg_stream_get_ttc(xg_stream* s, int32_t ring, int32_t which, int32_t dtype, 
   c->launches++;
   if (e == cudaSuccess) e = cudaMemcpyAsync(out, tmp, bytes, cudaMemcpyDeviceToHost, c->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
-  cudaFree(tmp);
   if (e != cudaSuccess) return cuda_fail(c, e, "stream get_ttc");
   return check_device_error(c);
 }

@@ -26,6 +26,7 @@ __host__ __device__ constexpr int ingest_smem_offset(int e) {  // band byte -> s
   return e + (INGEST_PITCH - INGEST_PIECE) * (e / INGEST_PIECE);
 }
 
+
 // The pixels of one ring inside one band form a "segment" of the ring-major
 // row: first every source word whose 4 pixels all belong to the ring (copied
 // as a word), then the remaining pixels packed 4 per group (gathered byte by
@@ -126,6 +127,13 @@ struct GramParams {
   // max |x_t|^2 over the series (K1b): G_ij <= it, so < 2^23 lets the fused g2
   // run in FP32 double-float arithmetic with exact float Gram values
   const unsigned long long* max_norm2;
+  // wave gate (K2): pair p takes tiles p, p + P, p + 2P, ... (P pairs); before
+  // starting its wave w the leader waits until every pair has started wave
+  // w - gate_lag (wave_ctr counts started tiles, zero at launch), so no pair
+  // drifts more than gate_lag waves ahead and the tiles in flight stay inside
+  // the L2-resident super-tile (null: ungated)
+  unsigned int* wave_ctr = nullptr;
+  int32_t gate_lag = 2;
 };
 size_t gram2_smem_bytes(int mode);
 cudaError_t launch_gram2_u8(const CUtensorMap& tmX, const CUtensorMap& tmOut, const GramParams& p,
