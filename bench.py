@@ -818,6 +818,40 @@ def run_c5(E):
     return out
 
 
+def run_dropin(E, sh, frames):
+    """The reference's own API through the drop-in source (integration/
+    correlate_b200.cpp linked into a reference program, oracle/_ref/
+    dropin_bench): xpcs::ttc_raw + g2_from_ttc of the ring the CPU baseline
+    times, f64 host frames in, the full f64 TTC out -- what a reference user
+    gets by swapping src/correlate.cpp.  Host wall clock, best of 3."""
+    import tempfile
+
+    exe = os.path.join(ROOT, "oracle", "_ref", "dropin_bench")
+    if not os.path.exists(exe):
+        return {"skipped": "oracle/_ref/dropin_bench not built (needs /root/reference at build time)"}
+    T = C2["T"]
+    r_s = reference_ring(sh.sizes, T)
+    cols = E.torch.from_numpy(sh.masks[r_s]).to(E.dev)
+    xq = E.torch.index_select(frames, 1, cols).cpu().numpy()
+    with tempfile.NamedTemporaryFile(suffix=".u8", delete=False) as f:
+        f.write(np.ascontiguousarray(xq).tobytes())
+        path = f.name
+    try:
+        out = subprocess.run([exe, path, str(T), str(xq.shape[1]), "3"], capture_output=True,
+                             text=True, timeout=300)
+        res = json.loads(out.stdout.strip().splitlines()[-1])
+    finally:
+        os.unlink(path)
+    factor = sum(sh.sizes) / sh.sizes[r_s]
+    return {"what": "xpcs::ttc_raw + xpcs::g2_from_ttc through integration/correlate_b200.cpp "
+                    "(u8 tensor-core path for integer counts), f64 FrameSeries in, f64 TTCMatrix "
+                    "+ G2Curve out, called from a C++ program linked like the reference",
+            "ring": r_s, "ring_pixels": sh.sizes[r_s], "T": T, "ms_per_call": res["ms_best"],
+            "ms_mean": res["ms_mean"],
+            "frames_per_s_extrapolated": T / (res["ms_best"] / 1e3 * factor),
+            "extrapolation": f"x sum(M_q) / M_ring = {factor:.2f} (as cpu_baseline)"}
+
+
 def cpu_baseline(E, args):
     cfg = C2
     times, r_s, sizes = time_reference_ring(cfg, 1, 0)
@@ -857,6 +891,11 @@ def main():
     sh, series, frames = run_headline(E, line)
     if not args.no_compressed and not args.only:
         line["compressed"] = run_compressed(E, sh, series, frames)
+    if E.world == 1 and not args.only:
+        try:
+            line["dropin"] = run_dropin(E, sh, frames)
+        except Exception as e:  # keep the main line
+            line["dropin"] = {"failed": repr(e)}
     del series, frames
     E.free()
     if not args.only:

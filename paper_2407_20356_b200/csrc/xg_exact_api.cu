@@ -20,14 +20,52 @@ using namespace xg;
 
 namespace {
 
-// Minimal RAII device buffer for the one-shot entries.
+// Device buffers of the one-shot entries: a per-thread pool of grow-only
+// slots (the entries are called in loops by the reference's code -- e.g.
+// ttc_extend once per frame -- so no cudaMalloc/cudaFree per call).
+struct Pool {
+  void* p[8] = {};
+  size_t cap[8] = {};
+  int device = -1;
+  ~Pool() {
+    for (void* q : p)
+      if (q) cudaFree(q);
+  }
+};
+thread_local Pool g_pool;
+thread_local int g_slot = 0;  // next slot of the current entry
+
 template <class T>
 struct DBuf {
   T* p = nullptr;
-  cudaError_t alloc(size_t n) { return cudaMalloc(reinterpret_cast<void**>(&p), (n ? n : 1) * sizeof(T)); }
-  ~DBuf() {
-    if (p) cudaFree(p);
+  cudaError_t alloc(size_t n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (g_pool.device != dev) {  // buffers belong to one device
+      for (int i = 0; i < 8; ++i) {
+        if (g_pool.p[i]) cudaFree(g_pool.p[i]);
+        g_pool.p[i] = nullptr;
+        g_pool.cap[i] = 0;
+      }
+      g_pool.device = dev;
+    }
+    const int s = g_slot++ & 7;
+    const size_t bytes = (n ? n : 1) * sizeof(T);
+    if (g_pool.cap[s] < bytes) {
+      if (g_pool.p[s]) cudaFree(g_pool.p[s]);
+      g_pool.p[s] = nullptr;
+      g_pool.cap[s] = 0;
+      const cudaError_t e = cudaMalloc(&g_pool.p[s], bytes);
+      if (e != cudaSuccess) return e;
+      g_pool.cap[s] = bytes;
+    }
+    p = static_cast<T*>(g_pool.p[s]);
+    return cudaSuccess;
   }
+};
+// every entry starts allocating at slot 0
+struct SlotScope {
+  SlotScope() { g_slot = 0; }
 };
 
 thread_local char g_err[256];
@@ -60,6 +98,7 @@ XG_API int64_t xg_f64_last_payload(void) { return g_payload; }
 
 // ttc_raw (correlate.cpp:19-25): gram(row_normalize(X)).
 XG_API int xg_f64_ttc_raw(const double* x, int64_t n, int64_t m, double* out) {
+  SlotScope slots_;
   if (!x || !out) return XG_ERR_INVALID;
   if (n < 1 || m < 1) return err(XG_ERR_CONTRACT, "matrix dimensions must be at least 1x1");
   if (n < 2) return err(XG_ERR_CONTRACT, "ttc_raw: need at least 2 frames");
@@ -88,6 +127,7 @@ XG_API int xg_f64_ttc_raw(const double* x, int64_t n, int64_t m, double* out) {
 // ttc_compressed (correlate.cpp:27-35): gram(Y); lossless = |diag - 1| <= 1e-10.
 XG_API int xg_f64_ttc_compressed(const double* y, int64_t n, int64_t k, double* out,
                                  int* lossless) {
+  SlotScope slots_;
   if (!y || !out) return XG_ERR_INVALID;
   if (n < 2) return err(XG_ERR_CONTRACT, "ttc_compressed: need at least 2 frames");
   if (k < 1) return err(XG_ERR_CONTRACT, "compressed series needs k >= 1");
@@ -108,6 +148,7 @@ XG_API int xg_f64_ttc_compressed(const double* y, int64_t n, int64_t k, double* 
 // ttc_extend (correlate.cpp:37-65): out is (n+1) x (n+1).
 XG_API int xg_f64_ttc_extend(const double* g, int64_t n, const double* y, int64_t k,
                              const double* row, double* out, int* lossless) {
+  SlotScope slots_;
   if (!g || !y || !row || !out) return XG_ERR_INVALID;
   if (k < 1) return err(XG_ERR_SHAPE, "ttc_extend: new row length does not match k");
   DBuf<double> dg, dy, dr, dout;
@@ -134,6 +175,7 @@ XG_API int xg_f64_ttc_extend(const double* g, int64_t n, const double* y, int64_
 // g2_from_ttc (correlate.cpp:67-85).
 XG_API int xg_f64_g2_from_ttc(const double* g, int64_t n, double period, double* lags,
                               double* values, int64_t* counts) {
+  SlotScope slots_;
   if (!g || !lags || !values || !counts) return XG_ERR_INVALID;
   if (n < 2) return err(XG_ERR_CONTRACT, "g2_from_ttc: need at least 2 frames");
   if (!(period > 0.0)) return err(XG_ERR_CONTRACT, "g2_from_ttc: frame_period must be positive");
@@ -155,6 +197,7 @@ XG_API int xg_f64_g2_from_ttc(const double* g, int64_t n, double period, double*
 // reported), then every row like compress_frame.  v is m x k.
 XG_API int xg_f64_compress_series(const double* x, int64_t n, int64_t m, const double* v,
                                   int64_t k, double* coeffs, double* norms) {
+  SlotScope slots_;
   if (!x || !v || !coeffs || !norms) return XG_ERR_INVALID;
   if (k < 1) return err(XG_ERR_CONTRACT, "compress: k must be >= 1");
   if (n == 0) return XG_OK;  // an empty store (compress.cpp:48-81 loops over no frames)
@@ -183,6 +226,7 @@ XG_API int xg_f64_compress_series(const double* x, int64_t n, int64_t m, const d
 // compress_frame (compress.cpp:34-46).
 XG_API int xg_f64_compress_frame(const double* frame, int64_t m, const double* v, int64_t k,
                                  double* coeffs, double* norm) {
+  SlotScope slots_;
   if (!frame || !v || !coeffs || !norm) return XG_ERR_INVALID;
   const int rc = xg_f64_compress_series(frame, 1, m, v, k, coeffs, norm);
   if (rc == XG_ERR_NORMALIZATION)
@@ -192,6 +236,7 @@ XG_API int xg_f64_compress_frame(const double* frame, int64_t m, const double* v
 
 // ttc_rel_error (correlate.cpp:87-108) over count = N*N entries.
 XG_API int xg_f64_ttc_rel_error(const double* a, const double* b, int64_t count, double* out) {
+  SlotScope slots_;
   if (!a || !b || !out) return XG_ERR_INVALID;
   DBuf<double> da, db, dr;
   XG_TRY(da.alloc(count));
