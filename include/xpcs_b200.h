@@ -299,6 +299,8 @@ XG_API int xg_stream_create(xg_ctx* ctx, const xg_layout* layout, const xg_basis
                             int64_t max_frames, uint32_t flags, xg_stream** out);
 XG_API void xg_stream_destroy(xg_stream* s);
 XG_API int xg_stream_push(xg_stream* s, const uint8_t* frame, int on_device);
+/* n consecutive frames (n x full_pixels, raster order) pushed in one call. */
+XG_API int xg_stream_push_batch(xg_stream* s, const uint8_t* frames, int64_t n, int on_device);
 XG_API int64_t xg_stream_frames(const xg_stream* s);
 /* which: 0 raw, 1 compressed */
 XG_API int xg_stream_get_g2(xg_stream* s, int32_t ring, int32_t which, double* values,

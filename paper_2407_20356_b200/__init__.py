@@ -787,6 +787,20 @@ class FrameStream:
             raise ShapeError(f"frame must have {self.layout.full_pixels} pixels, got {a.size}")
         _check(self.ctx.h, lib.xg_stream_push(self.h, _ptr(a), 0))
 
+    def push_many(self, frames) -> None:
+        """Push n frames (n x full_pixels) in one library call: the same as n
+        push() calls without the per-frame Python round trip."""
+        if hasattr(frames, "data_ptr"):
+            n, on_dev = _tensor_frames(frames, self.ctx, self.layout.full_pixels, None, "push_many")
+            _check(self.ctx.h, lib.xg_stream_push_batch(self.h, C.c_void_p(frames.data_ptr()), n,
+                                                        1 if on_dev else 0))
+            self._keep = None if on_dev else frames
+            return
+        a = _as_counts_u8(frames)
+        if a.ndim != 2 or a.shape[1] != self.layout.full_pixels:
+            raise ShapeError(f"frames must be n x {self.layout.full_pixels}, got {a.shape}")
+        _check(self.ctx.h, lib.xg_stream_push_batch(self.h, _ptr(a), a.shape[0], 0))
+
     def g2(self, ring: int, compressed: bool = False):
         n = self.n_frames
         vals = np.empty(n, np.float64)

@@ -81,6 +81,7 @@ _sigs = {
     "xg_stream_create": (C.c_int, [P, P, P, I64, U32, C.POINTER(P)]),
     "xg_stream_destroy": (None, [P]),
     "xg_stream_push": (C.c_int, [P, P, C.c_int]),
+    "xg_stream_push_batch": (C.c_int, [P, P, I64, C.c_int]),
     "xg_stream_frames": (I64, [P]),
     "xg_stream_get_g2": (C.c_int, [P, I32, I32, PD, PI64]),
     "xg_stream_get_coeffs": (C.c_int, [P, I32, PD, PD]),

@@ -288,30 +288,49 @@ __global__ void __launch_bounds__(128) k_stream_ingest(StreamParams p) {
 // meets in shared memory first (integer sums: exact, order-free).  Block 0
 // clears the next push's counters (nz_next, norm2 row t + 1).
 constexpr int SI_THREADS = 256;
+constexpr int SI_PX = 4;  // 16 per thread (256 CTAs) measured slower: 10.2 -> 14.2 us
 constexpr int SI_MAXQ = 1024;
+// Programmatic dependent launch (PDL) between the pushes of a raw sparse
+// stream: K5s(t) may be scheduled while ingest(t) runs and waits for it
+// (griddepcontrol.wait); ingest(t+1) may run beside K5s(t)'s tail -- it
+// touches only push t+1's buffers (hist column t+1, nonzero lists of parity
+// (t+1) & 1, counters (t+1) % 3) -- and waits for K5s(t) before it exits, so
+// a completed ingest(t+1) implies a completed K5s(t).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __global__ void __launch_bounds__(SI_THREADS) k_stream_ingest_sparse(StreamParams p) {
   __shared__ uint32_t cnt[SI_MAXQ], sq[SI_MAXQ];
   __shared__ int32_t base[SI_MAXQ];
+  pdl_launch_dependents();
   if (blockIdx.x == 0)
     for (int r = threadIdx.x; r < p.n_rings; r += blockDim.x) {
       p.nz_next[r] = 0;
       if (p.norm2_next) p.norm2_next[r] = 0ull;
     }
   for (int r = threadIdx.x; r < p.n_rings; r += blockDim.x) cnt[r] = sq[r] = 0;
-  const int64_t px0 = (static_cast<int64_t>(blockIdx.x) * SI_THREADS + threadIdx.x) * 4;
-  uint32_t w = 0;
-  if (px0 + 4 <= p.pixels) {
-    w = __ldcs(reinterpret_cast<const uint32_t*>(p.frame + px0));
+  // SI_PX pixels per thread (one 32-bit load)
+  const int64_t px0 = (static_cast<int64_t>(blockIdx.x) * SI_THREADS + threadIdx.x) * SI_PX;
+  uint32_t wv[SI_PX / 4];
+  if (px0 + SI_PX <= p.pixels) {
+    wv[0] = __ldcs(reinterpret_cast<const uint32_t*>(p.frame + px0));
   } else {
-    for (int b = 0; b < 4; ++b)
-      if (px0 + b < p.pixels) w |= static_cast<uint32_t>(p.frame[px0 + b]) << (8 * b);
+#pragma unroll
+    for (int k = 0; k < SI_PX / 4; ++k) {
+      wv[k] = 0;
+      for (int b = 0; b < 4; ++b)
+        if (px0 + 4 * k + b < p.pixels)
+          wv[k] |= static_cast<uint32_t>(p.frame[px0 + 4 * k + b]) << (8 * b);
+    }
   }
-  int ent[4], loc[4];
+  int ent[SI_PX], loc[SI_PX];
   __syncthreads();
 #pragma unroll
-  for (int b = 0; b < 4; ++b) {
+  for (int b = 0; b < SI_PX; ++b) {
     ent[b] = -1;
-    const uint32_t v = (w >> (8 * b)) & 0xFFu;
+    const uint32_t v = (wv[b >> 2] >> (8 * (b & 3))) & 0xFFu;
     if (!v) continue;
     const int e = p.pixcol[px0 + b];
     if (e < 0) continue;
@@ -329,10 +348,10 @@ __global__ void __launch_bounds__(SI_THREADS) k_stream_ingest_sparse(StreamParam
   }
   __syncthreads();
 #pragma unroll
-  for (int b = 0; b < 4; ++b) {
+  for (int b = 0; b < SI_PX; ++b) {
     if (ent[b] < 0) continue;
     const int r = ent[b] >> 22, col = ent[b] & 0x3FFFFF;
-    const uint8_t v = static_cast<uint8_t>((w >> (8 * b)) & 0xFFu);
+    const uint8_t v = static_cast<uint8_t>((wv[b >> 2] >> (8 * (b & 3))) & 0xFFu);
     const int64_t e = base[r] + loc[b];
     p.nz_col[e] = col;
     p.nz_val[e] = v;
@@ -347,6 +366,7 @@ __global__ void __launch_bounds__(SI_THREADS) k_stream_ingest_sparse(StreamParam
     last = atomicAdd(p.done, 1u) == gridDim.x - 1;
   }
   __syncthreads();
+  pdl_wait();  // the previous push's column kernel has completed (see above)
   if (!last) return;
   __threadfence();
   for (int r = threadIdx.x; r < p.n_rings; r += blockDim.x) {
@@ -405,6 +425,8 @@ __global__ void __launch_bounds__(32 * SS_W) k_stream_sparse(StreamParams p) {
   __shared__ uint32_t red[SS_W][SS_F + 1];
   const int r = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  pdl_wait();  // this push's ingest has completed: nonzero lists, hist column t, 1/|x_t|
+  pdl_launch_dependents();
   const int koff = p.ring_koff[r];
   const int n = p.nz_n[r];
   const int64_t sb = static_cast<int64_t>(blockIdx.x) * SS_F;
@@ -438,10 +460,15 @@ __global__ void __launch_bounds__(32 * SS_W) k_stream_sparse(StreamParams p) {
         for (int u = 0; u < SS_U; ++u) {
           uint32_t ww[SS_V / 4];
           SsVec<SS_V>::words(wv[u], ww);
+          // byte j of a history word times the new count: one dp4a against
+          // the count placed in byte lane j (exact integer arithmetic)
+          const int b0 = static_cast<int>(vv[u]);
 #pragma unroll
           for (int q = 0; q < SS_V / 4; ++q)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) acc[4 * q + j] += vv[u] * ((ww[q] >> (8 * j)) & 0xFFu);
+            for (int j = 0; j < 4; ++j)
+              acc[4 * q + j] = static_cast<uint32_t>(
+                  __dp4a(ww[q], static_cast<unsigned>(b0) << (8 * j), acc[4 * q + j]));
         }
       }
     }
@@ -472,17 +499,32 @@ cudaError_t launch_stream_ingest(const StreamParams& p, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_stream_ingest_sparse(const StreamParams& p, cudaStream_t s) {
-  if (p.n_rings > SI_MAXQ) return cudaErrorInvalidValue;
-  const unsigned blocks = static_cast<unsigned>((p.pixels + 4 * SI_THREADS - 1) / (4 * SI_THREADS));
-  k_stream_ingest_sparse<<<blocks, SI_THREADS, 0, s>>>(p);
-  return cudaGetLastError();
+template <typename K>
+static cudaError_t launch_maybe_pdl(K kernel, dim3 grid, dim3 block, cudaStream_t s, bool pdl,
+                                   const StreamParams& p) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, p);
 }
 
-cudaError_t launch_stream_sparse(const StreamParams& p, int32_t n_rings, cudaStream_t s) {
+cudaError_t launch_stream_ingest_sparse(const StreamParams& p, cudaStream_t s, bool pdl) {
+  if (p.n_rings > SI_MAXQ) return cudaErrorInvalidValue;
+  const unsigned blocks =
+      static_cast<unsigned>((p.pixels + SI_PX * SI_THREADS - 1) / (SI_PX * SI_THREADS));
+  return launch_maybe_pdl(k_stream_ingest_sparse, dim3(blocks), dim3(SI_THREADS), s, pdl, p);
+}
+
+cudaError_t launch_stream_sparse(const StreamParams& p, int32_t n_rings, cudaStream_t s, bool pdl) {
   dim3 grid(static_cast<unsigned>((p.t + 1 + SS_F - 1) / SS_F), n_rings);
-  k_stream_sparse<<<grid, 32 * SS_W, 0, s>>>(p);
-  return cudaGetLastError();
+  return launch_maybe_pdl(k_stream_sparse, grid, dim3(32 * SS_W), s, pdl, p);
 }
 
 cudaError_t launch_stream_raw(const StreamParams& p, int32_t n_rings, int64_t max_kpad,

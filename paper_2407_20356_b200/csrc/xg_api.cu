@@ -2267,7 +2267,7 @@ struct xg_stream {
   int64_t hp = 0;
   int32_t* d_nz_col = nullptr;
   uint8_t* d_nz_val = nullptr;
-  int32_t* d_nz_n = nullptr;     // [2][ring]: counts of even / odd pushes
+  int32_t* d_nz_n = nullptr;     // [3][ring]: counts of push t at t % 3
   unsigned int* d_done = nullptr;  // sparse ingest's CTA counter
 };
 
@@ -2343,14 +2343,16 @@ int xg_stream_create(xg_ctx* c, const xg_layout* L, const xg_basis* B, int64_t m
   }
   if ((flags & XG_STREAM_SPARSE) || B) {
     // the new frame's nonzeros per ring (sparse raw column, sparse projection)
-    if ((e = dalloc(&s->d_nz_col, (size_t)L->ktot)) != cudaSuccess ||
-        (e = dalloc(&s->d_nz_val, (size_t)L->ktot)) != cudaSuccess ||
-        (e = dalloc(&s->d_nz_n, (size_t)2 * Q)) != cudaSuccess ||
+    // nonzero lists double-buffered and counters triple-buffered by push, so
+    // push t + 1's ingest may run beside push t's column kernel (PDL)
+    if ((e = dalloc(&s->d_nz_col, (size_t)2 * L->ktot)) != cudaSuccess ||
+        (e = dalloc(&s->d_nz_val, (size_t)2 * L->ktot)) != cudaSuccess ||
+        (e = dalloc(&s->d_nz_n, (size_t)3 * Q)) != cudaSuccess ||
         (B && (e = dalloc(&s->d_pacc, (size_t)Q * 768)) != cudaSuccess)) {
       xg_stream_destroy(s);
       return cuda_fail(c, e, "stream nonzero lists alloc");
     }
-    cudaMemsetAsync(s->d_nz_n, 0, (size_t)2 * Q * 4, c->stream);
+    cudaMemsetAsync(s->d_nz_n, 0, (size_t)3 * Q * 4, c->stream);
     if (B) cudaMemsetAsync(s->d_pacc, 0, (size_t)Q * 768 * 4, c->stream);
   }
   {
@@ -2490,10 +2492,10 @@ int xg_stream_push(xg_stream* s, const uint8_t* frame, int on_device) {
   sp.y_ld = s->tp;
   sp.hist = s->d_hist;
   sp.hp = s->hp;
-  sp.nz_col = s->d_nz_col;
-  sp.nz_val = s->d_nz_val;
-  sp.nz_n = s->d_nz_n ? s->d_nz_n + (s->t & 1) * L->rings : nullptr;
-  sp.nz_next = s->d_nz_n ? s->d_nz_n + ((s->t + 1) & 1) * L->rings : nullptr;
+  sp.nz_col = s->d_nz_col ? s->d_nz_col + (s->t & 1) * L->ktot : nullptr;
+  sp.nz_val = s->d_nz_val ? s->d_nz_val + (s->t & 1) * L->ktot : nullptr;
+  sp.nz_n = s->d_nz_n ? s->d_nz_n + (s->t % 3) * L->rings : nullptr;
+  sp.nz_next = s->d_nz_n ? s->d_nz_n + ((s->t + 1) % 3) * L->rings : nullptr;
   sp.pacc = s->d_pacc;
   sp.frame = d_frame;
   sp.pixcol = s->d_pixcol;
@@ -2515,8 +2517,12 @@ int xg_stream_push(xg_stream* s, const uint8_t* frame, int on_device) {
   sp.ovf_check = (s->flags & XG_STREAM_NO_RAW) ? 0 : 1;
   sp.done = s->d_done;
   const bool sparse = (s->flags & XG_STREAM_SPARSE) != 0;
+  // raw sparse pushes chain ingest -> column -> next ingest with programmatic
+  // dependent launches (no launch gap; k_stream.cu); a forked compressed
+  // column or a staging copy in between takes the ordinary stream order
+  const bool pdl = sparse && !(s->flags & XG_STREAM_NO_RAW) && !s->B && d_frame == frame;
   if (sparse)  // its last CTA also finishes the frame's norms
-    XG_CUDA(c, launch_stream_ingest_sparse(sp, c->stream));
+    XG_CUDA(c, launch_stream_ingest_sparse(sp, c->stream, pdl && s->t > 0));
   else
     XG_CUDA(c, launch_stream_ingest(sp, c->stream));
   NormParams np;
@@ -2553,7 +2559,7 @@ int xg_stream_push(xg_stream* s, const uint8_t* frame, int on_device) {
   }
   if (raw) {
     if (s->flags & XG_STREAM_SPARSE)
-      XG_CUDA(c, launch_stream_sparse(sp, L->rings, c->stream));
+      XG_CUDA(c, launch_stream_sparse(sp, L->rings, c->stream, pdl));
     else
       XG_CUDA(c, launch_stream_raw(sp, L->rings, s->max_kpad, c->stream));
     c->launches++;
@@ -2563,6 +2569,18 @@ int xg_stream_push(xg_stream* s, const uint8_t* frame, int on_device) {
     XG_CUDA(c, cudaStreamWaitEvent(c->stream, s->ev_join, 0));
   }
   s->t++;
+  return XG_OK;
+}
+
+// n consecutive frames (n x pixels, raster order) in one call: the same as n
+// pushes, without the per-frame host round trip of the caller.
+int xg_stream_push_batch(xg_stream* s, const uint8_t* frames, int64_t n, int on_device) {
+  if (!s || !frames) return XG_ERR_INVALID;
+  if (n < 0) return fail(s->ctx, XG_ERR_SHAPE, "stream: negative frame count");
+  for (int64_t i = 0; i < n; ++i) {
+    const int rc = xg_stream_push(s, frames + i * s->L->pixels, on_device);
+    if (rc) return rc;
+  }
   return XG_OK;
 }
 

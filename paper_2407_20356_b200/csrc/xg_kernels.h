@@ -258,10 +258,10 @@ struct StreamParams {
 cudaError_t launch_stream_ingest(const StreamParams& p, cudaStream_t s);
 // Sparse mode: the same from the raster in pixel order (no ring-major row):
 // only the frame's nonzero pixels touch the tables.
-cudaError_t launch_stream_ingest_sparse(const StreamParams& p, cudaStream_t s);
+cudaError_t launch_stream_ingest_sparse(const StreamParams& p, cudaStream_t s, bool pdl);
 // Sparse raw streaming (photon-event data): the new column costs nnz * t
 // bytes instead of M * t; results equal the dense kernel's bitwise.
-cudaError_t launch_stream_sparse(const StreamParams& p, int32_t n_rings, cudaStream_t s);
+cudaError_t launch_stream_sparse(const StreamParams& p, int32_t n_rings, cudaStream_t s, bool pdl);
 cudaError_t launch_stream_raw(const StreamParams& p, int32_t n_rings, int64_t max_kpad,
                               cudaStream_t s);
 cudaError_t launch_stream_cmp(const StreamParams& p, int32_t n_rings, cudaStream_t s);

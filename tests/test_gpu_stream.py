@@ -94,3 +94,38 @@ def test_sparse_stream_equals_dense(ctx, orc, mu):
         _, g2d, cd = dense.g2(r)
         _, g2s, cs = sparse.g2(r)
         assert np.array_equal(g2s, g2d) and np.array_equal(cs, cd)
+
+
+@pytest.mark.parametrize("basis_k", [0, 6])
+def test_push_many_equals_single_pushes(ctx, orc, basis_k):
+    """push_many (one library call for n frames) == n push() calls, bitwise;
+    the raw sparse stream without a basis chains its kernels with
+    programmatic dependent launches (push t + 1's ingest beside push t's
+    column kernel), which must not change a bit."""
+    import torch
+
+    t, h, w, q = 300, 96, 96, 4
+    frames = orc.gen_speckle(t, h, w, q, 0.08, 93)
+    frames[40] = 0
+    ring, _ = orc.ring_map(h, w, q)
+    lay = xg.RingLayout.from_ring_map(ctx, ring, q)
+    basis = None
+    if basis_k:
+        basis = xg.Basis(lay, basis_k)
+        xg.FrameSeries(lay, 64).load(frames[64:128]).build_basis(basis_k, basis=basis)
+    dev = torch.from_numpy(frames).cuda()
+    a = xg.FrameStream(lay, t, basis=basis, store_ttc=True, sparse=True)
+    b = xg.FrameStream(lay, t, basis=basis, store_ttc=True, sparse=True)
+    for i in range(t):
+        a.push(dev[i])
+    b.push_many(dev[:100])
+    b.push_many(dev[100:])
+    for r in range(q):
+        ga, gb = a.ttc(r, dtype="gram"), b.ttc(r, dtype="gram")
+        assert np.array_equal(ga, gb)
+        assert np.array_equal(gb.astype(np.int64), orc.gram_u8(frames[:, ring == r]))
+        _, va, ca = a.g2(r)
+        _, vb, cb = b.g2(r)
+        assert np.array_equal(va, vb) and np.array_equal(ca, cb)
+        if basis_k:
+            assert np.array_equal(a.coeffs(r)[0], b.coeffs(r)[0])

@@ -75,6 +75,25 @@ def main():
             torch.cuda.synchronize()
             ms = sorted(a.elapsed_time(b) for a, b in ev)
             print(f"c2cmp {name}: median {ms[5]:.3f} ms")
+    elif what == "c3push":
+        H = W = 1024
+        Q, mu, D, n = 64, 0.02, 8192, 256
+        frames = torch.empty((D + n, H * W), dtype=torch.uint8, device=dev)
+        xg.synth_speckle(ctx, frames.data_ptr(), D + n, H, W, Q, mu, 3)
+        ring = xg.annular_rings(H, W, Q)
+        lay = xg.RingLayout(ctx, H * W, [np.nonzero(ring == r)[0] for r in range(Q)])
+        sr = xg.FrameStream(lay, D + n, sparse=True)
+        sr.push_many(frames[:D])
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        sr.push_many(frames[D:])
+        b.record(st)
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / n
+        nnz = float((frames[D:] != 0).float().mean()) * H * W
+        gbs = nnz * (D + n / 2) / (ms / 1e3) / 1e9
+        print(f"c3push depth {D}: {ms * 1e3:.1f} us/push, {gbs:.0f} GB/s of nnz*t")
     elif what == "c5":
         k = int(sys.argv[2]) if len(sys.argv) > 2 else 64
         H, W, Q, mu, ch = 1536, 2048, 128, 0.01, 4096
