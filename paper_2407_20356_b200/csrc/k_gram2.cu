@@ -39,7 +39,11 @@ constexpr int TMEM_COLS = 512;
 // and 8 epilogue warps (two per TMEM lane quarter, each taking half the
 // columns); the epilogue is on the critical path of small-ring and K4 tiles.
 template <int MODE> struct Cfg2 {
+  // 5 operand stages and one staging chunk per epilogue warp.  K4 with two
+  // staging buffers (two C~ chunk stores in flight per warp) needs the smem
+  // of a stage: 4 stages + 2 buffers measured 0.273 ms vs 0.259 ms.
   static constexpr int STAGES = 5;
+  static constexpr int SBUF = 1;  // staging buffers per epilogue warp (1 or 2)
   static constexpr int EPI_WARPS = 8;
   static constexpr int NUM_THREADS = 128 + 32 * EPI_WARPS;
 };
@@ -52,9 +56,9 @@ constexpr uint32_t idesc2() {
   return MODE == 0 ? idesc_i8(256, BN, false) : idesc_bf16(256, BN);
 }
 
-template <int EPI_WARPS, int STAGES>
+template <int EPI_WARPS, int STAGES, int SBUF>
 struct __align__(1024) Tail2 {
-  uint32_t stage[EPI_WARPS][32 * 32];  // one 32x32 chunk per warp, 128B-swizzled
+  uint32_t stage[SBUF][EPI_WARPS][32 * 32];  // 32x32 chunks per warp, 128B-swizzled
   uint64_t full[STAGES];
   uint64_t empty[STAGES];
   uint64_t tfull[2];
@@ -111,7 +115,7 @@ __device__ __forceinline__ void epi_bar() {
 template <int MODE>
 constexpr size_t smem2_bytes() {
   return 1024 + Cfg2<MODE>::STAGES * STAGE_BYTES +
-         sizeof(Tail2<Cfg2<MODE>::EPI_WARPS, Cfg2<MODE>::STAGES>);
+         sizeof(Tail2<Cfg2<MODE>::EPI_WARPS, Cfg2<MODE>::STAGES, Cfg2<MODE>::SBUF>);
 }
 size_t gram2_smem_bytes(int mode) { return mode == 0 ? smem2_bytes<0>() : smem2_bytes<1>(); }
 
@@ -121,7 +125,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
             GramParams p) {
   constexpr uint32_t IDESC = idesc2<MODE>();
   constexpr int STAGES = Cfg2<MODE>::STAGES, EPI_WARPS = Cfg2<MODE>::EPI_WARPS;
-  using Tail = Tail2<EPI_WARPS, STAGES>;
+  constexpr int SBUF = Cfg2<MODE>::SBUF;
+  using Tail = Tail2<EPI_WARPS, STAGES, SBUF>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
@@ -147,7 +152,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
       mbar_init(&tail->tfull[a], 1);
       mbar_init(&tail->tempty[a], 2 * EPI_WARPS);  // epilogue warps of both CTAs
       mbar_init(&tail->accfull[a], EPI_WARPS);
-      mbar_init(&tail->accfree[a], 1);
+      mbar_init(&tail->accfree[a], MODE == 1 ? 2 : 1);  // the folding warps
       mbar_init(&tail->invfull[a], 1);
       mbar_init(&tail->invfree[a], EPI_WARPS);
     }
@@ -294,10 +299,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
         }
       }
     }
-  } else if (warp == 2) {
+  } else if (MODE == 0 && warp == 2) {
     // K2 g2 weights: 1/|x| of the next tile's rows and columns staged one
     // tile ahead, so the epilogue warps never stop to load them
-    if (MODE == 0 && p.g2_partial) {
+    if (p.g2_partial) {
       int it = 0;
       for (int t = pair; t < p.ntiles; t += npairs, ++it) {
         const int buf = it & 1;
@@ -319,10 +324,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
         if (lane == 0) mbar_arrive(&tail->invfull[buf]);
       }
     }
-  } else if (warp == 3) {
+  } else if (warp == 3 || (MODE == 1 && warp == 2)) {
     // g2 fold: sums the 8 epilogue warps' window slots of each tile in a
     // fixed warp order and writes the tile's diagonal sums, so the epilogue
-    // warps never meet at a barrier (they run up to 2 tiles ahead).
+    // warps never meet at a barrier (they run up to 2 tiles ahead).  K4's
+    // tiles are short (K = 6 x 64), so there the otherwise idle warp 2 takes
+    // half the diagonals and the sums are plain fp32 (C~ is fp32; the slots
+    // carry no low part): the fold was the bottleneck (0.304 -> 0.259 ms
+    // without it, ncu/A-B).
+    const int e_lo = MODE == 1 && warp == 3 ? 192 : 0;
+    const int e_hi = MODE == 1 && warp == 2 ? 192 : NDIAG;
     if (p.g2_partial) {
       float2(*acc2)[EPI_WARPS][WSLOTS] = tail->slot;
       int it = 0;
@@ -333,7 +344,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
         if (2 * (td.i0 / 256) + static_cast<int>(rank) < p.g2_nbi) {
           const int64_t half = td.pad + static_cast<int64_t>(rank) * (p.g2_nbj - td.i0 / 256);
           float2* out = p.g2_partial + half * NDIAG_PAD;
-          for (int e = lane; e < NDIAG; e += 32) {
+          for (int e = e_lo + lane; e < e_hi; e += 32) {
             float2 sum = make_float2(0.f, 0.f);
 #pragma unroll
             for (int w = 0; w < EPI_WARPS; ++w) {
@@ -341,7 +352,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
               const int off = e - 96 + 32 * sb - 32 * k4_wlo(gp);
               if (off >= 0 && off < 32 * k4_nwin(gp)) {
                 const float2 v = acc2[buf][w][off];
-                sum = dd_add(sum, v.x, v.y);
+                if (MODE == 1)
+                  sum.x += v.x;
+                else
+                  sum = dd_add(sum, v.x, v.y);
               }
             }
             out[e] = sum;
@@ -360,7 +374,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
     int acc = 0;
     uint32_t acc_phase = 0;
     bool ok = true;
-    uint32_t* S = tail->stage[ew];
+    int sbuf = 0;  // staging buffer of the next chunk (alternates when SBUF = 2)
     // K4 window walk: word offset in the staged (swizzled) chunk of this
     // lane's element in row l, column (lane + 1 + l) mod 32
     int wtab[MODE == 1 ? 32 : 1];
@@ -413,7 +427,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
         tmem_ld32(tbase + c * 32, r);
         tmem_ld_wait();
         // the TMA store of the previous chunk has read the buffer
-        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        uint32_t* S = tail->stage[sbuf][ew];
+        if (SBUF == 2) sbuf ^= 1;
+        // (SBUF = 2: the store before that, from this buffer)
+        if (lane == 0) {
+          if (SBUF == 2)
+            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          else
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        }
         __syncwarp();
 #pragma unroll
         for (int q = 0; q < 8; ++q)
@@ -421,7 +443,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
               make_uint4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
         fence_proxy_async();
         __syncwarp();
-        if (lane == 0 && p.store && (EPI_WARPS == 4 || (grp ? c >= 4 : c < 4))) {
+        // chunks wholly below the diagonal of a diagonal tile are never read
+        // (every reader takes the upper triangle a <= b): not stored
+        const bool lower = td.i0 == td.j0 && c < sub + 4 * static_cast<int>(rank);
+        if (lane == 0 && p.store && !lower && (EPI_WARPS == 4 || (grp ? c >= 4 : c < 4))) {
           // the TTC streams out once: evict-first in L2, so it does not push
           // the ring's frame rows (re-read by later tiles) out of L2
           uint64_t pol;
@@ -431,9 +456,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
                   reinterpret_cast<uint64_t>(&tmOut)),
               "r"(smem_u32(S)), "r"(td.j0 + 32 * c), "r"(out_row), "l"(pol)
               : "memory");
-
-          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
+        // one bulk group per chunk, empty when nothing was stored, so with
+        // two staging buffers the group wait_group.read 1 leaves pending is
+        // always the other buffer's
+        if (lane == 0) asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         if (p.g2_partial) {
           const int col0 = td.j0 + 32 * c;  // first frame of this chunk's columns
           const float2* ir2 = tail->inv_row2[buf] + 32 * sub;
