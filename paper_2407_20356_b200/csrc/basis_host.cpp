@@ -1,5 +1,8 @@
-// basis_host.cpp -- rank-k encoding basis V_K (host, f64), the untimed setup
-// of the compressed path.
+// basis_host.cpp -- rank-k encoding basis V_K of NON-COUNT f64 training rows
+// (host, f64): the untimed setup of the compressed path for data the device
+// builder cannot take.  Photon counts (the detector's data) are factorised on
+// the device by K9 (k_basis.cu, xg_series_build_basis), which the xpcsvd
+// surface routes them to; this file is never on the correlation path.
 //
 // Follows the reference's Gram-trick SVD (SPEC.md core-linalg gram_svd;
 // src/linalg.cpp:184-439) and encoder (src/encoder.cpp:13-60):
@@ -10,7 +13,8 @@
 //   sign fix: the largest-magnitude entry of every column is positive.
 // It is not bit-identical to the reference (different summation order);
 // parity is V within 1e-10 after the shared sign convention, pinned in
-// tests/test_basis.py.  Rings are independent and built on separate threads.
+// tests/test_host.py (test_basis_builder_*).  Rings are independent and
+// built on separate threads.
 #include <algorithm>
 #include <cmath>
 #include <cstdint>

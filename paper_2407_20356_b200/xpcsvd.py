@@ -10,12 +10,19 @@ names, argument meanings, result types and exception classes for:
     TTCMatrix, ttc_raw, ttc_compressed, ttc_extend, G2Curve, g2_from_ttc,
     ttc_rel_error
 
-Every correlation / projection result is computed on the GPU by the
-``xg_f64_*`` entry points (k_exact.cu), which replay the reference's f64
-operation order, so the values are the reference's bits.  The basis
-(Gram-trick SVD) is the library's host f64 restatement, as in the reference.
+Routing, as the C++ drop-in (integration/b200_engine.hpp):
+  * intensities that are integer photon counts in [0, 255] (detector data)
+    take the tensor-core path: ``ttc_raw`` via the exact u8 int32 Gram (C
+    within 1e-12 of the reference), the basis (``build_offline`` /
+    ``build_online_from_frames``) via the device Gram-trick SVD (K9, V within
+    1e-10 of the reference);
+  * anything else, every other function, and every call under
+    ``XPCS_B200_EXACT=1`` use the ``xg_f64_*`` entry points (k_exact.cu),
+    which replay the reference's f64 operation order (the reference's bits),
+    and, for the basis of non-count data, the library's host f64 restatement
+    of gram_svd (setup only, untimed).
 For u8 count data at scale use the batched ring API (``FrameSeries`` /
-``RingLayout`` in the package root) instead.
+``RingLayout`` in the package root) directly.
 
 The validation rules and messages follow model.cpp:10-40 (masks, series),
 model.cpp:70-94 (encoders), model.cpp:139-212 (stores) and model.cpp:214-240
@@ -50,6 +57,31 @@ def _ctx():
     if _CTX is None:
         _CTX = Context(0)
     return _CTX
+
+
+def _exact_only() -> bool:
+    import os
+
+    return os.environ.get("XPCS_B200_EXACT") == "1"
+
+
+def _as_counts(x: np.ndarray):
+    """u8 copy when every intensity is an integer count in [0, 255], else None."""
+    if _exact_only() or x.size == 0 or x.min() < 0 or x.max() > 255:
+        return None
+    if not np.array_equal(x, np.floor(x)):
+        return None
+    return x.astype(np.uint8)
+
+
+def _one_ring_series(u8: np.ndarray):
+    """A device series over one ring holding every pixel of ``u8``."""
+    from . import FrameSeries as _Series, RingLayout as _Layout
+
+    ctx = _ctx()
+    n, m = u8.shape
+    lay = _Layout(ctx, m, [np.arange(m, dtype=np.int64)])
+    return _Series(lay, n).load(u8)
 
 
 # ------------------------------------------------------------------ model
@@ -168,6 +200,10 @@ def _encoder_from_rows(x: np.ndarray, mode: EncoderMode, k: int) -> EncodingMatr
     import ctypes as C
     x = np.ascontiguousarray(x, dtype=np.float64)
     n, m = x.shape
+    u8 = _as_counts(x) if n <= 2048 else None
+    if u8 is not None:  # counts: the device Gram-trick SVD (K9)
+        vs, sig, rank = _one_ring_series(u8).build_basis(k)
+        return EncodingMatrix(vs[0], sig[0], mode)
     kk = k if k > 0 else n
     v = np.empty((m, kk), np.float64)
     sig = np.empty(n, np.float64)
@@ -328,10 +364,20 @@ class G2Curve:
 
 
 def ttc_raw(frames: FrameSeries) -> TTCMatrix:
-    """xpcs::ttc_raw (correlate.cpp:19-25) on the GPU, bit-exact."""
+    """xpcs::ttc_raw (correlate.cpp:19-25) on the GPU: counts through the
+    exact u8 Gram (within 1e-12), other data bit-exact on the f64 replica."""
     if frames.n_frames < 2:
         raise ContractError("ttc_raw: need at least 2 frames")
     _ctx()
+    u8 = _as_counts(frames._x)
+    if u8 is not None:
+        s = _one_ring_series(u8)
+        try:
+            s.ttc_raw(strict=True)
+        except NormalizationError as e:  # the reference's message (linalg.cpp:446-449)
+            raise NormalizationError(f"row_normalize: frame {e.frame_index} has zero norm",
+                                     e.frame_index) from None
+        return TTCMatrix(s.ttc(0, "f64"), True)
     return TTCMatrix(_ttc_raw(frames._x), True)
 
 

@@ -88,3 +88,24 @@ def test_mask_selection_then_correlate(ref):
     assert masked.n_pixels == 3
     assert np.array_equal(masked.intensities, frames.intensities[:, [1, 5, 7]])
     assert np.array_equal(xv.ttc_raw(masked).values, ref.ttc_raw(masked.intensities))
+
+
+def test_count_data_takes_the_tensor_core_path(ref, monkeypatch):
+    """Integer photon counts go through the exact u8 Gram (C within 1e-12 of
+    the reference) and the device Gram-trick SVD (V within 1e-10); with
+    XPCS_B200_EXACT=1 the f64 replicas return the reference's bits."""
+    rng = np.random.default_rng(23)
+    frames = xv.FrameSeries(rng.poisson(1.5, size=(60, 300)).astype(np.float64), 1.0)
+    g = xv.ttc_raw(frames)
+    g_ref = ref.ttc_raw(frames.intensities)
+    assert np.abs(g.values - g_ref).max() <= 1e-12
+    enc = xv.build_online_from_frames(frames, 12)
+    v_ref, spec_ref = ref.build_online_from_frames(frames.intensities, 12)
+    assert np.abs(enc.v - v_ref).max() <= 1e-10
+    assert np.abs(np.asarray(enc.spectrum)[:spec_ref.size] - spec_ref).max() <= 1e-12 * spec_ref[0]
+    zero = xv.FrameSeries(np.vstack([np.ones(8), np.zeros(8), 2 * np.ones(8)]), 1.0)
+    with pytest.raises(xv.NormalizationError) as e:
+        xv.ttc_raw(zero)
+    assert e.value.frame_index == 1
+    monkeypatch.setenv("XPCS_B200_EXACT", "1")
+    assert np.array_equal(xv.ttc_raw(frames).values, g_ref)

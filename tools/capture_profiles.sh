@@ -1,26 +1,28 @@
 #!/bin/bash
 # Round-end measurement captures (run on the GPU box from the repo root, e.g.
-#   gpurun -- 'bash tools/capture_profiles.sh r1'), results into gpurun_out/,
+#   gpurun -- 'bash tools/capture_profiles.sh r2'), results into gpurun_out/,
 # then copied to profiles/ and summarised with tools/make_summary.py.
 # Every ncu command runs only after the same program exited 0 without ncu.
-R=${1:-r1}
+R=${1:-r2}
 O=gpurun_out
 mkdir -p $O
 NCU="ncu --set full --import-source on --clock-control none"
 python bench.py > $O/${R}_bench.json 2> $O/${R}_bench.err || exit 1
-python tools/time_gram.py > $O/time_gram.log 2>&1 || exit 1
-python tools/time_cmp.py > $O/time_cmp.log 2>&1 || exit 1
-DEPTH=8192 K=128 python tools/time_stream.py > $O/time_stream.log 2>&1 || exit 1
+python tools/prof_r2.py c2 > $O/${R}_p_c2.log 2>&1 || exit 1
+python tools/prof_r2.py c2cmp > $O/${R}_p_c2cmp.log 2>&1 || exit 1
+python tools/prof_r2.py c3push > $O/${R}_p_c3.log 2>&1 || exit 1
+python tools/prof_r2.py c4 > $O/${R}_p_c4.log 2>&1 || exit 1
+python tools/prof_r2.py c5 64 > $O/${R}_p_c5.log 2>&1 || exit 1
+# launch list of the headline step (cold, serialised: compare shares)
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/${R}_launches.csv \
-    python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-stream --no-compressed --no-e2e \
-    > /dev/null 2>&1
-$NCU -k regex:"k_ingest" -s 2 -c 1 -o $O/${R}_ingest python tools/time_gram.py > /dev/null 2>&1
-$NCU -k regex:"k_gram2" -c 1 -o $O/${R}_gram_raw python tools/time_gram.py > /dev/null 2>&1
-$NCU -k regex:"k_project" -c 1 -o $O/${R}_project python tools/time_cmp.py > /dev/null 2>&1
-$NCU -k regex:"k_gram2" -c 1 -o $O/${R}_gram_cmp python tools/time_cmp.py > /dev/null 2>&1
-# streaming: skip the history fill (3 kernels per sparse push + 3 compressed)
-DEPTH=8192 K=128 $NCU --cache-control none --kernel-name-base function -k k_stream_sparse --launch-skip 8000 \
-    --launch-count 1 -o $O/${R}_stream_sparse python tools/time_stream.py > /dev/null 2>&1
-DEPTH=8192 K=128 $NCU --cache-control none -k regex:"k_stream_cmp" --launch-skip 8000 \
-    --launch-count 1 -o $O/${R}_stream_cmp python tools/time_stream.py > /dev/null 2>&1
-ls -la $O
+    python bench.py --steps 3 --warmup 3 --only 1 --no-cpu-baseline --no-e2e > /dev/null 2>&1
+# full captures of the kernel each workload is about
+$NCU -k regex:"k_ingest" -s 1 -c 1 -o $O/${R}_ingest python tools/prof_r2.py c2 > /dev/null 2>&1
+$NCU -k regex:"k_gram2" -s 1 -c 1 -o $O/${R}_gram_raw python tools/prof_r2.py c2 > /dev/null 2>&1
+ONLY="store+fused g2" $NCU -k regex:"k_gram2" -s 5 -c 1 -o $O/${R}_gram_cmp python tools/prof_r2.py c2cmp > /dev/null 2>&1
+ONLY="store+fused g2" $NCU -k regex:"k_project" -c 1 -o $O/${R}_project python tools/prof_r2.py c2cmp > /dev/null 2>&1
+$NCU -k regex:"k_stream_sparse" -s 16000 -c 1 -o $O/${R}_stream_sparse python tools/prof_r2.py c3push > /dev/null 2>&1
+$NCU -k regex:"k_gram2" -s 1 -c 1 -o $O/${R}_c4_gram python tools/prof_r2.py c4 > /dev/null 2>&1
+$NCU -k regex:"k_ingest" -s 2 -c 1 -o $O/${R}_c5_ingest python tools/prof_r2.py c5 64 > /dev/null 2>&1
+$NCU -k regex:"k_project" -s 2 -c 1 -o $O/${R}_c5_project python tools/prof_r2.py c5 64 > /dev/null 2>&1
+ls -la $O | grep $R

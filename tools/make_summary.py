@@ -17,14 +17,14 @@ def run(*args):
 
 
 def main():
-    rnd = sys.argv[1] if len(sys.argv) > 1 else "r1"
+    rnd = sys.argv[1] if len(sys.argv) > 1 else "r2"
     lines = [f"# {rnd} launch list: ncu --metrics gpu__time_duration.sum --clock-control none "
              "(cold, serialised; compare SHARES)",
-             "# command: python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-stream "
-             "--no-compressed --no-e2e (tools/capture_profiles.sh): the device-resident raw step",
+             "# command: python bench.py --steps 3 --warmup 3 --only 1 --no-cpu-baseline --no-e2e "
+             "(tools/capture_profiles.sh): the device-resident raw C2 step",
              run("tools/launches.py", os.path.join(PROF, f"{rnd}_launches.csv")).rstrip(), ""]
     for name in ("ingest", "gram_raw", "project", "gram_cmp", "stream_dense", "stream_sparse",
-                 "stream_cmp"):
+                 "stream_cmp", "c4_gram", "c5_ingest", "c5_project"):
         rep = os.path.join(PROF, f"{rnd}_{name}.ncu-rep")
         if not os.path.exists(rep):
             continue
