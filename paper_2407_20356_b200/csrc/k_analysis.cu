@@ -17,7 +17,7 @@ namespace {
 // (k_expand), so the values equal the host TTC bitwise.
 __device__ __forceinline__ double bg_entry(const BgParams& p, int r, int64_t a, int64_t b,
                                            const double* inv) {
-  const int64_t o = r * p.ring_stride + a * p.ld + b;
+  const int64_t o = r * p.ring_stride + ttc_off(a, b, p.ld, p.nb);
   return p.cgram ? static_cast<double>(p.cgram[o])
                  : static_cast<double>(p.gram[o]) * (inv[a] * inv[b]);
 }

@@ -169,7 +169,7 @@ __global__ void k_basis_s(BasisSParams p) {
   double v = 0.0;
   if (i < p.n && j < p.n) {
     const int a = min(i, j), b = max(i, j);
-    const int32_t g = p.gram[(int64_t)ring * p.ld * p.ld + (int64_t)a * p.ld + b];
+    const int32_t g = p.gram[(int64_t)ring * p.ring_stride + ttc_off(a, b, p.ld, p.nb)];
     const double* inv = p.inv + ring * p.inv_ld;
     v = static_cast<double>(g) * inv[a] * inv[b];
   }

@@ -34,19 +34,19 @@ __global__ void __launch_bounds__(128) k_g2_partial(G2Params p) {
   int64_t cnt = 0;
   const double* inv = p.inv + r * p.inv_ld;
   if (MODE == 0) {
-    const int32_t* g = p.gram + r * p.ring_stride + d;
+    const int32_t* g = p.gram + r * p.ring_stride;
 #pragma unroll 4
     for (int64_t t = t_begin; t < t_end; ++t) {
       const double a = inv[t], b = inv[t + d];
-      const int32_t v = __ldcs(g + t * (p.ld + 1));
+      const int32_t v = __ldcs(g + ttc_off(t, t + d, p.ld, p.nb));
       acc += static_cast<double>(v) * (a * b);
       cnt += (a != 0.0 && b != 0.0);
     }
   } else {
-    const float* c = p.cf32 + r * p.ring_stride + d;
+    const float* c = p.cf32 + r * p.ring_stride;
 #pragma unroll 4
     for (int64_t t = t_begin; t < t_end; ++t) {
-      acc += static_cast<double>(__ldcs(c + t * (p.ld + 1)));
+      acc += static_cast<double>(__ldcs(c + ttc_off(t, t + d, p.ld, p.nb)));
       ++cnt;
     }
   }
@@ -89,11 +89,11 @@ __global__ void k_expand(ExpandParams p, int src_mode) {
       // inside a diagonal tile the lower half is taken from its mirror
       const int64_t a = si <= sj ? si : sj, b = si <= sj ? sj : si;
       if (src_mode == 0) {
-        const int32_t g = p.gram[a * p.ld + b];
+        const int32_t g = p.gram[ttc_off(a, b, p.ld, p.nb)];
         v = p.out_dtype == 2 ? static_cast<double>(g)
                              : static_cast<double>(g) * (p.inv[a] * p.inv[b]);
       } else {
-        v = static_cast<double>(p.cf32[a * p.ld + b]);
+        v = static_cast<double>(p.cf32[ttc_off(a, b, p.ld, p.nb)]);
       }
     }
     tile[rr][threadIdx.x] = v;
@@ -183,8 +183,9 @@ __global__ void __launch_bounds__(256) k_rel_error(RelErrParams p) {
   for (int64_t a = blockIdx.x; a < p.n; a += REL_BLOCKS) {
     const double ia = inv[a];
     for (int64_t b = a + threadIdx.x; b < p.n; b += blockDim.x) {
-      const double c = static_cast<double>(g[a * p.ld + b]) * (ia * inv[b]);
-      const double e = c - static_cast<double>(cf[a * p.ld + b]);
+      const int64_t o = ttc_off(a, b, p.ld, p.nb);
+      const double c = static_cast<double>(g[o]) * (ia * inv[b]);
+      const double e = c - static_cast<double>(cf[o]);
       const double w = a == b ? 1.0 : 2.0;
       num += w * e * e;
       den += w * c * c;
@@ -258,13 +259,13 @@ __global__ void k_pack_upper(ExpandParams p, int src_mode, int64_t row0) {
   for (int64_t j = i + threadIdx.x; j < p.n; j += blockDim.x) {
     const int64_t o = off + (j - i);
     if (src_mode == 0) {
-      const int32_t g = p.gram[i * p.ld + j];
+      const int32_t g = p.gram[ttc_off(i, j, p.ld, p.nb)];
       if (p.out_dtype == 2)
         static_cast<int32_t*>(p.out)[o] = g;
       else
         static_cast<double*>(p.out)[o] = static_cast<double>(g) * (p.inv[i] * p.inv[j]);
     } else {
-      static_cast<float*>(p.out)[o] = p.cf32[i * p.ld + j];
+      static_cast<float*>(p.out)[o] = p.cf32[ttc_off(i, j, p.ld, p.nb)];
     }
   }
 }
@@ -272,37 +273,6 @@ __global__ void k_pack_upper(ExpandParams p, int src_mode, int64_t row0) {
 cudaError_t launch_pack_upper(const ExpandParams& p, int src_mode, int64_t row0, int64_t rows,
                               cudaStream_t s) {
   k_pack_upper<<<static_cast<unsigned>(rows), 256, 0, s>>>(p, src_mode, row0);
-  return cudaGetLastError();
-}
-
-// Split-ring exchange: copy the upper pair tiles of one ring's Gram slab
-// to / from the packed tile buffer.  One CTA per tile; 16-byte accesses.
-__global__ void __launch_bounds__(256) k_tiles_copy(int32_t* slab, int64_t ld, int32_t nb,
-                                                    int32_t* packed, int dir) {
-  int64_t tile = blockIdx.x;
-  int32_t I = 0;
-  while (tile >= nb - I) {  // row I of the tile triangle holds nb - I tiles
-    tile -= nb - I;
-    ++I;
-  }
-  const int32_t J = I + static_cast<int32_t>(tile);
-  int4* pk = reinterpret_cast<int4*>(packed + static_cast<int64_t>(blockIdx.x) * 65536);
-  for (int e = threadIdx.x; e < 256 * 64; e += blockDim.x) {
-    const int row = e >> 6, c4 = e & 63;
-    int4* sp = reinterpret_cast<int4*>(slab + (static_cast<int64_t>(I) * 256 + row) * ld +
-                                       static_cast<int64_t>(J) * 256) + c4;
-    if (dir == 0)
-      pk[e] = *sp;
-    else
-      *sp = pk[e];
-  }
-}
-
-cudaError_t launch_tiles_copy(int32_t* slab, int64_t ld, int32_t nb, int32_t* packed, int dir,
-                              cudaStream_t s) {
-  const int64_t ntiles = static_cast<int64_t>(nb) * (nb + 1) / 2;
-  if (ntiles == 0) return cudaSuccess;
-  k_tiles_copy<<<static_cast<unsigned>(ntiles), 256, 0, s>>>(slab, ld, nb, packed, dir);
   return cudaGetLastError();
 }
 

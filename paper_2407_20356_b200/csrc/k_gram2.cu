@@ -398,7 +398,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
         if (!mbar_wait(&tail->invfull[buf], (it >> 1) & 1, p.err)) ok = false;
       const uint32_t tbase =
           tmem_base + static_cast<uint32_t>(acc * BN) + (static_cast<uint32_t>(sub * 32) << 16);
-      const int out_row = td.ring * p.ld + i0 + 32 * sub;
+      // packed pair tile (ttc_off): rows of tile (I, J) of ring r start at
+      // (r * tiles_per_slab + tile(I, J)) * 256; this CTA's half adds 128 rank
+      const int64_t tI = td.i0 >> 8, tJ = td.j0 >> 8;
+      const int out_row = static_cast<int>(
+          ((p.ring_stride >> 16) * td.ring + tI * p.nb - (tI * (tI - 1)) / 2 + (tJ - tI)) * 256 +
+          128 * static_cast<int>(rank) + 32 * sub);
       // Column chunks c (32 wide) are staged one at a time in this warp's
       // buffer, stored by TMA and read by the g2 window sums.  Window w
       // (lane L sums the diagonal elements (l, 32(w-1) + L + 1 + l), l =
@@ -454,7 +459,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
           asm volatile(
               "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3}], [%1], %4;" ::"l"(
                   reinterpret_cast<uint64_t>(&tmOut)),
-              "r"(smem_u32(S)), "r"(td.j0 + 32 * c), "r"(out_row), "l"(pol)
+              "r"(smem_u32(S)), "r"(32 * c), "r"(out_row), "l"(pol)
               : "memory");
         }
         // one bulk group per chunk, empty when nothing was stored, so with

@@ -682,6 +682,12 @@ void xg_series_destroy(xg_series* s) {
 
 int64_t xg_series_frames(const xg_series* s) { return s ? s->t : -1; }
 
+// Stored-TTC geometry (ttc_off, xg_kernels.h): one slab of packed upper pair
+// tiles per ring, sized for the series' capacity; the tiles of the current
+// frames use ttc_nb(s) per row.
+static int64_t slab_elems(const xg_series* s) { return ttc_slab(s->tp / 256); }
+static int32_t ttc_nb(const xg_series* s) { return static_cast<int32_t>((s->t + 255) / 256); }
+
 // The staging raster for frames that arrive from host memory.
 static int ensure_raster(xg_series* s) {
   if (s->d_raster) return XG_OK;
@@ -905,10 +911,11 @@ static int run_g2(xg_series* s, int mode, int32_t ring0 = 0, int32_t n_rings = -
     s->g2part_cap = need;
   }
   G2Params g;
-  g.gram = s->d_gram + (int64_t)ring0 * s->tp * s->tp;
+  g.gram = s->d_gram + (int64_t)ring0 * slab_elems(s);
   g.cf32 = nullptr;
-  g.ring_stride = s->tp * s->tp;
+  g.ring_stride = slab_elems(s);
   g.ld = static_cast<int32_t>(s->tp);
+  g.nb = ttc_nb(s);
   g.inv = s->d_inv + (int64_t)ring0 * s->tp;
   g.inv_ld = s->tp;
   g.n_frames = s->t;
@@ -952,8 +959,8 @@ static int raw_gram_setup(xg_series* s, bool g2, bool store, GramParams& gp, CUt
                           CUtensorMap& omap) {
   xg_ctx* c = s->ctx;
   const xg_layout* L = s->L;
-  if (store && !s->d_gram)  // the Q x T x T int32 TTC, allocated on first use
-    XG_CUDA(c, dalloc(&s->d_gram, (size_t)L->rings * s->tp * s->tp));
+  if (store && !s->d_gram)  // the packed int32 TTC (upper pair tiles), allocated on first use
+    XG_CUDA(c, dalloc(&s->d_gram, (size_t)L->rings * slab_elems(s)));
   int rc = build_tiles(s);
   if (rc) return rc;
   rc = make_map_u8(c, &map, s->d_x, L->ktot, s->t, L->ktot, 128, 128);
@@ -963,8 +970,9 @@ static int raw_gram_setup(xg_series* s, bool g2, bool store, GramParams& gp, CUt
   gp.ring_koff = L->d_ring_koff;
   gp.ring_nkb = L->d_ring_nkb;
   gp.gram = reinterpret_cast<uint32_t*>(s->d_gram);
-  gp.ring_stride = s->tp * s->tp;
+  gp.ring_stride = slab_elems(s);
   gp.ld = static_cast<int32_t>(s->tp);
+  gp.nb = ttc_nb(s);
   gp.err = c->d_err;
   gp.max_norm2 = reinterpret_cast<const unsigned long long*>(s->d_max_norm2);
   gp.inv = s->d_inv;
@@ -978,7 +986,7 @@ static int raw_gram_setup(xg_series* s, bool g2, bool store, GramParams& gp, CUt
   s->raw_stored = store;
   if (!store)  // a valid (never written) map over the frames buffer
     return make_map_out32(c, &omap, s->d_x, 32, 32);
-  return make_map_out32(c, &omap, s->d_gram, s->tp, (int64_t)L->rings * s->tp);
+  return make_map_out32(c, &omap, s->d_gram, 256, (int64_t)L->rings * slab_elems(s) / 256);
 }
 
 int xg_ttc_raw(xg_series* s, uint32_t flags) {
@@ -1121,21 +1129,16 @@ int xg_series_export_partial(xg_series* s, int32_t ring, int32_t* gram, int64_t*
   xg_ctx* c = s->ctx;
   int rc = partial_check(s, ring, "export_partial");
   if (rc) return rc;
+  // the stored slab already is the exchange format (packed upper pair tiles)
   const int64_t elems = xg_series_partial_elems(s);
-  const int32_t nb = static_cast<int32_t>((s->t + 255) / 256);
-  int32_t* slab = s->d_gram + (int64_t)ring * s->tp * s->tp;
-  int32_t* dst = gram;
-  if (!on_device) XG_CUDA(c, dalloc(&dst, (size_t)elems));
-  cudaError_t e = launch_tiles_copy(slab, s->tp, nb, dst, 0, c->stream);
-  if (e == cudaSuccess && !on_device)
-    e = cudaMemcpyAsync(gram, dst, (size_t)elems * 4, cudaMemcpyDeviceToHost, c->stream);
+  const cudaMemcpyKind dir = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  cudaError_t e = cudaMemcpyAsync(gram, s->d_gram + (int64_t)ring * slab_elems(s),
+                                  (size_t)elems * 4, dir, c->stream);
   if (e == cudaSuccess)
-    e = cudaMemcpy2DAsync(norm2, 8, s->d_norm2 + ring, (size_t)s->L->rings * 8, 8, s->t,
-                          on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->stream);
+    e = cudaMemcpy2DAsync(norm2, 8, s->d_norm2 + ring, (size_t)s->L->rings * 8, 8, s->t, dir,
+                          c->stream);
   if (e == cudaSuccess && !on_device) e = cudaStreamSynchronize(c->stream);
-  if (!on_device) cudaFree(dst);
   if (e != cudaSuccess) return cuda_fail(c, e, "export_partial");
-  c->launches++;
   return on_device ? XG_OK : check_device_error(c);
 }
 
@@ -1147,18 +1150,10 @@ int xg_series_import_partial(xg_series* s, int32_t ring, const int32_t* gram, co
   int rc = partial_check(s, ring, "import_partial");
   if (rc) return rc;
   const int64_t elems = xg_series_partial_elems(s);
-  const int32_t nb = static_cast<int32_t>((s->t + 255) / 256);
-  int32_t* src = const_cast<int32_t*>(gram);
-  if (!on_device) {
-    XG_CUDA(c, dalloc(&src, (size_t)elems));
-    cudaError_t e = cudaMemcpyAsync(src, gram, (size_t)elems * 4, cudaMemcpyHostToDevice, c->stream);
-    if (e != cudaSuccess) {
-      cudaFree(src);
-      return cuda_fail(c, e, "import_partial");
-    }
-  }
-  cudaError_t e = launch_tiles_copy(s->d_gram + (int64_t)ring * s->tp * s->tp, s->tp, nb, src, 1,
-                                    c->stream);
+  cudaError_t e = cudaMemcpyAsync(s->d_gram + (int64_t)ring * slab_elems(s), gram,
+                                  (size_t)elems * 4,
+                                  on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                                  c->stream);
   if (e == cudaSuccess)
     e = cudaMemcpy2DAsync(s->d_norm2 + ring, (size_t)L->rings * 8, norm2, 8, 8, s->t,
                           on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->stream);
@@ -1188,13 +1183,9 @@ int xg_series_import_partial(xg_series* s, int32_t ring, const int32_t* gram, co
     np.ring_count = 1;
     e = launch_norms(np, c->stream);
   }
-  if (!on_device) {
-    const cudaError_t e2 = cudaStreamSynchronize(c->stream);
-    cudaFree(src);
-    if (e == cudaSuccess) e = e2;
-  }
+  if (!on_device && e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
   if (e != cudaSuccess) return cuda_fail(c, e, "import_partial");
-  c->launches += 2;
+  c->launches++;
   if (flags & XG_STRICT) {
     int64_t fz = 0;
     XG_CUDA(c, cudaMemcpyAsync(&fz, s->d_first_zero + ring, 8, cudaMemcpyDeviceToHost, c->stream));
@@ -1233,8 +1224,9 @@ int xg_series_rel_error(xg_series* s, double* out) {
   RelErrParams p;
   p.gram = s->d_gram;
   p.cgram = s->d_cgram;
-  p.ring_stride = s->tp * s->tp;
+  p.ring_stride = slab_elems(s);
   p.ld = static_cast<int32_t>(s->tp);
+  p.nb = ttc_nb(s);
   p.inv = s->d_inv;
   p.inv_ld = s->tp;
   p.n = s->t;
@@ -1272,10 +1264,11 @@ int xg_series_get_ttc(xg_series* s, int32_t ring, int32_t dtype, void* out, int6
     dst = tmp;
   }
   ExpandParams p;
-  p.gram = s->d_gram + (int64_t)ring * s->tp * s->tp;
+  p.gram = s->d_gram + (int64_t)ring * slab_elems(s);
   p.cf32 = nullptr;
   p.ring_stride = 0;
   p.ld = static_cast<int32_t>(s->tp);
+  p.nb = ttc_nb(s);
   p.inv = s->d_inv + (int64_t)ring * s->tp;
   p.n = s->t;
   p.out = dst;
@@ -1661,7 +1654,7 @@ int xg_series_build_basis(xg_series* s, int32_t k, double* const* v_out, double*
   }
   XG_CUDA(c, db.get(&d_state, (size_t)Q));
   BasisSParams sp{s->d_gram, static_cast<int32_t>(s->tp), s->d_inv, s->tp,
-                  static_cast<int32_t>(n), np, d_a[0], d_v[0]};
+                  static_cast<int32_t>(n), np, d_a[0], d_v[0], ttc_nb(s), slab_elems(s)};
   phase("gram");
   XG_CUDA(c, launch_basis_s(sp, Q, st));
   c->launches++;
@@ -2034,7 +2027,7 @@ int xg_ttc_compressed(xg_series* s, uint32_t flags) {
     s->cmp_g2 = true;
     return check_device_error(c);
   }
-  if (store && !s->d_cgram) XG_CUDA(c, dalloc(&s->d_cgram, (size_t)L->rings * s->tp * s->tp));
+  if (store && !s->d_cgram) XG_CUDA(c, dalloc(&s->d_cgram, (size_t)L->rings * slab_elems(s)));
   int rc = build_tiles(s);
   if (rc) return rc;
   CUtensorMap my;
@@ -2046,8 +2039,9 @@ int xg_ttc_compressed(xg_series* s, uint32_t flags) {
   gp.ring_koff = L->d_ring_koff;
   gp.ring_nkb = L->d_ring_nkb;
   gp.gram = reinterpret_cast<uint32_t*>(s->d_cgram);
-  gp.ring_stride = s->tp * s->tp;
+  gp.ring_stride = slab_elems(s);
   gp.ld = static_cast<int32_t>(s->tp);
+  gp.nb = ttc_nb(s);
   gp.err = c->d_err;
   gp.max_norm2 = reinterpret_cast<const unsigned long long*>(s->d_max_norm2);
   const bool g2 = !(flags & XG_NO_G2);
@@ -2070,7 +2064,7 @@ int xg_ttc_compressed(xg_series* s, uint32_t flags) {
   gp.store = store ? 1 : 0;
   s->cmp_stored = store;
   CUtensorMap omap;
-  rc = store ? make_map_out32(c, &omap, s->d_cgram, s->tp, (int64_t)L->rings * s->tp)
+  rc = store ? make_map_out32(c, &omap, s->d_cgram, 256, (int64_t)L->rings * slab_elems(s) / 256)
              : make_map_out32(c, &omap, s->d_x, 32, 32);
   if (rc) return rc;
   XG_CUDA(c, launch_gram_any(s, 1, my, omap, gp));
@@ -2106,7 +2100,8 @@ int xg_series_ttc_background(xg_series* s, int32_t which, int64_t exclusion, dou
   BgParams p;
   p.gram = which == 0 ? s->d_gram : nullptr;
   p.cgram = which == 0 ? nullptr : s->d_cgram;
-  p.ring_stride = s->tp * s->tp;
+  p.ring_stride = slab_elems(s);
+  p.nb = ttc_nb(s);
   p.ld = static_cast<int32_t>(s->tp);
   p.inv = s->d_inv;
   p.inv_ld = s->tp;
@@ -2200,7 +2195,8 @@ int xg_series_get_cttc(xg_series* s, int32_t ring, int32_t dtype, void* out, int
   }
   ExpandParams p;
   p.gram = nullptr;
-  p.cf32 = s->d_cgram + (int64_t)ring * s->tp * s->tp;
+  p.cf32 = s->d_cgram + (int64_t)ring * slab_elems(s);
+  p.nb = ttc_nb(s);
   p.ring_stride = 0;
   p.ld = static_cast<int32_t>(s->tp);
   p.inv = nullptr;
@@ -2719,8 +2715,9 @@ int xg_series_write_ttc(xg_series* s, int32_t ring, int32_t which, int32_t dtype
   XG_CUDA(c, cudaMalloc(&d_stage, cap));
   std::vector<uint8_t> h(cap);
   ExpandParams p;
-  p.gram = which == 0 ? s->d_gram + (int64_t)ring * s->tp * s->tp : nullptr;
-  p.cf32 = which == 0 ? nullptr : s->d_cgram + (int64_t)ring * s->tp * s->tp;
+  p.gram = which == 0 ? s->d_gram + (int64_t)ring * slab_elems(s) : nullptr;
+  p.cf32 = which == 0 ? nullptr : s->d_cgram + (int64_t)ring * slab_elems(s);
+  p.nb = ttc_nb(s);
   p.ring_stride = 0;
   p.ld = static_cast<int32_t>(s->tp);
   p.inv = s->d_inv + (int64_t)ring * s->tp;

@@ -10,6 +10,23 @@
 
 namespace xg {
 
+// Stored TTC (int32 Gram / f32 C~) of a series, one slab per ring: the upper
+// 256 x 256 pair tiles (I <= J) packed in (I, J) row-major tile order, each
+// tile row-major -- half the memory of a full T x T square, and the same
+// bytes as the split-ring exchange format.  nb = tiles per row (ceil(T/256)).
+// nb <= 0 selects a plain row-major square with leading dimension ld (the
+// streaming columns).  Requires a <= b (every reader takes the upper triangle).
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+inline int64_t ttc_off(int64_t a, int64_t b, int64_t ld, int32_t nb) {
+  if (nb <= 0) return a * ld + b;
+  const int64_t I = a >> 8, J = b >> 8;
+  return ((I * nb - (I * (I - 1)) / 2 + (J - I)) << 16) + ((a & 255) << 8) + (b & 255);
+}
+inline int64_t ttc_slab(int64_t nb) { return nb * (nb + 1) / 2 * 65536; }
+
+
 // ---------------------------------------------------------------- K1 ingest
 // A detector band (8192 pixels) is staged in shared memory as 512-byte pieces
 // at a 528-byte pitch (+16 zero bytes that padding entries point to).
@@ -105,6 +122,7 @@ struct GramParams {
   uint32_t* gram;            // [ring][ld][ld] exact int32 Gram / f32 C~ (upper tiles)
   int64_t ring_stride;
   int32_t ld;
+  int32_t nb = 0;            // packed-tile row length ceil(T/256) of the stored TTC
   int* err;                  // bit 0: pipeline timeout
   // fused g2 (null g2_partial = off): per tile, the sums over each tile
   // diagonal (j - i + 127 in [0, 383)) of C(i,j) = G_ij inv_i inv_j, j >= i
@@ -289,6 +307,7 @@ struct G2Params {
   const float* cf32;         // ... or an already normalised f32 C (mode 1)
   int64_t ring_stride;
   int32_t ld;
+  int32_t nb = 0;            // > 0: packed upper pair tiles (ttc_off), else ld-square
   const double* inv;         // [ring][inv_ld] (mode 0)
   int64_t inv_ld;
   int64_t n_frames;
@@ -303,11 +322,6 @@ struct G2Params {
 };
 cudaError_t launch_g2(const G2Params& p, int mode, cudaStream_t s);
 
-// Split-ring exchange format: the upper 256 x 256 pair tiles (I <= J) of one
-// ring's Gram slab, packed in (I, J) row-major tile order, tile rows
-// row-major.  dir 0: slab -> packed, 1: packed -> slab.
-cudaError_t launch_tiles_copy(int32_t* slab, int64_t ld, int32_t nb, int32_t* packed, int dir,
-                              cudaStream_t s);
 
 // ---------------------------------------------------- TTC readback expand
 struct ExpandParams {
@@ -315,6 +329,7 @@ struct ExpandParams {
   const float* cf32;         // mode f32 source (already normalised)
   int64_t ring_stride;
   int32_t ld;
+  int32_t nb = 0;            // > 0: packed upper pair tiles (ttc_off), else ld-square
   const double* inv;         // [n] for this ring
   int64_t n;
   void* out;
@@ -334,6 +349,7 @@ struct RelErrParams {
   const float* cgram;        // [ring][ld][ld] upper tiles
   int64_t ring_stride;
   int32_t ld;
+  int32_t nb = 0;            // > 0: packed upper pair tiles (ttc_off), else ld-square
   const double* inv;         // [ring][inv_ld]
   int64_t inv_ld;
   int64_t n;
@@ -352,6 +368,7 @@ struct BgParams {
   const float* cgram;        // compressed C~ (or null)
   int64_t ring_stride;
   int32_t ld;
+  int32_t nb = 0;            // > 0: packed upper pair tiles (ttc_off), else ld-square
   const double* inv;         // [ring][inv_ld]
   int64_t inv_ld;
   int64_t n;
@@ -481,13 +498,15 @@ struct JacParams {
 cudaError_t launch_jacobi_step(const JacParams& p, int n_rings, cudaStream_t s);
 
 struct BasisSParams {
-  const int32_t* gram;       // [ring][ld][ld] upper tiles
+  const int32_t* gram;       // stored Gram, ring slabs of ring_stride elements (ttc_off)
   int32_t ld;
   const double* inv;         // [ring][inv_ld]
   int64_t inv_ld;
   int32_t n, np;
   double* a;                 // [ring][np][np] slot layout of step 0
   double* v;                 // [ring][np][np] identity in slot layout
+  int32_t nb;                // packed-tile row length (ttc_off)
+  int64_t ring_stride;       // elements per ring slab
 };
 cudaError_t launch_basis_s(const BasisSParams& p, int n_rings, cudaStream_t s);
 // diag of the converged A (slot layout of step 0) -> eig [ring][np]
