@@ -259,14 +259,20 @@ class Env:
         self.torch = torch
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.rank = int(os.environ.get("RANK", "0"))
-        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        # one GPU per process; XPCS_BENCH_BACKEND=gloo lets several processes
+        # share one GPU to validate the sharded path (NCCL needs distinct GPUs)
+        self.backend = os.environ.get("XPCS_BENCH_BACKEND", "nccl")
+        self.local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
         torch.cuda.set_device(self.local)
         self.dev = torch.device("cuda", self.local)
         if self.world > 1:
             import torch.distributed as tdist
 
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-            tdist.init_process_group("nccl", device_id=self.dev)
+            if self.backend == "nccl":
+                tdist.init_process_group("nccl", device_id=self.dev)
+            else:
+                tdist.init_process_group(self.backend)
         import paper_2407_20356_b200 as xg
         from paper_2407_20356_b200 import dist
 
@@ -287,7 +293,8 @@ class Env:
     def max_over_ranks(self, *vals):
         if self.world == 1:
             return vals if len(vals) > 1 else vals[0]
-        t = self.torch.tensor([float(v) for v in vals], device=self.dev, dtype=self.torch.float64)
+        t = self.torch.tensor([float(v) for v in vals], dtype=self.torch.float64,
+                              device=self.dev if self.backend == "nccl" else "cpu")
         self.torch.distributed.all_reduce(t, op=self.torch.distributed.ReduceOp.MAX)
         out = tuple(float(x) for x in t)
         return out if len(out) > 1 else out[0]
@@ -353,7 +360,7 @@ class Shard:
         return (f"{E.world} GPUs: one detector sharded along q-ring boundaries (LPT on pixel "
                 f"counts, imbalance {self.plan.imbalance():.3%}, split rings {sp}); each GPU holds "
                 f"only its pixel slice; split-ring shares summed on the owner; g2 all-gathered "
-                f"(NCCL) inside the timed region")
+                f"({E.backend}) inside the timed region")
 
 
 def raw_step(E, sh, series, frames, rec=None, gather=True):

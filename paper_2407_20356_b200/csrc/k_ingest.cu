@@ -31,7 +31,7 @@ namespace xg {
 namespace {
 
 constexpr int INGEST_THREADS = 32 * INGEST_CONSUMERS;
-constexpr int NBUF = 4;  // frames in flight per CTA
+constexpr int NBUF = 4;  // frames in flight per CTA (6 / 8: slower at C2 and C5, fewer CTAs per SM)
 constexpr int FR = 2;    // frames per consumer pass (divides NBUF)
 static_assert(NBUF % FR == 0, "NBUF must be a multiple of FR");
 constexpr int PIECE = INGEST_PIECE, PITCH = INGEST_PITCH;
