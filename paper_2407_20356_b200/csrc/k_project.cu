@@ -34,10 +34,7 @@ constexpr int BK = 128;
 #ifndef XG_K3_KPS
 #define XG_K3_KPS 2
 #endif
-constexpr int KPS = XG_K3_KPS;
-#ifndef XG_K3_HINT
-#define XG_K3_HINT 1
-#endif  // 128-byte K blocks per pipeline stage (one wait/commit each)
+constexpr int KPS = XG_K3_KPS;  // 128-byte K blocks per pipeline stage (one wait/commit each)
 constexpr int MAX_STAGES = 6;
 constexpr int A_BYTES = BM * BK;    // 16 KB
 constexpr int TMEM_COLS = 512;
@@ -140,15 +137,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     if (elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
-      // several N-tiles (large k): the ring's digit rows are re-read by every
-      // frame block of the ring, the frame blocks by the ring's few N-tiles
-      // at once -- keep the digits, let the streamed frames go first
-      uint64_t pol_x = 0, pol_v = 0;
-      const bool hint = XG_K3_HINT && p.ntiles_n > 1;
-      if (hint) {
-        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_x));
-        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_v));
-      }
       for (int t = pair; t < p.ntiles; t += npairs) {
         const TileDesc td = p.tiles[t];
         const int koff = p.ring_koff[td.ring], nkb = p.ring_nkb[td.ring];
@@ -159,16 +147,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           if (leader) mbar_arrive_expect_tx(&tail->full[stage], nsub * sub_tx);
           for (int sub = 0; sub < nsub; ++sub) {
             const int kc = koff + (kb + sub) * BK;
-            if (hint) {
-              tma_load_2sm_hint(sA + (stage * KPS + sub) * A_BYTES, &tmX, &tail->full[stage], kc,
-                                td.i0 + BM * static_cast<int>(rank), pol_x);
-              tma_load_2sm_hint(sB + (stage * KPS + sub) * B_BYTES, &tmV, &tail->full[stage], kc,
-                                vrow, pol_v);
-            } else {
-              tma_load_2sm(sA + (stage * KPS + sub) * A_BYTES, &tmX, &tail->full[stage], kc,
-                           td.i0 + BM * static_cast<int>(rank));
-              tma_load_2sm(sB + (stage * KPS + sub) * B_BYTES, &tmV, &tail->full[stage], kc, vrow);
-            }
+            tma_load_2sm(sA + (stage * KPS + sub) * A_BYTES, &tmX, &tail->full[stage], kc,
+                         td.i0 + BM * static_cast<int>(rank));
+            tma_load_2sm(sB + (stage * KPS + sub) * B_BYTES, &tmV, &tail->full[stage], kc, vrow);
           }
           if (++stage == STAGES) {
             stage = 0;

@@ -1521,7 +1521,6 @@ static int compress_rows(xg_series* s, xg_basis* B, int64_t t0, int64_t n) {
   p.ring_nkb = L->d_ring_nkb;
   p.n_digits = B->digits;
   p.kt = B->kt;
-  p.ntiles_n = B->ntiles_n;
   p.k = B->k;
   p.inv = s->d_inv;
   p.inv_ld = s->tp;

@@ -198,7 +198,6 @@ struct ProjParams {
   const int32_t* ring_nkb;
   int32_t n_digits;          // S in {1, 2, 3}
   int32_t kt;                // coefficients per N-tile (multiple of 16, S*kt <= 256)
-  int32_t ntiles_n;          // N-tiles per ring (ceil(k / kt))
   int32_t k;                 // rank
   const double* inv;         // [ring][inv_ld] 1/|x_t|
   int64_t inv_ld;

@@ -190,16 +190,6 @@ __device__ __forceinline__ void cluster_sync() {
                    : "memory");
 }
 
-// the same with an L2 cache policy (createpolicy)
-__device__ __forceinline__ void tma_load_2sm_hint(void* dst, const CUtensorMap* map, uint64_t* bar,
-                                                  int32_t c0, int32_t c1, uint64_t pol) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-      ".L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & kPeerMask), "r"(c0), "r"(c1),
-      "l"(pol)
-      : "memory");
-}
 __device__ __forceinline__ void tma_load_2sm(void* dst, const CUtensorMap* map, uint64_t* bar,
                                              int32_t c0, int32_t c1) {
   asm volatile(
