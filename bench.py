@@ -327,7 +327,7 @@ class Shard:
         if E.world == 1:
             self.pixels = None
             self.rings = list(range(Q))
-            self.layout = xg.RingLayout(E.ctx, H * W, self.masks)
+            self.layout = xg.RingLayout(E.ctx, H * W, self.masks, shape=(H, W))
         else:
             self.pixels, local, self.rings = dist.rank_slice(self.plan, E.rank, self.masks)
             self.layout = xg.RingLayout(E.ctx, int(self.pixels.size), local)

@@ -96,6 +96,14 @@ XG_API int64_t xg_kernel_launches(const xg_ctx* ctx);
 XG_API int xg_layout_create(xg_ctx* ctx, int64_t full_pixels, int32_t n_rings,
                      const int64_t* mask_offsets, const int64_t* mask_indices,
                      xg_layout** out);
+/* The same for a height x width row-major detector (full_pixels = height *
+ * width): on a detector wider than 512 pixels the ingest reads 32-row x
+ * 512-column blocks instead of 16384-pixel raster strips, so each band holds
+ * longer pieces of every annulus (the ring-major column order differs;
+ * every result is the same). */
+XG_API int xg_layout_create_2d(xg_ctx* ctx, int64_t height, int64_t width, int32_t n_rings,
+                               const int64_t* mask_offsets, const int64_t* mask_indices,
+                               xg_layout** out);
 XG_API void xg_layout_destroy(xg_layout* layout);
 XG_API int64_t xg_layout_ring_pixels(const xg_layout* layout, int32_t ring);
 

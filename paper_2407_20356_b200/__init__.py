@@ -270,26 +270,43 @@ class RingLayout:
     """A set of q-ring ``PixelMask``s (model.hpp:16-24) over a detector of
     ``full_pixels`` pixels.  ``masks[r]`` are strictly ascending indices."""
 
-    def __init__(self, ctx: Context, full_pixels: int, masks: Sequence[np.ndarray]):
+    def __init__(self, ctx: Context, full_pixels: int, masks: Sequence[np.ndarray],
+                 shape: tuple | None = None):
+        """``shape`` = (height, width) of a row-major detector (full_pixels =
+        height * width): on a detector wider than 512 pixels the ingest then
+        reads 2D blocks (xg_layout_create_2d); results are identical."""
         self.ctx = ctx
         self.full_pixels = int(full_pixels)
+        if shape is not None and int(shape[0]) * int(shape[1]) != self.full_pixels:
+            raise ShapeError(f"shape {tuple(shape)} does not hold {self.full_pixels} pixels")
+        self.shape = tuple(int(v) for v in shape) if shape is not None else None
         self.masks = [np.ascontiguousarray(m, dtype=np.int64) for m in masks]
         offs = np.zeros(len(self.masks) + 1, np.int64)
         offs[1:] = np.cumsum([m.size for m in self.masks])
         idx = np.concatenate(self.masks) if self.masks else np.zeros(0, np.int64)
         idx = np.ascontiguousarray(idx, dtype=np.int64)
         h = C.c_void_p()
-        _check(ctx.h, lib.xg_layout_create(ctx.h, self.full_pixels, len(self.masks),
-                                           offs.ctypes.data_as(_abi.PI64),
-                                           idx.ctypes.data_as(_abi.PI64), C.byref(h)))
+        if self.shape is not None:
+            _check(ctx.h, lib.xg_layout_create_2d(ctx.h, self.shape[0], self.shape[1],
+                                                  len(self.masks), offs.ctypes.data_as(_abi.PI64),
+                                                  idx.ctypes.data_as(_abi.PI64), C.byref(h)))
+        else:
+            _check(ctx.h, lib.xg_layout_create(ctx.h, self.full_pixels, len(self.masks),
+                                               offs.ctypes.data_as(_abi.PI64),
+                                               idx.ctypes.data_as(_abi.PI64), C.byref(h)))
         self.h = h
 
     @classmethod
-    def from_ring_map(cls, ctx: Context, ring_of_pixel: np.ndarray, n_rings: int):
-        """Masks from a per-pixel ring index (-1 = no ring)."""
-        rp = np.asarray(ring_of_pixel).ravel()
+    def from_ring_map(cls, ctx: Context, ring_of_pixel: np.ndarray, n_rings: int,
+                      shape: tuple | None = None):
+        """Masks from a per-pixel ring index (-1 = no ring); a 2D map (or
+        ``shape``) gives the detector geometry to the ingest."""
+        rp = np.asarray(ring_of_pixel)
+        if shape is None and rp.ndim == 2:
+            shape = rp.shape
+        rp = rp.ravel()
         masks = [np.nonzero(rp == r)[0] for r in range(n_rings)]
-        return cls(ctx, rp.size, masks)
+        return cls(ctx, rp.size, masks, shape=shape)
 
     @property
     def n_rings(self) -> int:

@@ -39,6 +39,7 @@ _sigs = {
     "xg_synchronize": (C.c_int, [P]),
     "xg_kernel_launches": (I64, [P]),
     "xg_layout_create": (C.c_int, [P, I64, I32, PI64, PI64, C.POINTER(P)]),
+    "xg_layout_create_2d": (C.c_int, [P, I64, I64, I32, PI64, PI64, C.POINTER(P)]),
     "xg_layout_destroy": (None, [P]),
     "xg_layout_ring_pixels": (I64, [P, I32]),
     "xg_series_create": (C.c_int, [P, P, I64, C.POINTER(P)]),

@@ -200,7 +200,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
           atomicAdd(p.wave_ctr, 1u);
         }
         const TileDesc td = p.tiles[t];
-        const int koff = MODE == 0 ? p.ring_koff[td.ring] : 0;
+        // raw: the ring's own block of x (ring-blocked, per-ring TMA map)
+        const CUtensorMap* mapA = MODE == 0 ? p.xmaps + td.ring : &tmX;
         // K4: per 64-coefficient block, one stage per bf16 plane (A and B
         // rows of that plane); the MMA warp forms every precision pair from
         // the resident planes, so each plane block is fetched once, not once
@@ -211,7 +212,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
           if (leader) mbar_arrive_expect_tx(&tail->full[stage], 2 * STAGE_BYTES);
           int kc, ra, rb;
           if (MODE == 0) {
-            kc = koff + kb * BK;
+            kc = kb * BK;
             ra = td.i0 + 128 * rank;
             rb = td.j0 + 128 * rank;
           } else {
@@ -220,8 +221,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
             ra = (td.ring * 3 + q) * p.plane_rows + td.i0 + 128 * rank;
             rb = (td.ring * 3 + q) * p.plane_rows + td.j0 + 128 * rank;
           }
-          tma_load_2sm(sA + stage * A_BYTES, &tmX, &tail->full[stage], kc, ra);
-          tma_load_2sm(sB + stage * B_BYTES, &tmX, &tail->full[stage], kc, rb);
+          tma_load_2sm(sA + stage * A_BYTES, mapA, &tail->full[stage], kc, ra);
+          tma_load_2sm(sB + stage * B_BYTES, mapA, &tail->full[stage], kc, rb);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;

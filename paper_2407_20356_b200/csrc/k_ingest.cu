@@ -104,11 +104,25 @@ __global__ void __launch_bounds__(INGEST_THREADS + 32)
   if (threadIdx.x < NBUF * 4)
     reinterpret_cast<uint32_t*>(bufs + (threadIdx.x >> 2) * bstride + zero_at)[threadIdx.x & 3] = 0;
 
-  const int64_t pix0 = static_cast<int64_t>(b) * p.band;
-  const int blen = static_cast<int>((p.pixels - pix0) < p.band ? (p.pixels - pix0) : p.band);
+  // 1D band: pixels [pix0, pix0 + blen).  2D band: rows [y0, y0 + rows) x
+  // columns [x0, x0 + bw) of a width-wide detector, pix0 = its first pixel,
+  // one piece per row.
+  const bool two_d = p.width > 0;
+  int64_t pix0;
+  int blen, rows = 0, bw = 0;
+  if (two_d) {
+    const int y0 = (b / p.blocks_x) * kBandH, x0 = (b % p.blocks_x) * kBandW;
+    rows = min(kBandH, p.height - y0);
+    bw = min(kBandW, p.width - x0);
+    pix0 = static_cast<int64_t>(y0) * p.width + x0;
+    blen = rows * bw;
+  } else {
+    pix0 = static_cast<int64_t>(b) * p.band;
+    blen = static_cast<int>((p.pixels - pix0) < p.band ? (p.pixels - pix0) : p.band);
+  }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const bool bulk = ((p.pixels | blen) & 15) == 0 &&
-                    (reinterpret_cast<uintptr_t>(p.raster) & 15) == 0;
+  const bool bulk = ((two_d ? (p.width | bw) : (p.pixels | blen)) & 15) == 0 &&
+                    (p.pixels & 15) == 0 && (reinterpret_cast<uintptr_t>(p.raster) & 15) == 0;
 
   const int64_t f_begin = static_cast<int64_t>(blockIdx.y) * p.frames_per_cta;
   int64_t f_end = f_begin + p.frames_per_cta;
@@ -158,14 +172,33 @@ __global__ void __launch_bounds__(INGEST_THREADS + 32)
                        : "memory");
         __syncwarp();
         // one piece per lane: the band's bulk copies are issued in parallel
-        for (int o = lane * PIECE; o < blen; o += 32 * PIECE) {
-          const int len = blen - o < PIECE ? blen - o : PIECE;
-          asm volatile(
-              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], "
-              "%2, [%3];" ::"r"(smem_addr(dst + (o / PIECE) * PITCH)),
-              "l"(src + o), "r"(len), "r"(smem_addr(&full[slot]))
-              : "memory");
+        if (two_d) {
+          for (int rr = lane; rr < rows; rr += 32)
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], "
+                "%2, [%3];" ::"r"(smem_addr(dst + rr * PITCH)),
+                "l"(src + static_cast<int64_t>(rr) * p.width), "r"(bw),
+                "r"(smem_addr(&full[slot]))
+                : "memory");
+        } else {
+          for (int o = lane * PIECE; o < blen; o += 32 * PIECE) {
+            const int len = blen - o < PIECE ? blen - o : PIECE;
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], "
+                "%2, [%3];" ::"r"(smem_addr(dst + (o / PIECE) * PITCH)),
+                "l"(src + o), "r"(len), "r"(smem_addr(&full[slot]))
+                : "memory");
+          }
         }
+      } else if (two_d) {
+        for (int k = lane; k < blen; k += 32) {
+          const int rr = k / bw, cc = k % bw;
+          dst[rr * PITCH + cc] = src[static_cast<int64_t>(rr) * p.width + cc];
+        }
+        __syncwarp();
+        if (lane == 0)
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&full[slot]))
+                       : "memory");
       } else {
         for (int k = lane; k < blen; k += 32) dst[ingest_smem_offset(k)] = src[k];
         __syncwarp();
@@ -189,7 +222,7 @@ __global__ void __launch_bounds__(INGEST_THREADS + 32)
     const int slot = static_cast<int>(i % NBUF);  // FR consecutive slots
     const int nfr = nf - i < FR ? static_cast<int>(nf - i) : FR;
     uint32_t band_s[FR];
-    uint8_t* xrow[FR];
+    int64_t xrow[FR];  // frame's row within its ring block
     unsigned long long* nrow[FR];
 #pragma unroll
     for (int f = 0; f < FR; ++f) {
@@ -197,12 +230,17 @@ __global__ void __launch_bounds__(INGEST_THREADS + 32)
       if (f < nfr) wait(&full[slot + f], static_cast<uint32_t>(((i + f) / NBUF) & 1));
       band_s[f] = bufs_s + (slot + ff) * bstride;
       const int64_t t = p.t0 + f_begin + i + ff;
-      xrow[f] = p.x + (t - p.x_row0) * p.ktot;
+      xrow[f] = t - p.x_row0;
       nrow[f] = p.norm2 + t * p.n_rings;
       asm volatile("" : "+l"(xrow[f]), "+l"(nrow[f]));  // once per frame, not per piece
     }
     for (int k = k0; k < k1; ++k) {
       const int4 pa = spieces[2 * k], pb = spieces[2 * k + 1];  // see Piece
+      // the piece's output: row xrow[f] of its ring's block (ring-blocked x)
+      uint8_t* xseg[FR];
+#pragma unroll
+      for (int f = 0; f < FR; ++f)
+        xseg[f] = p.x + p.xmax * pb.z + xrow[f] * pb.w + (pa.y - pb.z);
       uint32_t sq[FR];
 #pragma unroll
       for (int f = 0; f < FR; ++f) sq[f] = 0;
@@ -214,12 +252,12 @@ __global__ void __launch_bounds__(INGEST_THREADS + 32)
 #pragma unroll
         for (int f = 0; f < FR; ++f) {
           const uint32_t word = lds_u32(band_s[f] + w4);
-          if (f < nfr) stg_u32(xrow[f] + pa.y + 4 * g, word);
+          if (f < nfr) stg_u32(xseg[f] + 4 * g, word);
           sq[f] = __dp4a(word, word, sq[f]);
         }
       }
       // leftover pixels: 4-byte gather
-      const int ob = pa.y + 4 * pa.z;
+      const int ob = 4 * pa.z;
       const uint32_t bt = bytes_s + 8u * static_cast<uint32_t>(pb.y);
 #pragma unroll 1
       for (int g = lane; g < pb.x; g += 32) {
@@ -230,7 +268,7 @@ __global__ void __launch_bounds__(INGEST_THREADS + 32)
           const uint32_t v0 = lds_u8(band_s[f] + o0), v1 = lds_u8(band_s[f] + o1);
           const uint32_t v2 = lds_u8(band_s[f] + o2), v3 = lds_u8(band_s[f] + o3);
           const uint32_t word = prmt(v0 | (v1 << 8), v2 | (v3 << 8), 0x5410);
-          if (f < nfr) stg_u32(xrow[f] + ob + 4 * g, word);
+          if (f < nfr) stg_u32(xseg[f] + ob + 4 * g, word);
           sq[f] = __dp4a(word, word, sq[f]);
         }
       }

@@ -139,17 +139,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       uint32_t phase = 0;
       for (int t = pair; t < p.ntiles; t += npairs) {
         const TileDesc td = p.tiles[t];
-        const int koff = p.ring_koff[td.ring], nkb = p.ring_nkb[td.ring];
+        const int nkb = p.ring_nkb[td.ring];
         const int vrow = td.j0 * nt_rows + static_cast<int>(rank) * half_rows;
+        // the ring's own blocks of x and of the digits (ring-blocked layouts)
+        const CUtensorMap* mapX = p.xmaps + td.ring;
+        const CUtensorMap* mapV = p.vmaps + td.ring;
         for (int kb = 0; kb < nkb; kb += KPS) {
           if (!mbar_wait(&tail->empty[stage], phase ^ 1, p.err)) goto done;
           const int nsub = nkb - kb < KPS ? nkb - kb : KPS;
           if (leader) mbar_arrive_expect_tx(&tail->full[stage], nsub * sub_tx);
           for (int sub = 0; sub < nsub; ++sub) {
-            const int kc = koff + (kb + sub) * BK;
-            tma_load_2sm(sA + (stage * KPS + sub) * A_BYTES, &tmX, &tail->full[stage], kc,
+            const int kc = (kb + sub) * BK;
+            tma_load_2sm(sA + (stage * KPS + sub) * A_BYTES, mapX, &tail->full[stage], kc,
                          td.i0 + BM * static_cast<int>(rank));
-            tma_load_2sm(sB + (stage * KPS + sub) * B_BYTES, &tmV, &tail->full[stage], kc, vrow);
+            tma_load_2sm(sB + (stage * KPS + sub) * B_BYTES, mapV, &tail->full[stage], kc, vrow);
           }
           if (++stage == STAGES) {
             stage = 0;

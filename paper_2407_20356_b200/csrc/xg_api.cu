@@ -76,6 +76,7 @@ struct xg_layout {
   uint16_t* d_bytes = nullptr;
   int32_t* d_ring_koff = nullptr;
   int32_t* d_ring_nkb = nullptr;
+  int32_t width = 0, height = 0, blocks_x = 0;  // 2D bands (xg_layout_create_2d)
 };
 
 struct xg_series {
@@ -130,6 +131,8 @@ struct xg_series {
   int32_t n_ptiles = 0;
   int64_t ptiles_key = -1;
   unsigned int* d_wave = nullptr;  // K2 wave-gate counter (zeroed before each launch)
+  CUtensorMap* d_xmaps = nullptr;  // per-ring TMA maps of the ring blocks of x
+  int64_t xmaps_rows = -1;         // frame rows they were encoded for (zero fill beyond)
 };
 
 struct xg_basis {
@@ -140,8 +143,9 @@ struct xg_basis {
   std::vector<int8_t> h_vd;        // [vrows][ktot]
   std::vector<double> h_scale;     // [rings][k]
   std::vector<uint8_t> ring_set;
-  int8_t* d_vd = nullptr;
+  int8_t* d_vd = nullptr;           // ring-blocked digits: ring q at vrows koff_q, [vrows][kpad_q]
   double* d_scale = nullptr;
+  CUtensorMap* d_vmaps = nullptr;   // per-ring TMA maps of the digit blocks
   bool dirty = true;
 };
 
@@ -241,6 +245,26 @@ int make_map_u8(xg_ctx* c, CUtensorMap* map, const void* base, int64_t cols, int
                          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(c, XG_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return XG_OK;
+}
+
+// Per-ring 2D TMA maps (128-byte x box_rows boxes, 128B swizzle) of ring-
+// blocked u8 data: ring q's block starts at base + rows_cap * koff_q and holds
+// `rows` valid rows of kpad_q bytes (rows beyond read as zeros).  Encoded on
+// the host and copied (stream-ordered) to the device array *dev.
+int upload_ring_maps(xg_ctx* c, const xg_layout* L, const uint8_t* base, int64_t rows_cap,
+                     int64_t rows, uint32_t box_rows, CUtensorMap** dev) {
+  std::vector<CUtensorMap> maps(static_cast<size_t>(L->rings));
+  for (int32_t r = 0; r < L->rings; ++r) {
+    const int rc = make_map_u8(c, &maps[r], base + rows_cap * L->koff[r], L->kpad[r], rows,
+                               L->kpad[r], 128, box_rows);
+    if (rc) return rc;
+  }
+  if (!*dev) XG_CUDA(c, dalloc(dev, maps.size()));
+  // pageable source: staged before the call returns; stream-ordered after
+  // every earlier kernel that read the previous maps
+  XG_CUDA(c, cudaMemcpyAsync(*dev, maps.data(), maps.size() * sizeof(CUtensorMap),
+                             cudaMemcpyHostToDevice, c->stream));
   return XG_OK;
 }
 
@@ -352,8 +376,13 @@ int xg_synchronize(xg_ctx* c) {
 int64_t xg_kernel_launches(const xg_ctx* c) { return c ? c->launches : -1; }
 
 // ------------------------------------------------------------------ layout
-int xg_layout_create(xg_ctx* c, int64_t full_pixels, int32_t n_rings, const int64_t* offsets,
-                     const int64_t* indices, xg_layout** out) {
+// Layout builder.  width > 0 (a height x width row-major detector wider than
+// one 512-pixel piece): K1 bands are blocks of 32 rows x 512 columns, else
+// 16384-pixel raster strips.  A ring's pixels in one band form one segment
+// of its ring-major row.
+static int layout_build(xg_ctx* c, int64_t full_pixels, int64_t height, int64_t width,
+                        int32_t n_rings, const int64_t* offsets, const int64_t* indices,
+                        xg_layout** out) {
   if (!c || !out || !offsets || !indices) return XG_ERR_INVALID;
   *out = nullptr;
   if (full_pixels < 1) return fail(c, XG_ERR_CONTRACT, "layout: full_pixels must be >= 1");
@@ -375,17 +404,38 @@ int xg_layout_create(xg_ctx* c, int64_t full_pixels, int32_t n_rings, const int6
   L->ctx = c;
   L->pixels = full_pixels;
   L->rings = n_rings;
-  // 16384-pixel row strips: a consumer pass moves twice the bytes of an 8192
+  // 16384-pixel bands: a consumer pass moves twice the bytes of an 8192
   // band for the same bookkeeping (measured: K1 0.475 -> 0.441 ms at C2;
-  // 4096 and >= 24576 are slower: fewer passes vs fewer CTAs per SM).  128 x
-  // 128-pixel 2D blocks were tried and are slower (C2 0.40 -> 0.90 ms, C5
-  // 8.8 -> 10.8 ms per 4096 frames): an annulus crosses a square block in
-  // short row runs, so far fewer of its pixels form whole aligned words.
-  L->band = static_cast<int32_t>(std::min<int64_t>(16384, round_up(full_pixels, 16)));
-  L->n_bands = static_cast<int32_t>((full_pixels + L->band - 1) / L->band);
+  // 4096 and >= 24576 are slower: fewer passes vs fewer CTAs per SM).  On a
+  // wide detector a 16384-pixel raster strip is only 16384 / W rows tall, so
+  // an annulus crosses it in many short segments (C5: 8 rows, ~200 segments
+  // per band, K1 at 0.45 of HBM): 2D bands of 32 rows x 512 columns keep the
+  // segments as long as on a 512-wide detector (the band of C2), and keep
+  // the shared-memory layout (one 512-byte piece per row).  128 x 128 blocks
+  // were slower (short row runs -> few whole words: C5 8.8 -> 10.8 ms).
+  const bool two_d = width > kBandW && width % 16 == 0;
+  if (two_d) {
+    L->width = static_cast<int32_t>(width);
+    L->height = static_cast<int32_t>(height);
+    L->blocks_x = static_cast<int32_t>((width + kBandW - 1) / kBandW);
+    L->band = kBandH * kBandW;
+    L->n_bands = L->blocks_x * static_cast<int32_t>((height + kBandH - 1) / kBandH);
+  } else {
+    L->band = static_cast<int32_t>(std::min<int64_t>(16384, round_up(full_pixels, 16)));
+    L->n_bands = static_cast<int32_t>((full_pixels + L->band - 1) / L->band);
+  }
   const int32_t nb = L->n_bands;
-  auto band_of = [&](int64_t px) -> int32_t { return static_cast<int32_t>(px / L->band); };
-  auto e_of = [&](int64_t px) -> int32_t { return static_cast<int32_t>(px % L->band); };
+  // band of a detector pixel and its index e inside the band (2D: row-major
+  // in a 512-wide block, so e's shared-memory byte is ingest_smem_offset(e)
+  // in both forms)
+  auto band_of = [&](int64_t px) -> int32_t {
+    if (!two_d) return static_cast<int32_t>(px / L->band);
+    return static_cast<int32_t>((px / width) / kBandH * L->blocks_x + (px % width) / kBandW);
+  };
+  auto e_of = [&](int64_t px) -> int32_t {
+    if (!two_d) return static_cast<int32_t>(px % L->band);
+    return static_cast<int32_t>((px / width) % kBandH * kBandW + (px % width) % kBandW);
+  };
   auto smem_of = [&](int32_t e) -> int32_t { return ingest_smem_offset(e); };
   // mask entries bucketed by band: ring order, ascending inside a ring
   std::vector<int64_t> cnt(static_cast<size_t>(n_rings) * nb, 0);
@@ -525,6 +575,8 @@ int xg_layout_create(xg_ctx* c, int64_t full_pixels, int32_t n_rings, const int6
           pc.word_off = s.woff + std::min(j0, s.nw);
           pc.n_byte = (j1 - j0) - pc.n_word;
           pc.byte_off = s.boff + std::max(0, j0 - s.nw);
+          pc.koff = static_cast<int32_t>(L->koff[s.ring]);
+          pc.kpad = static_cast<int32_t>(L->kpad[s.ring]);
           pieces.push_back(pc);
         }
         if (j1 < ng) { j0 = j1; break; }
@@ -578,6 +630,19 @@ int xg_layout_create(xg_ctx* c, int64_t full_pixels, int32_t n_rings, const int6
   }
   *out = L;
   return XG_OK;
+}
+
+int xg_layout_create(xg_ctx* c, int64_t full_pixels, int32_t n_rings, const int64_t* offsets,
+                     const int64_t* indices, xg_layout** out) {
+  return layout_build(c, full_pixels, 0, 0, n_rings, offsets, indices, out);
+}
+
+int xg_layout_create_2d(xg_ctx* c, int64_t height, int64_t width, int32_t n_rings,
+                        const int64_t* offsets, const int64_t* indices, xg_layout** out) {
+  if (!c) return XG_ERR_INVALID;
+  if (height < 1 || width < 1 || height > INT32_MAX || width > INT32_MAX)
+    return fail(c, XG_ERR_CONTRACT, "layout: detector height and width must be >= 1");
+  return layout_build(c, height * width, height, width, n_rings, offsets, indices, out);
 }
 
 void xg_layout_destroy(xg_layout* L) {
@@ -677,6 +742,7 @@ void xg_series_destroy(xg_series* s) {
   dfree(s->d_cg2cnt);
   dfree(s->d_ptiles);
   dfree(s->d_wave);
+  dfree(s->d_xmaps);
   delete s;
 }
 
@@ -687,6 +753,15 @@ int64_t xg_series_frames(const xg_series* s) { return s ? s->t : -1; }
 // frames use ttc_nb(s) per row.
 static int64_t slab_elems(const xg_series* s) { return ttc_slab(s->tp / 256); }
 static int32_t ttc_nb(const xg_series* s) { return static_cast<int32_t>((s->t + 255) / 256); }
+
+// Per-ring TMA maps of the series' ring blocks for `rows` valid frames.
+static int ensure_xmaps(xg_series* s, int64_t rows) {
+  if (s->xmaps_rows == rows && s->d_xmaps) return XG_OK;
+  const int rc = upload_ring_maps(s->ctx, s->L, s->d_x, s->xmax, rows, 128, &s->d_xmaps);
+  if (rc) return rc;
+  s->xmaps_rows = rows;
+  return XG_OK;
+}
 
 // The staging raster for frames that arrive from host memory.
 static int ensure_raster(xg_series* s) {
@@ -716,6 +791,7 @@ static int ingest_range(xg_series* s, const uint8_t* raster, int64_t t0, int64_t
   IngestParams p;
   p.raster = raster;
   p.x = s->d_x;
+  p.xmax = s->xmax;
   p.pixels = L->pixels;
   p.ktot = L->ktot;
   p.band = L->band;
@@ -733,6 +809,9 @@ static int ingest_range(xg_series* s, const uint8_t* raster, int64_t t0, int64_t
   p.t0 = t0;
   p.x_row0 = s->x_row0;
   p.n_frames = n;
+  p.width = L->width;
+  p.height = L->height;
+  p.blocks_x = L->blocks_x;
   // one wave of ~4 resident CTAs per SM, each streaming a run of frames of one band
   const int64_t want = std::max<int64_t>(1, (int64_t)c->num_sms * 4 / std::max(1, L->n_bands));
   p.frames_per_cta = static_cast<int32_t>(std::max<int64_t>(1, (n + want - 1) / want));
@@ -963,8 +1042,12 @@ static int raw_gram_setup(xg_series* s, bool g2, bool store, GramParams& gp, CUt
     XG_CUDA(c, dalloc(&s->d_gram, (size_t)L->rings * slab_elems(s)));
   int rc = build_tiles(s);
   if (rc) return rc;
-  rc = make_map_u8(c, &map, s->d_x, L->ktot, s->t, L->ktot, 128, 128);
+  rc = ensure_xmaps(s, s->t);
   if (rc) return rc;
+  // the kernel's parameter map is unused in raw mode (per-ring maps above)
+  rc = make_map_u8(c, &map, s->d_x, L->kpad[0], s->t, L->kpad[0], 128, 128);
+  if (rc) return rc;
+  gp.xmaps = s->d_xmaps;
   gp.tiles = s->d_tiles;
   gp.ntiles = s->ntiles;
   gp.ring_koff = L->d_ring_koff;
@@ -1410,6 +1493,7 @@ void xg_basis_destroy(xg_basis* B) {
   if (!B) return;
   dfree(B->d_vd);
   dfree(B->d_scale);
+  dfree(B->d_vmaps);
   delete B;
 }
 
@@ -1438,7 +1522,8 @@ int xg_basis_set_ring(xg_basis* B, int32_t ring, const double* v) {
         double d = std::nearbyint(u);
         d = std::min(127.0, std::max(-127.0, d));
         const int64_t row = (nt * B->digits + s) * B->kt + jj;
-        B->h_vd[(size_t)(row * L->ktot + col[i])] = static_cast<int8_t>(d);
+        B->h_vd[(size_t)(B->vrows * L->koff[ring] + row * L->kpad[ring] +
+                         (col[i] - L->koff[ring]))] = static_cast<int8_t>(d);
         u = (u - d) * 254.0;
       }
     }
@@ -1467,16 +1552,28 @@ static int strict_zero_check(xg_series* s, const char* what) {
   return XG_OK;
 }
 
+// Digits, scales and the per-ring digit maps of a basis to the device (once
+// per change of the basis).
+static int basis_upload(xg_basis* B) {
+  if (!B->dirty) return XG_OK;
+  xg_ctx* c = B->ctx;
+  XG_CUDA(c, cudaMemcpy(B->d_vd, B->h_vd.data(), B->h_vd.size(), cudaMemcpyHostToDevice));
+  XG_CUDA(c, cudaMemcpy(B->d_scale, B->h_scale.data(), B->h_scale.size() * 8,
+                        cudaMemcpyHostToDevice));
+  // one box = a CTA's half of the S*kt digit rows of an N-tile
+  const int rc = upload_ring_maps(c, B->L, reinterpret_cast<const uint8_t*>(B->d_vd), B->vrows,
+                                  B->vrows, static_cast<uint32_t>(B->digits * B->kt / 2),
+                                  &B->d_vmaps);
+  if (rc) return rc;
+  B->dirty = false;
+  return XG_OK;
+}
+
 // K3 over the n ring-major rows in x, which hold series frames [t0, t0 + n).
 static int compress_rows(xg_series* s, xg_basis* B, int64_t t0, int64_t n) {
   xg_ctx* c = s->ctx;
   const xg_layout* L = s->L;
-  if (B->dirty) {
-    XG_CUDA(c, cudaMemcpy(B->d_vd, B->h_vd.data(), B->h_vd.size(), cudaMemcpyHostToDevice));
-    XG_CUDA(c, cudaMemcpy(B->d_scale, B->h_scale.data(), B->h_scale.size() * 8,
-                          cudaMemcpyHostToDevice));
-    B->dirty = false;
-  }
+  if (int rc0 = basis_upload(B)) return rc0;
   const int32_t kp = static_cast<int32_t>(round_up(B->k, 64));
   if (s->ck != B->k || !s->d_y) {
     dfree(s->d_y);
@@ -1496,6 +1593,19 @@ static int compress_rows(xg_series* s, xg_basis* B, int64_t t0, int64_t n) {
       for (int64_t ib = 0; ib < nbi; ++ib)
         for (int32_t nt = 0; nt < B->ntiles_n; ++nt)
           tiles.push_back({r, (int32_t)(ib * 256), nt, 0});
+    // The persistent kernel deals tile t to pair t mod P.  A tile costs its
+    // ring's K (ring widths span 150x at C5), and a ring has fewer tiles than
+    // there are pairs, so the dealt sums drift apart: order the tiles by
+    // cost (descending, stable) and deal them in a snake (pairs 0..P-1, then
+    // P-1..0, ...), which keeps every pair's total within one tile's cost.
+    const int64_t P = std::max(1, c->num_sms / 2);
+    std::stable_sort(tiles.begin(), tiles.end(), [&](const TileDesc& a, const TileDesc& b) {
+      return L->kpad[a.ring] > L->kpad[b.ring];
+    });
+    for (size_t r0 = 0; r0 < tiles.size(); r0 += 2 * P) {  // reverse every second round
+      const size_t a = std::min(tiles.size(), r0 + P), b = std::min(tiles.size(), r0 + 2 * P);
+      if (a < b && b - a == (size_t)P) std::reverse(tiles.begin() + a, tiles.begin() + b);
+    }
     dfree(s->d_ptiles);
     XG_CUDA(c, dalloc(&s->d_ptiles, tiles.size()));
     XG_CUDA(c, cudaMemcpy(s->d_ptiles, tiles.data(), tiles.size() * sizeof(TileDesc),
@@ -1504,14 +1614,15 @@ static int compress_rows(xg_series* s, xg_basis* B, int64_t t0, int64_t n) {
     s->ptiles_key = key;
   }
   CUtensorMap mx, mv, mp;
-  int rc = make_map_u8(c, &mx, s->d_x, L->ktot, n, L->ktot, 128, 128);
+  int rc = ensure_xmaps(s, n);
+  if (!rc) rc = make_map_u8(c, &mx, s->d_x, L->kpad[0], n, L->kpad[0], 128, 128);  // unused
   // bf16 planes: 16 coefficients x 32 frames boxes, stored by the K3 epilogue
   if (!rc)
     rc = make_map_bf16_box(c, &mp, s->d_planes, kp, (int64_t)L->rings * 3 * s->tp, 16, 32,
                            CU_TENSOR_MAP_SWIZZLE_NONE);
-  // one box = this CTA's half of the S*kt digit rows of an N-tile
-  if (!rc)
-    rc = make_map_u8(c, &mv, B->d_vd, L->ktot, B->vrows, L->ktot, 128, B->digits * B->kt / 2);
+  if (!rc)  // unused (per-ring digit maps)
+    rc = make_map_u8(c, &mv, B->d_vd, L->kpad[0], B->vrows, L->kpad[0], 128,
+                     B->digits * B->kt / 2);
   if (rc) return rc;
   ProjParams p;
   p.tiles = s->d_ptiles;
@@ -1519,6 +1630,8 @@ static int compress_rows(xg_series* s, xg_basis* B, int64_t t0, int64_t n) {
   p.ntiles = s->n_ptiles;
   p.ring_koff = L->d_ring_koff;
   p.ring_nkb = L->d_ring_nkb;
+  p.xmaps = s->d_xmaps;
+  p.vmaps = B->d_vmaps;
   p.n_digits = B->digits;
   p.kt = B->kt;
   p.k = B->k;
@@ -1730,7 +1843,7 @@ int xg_series_build_basis(xg_series* s, int32_t k, double* const* v_out, double*
   std::vector<DGemmRing> gr(Q);
   for (int32_t r = 0; r < Q; ++r) {
     kpad_max = std::max(kpad_max, L->kpad[r]);
-    gr[r] = DGemmRing{d_bt + (size_t)r * n * n, n, s->d_x + L->koff[r], L->ktot,
+    gr[r] = DGemmRing{d_bt + (size_t)r * n * n, n, s->d_x + s->xmax * L->koff[r], L->kpad[r],
                       d_w + n * L->koff[r], L->kpad[r], (int32_t)n, (int32_t)L->kpad[r], (int32_t)n};
   }
   DGemmRing* d_gr;
@@ -2384,9 +2497,12 @@ int xg_stream_create(xg_ctx* c, const xg_layout* L, const xg_basis* B, int64_t m
       const int64_t nt = row / (b->digits * b->kt), rem = row % (b->digits * b->kt);
       const int64_t dig = rem / b->kt, j = nt * b->kt + rem % b->kt;
       if (j >= b->k) continue;
-      const int8_t* src = b->h_vd.data() + row * L->ktot;
-      for (int64_t col = 0; col < L->ktot; ++col)
-        if (src[col]) vdt[(size_t)col * s->vdt_ld + dig * b->k + j] = src[col];
+      for (int32_t q = 0; q < L->rings; ++q) {  // ring-blocked digits
+        const int8_t* src = b->h_vd.data() + b->vrows * L->koff[q] + row * L->kpad[q];
+        for (int64_t cc = 0; cc < L->kpad[q]; ++cc)
+          if (src[cc])
+            vdt[(size_t)(L->koff[q] + cc) * s->vdt_ld + dig * b->k + j] = src[cc];
+      }
     }
     if ((e = dalloc(&s->d_vdt, vdt.size())) != cudaSuccess ||
         (e = dalloc(&s->d_y, (size_t)Q * s->tp * b->k)) != cudaSuccess ||
@@ -2396,10 +2512,9 @@ int xg_stream_create(xg_ctx* c, const xg_layout* L, const xg_basis* B, int64_t m
       return cuda_fail(c, e, "stream basis");
     }
     cudaMemsetAsync(s->d_yf, 0, (size_t)Q * s->tp * ((b->k + 3) / 4 * 4) * 4, c->stream);
-    if (b->dirty) {
-      cudaMemcpy(b->d_vd, b->h_vd.data(), b->h_vd.size(), cudaMemcpyHostToDevice);
-      cudaMemcpy(b->d_scale, b->h_scale.data(), b->h_scale.size() * 8, cudaMemcpyHostToDevice);
-      b->dirty = false;
+    if (int rc0 = basis_upload(b)) {
+      xg_stream_destroy(s);
+      return rc0;
     }
   }
   *out = s;

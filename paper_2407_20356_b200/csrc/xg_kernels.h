@@ -42,6 +42,10 @@ __host__ __device__ constexpr int ingest_band_stride(int band) {
 __host__ __device__ constexpr int ingest_smem_offset(int e) {  // band byte -> smem byte
   return e + (INGEST_PITCH - INGEST_PIECE) * (e / INGEST_PIECE);
 }
+// 2D bands (xg_layout_create_2d on a detector wider than a piece): kBandH
+// rows x kBandW columns, one piece per row.
+constexpr int kBandW = INGEST_PIECE;
+constexpr int kBandH = 16384 / INGEST_PIECE;
 
 
 // The pixels of one ring inside one band form a "segment" of the ring-major
@@ -56,12 +60,18 @@ struct Piece {
   int32_t word_off;  // into the band's word table (u16 smem word index each)
   int32_t n_byte;    // byte-gathered groups (after the word groups)
   int32_t byte_off;  // into the band's byte table (4 u16 smem byte offsets each)
-  int32_t pad0, pad1;
+  int32_t koff;      // the ring's first ring-major column (ring-blocked x, below)
+  int32_t kpad;      // the ring's padded width (its row stride in x)
 };
 
+// Ring-major frames x are ring-BLOCKED: ring q owns the rows x + xmax koff_q
+// .. + xmax (koff_q + kpad_q), a [xmax frames][kpad_q] matrix (row stride
+// kpad_q), so a TMA box of 128 frames spans 128 kpad_q bytes instead of 128
+// ktot (C5: 3 MB instead of 400 MB of address space: K3 at C5 geometry ran
+// at half its per-byte speed with the interleaved rows).
 struct IngestParams {
   const uint8_t* raster;     // n_frames x pixels (device)
-  uint8_t* x;                // n_frames x ktot ring-major (device)
+  uint8_t* x;                // ring-blocked (above), xmax frames per ring block
   int64_t pixels;
   int64_t ktot;
   int32_t band;              // pixels per band
@@ -81,6 +91,10 @@ struct IngestParams {
   int64_t n_frames;
   int32_t frames_per_cta;
   unsigned long long* norm2;  // [frame][ring] |x|^2, accumulated per piece (rows pre-zeroed)
+  int64_t xmax;               // frames per ring block of x
+  int32_t width = 0;          // > 0: 2D bands of kBandH x kBandW over a height x width
+  int32_t height = 0;         //      detector; band b = block (b / blocks_x, b % blocks_x)
+  int32_t blocks_x = 0;
 };
 cudaError_t launch_ingest(const IngestParams& p, cudaStream_t s);
 
@@ -119,6 +133,7 @@ struct GramParams {
   int32_t ntiles;
   const int32_t* ring_koff;  // byte column of each ring in the ring-major row
   const int32_t* ring_nkb;   // 128-byte K blocks per ring
+  const CUtensorMap* xmaps;  // raw mode: per-ring TMA maps of the ring blocks of x (global)
   uint32_t* gram;            // [ring][ld][ld] exact int32 Gram / f32 C~ (upper tiles)
   int64_t ring_stride;
   int32_t ld;
@@ -196,6 +211,8 @@ struct ProjParams {
   int32_t ntiles;
   const int32_t* ring_koff;
   const int32_t* ring_nkb;
+  const CUtensorMap* xmaps;  // per-ring TMA maps of the ring blocks of x (global)
+  const CUtensorMap* vmaps;  // per-ring TMA maps of the ring blocks of the basis digits
   int32_t n_digits;          // S in {1, 2, 3}
   int32_t kt;                // coefficients per N-tile (multiple of 16, S*kt <= 256)
   int32_t k;                 // rank

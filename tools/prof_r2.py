@@ -28,7 +28,8 @@ def main():
         frames = torch.empty((T, H * W), dtype=torch.uint8, device=dev)
         xg.synth_speckle(ctx, frames.data_ptr(), T, H, W, Q, mu, 4, gamma_mode=gm, gamma_a=ga)
         ring = xg.annular_rings(H, W, Q)
-        lay = xg.RingLayout(ctx, H * W, [np.nonzero(ring == r)[0] for r in range(Q)])
+        lay = xg.RingLayout(ctx, H * W, [np.nonzero(ring == r)[0] for r in range(Q)],
+                            shape=None if os.environ.get("LAYOUT") == "1d" else (H, W))
         s = xg.FrameSeries(lay, T)
         for _ in range(2):
             torch.cuda.synchronize()
@@ -99,7 +100,12 @@ def main():
         H, W, Q, mu, ch = 1536, 2048, 128, 0.01, 4096
         ring = xg.annular_rings(H, W, Q)
         masks = [np.nonzero(ring == r)[0] for r in range(Q)]
-        lay = xg.RingLayout(ctx, H * W, masks)
+        if os.environ.get("RINGS"):  # a subset of the rings (shorter ring-major rows)
+            sel = [int(v) for v in os.environ["RINGS"].split(",")]
+            masks = [masks[r] for r in sel]
+            Q = len(masks)
+        lay = xg.RingLayout(ctx, H * W, masks,
+                            shape=None if os.environ.get("LAYOUT") == "1d" else (H, W))
         rng = np.random.default_rng(1)
         basis = xg.Basis(lay, k)
         for r in range(Q):
