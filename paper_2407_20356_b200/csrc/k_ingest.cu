@@ -222,7 +222,8 @@ __global__ void __launch_bounds__(INGEST_THREADS + 32)
     const int slot = static_cast<int>(i % NBUF);  // FR consecutive slots
     const int nfr = nf - i < FR ? static_cast<int>(nf - i) : FR;
     uint32_t band_s[FR];
-    int64_t xrow[FR];  // frame's row within its ring block
+    int64_t xrow[FR];  // frame's row in x
+    uint8_t* xbase[FR];  // interleaved rows: the frame's ring-major row
     unsigned long long* nrow[FR];
 #pragma unroll
     for (int f = 0; f < FR; ++f) {
@@ -231,16 +232,19 @@ __global__ void __launch_bounds__(INGEST_THREADS + 32)
       band_s[f] = bufs_s + (slot + ff) * bstride;
       const int64_t t = p.t0 + f_begin + i + ff;
       xrow[f] = t - p.x_row0;
+      xbase[f] = p.x + xrow[f] * p.ktot;
       nrow[f] = p.norm2 + t * p.n_rings;
-      asm volatile("" : "+l"(xrow[f]), "+l"(nrow[f]));  // once per frame, not per piece
+      asm volatile("" : "+l"(xrow[f]), "+l"(xbase[f]), "+l"(nrow[f]));  // once per frame
     }
     for (int k = k0; k < k1; ++k) {
       const int4 pa = spieces[2 * k], pb = spieces[2 * k + 1];  // see Piece
       // the piece's output: row xrow[f] of its ring's block (ring-blocked x)
+      // or of the interleaved ring-major row
       uint8_t* xseg[FR];
 #pragma unroll
       for (int f = 0; f < FR; ++f)
-        xseg[f] = p.x + p.xmax * pb.z + xrow[f] * pb.w + (pa.y - pb.z);
+        xseg[f] = p.blocked ? p.x + p.xmax * pb.z + xrow[f] * pb.w + (pa.y - pb.z)
+                            : xbase[f] + pa.y;
       uint32_t sq[FR];
 #pragma unroll
       for (int f = 0; f < FR; ++f) sq[f] = 0;

@@ -77,7 +77,23 @@ struct xg_layout {
   int32_t* d_ring_koff = nullptr;
   int32_t* d_ring_nkb = nullptr;
   int32_t width = 0, height = 0, blocks_x = 0;  // 2D bands (xg_layout_create_2d)
+  // Ring-major frames (and basis digits) ring-BLOCKED -- ring q's frames a
+  // contiguous [rows][kpad_q] block -- when a ring-major row is long (C3-C5:
+  // a TMA box of 128 frame rows then spans 128 kpad_q bytes instead of
+  // 128 ktot, C4 K2 104.7 -> 82.6 ms, C5 K3 2.2x); else rows interleaved
+  // [frame][ktot] (C2: one frame's ingest writes stay in 262 KB, 0.39 ms vs
+  // 0.43 ms blocked).
+  bool blocked = false;
 };
+
+// Ring q's part of a [rows] x ktot ring-major buffer: element offset of its
+// first row and its row stride.
+static int64_t ring_base(const xg_layout* L, int64_t rows, int32_t q) {
+  return L->blocked ? rows * L->koff[q] : L->koff[q];
+}
+static int64_t ring_ld(const xg_layout* L, int32_t q) {
+  return L->blocked ? L->kpad[q] : L->ktot;
+}
 
 struct xg_series {
   xg_ctx* ctx = nullptr;
@@ -256,8 +272,8 @@ int upload_ring_maps(xg_ctx* c, const xg_layout* L, const uint8_t* base, int64_t
                      int64_t rows, uint32_t box_rows, CUtensorMap** dev) {
   std::vector<CUtensorMap> maps(static_cast<size_t>(L->rings));
   for (int32_t r = 0; r < L->rings; ++r) {
-    const int rc = make_map_u8(c, &maps[r], base + rows_cap * L->koff[r], L->kpad[r], rows,
-                               L->kpad[r], 128, box_rows);
+    const int rc = make_map_u8(c, &maps[r], base + ring_base(L, rows_cap, r), L->kpad[r], rows,
+                               ring_ld(L, r), 128, box_rows);
     if (rc) return rc;
   }
   if (!*dev) XG_CUDA(c, dalloc(dev, maps.size()));
@@ -472,6 +488,7 @@ static int layout_build(xg_ctx* c, int64_t full_pixels, int64_t height, int64_t 
     koff += L->kpad[r];
   }
   L->ktot = koff;
+  L->blocked = L->ktot > 400000;
   if (L->ktot > INT32_MAX) {
     delete L;
     return fail(c, XG_ERR_CONTRACT, "layout: padded ring width exceeds 2^31 bytes");
@@ -575,8 +592,10 @@ static int layout_build(xg_ctx* c, int64_t full_pixels, int64_t height, int64_t 
           pc.word_off = s.woff + std::min(j0, s.nw);
           pc.n_byte = (j1 - j0) - pc.n_word;
           pc.byte_off = s.boff + std::max(0, j0 - s.nw);
-          pc.koff = static_cast<int32_t>(L->koff[s.ring]);
-          pc.kpad = static_cast<int32_t>(L->kpad[s.ring]);
+          // K1 writes frame row r of the piece at x + xmax koff + r kpad + (dst - koff):
+          // ring-blocked, or (koff 0, kpad ktot) the interleaved rows
+          pc.koff = L->blocked ? static_cast<int32_t>(L->koff[s.ring]) : 0;
+          pc.kpad = static_cast<int32_t>(L->blocked ? L->kpad[s.ring] : L->ktot);
           pieces.push_back(pc);
         }
         if (j1 < ng) { j0 = j1; break; }
@@ -792,6 +811,7 @@ static int ingest_range(xg_series* s, const uint8_t* raster, int64_t t0, int64_t
   p.raster = raster;
   p.x = s->d_x;
   p.xmax = s->xmax;
+  p.blocked = L->blocked ? 1 : 0;
   p.pixels = L->pixels;
   p.ktot = L->ktot;
   p.band = L->band;
@@ -1522,7 +1542,7 @@ int xg_basis_set_ring(xg_basis* B, int32_t ring, const double* v) {
         double d = std::nearbyint(u);
         d = std::min(127.0, std::max(-127.0, d));
         const int64_t row = (nt * B->digits + s) * B->kt + jj;
-        B->h_vd[(size_t)(B->vrows * L->koff[ring] + row * L->kpad[ring] +
+        B->h_vd[(size_t)(ring_base(L, B->vrows, ring) + row * ring_ld(L, ring) +
                          (col[i] - L->koff[ring]))] = static_cast<int8_t>(d);
         u = (u - d) * 254.0;
       }
@@ -1843,7 +1863,7 @@ int xg_series_build_basis(xg_series* s, int32_t k, double* const* v_out, double*
   std::vector<DGemmRing> gr(Q);
   for (int32_t r = 0; r < Q; ++r) {
     kpad_max = std::max(kpad_max, L->kpad[r]);
-    gr[r] = DGemmRing{d_bt + (size_t)r * n * n, n, s->d_x + s->xmax * L->koff[r], L->kpad[r],
+    gr[r] = DGemmRing{d_bt + (size_t)r * n * n, n, s->d_x + ring_base(L, s->xmax, r), ring_ld(L, r),
                       d_w + n * L->koff[r], L->kpad[r], (int32_t)n, (int32_t)L->kpad[r], (int32_t)n};
   }
   DGemmRing* d_gr;
@@ -2498,7 +2518,7 @@ int xg_stream_create(xg_ctx* c, const xg_layout* L, const xg_basis* B, int64_t m
       const int64_t dig = rem / b->kt, j = nt * b->kt + rem % b->kt;
       if (j >= b->k) continue;
       for (int32_t q = 0; q < L->rings; ++q) {  // ring-blocked digits
-        const int8_t* src = b->h_vd.data() + b->vrows * L->koff[q] + row * L->kpad[q];
+        const int8_t* src = b->h_vd.data() + ring_base(L, b->vrows, q) + row * ring_ld(L, q);
         for (int64_t cc = 0; cc < L->kpad[q]; ++cc)
           if (src[cc])
             vdt[(size_t)(L->koff[q] + cc) * s->vdt_ld + dig * b->k + j] = src[cc];

@@ -64,11 +64,12 @@ struct Piece {
   int32_t kpad;      // the ring's padded width (its row stride in x)
 };
 
-// Ring-major frames x are ring-BLOCKED: ring q owns the rows x + xmax koff_q
-// .. + xmax (koff_q + kpad_q), a [xmax frames][kpad_q] matrix (row stride
-// kpad_q), so a TMA box of 128 frames spans 128 kpad_q bytes instead of 128
-// ktot (C5: 3 MB instead of 400 MB of address space: K3 at C5 geometry ran
-// at half its per-byte speed with the interleaved rows).
+// Ring-major frames x: on a layout with long rows ring-BLOCKED -- ring q owns
+// x + xmax koff_q .. + xmax (koff_q + kpad_q), a [xmax frames][kpad_q] matrix
+// -- so a TMA box of 128 frames spans 128 kpad_q bytes instead of 128 ktot
+// (C5: 3 MB instead of 400 MB of address space: K3 at C5 geometry ran at
+// half its per-byte speed with the interleaved rows); else interleaved
+// [frame][ktot] rows.  Pieces carry the addressing (Piece::koff / kpad).
 struct IngestParams {
   const uint8_t* raster;     // n_frames x pixels (device)
   uint8_t* x;                // ring-blocked (above), xmax frames per ring block
@@ -92,6 +93,7 @@ struct IngestParams {
   int32_t frames_per_cta;
   unsigned long long* norm2;  // [frame][ring] |x|^2, accumulated per piece (rows pre-zeroed)
   int64_t xmax;               // frames per ring block of x
+  int32_t blocked;            // x ring-blocked (else interleaved [frame][ktot] rows)
   int32_t width = 0;          // > 0: 2D bands of kBandH x kBandW over a height x width
   int32_t height = 0;         //      detector; band b = block (b / blocks_x, b % blocks_x)
   int32_t blocks_x = 0;

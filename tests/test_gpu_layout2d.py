@@ -75,3 +75,33 @@ def test_2d_layout_chunked_host_and_stream(ctx, orc):
         assert np.array_equal(one.coeffs(r)[0], st.coeffs(r)[0])
         assert np.array_equal(host.ttc(r, "gram").astype(np.int64), g_ref)
         assert np.array_equal(st.ttc(r, dtype="gram").astype(np.int64), g_ref)
+
+
+def test_ring_blocked_frames_on_a_large_detector(ctx, orc, ref):
+    """> 400 kB ring-major rows: the frames (and basis digits) are stored
+    ring-blocked with per-ring TMA maps.  Exact Gram bitwise, projection
+    against the reference's compress_series, the chunked path, and the device
+    basis (whose W = Xn^T U GEMM reads the ring blocks) against the
+    reference's build_online_from_frames."""
+    import torch
+
+    t, h, w, q, k = 300, 640, 704, 6, 8
+    frames = orc.gen_speckle(t, h, w, q, 0.05, 94)
+    ring, _ = orc.ring_map(h, w, q)
+    lay = xg.RingLayout.from_ring_map(ctx, ring.reshape(h, w), q)
+    s = xg.FrameSeries(lay, t).load(torch.from_numpy(frames).cuda()).ttc_raw()
+    basis = xg.Basis(lay, k)
+    vs, _, _ = xg.FrameSeries(lay, 64).load(frames[:64]).build_basis(k, basis=basis)
+    s.compress(basis)
+    ch = xg.FrameSeries(lay, t, x_frames=128)
+    for i in range(0, t, 128):
+        ch.compress_chunk(basis, frames[i:i + 128], first=(i == 0))
+    for r in range(q):
+        xq = frames[:, ring == r]
+        assert np.array_equal(s.ttc(r, "gram").astype(np.int64), orc.gram_u8(xq)), r
+        v_ref, _ = ref.build_online_from_frames(xq[:64].astype(np.float64), k)
+        assert np.abs(vs[r] - v_ref).max() <= 1e-10, r
+        y_ref, _ = ref.compress_series(xq.astype(np.float64), vs[r])
+        y, _ = s.coeffs(r)
+        assert np.abs(y - y_ref).max() <= 1e-6 * np.abs(y_ref).max(), r
+        assert np.array_equal(ch.coeffs(r)[0], y)
