@@ -829,6 +829,7 @@ def run_c5(E):
         t_spec = a.elapsed_time(b) / 1e3
         tc, tt, ts = E.max_over_ranks(t_cmp[k], t_tiles, t_spec)
         ingest_bytes = 3.0 * T * sh.my_pixels  # K1 raster read + ring-major write, K3 read
+        proj_ops = 2.0 * T * sh.my_pixels * 3 * k  # K3: u8 x s8 over 3 int8 digits per column
         out["by_k"][str(k)] = {
             "ingest_project_s": tc, "frames_per_s_ingest_project": T / tc,
             "g2_tiles_s": tt, "g2_spectral_s": ts,
@@ -836,7 +837,10 @@ def run_c5(E):
             "ingest_project_hbm": {"bytes": ingest_bytes, "achieved_gbs": ingest_bytes / tc / 1e9,
                                    "frac": ingest_bytes / tc / 1e9 / hbm,
                                    "note": "K1 reads the raster + writes the ring-major copy, K3 "
-                                           "re-reads it (3 B per pixel per frame)"}}
+                                           "re-reads it (3 B per pixel per frame)"},
+            "projection_int8_tops_over_ingest_project": proj_ops / tc / 1e12,
+            "projection_note": "2 T M 3k int8 ops (3 digits); at k = 256 K3 is tensor-bound "
+                               "(ops / the whole K1 + K3 time, a lower bound on K3's rate)"}
         del s
         E.free()
     del series, bases
