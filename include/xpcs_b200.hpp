@@ -153,6 +153,19 @@ class RingLayout {
                                off.data(), idx.data(), &h_));
     rings_ = static_cast<int32_t>(masks.size());
   }
+  // a height x width row-major detector (2D ingest bands on wide detectors)
+  RingLayout(const Context& ctx, int64_t height, int64_t width,
+             const std::vector<std::vector<int64_t>>& masks)
+      : ctx_(ctx) {
+    std::vector<int64_t> off(1, 0), idx;
+    for (const auto& m : masks) {
+      idx.insert(idx.end(), m.begin(), m.end());
+      off.push_back(static_cast<int64_t>(idx.size()));
+    }
+    ctx.check(xg_layout_create_2d(ctx.get(), height, width, static_cast<int32_t>(masks.size()),
+                                  off.data(), idx.data(), &h_));
+    rings_ = static_cast<int32_t>(masks.size());
+  }
   ~RingLayout() { xg_layout_destroy(h_); }
   RingLayout(const RingLayout&) = delete;
   RingLayout& operator=(const RingLayout&) = delete;
@@ -222,6 +235,29 @@ class Series {
     std::vector<double> out(static_cast<size_t>(n * n));
     L_.ctx().check(xg_series_get_ttc(h_, ring, XG_F64, out.data(), n, 0));
     return out;
+  }
+  // the exact int32 Gram (full symmetric n x n)
+  std::vector<int32_t> gram(int32_t ring) const {
+    const int64_t n = frames();
+    std::vector<int32_t> out(static_cast<size_t>(n * n));
+    L_.ctx().check(xg_series_get_ttc(h_, ring, XG_I32_GRAM, out.data(), n, 0));
+    return out;
+  }
+  // Split rings (multi-GPU): this process's share of a ring as packed upper
+  // pair tiles + |x_t|^2, and the summed total installed back (host buffers
+  // here; the C ABI also takes device buffers for NCCL).
+  struct Partial {
+    std::vector<int32_t> gram;
+    std::vector<int64_t> norm2;
+  };
+  Partial export_partial(int32_t ring) {
+    Partial p{std::vector<int32_t>(static_cast<size_t>(xg_series_partial_elems(h_))),
+              std::vector<int64_t>(static_cast<size_t>(frames()))};
+    L_.ctx().check(xg_series_export_partial(h_, ring, p.gram.data(), p.norm2.data(), 0));
+    return p;
+  }
+  void import_partial(int32_t ring, const Partial& p, uint32_t flags = 0) {
+    L_.ctx().check(xg_series_import_partial(h_, ring, p.gram.data(), p.norm2.data(), 0, flags));
   }
   std::vector<double> g2(int32_t ring, std::vector<int64_t>* counts = nullptr) const {
     const int64_t n = frames();
@@ -295,6 +331,9 @@ class Stream {
   Stream& operator=(const Stream&) = delete;
   void push(const uint8_t* frame, bool on_device = false) {
     L_.ctx().check(xg_stream_push(h_, frame, on_device ? 1 : 0));
+  }
+  void push_batch(const uint8_t* frames, int64_t n, bool on_device = false) {
+    L_.ctx().check(xg_stream_push_batch(h_, frames, n, on_device ? 1 : 0));
   }
   int64_t frames() const { return xg_stream_frames(h_); }
   std::vector<double> g2(int32_t ring, bool compressed = false) const {

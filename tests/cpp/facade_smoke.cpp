@@ -85,6 +85,30 @@ int main(int argc, char** argv) {
     } catch (const xpcs_b200::NormalizationError& e) {
       std::printf("NormalizationError frame %zu\n", e.frame_index());
     }
+    // round-2 entries: a split ring summed from two half-shares equals the
+    // whole ring's Gram; the batch push equals n single pushes
+    {
+      const auto& m0 = masks[0];
+      const size_t half = m0.size() / 2;
+      std::vector<std::vector<int64_t>> ma{std::vector<int64_t>(m0.begin(), m0.begin() + half)};
+      std::vector<std::vector<int64_t>> mb{std::vector<int64_t>(m0.begin() + half, m0.end())};
+      xpcs_b200::RingLayout la(ctx, m, ma), lb(ctx, m, mb);
+      xpcs_b200::Series sa(la, n), sb(lb, n);
+      sa.load(frames.data(), n);
+      sb.load(frames.data(), n);
+      sa.ttc_raw();
+      sb.ttc_raw();
+      auto pa = sa.export_partial(0);
+      const auto pb = sb.export_partial(0);
+      for (size_t i = 0; i < pa.gram.size(); ++i) pa.gram[i] += pb.gram[i];
+      for (size_t i = 0; i < pa.norm2.size(); ++i) pa.norm2[i] += pb.norm2[i];
+      sa.import_partial(0, pa);
+      std::printf("split ring %s\n", sa.gram(0) == s.gram(0) ? "equal" : "DIFFERENT");
+      xpcs_b200::Stream st1(layout, n), st2(layout, n);
+      for (int64_t t = 0; t < n; ++t) st1.push(frames.data() + t * m);
+      st2.push_batch(frames.data(), n);
+      std::printf("push batch %s\n", st1.g2(0) == st2.g2(0) ? "equal" : "DIFFERENT");
+    }
   } catch (const std::exception& e) {
     std::fprintf(stderr, "error: %s\n", e.what());
     return 1;

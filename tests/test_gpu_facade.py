@@ -43,3 +43,5 @@ def test_cpp_facade(tmp_path, orc):
     assert lines[q + 3] == "f64 load equal"
     assert lines[q + 4] == "ContractError non-integer"
     assert lines[q + 5] == "NormalizationError frame 1"
+    assert lines[q + 6] == "split ring equal"
+    assert lines[q + 7] == "push batch equal"
