@@ -984,7 +984,7 @@ static cudaError_t launch_gram_any(xg_series* s, int mode, const CUtensorMap& in
     if (ring_bytes <= 64e6) {
       gp.wave_ctr = nullptr;
     } else {
-      gp.gate_lag = 2;
+      gp.gate_lag = 2;  // C4 (ring-blocked): 86.1 ms ungated, 82.4 ms at lag 2
       const cudaError_t e = cudaMemsetAsync(gp.wave_ctr, 0, sizeof(unsigned int), s->ctx->stream);
       if (e != cudaSuccess) return e;
     }
