@@ -114,55 +114,77 @@ __global__ void k_expand(ExpandParams p, int src_mode) {
 }
 
 // Fold of the K2 epilogue's per-tile diagonal sums (fused g2).  For lag d
-// the contributing tiles are those with 128 * (2 jb - ib) in [d-255, d+127];
-// they are visited in ascending (delta, ib) order, so the sum order is fixed.
-__global__ void k_g2_fold(G2FoldParams p) {
+// the contributing tiles are those with 128 * (2 jb - ib) in [d-255, d+127],
+// visited in (delta, ib) order.  A block holds 32 consecutive lags; its 4
+// warps take every 4th contributing tile of each delta run (loads of one
+// warp instruction are 32 consecutive diagonals of one tile: coalesced) and
+// their 4 partial sums are combined in a fixed order, so the result is
+// deterministic (one thread per lag walking every tile was latency-bound:
+// 27 us at C2).
+__global__ void __launch_bounds__(128) k_g2_fold(G2FoldParams p) {
   __shared__ int32_t tile_off[257];  // ib_tile_off, staged (nbi <= 256 here)
+  __shared__ double part_sum[4][32];
+  __shared__ long long part_cnt[4][32];
   for (int i = threadIdx.x; i <= p.nbi && i < 257; i += blockDim.x) tile_off[i] = p.ib_tile_off[i];
   __syncthreads();
   const int32_t* ib_tile_off = p.nbi < 257 ? tile_off : p.ib_tile_off;
-  const int64_t d = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t d = static_cast<int64_t>(blockIdx.x) * 32 + lane;
   const int r = blockIdx.y;
-  if (d >= p.n_frames) return;
+  const bool live = d < p.n_frames;
   const float2* part = p.g2_partial + static_cast<int64_t>(r) * p.tiles_per_ring * 384;
   double acc = 0.0;
-  // delta range: ceil((d-255)/128) .. floor((d+127)/128)
-  const int64_t dlo = (d - 255 >= 0) ? (d - 255 + 127) / 128 : -((255 - d) / 128);
-  const int64_t dhi = (d + 127) / 128;
-  for (int64_t delta = dlo; delta <= dhi; ++delta) {
-    const int dl = static_cast<int>(d - 128 * delta + 127);
-    if (dl < 0 || dl >= 383) continue;
-    if (delta < -1) continue;  // jb = (delta + ib) / 2 would fall below ib / 2
-    // (delta + ib) even; jb < nbj  <=>  ib < 2 nbj - delta: a branch-free run
-    const int ib_end = static_cast<int>(min(static_cast<int64_t>(p.nbi), 2 * p.nbj - delta));
+  if (live) {
+    // delta range: ceil((d-255)/128) .. floor((d+127)/128)
+    const int64_t dlo = (d - 255 >= 0) ? (d - 255 + 127) / 128 : -((255 - d) / 128);
+    const int64_t dhi = (d + 127) / 128;
+    for (int64_t delta = dlo; delta <= dhi; ++delta) {
+      const int dl = static_cast<int>(d - 128 * delta + 127);
+      if (dl < 0 || dl >= 383) continue;
+      if (delta < -1) continue;  // jb = (delta + ib) / 2 would fall below ib / 2
+      // (delta + ib) even; jb < nbj  <=>  ib < 2 nbj - delta: a branch-free run
+      const int ib_end = static_cast<int>(min(static_cast<int64_t>(p.nbi), 2 * p.nbj - delta));
 #pragma unroll 4
-    for (int ib = static_cast<int>(delta & 1); ib < ib_end; ib += 2) {
-      const int64_t jb = (delta + ib) / 2;
-      const int64_t tile = ib_tile_off[ib] + (jb - ib / 2);
-      const float2 v = part[tile * 384 + dl];
-      acc += static_cast<double>(v.x) + static_cast<double>(v.y);
+      for (int ib = static_cast<int>(delta & 1) + 2 * w; ib < ib_end; ib += 8) {
+        const int64_t jb = (delta + ib) / 2;
+        const int64_t tile = ib_tile_off[ib] + (jb - ib / 2);
+        const float2 v = part[tile * 384 + dl];
+        acc += static_cast<double>(v.x) + static_cast<double>(v.y);
+      }
     }
   }
-  // valid pairs: sum_t nz(t) nz(t+d), t <= T-1-d
-  const uint32_t* W = p.nz_bits + static_cast<int64_t>(r) * p.nz_words;
+  // valid pairs: sum_t nz(t) nz(t+d), t <= T-1-d (integer: split freely)
   int64_t cnt = 0;
   const int64_t last = p.n_frames - 1 - d;
-  if (p.zero_count[r] == 0) cnt = last + 1;  // no zero-norm frame in this ring
-  else
-  for (int i = 0; i < p.nz_words; ++i) {
-    const int64_t t0 = 32ll * i;
-    if (t0 > last) break;
-    const int64_t sft = t0 + d;
-    const int w0 = static_cast<int>(sft >> 5), sh = static_cast<int>(sft & 31);
-    const uint32_t lo = w0 < p.nz_words ? W[w0] : 0u;
-    const uint32_t hi = w0 + 1 < p.nz_words ? W[w0 + 1] : 0u;
-    uint32_t m = W[i] & __funnelshift_r(lo, hi, sh);
-    const int64_t lim = last - t0;
-    if (lim < 31) m &= (2u << lim) - 1u;
-    cnt += __popc(m);
+  if (live) {
+    if (p.zero_count[r] == 0) {
+      if (w == 0) cnt = last + 1;  // no zero-norm frame in this ring
+    } else {
+      const uint32_t* W = p.nz_bits + static_cast<int64_t>(r) * p.nz_words;
+      for (int i = w; i < p.nz_words; i += 4) {
+        const int64_t t0 = 32ll * i;
+        if (t0 > last) break;
+        const int64_t sft = t0 + d;
+        const int w0 = static_cast<int>(sft >> 5), sh = static_cast<int>(sft & 31);
+        const uint32_t lo = w0 < p.nz_words ? W[w0] : 0u;
+        const uint32_t hi = w0 + 1 < p.nz_words ? W[w0 + 1] : 0u;
+        uint32_t m = W[i] & __funnelshift_r(lo, hi, sh);
+        const int64_t lim = last - t0;
+        if (lim < 31) m &= (2u << lim) - 1u;
+        cnt += __popc(m);
+      }
+    }
   }
-  p.g2[r * p.g2_ld + d] = cnt > 0 ? acc / static_cast<double>(cnt) : 0.0;
-  p.counts[r * p.g2_ld + d] = cnt;
+  part_sum[w][lane] = acc;
+  part_cnt[w][lane] = cnt;
+  __syncthreads();
+  if (w == 0 && live) {
+    const double sum = (part_sum[0][lane] + part_sum[1][lane]) +
+                       (part_sum[2][lane] + part_sum[3][lane]);
+    const int64_t c = part_cnt[0][lane] + part_cnt[1][lane] + part_cnt[2][lane] + part_cnt[3][lane];
+    p.g2[r * p.g2_ld + d] = c > 0 ? sum / static_cast<double>(c) : 0.0;
+    p.counts[r * p.g2_ld + d] = c;
+  }
 }
 
 // Streaming g2: running lag sums / pair counts.
@@ -231,7 +253,7 @@ cudaError_t launch_g2_div(const double* sum, const int64_t* cnt, double* out, in
 }
 
 cudaError_t launch_g2_fold(const G2FoldParams& p, cudaStream_t s) {
-  dim3 grid(static_cast<unsigned>((p.n_frames + 127) / 128), p.n_rings);
+  dim3 grid(static_cast<unsigned>((p.n_frames + 31) / 32), p.n_rings);
   k_g2_fold<<<grid, 128, 0, s>>>(p);
   return cudaGetLastError();
 }
