@@ -86,6 +86,23 @@ __global__ void __launch_bounds__(SR_THREADS) k_stream_raw(StreamParams p) {
 // zeros too, compress.cpp:17) and accumulates x * digit for every (digit,
 // coefficient) pair from the pixel-major int8 digits; slices meet in pacc
 // (integer atomics: exact, order-free).
+// Programmatic dependent launch (PDL) chains the kernels of a photon-event
+// push on ONE stream (no launch gaps, no events).  Each kernel waits
+// (griddepcontrol.wait) for its predecessor where it reads its output and
+// then lets its successor be scheduled (launch_dependents):
+//   ingest(t) -> [proj_acc -> proj_fin -> cmp](t) -> K5s(t) -> ingest(t+1)
+// K5s(t) needs only ingest(t) (complete, transitively, once cmp(t) got past
+// its wait), so it skips the start wait and overlaps cmp(t); it waits at its
+// END instead, so a completed K5s(t) implies a completed cmp(t).  ingest(t+1)
+// touches only push t+1's buffers (hist column t+1, nonzero lists of parity
+// (t+1) & 1, counters (t+1) % 3), runs beside the previous push's tail and
+// waits for its predecessor before it exits: completion stays transitive.
+// Without the launch attribute these instructions are no-ops.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 constexpr int PZ = 8;
 constexpr int PA_MAXW = 6;  // 32-bit digit words per lane: 3 digits x k <= 768
 constexpr int PA_U = 4;     // pixels in flight per warp
@@ -97,6 +114,8 @@ __global__ void __launch_bounds__(256) k_stream_proj_acc(StreamParams p) {
   __shared__ int32_t red[8][768];
   const int r = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  pdl_wait();  // ingest(t): nonzero lists, 1/|x_t|
+  pdl_launch_dependents();
   const int koff = p.ring_koff[r];
   const int n = p.nz_n[r];
   const int zb = static_cast<int>((static_cast<int64_t>(n) * blockIdx.y) / PZ);
@@ -153,6 +172,8 @@ __global__ void __launch_bounds__(256) k_stream_proj_acc(StreamParams p) {
 // (bitwise-equal rows); resets pacc.
 __global__ void __launch_bounds__(128) k_stream_proj_fin(StreamParams p) {
   const int r = blockIdx.x;
+  pdl_wait();  // proj_acc(t): the digit sums
+  pdl_launch_dependents();
   int32_t* pa = p.pacc + static_cast<int64_t>(r) * 768;
   const double inv = p.inv[static_cast<int64_t>(r) * p.inv_ld + p.t];
   for (int j = threadIdx.x; j < p.k; j += blockDim.x) {
@@ -176,6 +197,8 @@ __global__ void __launch_bounds__(SR_THREADS, 4) k_stream_cmp(StreamParams p) {
   // row) before any arithmetic; fp32 products summed over k, lags in f64
   const int r = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  pdl_wait();  // proj_fin(t): y_t
+  pdl_launch_dependents();
   const int kq = p.kq, nv = kq >> 2;
   const float* ybase = p.yf + static_cast<int64_t>(r) * p.y_ld * kq;
   float4 yn[MAXV];
@@ -290,17 +313,6 @@ __global__ void __launch_bounds__(128) k_stream_ingest(StreamParams p) {
 constexpr int SI_THREADS = 256;
 constexpr int SI_PX = 4;  // 16 per thread (256 CTAs) measured slower: 10.2 -> 14.2 us
 constexpr int SI_MAXQ = 1024;
-// Programmatic dependent launch (PDL) between the pushes of a raw sparse
-// stream: K5s(t) may be scheduled while ingest(t) runs and waits for it
-// (griddepcontrol.wait); ingest(t+1) may run beside K5s(t)'s tail -- it
-// touches only push t+1's buffers (hist column t+1, nonzero lists of parity
-// (t+1) & 1, counters (t+1) % 3) -- and waits for K5s(t) before it exits, so
-// a completed ingest(t+1) implies a completed K5s(t).
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-__device__ __forceinline__ void pdl_launch_dependents() {
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-}
-
 __global__ void __launch_bounds__(SI_THREADS) k_stream_ingest_sparse(StreamParams p) {
   __shared__ uint32_t cnt[SI_MAXQ], sq[SI_MAXQ];
   __shared__ int32_t base[SI_MAXQ];
@@ -425,7 +437,9 @@ __global__ void __launch_bounds__(32 * SS_W) k_stream_sparse(StreamParams p) {
   __shared__ uint32_t red[SS_W][SS_F + 1];
   const int r = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  pdl_wait();  // this push's ingest has completed: nonzero lists, hist column t, 1/|x_t|
+  // this push's ingest has completed: nonzero lists, hist column t, 1/|x_t|
+  // (waited for here, or transitively through the compressed kernels)
+  if (!p.pdl_wait_end) pdl_wait();
   pdl_launch_dependents();
   const int koff = p.ring_koff[r];
   const int n = p.nz_n[r];
@@ -491,6 +505,7 @@ __global__ void __launch_bounds__(32 * SS_W) k_stream_sparse(StreamParams p) {
     p.g2cnt[gi] += (inv_s != 0.0 && inv_t != 0.0) ? 1 : 0;
     if (p.gcol) p.gcol[static_cast<int64_t>(r) * p.col_ring_stride + s * p.col_ld + p.t] = accv;
   }
+  if (p.pdl_wait_end) pdl_wait();  // cmp(t) has completed too (see above)
 }
 
 cudaError_t launch_stream_ingest(const StreamParams& p, cudaStream_t s) {
@@ -540,20 +555,15 @@ cudaError_t launch_stream_raw(const StreamParams& p, int32_t n_rings, int64_t ma
   return cudaGetLastError();
 }
 
-cudaError_t launch_stream_cmp(const StreamParams& p, int32_t n_rings, cudaStream_t s) {
-  k_stream_proj_acc<<<dim3(n_rings, PZ), 256, 0, s>>>(p);
-  cudaError_t e = cudaGetLastError();
+cudaError_t launch_stream_cmp(const StreamParams& p, int32_t n_rings, cudaStream_t s, bool pdl) {
+  cudaError_t e = launch_maybe_pdl(k_stream_proj_acc, dim3(n_rings, PZ), dim3(256), s, pdl, p);
   if (e != cudaSuccess) return e;
-  k_stream_proj_fin<<<n_rings, 128, 0, s>>>(p);
-  e = cudaGetLastError();
+  e = launch_maybe_pdl(k_stream_proj_fin, dim3(n_rings), dim3(128), s, pdl, p);
   if (e != cudaSuccess) return e;
   dim3 grid(static_cast<unsigned>((p.t + 1 + SR_ROWS - 1) / SR_ROWS), n_rings);
   const int nv = p.kq / 4;  // float4 chunks per coefficient row (k <= 256)
-  if (nv <= 32)
-    k_stream_cmp<1><<<grid, SR_THREADS, 0, s>>>(p);
-  else
-    k_stream_cmp<2><<<grid, SR_THREADS, 0, s>>>(p);
-  return cudaGetLastError();
+  if (nv <= 32) return launch_maybe_pdl(k_stream_cmp<1>, grid, dim3(SR_THREADS), s, pdl, p);
+  return launch_maybe_pdl(k_stream_cmp<2>, grid, dim3(SR_THREADS), s, pdl, p);
 }
 
 }  // namespace xg

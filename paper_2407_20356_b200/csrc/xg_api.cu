@@ -2648,10 +2648,12 @@ int xg_stream_push(xg_stream* s, const uint8_t* frame, int on_device) {
   sp.ovf_check = (s->flags & XG_STREAM_NO_RAW) ? 0 : 1;
   sp.done = s->d_done;
   const bool sparse = (s->flags & XG_STREAM_SPARSE) != 0;
-  // raw sparse pushes chain ingest -> column -> next ingest with programmatic
-  // dependent launches (no launch gap; k_stream.cu); a forked compressed
-  // column or a staging copy in between takes the ordinary stream order
-  const bool pdl = sparse && !(s->flags & XG_STREAM_NO_RAW) && !s->B && d_frame == frame;
+  // raw sparse pushes chain ingest -> [compressed column ->] raw column ->
+  // next ingest with programmatic dependent launches on one stream (no launch
+  // gaps, no events; k_stream.cu); a staging copy in between takes the
+  // ordinary stream order
+  const bool pdl = sparse && !(s->flags & XG_STREAM_NO_RAW) && d_frame == frame;
+  sp.pdl_wait_end = (pdl && s->B) ? 1 : 0;
   if (sparse)  // its last CTA also finishes the frame's norms
     XG_CUDA(c, launch_stream_ingest_sparse(sp, c->stream, pdl && s->t > 0));
   else
@@ -2674,7 +2676,7 @@ int xg_stream_push(xg_stream* s, const uint8_t* frame, int on_device) {
   if (!sparse) XG_CUDA(c, launch_norms(np, c->stream));
   c->launches += sparse ? 1 : 2;
   const bool raw = !(s->flags & XG_STREAM_NO_RAW);
-  const bool fork = raw && s->B;  // compressed column on the side stream, overlapped
+  const bool fork = raw && s->B && !pdl;  // compressed column on the side stream, overlapped
   if (fork) {
     if (!s->side) {
       XG_CUDA(c, cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking));
@@ -2685,7 +2687,7 @@ int xg_stream_push(xg_stream* s, const uint8_t* frame, int on_device) {
     XG_CUDA(c, cudaStreamWaitEvent(s->side, s->ev_fork, 0));
   }
   if (s->B) {
-    XG_CUDA(c, launch_stream_cmp(sp, L->rings, fork ? s->side : c->stream));
+    XG_CUDA(c, launch_stream_cmp(sp, L->rings, fork ? s->side : c->stream, pdl));
     c->launches += 3;
   }
   if (raw) {

@@ -287,6 +287,7 @@ struct StreamParams {
   int32_t nz_words;
   int* err;
   int32_t ovf_check;         // raw columns formed: |x|^2 >= 2^31 sets err bit 2
+  int32_t pdl_wait_end;      // K5s in a compressed PDL chain: wait at the end (k_stream.cu)
   unsigned int* done;        // CTA counter (zero on entry, reset by the last CTA)
 };
 // One-frame ingest for the streaming path: ring-major row t of the history,
@@ -301,7 +302,7 @@ cudaError_t launch_stream_ingest_sparse(const StreamParams& p, cudaStream_t s, b
 cudaError_t launch_stream_sparse(const StreamParams& p, int32_t n_rings, cudaStream_t s, bool pdl);
 cudaError_t launch_stream_raw(const StreamParams& p, int32_t n_rings, int64_t max_kpad,
                               cudaStream_t s);
-cudaError_t launch_stream_cmp(const StreamParams& p, int32_t n_rings, cudaStream_t s);
+cudaError_t launch_stream_cmp(const StreamParams& p, int32_t n_rings, cudaStream_t s, bool pdl);
 cudaError_t launch_g2_div(const double* sum, const int64_t* cnt, double* out, int64_t n,
                           cudaStream_t s);
 
