@@ -79,10 +79,11 @@ struct __align__(1024) Tail2 {
 };
 constexpr int WSLOTS = 160;  // 5 windows x 32 diagonals per K4 epilogue warp
 
-// K4 epilogue warp (sub, grp): windows [w_lo, w_lo + nwin) -- group 0 takes
-// windows 0..4, group 1 windows 5..8 (window 4 belongs to group 0).
-__device__ __forceinline__ int k4_wlo(int grp) { return grp ? 5 : 0; }
-__device__ __forceinline__ int k4_nwin(int grp) { return grp ? 4 : 5; }
+// Epilogue warp (sub, grp): window slots [w_lo, w_lo + 5) -- group 0 takes
+// windows 0..4, group 1 windows 4..8; window 4 straddles the groups' chunks
+// (3 | 4) and each holds its part, summed by the fold.
+__device__ __forceinline__ int k4_wlo(int grp) { return grp ? 4 : 0; }
+__device__ __forceinline__ int k4_nwin(int) { return 5; }
 
 // f32 bits -> f64 with integer ops only (normal numbers; zero and
 // denormals -> +-0, far below the compressed path's 1e-5 tolerance)
@@ -412,12 +413,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
       // c finishes window c when L+1+l >= 32 and starts window c+1 otherwise.
       // Both sums advance in ascending l, so every window keeps its
       // one-pass order with a single staged chunk.  With 8 epilogue warps
-      // group 0 stores chunks 0..3 and also reads chunk 4 (to finish window
-      // 4); group 1 stores 4..7 and owns windows 5..8.
+      // group 0 reads and stores chunks 0..3 (windows 0..3 and the first
+      // part of window 4), group 1 chunks 4..7 (the rest of window 4 and
+      // windows 5..8): four chunks per warp, the fold adds window 4's parts.
       const int grp = EPI_WARPS == 8 ? (ew >> 2) : 0;
       const int c_first = grp ? 4 : 0;
-      const int c_last = EPI_WARPS == 8 ? (grp ? 7 : 4) : 7;
-      const int w_lo = EPI_WARPS == 8 ? (grp ? 5 : 0) : 0;
+      const int c_last = EPI_WARPS == 8 ? (grp ? 7 : 3) : 7;
+      const int w_lo = EPI_WARPS == 8 ? (grp ? 4 : 0) : 0;
       const int w_hi = EPI_WARPS == 8 ? (grp ? 8 : 4) : 8;
       const bool fp32 = MODE == 1 || dd_ok;  // FP32 (double-float) sums, else FP64
       float cur_h = 0.f, cur_l = 0.f, nxt_h = 0.f, nxt_l = 0.f;
@@ -472,12 +474,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
           const float2* ir2 = tail->inv_row2[buf] + 32 * sub;
           const float2* ic2 = tail->inv_col2_ext[buf] + 32 + 32 * c;  // + kk
           if (MODE == 1 && col0 + 32 <= p.n_frames) {
-            // every column is a frame: the precomputed walk, no mask
+            // every column is a frame: the precomputed walk, no mask; four
+            // interleaved partial sums (l mod 4) shorten the dependent chain
+            float ch[4] = {0.f, 0.f, 0.f, 0.f}, nx[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
             for (int l = 0; l < 32; ++l) {
               const float v = __uint_as_float(S[wtab[l]]);
-              if (lane + 1 + l >= 32) cur_h += v; else nxt_h += v;
+              const bool fin = lane + 1 + l >= 32;
+              ch[l & 3] += fin ? v : 0.f;
+              nx[l & 3] += fin ? 0.f : v;
             }
+            cur_h += (ch[0] + ch[1]) + (ch[2] + ch[3]);
+            nxt_h += (nx[0] + nx[1]) + (nx[2] + nx[3]);
           } else
 #pragma unroll
           for (int l = 0; l < 32; ++l) {
