@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "xg_kernels.h"
 #include "xg_ptx.cuh"
@@ -44,8 +45,12 @@ template <int MODE> struct Cfg2 {
   // of a stage: 4 stages + 2 buffers measured 0.273 ms vs 0.259 ms.
   static constexpr int STAGES = 5;
   static constexpr int SBUF = 1;  // staging buffers per epilogue warp (1 or 2)
-  static constexpr int EPI_WARPS = 8;
+  // K4's epilogue is latency-bound (TMEM load -> staging -> TMA store and
+  // the diagonal walk per chunk): 12 warps, three per TMEM lane quarter
+  static constexpr int EPI_WARPS = MODE == 1 ? 12 : 8;
   static constexpr int NUM_THREADS = 128 + 32 * EPI_WARPS;
+  // g2 window slots per epilogue warp: its chunks + 1 windows of 32 lags
+  static constexpr int WSLOTS = EPI_WARPS == 8 ? 160 : 128;
 };
 constexpr int NDIAG = BM + BN - 1;
 constexpr int NDIAG_PAD = 384;
@@ -56,7 +61,7 @@ constexpr uint32_t idesc2() {
   return MODE == 0 ? idesc_i8(256, BN, false) : idesc_bf16(256, BN);
 }
 
-template <int EPI_WARPS, int STAGES, int SBUF>
+template <int MODE, int EPI_WARPS, int STAGES, int SBUF, int WSLOTS>
 struct __align__(1024) Tail2 {
   uint32_t stage[SBUF][EPI_WARPS][32 * 32];  // 32x32 chunks per warp, 128B-swizzled
   uint64_t full[STAGES];
@@ -67,23 +72,26 @@ struct __align__(1024) Tail2 {
   uint32_t pad_;
   // 1/|x| of the tile's rows and columns as (hi, lo) floats, staged by warp 2
   // one tile ahead (two buffers); the columns reach 32 past either side
-  float2 inv_row2[2][BM];
-  float2 inv_col2_ext[2][BN + 64];
+  float2 inv_row2[2][MODE == 0 ? BM : 1];
+  float2 inv_col2_ext[2][MODE == 0 ? BN + 64 : 1];
   // each epilogue warp's window sums of one tile (2 tiles in flight),
   // folded by warp 3
-  float2 slot[2][EPI_WARPS][160];
+  // ((hi, lo) double-float for the raw Gram, fp32 for C~)
+  typename std::conditional<MODE == 0, float2, float>::type slot[2][EPI_WARPS][WSLOTS];
   uint64_t accfull[2];
   uint64_t accfree[2];
   uint64_t invfull[2];
   uint64_t invfree[2];
 };
-constexpr int WSLOTS = 160;  // 5 windows x 32 diagonals per K4 epilogue warp
 
-// Epilogue warp (sub, grp): window slots [w_lo, w_lo + 5) -- group 0 takes
-// windows 0..4, group 1 windows 4..8; window 4 straddles the groups' chunks
-// (3 | 4) and each holds its part, summed by the fold.
-__device__ __forceinline__ int k4_wlo(int grp) { return grp ? 4 : 0; }
-__device__ __forceinline__ int k4_nwin(int) { return 5; }
+// Epilogue warp (sub, grp) of NG = EPI_WARPS / 4 column groups: chunks
+// [grp_c0(grp), grp_c0(grp + 1)) of the 8 in a 256-wide tile row, window
+// slots [grp_c0(grp), grp_c0(grp + 1)] -- the window at a group boundary
+// straddles two groups' chunks, each holds its part, the fold adds them.
+template <int NG>
+__device__ __forceinline__ int grp_c0(int g) {
+  return NG == 2 ? 4 * g : (g == 3 ? 8 : 3 * g);
+}
 
 // f32 bits -> f64 with integer ops only (normal numbers; zero and
 // denormals -> +-0, far below the compressed path's 1e-5 tolerance)
@@ -116,7 +124,8 @@ __device__ __forceinline__ void epi_bar() {
 template <int MODE>
 constexpr size_t smem2_bytes() {
   return 1024 + Cfg2<MODE>::STAGES * STAGE_BYTES +
-         sizeof(Tail2<Cfg2<MODE>::EPI_WARPS, Cfg2<MODE>::STAGES, Cfg2<MODE>::SBUF>);
+         sizeof(Tail2<MODE, Cfg2<MODE>::EPI_WARPS, Cfg2<MODE>::STAGES, Cfg2<MODE>::SBUF,
+                       Cfg2<MODE>::WSLOTS>);
 }
 size_t gram2_smem_bytes(int mode) { return mode == 0 ? smem2_bytes<0>() : smem2_bytes<1>(); }
 
@@ -127,7 +136,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
   constexpr uint32_t IDESC = idesc2<MODE>();
   constexpr int STAGES = Cfg2<MODE>::STAGES, EPI_WARPS = Cfg2<MODE>::EPI_WARPS;
   constexpr int SBUF = Cfg2<MODE>::SBUF;
-  using Tail = Tail2<EPI_WARPS, STAGES, SBUF>;
+  constexpr int WSLOTS = Cfg2<MODE>::WSLOTS, NG = EPI_WARPS / 4;
+  using Tail = Tail2<MODE, EPI_WARPS, STAGES, SBUF, WSLOTS>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
@@ -138,10 +148,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
   const bool leader = rank == 0;
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
   int n_planes = 1;  // K4: bf16 planes the precision pairs touch
+  int plast[3] = {0, 0, 0};  // K4: index of each plane's last product
   if (MODE == 1)
     for (int pr = 0; pr < p.n_pairs; ++pr) {
       const int pa = (p.pairs >> (4 * pr)) & 3, pb = (p.pairs >> (4 * pr + 2)) & 3;
       n_planes = max(n_planes, max(pa, pb) + 1);
+      plast[pa] = pr;
+      plast[pb] = pr;
     }
 
   if (threadIdx.x == 0) {
@@ -244,31 +257,38 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
         const uint32_t tmem_d = tmem_base + static_cast<uint32_t>(acc * BN);
         bool ok = true;
         if (MODE == 1) {
+          // products in the host's order (ascending highest plane): each
+          // waits only for the planes it reads, so the first products run
+          // while the later planes land, and a plane's stage is released
+          // right after its last product (plane 1 of the f32 mode before
+          // the plane-2 products), letting the next tile's loads start
           for (int kb = 0; ok && kb < nkb; ++kb) {
             int st[3];
-            for (int q = 0; q < n_planes; ++q) {
-              if (!mbar_wait(&tail->full[stage], phase, p.err)) {
-                ok = false;
-                break;
-              }
-              st[q] = stage;
-              if (++stage == STAGES) {
-                stage = 0;
-                phase ^= 1;
-              }
-            }
-            if (!ok) break;
-            tc_fence_after();
+            int have = 0;
             for (int pr = 0; pr < p.n_pairs; ++pr) {
               const int pa = (p.pairs >> (4 * pr)) & 3, pb = (p.pairs >> (4 * pr + 2)) & 3;
+              for (; have <= max(pa, pb); ++have) {
+                if (!mbar_wait(&tail->full[stage], phase, p.err)) {
+                  ok = false;
+                  break;
+                }
+                st[have] = stage;
+                if (++stage == STAGES) {
+                  stage = 0;
+                  phase ^= 1;
+                }
+              }
+              if (!ok) break;
+              tc_fence_after();
               const uint32_t a0 = smem_u32(sA + st[pa] * A_BYTES);
               const uint32_t b0 = smem_u32(sB + st[pb] * B_BYTES);
 #pragma unroll
               for (int k = 0; k < BK / 32; ++k)
                 mma2_bf16(tmem_d, sdesc_k128(a0 + k * 32), sdesc_k128(b0 + k * 32), IDESC,
                           (kb | pr | k) != 0 ? 1u : 0u);
+              for (int q = 0; q < have; ++q)
+                if (plast[q] == pr) commit2(&tail->empty[st[q]]);
             }
-            for (int q = 0; q < n_planes; ++q) commit2(&tail->empty[st[q]]);
           }
         } else
         for (int kb = 0; kb < nkb; ++kb) {
@@ -337,7 +357,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
     const int e_lo = MODE == 1 && warp == 3 ? 192 : 0;
     const int e_hi = MODE == 1 && warp == 2 ? 192 : NDIAG;
     if (p.g2_partial) {
-      float2(*acc2)[EPI_WARPS][WSLOTS] = tail->slot;
+      auto* acc2 = tail->slot;
       int it = 0;
       for (int t = pair; t < p.ntiles; t += npairs, ++it) {
         const int buf = it & 1;
@@ -351,13 +371,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
 #pragma unroll
             for (int w = 0; w < EPI_WARPS; ++w) {
               const int sb = w & 3, gp = w >> 2;
-              const int off = e - 96 + 32 * sb - 32 * k4_wlo(gp);
-              if (off >= 0 && off < 32 * k4_nwin(gp)) {
-                const float2 v = acc2[buf][w][off];
-                if (MODE == 1)
-                  sum.x += v.x;
-                else
+              const int off = e - 96 + 32 * sb - 32 * grp_c0<NG>(gp);
+              if (off >= 0 && off < 32 * (grp_c0<NG>(gp + 1) - grp_c0<NG>(gp) + 1)) {
+                if constexpr (MODE == 1) {
+                  sum.x += acc2[buf][w][off];
+                } else {
+                  const float2 v = acc2[buf][w][off];
                   sum = dd_add(sum, v.x, v.y);
+                }
               }
             }
             out[e] = sum;
@@ -393,7 +414,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
       ok = __all_sync(0xffffffffu, ok);
       if (ok) tc_fence_after();
       const int it = (t - pair) / npairs, buf = it & 1;
-      float2* slots = &tail->slot[buf][ew][0];
+      auto* slots = &tail->slot[buf][ew][0];
       if (p.g2_partial && it >= 2)  // warp 3 has folded this buffer's last tile
         if (!mbar_wait(&tail->accfree[buf], ((it >> 1) - 1) & 1, p.err)) ok = false;
       if (MODE == 0 && p.g2_partial)  // warp 2 has staged this tile's 1/|x|
@@ -412,22 +433,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
       // 0..31) spans chunks w-1 and w: element (l, kk = (L+1+l) & 31) of chunk
       // c finishes window c when L+1+l >= 32 and starts window c+1 otherwise.
       // Both sums advance in ascending l, so every window keeps its
-      // one-pass order with a single staged chunk.  With 8 epilogue warps
-      // group 0 reads and stores chunks 0..3 (windows 0..3 and the first
-      // part of window 4), group 1 chunks 4..7 (the rest of window 4 and
-      // windows 5..8): four chunks per warp, the fold adds window 4's parts.
-      const int grp = EPI_WARPS == 8 ? (ew >> 2) : 0;
-      const int c_first = grp ? 4 : 0;
-      const int c_last = EPI_WARPS == 8 ? (grp ? 7 : 3) : 7;
-      const int w_lo = EPI_WARPS == 8 ? (grp ? 4 : 0) : 0;
-      const int w_hi = EPI_WARPS == 8 ? (grp ? 8 : 4) : 8;
+      // one-pass order with a single staged chunk.  Each column group reads
+      // and stores its own chunks (K2: 0..3 | 4..7, K4: 0..2 | 3..5 | 6..7);
+      // a window at a group boundary is summed in two parts.
+      const int grp = ew >> 2;
+      const int c_first = grp_c0<NG>(grp);
+      const int c_last = grp_c0<NG>(grp + 1) - 1;
+      const int w_lo = c_first, w_hi = c_last + 1;
       const bool fp32 = MODE == 1 || dd_ok;  // FP32 (double-float) sums, else FP64
       float cur_h = 0.f, cur_l = 0.f, nxt_h = 0.f, nxt_l = 0.f;
       double cur_d = 0.0, nxt_d = 0.0;
       auto finish = [&](int w, float wh, float wl) {
         if (w < w_lo || w > w_hi) return;
         const int lagw = td.j0 - i0 + 32 * (w - 1 - sub) + lane + 1;  // this lane's lag
-        slots[32 * (w - w_lo) + lane] = lagw >= 0 ? make_float2(wh, wl) : make_float2(0.f, 0.f);
+        if constexpr (MODE == 1)
+          slots[32 * (w - w_lo) + lane] = lagw >= 0 ? wh : 0.f;
+        else
+          slots[32 * (w - w_lo) + lane] = lagw >= 0 ? make_float2(wh, wl) : make_float2(0.f, 0.f);
       };
 #pragma unroll 1
       for (int c = c_first; ok && c <= c_last; ++c) {
@@ -454,7 +476,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
         // chunks wholly below the diagonal of a diagonal tile are never read
         // (every reader takes the upper triangle a <= b): not stored
         const bool lower = td.i0 == td.j0 && c < sub + 4 * static_cast<int>(rank);
-        if (lane == 0 && p.store && !lower && (EPI_WARPS == 4 || (grp ? c >= 4 : c < 4))) {
+        if (lane == 0 && p.store && !lower) {
           // the TTC streams out once: evict-first in L2, so it does not push
           // the ring's frame rows (re-read by later tiles) out of L2
           uint64_t pol;

@@ -2186,8 +2186,9 @@ int xg_ttc_compressed(xg_series* s, uint32_t flags) {
   if (flags & XG_CMP_BF16) {  // single bf16 product: hi x hi
     gp.n_pairs = 1;
     gp.pairs = 0x0;
-  } else {  // (0,0) (0,1) (1,0) (0,2) (2,0) (1,1): ~24-bit products, f32 accumulate
-    const int pa[6] = {0, 0, 1, 0, 2, 1}, pb[6] = {0, 1, 0, 2, 0, 1};
+  } else {  // (0,0) (0,1) (1,0) (1,1) (0,2) (2,0): ~24-bit products, f32 accumulate;
+    // ascending highest plane (k_gram2.cu: each product waits only for its planes)
+    const int pa[6] = {0, 0, 1, 1, 0, 2}, pb[6] = {0, 1, 0, 1, 2, 0};
     gp.n_pairs = 6;
     gp.pairs = 0;
     for (int i = 0; i < 6; ++i) gp.pairs |= (pa[i] | (pb[i] << 2)) << (4 * i);
