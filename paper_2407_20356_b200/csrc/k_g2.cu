@@ -113,44 +113,66 @@ __global__ void k_expand(ExpandParams p, int src_mode) {
   }
 }
 
-// Fold of the K2 epilogue's per-tile diagonal sums (fused g2).  For lag d
-// the contributing tiles are those with 128 * (2 jb - ib) in [d-255, d+127],
-// visited in (delta, ib) order.  A block holds 32 consecutive lags; its 4
-// warps take every 4th contributing tile of each delta run (loads of one
-// warp instruction are 32 consecutive diagonals of one tile: coalesced) and
-// their 4 partial sums are combined in a fixed order, so the result is
-// deterministic (one thread per lag walking every tile was latency-bound:
-// 27 us at C2).
+// Fold of the K2/K4 epilogue's per-tile diagonal sums (fused g2), in two
+// fixed-order passes.  A tile (half-tile row ib, column block jb) adds to
+// lag d = 128 delta + e - 127 with delta = 2 jb - ib in [-1, 2 nbj - 2] and
+// e its diagonal.  Pass 1 (k_g2_runs, one block per (delta, ring), one
+// thread per diagonal e) sums the run of tiles of each delta in ascending
+// ib: 384 consecutive partials per tile, coalesced.  Pass 2 (k_g2_fold, one
+// thread per lag) adds its <= 3 runs in ascending delta.  (One thread per
+// lag walking every tile: 27 us at C2; the walk split over 4 warps 19-21 us
+// -- latency-bound; the two passes 16-18 us in ncu, ~4 us less in the step.
+// Summing each run in k_gram2 by the CTA completing it stalled the
+// epilogue: 4x slower.)
+template <bool SINGLE>
+__global__ void __launch_bounds__(384) k_g2_runs(G2FoldParams p) {
+  const int64_t delta = static_cast<int64_t>(blockIdx.x) - 1;
+  const int r = blockIdx.y, e = threadIdx.x;
+  const int64_t ring_off = static_cast<int64_t>(r) * p.tiles_per_ring * 384;
+  const float2* part = p.g2_partial + ring_off;
+  const float* part1 = reinterpret_cast<const float*>(p.g2_partial) + ring_off;
+  // (delta + ib) even; jb = (delta + ib) / 2 < nbj  <=>  ib < 2 nbj - delta
+  const int ib0 = static_cast<int>(delta & 1);
+  const int ib_end = static_cast<int>(min(static_cast<int64_t>(p.nbi), 2 * p.nbj - delta));
+  double acc = 0.0;
+  if (e < 383 && ib0 < ib_end) {
+    // element offset of (ib, diagonal e) in the ring's tiles: rows ib hold
+    // nbj - ib / 2 tiles, and jb - ib / 2 is constant along the run, so
+    // o(ib + 2) = o(ib) + (2 nbj - ib) * 384
+    const int nbj = static_cast<int>(p.nbj);
+    const int jrel = static_cast<int>((delta + ib0) / 2) - (ib0 >> 1);
+    int o = ((ib0 ? nbj : 0) + jrel) * 384 + e;
+#pragma unroll 8
+    for (int ib = ib0; ib < ib_end; ib += 2) {
+      if (SINGLE) {
+        acc += static_cast<double>(part1[o]);
+      } else {
+        const float2 hl = part[o];
+        acc += static_cast<double>(hl.x) + static_cast<double>(hl.y);
+      }
+      o += (2 * nbj - ib) * 384;
+    }
+  }
+  p.runs[(static_cast<int64_t>(r) * 2 * p.nbj + blockIdx.x) * 384 + e] = acc;
+}
+
 __global__ void __launch_bounds__(128) k_g2_fold(G2FoldParams p) {
-  __shared__ int32_t tile_off[257];  // ib_tile_off, staged (nbi <= 256 here)
   __shared__ double part_sum[4][32];
   __shared__ long long part_cnt[4][32];
-  for (int i = threadIdx.x; i <= p.nbi && i < 257; i += blockDim.x) tile_off[i] = p.ib_tile_off[i];
-  __syncthreads();
-  const int32_t* ib_tile_off = p.nbi < 257 ? tile_off : p.ib_tile_off;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t d = static_cast<int64_t>(blockIdx.x) * 32 + lane;
   const int r = blockIdx.y;
   const bool live = d < p.n_frames;
-  const float2* part = p.g2_partial + static_cast<int64_t>(r) * p.tiles_per_ring * 384;
   double acc = 0.0;
-  if (live) {
-    // delta range: ceil((d-255)/128) .. floor((d+127)/128)
+  if (live && w == 0) {
+    // delta range: ceil((d-255)/128) .. floor((d+127)/128), at most 3 runs
     const int64_t dlo = (d - 255 >= 0) ? (d - 255 + 127) / 128 : -((255 - d) / 128);
     const int64_t dhi = (d + 127) / 128;
-    for (int64_t delta = dlo; delta <= dhi; ++delta) {
+    const double* runs = p.runs + static_cast<int64_t>(r) * 2 * p.nbj * 384;
+    for (int64_t delta = max(dlo, static_cast<int64_t>(-1)); delta <= dhi; ++delta) {
       const int dl = static_cast<int>(d - 128 * delta + 127);
-      if (dl < 0 || dl >= 383) continue;
-      if (delta < -1) continue;  // jb = (delta + ib) / 2 would fall below ib / 2
-      // (delta + ib) even; jb < nbj  <=>  ib < 2 nbj - delta: a branch-free run
-      const int ib_end = static_cast<int>(min(static_cast<int64_t>(p.nbi), 2 * p.nbj - delta));
-#pragma unroll 4
-      for (int ib = static_cast<int>(delta & 1) + 2 * w; ib < ib_end; ib += 8) {
-        const int64_t jb = (delta + ib) / 2;
-        const int64_t tile = ib_tile_off[ib] + (jb - ib / 2);
-        const float2 v = part[tile * 384 + dl];
-        acc += static_cast<double>(v.x) + static_cast<double>(v.y);
-      }
+      if (dl < 0 || dl >= 383 || delta > 2 * p.nbj - 2) continue;
+      acc += runs[(delta + 1) * 384 + dl];
     }
   }
   // valid pairs: sum_t nz(t) nz(t+d), t <= T-1-d (integer: split freely)
@@ -253,6 +275,13 @@ cudaError_t launch_g2_div(const double* sum, const int64_t* cnt, double* out, in
 }
 
 cudaError_t launch_g2_fold(const G2FoldParams& p, cudaStream_t s) {
+  const dim3 rg(static_cast<unsigned>(2 * p.nbj), p.n_rings);
+  if (p.single)
+    k_g2_runs<true><<<rg, 384, 0, s>>>(p);
+  else
+    k_g2_runs<false><<<rg, 384, 0, s>>>(p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
   dim3 grid(static_cast<unsigned>((p.n_frames + 31) / 32), p.n_rings);
   k_g2_fold<<<grid, 128, 0, s>>>(p);
   return cudaGetLastError();

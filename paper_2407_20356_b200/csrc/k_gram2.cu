@@ -113,10 +113,6 @@ __device__ __forceinline__ float2 dd_add(float2 a, float bh, float bl) {
   return make_float2(hi, __fsub_rn(e, __fsub_rn(hi, s)));
 }
 
-template <int EPI_WARPS>
-__device__ __forceinline__ void epi_bar() {
-  asm volatile("bar.sync 1, %0;" ::"n"(32 * EPI_WARPS) : "memory");
-}
 
 
 }  // namespace
@@ -365,7 +361,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
         const TileDesc td = p.tiles[t];
         if (2 * (td.i0 / 256) + static_cast<int>(rank) < p.g2_nbi) {
           const int64_t half = td.pad + static_cast<int64_t>(rank) * (p.g2_nbj - td.i0 / 256);
+          // K4: fp32 sums (the low parts would be zero), half the bytes
           float2* out = p.g2_partial + half * NDIAG_PAD;
+          float* out1 = reinterpret_cast<float*>(p.g2_partial) + half * NDIAG_PAD;
           for (int e = e_lo + lane; e < e_hi; e += 32) {
             float2 sum = make_float2(0.f, 0.f);
 #pragma unroll
@@ -381,7 +379,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
                 }
               }
             }
-            out[e] = sum;
+            if (MODE == 1)
+              out1[e] = sum.x;
+            else
+              out[e] = sum;
           }
         }
         __syncwarp();

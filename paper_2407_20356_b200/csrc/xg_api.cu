@@ -118,7 +118,7 @@ struct xg_series {
   uint32_t* d_nz_bits = nullptr;   // [ring][nz_words] nonzero-frame bitmask
   int32_t nz_words = 0;
   float2* d_g2tile = nullptr;      // [ntiles][384] fused-g2 tile diagonal sums (hi, lo)
-  int32_t* d_ib_tile_off = nullptr;
+  double* d_g2runs = nullptr;      // [ring][2 nbj][384] their per-delta run sums (g2 fold)
   int32_t tiles_per_ring = 0;
   TileDesc* d_tiles = nullptr;
   TileDesc* d_tiles2 = nullptr;    // 256 x 256 pair tiles
@@ -752,7 +752,7 @@ void xg_series_destroy(xg_series* s) {
   dfree(s->d_tiles2_j);
   dfree(s->d_nz_bits);
   dfree(s->d_g2tile);
-  dfree(s->d_ib_tile_off);
+  dfree(s->d_g2runs);
   dfree(s->d_y);
   dfree(s->d_planes);
   dfree(s->d_cgram);
@@ -909,19 +909,18 @@ static int build_tiles(xg_series* s) {
         d.pad = 0;
         tiles.push_back(d);
       }
-  // tile offset of each tile row within a ring (for the fixed-order g2 fold)
+  // tile offset of each tile row within a ring (pair-tile pad indices below)
   std::vector<int32_t> iboff(nbi + 1, 0);
   for (int64_t ib = 0; ib < nbi; ++ib) iboff[ib + 1] = iboff[ib] + static_cast<int32_t>(nbj - ib / 2);
   s->tiles_per_ring = iboff[nbi];
   dfree(s->d_tiles);
   dfree(s->d_g2tile);
-  dfree(s->d_ib_tile_off);
+  dfree(s->d_g2runs);
   XG_CUDA(c, dalloc(&s->d_tiles, tiles.size()));
   XG_CUDA(c, dalloc(&s->d_g2tile, tiles.size() * 384));
-  XG_CUDA(c, dalloc(&s->d_ib_tile_off, iboff.size()));
+  XG_CUDA(c, dalloc(&s->d_g2runs, (size_t)s->L->rings * 2 * nbj * 384));
   XG_CUDA(c, cudaMemcpy(s->d_tiles, tiles.data(), tiles.size() * sizeof(TileDesc),
                         cudaMemcpyHostToDevice));
-  XG_CUDA(c, cudaMemcpy(s->d_ib_tile_off, iboff.data(), iboff.size() * 4, cudaMemcpyHostToDevice));
   s->ntiles = static_cast<int32_t>(tiles.size());
   // 256 x 256 pair tiles (k_gram2): pad = 1-CTA index of the upper half tile.
   // The persistent kernel deals consecutive tiles to the CTA pairs, so ~one
@@ -1032,11 +1031,12 @@ static int run_g2(xg_series* s, int mode, int32_t ring0 = 0, int32_t n_rings = -
 }
 
 // Fold the per-tile diagonal sums left by a K2/K4 launch into g2 (fixed order).
-static int fold_g2(xg_series* s, double* g2, int64_t* cnt) {
+static int fold_g2(xg_series* s, double* g2, int64_t* cnt, bool single = false) {
   xg_ctx* c = s->ctx;
   G2FoldParams f;
   f.g2_partial = s->d_g2tile;
-  f.ib_tile_off = s->d_ib_tile_off;
+  f.single = single ? 1 : 0;
+  f.runs = s->d_g2runs;
   f.tiles_per_ring = s->tiles_per_ring;
   f.nbi = static_cast<int32_t>((s->t + 127) / 128);
   f.nbj = static_cast<int32_t>((s->t + 255) / 256);
@@ -2204,7 +2204,7 @@ int xg_ttc_compressed(xg_series* s, uint32_t flags) {
   XG_CUDA(c, launch_gram_any(s, 1, my, omap, gp));
   c->launches++;
   if (g2) {
-    rc = fold_g2(s, s->d_cg2, s->d_cg2cnt);
+    rc = fold_g2(s, s->d_cg2, s->d_cg2cnt, true);
     if (rc) return rc;
   }
   s->have_cttc = true;

@@ -179,8 +179,9 @@ cudaError_t launch_gram2_cmp(const CUtensorMap& tmY, const CUtensorMap& tmOut, c
 // Fold the per-tile diagonal sums of K2 into g2[ring][d] (fixed order) and
 // count the valid (t, t+d) pairs from the nonzero-frame bitmask.
 struct G2FoldParams {
-  const float2* g2_partial;  // [ntiles][384] (hi, lo)
-  const int32_t* ib_tile_off;  // [nbi+1] tile offset of tile row ib within a ring
+  const float2* g2_partial;  // [ntiles][384] (hi, lo); K4: [ntiles][384] float
+  int32_t single;            // 1: fp32 partials (K4)
+  double* runs;              // [ring][2 nbj][384] per-delta run sums (k_g2_runs)
   int32_t tiles_per_ring;
   int32_t nbi, nbj;
   int64_t n_frames;
