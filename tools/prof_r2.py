@@ -88,10 +88,13 @@ def main():
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(st)
+        h0 = time.perf_counter()
         sr.push_many(frames[D:])
+        h1 = time.perf_counter()
         b.record(st)
         torch.cuda.synchronize()
         ms = a.elapsed_time(b) / n
+        print(f"c3push host enqueue {1e6 * (h1 - h0) / n:.1f} us/push")
         nnz = float((frames[D:] != 0).float().mean()) * H * W
         gbs = nnz * (D + n / 2) / (ms / 1e3) / 1e9
         print(f"c3push depth {D}: {ms * 1e3:.1f} us/push, {gbs:.0f} GB/s of nnz*t")
