@@ -317,7 +317,14 @@ __global__ void __launch_bounds__(SI_THREADS) k_stream_ingest_sparse(StreamParam
   __shared__ uint32_t cnt[SI_MAXQ], sq[SI_MAXQ];
   __shared__ int32_t base[SI_MAXQ];
   pdl_launch_dependents();
-  if (blockIdx.x == 0)
+  // frame t + f of a batch (f = 0 for a single push)
+  const int f = blockIdx.y;
+  const int64_t tf = p.t + f;
+  const uint8_t* frame = p.frame + static_cast<int64_t>(f) * p.pixels;
+  int32_t* nz_col = p.nz_col + f * p.nz_bstride;
+  uint8_t* nz_val = p.nz_val + f * p.nz_bstride;
+  int32_t* nz_n = p.nz_n + f * p.n_rings;
+  if (blockIdx.x == 0 && f == 0 && p.nz_next)
     for (int r = threadIdx.x; r < p.n_rings; r += blockDim.x) {
       p.nz_next[r] = 0;
       if (p.norm2_next) p.norm2_next[r] = 0ull;
@@ -327,14 +334,14 @@ __global__ void __launch_bounds__(SI_THREADS) k_stream_ingest_sparse(StreamParam
   const int64_t px0 = (static_cast<int64_t>(blockIdx.x) * SI_THREADS + threadIdx.x) * SI_PX;
   uint32_t wv[SI_PX / 4];
   if (px0 + SI_PX <= p.pixels) {
-    wv[0] = __ldcs(reinterpret_cast<const uint32_t*>(p.frame + px0));
+    wv[0] = __ldcs(reinterpret_cast<const uint32_t*>(frame + px0));
   } else {
 #pragma unroll
     for (int k = 0; k < SI_PX / 4; ++k) {
       wv[k] = 0;
       for (int b = 0; b < 4; ++b)
         if (px0 + 4 * k + b < p.pixels)
-          wv[k] |= static_cast<uint32_t>(p.frame[px0 + 4 * k + b]) << (8 * b);
+          wv[k] |= static_cast<uint32_t>(frame[px0 + 4 * k + b]) << (8 * b);
     }
   }
   int ent[SI_PX], loc[SI_PX];
@@ -354,8 +361,8 @@ __global__ void __launch_bounds__(SI_THREADS) k_stream_ingest_sparse(StreamParam
   __syncthreads();
   for (int r = threadIdx.x; r < p.n_rings; r += blockDim.x) {
     if (cnt[r]) {
-      base[r] = p.ring_koff[r] + atomicAdd(p.nz_n + r, static_cast<int>(cnt[r]));
-      atomicAdd(p.norm2 + p.t * p.n_rings + r, static_cast<unsigned long long>(sq[r]));
+      base[r] = p.ring_koff[r] + atomicAdd(nz_n + r, static_cast<int>(cnt[r]));
+      atomicAdd(p.norm2 + tf * p.n_rings + r, static_cast<unsigned long long>(sq[r]));
     }
   }
   __syncthreads();
@@ -365,9 +372,9 @@ __global__ void __launch_bounds__(SI_THREADS) k_stream_ingest_sparse(StreamParam
     const int r = ent[b] >> 22, col = ent[b] & 0x3FFFFF;
     const uint8_t v = static_cast<uint8_t>((wv[b >> 2] >> (8 * (b & 3))) & 0xFFu);
     const int64_t e = base[r] + loc[b];
-    p.nz_col[e] = col;
-    p.nz_val[e] = v;
-    if (p.hist) p.hist[static_cast<int64_t>(col) * p.hp + p.t] = v;
+    nz_col[e] = col;
+    nz_val[e] = v;
+    if (p.hist) p.hist[static_cast<int64_t>(col) * p.hp + tf] = v;
   }
   // the last CTA to finish computes frame t's norms, 1/|x|, nonzero bit and
   // zero-frame bookkeeping (k_norms' expressions) -- no separate launch
@@ -375,22 +382,25 @@ __global__ void __launch_bounds__(SI_THREADS) k_stream_ingest_sparse(StreamParam
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
-    last = atomicAdd(p.done, 1u) == gridDim.x - 1;
+    last = atomicAdd(p.done, 1u) == gridDim.x * gridDim.y - 1;
   }
   __syncthreads();
   pdl_wait();  // the previous push's column kernel has completed (see above)
   if (!last) return;
   __threadfence();
-  for (int r = threadIdx.x; r < p.n_rings; r += blockDim.x) {
-    const long long n2 = static_cast<long long>(atomicAdd(p.norm2 + p.t * p.n_rings + r, 0ull));
+  // every frame of the batch, in ascending t (first_zero / zero counts)
+  for (int i = threadIdx.x; i < static_cast<int>(gridDim.y) * p.n_rings; i += blockDim.x) {
+    const int r = i % p.n_rings;
+    const int64_t tt = p.t + i / p.n_rings;
+    const long long n2 = static_cast<long long>(atomicAdd(p.norm2 + tt * p.n_rings + r, 0ull));
     const double nrm = sqrt(static_cast<double>(n2));
-    p.norms_w[r * p.inv_ld + p.t] = nrm;
-    p.inv_w[r * p.inv_ld + p.t] = n2 > 0 ? 1.0 / nrm : 0.0;
+    p.norms_w[r * p.inv_ld + tt] = nrm;
+    p.inv_w[r * p.inv_ld + tt] = n2 > 0 ? 1.0 / nrm : 0.0;
     if (n2 > 0) {
-      atomicOr(p.nz_bits + static_cast<int64_t>(r) * p.nz_words + (p.t >> 5), 1u << (p.t & 31));
+      atomicOr(p.nz_bits + static_cast<int64_t>(r) * p.nz_words + (tt >> 5), 1u << (tt & 31));
     } else {
       atomicAdd(reinterpret_cast<unsigned long long*>(p.zero_count + r), 1ull);
-      atomicMin(reinterpret_cast<long long*>(p.first_zero + r), static_cast<long long>(p.t));
+      atomicMin(reinterpret_cast<long long*>(p.first_zero + r), static_cast<long long>(tt));
     }
     if (n2 >= (1ll << 31) && p.ovf_check) atomicOr(p.err, 4);
   }
@@ -534,11 +544,13 @@ static cudaError_t launch_maybe_pdl(K kernel, dim3 grid, dim3 block, cudaStream_
   return cudaLaunchKernelEx(&cfg, kernel, p);
 }
 
-cudaError_t launch_stream_ingest_sparse(const StreamParams& p, cudaStream_t s, bool pdl) {
+cudaError_t launch_stream_ingest_sparse(const StreamParams& p, cudaStream_t s, bool pdl,
+                                        int32_t n_frames) {
   if (p.n_rings > SI_MAXQ) return cudaErrorInvalidValue;
   const unsigned blocks =
       static_cast<unsigned>((p.pixels + SI_PX * SI_THREADS - 1) / (SI_PX * SI_THREADS));
-  return launch_maybe_pdl(k_stream_ingest_sparse, dim3(blocks), dim3(SI_THREADS), s, pdl, p);
+  return launch_maybe_pdl(k_stream_ingest_sparse, dim3(blocks, n_frames), dim3(SI_THREADS), s,
+                          pdl, p);
 }
 
 cudaError_t launch_stream_sparse(const StreamParams& p, int32_t n_rings, cudaStream_t s, bool pdl) {

@@ -290,6 +290,10 @@ struct StreamParams {
   int32_t ovf_check;         // raw columns formed: |x|^2 >= 2^31 sets err bit 2
   int32_t pdl_wait_end;      // K5s in a compressed PDL chain: wait at the end (k_stream.cu)
   unsigned int* done;        // CTA counter (zero on entry, reset by the last CTA)
+  // batched sparse ingest (grid.y = frames t .. t + gridDim.y - 1): frame f
+  // at frame + f * pixels, its nonzero lists at nz_col/nz_val + f * nz_bstride
+  // and counts at nz_n + f * n_rings (zeroed before the launch)
+  int64_t nz_bstride;
 };
 // One-frame ingest for the streaming path: ring-major row t of the history,
 // |x_t|^2 per ring, and in sparse mode the frame's nonzeros per ring plus
@@ -297,7 +301,8 @@ struct StreamParams {
 cudaError_t launch_stream_ingest(const StreamParams& p, cudaStream_t s);
 // Sparse mode: the same from the raster in pixel order (no ring-major row):
 // only the frame's nonzero pixels touch the tables.
-cudaError_t launch_stream_ingest_sparse(const StreamParams& p, cudaStream_t s, bool pdl);
+cudaError_t launch_stream_ingest_sparse(const StreamParams& p, cudaStream_t s, bool pdl,
+                                        int32_t n_frames = 1);
 // Sparse raw streaming (photon-event data): the new column costs nnz * t
 // bytes instead of M * t; results equal the dense kernel's bitwise.
 cudaError_t launch_stream_sparse(const StreamParams& p, int32_t n_rings, cudaStream_t s, bool pdl);

@@ -117,8 +117,9 @@ def test_c3_stream_to_depth_4352(ctx, orc, ref):
     basis = xg.Basis(lay, k)
     vs, _, _ = xg.FrameSeries(lay, 256).load(dev[:256]).build_basis(k, basis=basis)
     st = xg.FrameStream(lay, depth, basis=basis, store_ttc=True, sparse=True)
-    for i in range(depth):
+    for i in range(2000):  # single pushes, then the batched photon-event ingest
         st.push(dev[i])
+    st.push_many(dev[2000:])
     assert st.n_frames == depth
     host = dev.cpu().numpy()
     for r in (0, 63, 40):  # 392, 592, ~33k px

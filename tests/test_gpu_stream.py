@@ -96,12 +96,14 @@ def test_sparse_stream_equals_dense(ctx, orc, mu):
         assert np.array_equal(g2s, g2d) and np.array_equal(cs, cd)
 
 
-@pytest.mark.parametrize("basis_k", [0, 6])
-def test_push_many_equals_single_pushes(ctx, orc, basis_k):
-    """push_many (one library call for n frames) == n push() calls, bitwise;
-    the raw sparse stream without a basis chains its kernels with
-    programmatic dependent launches (push t + 1's ingest beside push t's
-    column kernel), which must not change a bit."""
+@pytest.mark.parametrize("basis_k,raw", [(0, True), (6, True), (6, False)])
+def test_push_many_equals_single_pushes(ctx, orc, basis_k, raw):
+    """push_many (one library call for n frames) == n push() calls, bitwise:
+    photon-event push_many ingests 16 frames per launch (batch slots for the
+    nonzero lists, a zero frame inside a batch, a partial last batch) and
+    chains the columns with programmatic dependent launches; single pushes
+    chain push t + 1's ingest beside push t's column kernel.  Neither may
+    change a bit, raw or compressed-only."""
     import torch
 
     t, h, w, q = 300, 96, 96, 4
@@ -114,18 +116,23 @@ def test_push_many_equals_single_pushes(ctx, orc, basis_k):
         basis = xg.Basis(lay, basis_k)
         xg.FrameSeries(lay, 64).load(frames[64:128]).build_basis(basis_k, basis=basis)
     dev = torch.from_numpy(frames).cuda()
-    a = xg.FrameStream(lay, t, basis=basis, store_ttc=True, sparse=True)
-    b = xg.FrameStream(lay, t, basis=basis, store_ttc=True, sparse=True)
+    a = xg.FrameStream(lay, t, basis=basis, store_ttc=raw, sparse=True, raw=raw)
+    b = xg.FrameStream(lay, t, basis=basis, store_ttc=raw, sparse=True, raw=raw)
     for i in range(t):
         a.push(dev[i])
     b.push_many(dev[:100])
-    b.push_many(dev[100:])
+    b.push(dev[100])  # single pushes between batches
+    b.push_many(dev[101:])
     for r in range(q):
-        ga, gb = a.ttc(r, dtype="gram"), b.ttc(r, dtype="gram")
-        assert np.array_equal(ga, gb)
-        assert np.array_equal(gb.astype(np.int64), orc.gram_u8(frames[:, ring == r]))
-        _, va, ca = a.g2(r)
-        _, vb, cb = b.g2(r)
-        assert np.array_equal(va, vb) and np.array_equal(ca, cb)
+        if raw:
+            ga, gb = a.ttc(r, dtype="gram"), b.ttc(r, dtype="gram")
+            assert np.array_equal(ga, gb)
+            assert np.array_equal(gb.astype(np.int64), orc.gram_u8(frames[:, ring == r]))
+            _, va, ca = a.g2(r)
+            _, vb, cb = b.g2(r)
+            assert np.array_equal(va, vb) and np.array_equal(ca, cb)
         if basis_k:
             assert np.array_equal(a.coeffs(r)[0], b.coeffs(r)[0])
+            _, va, ca = a.g2(r, compressed=True)
+            _, vb, cb = b.g2(r, compressed=True)
+            assert np.array_equal(va, vb) and np.array_equal(ca, cb)
