@@ -6,7 +6,8 @@ reference's own functions (oracle/_ref) on the same inputs:
   the summation order differs -> 1e-12 relative);
 * fit_kww (analysis.cpp:77-172) of the device g2 curve, fed to the reference
   as the same curve (identical points; lane-split sums and the device exp ->
-  parameters within 1e-8 relative, identical status)."""
+  parameters within 1e-6 relative and the residual within 1e-9, identical
+  status)."""
 import numpy as np
 import pytest
 
@@ -72,7 +73,12 @@ def test_fit_kww_matches_reference(ctx, orc, ref, period, window):
         code = {0: 0, 10: 1, 11: 2, 2: 3}[rc]
         assert st[r] == code, (r, st[r], rc)
         if code in (0, 2):
-            assert np.allclose(fits[r], want, rtol=1e-8, atol=1e-12), (r, fits[r], want)
+            # the damped Gauss-Newton stops where no step lowers the SSE
+            # (analysis.cpp:155-163): on a flat optimum different rounding
+            # stops at parameters up to ~1e-7 apart (seen: beta, ring 2)
+            # with the same residual, so the residual is pinned tighter
+            assert np.allclose(fits[r][:3], want[:3], rtol=1e-6, atol=1e-12), (r, fits[r], want)
+            assert np.allclose(fits[r][3], want[3], rtol=1e-9, atol=1e-14), (r, fits[r], want)
             n_ok += code == 0
     assert n_ok >= 1
 

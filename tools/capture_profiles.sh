@@ -21,7 +21,7 @@ $NCU -k regex:"k_ingest" -s 1 -c 1 -o $O/${R}_ingest python tools/prof_r2.py c2 
 $NCU -k regex:"k_gram2" -s 1 -c 1 -o $O/${R}_gram_raw python tools/prof_r2.py c2 > /dev/null 2>&1
 ONLY="store+fused g2" $NCU -k regex:"k_gram2" -s 5 -c 1 -o $O/${R}_gram_cmp python tools/prof_r2.py c2cmp > /dev/null 2>&1
 ONLY="store+fused g2" $NCU -k regex:"k_project" -c 1 -o $O/${R}_project python tools/prof_r2.py c2cmp > /dev/null 2>&1
-$NCU -k regex:"k_stream_sparse" -s 16000 -c 1 -o $O/${R}_stream_sparse python tools/prof_r2.py c3push > /dev/null 2>&1
+$NCU -k regex:"k_stream_sparse" -s 8300 -c 1 -o $O/${R}_stream_sparse python tools/prof_r2.py c3push > /dev/null 2>&1
 $NCU -k regex:"k_gram2" -s 1 -c 1 -o $O/${R}_c4_gram python tools/prof_r2.py c4 > /dev/null 2>&1
 $NCU -k regex:"k_ingest" -s 2 -c 1 -o $O/${R}_c5_ingest python tools/prof_r2.py c5 64 > /dev/null 2>&1
 $NCU -k regex:"k_project" -s 2 -c 1 -o $O/${R}_c5_project python tools/prof_r2.py c5 64 > /dev/null 2>&1
