@@ -420,7 +420,7 @@ constexpr int SS_CHUNK = 1024;
 #define XG_SS_V 8
 #endif
 #ifndef XG_SS_U
-#define XG_SS_U 8
+#define XG_SS_U 12
 #endif
 constexpr int SS_V = XG_SS_V;  // history frames per lane (one 8- or 16-byte load)
 constexpr int SS_U = XG_SS_U;  // loads in flight per lane
@@ -429,10 +429,13 @@ constexpr int SS_F = 32 * SS_V;  // history frames per CTA
 #define XG_SS_W 8
 #endif
 constexpr int SS_W = XG_SS_W;  // warps per CTA, splitting the ring's nonzeros
-// 48 registers, 5 CTAs per SM: 41.1 -> 40.5 us per push at depth 8192 (a
-// second register set keeping the next round's loads in flight: 40.0 us at
-// 4 CTAs per SM, not kept)
-constexpr int SS_MINB = 5;
+// 12 loads in flight per lane at 4 CTAs per SM (64 registers): 41.5 -> 40.1
+// us per push at depth 8192 (8 loads at 4-5 CTAs: 40.5-41.5 us; 16 loads at 3
+// CTAs: 50 us).  A persistent form (CTAs walking (ring, window) items, warps
+// reading their nonzero entries straight from global, one warp finishing an
+// item while the others stream the next) ran 71 us: each item became a longer
+// chain of dependent round trips.
+constexpr int SS_MINB = 4;
 template <int V> struct SsVec;
 template <> struct SsVec<8> {
   using T = uint2;
