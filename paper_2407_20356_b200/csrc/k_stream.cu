@@ -455,8 +455,11 @@ __global__ void __launch_bounds__(32 * SS_W, SS_MINB) k_stream_sparse(StreamPara
   const int r = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // this push's ingest has completed: nonzero lists, hist column t, 1/|x_t|
-  // (waited for here, or transitively through the compressed kernels)
-  if (!p.pdl_wait_end) pdl_wait();
+  // (waited for here, or transitively through the compressed kernels; in a
+  // photon-event batch the ingest of every frame completed before the
+  // batch's first K5s started, so K5s(t+1) may stream its history while
+  // K5s(t) still runs and waits for it only before touching the g2 sums)
+  if (!p.pdl_wait_end && !p.pdl_wait_fin) pdl_wait();
   pdl_launch_dependents();
   const int koff = p.ring_koff[r];
   const int n = p.nz_n[r];
@@ -506,6 +509,7 @@ __global__ void __launch_bounds__(32 * SS_W, SS_MINB) k_stream_sparse(StreamPara
   }
 #pragma unroll
   for (int j = 0; j < SS_V; ++j) red[warp][SS_V * lane + j] = acc[j];
+  if (p.pdl_wait_fin) pdl_wait();  // K5s(t-1) done: lag sums in push order
   __syncthreads();
   const double inv_t = p.inv[static_cast<int64_t>(r) * p.inv_ld + p.t];
 #pragma unroll

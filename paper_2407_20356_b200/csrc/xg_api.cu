@@ -2671,6 +2671,8 @@ static int push_one(xg_stream* s, const uint8_t* frame, int on_device, int slot)
   // ordinary stream order
   const bool pdl = sparse && !(s->flags & XG_STREAM_NO_RAW) && d_frame == frame;
   sp.pdl_wait_end = (pdl && s->B) ? 1 : 0;
+  // raw batch members after the first: K5s follows K5s (see k_stream_sparse)
+  sp.pdl_wait_fin = (pdl && !s->B && slot > 0) ? 1 : 0;
   if (slot >= 0)
     ;  // ingested with its batch
   else if (sparse)  // its last CTA also finishes the frame's norms

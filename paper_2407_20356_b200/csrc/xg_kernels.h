@@ -289,6 +289,7 @@ struct StreamParams {
   int* err;
   int32_t ovf_check;         // raw columns formed: |x|^2 >= 2^31 sets err bit 2
   int32_t pdl_wait_end;      // K5s in a compressed PDL chain: wait at the end (k_stream.cu)
+  int32_t pdl_wait_fin;      // K5s after K5s in a batch: wait before the finishing step
   unsigned int* done;        // CTA counter (zero on entry, reset by the last CTA)
   // batched sparse ingest (grid.y = frames t .. t + gridDim.y - 1): frame f
   // at frame + f * pixels, its nonzero lists at nz_col/nz_val + f * nz_bstride
