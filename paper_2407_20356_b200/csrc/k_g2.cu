@@ -124,8 +124,15 @@ __global__ void k_expand(ExpandParams p, int src_mode) {
 // -- latency-bound; the two passes 16-18 us in ncu, ~4 us less in the step.
 // Summing each run in k_gram2 by the CTA completing it stalled the
 // epilogue: 4x slower.)
+// Both passes are launched as programmatic dependents (of the Gram kernel,
+// then of pass 1): the grid is set up while its predecessor drains and waits
+// for it here before reading its output.
+__device__ __forceinline__ void g2_pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 template <bool SINGLE>
 __global__ void __launch_bounds__(384) k_g2_runs(G2FoldParams p) {
+  g2_pdl_wait();
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int64_t delta = static_cast<int64_t>(blockIdx.x) - 1;
   const int r = blockIdx.y, e = threadIdx.x;
   const int64_t ring_off = static_cast<int64_t>(r) * p.tiles_per_ring * 384;
@@ -157,6 +164,7 @@ __global__ void __launch_bounds__(384) k_g2_runs(G2FoldParams p) {
 }
 
 __global__ void __launch_bounds__(128) k_g2_fold(G2FoldParams p) {
+  g2_pdl_wait();
   __shared__ double part_sum[4][32];
   __shared__ long long part_cnt[4][32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -274,17 +282,27 @@ cudaError_t launch_g2_div(const double* sum, const int64_t* cnt, double* out, in
   return cudaGetLastError();
 }
 
+template <typename K>
+static cudaError_t launch_pdl(K kernel, dim3 grid, dim3 block, cudaStream_t s, const G2FoldParams& p) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, p);
+}
+
 cudaError_t launch_g2_fold(const G2FoldParams& p, cudaStream_t s) {
   const dim3 rg(static_cast<unsigned>(2 * p.nbj), p.n_rings);
-  if (p.single)
-    k_g2_runs<true><<<rg, 384, 0, s>>>(p);
-  else
-    k_g2_runs<false><<<rg, 384, 0, s>>>(p);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = p.single ? launch_pdl(k_g2_runs<true>, rg, dim3(384), s, p)
+                           : launch_pdl(k_g2_runs<false>, rg, dim3(384), s, p);
   if (e != cudaSuccess) return e;
-  dim3 grid(static_cast<unsigned>((p.n_frames + 31) / 32), p.n_rings);
-  k_g2_fold<<<grid, 128, 0, s>>>(p);
-  return cudaGetLastError();
+  const dim3 grid(static_cast<unsigned>((p.n_frames + 31) / 32), p.n_rings);
+  return launch_pdl(k_g2_fold, grid, dim3(128), s, p);
 }
 
 cudaError_t launch_g2(const G2Params& p, int mode, cudaStream_t s) {
