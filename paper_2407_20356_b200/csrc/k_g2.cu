@@ -149,15 +149,27 @@ __global__ void __launch_bounds__(384) k_g2_runs(G2FoldParams p) {
     const int nbj = static_cast<int>(p.nbj);
     const int jrel = static_cast<int>((delta + ib0) / 2) - (ib0 >> 1);
     int o = ((ib0 ? nbj : 0) + jrel) * 384 + e;
-#pragma unroll 8
-    for (int ib = ib0; ib < ib_end; ib += 2) {
-      if (SINGLE) {
-        acc += static_cast<double>(part1[o]);
-      } else {
-        const float2 hl = part[o];
-        acc += static_cast<double>(hl.x) + static_cast<double>(hl.y);
+    // batches of 16 predicated loads issued back to back (a runtime-count
+    // loop left the remainder iterations as dependent L2 round trips)
+    constexpr int U = 16;
+    for (int ib1 = ib0; ib1 < ib_end; ib1 += 2 * U) {
+      double v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int ib = ib1 + 2 * u;
+        v[u] = 0.0;
+        if (ib < ib_end) {
+          if (SINGLE) {
+            v[u] = static_cast<double>(part1[o]);
+          } else {
+            const float2 hl = part[o];
+            v[u] = static_cast<double>(hl.x) + static_cast<double>(hl.y);
+          }
+        }
+        o += (2 * nbj - ib) * 384;
       }
-      o += (2 * nbj - ib) * 384;
+#pragma unroll
+      for (int u = 0; u < U; ++u) acc += v[u];
     }
   }
   p.runs[(static_cast<int64_t>(r) * 2 * p.nbj + blockIdx.x) * 384 + e] = acc;
