@@ -688,6 +688,19 @@ def run_c3(E):
     nnz8 = float((frames[D8:D8 + n8] != 0).float().mean()) * H * W
     sparse_bytes = nnz8 * (D8 + n8 / 2)
     del sr
+    # the same frames pushed one call per frame (push(): one frame's columns
+    # per launch chain, no batch)
+    sr = xg.FrameStream(lay, D8 + n8, sparse=True)
+    sr.push_many(frames[:D8])
+    E.sync()
+    a, b = E.ev(), E.ev()
+    a.record(E.stream)
+    for i in range(D8, D8 + n8):
+        sr.push(frames[i])
+    b.record(E.stream)
+    E.sync()
+    ms_r1 = a.elapsed_time(b) / n8
+    del sr
     # dense raw column (K5) at a bounded history depth: the HBM roofline
     D, n = 4096, 64
     sd = xg.FrameStream(lay, D + n)
@@ -716,8 +729,13 @@ def run_c3(E):
                                  "achieved_gbs": (raw_bytes_tail + cmp_bytes_tail) / (tail_ms / 1e3) / 1e9},
         "raw_sparse_push": {
             "depth": D8, "frames_per_s": 1e3 / ms_r, "ms_per_frame": ms_r,
-            "what": "raw-only photon-event stream, whole push timed (ingest + K5s column + g2)",
-            "roofline": {"kernel": "k_stream_ingest_sparse + k_stream_sparse (whole push)",
+            "what": "raw-only photon-event stream through push_many (batches of 16: one ingest, "
+                    "one K5s grid over the batch's frames, in-order lag fold), whole batch timed",
+            "single_push": {"frames_per_s": 1e3 / ms_r1, "ms_per_frame": ms_r1,
+                            "frac_of_hbm": sparse_bytes / (ms_r1 / 1e3) / 1e9 / E.peaks["hbm_gbs"],
+                            "what": "push() per frame: ingest -> K5s chained by programmatic "
+                                    "dependent launch"},
+            "roofline": {"kernel": "k_stream_ingest_sparse + k_stream_sparse<batch> + fold (whole batch)",
                          "bound": "hbm", "bytes_per_frame": sparse_bytes,
                          "bytes_note": "nnz x t: the new frame's nonzero pixels' history rows",
                          "achieved": sparse_bytes / (ms_r / 1e3) / 1e9, "peak": hbm,
@@ -913,6 +931,9 @@ def main():
         return
 
     E = Env(args)
+    if args.only == "c3":  # development: the streaming section alone
+        print(json.dumps(run_c3(E)), flush=True)
+        return
     line = {"metric": METRIC, "value": None, "unit": "frames/s", "n_gpus": E.world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",

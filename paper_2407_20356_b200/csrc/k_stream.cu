@@ -113,11 +113,14 @@ __global__ void __launch_bounds__(256) k_stream_proj_acc(StreamParams p) {
   // slices in pacc (integer atomics: exact, order-free)
   __shared__ int32_t red[8][768];
   const int r = blockIdx.x;
+  const int f = blockIdx.z;  // frame t + f of a batch (0 for a single push)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   pdl_wait();  // ingest(t): nonzero lists, 1/|x_t|
   pdl_launch_dependents();
   const int koff = p.ring_koff[r];
-  const int n = p.nz_n[r];
+  const int n = p.nz_n[f * p.n_rings + r];
+  const int32_t* nz_col = p.nz_col + f * p.nz_bstride;
+  const uint8_t* nz_val = p.nz_val + f * p.nz_bstride;
   const int zb = static_cast<int>((static_cast<int64_t>(n) * blockIdx.y) / PZ);
   const int ze = static_cast<int>((static_cast<int64_t>(n) * (blockIdx.y + 1)) / PZ);
   const int nw = p.vdt_ld >> 2;
@@ -133,8 +136,8 @@ __global__ void __launch_bounds__(256) k_stream_proj_acc(StreamParams p) {
     for (int u = 0; u < PA_U; ++u) {
       const int e = e0 + 8 * u;
       const bool in = e < ze;
-      const int col = in ? p.nz_col[koff + e] : 0;
-      xv[u] = in ? p.nz_val[koff + e] : 0;
+      const int col = in ? nz_col[koff + e] : 0;
+      xv[u] = in ? nz_val[koff + e] : 0;
       const uint32_t* row = reinterpret_cast<const uint32_t*>(p.vdt + static_cast<int64_t>(col) * p.vdt_ld);
 #pragma unroll
       for (int m = 0; m < PA_MAXW; ++m) {
@@ -159,7 +162,7 @@ __global__ void __launch_bounds__(256) k_stream_proj_acc(StreamParams p) {
   }
   __syncthreads();
   const int nacc = p.n_digits * p.k;  // <= 768
-  int32_t* pa = p.pacc + static_cast<int64_t>(r) * 768;
+  int32_t* pa = p.pacc + f * p.pacc_bstride + static_cast<int64_t>(r) * 768;
   for (int j = threadIdx.x; j < nacc; j += 256) {
     int32_t tot = 0;
 #pragma unroll
@@ -172,17 +175,18 @@ __global__ void __launch_bounds__(256) k_stream_proj_acc(StreamParams p) {
 // (bitwise-equal rows); resets pacc.
 __global__ void __launch_bounds__(128) k_stream_proj_fin(StreamParams p) {
   const int r = blockIdx.x;
+  const int64_t t = p.t + blockIdx.y;  // frame t + f of a batch
   pdl_wait();  // proj_acc(t): the digit sums
   pdl_launch_dependents();
-  int32_t* pa = p.pacc + static_cast<int64_t>(r) * 768;
-  const double inv = p.inv[static_cast<int64_t>(r) * p.inv_ld + p.t];
+  int32_t* pa = p.pacc + blockIdx.y * p.pacc_bstride + static_cast<int64_t>(r) * 768;
+  const double inv = p.inv[static_cast<int64_t>(r) * p.inv_ld + t];
   for (int j = threadIdx.x; j < p.k; j += blockDim.x) {
     const int32_t a0 = pa[j], a1 = p.n_digits > 1 ? pa[p.k + j] : 0;
     const int32_t a2 = p.n_digits > 2 ? pa[2 * p.k + j] : 0;
     const double y =
         combine_digits(a0, a1, a2, p.n_digits, p.scale[static_cast<int64_t>(r) * p.k + j], inv);
-    p.y[(static_cast<int64_t>(r) * p.y_ld + p.t) * p.k + j] = y;
-    p.yf[(static_cast<int64_t>(r) * p.y_ld + p.t) * p.kq + j] = static_cast<float>(y);
+    p.y[(static_cast<int64_t>(r) * p.y_ld + t) * p.k + j] = y;
+    p.yf[(static_cast<int64_t>(r) * p.y_ld + t) * p.kq + j] = static_cast<float>(y);
   }
   __syncthreads();
   for (int j = threadIdx.x; j < p.n_digits * p.k; j += blockDim.x) pa[j] = 0;
@@ -447,6 +451,10 @@ template <> struct SsVec<16> {
   __device__ static void words(const T& v, uint32_t* w) { w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w; }
   __device__ static T zero() { return make_uint4(0u, 0u, 0u, 0u); }
 };
+// BATCH: grid.z = frame t + j of a batch (its nonzero lists in slot j); the
+// column entries go to the scratch column (r, j) and k_stream_fold adds them
+// to the lag sums in frame order -- the frames' loads all overlap.
+template <bool BATCH>
 __global__ void __launch_bounds__(32 * SS_W, SS_MINB) k_stream_sparse(StreamParams p) {
   using VT = typename SsVec<SS_V>::T;
   __shared__ int32_t sc[SS_CHUNK];
@@ -454,16 +462,23 @@ __global__ void __launch_bounds__(32 * SS_W, SS_MINB) k_stream_sparse(StreamPara
   __shared__ uint32_t red[SS_W][SS_F + 1];
   const int r = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int j = BATCH ? static_cast<int>(blockIdx.z) : 0;
+  const int64_t t = p.t + j;
+  const int64_t sb = static_cast<int64_t>(blockIdx.x) * SS_F;
+  if (BATCH && sb > t) return;  // CTA-uniform
+  const int32_t* nz_col = p.nz_col + j * p.nz_bstride;
+  const uint8_t* nz_val = p.nz_val + j * p.nz_bstride;
   // this push's ingest has completed: nonzero lists, hist column t, 1/|x_t|
   // (waited for here, or transitively through the compressed kernels; in a
   // photon-event batch the ingest of every frame completed before the
   // batch's first K5s started, so K5s(t+1) may stream its history while
   // K5s(t) still runs and waits for it only before touching the g2 sums)
-  if (!p.pdl_wait_end && !p.pdl_wait_fin) pdl_wait();
-  pdl_launch_dependents();
+  if (!BATCH) {
+    if (!p.pdl_wait_end && !p.pdl_wait_fin) pdl_wait();
+    pdl_launch_dependents();
+  }
   const int koff = p.ring_koff[r];
-  const int n = p.nz_n[r];
-  const int64_t sb = static_cast<int64_t>(blockIdx.x) * SS_F;
+  const int n = p.nz_n[j * p.n_rings + r];
   const int64_t s0 = sb + SS_V * lane;
   uint32_t acc[SS_V];
 #pragma unroll
@@ -473,11 +488,11 @@ __global__ void __launch_bounds__(32 * SS_W, SS_MINB) k_stream_sparse(StreamPara
     const int cn = n - c0 < SS_CHUNK ? n - c0 : SS_CHUNK;
     __syncthreads();
     for (int i = threadIdx.x; i < cn; i += 32 * SS_W) {
-      sc[i] = p.nz_col[koff + c0 + i];
-      sv[i] = p.nz_val[koff + c0 + i];
+      sc[i] = nz_col[koff + c0 + i];
+      sv[i] = nz_val[koff + c0 + i];
     }
     __syncthreads();
-    if (s0 <= p.t) {
+    if (s0 <= t) {
       // SS_U independent loads in flight per lane before any use
       for (int i0 = warp; i0 < cn; i0 += SS_W * SS_U) {
         VT wv[SS_U];
@@ -508,25 +523,146 @@ __global__ void __launch_bounds__(32 * SS_W, SS_MINB) k_stream_sparse(StreamPara
     }
   }
 #pragma unroll
-  for (int j = 0; j < SS_V; ++j) red[warp][SS_V * lane + j] = acc[j];
-  if (p.pdl_wait_fin) pdl_wait();  // K5s(t-1) done: lag sums in push order
+  for (int q = 0; q < SS_V; ++q) red[warp][SS_V * lane + q] = acc[q];
+  if (!BATCH && p.pdl_wait_fin) pdl_wait();  // K5s(t-1) done: lag sums in push order
   __syncthreads();
-  const double inv_t = p.inv[static_cast<int64_t>(r) * p.inv_ld + p.t];
+  const double inv_t = BATCH ? 0.0 : p.inv[static_cast<int64_t>(r) * p.inv_ld + t];
 #pragma unroll
   for (int f = threadIdx.x; f < SS_F; f += 32 * SS_W) {
     const int64_t s = sb + f;
-    if (s > p.t) break;
+    if (s > t) break;
     uint32_t tot = 0;
 #pragma unroll
     for (int w = 0; w < SS_W; ++w) tot += red[w][f];
     const int accv = static_cast<int>(tot);
-    const double inv_s = p.inv[static_cast<int64_t>(r) * p.inv_ld + s];
-    const int64_t gi = static_cast<int64_t>(r) * p.g2_ld + (p.t - s);
-    p.g2sum[gi] += static_cast<double>(accv) * (inv_s * inv_t);
-    p.g2cnt[gi] += (inv_s != 0.0 && inv_t != 0.0) ? 1 : 0;
-    if (p.gcol) p.gcol[static_cast<int64_t>(r) * p.col_ring_stride + s * p.col_ld + p.t] = accv;
+    if (BATCH) {
+      p.gscr[(static_cast<int64_t>(r) * p.scr_nb + j) * p.scr_ld + s] = accv;
+    } else {
+      const double inv_s = p.inv[static_cast<int64_t>(r) * p.inv_ld + s];
+      const int64_t gi = static_cast<int64_t>(r) * p.g2_ld + (t - s);
+      p.g2sum[gi] += static_cast<double>(accv) * (inv_s * inv_t);
+      p.g2cnt[gi] += (inv_s != 0.0 && inv_t != 0.0) ? 1 : 0;
+    }
+    if (p.gcol) p.gcol[static_cast<int64_t>(r) * p.col_ring_stride + s * p.col_ld + t] = accv;
   }
-  if (p.pdl_wait_end) pdl_wait();  // cmp(t) has completed too (see above)
+  if (!BATCH && p.pdl_wait_end) pdl_wait();  // cmp(t) has completed too (see above)
+}
+
+// K6c: the compressed columns of a batch of nb new frames t .. t + nb - 1,
+// grid (ceil((t + nb) / SR_ROWS), rings).  A warp loads its 8 history rows
+// once (as K6b does) and forms C~(s, t + j) for every frame j of the batch:
+// the new rows come from shared memory, the products are K6b's per-lane fmaf
+// chains, and the cross-lane sums are K6b's xor-butterfly tree taken by
+// recursive halving (8 rows per 9 shuffles instead of 40; every pair sum is
+// the butterfly's, so C~ equals K6b's bitwise).  History bytes are read once
+// per batch instead of once per frame.
+constexpr int CB_MAXNB = 16;
+template <int MAXV>
+__global__ void __launch_bounds__(SR_THREADS, 2) k_stream_cmp_batch(StreamParams p) {
+  __shared__ float4 ynew[CB_MAXNB][32 * MAXV];
+  const int r = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kq = p.kq, nv = kq >> 2, nb = p.scr_nb;
+  const float* ybase = p.yf + static_cast<int64_t>(r) * p.y_ld * kq;
+  for (int i = threadIdx.x; i < nb * 32 * MAXV; i += SR_THREADS) {
+    const int jj = i / (32 * MAXV), v = i % (32 * MAXV);
+    ynew[jj][v] = v < nv ? *reinterpret_cast<const float4*>(ybase + (p.t + jj) * kq + 4 * v)
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  constexpr int RPW = SR_ROWS / (SR_THREADS / 32);
+  static_assert(RPW == 8, "recursive halving below is written for 8 rows per warp");
+  const int64_t t_last = p.t + nb - 1;
+  const int64_t s_first = static_cast<int64_t>(blockIdx.x) * SR_ROWS + warp * RPW;
+  float4 ld[RPW][MAXV];
+#pragma unroll
+  for (int m = 0; m < MAXV; ++m) {
+    const int v = lane + 32 * m;
+#pragma unroll
+    for (int q = 0; q < RPW; ++q) {
+      const int64_t s = s_first + q;
+      ld[q][m] = (32 * m < nv && v < nv && s <= t_last)
+                     ? __ldcs(reinterpret_cast<const float4*>(ybase + s * kq + 4 * v))
+                     : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+  __syncthreads();
+  const int b4 = (lane >> 4) & 1, b3 = (lane >> 3) & 1, b2 = (lane >> 2) & 1;
+  const int qme = (lane >> 2) & 7;  // the row this lane's sum belongs to
+  const int64_t s_me = s_first + qme;
+  for (int j = 0; j < nb; ++j) {
+    const int64_t t = p.t + j;
+    if (s_first > t) continue;  // warp-uniform
+    float part[RPW];
+#pragma unroll
+    for (int q = 0; q < RPW; ++q) part[q] = 0.f;
+#pragma unroll
+    for (int m = 0; m < MAXV; ++m) {
+      if (32 * m >= nv) break;
+      const float4 yn = ynew[j][lane + 32 * m];
+#pragma unroll
+      for (int q = 0; q < RPW; ++q)
+        part[q] = fmaf(ld[q][m].x, yn.x,
+                       fmaf(ld[q][m].y, yn.y, fmaf(ld[q][m].z, yn.z, fmaf(ld[q][m].w, yn.w, part[q]))));
+    }
+    // recursive halving over lane bits 4, 3, 2, then butterflies over 1, 0
+    float w4[4], w3[2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float send = b4 ? part[i] : part[i + 4];
+      const float keep = b4 ? part[i + 4] : part[i];
+      w4[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const float send = b3 ? w4[i] : w4[i + 2];
+      const float keep = b3 ? w4[i + 2] : w4[i];
+      w3[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+    float a;
+    {
+      const float send = b2 ? w3[0] : w3[1];
+      const float keep = b2 ? w3[1] : w3[0];
+      a = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+    a += __shfl_xor_sync(0xffffffffu, a, 2);
+    a += __shfl_xor_sync(0xffffffffu, a, 1);
+    if ((lane & 3) == 0 && s_me <= t) {
+      p.cscr[(static_cast<int64_t>(r) * nb + j) * p.scr_ld + s_me] = a;
+      if (p.ccol) p.ccol[static_cast<int64_t>(r) * p.col_ring_stride + s_me * p.col_ld + t] = a;
+    }
+  }
+}
+
+// The lag sums of a batch: thread per lag d of ring r, frames in ascending
+// order -- exactly the per-push updates of K5s (RAW) / K6b, in push order.
+template <bool RAW>
+__global__ void __launch_bounds__(256) k_stream_fold(StreamParams p) {
+  const int r = blockIdx.y;
+  const int nb = p.scr_nb;
+  const int64_t d = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x;
+  if (d > p.t + nb - 1) return;
+  const int64_t gi = static_cast<int64_t>(r) * p.g2_ld + d;
+  double* sump = RAW ? p.g2sum : p.cg2sum;
+  int64_t* cntp = RAW ? p.g2cnt : p.cg2cnt;
+  double sum = sump[gi];
+  int64_t cnt = cntp[gi];
+  const double* inv = p.inv + static_cast<int64_t>(r) * p.inv_ld;
+  for (int j = 0; j < nb; ++j) {
+    const int64_t t = p.t + j, s = t - d;
+    if (s < 0) continue;
+    const double inv_s = inv[s], inv_t = inv[t];
+    const int64_t si = (static_cast<int64_t>(r) * nb + j) * p.scr_ld + s;
+    if (RAW) {
+      const int accv = p.gscr[si];
+      sum += static_cast<double>(accv) * (inv_s * inv_t);
+    } else {
+      const double acc = p.cscr[si];
+      sum += acc;
+    }
+    cnt += (inv_s != 0.0 && inv_t != 0.0) ? 1 : 0;
+  }
+  sump[gi] = sum;
+  cntp[gi] = cnt;
 }
 
 cudaError_t launch_stream_ingest(const StreamParams& p, cudaStream_t s) {
@@ -562,7 +698,31 @@ cudaError_t launch_stream_ingest_sparse(const StreamParams& p, cudaStream_t s, b
 
 cudaError_t launch_stream_sparse(const StreamParams& p, int32_t n_rings, cudaStream_t s, bool pdl) {
   dim3 grid(static_cast<unsigned>((p.t + 1 + SS_F - 1) / SS_F), n_rings);
-  return launch_maybe_pdl(k_stream_sparse, grid, dim3(32 * SS_W), s, pdl, p);
+  return launch_maybe_pdl(k_stream_sparse<false>, grid, dim3(32 * SS_W), s, pdl, p);
+}
+
+cudaError_t launch_stream_batch(const StreamParams& p, int32_t n_rings, bool raw, bool cmp,
+                                cudaStream_t s) {
+  const int nb = p.scr_nb;
+  if (nb < 1 || nb > CB_MAXNB) return cudaErrorInvalidValue;
+  const int64_t rows = p.t + nb;
+  const dim3 fold_grid(static_cast<unsigned>((rows + 255) / 256), n_rings);
+  if (cmp) {
+    k_stream_proj_acc<<<dim3(n_rings, PZ, nb), 256, 0, s>>>(p);
+    k_stream_proj_fin<<<dim3(n_rings, nb), 128, 0, s>>>(p);
+    const dim3 grid(static_cast<unsigned>((rows + SR_ROWS - 1) / SR_ROWS), n_rings);
+    if (p.kq / 4 <= 32)
+      k_stream_cmp_batch<1><<<grid, SR_THREADS, 0, s>>>(p);
+    else
+      k_stream_cmp_batch<2><<<grid, SR_THREADS, 0, s>>>(p);
+    k_stream_fold<false><<<fold_grid, 256, 0, s>>>(p);
+  }
+  if (raw) {
+    const dim3 grid(static_cast<unsigned>((rows + SS_F - 1) / SS_F), n_rings, nb);
+    k_stream_sparse<true><<<grid, 32 * SS_W, 0, s>>>(p);
+    k_stream_fold<true><<<fold_grid, 256, 0, s>>>(p);
+  }
+  return cudaGetLastError();
 }
 
 cudaError_t launch_stream_raw(const StreamParams& p, int32_t n_rings, int64_t max_kpad,

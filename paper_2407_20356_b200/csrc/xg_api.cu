@@ -2403,6 +2403,12 @@ struct xg_stream {
   int32_t* d_nzb_col = nullptr;
   uint8_t* d_nzb_val = nullptr;
   int32_t* d_nzb_n = nullptr;
+  // batched columns: per-frame scratch columns [ring][kIngestBatch][tp] and
+  // per-frame projection digit sums [kIngestBatch][ring][768]
+  int32_t* d_gscr = nullptr;
+  float* d_cscr = nullptr;
+  int32_t* d_paccb = nullptr;
+  bool scr_ready = false;
   unsigned int* d_done = nullptr;  // sparse ingest's CTA counter
 };
 
@@ -2585,27 +2591,19 @@ void xg_stream_destroy(xg_stream* s) {
   dfree(s->d_nzb_col);
   dfree(s->d_nzb_val);
   dfree(s->d_nzb_n);
+  dfree(s->d_gscr);
+  dfree(s->d_cscr);
+  dfree(s->d_paccb);
   delete s;
 }
 
 int64_t xg_stream_frames(const xg_stream* s) { return s ? s->t : -1; }
 
-// One push.  slot >= 0: photon-event batch member whose ingest already ran
-// (xg_stream_push_batch), its nonzero lists in batch slot `slot`.
-static int push_one(xg_stream* s, const uint8_t* frame, int on_device, int slot) {
-  xg_ctx* c = s->ctx;
+// The stream's column-kernel parameters for frame s->t (the per-push nonzero
+// list / counter slots and the frame pointer are set by the caller).
+static StreamParams column_params(const xg_stream* s) {
   const xg_layout* L = s->L;
-  if (s->t >= s->tmax) return fail(c, XG_ERR_SHAPE, "stream: capacity %lld reached", (long long)s->tmax);
-  // a device frame is read in place when 16-byte aligned (stream-ordered:
-  // the caller keeps it valid until the push's work has run)
-  const uint8_t* d_frame = s->d_frame;
-  if (on_device && (reinterpret_cast<uintptr_t>(frame) & 15u) == 0)
-    d_frame = frame;
-  else
-    XG_CUDA(c, cudaMemcpyAsync(s->d_frame, frame, (size_t)L->pixels,
-                               on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
-                               c->stream));
-  StreamParams sp;
+  StreamParams sp{};
   sp.x = s->d_x;
   sp.ktot = L->ktot;
   sp.t = s->t;
@@ -2633,6 +2631,41 @@ static int push_one(xg_stream* s, const uint8_t* frame, int on_device, int slot)
   sp.y_ld = s->tp;
   sp.hist = s->d_hist;
   sp.hp = s->hp;
+  sp.pacc = s->d_pacc;
+  sp.pixcol = s->d_pixcol;
+  sp.pixels = L->pixels;
+  sp.colpix = s->d_colpix;
+  sp.blk_ring = s->d_blk_ring;
+  sp.n_rings = L->rings;
+  sp.norm2 = reinterpret_cast<unsigned long long*>(s->d_norm2);
+  sp.norms_w = s->d_norms;
+  sp.inv_w = s->d_inv;
+  sp.zero_count = s->d_zero;
+  sp.first_zero = s->d_first_zero;
+  sp.nz_bits = s->d_nz_bits;
+  sp.nz_words = static_cast<int32_t>(s->tp / 32);
+  sp.err = s->ctx->d_err;
+  sp.ovf_check = (s->flags & XG_STREAM_NO_RAW) ? 0 : 1;
+  sp.done = s->d_done;
+  return sp;
+}
+
+// One push.  slot >= 0: photon-event batch member whose ingest already ran
+// (xg_stream_push_batch), its nonzero lists in batch slot `slot`.
+static int push_one(xg_stream* s, const uint8_t* frame, int on_device, int slot) {
+  xg_ctx* c = s->ctx;
+  const xg_layout* L = s->L;
+  if (s->t >= s->tmax) return fail(c, XG_ERR_SHAPE, "stream: capacity %lld reached", (long long)s->tmax);
+  // a device frame is read in place when 16-byte aligned (stream-ordered:
+  // the caller keeps it valid until the push's work has run)
+  const uint8_t* d_frame = s->d_frame;
+  if (on_device && (reinterpret_cast<uintptr_t>(frame) & 15u) == 0)
+    d_frame = frame;
+  else
+    XG_CUDA(c, cudaMemcpyAsync(s->d_frame, frame, (size_t)L->pixels,
+                               on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                               c->stream));
+  StreamParams sp = column_params(s);
   sp.nz_col = s->d_nz_col ? s->d_nz_col + (s->t & 1) * L->ktot : nullptr;
   sp.nz_val = s->d_nz_val ? s->d_nz_val + (s->t & 1) * L->ktot : nullptr;
   sp.nz_n = s->d_nz_n ? s->d_nz_n + (s->t % 3) * L->rings : nullptr;
@@ -2644,26 +2677,10 @@ static int push_one(xg_stream* s, const uint8_t* frame, int on_device, int slot)
     sp.nz_n = s->d_nzb_n + slot * L->rings;
     sp.nz_next = nullptr;
   }
-  sp.pacc = s->d_pacc;
   sp.frame = d_frame;
-  sp.pixcol = s->d_pixcol;
-  sp.pixels = L->pixels;
-  sp.colpix = s->d_colpix;
-  sp.blk_ring = s->d_blk_ring;
-  sp.n_rings = L->rings;
-  sp.norm2 = reinterpret_cast<unsigned long long*>(s->d_norm2);
   sp.norm2_next = s->t + 1 < s->tmax
                       ? reinterpret_cast<unsigned long long*>(s->d_norm2 + (s->t + 1) * L->rings)
                       : nullptr;
-  sp.norms_w = s->d_norms;
-  sp.inv_w = s->d_inv;
-  sp.zero_count = s->d_zero;
-  sp.first_zero = s->d_first_zero;
-  sp.nz_bits = s->d_nz_bits;
-  sp.nz_words = static_cast<int32_t>(s->tp / 32);
-  sp.err = c->d_err;
-  sp.ovf_check = (s->flags & XG_STREAM_NO_RAW) ? 0 : 1;
-  sp.done = s->d_done;
   const bool sparse = (s->flags & XG_STREAM_SPARSE) != 0;
   // raw sparse pushes chain ingest -> [compressed column ->] raw column ->
   // next ingest with programmatic dependent launches on one stream (no launch
@@ -2735,8 +2752,19 @@ int xg_stream_push(xg_stream* s, const uint8_t* frame, int on_device) {
 // pushes, without the per-frame host round trip of the caller.  Photon-event
 // streams fed device frames ingest kIngestBatch frames per launch (one
 // latency-bound ingest of ~10 us amortised over the batch instead of paid in
-// front of every column); each frame's columns then run as in a push.
+// front of every column), then form the batch's columns together
+// (launch_stream_batch): the raw columns of all its frames in one grid, the
+// compressed columns with every history row read once for the whole batch,
+// and the lag sums folded in frame order -- bitwise the same as n pushes.
+// XG_STREAM_BATCH_COLUMNS=0 runs each frame's columns as in a push instead.
 constexpr int kIngestBatch = 16;
+static bool batch_columns_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("XG_STREAM_BATCH_COLUMNS");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 int xg_stream_push_batch(xg_stream* s, const uint8_t* frames, int64_t n, int on_device) {
   if (!s || !frames) return XG_ERR_INVALID;
   xg_ctx* c = s->ctx;
@@ -2790,6 +2818,36 @@ int xg_stream_push_batch(xg_stream* s, const uint8_t* frames, int64_t n, int on_
     XG_CUDA(c, cudaMemsetAsync(s->d_nzb_n, 0, (size_t)nb * L->rings * sizeof(int32_t), c->stream));
     XG_CUDA(c, launch_stream_ingest_sparse(sp, c->stream, false, nb));
     c->launches++;
+    const bool raw = !(s->flags & XG_STREAM_NO_RAW);
+    if (batch_columns_enabled()) {
+      if (!s->scr_ready) {
+        const size_t cols = (size_t)L->rings * kIngestBatch * s->tp;
+        if (raw) XG_CUDA(c, dalloc(&s->d_gscr, cols));
+        if (s->B) {
+          XG_CUDA(c, dalloc(&s->d_cscr, cols));
+          XG_CUDA(c, dalloc(&s->d_paccb, (size_t)kIngestBatch * L->rings * 768));
+          XG_CUDA(c, cudaMemsetAsync(s->d_paccb, 0,
+                                     (size_t)kIngestBatch * L->rings * 768 * sizeof(int32_t),
+                                     c->stream));
+        }
+        s->scr_ready = true;
+      }
+      StreamParams bp = column_params(s);
+      bp.nz_col = s->d_nzb_col;
+      bp.nz_val = s->d_nzb_val;
+      bp.nz_n = s->d_nzb_n;
+      bp.nz_bstride = L->ktot;
+      bp.pacc = s->d_paccb;
+      bp.pacc_bstride = (int64_t)L->rings * 768;
+      bp.gscr = raw ? s->d_gscr : nullptr;
+      bp.cscr = s->d_cscr;
+      bp.scr_ld = s->tp;
+      bp.scr_nb = nb;
+      XG_CUDA(c, launch_stream_batch(bp, L->rings, raw, s->B != nullptr, c->stream));
+      c->launches += (raw ? 2 : 0) + (s->B ? 4 : 0);
+      s->t += nb;
+      continue;
+    }
     for (int j = 0; j < nb; ++j) {
       const int rc = push_one(s, frames + (i0 + j) * L->pixels, on_device, j);
       if (rc) return rc;

@@ -295,6 +295,15 @@ struct StreamParams {
   // at frame + f * pixels, its nonzero lists at nz_col/nz_val + f * nz_bstride
   // and counts at nz_n + f * n_rings (zeroed before the launch)
   int64_t nz_bstride;
+  // batched columns (push_batch, grid.z = frames t .. t + nb - 1): the column
+  // kernels write their entries to per-frame scratch columns
+  // [ring][scr_nb][scr_ld] (raw: int32 Gram, compressed: fp32 C~) and
+  // k_stream_fold adds them to the lag sums in ascending frame order.
+  int32_t* gscr;
+  float* cscr;
+  int64_t scr_ld;
+  int32_t scr_nb;            // frames of the batch
+  int64_t pacc_bstride;      // proj_acc/proj_fin: frame f's digit sums at pacc + f * pacc_bstride
 };
 // One-frame ingest for the streaming path: ring-major row t of the history,
 // |x_t|^2 per ring, and in sparse mode the frame's nonzeros per ring plus
@@ -310,6 +319,13 @@ cudaError_t launch_stream_sparse(const StreamParams& p, int32_t n_rings, cudaStr
 cudaError_t launch_stream_raw(const StreamParams& p, int32_t n_rings, int64_t max_kpad,
                               cudaStream_t s);
 cudaError_t launch_stream_cmp(const StreamParams& p, int32_t n_rings, cudaStream_t s, bool pdl);
+// Batched columns of frames t .. t + nb - 1 (p.scr_nb = nb, ingested): the
+// photon-event raw columns (K5s, grid.z = frame), the projections (K6a, one
+// launch each for the batch) and the compressed columns (K6c: every history
+// row loaded once for all nb new rows), each to its scratch columns, then
+// the in-order lag-sum fold.  Results equal nb single pushes bitwise.
+cudaError_t launch_stream_batch(const StreamParams& p, int32_t n_rings, bool raw, bool cmp,
+                                cudaStream_t s);
 cudaError_t launch_g2_div(const double* sum, const int64_t* cnt, double* out, int64_t n,
                           cudaStream_t s);
 

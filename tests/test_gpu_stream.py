@@ -96,14 +96,17 @@ def test_sparse_stream_equals_dense(ctx, orc, mu):
         assert np.array_equal(g2s, g2d) and np.array_equal(cs, cd)
 
 
-@pytest.mark.parametrize("basis_k,raw", [(0, True), (6, True), (6, False)])
+@pytest.mark.parametrize("basis_k,raw", [(0, True), (6, True), (6, False), (37, True), (130, True)])
 def test_push_many_equals_single_pushes(ctx, orc, basis_k, raw):
     """push_many (one library call for n frames) == n push() calls, bitwise:
     photon-event push_many ingests 16 frames per launch (batch slots for the
     nonzero lists, a zero frame inside a batch, a partial last batch) and
-    chains the columns with programmatic dependent launches; single pushes
-    chain push t + 1's ingest beside push t's column kernel.  Neither may
-    change a bit, raw or compressed-only."""
+    forms the batch's columns together (K5s over all its frames, K6c reading
+    each coefficient row once for the batch, lag sums folded in frame
+    order); single pushes chain push t + 1's ingest beside push t's column
+    kernel.  Neither may change a bit of the Gram, the C~ columns, the
+    coefficients or the lag sums, raw or compressed-only; k = 130 takes the
+    two-chunk (k > 128) compressed kernels."""
     import torch
 
     t, h, w, q = 300, 96, 96, 4
@@ -114,10 +117,10 @@ def test_push_many_equals_single_pushes(ctx, orc, basis_k, raw):
     basis = None
     if basis_k:
         basis = xg.Basis(lay, basis_k)
-        xg.FrameSeries(lay, 64).load(frames[64:128]).build_basis(basis_k, basis=basis)
+        xg.FrameSeries(lay, 200).load(frames[64:264]).build_basis(basis_k, basis=basis)
     dev = torch.from_numpy(frames).cuda()
-    a = xg.FrameStream(lay, t, basis=basis, store_ttc=raw, sparse=True, raw=raw)
-    b = xg.FrameStream(lay, t, basis=basis, store_ttc=raw, sparse=True, raw=raw)
+    a = xg.FrameStream(lay, t, basis=basis, store_ttc=True, sparse=True, raw=raw)
+    b = xg.FrameStream(lay, t, basis=basis, store_ttc=True, sparse=True, raw=raw)
     for i in range(t):
         a.push(dev[i])
     b.push_many(dev[:100])
@@ -133,6 +136,8 @@ def test_push_many_equals_single_pushes(ctx, orc, basis_k, raw):
             assert np.array_equal(va, vb) and np.array_equal(ca, cb)
         if basis_k:
             assert np.array_equal(a.coeffs(r)[0], b.coeffs(r)[0])
+            assert np.array_equal(a.ttc(r, compressed=True, dtype="f32"),
+                                  b.ttc(r, compressed=True, dtype="f32"))
             _, va, ca = a.g2(r, compressed=True)
             _, vb, cb = b.g2(r, compressed=True)
             assert np.array_equal(va, vb) and np.array_equal(ca, cb)
