@@ -729,13 +729,21 @@ def run_c3(E):
                                  "achieved_gbs": (raw_bytes_tail + cmp_bytes_tail) / (tail_ms / 1e3) / 1e9},
         "raw_sparse_push": {
             "depth": D8, "frames_per_s": 1e3 / ms_r, "ms_per_frame": ms_r,
-            "what": "raw-only photon-event stream through push_many (batches of 16: one ingest, "
-                    "one K5s grid over the batch's frames, in-order lag fold), whole batch timed",
+            "what": "raw-only photon-event stream through push_many (batches of 16: one ingest; "
+                    "sealed 1024-frame event blocks merged into 8192-frame segments read by K5e "
+                    "(per-pixel event lists), the unsealed tail by one K5s grid over the batch's "
+                    "frames; in-order lag fold), whole batch timed incl. the block seal that "
+                    "falls in the window",
+            "event_history_speedup_vs_dense_column": ms_r1 / ms_r,
             "single_push": {"frames_per_s": 1e3 / ms_r1, "ms_per_frame": ms_r1,
                             "frac_of_hbm": sparse_bytes / (ms_r1 / 1e3) / 1e9 / E.peaks["hbm_gbs"],
-                            "what": "push() per frame: ingest -> K5s chained by programmatic "
-                                    "dependent launch"},
-            "roofline": {"kernel": "k_stream_ingest_sparse + k_stream_sparse<batch> + fold (whole batch)",
+                            "what": "push() per frame: ingest -> K5s over the dense pixel-major "
+                                    "history (nnz x t bytes), chained by programmatic dependent "
+                                    "launch"},
+            "roofline": {"kernel": "push_many (K1s + K5e + K5s + fold): DENSE-EQUIVALENT rate -- "
+                                   "the event path reads ~1/5 of these bytes, so frac > 1 is "
+                                   "algorithmic, not a bandwidth claim; K5e itself is latency-bound "
+                                   "(profiles/r2_summary.txt)",
                          "bound": "hbm", "bytes_per_frame": sparse_bytes,
                          "bytes_note": "nnz x t: the new frame's nonzero pixels' history rows",
                          "achieved": sparse_bytes / (ms_r / 1e3) / 1e9, "peak": hbm,

@@ -315,8 +315,11 @@ __global__ void __launch_bounds__(128) k_stream_ingest(StreamParams p) {
 // meets in shared memory first (integer sums: exact, order-free).  Block 0
 // clears the next push's counters (nz_next, norm2 row t + 1).
 constexpr int SI_THREADS = 256;
-constexpr int SI_PX = 4;  // 16 per thread (256 CTAs) measured slower: 10.2 -> 14.2 us
+// pixels per thread: 4 for a single frame (16 per thread = 256 CTAs measured
+// slower: 10.2 -> 14.2 us), 16 for a batch (16 frames x 1024 CTAs of 4 were
+// bound by the CTAs' fixed costs -- barriers, ring counters)
 constexpr int SI_MAXQ = 1024;
+template <int SI_PX>
 __global__ void __launch_bounds__(SI_THREADS) k_stream_ingest_sparse(StreamParams p) {
   __shared__ uint32_t cnt[SI_MAXQ], sq[SI_MAXQ];
   __shared__ int32_t base[SI_MAXQ];
@@ -338,7 +341,15 @@ __global__ void __launch_bounds__(SI_THREADS) k_stream_ingest_sparse(StreamParam
   const int64_t px0 = (static_cast<int64_t>(blockIdx.x) * SI_THREADS + threadIdx.x) * SI_PX;
   uint32_t wv[SI_PX / 4];
   if (px0 + SI_PX <= p.pixels) {
-    wv[0] = __ldcs(reinterpret_cast<const uint32_t*>(frame + px0));
+    if (SI_PX == 16) {
+      const uint4 q = __ldcs(reinterpret_cast<const uint4*>(frame + px0));
+      wv[0] = q.x;
+      wv[SI_PX / 4 > 1 ? 1 : 0] = q.y;
+      wv[SI_PX / 4 > 2 ? 2 : 0] = q.z;
+      wv[SI_PX / 4 > 3 ? 3 : 0] = q.w;
+    } else {
+      wv[0] = __ldcs(reinterpret_cast<const uint32_t*>(frame + px0));
+    }
   } else {
 #pragma unroll
     for (int k = 0; k < SI_PX / 4; ++k) {
@@ -380,22 +391,21 @@ __global__ void __launch_bounds__(SI_THREADS) k_stream_ingest_sparse(StreamParam
     nz_val[e] = v;
     if (p.hist) p.hist[static_cast<int64_t>(col) * p.hp + tf] = v;
   }
-  // the last CTA to finish computes frame t's norms, 1/|x|, nonzero bit and
-  // zero-frame bookkeeping (k_norms' expressions) -- no separate launch
+  // the last CTA of frame t + f to finish computes its norms, 1/|x|, nonzero
+  // bit and zero-frame bookkeeping (k_norms' expressions; the zero count and
+  // first zero are order-free atomics) -- no separate launch
   __shared__ bool last;
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
-    last = atomicAdd(p.done, 1u) == gridDim.x * gridDim.y - 1;
+    last = atomicAdd(p.done + f, 1u) == gridDim.x - 1;
   }
   __syncthreads();
   pdl_wait();  // the previous push's column kernel has completed (see above)
   if (!last) return;
   __threadfence();
-  // every frame of the batch, in ascending t (first_zero / zero counts)
-  for (int i = threadIdx.x; i < static_cast<int>(gridDim.y) * p.n_rings; i += blockDim.x) {
-    const int r = i % p.n_rings;
-    const int64_t tt = p.t + i / p.n_rings;
+  for (int r = threadIdx.x; r < p.n_rings; r += blockDim.x) {
+    const int64_t tt = tf;
     const long long n2 = static_cast<long long>(atomicAdd(p.norm2 + tt * p.n_rings + r, 0ull));
     const double nrm = sqrt(static_cast<double>(n2));
     p.norms_w[r * p.inv_ld + tt] = nrm;
@@ -408,7 +418,7 @@ __global__ void __launch_bounds__(SI_THREADS) k_stream_ingest_sparse(StreamParam
     }
     if (n2 >= (1ll << 31) && p.ovf_check) atomicOr(p.err, 4);
   }
-  if (threadIdx.x == 0) *p.done = 0u;
+  if (threadIdx.x == 0) p.done[f] = 0u;
 }
 
 // K5s: grid (ceil((t+1)/SS_F), rings), 8 warps.  A CTA owns SS_F = 32 SS_V
@@ -464,7 +474,7 @@ __global__ void __launch_bounds__(32 * SS_W, SS_MINB) k_stream_sparse(StreamPara
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int j = BATCH ? static_cast<int>(blockIdx.z) : 0;
   const int64_t t = p.t + j;
-  const int64_t sb = static_cast<int64_t>(blockIdx.x) * SS_F;
+  const int64_t sb = (BATCH ? p.s_begin : 0) + static_cast<int64_t>(blockIdx.x) * SS_F;
   if (BATCH && sb > t) return;  // CTA-uniform
   const int32_t* nz_col = p.nz_col + j * p.nz_bstride;
   const uint8_t* nz_val = p.nz_val + j * p.nz_bstride;
@@ -633,6 +643,289 @@ __global__ void __launch_bounds__(SR_THREADS, 2) k_stream_cmp_batch(StreamParams
   }
 }
 
+// ---------------------------------------------------------- event history
+// Photon-event data at mu ~ 0.02 leaves ~98% of the dense history bytes
+// zero, and the dense column reads all of them (nnz * t bytes per frame).
+// A sealed block of EV tb frames keeps, per pixel column, the list of its
+// (s_local, count) events: a column entry then costs one 8-byte index load
+// plus ~tb * occupancy 4-byte events instead of tb bytes.
+
+// nonzero bytes of a 32-bit word
+__device__ __forceinline__ uint32_t nzbytes(uint32_t x) {
+  return __popc((((x & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | x) & 0x80808080u);
+}
+
+constexpr int EV_MAXTB = 8192;  // frames of a segment (its column entries in shared memory)
+// Seal: grid ceil(ktot / 256), 8 warps; warp w takes pixel columns c0 + 32 w
+// .. + 32 one at a time, lane L the words [L wpl, (L + 1) wpl) of the row's
+// block (wpl = tb / 128).  Pass 1 counts each column's events; the CTA scans
+// its 256 counts and reserves its run of the block's list with one atomic;
+// pass 2 re-reads the rows (L2) and writes the events in ascending s.
+__global__ void __launch_bounds__(256) k_stream_seal(SealParams p) {
+  __shared__ int32_t cnt[256], offs[256];
+  __shared__ int32_t wsum[8];
+  __shared__ long long base;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t c0 = static_cast<int64_t>(blockIdx.x) * 256;
+  const int wpl = p.tb >> 7;
+  const int64_t boff = static_cast<int64_t>(p.block) * p.tb;
+  for (int i = 0; i < 32; ++i) {
+    const int64_t c = c0 + warp * 32 + i;
+    uint32_t n = 0;
+    if (c < p.ktot) {
+      const uint32_t* row = reinterpret_cast<const uint32_t*>(p.hist + c * p.hp + boff) + lane * wpl;
+      for (int w = 0; w < wpl; ++w) n += nzbytes(row[w]);
+    }
+    n = __reduce_add_sync(0xffffffffu, n);
+    if (lane == 0) cnt[warp * 32 + i] = static_cast<int32_t>(n);
+  }
+  __syncthreads();
+  // exclusive scan of the 256 counts (thread = column)
+  const int mine = cnt[threadIdx.x];
+  int incl = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  int wb = 0;
+  for (int w = 0; w < warp; ++w) wb += wsum[w];
+  const int excl = wb + incl - mine;
+  offs[threadIdx.x] = excl;
+  if (threadIdx.x == 255) {
+    const long long tot = wb + incl;
+    base = tot ? static_cast<long long>(atomicAdd(p.cursor + p.slot, static_cast<unsigned long long>(tot)))
+               : 0ll;
+    if (base + tot > p.cap) {
+      atomicExch(p.dense + p.slot, 1);
+      base = -1;
+    }
+  }
+  __syncthreads();
+  if (base < 0) return;  // the block stays dense
+  if (c0 + threadIdx.x < p.ktot)  // offsets relative to the block's list
+    p.evidx[static_cast<int64_t>(p.slot) * p.ktot + c0 + threadIdx.x] =
+        make_int2(static_cast<int>(base + excl), mine);
+  uint32_t* evb = p.ev + static_cast<int64_t>(p.slot) * p.cap;
+  for (int i = 0; i < 32; ++i) {
+    const int cl = warp * 32 + i;
+    const int64_t c = c0 + cl;
+    if (c >= p.ktot || cnt[cl] == 0) continue;  // warp-uniform
+    const uint32_t* row = reinterpret_cast<const uint32_t*>(p.hist + c * p.hp + boff) + lane * wpl;
+    uint32_t wv[8];
+    uint32_t n = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      wv[w] = w < wpl ? row[w] : 0u;
+      n += nzbytes(wv[w]);
+    }
+    uint32_t pre = n;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, pre, o);
+      if (lane >= o) pre += v;
+    }
+    pre -= n;
+    int64_t pos = base + offs[cl] + pre;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      if (w >= wpl) break;
+      uint32_t x = wv[w];
+      while (x) {
+        const int b = (__ffs(x) - 1) >> 3;
+        const uint32_t v = (x >> (8 * b)) & 0xFFu;
+        evb[pos++] = (static_cast<uint32_t>((lane * wpl + w) * 4 + b) << 8) | v;
+        x &= ~(0xFFu << (8 * b));
+      }
+    }
+  }
+}
+
+// Merge: grid ceil(ktot / 256), thread = pixel column for the counts and
+// scan, then warp w copies the lists of its 32 columns one column at a time
+// (lanes over events, coalesced), adding b tb to the s_local of block b.
+__global__ void __launch_bounds__(256) k_stream_merge(MergeParams p) {
+  __shared__ int32_t offs[256];
+  __shared__ int32_t wsum[8];
+  __shared__ long long base;
+  __shared__ int dense;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    int d = 0;
+    for (int b = 0; b < p.nf; ++b) d |= p.dense0[b];
+    dense = d;
+    if (d && blockIdx.x == 0) p.dense1[p.seg] = 1;
+  }
+  __syncthreads();
+  if (dense) return;
+  const int64_t c = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x;
+  int mine = 0;
+  if (c < p.ktot)
+    for (int b = 0; b < p.nf; ++b) mine += p.evidx0[b * p.ktot + c].y;
+  int incl = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  int wb = 0;
+  for (int w = 0; w < warp; ++w) wb += wsum[w];
+  offs[threadIdx.x] = wb + incl - mine;
+  if (threadIdx.x == 255) {
+    const long long tot = wb + incl;
+    base = tot ? static_cast<long long>(atomicAdd(p.cursor1 + p.seg, static_cast<unsigned long long>(tot)))
+               : 0ll;
+    if (base + tot > p.cap1) {
+      atomicExch(p.dense1 + p.seg, 1);
+      base = -1;
+    }
+  }
+  __syncthreads();
+  if (base < 0) return;
+  if (c < p.ktot)
+    p.evidx1[static_cast<int64_t>(p.seg) * p.ktot + c] =
+        make_int2(static_cast<int>(base + offs[threadIdx.x]), mine);
+  uint32_t* dst0 = p.ev1 + static_cast<int64_t>(p.seg) * p.cap1 + base;
+  for (int i = 0; i < 32; ++i) {
+    const int cl = warp * 32 + i;
+    const int64_t cc = static_cast<int64_t>(blockIdx.x) * 256 + cl;
+    if (cc >= p.ktot) break;
+    uint32_t* dst = dst0 + offs[cl];
+    for (int b = 0; b < p.nf; ++b) {
+      const int2 e = p.evidx0[b * p.ktot + cc];
+      const uint32_t* src = p.ev0 + b * p.cap0 + e.x;
+      const uint32_t add = static_cast<uint32_t>(b * p.tb) << 8;
+      for (int k = lane; k < e.y; k += 32) dst[k] = __ldg(src + k) + add;
+      dst += e.y;
+    }
+  }
+}
+
+// K5e: grid (segments, rings, nb) for one level; CTA (g, r, j) forms the
+// column entries G(s, t + j) of segment g's frames for ring r from the new
+// frame's nonzero pixels: a thread per pixel walks the pixel's event list
+// and adds count x count into shared memory (integer atomics: exact, order-
+// free); a dense-flagged segment is read from the dense history instead.
+#ifndef XG_EV_COOP
+#define XG_EV_COOP 0
+#endif
+#ifndef XG_EV_U
+#define XG_EV_U 32
+#endif
+#ifndef XG_EV_MINB
+#define XG_EV_MINB 4
+#endif
+constexpr int EV_P = 8;         // cooperative: pixels per warp step
+constexpr int EV_U = XG_EV_U;   // events in flight per lane
+__global__ void __launch_bounds__(256, XG_EV_MINB) k_stream_events(StreamParams p, int lvl) {
+  extern __shared__ int32_t acc[];
+  const int g = blockIdx.x, r = blockIdx.y, j = blockIdx.z;
+  const int64_t t = p.t + j;
+  const int tb = p.ev_tb[lvl];
+  const int seg = p.ev_first[lvl] + g;
+  const int slot = p.ev_ring[lvl] ? seg % p.ev_ring[lvl] : seg;
+  for (int i = threadIdx.x; i < tb; i += 256) acc[i] = 0;
+  __syncthreads();
+  const int koff = p.ring_koff[r];
+  const int n = p.nz_n[j * p.n_rings + r];
+  const int32_t* nz_col = p.nz_col + j * p.nz_bstride + koff;
+  const uint8_t* nz_val = p.nz_val + j * p.nz_bstride + koff;
+  const int64_t s0 = static_cast<int64_t>(seg) * tb;
+  if (!p.ev_dense[lvl][slot]) {
+    const int2* idx = p.evidx[lvl] + static_cast<int64_t>(slot) * p.ktot;
+    const uint32_t* ev = p.ev[lvl] + static_cast<int64_t>(slot) * p.ev_cap[lvl];
+#if XG_EV_COOP
+    // warp-cooperative: a warp takes EV_P pixels at a time and its lanes walk
+    // the concatenation of their lists (consecutive lanes, consecutive events
+    // of a list: coalesced), EV_U events per lane in flight before the first
+    // atomic; the owner pixel of concatenated event g is found by a binary
+    // search over the pixels' exclusive offsets (shuffles)
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int c0 = warp * EV_P; c0 < n; c0 += 8 * EV_P) {
+      int xv = 0, len = 0, start = 0;
+      if (lane < EV_P && c0 + lane < n) {
+        const int col = nz_col[c0 + lane];
+        xv = nz_val[c0 + lane];
+        const int2 e = __ldg(idx + col);
+        start = e.x;
+        len = e.y;
+      }
+      int incl = len;
+#pragma unroll
+      for (int o = 1; o < EV_P; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      const int tot = __shfl_sync(0xffffffffu, incl, EV_P - 1);
+      const int excl = incl - len;
+      for (int g0 = 0; g0 < tot; g0 += 32 * EV_U) {
+        uint32_t w[EV_U];
+        int xs[EV_U];
+#pragma unroll
+        for (int u = 0; u < EV_U; ++u) {
+          const int gi = g0 + 32 * u + lane;
+          int lo = 0;
+#pragma unroll
+          for (int step = EV_P / 2; step > 0; step >>= 1) {
+            const int cand = lo + step;
+            if (__shfl_sync(0xffffffffu, excl, cand) <= gi) lo = cand;
+          }
+          const int st = __shfl_sync(0xffffffffu, start, lo);
+          const int ex = __shfl_sync(0xffffffffu, excl, lo);
+          xs[u] = __shfl_sync(0xffffffffu, xv, lo);
+          w[u] = gi < tot ? __ldg(ev + st + (gi - ex)) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < EV_U; ++u)
+          if (w[u]) atomicAdd(&acc[w[u] >> 8], static_cast<int>(w[u] & 0xFFu) * xs[u]);
+      }
+    }
+#else
+    // a thread per pixel: its list loaded EV_U events at a time, all loads
+    // issued before the first atomic
+    for (int i = threadIdx.x; i < n; i += 256) {
+      const int col = nz_col[i];
+      const int xv = nz_val[i];
+      const int2 e = __ldg(idx + col);
+      for (int k = 0; k < e.y; k += EV_U) {
+        uint32_t w[EV_U];
+#pragma unroll
+        for (int u = 0; u < EV_U; ++u) w[u] = k + u < e.y ? __ldg(ev + e.x + k + u) : 0u;
+#pragma unroll
+        for (int u = 0; u < EV_U; ++u)
+          if (w[u]) atomicAdd(&acc[w[u] >> 8], static_cast<int>(w[u] & 0xFFu) * xv);
+      }
+    }
+#endif
+  } else {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int wpl = tb >> 7;
+    for (int i = warp; i < n; i += 8) {
+      const int col = nz_col[i];
+      const int xv = nz_val[i];
+      const uint32_t* row = reinterpret_cast<const uint32_t*>(p.hist + static_cast<int64_t>(col) * p.hp + s0) + lane * wpl;
+      for (int w = 0; w < wpl; ++w) {
+        uint32_t x = row[w];
+        while (x) {
+          const int bb = (__ffs(x) - 1) >> 3;
+          atomicAdd(&acc[(lane * wpl + w) * 4 + bb], static_cast<int>((x >> (8 * bb)) & 0xFFu) * xv);
+          x &= ~(0xFFu << (8 * bb));
+        }
+      }
+    }
+  }
+  __syncthreads();
+  int32_t* dst = p.gscr + (static_cast<int64_t>(r) * p.scr_nb + j) * p.scr_ld + s0;
+  for (int i = threadIdx.x; i < tb; i += 256) {
+    dst[i] = acc[i];
+    if (p.gcol) p.gcol[static_cast<int64_t>(r) * p.col_ring_stride + (s0 + i) * p.col_ld + t] = acc[i];
+  }
+}
+
 // The lag sums of a batch: thread per lag d of ring r, frames in ascending
 // order -- exactly the per-push updates of K5s (RAW) / K6b, in push order.
 template <bool RAW>
@@ -690,9 +983,15 @@ static cudaError_t launch_maybe_pdl(K kernel, dim3 grid, dim3 block, cudaStream_
 cudaError_t launch_stream_ingest_sparse(const StreamParams& p, cudaStream_t s, bool pdl,
                                         int32_t n_frames) {
   if (p.n_rings > SI_MAXQ) return cudaErrorInvalidValue;
-  const unsigned blocks =
-      static_cast<unsigned>((p.pixels + SI_PX * SI_THREADS - 1) / (SI_PX * SI_THREADS));
-  return launch_maybe_pdl(k_stream_ingest_sparse, dim3(blocks, n_frames), dim3(SI_THREADS), s,
+  // 16 pixels per thread need 16-byte aligned frames (the batched path's)
+  const bool wide = n_frames > 1 && (p.pixels & 15) == 0 &&
+                    (reinterpret_cast<uintptr_t>(p.frame) & 15u) == 0;
+  const int px = wide ? 16 : 4;
+  const unsigned blocks = static_cast<unsigned>((p.pixels + px * SI_THREADS - 1) / (px * SI_THREADS));
+  if (wide)
+    return launch_maybe_pdl(k_stream_ingest_sparse<16>, dim3(blocks, n_frames), dim3(SI_THREADS), s,
+                            pdl, p);
+  return launch_maybe_pdl(k_stream_ingest_sparse<4>, dim3(blocks, n_frames), dim3(SI_THREADS), s,
                           pdl, p);
 }
 
@@ -718,10 +1017,33 @@ cudaError_t launch_stream_batch(const StreamParams& p, int32_t n_rings, bool raw
     k_stream_fold<false><<<fold_grid, 256, 0, s>>>(p);
   }
   if (raw) {
-    const dim3 grid(static_cast<unsigned>((rows + SS_F - 1) / SS_F), n_rings, nb);
+    for (int l = 0; l < 2; ++l) {
+      if (p.ev_n[l] <= 0) continue;
+      if (p.ev_tb[l] > EV_MAXTB || p.ev_tb[l] % 128) return cudaErrorInvalidValue;
+      const size_t smem = static_cast<size_t>(p.ev_tb[l]) * sizeof(int32_t);
+      if (smem > 48 * 1024) {
+        const cudaError_t e = cudaFuncSetAttribute(
+            k_stream_events, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+      }
+      k_stream_events<<<dim3(p.ev_n[l], n_rings, nb), 256, smem, s>>>(p, l);
+    }
+    const dim3 grid(static_cast<unsigned>((rows - p.s_begin + SS_F - 1) / SS_F), n_rings, nb);
     k_stream_sparse<true><<<grid, 32 * SS_W, 0, s>>>(p);
     k_stream_fold<true><<<fold_grid, 256, 0, s>>>(p);
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_stream_merge(const MergeParams& p, cudaStream_t s) {
+  if (int64_t{p.nf} * p.tb > EV_MAXTB || int64_t{p.nf} * p.tb >= (1 << 24)) return cudaErrorInvalidValue;
+  k_stream_merge<<<static_cast<unsigned>((p.ktot + 255) / 256), 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_stream_seal(const SealParams& p, cudaStream_t s) {
+  if (p.tb > 1024 || p.tb % 128) return cudaErrorInvalidValue;
+  k_stream_seal<<<static_cast<unsigned>((p.ktot + 255) / 256), 256, 0, s>>>(p);
   return cudaGetLastError();
 }
 

@@ -2409,7 +2409,20 @@ struct xg_stream {
   float* d_cscr = nullptr;
   int32_t* d_paccb = nullptr;
   bool scr_ready = false;
-  unsigned int* d_done = nullptr;  // sparse ingest's CTA counter
+  // photon-event history of a sparse raw stream (batched columns): blocks
+  // of ev_tb frames sealed from the dense history into kEvL1 level-0 slots
+  // (k_stream_seal), every kEvL1 consecutive blocks merged into one level-1
+  // segment (k_stream_merge); allocated at the first seal.  ev_tb = 0: dense
+  // history only (XG_STREAM_EVENT_FRAMES=0, or no memory for the pools).
+  int32_t ev_tb = 0;
+  int32_t ev_sealed = 0;   // blocks sealed
+  int32_t ev_merged = 0;   // level-1 segments
+  int64_t ev_cap0 = 0, ev_cap1 = 0;
+  uint32_t *d_ev0 = nullptr, *d_ev1 = nullptr;
+  int2 *d_evidx0 = nullptr, *d_evidx1 = nullptr;
+  unsigned long long *d_ev_cursor0 = nullptr, *d_ev_cursor1 = nullptr;
+  int32_t *d_ev_dense0 = nullptr, *d_ev_dense1 = nullptr;
+  unsigned int* d_done = nullptr;  // sparse ingest's CTA counters, one per batch frame
 };
 
 extern "C" {
@@ -2464,6 +2477,11 @@ int xg_stream_create(xg_ctx* c, const xg_layout* L, const xg_basis* B, int64_t m
       return cuda_fail(c, e, "stream sparse history alloc");
     }
     cudaMemsetAsync(s->d_hist, 0, (size_t)L->ktot * s->hp, c->stream);
+    if (!(flags & XG_STREAM_NO_RAW)) {
+      const char* ev = getenv("XG_STREAM_EVENT_FRAMES");
+      const int tb = ev ? atoi(ev) : 1024;
+      s->ev_tb = (tb >= 128 && tb <= 1024 && tb % 128 == 0) ? tb : 0;
+    }
     // packed (ring << 22 | column) of every pixel, -1 outside the rings
     std::vector<int32_t> pc(static_cast<size_t>(L->pixels), -1);
     if (L->ktot >= (1 << 22) || L->rings > 512) {
@@ -2473,8 +2491,8 @@ int xg_stream_create(xg_ctx* c, const xg_layout* L, const xg_basis* B, int64_t m
     for (int32_t r = 0; r < L->rings; ++r)
       for (int64_t col = L->koff[r]; col < L->koff[r] + L->kpad[r]; ++col)
         if (L->colpix[col] >= 0) pc[L->colpix[col]] = (r << 22) | static_cast<int32_t>(col);
-    if ((e = dalloc(&s->d_done, 1)) != cudaSuccess ||
-        (e = cudaMemset(s->d_done, 0, 4)) != cudaSuccess ||
+    if ((e = dalloc(&s->d_done, 16)) != cudaSuccess ||  // one per batch frame
+        (e = cudaMemset(s->d_done, 0, 16 * sizeof(unsigned int))) != cudaSuccess ||
         (e = dalloc(&s->d_pixcol, pc.size())) != cudaSuccess ||
         (e = cudaMemcpy(s->d_pixcol, pc.data(), pc.size() * 4, cudaMemcpyHostToDevice)) !=
             cudaSuccess) {
@@ -2594,6 +2612,14 @@ void xg_stream_destroy(xg_stream* s) {
   dfree(s->d_gscr);
   dfree(s->d_cscr);
   dfree(s->d_paccb);
+  dfree(s->d_ev0);
+  dfree(s->d_evidx0);
+  dfree(s->d_ev_cursor0);
+  dfree(s->d_ev_dense0);
+  dfree(s->d_ev1);
+  dfree(s->d_evidx1);
+  dfree(s->d_ev_cursor1);
+  dfree(s->d_ev_dense1);
   delete s;
 }
 
@@ -2758,6 +2784,99 @@ int xg_stream_push(xg_stream* s, const uint8_t* frame, int on_device) {
 // and the lag sums folded in frame order -- bitwise the same as n pushes.
 // XG_STREAM_BATCH_COLUMNS=0 runs each frame's columns as in a push instead.
 constexpr int kIngestBatch = 16;
+constexpr int kEvL1 = 8;  // level-0 blocks per level-1 event segment
+
+static void free_event_pools(xg_stream* s) {
+  dfree(s->d_ev0);
+  dfree(s->d_evidx0);
+  dfree(s->d_ev_cursor0);
+  dfree(s->d_ev_dense0);
+  dfree(s->d_ev1);
+  dfree(s->d_evidx1);
+  dfree(s->d_ev_cursor1);
+  dfree(s->d_ev_dense1);
+  s->d_ev0 = s->d_ev1 = nullptr;
+  s->d_evidx0 = s->d_evidx1 = nullptr;
+  s->d_ev_cursor0 = s->d_ev_cursor1 = nullptr;
+  s->d_ev_dense0 = s->d_ev_dense1 = nullptr;
+}
+
+// Seal the blocks of ev_tb frames that precede the next push (s->t) into the
+// level-0 slots, merging every kEvL1 of them into a level-1 segment.  Event
+// pools are sized for 1/8 occupancy (ev_cap0 = ktot tb / 8 events per
+// block); a block with more events stays dense (k_stream_seal's flag).
+static int seal_event_blocks(xg_stream* s) {
+  xg_ctx* c = s->ctx;
+  const xg_layout* L = s->L;
+  const int tb = s->ev_tb;
+  const int64_t nseg_max = s->tmax / (int64_t{tb} * kEvL1);
+  auto sealable = [&] {
+    return int64_t{s->ev_sealed + 1} * tb <= s->t && s->ev_sealed - s->ev_merged * kEvL1 < kEvL1;
+  };
+  if (!sealable()) return XG_OK;
+  if (!s->d_ev0) {
+    s->ev_cap0 = L->ktot * tb / 8;
+    s->ev_cap1 = s->ev_cap0 * kEvL1;
+    const int64_t n1 = std::max<int64_t>(nseg_max, 1);
+    cudaError_t e = dalloc(&s->d_ev0, (size_t)(s->ev_cap0 * kEvL1));
+    if (e == cudaSuccess) e = dalloc(&s->d_evidx0, (size_t)(L->ktot * kEvL1));
+    if (e == cudaSuccess) e = dalloc(&s->d_ev_cursor0, (size_t)kEvL1);
+    if (e == cudaSuccess) e = dalloc(&s->d_ev_dense0, (size_t)kEvL1);
+    if (e == cudaSuccess && nseg_max) e = dalloc(&s->d_ev1, (size_t)(s->ev_cap1 * n1));
+    if (e == cudaSuccess) e = dalloc(&s->d_evidx1, (size_t)(L->ktot * n1));
+    if (e == cudaSuccess) e = dalloc(&s->d_ev_cursor1, (size_t)n1);
+    if (e == cudaSuccess) e = dalloc(&s->d_ev_dense1, (size_t)n1);
+    if (e != cudaSuccess) {  // no room: keep the dense history
+      cudaGetLastError();
+      free_event_pools(s);
+      s->ev_tb = 0;
+      return XG_OK;
+    }
+    XG_CUDA(c, cudaMemsetAsync(s->d_ev_cursor1, 0, n1 * sizeof(unsigned long long), c->stream));
+    XG_CUDA(c, cudaMemsetAsync(s->d_ev_dense1, 0, n1 * sizeof(int32_t), c->stream));
+  }
+  while (sealable()) {
+    const int slot = s->ev_sealed % kEvL1;
+    XG_CUDA(c, cudaMemsetAsync(s->d_ev_cursor0 + slot, 0, sizeof(unsigned long long), c->stream));
+    XG_CUDA(c, cudaMemsetAsync(s->d_ev_dense0 + slot, 0, sizeof(int32_t), c->stream));
+    SealParams sl;
+    sl.hist = s->d_hist;
+    sl.hp = s->hp;
+    sl.ktot = L->ktot;
+    sl.block = s->ev_sealed;
+    sl.slot = slot;
+    sl.tb = tb;
+    sl.cap = s->ev_cap0;
+    sl.ev = s->d_ev0;
+    sl.evidx = s->d_evidx0;
+    sl.cursor = s->d_ev_cursor0;
+    sl.dense = s->d_ev_dense0;
+    XG_CUDA(c, launch_stream_seal(sl, c->stream));
+    c->launches++;
+    s->ev_sealed++;
+    if (s->ev_sealed % kEvL1 == 0 && s->ev_merged < nseg_max) {
+      MergeParams mp;
+      mp.ev0 = s->d_ev0;
+      mp.evidx0 = s->d_evidx0;
+      mp.dense0 = s->d_ev_dense0;
+      mp.cap0 = s->ev_cap0;
+      mp.tb = tb;
+      mp.nf = kEvL1;
+      mp.ktot = L->ktot;
+      mp.seg = s->ev_merged;
+      mp.cap1 = s->ev_cap1;
+      mp.ev1 = s->d_ev1;
+      mp.evidx1 = s->d_evidx1;
+      mp.cursor1 = s->d_ev_cursor1;
+      mp.dense1 = s->d_ev_dense1;
+      XG_CUDA(c, launch_stream_merge(mp, c->stream));
+      c->launches++;
+      s->ev_merged++;
+    }
+  }
+  return XG_OK;
+}
+
 static bool batch_columns_enabled() {
   static const bool on = [] {
     const char* e = getenv("XG_STREAM_BATCH_COLUMNS");
@@ -2832,7 +2951,34 @@ int xg_stream_push_batch(xg_stream* s, const uint8_t* frames, int64_t n, int on_
         }
         s->scr_ready = true;
       }
+      // seal every event block whose frames all precede this batch (while a
+      // level-0 slot is free), merging each run of kEvL1 blocks into a
+      // level-1 segment
+      if (raw && s->ev_tb) {
+        const int rc = seal_event_blocks(s);
+        if (rc) return rc;
+      }
       StreamParams bp = column_params(s);
+      if (raw && s->ev_tb && s->ev_sealed) {
+        const int l0 = s->ev_sealed - s->ev_merged * kEvL1;  // level-0 blocks not merged
+        bp.ev[0] = s->d_ev1;
+        bp.evidx[0] = s->d_evidx1;
+        bp.ev_dense[0] = s->d_ev_dense1;
+        bp.ev_cap[0] = s->ev_cap1;
+        bp.ev_tb[0] = s->ev_tb * kEvL1;
+        bp.ev_n[0] = s->ev_merged;
+        bp.ev_first[0] = 0;
+        bp.ev_ring[0] = 0;
+        bp.ev[1] = s->d_ev0;
+        bp.evidx[1] = s->d_evidx0;
+        bp.ev_dense[1] = s->d_ev_dense0;
+        bp.ev_cap[1] = s->ev_cap0;
+        bp.ev_tb[1] = s->ev_tb;
+        bp.ev_n[1] = l0;
+        bp.ev_first[1] = s->ev_merged * kEvL1;
+        bp.ev_ring[1] = kEvL1;
+        bp.s_begin = int64_t{s->ev_sealed} * s->ev_tb;
+      }
       bp.nz_col = s->d_nzb_col;
       bp.nz_val = s->d_nzb_val;
       bp.nz_n = s->d_nzb_n;
@@ -2844,7 +2990,7 @@ int xg_stream_push_batch(xg_stream* s, const uint8_t* frames, int64_t n, int on_
       bp.scr_ld = s->tp;
       bp.scr_nb = nb;
       XG_CUDA(c, launch_stream_batch(bp, L->rings, raw, s->B != nullptr, c->stream));
-      c->launches += (raw ? 2 : 0) + (s->B ? 4 : 0);
+      c->launches += (raw ? 2 + (bp.ev_n[0] > 0) + (bp.ev_n[1] > 0) : 0) + (s->B ? 4 : 0);
       s->t += nb;
       continue;
     }

@@ -304,7 +304,61 @@ struct StreamParams {
   int64_t scr_ld;
   int32_t scr_nb;            // frames of the batch
   int64_t pacc_bstride;      // proj_acc/proj_fin: frame f's digit sums at pacc + f * pacc_bstride
+  // photon-event history (batched raw columns): frames [0, s_begin) are
+  // sealed event segments -- per segment and pixel column an (offset, count)
+  // entry into the segment's event list (s_local << 8 | count, ascending s),
+  // or the segment's dense flag when its events did not fit -- and K5s
+  // covers only [s_begin, t].  One launch_stream_batch call covers up to two
+  // segment levels: ev_n[l] segments of ev_tb[l] frames, the first being
+  // segment ev_first[l] of its level, stored in slot (index % ev_ring[l]).
+  int64_t s_begin;
+  const uint32_t* ev[2];
+  const int2* evidx[2];
+  const int32_t* ev_dense[2];
+  int64_t ev_cap[2];         // events per segment
+  int32_t ev_tb[2];          // frames per segment (multiple of 128)
+  int32_t ev_n[2];
+  int32_t ev_first[2];
+  int32_t ev_ring[2];        // 0: slot = index
 };
+
+// Seal block `block` of a photon-event history (frames [block tb, + tb)):
+// pixel-major events from the dense history into slot `slot` (its list at
+// ev + slot cap, entries at evidx + slot ktot, cursor/dense[slot] zero on
+// entry); a block whose events do not fit is flagged dense.
+struct SealParams {
+  const uint8_t* hist;
+  int64_t hp;
+  int64_t ktot;
+  int32_t block;
+  int32_t slot;
+  int32_t tb;
+  int64_t cap;
+  uint32_t* ev;
+  int2* evidx;
+  unsigned long long* cursor;
+  int32_t* dense;
+};
+cudaError_t launch_stream_seal(const SealParams& p, cudaStream_t s);
+// Merge the nf sealed blocks in slots 0 .. nf - 1 (consecutive, ascending)
+// into segment `seg` of nf * tb frames: each pixel's lists concatenated with
+// the block offset added to s_local; any dense block makes the segment dense.
+struct MergeParams {
+  const uint32_t* ev0;
+  const int2* evidx0;
+  const int32_t* dense0;
+  int64_t cap0;
+  int32_t tb;
+  int32_t nf;
+  int64_t ktot;
+  int32_t seg;
+  int64_t cap1;
+  uint32_t* ev1;
+  int2* evidx1;
+  unsigned long long* cursor1;  // [seg], zero on entry
+  int32_t* dense1;              // [seg], zero on entry
+};
+cudaError_t launch_stream_merge(const MergeParams& p, cudaStream_t s);
 // One-frame ingest for the streaming path: ring-major row t of the history,
 // |x_t|^2 per ring, and in sparse mode the frame's nonzeros per ring plus
 // their scatter into the pixel-major history.

@@ -141,3 +141,41 @@ def test_push_many_equals_single_pushes(ctx, orc, basis_k, raw):
             _, va, ca = a.g2(r, compressed=True)
             _, vb, cb = b.g2(r, compressed=True)
             assert np.array_equal(va, vb) and np.array_equal(ca, cb)
+
+
+@pytest.mark.parametrize("mus", [(0.08,), (0.5,), (0.6, 0.03)])
+def test_event_history_equals_dense(ctx, orc, monkeypatch, mus):
+    """Sealed photon-event blocks (XG_STREAM_EVENT_FRAMES frames each, the
+    per-pixel event lists the batched raw columns read instead of the dense
+    history; every 8 blocks merged into one level-1 segment) give the dense
+    columns' results bitwise: Gram == oracle gram, g2 == single pushes.
+    T = 1300 at 128-frame blocks: one merged segment (frames 0-1023) plus
+    level-0 blocks 8-9 plus the dense tail.  mu = 0.5 overflows the
+    1/8-occupancy event pool, so its blocks (and the segment) stay dense
+    (the fallback read of the dense history); the mixed run has bright dense
+    blocks first, then sparse ones."""
+    import torch
+
+    monkeypatch.setenv("XG_STREAM_EVENT_FRAMES", "128")
+    t, h, w, q = 1300, 96, 96, 4
+    parts = np.array_split(np.arange(t), len(mus))
+    frames = np.concatenate([orc.gen_speckle(len(ix), h, w, q, mu, 31 + i)
+                             for i, (ix, mu) in enumerate(zip(parts, mus))])
+    frames[200] = 0
+    ring, _ = orc.ring_map(h, w, q)
+    lay = xg.RingLayout.from_ring_map(ctx, ring, q)
+    dev = torch.from_numpy(frames).cuda()
+    a = xg.FrameStream(lay, t, store_ttc=True, sparse=True)
+    b = xg.FrameStream(lay, t, store_ttc=True, sparse=True)
+    for i in range(t):
+        a.push(dev[i])
+    b.push_many(dev[:333])  # seals block 0 at the batch starting at frame 128, block 1 at 256
+    b.push(dev[333])
+    b.push_many(dev[334:])
+    for r in range(q):
+        ga, gb = a.ttc(r, dtype="gram"), b.ttc(r, dtype="gram")
+        assert np.array_equal(ga, gb), r
+        assert np.array_equal(gb.astype(np.int64), orc.gram_u8(frames[:, ring == r])), r
+        _, va, ca = a.g2(r)
+        _, vb, cb = b.g2(r)
+        assert np.array_equal(va, vb) and np.array_equal(ca, cb), r
