@@ -2989,7 +2989,24 @@ int xg_stream_push_batch(xg_stream* s, const uint8_t* frames, int64_t n, int on_
       bp.cscr = s->d_cscr;
       bp.scr_ld = s->tp;
       bp.scr_nb = nb;
-      XG_CUDA(c, launch_stream_batch(bp, L->rings, raw, s->B != nullptr, c->stream));
+      if (raw && s->B) {
+        // the compressed columns (issue-bound) on the side stream beside the
+        // raw columns (latency-bound event walks): both read only this
+        // batch's ingest and write disjoint sums
+        if (!s->side) {
+          XG_CUDA(c, cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking));
+          XG_CUDA(c, cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming));
+          XG_CUDA(c, cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming));
+        }
+        XG_CUDA(c, cudaEventRecord(s->ev_fork, c->stream));
+        XG_CUDA(c, cudaStreamWaitEvent(s->side, s->ev_fork, 0));
+        XG_CUDA(c, launch_stream_batch(bp, L->rings, false, true, s->side));
+        XG_CUDA(c, launch_stream_batch(bp, L->rings, true, false, c->stream));
+        XG_CUDA(c, cudaEventRecord(s->ev_join, s->side));
+        XG_CUDA(c, cudaStreamWaitEvent(c->stream, s->ev_join, 0));
+      } else {
+        XG_CUDA(c, launch_stream_batch(bp, L->rings, raw, s->B != nullptr, c->stream));
+      }
       c->launches += (raw ? 2 + (bp.ev_n[0] > 0) + (bp.ev_n[1] > 0) : 0) + (s->B ? 4 : 0);
       s->t += nb;
       continue;
