@@ -104,6 +104,9 @@ __device__ __forceinline__ void pdl_launch_dependents() {
 }
 
 constexpr int PZ = 8;
+#ifndef XG_PZ_BATCH
+#define XG_PZ_BATCH 2
+#endif
 constexpr int PA_MAXW = 6;  // 32-bit digit words per lane: 3 digits x k <= 768
 constexpr int PA_U = 4;     // pixels in flight per warp
 __global__ void __launch_bounds__(256) k_stream_proj_acc(StreamParams p) {
@@ -121,8 +124,8 @@ __global__ void __launch_bounds__(256) k_stream_proj_acc(StreamParams p) {
   const int n = p.nz_n[f * p.n_rings + r];
   const int32_t* nz_col = p.nz_col + f * p.nz_bstride;
   const uint8_t* nz_val = p.nz_val + f * p.nz_bstride;
-  const int zb = static_cast<int>((static_cast<int64_t>(n) * blockIdx.y) / PZ);
-  const int ze = static_cast<int>((static_cast<int64_t>(n) * (blockIdx.y + 1)) / PZ);
+  const int zb = static_cast<int>((static_cast<int64_t>(n) * blockIdx.y) / gridDim.y);
+  const int ze = static_cast<int>((static_cast<int64_t>(n) * (blockIdx.y + 1)) / gridDim.y);
   const int nw = p.vdt_ld >> 2;
   int32_t acc[PA_MAXW][4];
 #pragma unroll
@@ -567,7 +570,7 @@ __global__ void __launch_bounds__(32 * SS_W, SS_MINB) k_stream_sparse(StreamPara
 // the butterfly's, so C~ equals K6b's bitwise).  History bytes are read once
 // per batch instead of once per frame.
 constexpr int CB_MAXNB = 16;
-template <int MAXV>
+template <int MAXV, int RPW>
 __global__ void __launch_bounds__(SR_THREADS, 2) k_stream_cmp_batch(StreamParams p) {
   __shared__ float4 ynew[CB_MAXNB][32 * MAXV];
   const int r = blockIdx.y;
@@ -579,10 +582,10 @@ __global__ void __launch_bounds__(SR_THREADS, 2) k_stream_cmp_batch(StreamParams
     ynew[jj][v] = v < nv ? *reinterpret_cast<const float4*>(ybase + (p.t + jj) * kq + 4 * v)
                          : make_float4(0.f, 0.f, 0.f, 0.f);
   }
-  constexpr int RPW = SR_ROWS / (SR_THREADS / 32);
-  static_assert(RPW == 8, "recursive halving below is written for 8 rows per warp");
+  static_assert(RPW == 8 || RPW == 16, "recursive halving below covers 8 or 16 rows per warp");
   const int64_t t_last = p.t + nb - 1;
-  const int64_t s_first = static_cast<int64_t>(blockIdx.x) * SR_ROWS + warp * RPW;
+  const int64_t s_first =
+      static_cast<int64_t>(blockIdx.x) * (RPW * (SR_THREADS / 32)) + warp * RPW;
   float4 ld[RPW][MAXV];
 #pragma unroll
   for (int m = 0; m < MAXV; ++m) {
@@ -590,54 +593,50 @@ __global__ void __launch_bounds__(SR_THREADS, 2) k_stream_cmp_batch(StreamParams
 #pragma unroll
     for (int q = 0; q < RPW; ++q) {
       const int64_t s = s_first + q;
-      ld[q][m] = (32 * m < nv && v < nv && s <= t_last)
+      ld[q][m] = (v < nv && s <= t_last)
                      ? __ldcs(reinterpret_cast<const float4*>(ybase + s * kq + 4 * v))
                      : make_float4(0.f, 0.f, 0.f, 0.f);
     }
   }
   __syncthreads();
-  const int b4 = (lane >> 4) & 1, b3 = (lane >> 3) & 1, b2 = (lane >> 2) & 1;
-  const int qme = (lane >> 2) & 7;  // the row this lane's sum belongs to
+  // after the halvings lane L holds the sum of row qme; lanes with the low
+  // bits clear store it
+  constexpr int LOWB = RPW == 16 ? 1 : 2;  // lane bits left to butterflies
+  const int qme = (lane >> LOWB) & (RPW - 1);
   const int64_t s_me = s_first + qme;
+  float* cdst = p.cscr + static_cast<int64_t>(r) * nb * p.scr_ld + s_me;
   for (int j = 0; j < nb; ++j) {
     const int64_t t = p.t + j;
     if (s_first > t) continue;  // warp-uniform
-    float part[RPW];
+    float v[RPW];
 #pragma unroll
-    for (int q = 0; q < RPW; ++q) part[q] = 0.f;
+    for (int q = 0; q < RPW; ++q) v[q] = 0.f;
 #pragma unroll
     for (int m = 0; m < MAXV; ++m) {
       if (32 * m >= nv) break;
       const float4 yn = ynew[j][lane + 32 * m];
 #pragma unroll
       for (int q = 0; q < RPW; ++q)
-        part[q] = fmaf(ld[q][m].x, yn.x,
-                       fmaf(ld[q][m].y, yn.y, fmaf(ld[q][m].z, yn.z, fmaf(ld[q][m].w, yn.w, part[q]))));
+        v[q] = fmaf(ld[q][m].x, yn.x,
+                    fmaf(ld[q][m].y, yn.y, fmaf(ld[q][m].z, yn.z, fmaf(ld[q][m].w, yn.w, v[q]))));
     }
-    // recursive halving over lane bits 4, 3, 2, then butterflies over 1, 0
-    float w4[4], w3[2];
+    // K6b's xor-butterfly tree by recursive halving: at lane bit o a lane
+    // keeps half its rows and adds the partner's partial of each
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const float send = b4 ? part[i] : part[i + 4];
-      const float keep = b4 ? part[i + 4] : part[i];
-      w4[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-    }
+    for (int o = 16, R = RPW; R > 1; o >>= 1, R >>= 1) {
+      const bool hi = (lane & o) != 0;
 #pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      const float send = b3 ? w4[i] : w4[i + 2];
-      const float keep = b3 ? w4[i + 2] : w4[i];
-      w3[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+      for (int i = 0; i < R / 2; ++i) {
+        const float send = hi ? v[i] : v[i + R / 2];
+        const float keep = hi ? v[i + R / 2] : v[i];
+        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+      }
     }
-    float a;
-    {
-      const float send = b2 ? w3[0] : w3[1];
-      const float keep = b2 ? w3[1] : w3[0];
-      a = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-    }
-    a += __shfl_xor_sync(0xffffffffu, a, 2);
-    a += __shfl_xor_sync(0xffffffffu, a, 1);
-    if ((lane & 3) == 0 && s_me <= t) {
-      p.cscr[(static_cast<int64_t>(r) * nb + j) * p.scr_ld + s_me] = a;
+    float a = v[0];
+#pragma unroll
+    for (int o = 1 << (LOWB - 1); o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if ((lane & ((1 << LOWB) - 1)) == 0 && s_me <= t) {
+      cdst[static_cast<int64_t>(j) * p.scr_ld] = a;
       if (p.ccol) p.ccol[static_cast<int64_t>(r) * p.col_ring_stride + s_me * p.col_ld + t] = a;
     }
   }
@@ -1007,13 +1006,19 @@ cudaError_t launch_stream_batch(const StreamParams& p, int32_t n_rings, bool raw
   const int64_t rows = p.t + nb;
   const dim3 fold_grid(static_cast<unsigned>((rows + 255) / 256), n_rings);
   if (cmp) {
-    k_stream_proj_acc<<<dim3(n_rings, PZ, nb), 256, 0, s>>>(p);
+    // a batch has nb x rings CTAs without slicing a ring's nonzeros (PZ
+    // slices per frame multiplied the integer atomics on pacc: 78 us / 16)
+    k_stream_proj_acc<<<dim3(n_rings, XG_PZ_BATCH, nb), 256, 0, s>>>(p);
     k_stream_proj_fin<<<dim3(n_rings, nb), 128, 0, s>>>(p);
-    const dim3 grid(static_cast<unsigned>((rows + SR_ROWS - 1) / SR_ROWS), n_rings);
-    if (p.kq / 4 <= 32)
-      k_stream_cmp_batch<1><<<grid, SR_THREADS, 0, s>>>(p);
-    else
-      k_stream_cmp_batch<2><<<grid, SR_THREADS, 0, s>>>(p);
+    // 16 history rows per warp for k <= 128 (the reduction amortised over
+    // twice the rows), 8 for the two-chunk k <= 256 (registers)
+    if (p.kq / 4 <= 32) {
+      const dim3 grid(static_cast<unsigned>((rows + 16 * 8 - 1) / (16 * 8)), n_rings);
+      k_stream_cmp_batch<1, 16><<<grid, SR_THREADS, 0, s>>>(p);
+    } else {
+      const dim3 grid(static_cast<unsigned>((rows + 8 * 8 - 1) / (8 * 8)), n_rings);
+      k_stream_cmp_batch<2, 8><<<grid, SR_THREADS, 0, s>>>(p);
+    }
     k_stream_fold<false><<<fold_grid, 256, 0, s>>>(p);
   }
   if (raw) {
