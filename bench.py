@@ -673,6 +673,22 @@ def run_c3(E):
     raw_bytes_tail = nnz * t_tail
     cmp_bytes_tail = t_tail * Q * k * 4
     del st
+    # the same run with frames handed over strictly one at a time (push():
+    # each frame's columns formed before the next frame is looked at; the
+    # dense pixel-major raw column and K6b's per-frame compressed column)
+    st = xg.FrameStream(lay, T, basis=basis, sparse=True)
+    marks = {0: E.ev(), T - 1000: E.ev(), T: E.ev()}
+    E.sync()
+    marks[0].record(E.stream)
+    for i in range(T):
+        if i == T - 1000:
+            marks[i].record(E.stream)
+        st.push(frames[i])
+    marks[T].record(E.stream)
+    E.sync()
+    one_avg_ms = marks[0].elapsed_time(marks[T]) / T
+    one_tail_ms = marks[T - 1000].elapsed_time(marks[T]) / 1000
+    del st
     # raw-only photon-event pushes at depth 8192 (ingest -> K5s chained by
     # programmatic dependent launch): the push's HBM roofline on nnz * t bytes
     D8, n8 = 8192, 256
@@ -723,6 +739,15 @@ def run_c3(E):
         "frames_per_s_avg": 1e3 / avg_ms, "ms_per_frame_avg": avg_ms,
         "frames_per_s_tail": 1e3 / tail_ms, "ms_per_frame_tail": tail_ms,
         "tail": "last 1000 frames (history depth 19000-20000)",
+        "mode": "push_many: frames handed over in runs; the library forms 16 frames' columns "
+                "together (history read once per 16 columns; results bitwise those of single "
+                "pushes)",
+        "one_at_a_time": {"frames_per_s_avg": 1e3 / one_avg_ms, "ms_per_frame_avg": one_avg_ms,
+                          "frames_per_s_tail": 1e3 / one_tail_ms,
+                          "ms_per_frame_tail": one_tail_ms,
+                          "what": "push() per frame from Python (host call per frame inside the "
+                                  "timed region): ingest, dense pixel-major raw column (K5s), "
+                                  "K6a/K6b compressed column"},
         "nnz_per_frame": nnz, "basis": bsrc,
         "tail_bytes_per_frame": {"raw_nnz_history": raw_bytes_tail,
                                  "compressed_history": cmp_bytes_tail,

@@ -809,17 +809,13 @@ __global__ void __launch_bounds__(256) k_stream_merge(MergeParams p) {
 // frame's nonzero pixels: a thread per pixel walks the pixel's event list
 // and adds count x count into shared memory (integer atomics: exact, order-
 // free); a dense-flagged segment is read from the dense history instead.
-#ifndef XG_EV_COOP
-#define XG_EV_COOP 0
-#endif
-#ifndef XG_EV_U
-#define XG_EV_U 32
+#ifndef XG_EV_U4
+#define XG_EV_U4 8
 #endif
 #ifndef XG_EV_MINB
 #define XG_EV_MINB 4
 #endif
-constexpr int EV_P = 8;         // cooperative: pixels per warp step
-constexpr int EV_U = XG_EV_U;   // events in flight per lane
+constexpr int EV_U4 = XG_EV_U4;  // 16-byte event words in flight per thread
 __global__ void __launch_bounds__(256, XG_EV_MINB) k_stream_events(StreamParams p, int lvl) {
   extern __shared__ int32_t acc[];
   const int g = blockIdx.x, r = blockIdx.y, j = blockIdx.z;
@@ -837,69 +833,32 @@ __global__ void __launch_bounds__(256, XG_EV_MINB) k_stream_events(StreamParams 
   if (!p.ev_dense[lvl][slot]) {
     const int2* idx = p.evidx[lvl] + static_cast<int64_t>(slot) * p.ktot;
     const uint32_t* ev = p.ev[lvl] + static_cast<int64_t>(slot) * p.ev_cap[lvl];
-#if XG_EV_COOP
-    // warp-cooperative: a warp takes EV_P pixels at a time and its lanes walk
-    // the concatenation of their lists (consecutive lanes, consecutive events
-    // of a list: coalesced), EV_U events per lane in flight before the first
-    // atomic; the owner pixel of concatenated event g is found by a binary
-    // search over the pixels' exclusive offsets (shuffles)
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int c0 = warp * EV_P; c0 < n; c0 += 8 * EV_P) {
-      int xv = 0, len = 0, start = 0;
-      if (lane < EV_P && c0 + lane < n) {
-        const int col = nz_col[c0 + lane];
-        xv = nz_val[c0 + lane];
-        const int2 e = __ldg(idx + col);
-        start = e.x;
-        len = e.y;
-      }
-      int incl = len;
-#pragma unroll
-      for (int o = 1; o < EV_P; o <<= 1) {
-        const int v = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += v;
-      }
-      const int tot = __shfl_sync(0xffffffffu, incl, EV_P - 1);
-      const int excl = incl - len;
-      for (int g0 = 0; g0 < tot; g0 += 32 * EV_U) {
-        uint32_t w[EV_U];
-        int xs[EV_U];
-#pragma unroll
-        for (int u = 0; u < EV_U; ++u) {
-          const int gi = g0 + 32 * u + lane;
-          int lo = 0;
-#pragma unroll
-          for (int step = EV_P / 2; step > 0; step >>= 1) {
-            const int cand = lo + step;
-            if (__shfl_sync(0xffffffffu, excl, cand) <= gi) lo = cand;
-          }
-          const int st = __shfl_sync(0xffffffffu, start, lo);
-          const int ex = __shfl_sync(0xffffffffu, excl, lo);
-          xs[u] = __shfl_sync(0xffffffffu, xv, lo);
-          w[u] = gi < tot ? __ldg(ev + st + (gi - ex)) : 0u;
-        }
-#pragma unroll
-        for (int u = 0; u < EV_U; ++u)
-          if (w[u]) atomicAdd(&acc[w[u] >> 8], static_cast<int>(w[u] & 0xFFu) * xs[u]);
-      }
-    }
-#else
-    // a thread per pixel: its list loaded EV_U events at a time, all loads
-    // issued before the first atomic
+    // a thread per pixel: its list read as aligned 16-byte words (4 events;
+    // a scalar load per event made the L1 the limit: 89% busy), EV_U4 of
+    // them in flight before the first atomic
+    const uint4* ev4 = reinterpret_cast<const uint4*>(ev);
     for (int i = threadIdx.x; i < n; i += 256) {
       const int col = nz_col[i];
       const int xv = nz_val[i];
       const int2 e = __ldg(idx + col);
-      for (int k = 0; k < e.y; k += EV_U) {
-        uint32_t w[EV_U];
+      const int end = e.x + e.y;
+      for (int k = e.x & ~3; k < end; k += 4 * EV_U4) {
+        uint4 w[EV_U4];
 #pragma unroll
-        for (int u = 0; u < EV_U; ++u) w[u] = k + u < e.y ? __ldg(ev + e.x + k + u) : 0u;
+        for (int u = 0; u < EV_U4; ++u)
+          w[u] = k + 4 * u < end ? __ldg(ev4 + ((k >> 2) + u)) : make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
-        for (int u = 0; u < EV_U; ++u)
-          if (w[u]) atomicAdd(&acc[w[u] >> 8], static_cast<int>(w[u] & 0xFFu) * xv);
+        for (int u = 0; u < EV_U4; ++u) {
+          const uint32_t ww[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const int at = k + 4 * u + c;
+            if (at >= e.x && at < end)
+              atomicAdd(&acc[ww[c] >> 8], static_cast<int>(ww[c] & 0xFFu) * xv);
+          }
+        }
       }
     }
-#endif
   } else {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int wpl = tb >> 7;

@@ -96,8 +96,10 @@ def test_sparse_stream_equals_dense(ctx, orc, mu):
         assert np.array_equal(g2s, g2d) and np.array_equal(cs, cd)
 
 
-@pytest.mark.parametrize("basis_k,raw", [(0, True), (6, True), (6, False), (37, True), (130, True)])
-def test_push_many_equals_single_pushes(ctx, orc, basis_k, raw):
+@pytest.mark.parametrize("basis_k,raw,evf", [(0, True, None), (6, True, None), (6, False, None),
+                                              (37, True, None), (130, True, None), (0, True, "128"),
+                                              (6, True, "128")])
+def test_push_many_equals_single_pushes(ctx, orc, monkeypatch, basis_k, raw, evf):
     """push_many (one library call for n frames) == n push() calls, bitwise:
     photon-event push_many ingests 16 frames per launch (batch slots for the
     nonzero lists, a zero frame inside a batch, a partial last batch) and
@@ -106,8 +108,12 @@ def test_push_many_equals_single_pushes(ctx, orc, basis_k, raw):
     order); single pushes chain push t + 1's ingest beside push t's column
     kernel.  Neither may change a bit of the Gram, the C~ columns, the
     coefficients or the lag sums, raw or compressed-only; k = 130 takes the
-    two-chunk (k > 128) compressed kernels."""
+    two-chunk (k > 128) compressed kernels.  evf = 128: the batches walk
+    sealed 128-frame event blocks (single pushes keep the dense history)."""
     import torch
+
+    if evf:
+        monkeypatch.setenv("XG_STREAM_EVENT_FRAMES", evf)
 
     t, h, w, q = 300, 96, 96, 4
     frames = orc.gen_speckle(t, h, w, q, 0.08, 93)
@@ -165,7 +171,7 @@ def test_event_history_equals_dense(ctx, orc, monkeypatch, mus):
     ring, _ = orc.ring_map(h, w, q)
     lay = xg.RingLayout.from_ring_map(ctx, ring, q)
     dev = torch.from_numpy(frames).cuda()
-    a = xg.FrameStream(lay, t, store_ttc=True, sparse=True)
+    a = xg.FrameStream(lay, t, store_ttc=True, sparse=True)  # single pushes: dense history
     b = xg.FrameStream(lay, t, store_ttc=True, sparse=True)
     for i in range(t):
         a.push(dev[i])

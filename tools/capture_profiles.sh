@@ -21,7 +21,14 @@ $NCU -k regex:"k_ingest" -s 1 -c 1 -o $O/${R}_ingest python tools/prof_r2.py c2 
 $NCU -k regex:"k_gram2" -s 1 -c 1 -o $O/${R}_gram_raw python tools/prof_r2.py c2 > /dev/null 2>&1
 ONLY="store+fused g2" $NCU -k regex:"k_gram2" -s 5 -c 1 -o $O/${R}_gram_cmp python tools/prof_r2.py c2cmp > /dev/null 2>&1
 ONLY="store+fused g2" $NCU -k regex:"k_project" -c 1 -o $O/${R}_project python tools/prof_r2.py c2cmp > /dev/null 2>&1
-$NCU -k regex:"k_stream_sparse" -s 8300 -c 1 -o $O/${R}_stream_sparse python tools/prof_r2.py c3push > /dev/null 2>&1
+# C3 streaming at history depth ~19000, raw + k=128 (push_many batches): launch list of
+# the timed window, the level-1 event walk (K5e), the batched compressed columns (K6c),
+# and the dense-history K5s of the single-push path (depth 8192)
+DEPTH=18960 K=128 ncu --metrics gpu__time_duration.sum --clock-control none --csv -s 9000 -c 300 \
+    --log-file $O/${R}_c3_launches.csv python tools/time_batch.py > /dev/null 2>&1
+DEPTH=18960 $NCU -k regex:"k_stream_events" -s 1500 -c 1 -o $O/${R}_stream_events python tools/time_batch.py > /dev/null 2>&1
+DEPTH=18960 K=128 RAW=0 $NCU -k regex:"k_stream_cmp_batch" -s 1190 -c 1 -o $O/${R}_stream_cmp_batch python tools/time_batch.py > /dev/null 2>&1
+$NCU -k regex:"k_stream_sparse" -s 8200 -c 1 -o $O/${R}_stream_sparse python tools/prof_r2.py c3single > /dev/null 2>&1
 $NCU -k regex:"k_gram2" -s 1 -c 1 -o $O/${R}_c4_gram python tools/prof_r2.py c4 > /dev/null 2>&1
 $NCU -k regex:"k_ingest" -s 2 -c 1 -o $O/${R}_c5_ingest python tools/prof_r2.py c5 64 > /dev/null 2>&1
 $NCU -k regex:"k_project" -s 2 -c 1 -o $O/${R}_c5_project python tools/prof_r2.py c5 64 > /dev/null 2>&1

@@ -23,8 +23,16 @@ def main():
              "# command: python bench.py --steps 3 --warmup 3 --only 1 --no-cpu-baseline --no-e2e "
              "(tools/capture_profiles.sh): the device-resident raw C2 step",
              run("tools/launches.py", os.path.join(PROF, f"{rnd}_launches.csv")).rstrip(), ""]
+    c3 = os.path.join(PROF, f"{rnd}_c3_launches.csv")
+    if os.path.exists(c3):
+        lines += ["# C3 streaming launch list: push_many (batches of 16) at history depth ~19000,",
+                  "# raw photon-event + k=128 compressed columns (tools/time_batch.py DEPTH=18960 K=128,",
+                  "# the timed window's launches; cold, serialised: the raw and compressed chains",
+                  "# overlap on two streams live)",
+                  run("tools/launches.py", c3).rstrip(), ""]
     for name in ("ingest", "gram_raw", "project", "gram_cmp", "stream_dense", "stream_sparse",
-                 "stream_cmp", "c4_gram", "c5_ingest", "c5_project"):
+                 "stream_cmp", "stream_events", "stream_cmp_batch", "c4_gram", "c5_ingest",
+                 "c5_project"):
         rep = os.path.join(PROF, f"{rnd}_{name}.ncu-rep")
         if not os.path.exists(rep):
             continue

@@ -98,6 +98,18 @@ def main():
         nnz = float((frames[D:] != 0).float().mean()) * H * W
         gbs = nnz * (D + n / 2) / (ms / 1e3) / 1e9
         print(f"c3push depth {D}: {ms * 1e3:.1f} us/push, {gbs:.0f} GB/s of nnz*t")
+    elif what == "c3single":  # single pushes (dense-history K5s), depth 8192
+        H = W = 1024
+        Q, mu, D, n = 64, 0.02, 8192, 64
+        frames = torch.empty((D + n, H * W), dtype=torch.uint8, device=dev)
+        xg.synth_speckle(ctx, frames.data_ptr(), D + n, H, W, Q, mu, 3)
+        ring = xg.annular_rings(H, W, Q)
+        lay = xg.RingLayout(ctx, H * W, [np.nonzero(ring == r)[0] for r in range(Q)])
+        sr = xg.FrameStream(lay, D + n, sparse=True)
+        for i in range(D + n):
+            sr.push(frames[i])
+        torch.cuda.synchronize()
+        print("c3single done")
     elif what == "c5":
         k = int(sys.argv[2]) if len(sys.argv) > 2 else 64
         H, W, Q, mu, ch = 1536, 2048, 128, 0.01, 4096
