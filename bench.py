@@ -506,6 +506,43 @@ def run_headline(E, line):
         ttc_s = E.max_over_ranks((time.perf_counter() - t0) / n_ttc)
         g2_bytes = cfg["Q"] * T * 16
         ttc_bytes = cfg["Q"] * T * T * 4
+        # the same frames as photon-event lists (what event-mode detectors
+        # emit; built once outside the timed region): pinned CSR by frame ->
+        # load_events (H2D of 8 (T + 1) + 5 nnz bytes, scatter into cleared
+        # ring-major rows) + ttc_raw + every ring's g2 to the host
+        ev = None
+        if E.world == 1:
+            nz = frames.nonzero()
+            nnz = int(nz.shape[0])
+            off = torch.zeros(T + 1, dtype=torch.int64, device=frames.device)
+            off[1:] = torch.cumsum(torch.bincount(nz[:, 0], minlength=T), 0)
+            ev_host = [torch.empty(tuple(a.shape), dtype=a.dtype, pin_memory=True)
+                       for a in (off, nz[:, 1].to(torch.int32), frames[nz[:, 0], nz[:, 1]])]
+            ev_host[0].copy_(off)
+            ev_host[1].copy_(nz[:, 1].to(torch.int32))
+            ev_host[2].copy_(frames[nz[:, 0], nz[:, 1]])
+            del nz, off
+
+            def step_ev():
+                series.load_events(*ev_host).ttc_raw()
+                series.g2_all()
+
+            for _ in range(2):
+                step_ev()
+            E.sync()
+            t0 = time.perf_counter()
+            for _ in range(n_e2e):
+                step_ev()
+            E.sync()
+            ev_s = (time.perf_counter() - t0) / n_e2e
+            ev = {"value": T / ev_s, "unit": "frames/s", "ms_per_step": ev_s * 1e3,
+                  "h2d_bytes_per_step": 8 * (T + 1) + 5 * nnz, "d2h_bytes_per_step": g2_bytes,
+                  "nnz_per_frame": nnz / T,
+                  "what": "public API from pinned host photon-event lists (CSR by frame: "
+                          "offsets, int32 raster pixel, u8 count -- the same frames): "
+                          "FrameSeries.load_events + ttc_raw + every ring's g2 to the host; "
+                          "results bitwise those of the dense load (tests/test_gpu_events.py)"}
+            del ev_host
         line["e2e"] = {
             "value": T / e2e_s, "unit": "frames/s", "h2d_bytes_per_step": T * cfg["H"] * cfg["W"],
             "d2h_bytes_per_step": g2_bytes, "ms_per_step": e2e_s * 1e3,
@@ -517,6 +554,8 @@ def run_headline(E, line):
                     "d2h_bytes_per_step": g2_bytes + ttc_bytes,
                     "what": "same + every ring's TTC (the exact int32 Gram, full symmetric "
                             "T x T) read back into pinned host memory, as ttc_raw returns it"}}
+        if ev is not None:
+            line["e2e"]["events"] = ev
         del host, ttc_host
     else:
         line["e2e"] = {"skipped": "--no-e2e (profiling run)"}

@@ -120,6 +120,20 @@ XG_API void xg_series_destroy(xg_series* s);
  * [H2D] + ring permutation + per-(frame, ring) statistics. */
 XG_API int xg_series_load_frames(xg_series* s, const uint8_t* frames, int64_t n_frames,
                           int frames_on_device);
+/* Photon-event frames (what event-mode photon-counting detectors emit, and
+ * ~1/4 of the raster's PCIe bytes at 0.05 photons/pixel): frame f's events
+ * are pix[frame_off[f] .. frame_off[f+1]) (raster pixel indices, unique
+ * within a frame) with counts val[...] (>= 1); every other pixel is 0.
+ * Loads the same series as xg_series_load_frames of the dense frames (Gram,
+ * norms, g2 bitwise identical): the ring-major rows are cleared and the
+ * events scattered into them, |x|^2 summed per (frame, ring).  Pixels
+ * outside every ring are ignored; an index outside [0, full_pixels) is an
+ * XG_ERR_SHAPE at the next synchronising call.  Buffers on the host (copied
+ * H2D: 8 (n + 1) + 5 nnz bytes) or, with on_device, in device memory.
+ * Replaces the frame-by-frame raster fill in front of
+ * FrameSeries::push_back (model.cpp:28-40). */
+XG_API int xg_series_load_events(xg_series* s, const int64_t* frame_off, const int32_t* pix,
+                                 const uint8_t* val, int64_t n_frames, int on_device);
 /* Raw two-time correlation of every ring (ttc_raw, correlate.cpp:19-25):
  * exact u8 x u8 -> int32 Gram on tcgen05 tensor cores, f64 normalisation and
  * g2 (g2_from_ttc, correlate.cpp:67-85) on the device.  Asynchronous: a

@@ -453,6 +453,41 @@ class FrameSeries:
         self._keep = a
         return self
 
+    def load_events(self, frame_off, pix, val) -> "FrameSeries":
+        """Ingest photon-event frames: frame f's events are pix[frame_off[f]:
+        frame_off[f+1]] (raster pixel indices, unique within a frame) with
+        counts val[...]; every other pixel is 0.  The same series as
+        ``load`` of the dense frames (xg_series_load_events).  numpy arrays
+        (host: int64 / int32 / uint8, copied H2D) or torch tensors of those
+        dtypes, all on the context's device or all in (pinned) host memory."""
+        if hasattr(frame_off, "data_ptr"):
+            ts = (frame_off, pix, val)
+            for t_, dt in zip(ts, ("torch.int64", "torch.int32", "torch.uint8")):
+                if str(t_.dtype) != dt or not t_.is_contiguous() or t_.dim() != 1:
+                    raise ShapeError(f"load_events: expected contiguous 1-D {dt} tensors")
+            on_dev = frame_off.is_cuda
+            if any(t_.is_cuda != on_dev for t_ in ts):
+                raise ShapeError("load_events: frame_off, pix and val must share a device")
+            if on_dev and frame_off.device.index != self.ctx.device:
+                raise ShapeError("load_events: tensors on another device than the context")
+            n = frame_off.numel() - 1
+            if pix.numel() != val.numel():
+                raise ShapeError("load_events: pix and val differ in length")
+            _check(self.ctx.h, lib.xg_series_load_events(
+                self.h, C.c_void_p(frame_off.data_ptr()), C.c_void_p(pix.data_ptr()),
+                C.c_void_p(val.data_ptr()), n, 1 if on_dev else 0))
+            self._keep = None if on_dev else ts
+            return self
+        off = np.ascontiguousarray(frame_off, dtype=np.int64)
+        px = np.ascontiguousarray(pix, dtype=np.int32)
+        vv = np.ascontiguousarray(val, dtype=np.uint8)
+        if off.ndim != 1 or off.size < 2 or px.shape != vv.shape or off[-1] != px.size:
+            raise ShapeError("load_events: frame_off must hold n + 1 offsets ending at len(pix)")
+        _check(self.ctx.h, lib.xg_series_load_events(self.h, _ptr(off), _ptr(px), _ptr(vv),
+                                                      off.size - 1, 0))
+        self._keep = (off, px, vv)
+        return self
+
     def ttc_raw(self, strict: bool = False, g2: bool = True, store: bool = True) -> "FrameSeries":
         """Raw TTC of every ring (ttc_raw, correlate.cpp:19-25).  store=False
         keeps only g2 (the TTC tiles never leave the chip)."""
@@ -842,6 +877,17 @@ class FrameStream:
         _check(self.ctx.h, lib.xg_stream_get_ttc(self.h, ring, 1 if compressed else 0, code,
                                                  _ptr(out), n))
         return out
+
+
+def frames_to_events(frames):
+    """Dense u8 frames (n x pixels, numpy) -> photon-event CSR (frame_off
+    int64 [n + 1], pix int32, val uint8): the format event-mode detectors
+    deliver (host-side format conversion for tests and benchmarks)."""
+    a = np.ascontiguousarray(frames)
+    f, p = np.nonzero(a)
+    off = np.zeros(a.shape[0] + 1, np.int64)
+    np.cumsum(np.bincount(f, minlength=a.shape[0]), out=off[1:])
+    return off, p.astype(np.int32), a[f, p].astype(np.uint8)
 
 
 # --------------------------------------------- reference-facing f64 functions

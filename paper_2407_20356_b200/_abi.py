@@ -46,6 +46,7 @@ _sigs = {
     "xg_series_create2": (C.c_int, [P, P, I64, I64, C.POINTER(P)]),
     "xg_series_destroy": (None, [P]),
     "xg_series_load_frames": (C.c_int, [P, P, I64, C.c_int]),
+    "xg_series_load_events": (C.c_int, [P, P, P, P, I64, C.c_int]),
     "xg_ttc_raw": (C.c_int, [P, U32]),
     "xg_series_ttc_raw_host": (C.c_int, [P, P, I64, U32]),
     "xg_series_g2": (C.c_int, [P]),

@@ -364,4 +364,43 @@ cudaError_t launch_norms(const NormParams& p, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// K1e: CTA = frame.  Threads stride over the frame's events (coalesced
+// pix/val reads), look up (ring, column), store the count into the cleared
+// ring-major row and add its square into the ring's shared-memory |x|^2;
+// the CTA then writes the frame's |x|^2 row (exact integers: the same
+// statistics as K1 on the dense raster).
+__global__ void __launch_bounds__(256) k_ingest_events(EventIngestParams p) {
+  extern __shared__ unsigned long long sq[];
+  const int64_t f = blockIdx.x;
+  for (int r = threadIdx.x; r < p.n_rings; r += blockDim.x) sq[r] = 0ull;
+  __syncthreads();
+  const int64_t e0 = p.frame_off[f], e1 = p.frame_off[f + 1];
+  for (int64_t i = e0 + threadIdx.x; i < e1; i += blockDim.x) {
+    const int32_t px = p.pix[i];
+    if (px < 0 || px >= p.pixels) {
+      atomicOr(p.err, 8);
+      continue;
+    }
+    const int32_t e = p.pixcol[px];
+    if (e < 0) continue;
+    const int r = e >> 22, col = e & 0x3FFFFF;
+    const uint32_t v = p.val[i];
+    const int64_t koff = p.ring_koff[r];
+    uint8_t* row = p.blocked
+                       ? p.x + p.xmax * koff + f * (static_cast<int64_t>(p.ring_nkb[r]) * 128) + (col - koff)
+                       : p.x + f * p.ktot + col;
+    *row = static_cast<uint8_t>(v);
+    atomicAdd(&sq[r], static_cast<unsigned long long>(v * v));
+  }
+  __syncthreads();
+  for (int r = threadIdx.x; r < p.n_rings; r += blockDim.x) p.norm2[f * p.n_rings + r] = sq[r];
+}
+
+cudaError_t launch_ingest_events(const EventIngestParams& p, cudaStream_t s) {
+  if (p.n_frames < 1) return cudaSuccess;
+  const size_t smem = static_cast<size_t>(p.n_rings) * sizeof(unsigned long long);
+  k_ingest_events<<<static_cast<unsigned>(p.n_frames), 256, smem, s>>>(p);
+  return cudaGetLastError();
+}
+
 }  // namespace xg

@@ -103,6 +103,13 @@ struct xg_series {
   int64_t tp = 0;  // padded frame count (Gram leading dimension)
   uint8_t* d_raster = nullptr;
   uint8_t* d_x = nullptr;
+  // photon-event loads (xg_series_load_events): pixel -> (ring, column)
+  // table and grow-only staging for host event lists
+  int32_t* d_pixcol = nullptr;
+  int64_t* d_evoff = nullptr;
+  int32_t* d_evpix = nullptr;
+  uint8_t* d_evval = nullptr;
+  int64_t evoff_cap = 0, ev_cap = 0;
   int64_t* d_norm2 = nullptr;
   double* d_norms = nullptr;
   double* d_inv = nullptr;
@@ -314,6 +321,10 @@ int check_device_error(xg_ctx* c) {
     cudaMemsetAsync(c->d_err, 0, sizeof(int), c->stream);
     return fail(c, XG_ERR_CONTRACT,
                 "ttc_raw: a frame norm^2 exceeds 2^31-1; the exact int32 Gram would overflow");
+  }
+  if (h & 8) {
+    cudaMemsetAsync(c->d_err, 0, sizeof(int), c->stream);
+    return fail(c, XG_ERR_SHAPE, "load_events: a pixel index outside [0, full_pixels)");
   }
   return XG_OK;
 }
@@ -734,6 +745,10 @@ int xg_series_create2(xg_ctx* c, const xg_layout* L, int64_t max_frames, int64_t
 void xg_series_destroy(xg_series* s) {
   if (!s) return;
   dfree(s->d_raster);
+  dfree(s->d_pixcol);
+  dfree(s->d_evoff);
+  dfree(s->d_evpix);
+  dfree(s->d_evval);
   dfree(s->d_x);
   dfree(s->d_norm2);
   dfree(s->d_norms);
@@ -890,6 +905,106 @@ int xg_series_load_frames(xg_series* s, const uint8_t* frames, int64_t n, int on
   invalidate_results(s);
   rc = ingest_range(s, src, 0, n);
   if (rc) return rc;
+  s->t = n;
+  return XG_OK;
+}
+
+int xg_series_load_events(xg_series* s, const int64_t* frame_off, const int32_t* pix,
+                          const uint8_t* val, int64_t n, int on_device) {
+  if (!s || !frame_off) return XG_ERR_INVALID;
+  xg_ctx* c = s->ctx;
+  const xg_layout* L = s->L;
+  if (n < 1 || n > s->xmax)
+    return fail(c, XG_ERR_SHAPE, "load_events: %lld frames, capacity %lld", (long long)n,
+                (long long)s->xmax);
+  if (L->ktot >= (1 << 22) || L->rings > 512)
+    return fail(c, XG_ERR_CONTRACT, "load_events: at most 2^22 columns and 512 rings");
+  if (!s->d_pixcol) {
+    std::vector<int32_t> pc(static_cast<size_t>(L->pixels), -1);
+    for (int32_t r = 0; r < L->rings; ++r)
+      for (int64_t col = L->koff[r]; col < L->koff[r] + L->kpad[r]; ++col)
+        if (L->colpix[col] >= 0) pc[L->colpix[col]] = (r << 22) | static_cast<int32_t>(col);
+    XG_CUDA(c, dalloc(&s->d_pixcol, pc.size()));
+    XG_CUDA(c, cudaMemcpy(s->d_pixcol, pc.data(), pc.size() * 4, cudaMemcpyHostToDevice));
+  }
+  const int64_t* d_off = frame_off;
+  const int32_t* d_pix = pix;
+  const uint8_t* d_val = val;
+  if (!on_device) {
+    if (frame_off[0] != 0) return fail(c, XG_ERR_SHAPE, "load_events: frame_off[0] must be 0");
+    for (int64_t f = 0; f < n; ++f)
+      if (frame_off[f + 1] < frame_off[f])
+        return fail(c, XG_ERR_SHAPE, "load_events: frame_off must be non-decreasing");
+    const int64_t nnz = frame_off[n];
+    if (nnz > 0 && (!pix || !val)) return XG_ERR_INVALID;
+    if (s->evoff_cap < n + 1) {
+      dfree(s->d_evoff);
+      XG_CUDA(c, dalloc(&s->d_evoff, (size_t)(n + 1)));
+      s->evoff_cap = n + 1;
+    }
+    if (s->ev_cap < nnz) {
+      dfree(s->d_evpix);
+      dfree(s->d_evval);
+      XG_CUDA(c, dalloc(&s->d_evpix, (size_t)nnz));
+      XG_CUDA(c, dalloc(&s->d_evval, (size_t)nnz));
+      s->ev_cap = nnz;
+    }
+    XG_CUDA(c, cudaMemcpyAsync(s->d_evoff, frame_off, (size_t)(n + 1) * 8, cudaMemcpyHostToDevice,
+                               c->stream));
+    if (nnz > 0) {
+      XG_CUDA(c, cudaMemcpyAsync(s->d_evpix, pix, (size_t)nnz * 4, cudaMemcpyHostToDevice, c->stream));
+      XG_CUDA(c, cudaMemcpyAsync(s->d_evval, val, (size_t)nnz, cudaMemcpyHostToDevice, c->stream));
+    }
+    d_off = s->d_evoff;
+    d_pix = s->d_evpix;
+    d_val = s->d_evval;
+  }
+  s->x_row0 = 0;
+  int rc = reset_stats(s, n);
+  if (rc) return rc;
+  invalidate_results(s);
+  // clear the rows the events land in (zero pixels and the ring padding)
+  if (L->blocked) {
+    for (int32_t r = 0; r < L->rings; ++r)
+      XG_CUDA(c, cudaMemsetAsync(s->d_x + ring_base(L, s->xmax, r), 0,
+                                 (size_t)n * ring_ld(L, r), c->stream));
+  } else {
+    XG_CUDA(c, cudaMemsetAsync(s->d_x, 0, (size_t)n * L->ktot, c->stream));
+  }
+  EventIngestParams ep;
+  ep.frame_off = d_off;
+  ep.pix = d_pix;
+  ep.val = d_val;
+  ep.n_frames = n;
+  ep.pixels = L->pixels;
+  ep.pixcol = s->d_pixcol;
+  ep.ring_koff = L->d_ring_koff;
+  ep.ring_nkb = L->d_ring_nkb;
+  ep.n_rings = L->rings;
+  ep.x = s->d_x;
+  ep.xmax = s->xmax;
+  ep.ktot = L->ktot;
+  ep.blocked = L->blocked ? 1 : 0;
+  ep.norm2 = reinterpret_cast<unsigned long long*>(s->d_norm2);
+  ep.err = c->d_err;
+  XG_CUDA(c, launch_ingest_events(ep, c->stream));
+  NormParams np;
+  np.t0 = 0;
+  np.norm2 = s->d_norm2;
+  np.n_frames = n;
+  np.ld = s->tp;
+  np.n_rings = L->rings;
+  np.norms = s->d_norms;
+  np.inv = s->d_inv;
+  np.inv2 = s->d_inv2;
+  np.zero_count = s->d_zero;
+  np.first_zero = s->d_first_zero;
+  np.nz_bits = s->d_nz_bits;
+  np.nz_words = s->nz_words;
+  np.max_norm2 = reinterpret_cast<unsigned long long*>(s->d_max_norm2);
+  np.err = nullptr;  // the int32 overflow is checked by K2, where the raw Gram is formed
+  XG_CUDA(c, launch_norms(np, c->stream));
+  c->launches += 2;
   s->t = n;
   return XG_OK;
 }

@@ -100,6 +100,26 @@ struct IngestParams {
 };
 cudaError_t launch_ingest(const IngestParams& p, cudaStream_t s);
 
+// K1e: photon-event frames (CSR by frame) scattered into cleared ring-major
+// rows; |x|^2 per (frame, ring) summed in shared memory, one row per CTA.
+struct EventIngestParams {
+  const int64_t* frame_off;  // [n_frames + 1]
+  const int32_t* pix;        // raster pixel index per event
+  const uint8_t* val;        // count per event
+  int64_t n_frames;
+  int64_t pixels;
+  const int32_t* pixcol;     // [pixels] ring << 22 | column (-1: no ring)
+  const int32_t* ring_koff;
+  const int32_t* ring_nkb;
+  int32_t n_rings;
+  uint8_t* x;
+  int64_t xmax, ktot;
+  int32_t blocked;
+  unsigned long long* norm2; // [frame][ring], written (not accumulated)
+  int* err;                  // bit 3: pixel index out of range
+};
+cudaError_t launch_ingest_events(const EventIngestParams& p, cudaStream_t s);
+
 // --------------------------------------------------------- per-ring norms
 // norms[r][t] = sqrt(norm2[t][r]), inv = 1/norms (0 for zero frames);
 // counts zero frames per ring and flags int32-Gram overflow (norm2 >= 2^31).

@@ -130,3 +130,23 @@ def test_pyapi_host_contracts():
         xv.TTCMatrix(np.array([[1.0, 0.5], [0.4, 1.0]]), True)
     with pytest.raises(xv.ContractError):
         xv.TTCMatrix(np.array([[0.9, 0.5], [0.5, 1.0]]), True)
+
+
+def test_frames_to_events_roundtrip():
+    """The photon-event CSR helper (the format xg_series_load_events takes):
+    offsets per frame, raster pixel indices ascending within a frame, counts;
+    scattering it back gives the dense frames, empty frames included."""
+    import paper_2407_20356_b200 as xg
+
+    rng = np.random.default_rng(4)
+    frames = (rng.poisson(0.2, (37, 300)) * (rng.random((37, 300)) < 0.5)).astype(np.uint8)
+    frames[5] = 0
+    off, pix, val = xg.frames_to_events(frames)
+    assert off.dtype == np.int64 and pix.dtype == np.int32 and val.dtype == np.uint8
+    assert off[0] == 0 and off[-1] == pix.size and off[6] == off[5]
+    back = np.zeros_like(frames)
+    for f in range(frames.shape[0]):
+        sl = slice(off[f], off[f + 1])
+        assert np.all(np.diff(pix[sl]) > 0)
+        back[f, pix[sl]] = val[sl]
+    assert np.array_equal(back, frames) and np.all(val > 0)
