@@ -523,8 +523,8 @@ def run_headline(E, line):
             ev_host[2].copy_(frames[nz[:, 0], nz[:, 1]])
             del nz, off
 
-            def step_ev():
-                series.load_events(*ev_host).ttc_raw()
+            def step_ev():  # chunked H2D overlapped with the scatter + Gram tiles
+                series.ttc_raw_events_host(*ev_host)
                 series.g2_all()
 
             for _ in range(2):
@@ -540,7 +540,8 @@ def run_headline(E, line):
                   "nnz_per_frame": nnz / T,
                   "what": "public API from pinned host photon-event lists (CSR by frame: "
                           "offsets, int32 raster pixel, u8 count -- the same frames): "
-                          "FrameSeries.load_events + ttc_raw + every ring's g2 to the host; "
+                          "FrameSeries.ttc_raw_events_host (chunked H2D overlapped with the "
+                          "scatter and the Gram tiles) + every ring's g2 to the host; "
                           "results bitwise those of the dense load (tests/test_gpu_events.py)"}
             del ev_host
         line["e2e"] = {

@@ -147,6 +147,13 @@ XG_API int xg_ttc_raw(xg_series* s, uint32_t flags);
  * the Gram tiles each arrived chunk completes.  Same results. */
 XG_API int xg_series_ttc_raw_host(xg_series* s, const uint8_t* frames, int64_t n_frames,
                                   uint32_t flags);
+/* xg_series_load_events + xg_ttc_raw for event lists in host memory (pinned
+ * for full overlap): the frames' events cross PCIe in chunks of whole
+ * 256-frame column blocks on a second stream, each chunk scattered and its
+ * Gram tiles run as it lands.  Same results. */
+XG_API int xg_series_ttc_raw_events_host(xg_series* s, const int64_t* frame_off,
+                                         const int32_t* pix, const uint8_t* val, int64_t n_frames,
+                                         uint32_t flags);
 /* g2 of every ring from the current raw TTC (run separately after
  * xg_ttc_raw(..., XG_NO_G2)). */
 XG_API int xg_series_g2(xg_series* s);

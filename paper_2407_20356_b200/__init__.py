@@ -488,6 +488,39 @@ class FrameSeries:
         self._keep = (off, px, vv)
         return self
 
+    def ttc_raw_events_host(self, frame_off, pix, val, strict: bool = False, g2: bool = True,
+                            store: bool = True) -> "FrameSeries":
+        """load_events() + ttc_raw() for event lists in HOST memory, the PCIe
+        transfer of each chunk of frames overlapped with the scatter and the
+        Gram tiles it completes (xg_series_ttc_raw_events_host).  Pinned torch
+        tensors (int64 / int32 / uint8) for full overlap, or numpy arrays."""
+        flags = ((_abi.STRICT if strict else 0) | (0 if g2 else _abi.NO_G2)
+                 | (0 if store else _abi.NO_STORE))
+        if hasattr(frame_off, "data_ptr"):
+            ts = (frame_off, pix, val)
+            for t_, dt in zip(ts, ("torch.int64", "torch.int32", "torch.uint8")):
+                if (str(t_.dtype) != dt or not t_.is_contiguous() or t_.dim() != 1
+                        or t_.is_cuda):
+                    raise ShapeError(f"ttc_raw_events_host: expected contiguous 1-D host {dt}")
+            if pix.numel() != val.numel():
+                raise ShapeError("ttc_raw_events_host: pix and val differ in length")
+            ptrs = [C.c_void_p(t_.data_ptr()) for t_ in ts]
+            n = frame_off.numel() - 1
+            keep = ts
+        else:
+            off = np.ascontiguousarray(frame_off, dtype=np.int64)
+            px = np.ascontiguousarray(pix, dtype=np.int32)
+            vv = np.ascontiguousarray(val, dtype=np.uint8)
+            if off.ndim != 1 or off.size < 2 or px.shape != vv.shape or off[-1] != px.size:
+                raise ShapeError("ttc_raw_events_host: frame_off must hold n + 1 offsets ending "
+                                 "at len(pix)")
+            ptrs = [_ptr(off), _ptr(px), _ptr(vv)]
+            n = off.size - 1
+            keep = (off, px, vv)
+        _check(self.ctx.h, lib.xg_series_ttc_raw_events_host(self.h, *ptrs, n, flags))
+        self._keep = keep
+        return self
+
     def ttc_raw(self, strict: bool = False, g2: bool = True, store: bool = True) -> "FrameSeries":
         """Raw TTC of every ring (ttc_raw, correlate.cpp:19-25).  store=False
         keeps only g2 (the TTC tiles never leave the chip)."""

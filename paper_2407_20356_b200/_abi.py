@@ -47,6 +47,7 @@ _sigs = {
     "xg_series_destroy": (None, [P]),
     "xg_series_load_frames": (C.c_int, [P, P, I64, C.c_int]),
     "xg_series_load_events": (C.c_int, [P, P, P, P, I64, C.c_int]),
+    "xg_series_ttc_raw_events_host": (C.c_int, [P, P, P, P, I64, C.c_uint32]),
     "xg_ttc_raw": (C.c_int, [P, U32]),
     "xg_series_ttc_raw_host": (C.c_int, [P, P, I64, U32]),
     "xg_series_g2": (C.c_int, [P]),

@@ -371,7 +371,7 @@ cudaError_t launch_norms(const NormParams& p, cudaStream_t s) {
 // statistics as K1 on the dense raster).
 __global__ void __launch_bounds__(256) k_ingest_events(EventIngestParams p) {
   extern __shared__ unsigned long long sq[];
-  const int64_t f = blockIdx.x;
+  const int64_t f = p.t0 + blockIdx.x;
   for (int r = threadIdx.x; r < p.n_rings; r += blockDim.x) sq[r] = 0ull;
   __syncthreads();
   const int64_t e0 = p.frame_off[f], e1 = p.frame_off[f + 1];

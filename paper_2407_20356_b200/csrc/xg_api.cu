@@ -909,9 +909,9 @@ int xg_series_load_frames(xg_series* s, const uint8_t* frames, int64_t n, int on
   return XG_OK;
 }
 
-int xg_series_load_events(xg_series* s, const int64_t* frame_off, const int32_t* pix,
-                          const uint8_t* val, int64_t n, int on_device) {
-  if (!s || !frame_off) return XG_ERR_INVALID;
+// Photon-event loads: the pixel -> (ring, column) table, host-side checks of
+// the offsets, staging capacity, and the per-range scatter + norms.
+static int events_prepare(xg_series* s, int64_t n) {
   xg_ctx* c = s->ctx;
   const xg_layout* L = s->L;
   if (n < 1 || n > s->xmax)
@@ -927,43 +927,39 @@ int xg_series_load_events(xg_series* s, const int64_t* frame_off, const int32_t*
     XG_CUDA(c, dalloc(&s->d_pixcol, pc.size()));
     XG_CUDA(c, cudaMemcpy(s->d_pixcol, pc.data(), pc.size() * 4, cudaMemcpyHostToDevice));
   }
-  const int64_t* d_off = frame_off;
-  const int32_t* d_pix = pix;
-  const uint8_t* d_val = val;
-  if (!on_device) {
-    if (frame_off[0] != 0) return fail(c, XG_ERR_SHAPE, "load_events: frame_off[0] must be 0");
-    for (int64_t f = 0; f < n; ++f)
-      if (frame_off[f + 1] < frame_off[f])
-        return fail(c, XG_ERR_SHAPE, "load_events: frame_off must be non-decreasing");
-    const int64_t nnz = frame_off[n];
-    if (nnz > 0 && (!pix || !val)) return XG_ERR_INVALID;
-    if (s->evoff_cap < n + 1) {
-      dfree(s->d_evoff);
-      XG_CUDA(c, dalloc(&s->d_evoff, (size_t)(n + 1)));
-      s->evoff_cap = n + 1;
-    }
-    if (s->ev_cap < nnz) {
-      dfree(s->d_evpix);
-      dfree(s->d_evval);
-      XG_CUDA(c, dalloc(&s->d_evpix, (size_t)nnz));
-      XG_CUDA(c, dalloc(&s->d_evval, (size_t)nnz));
-      s->ev_cap = nnz;
-    }
-    XG_CUDA(c, cudaMemcpyAsync(s->d_evoff, frame_off, (size_t)(n + 1) * 8, cudaMemcpyHostToDevice,
-                               c->stream));
-    if (nnz > 0) {
-      XG_CUDA(c, cudaMemcpyAsync(s->d_evpix, pix, (size_t)nnz * 4, cudaMemcpyHostToDevice, c->stream));
-      XG_CUDA(c, cudaMemcpyAsync(s->d_evval, val, (size_t)nnz, cudaMemcpyHostToDevice, c->stream));
-    }
-    d_off = s->d_evoff;
-    d_pix = s->d_evpix;
-    d_val = s->d_evval;
+  return XG_OK;
+}
+
+static int events_stage(xg_series* s, const int64_t* frame_off, const int32_t* pix,
+                        const uint8_t* val, int64_t n) {
+  xg_ctx* c = s->ctx;
+  if (frame_off[0] != 0) return fail(c, XG_ERR_SHAPE, "load_events: frame_off[0] must be 0");
+  for (int64_t f = 0; f < n; ++f)
+    if (frame_off[f + 1] < frame_off[f])
+      return fail(c, XG_ERR_SHAPE, "load_events: frame_off must be non-decreasing");
+  const int64_t nnz = frame_off[n];
+  if (nnz > 0 && (!pix || !val)) return XG_ERR_INVALID;
+  if (s->evoff_cap < n + 1) {
+    dfree(s->d_evoff);
+    s->evoff_cap = 0;
+    XG_CUDA(c, dalloc(&s->d_evoff, (size_t)(n + 1)));
+    s->evoff_cap = n + 1;
   }
-  s->x_row0 = 0;
-  int rc = reset_stats(s, n);
-  if (rc) return rc;
-  invalidate_results(s);
-  // clear the rows the events land in (zero pixels and the ring padding)
+  if (s->ev_cap < nnz) {
+    dfree(s->d_evpix);
+    dfree(s->d_evval);
+    s->ev_cap = 0;
+    XG_CUDA(c, dalloc(&s->d_evpix, (size_t)nnz));
+    XG_CUDA(c, dalloc(&s->d_evval, (size_t)nnz));
+    s->ev_cap = nnz;
+  }
+  return XG_OK;
+}
+
+// clear rows [0, n) of the ring-major buffer (zero pixels, ring padding)
+static int events_clear(xg_series* s, int64_t n) {
+  xg_ctx* c = s->ctx;
+  const xg_layout* L = s->L;
   if (L->blocked) {
     for (int32_t r = 0; r < L->rings; ++r)
       XG_CUDA(c, cudaMemsetAsync(s->d_x + ring_base(L, s->xmax, r), 0,
@@ -971,8 +967,17 @@ int xg_series_load_events(xg_series* s, const int64_t* frame_off, const int32_t*
   } else {
     XG_CUDA(c, cudaMemsetAsync(s->d_x, 0, (size_t)n * L->ktot, c->stream));
   }
+  return XG_OK;
+}
+
+// K1e + K1b for frames [t0, t0 + n) of device event lists (global offsets)
+static int events_ingest(xg_series* s, const int64_t* d_off, const int32_t* d_pix,
+                         const uint8_t* d_val, int64_t t0, int64_t n) {
+  xg_ctx* c = s->ctx;
+  const xg_layout* L = s->L;
   EventIngestParams ep;
   ep.frame_off = d_off;
+  ep.t0 = t0;
   ep.pix = d_pix;
   ep.val = d_val;
   ep.n_frames = n;
@@ -989,7 +994,7 @@ int xg_series_load_events(xg_series* s, const int64_t* frame_off, const int32_t*
   ep.err = c->d_err;
   XG_CUDA(c, launch_ingest_events(ep, c->stream));
   NormParams np;
-  np.t0 = 0;
+  np.t0 = t0;
   np.norm2 = s->d_norm2;
   np.n_frames = n;
   np.ld = s->tp;
@@ -1005,6 +1010,40 @@ int xg_series_load_events(xg_series* s, const int64_t* frame_off, const int32_t*
   np.err = nullptr;  // the int32 overflow is checked by K2, where the raw Gram is formed
   XG_CUDA(c, launch_norms(np, c->stream));
   c->launches += 2;
+  return XG_OK;
+}
+
+int xg_series_load_events(xg_series* s, const int64_t* frame_off, const int32_t* pix,
+                          const uint8_t* val, int64_t n, int on_device) {
+  if (!s || !frame_off) return XG_ERR_INVALID;
+  xg_ctx* c = s->ctx;
+  int rc = events_prepare(s, n);
+  if (rc) return rc;
+  const int64_t* d_off = frame_off;
+  const int32_t* d_pix = pix;
+  const uint8_t* d_val = val;
+  if (!on_device) {
+    rc = events_stage(s, frame_off, pix, val, n);
+    if (rc) return rc;
+    const int64_t nnz = frame_off[n];
+    XG_CUDA(c, cudaMemcpyAsync(s->d_evoff, frame_off, (size_t)(n + 1) * 8, cudaMemcpyHostToDevice,
+                               c->stream));
+    if (nnz > 0) {
+      XG_CUDA(c, cudaMemcpyAsync(s->d_evpix, pix, (size_t)nnz * 4, cudaMemcpyHostToDevice, c->stream));
+      XG_CUDA(c, cudaMemcpyAsync(s->d_evval, val, (size_t)nnz, cudaMemcpyHostToDevice, c->stream));
+    }
+    d_off = s->d_evoff;
+    d_pix = s->d_evpix;
+    d_val = s->d_evval;
+  }
+  s->x_row0 = 0;
+  rc = reset_stats(s, n);
+  if (rc) return rc;
+  invalidate_results(s);
+  rc = events_clear(s, n);
+  if (rc) return rc;
+  rc = events_ingest(s, d_off, d_pix, d_val, 0, n);
+  if (rc) return rc;
   s->t = n;
   return XG_OK;
 }
@@ -1295,6 +1334,72 @@ int xg_series_ttc_raw_host(xg_series* s, const uint8_t* frames, int64_t n, uint3
     XG_CUDA(c, cudaEventRecord(c->events[k], c->copy_stream));
     XG_CUDA(c, cudaStreamWaitEvent(c->stream, c->events[k], 0));
     rc = ingest_range(s, s->d_raster + t0 * L->pixels, t0, t1 - t0);
+    if (rc) return rc;
+    const int32_t o0 = s->tiles2_joff[jb0], o1 = s->tiles2_joff[jb1];
+    XG_CUDA(c, launch_gram_any(s, 0, map, omap, gp, s->d_tiles2_j + o0, o1 - o0));
+    c->launches++;
+  }
+  if (g2) {
+    rc = fold_g2(s, s->d_g2, s->d_g2cnt);
+    if (rc) return rc;
+  }
+  s->have_raw = true;
+  s->raw_g2 = g2;
+  return XG_OK;
+}
+
+int xg_series_ttc_raw_events_host(xg_series* s, const int64_t* frame_off, const int32_t* pix,
+                                  const uint8_t* val, int64_t n, uint32_t flags) {
+  if (!s || !frame_off) return XG_ERR_INVALID;
+  xg_ctx* c = s->ctx;
+  if (n < 2) return fail(c, XG_ERR_CONTRACT, "ttc_raw: need at least 2 frames");
+  if (flags & XG_STRICT) {  // strict needs every frame before the Gram
+    int rc = xg_series_load_events(s, frame_off, pix, val, n, 0);
+    return rc ? rc : xg_ttc_raw(s, flags);
+  }
+  int rc = events_prepare(s, n);
+  if (rc) return rc;
+  rc = events_stage(s, frame_off, pix, val, n);
+  if (rc) return rc;
+  if (!c->copy_stream) XG_CUDA(c, cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+  const int64_t nbj = (n + 255) / 256;
+  const int64_t jb_per = std::max<int64_t>(1, (nbj + 7) / 8);
+  const int64_t nchunks = (nbj + jb_per - 1) / jb_per;
+  while ((int64_t)c->events.size() < nchunks + 1) {
+    cudaEvent_t ev;
+    XG_CUDA(c, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    c->events.push_back(ev);
+  }
+  s->x_row0 = 0;
+  rc = reset_stats(s, n);
+  if (rc) return rc;
+  s->t = n;
+  invalidate_results(s);
+  rc = events_clear(s, n);
+  if (rc) return rc;
+  const bool g2 = !(flags & XG_NO_G2);
+  GramParams gp;
+  CUtensorMap map, omap;
+  rc = raw_gram_setup(s, g2, !(flags & XG_NO_STORE), gp, map, omap);
+  if (rc) return rc;
+  // the staging lists may still be read by earlier work on the compute stream
+  XG_CUDA(c, cudaEventRecord(c->events[nchunks], c->stream));
+  XG_CUDA(c, cudaStreamWaitEvent(c->copy_stream, c->events[nchunks], 0));
+  XG_CUDA(c, cudaMemcpyAsync(s->d_evoff, frame_off, (size_t)(n + 1) * 8, cudaMemcpyHostToDevice,
+                             c->copy_stream));
+  for (int64_t k = 0; k < nchunks; ++k) {
+    const int64_t jb0 = k * jb_per, jb1 = std::min(nbj, jb0 + jb_per);
+    const int64_t t0 = jb0 * 256, t1 = std::min(n, jb1 * 256);
+    const int64_t e0 = frame_off[t0], e1 = frame_off[t1];
+    if (e1 > e0) {
+      XG_CUDA(c, cudaMemcpyAsync(s->d_evpix + e0, pix + e0, (size_t)(e1 - e0) * 4,
+                                 cudaMemcpyHostToDevice, c->copy_stream));
+      XG_CUDA(c, cudaMemcpyAsync(s->d_evval + e0, val + e0, (size_t)(e1 - e0),
+                                 cudaMemcpyHostToDevice, c->copy_stream));
+    }
+    XG_CUDA(c, cudaEventRecord(c->events[k], c->copy_stream));
+    XG_CUDA(c, cudaStreamWaitEvent(c->stream, c->events[k], 0));
+    rc = events_ingest(s, s->d_evoff, s->d_evpix, s->d_evval, t0, t1 - t0);
     if (rc) return rc;
     const int32_t o0 = s->tiles2_joff[jb0], o1 = s->tiles2_joff[jb1];
     XG_CUDA(c, launch_gram_any(s, 0, map, omap, gp, s->d_tiles2_j + o0, o1 - o0));

@@ -103,7 +103,8 @@ cudaError_t launch_ingest(const IngestParams& p, cudaStream_t s);
 // K1e: photon-event frames (CSR by frame) scattered into cleared ring-major
 // rows; |x|^2 per (frame, ring) summed in shared memory, one row per CTA.
 struct EventIngestParams {
-  const int64_t* frame_off;  // [n_frames + 1]
+  const int64_t* frame_off;  // [t0 + n_frames + 1] (event indices into pix / val)
+  int64_t t0;                // first frame of this launch
   const int32_t* pix;        // raster pixel index per event
   const uint8_t* val;        // count per event
   int64_t n_frames;

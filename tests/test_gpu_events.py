@@ -43,6 +43,9 @@ def test_events_equal_dense_load(ctx, orc, t, h, w, q, mu, seed):
     s_ev = xg.FrameSeries(lay, t).load_events(off, pix, val).ttc_raw()
     s_dn = xg.FrameSeries(lay, t).load(frames).ttc_raw()
     _compare(s_ev, s_dn, frames, ring, q, orc)
+    # host lists in chunks of 256-frame column blocks, overlapped with the tiles
+    s_hx = xg.FrameSeries(lay, t).ttc_raw_events_host(off, pix, val)
+    _compare(s_hx, s_dn, frames, ring, q, orc, check_oracle=False)
 
 
 def test_events_blocked_layout_device_tensors_and_reload(ctx, orc):
@@ -63,6 +66,9 @@ def test_events_blocked_layout_device_tensors_and_reload(ctx, orc):
     s_ev.load_events(torch.from_numpy(off).cuda(), torch.from_numpy(pix).cuda(),
                      torch.from_numpy(val).cuda()).ttc_raw()
     s_dn = xg.FrameSeries(lay, t).load(dev).ttc_raw()
+    _compare(s_ev, s_dn, frames, ring, q, orc, check_oracle=False)
+    pinned = [torch.from_numpy(a).pin_memory() for a in (off, pix, val)]
+    s_ev.ttc_raw_events_host(*pinned)  # the chunked host path over the same series
     _compare(s_ev, s_dn, frames, ring, q, orc, check_oracle=False)
     for r in (0, 3):  # the oracle on two rings (the 1024^2 oracle Gram is slow)
         assert np.array_equal(s_ev.ttc(r, "gram").astype(np.int64),
