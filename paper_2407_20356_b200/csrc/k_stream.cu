@@ -842,11 +842,12 @@ __global__ void __launch_bounds__(256, XG_EV_MINB) k_stream_events(StreamParams 
       const int xv = nz_val[i];
       const int2 e = __ldg(idx + col);
       const int end = e.x + e.y;
-      for (int k = e.x & ~3; k < end; k += 4 * EV_U4) {
-        uint4 w[EV_U4];
+      int k = e.x & ~3;
+      uint4 w[EV_U4];
 #pragma unroll
-        for (int u = 0; u < EV_U4; ++u)
-          w[u] = k + 4 * u < end ? __ldg(ev4 + ((k >> 2) + u)) : make_uint4(0u, 0u, 0u, 0u);
+      for (int u = 0; u < EV_U4; ++u)
+        w[u] = k + 4 * u < end ? __ldg(ev4 + ((k >> 2) + u)) : make_uint4(0u, 0u, 0u, 0u);
+      while (k < end) {
 #pragma unroll
         for (int u = 0; u < EV_U4; ++u) {
           const uint32_t ww[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
@@ -857,6 +858,10 @@ __global__ void __launch_bounds__(256, XG_EV_MINB) k_stream_events(StreamParams 
               atomicAdd(&acc[ww[c] >> 8], static_cast<int>(ww[c] & 0xFFu) * xv);
           }
         }
+        k += 4 * EV_U4;
+#pragma unroll
+        for (int u = 0; u < EV_U4; ++u)
+          w[u] = k + 4 * u < end ? __ldg(ev4 + ((k >> 2) + u)) : make_uint4(0u, 0u, 0u, 0u);
       }
     }
   } else {
