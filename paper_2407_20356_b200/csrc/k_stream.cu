@@ -21,6 +21,7 @@
 //   K6b cmp:  C~(s,t) = y_s . y_t over an fp32 copy of the coefficient
 //             history (C~ is fp32-accurate by contract), g2 accumulated like
 //             K5 in f64.  HBM-bound: t * Q * k * 4 B.
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -193,68 +194,6 @@ __global__ void __launch_bounds__(128) k_stream_proj_fin(StreamParams p) {
   }
   __syncthreads();
   for (int j = threadIdx.x; j < p.n_digits * p.k; j += blockDim.x) pa[j] = 0;
-}
-
-// K6b: grid (ceil((t+1)/SR_ROWS), rings); a warp per history row.
-template <int MAXV>
-__global__ void __launch_bounds__(SR_THREADS, 4) k_stream_cmp(StreamParams p) {
-  // fp32 coefficient history (C~ is fp32-accurate by contract), rows padded
-  // to kq = k rounded up to 4 (zero pad): lane L holds float4 chunks L, L+32,
-  // ... of the new row; a warp's 8 history rows are loaded (16 B per lane per
-  // row) before any arithmetic; fp32 products summed over k, lags in f64
-  const int r = blockIdx.y;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  pdl_wait();  // proj_fin(t): y_t
-  pdl_launch_dependents();
-  const int kq = p.kq, nv = kq >> 2;
-  const float* ybase = p.yf + static_cast<int64_t>(r) * p.y_ld * kq;
-  float4 yn[MAXV];
-#pragma unroll
-  for (int m = 0; m < MAXV; ++m) {
-    const int v = lane + 32 * m;
-    yn[m] = v < nv ? *reinterpret_cast<const float4*>(ybase + p.t * kq + 4 * v)
-                   : make_float4(0.f, 0.f, 0.f, 0.f);
-  }
-  const double inv_t = p.inv[static_cast<int64_t>(r) * p.inv_ld + p.t];
-  constexpr int RPW = SR_ROWS / (SR_THREADS / 32);
-  const int64_t s_first = static_cast<int64_t>(blockIdx.x) * SR_ROWS + warp * RPW;
-  float part[RPW];
-#pragma unroll
-  for (int q = 0; q < RPW; ++q) part[q] = 0.f;
-#pragma unroll
-  for (int m = 0; m < MAXV; ++m) {
-    if (32 * m >= nv) break;
-    const int v = lane + 32 * m;
-    float4 ld[RPW];
-#pragma unroll
-    for (int q = 0; q < RPW; ++q) {
-      const int64_t s = s_first + q;
-      ld[q] = (v < nv && s <= p.t)
-                  ? __ldcs(reinterpret_cast<const float4*>(ybase + s * kq + 4 * v))
-                  : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-#pragma unroll
-    for (int q = 0; q < RPW; ++q)
-      part[q] = fmaf(ld[q].x, yn[m].x,
-                     fmaf(ld[q].y, yn[m].y, fmaf(ld[q].z, yn[m].z, fmaf(ld[q].w, yn[m].w, part[q]))));
-  }
-  float mine = 0.f;
-#pragma unroll
-  for (int q = 0; q < RPW; ++q) {
-    float a = part[q];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-    if (lane == q) mine = a;
-  }
-  const int64_t s = s_first + lane;
-  if (lane < RPW && s <= p.t) {
-    const double acc = mine;
-    const double inv_s = p.inv[static_cast<int64_t>(r) * p.inv_ld + s];
-    const int64_t gi = static_cast<int64_t>(r) * p.g2_ld + (p.t - s);
-    p.cg2sum[gi] += acc;
-    p.cg2cnt[gi] += (inv_s != 0.0 && inv_t != 0.0) ? 1 : 0;
-    if (p.ccol) p.ccol[static_cast<int64_t>(r) * p.col_ring_stride + s * p.col_ld + p.t] = mine;
-  }
 }
 
 }  // namespace
@@ -561,85 +500,124 @@ __global__ void __launch_bounds__(32 * SS_W, SS_MINB) k_stream_sparse(StreamPara
   if (!BATCH && p.pdl_wait_end) pdl_wait();  // cmp(t) has completed too (see above)
 }
 
-// K6c: the compressed columns of a batch of nb new frames t .. t + nb - 1,
-// grid (ceil((t + nb) / SR_ROWS), rings).  A warp loads its 8 history rows
-// once (as K6b does) and forms C~(s, t + j) for every frame j of the batch:
-// the new rows come from shared memory, the products are K6b's per-lane fmaf
-// chains, and the cross-lane sums are K6b's xor-butterfly tree taken by
-// recursive halving (8 rows per 9 shuffles instead of 40; every pair sum is
-// the butterfly's, so C~ equals K6b's bitwise).  History bytes are read once
-// per batch instead of once per frame.
+// K6: the compressed columns C~(s, t + j) of nb <= 16 new frames (a single
+// push: nb = 1) on tensor cores, grid (ceil((t + nb) / 128), rings), a warp
+// per 16 history rows: mma.sync m16n8k16 bf16 -> fp32 over the history
+// rows (A, from global) and the new rows (B, shared memory), each fp32 value
+// split into three bf16 planes (h + m + l carries its 24 bits) and six of
+// the nine plane products accumulated (the dropped ones are ~2^-24
+// relative, as K4).  Every (s, t) entry depends only on its two rows and the
+// fixed k order, so single pushes (one 8-frame n-tile, one column used) and
+// batches (two n-tiles) give the same bits.  HBM-bound: the history is read
+// once per launch (per 16 frames in a batch).
+__device__ __forceinline__ void split3(float x, __nv_bfloat16& h, __nv_bfloat16& m,
+                                       __nv_bfloat16& l) {
+  h = __float2bfloat16_rn(x);
+  const float r1 = x - __bfloat162float(h);
+  m = __float2bfloat16_rn(r1);
+  l = __float2bfloat16_rn(r1 - __bfloat162float(m));
+}
+__device__ __forceinline__ uint32_t pack_bf16(__nv_bfloat16 lo, __nv_bfloat16 hi) {
+  __nv_bfloat162 v = __halves2bfloat162(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+__device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0,
+                                         uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
 constexpr int CB_MAXNB = 16;
-template <int MAXV, int RPW>
-__global__ void __launch_bounds__(SR_THREADS, 2) k_stream_cmp_batch(StreamParams p) {
-  __shared__ float4 ynew[CB_MAXNB][32 * MAXV];
+constexpr int TC_KMAX = 256;
+constexpr int TC_BLD = TC_KMAX + 8;  // padded plane rows: conflict-free B fragment loads
+constexpr int TC_KG = 4;             // k-steps of A loaded before their MMAs
+template <int NT>
+__global__ void __launch_bounds__(256) k_stream_cmp_tc(StreamParams p) {
+  __shared__ __align__(16) __nv_bfloat16 bpl[3][8 * NT][TC_BLD];
   const int r = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int kq = p.kq, nv = kq >> 2, nb = p.scr_nb;
+  const int gid = lane >> 2, tig = lane & 3;
+  pdl_wait();  // proj_fin: the new rows
+  pdl_launch_dependents();
+  const int kq = p.kq, ks = (kq + 15) >> 4, nb = p.scr_nb;
   const float* ybase = p.yf + static_cast<int64_t>(r) * p.y_ld * kq;
-  for (int i = threadIdx.x; i < nb * 32 * MAXV; i += SR_THREADS) {
-    const int jj = i / (32 * MAXV), v = i % (32 * MAXV);
-    ynew[jj][v] = v < nv ? *reinterpret_cast<const float4*>(ybase + (p.t + jj) * kq + 4 * v)
-                         : make_float4(0.f, 0.f, 0.f, 0.f);
-  }
-  static_assert(RPW == 8 || RPW == 16, "recursive halving below covers 8 or 16 rows per warp");
-  const int64_t t_last = p.t + nb - 1;
-  const int64_t s_first =
-      static_cast<int64_t>(blockIdx.x) * (RPW * (SR_THREADS / 32)) + warp * RPW;
-  float4 ld[RPW][MAXV];
-#pragma unroll
-  for (int m = 0; m < MAXV; ++m) {
-    const int v = lane + 32 * m;
-#pragma unroll
-    for (int q = 0; q < RPW; ++q) {
-      const int64_t s = s_first + q;
-      ld[q][m] = (v < nv && s <= t_last)
-                     ? __ldcs(reinterpret_cast<const float4*>(ybase + s * kq + 4 * v))
-                     : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
+  for (int i = threadIdx.x; i < 8 * NT * ks * 16; i += 256) {
+    const int jj = i / (ks * 16), kk = i % (ks * 16);
+    const float v = (jj < nb && kk < kq) ? ybase[(p.t + jj) * kq + kk] : 0.f;
+    split3(v, bpl[0][jj][kk], bpl[1][jj][kk], bpl[2][jj][kk]);
   }
   __syncthreads();
-  // after the halvings lane L holds the sum of row qme; lanes with the low
-  // bits clear store it
-  constexpr int LOWB = RPW == 16 ? 1 : 2;  // lane bits left to butterflies
-  const int qme = (lane >> LOWB) & (RPW - 1);
-  const int64_t s_me = s_first + qme;
-  float* cdst = p.cscr + static_cast<int64_t>(r) * nb * p.scr_ld + s_me;
-  for (int j = 0; j < nb; ++j) {
-    const int64_t t = p.t + j;
-    if (s_first > t) continue;  // warp-uniform
-    float v[RPW];
+  const int64_t t_last = p.t + nb - 1;
+  const int64_t s_base = static_cast<int64_t>(blockIdx.x) * 128 + warp * 16;
+  if (s_base > t_last) return;  // warp-uniform, no barrier follows
+  const int64_t ra = s_base + gid, rb = ra + 8;
+  const float* rowa = ybase + ra * kq;
+  const float* rowb = ybase + rb * kq;
+  const bool va = ra <= t_last, vb = rb <= t_last;
+  float acc[NT][4];
 #pragma unroll
-    for (int q = 0; q < RPW; ++q) v[q] = 0.f;
+  for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-    for (int m = 0; m < MAXV; ++m) {
-      if (32 * m >= nv) break;
-      const float4 yn = ynew[j][lane + 32 * m];
+    for (int q = 0; q < 4; ++q) acc[nt][q] = 0.f;
+  for (int kb0 = 0; kb0 < ks; kb0 += TC_KG) {
+    float2 ld[TC_KG][4];
 #pragma unroll
-      for (int q = 0; q < RPW; ++q)
-        v[q] = fmaf(ld[q][m].x, yn.x,
-                    fmaf(ld[q][m].y, yn.y, fmaf(ld[q][m].z, yn.z, fmaf(ld[q][m].w, yn.w, v[q]))));
+    for (int g = 0; g < TC_KG; ++g) {
+      const int c0 = (kb0 + g) * 16 + tig * 2, c1 = c0 + 8;
+      const float2 z = make_float2(0.f, 0.f);
+      ld[g][0] = (va && c0 < kq) ? __ldcs(reinterpret_cast<const float2*>(rowa + c0)) : z;
+      ld[g][1] = (vb && c0 < kq) ? __ldcs(reinterpret_cast<const float2*>(rowb + c0)) : z;
+      ld[g][2] = (va && c1 < kq) ? __ldcs(reinterpret_cast<const float2*>(rowa + c1)) : z;
+      ld[g][3] = (vb && c1 < kq) ? __ldcs(reinterpret_cast<const float2*>(rowb + c1)) : z;
     }
-    // K6b's xor-butterfly tree by recursive halving: at lane bit o a lane
-    // keeps half its rows and adds the partner's partial of each
 #pragma unroll
-    for (int o = 16, R = RPW; R > 1; o >>= 1, R >>= 1) {
-      const bool hi = (lane & o) != 0;
+    for (int g = 0; g < TC_KG; ++g) {
+      const int kb = kb0 + g;
+      if (kb >= ks) break;
+      uint32_t ah[4], am[4], al[4];
 #pragma unroll
-      for (int i = 0; i < R / 2; ++i) {
-        const float send = hi ? v[i] : v[i + R / 2];
-        const float keep = hi ? v[i + R / 2] : v[i];
-        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+      for (int q = 0; q < 4; ++q) {
+        __nv_bfloat16 h0, m0, l0, h1, m1, l1;
+        split3(ld[g][q].x, h0, m0, l0);
+        split3(ld[g][q].y, h1, m1, l1);
+        ah[q] = pack_bf16(h0, h1);
+        am[q] = pack_bf16(m0, m1);
+        al[q] = pack_bf16(l0, l1);
+      }
+      const int kc = kb * 16 + tig * 2;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int n = nt * 8 + gid;
+        const uint32_t bh0 = *reinterpret_cast<const uint32_t*>(&bpl[0][n][kc]);
+        const uint32_t bh1 = *reinterpret_cast<const uint32_t*>(&bpl[0][n][kc + 8]);
+        const uint32_t bm0 = *reinterpret_cast<const uint32_t*>(&bpl[1][n][kc]);
+        const uint32_t bm1 = *reinterpret_cast<const uint32_t*>(&bpl[1][n][kc + 8]);
+        const uint32_t bl0 = *reinterpret_cast<const uint32_t*>(&bpl[2][n][kc]);
+        const uint32_t bl1 = *reinterpret_cast<const uint32_t*>(&bpl[2][n][kc + 8]);
+        // small products first
+        mma16816(acc[nt], am, bm0, bm1);
+        mma16816(acc[nt], al, bh0, bh1);
+        mma16816(acc[nt], ah, bl0, bl1);
+        mma16816(acc[nt], am, bh0, bh1);
+        mma16816(acc[nt], ah, bm0, bm1);
+        mma16816(acc[nt], ah, bh0, bh1);
       }
     }
-    float a = v[0];
-#pragma unroll
-    for (int o = 1 << (LOWB - 1); o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-    if ((lane & ((1 << LOWB) - 1)) == 0 && s_me <= t) {
-      cdst[static_cast<int64_t>(j) * p.scr_ld] = a;
-      if (p.ccol) p.ccol[static_cast<int64_t>(r) * p.col_ring_stride + s_me * p.col_ld + t] = a;
-    }
   }
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int j = nt * 8 + tig * 2 + (q & 1);
+      const int64_t srow = q < 2 ? ra : rb;
+      const int64_t t = p.t + j;
+      if (j < nb && srow <= t) {
+        p.cscr[(static_cast<int64_t>(r) * nb + j) * p.scr_ld + srow] = acc[nt][q];
+        if (p.ccol) p.ccol[static_cast<int64_t>(r) * p.col_ring_stride + srow * p.col_ld + t] = acc[nt][q];
+      }
+    }
 }
 
 // ---------------------------------------------------------- event history
@@ -893,6 +871,8 @@ __global__ void __launch_bounds__(256, XG_EV_MINB) k_stream_events(StreamParams 
 // order -- exactly the per-push updates of K5s (RAW) / K6b, in push order.
 template <bool RAW>
 __global__ void __launch_bounds__(256) k_stream_fold(StreamParams p) {
+  pdl_wait();  // single pushes: chained after the column kernel
+  pdl_launch_dependents();
   const int r = blockIdx.y;
   const int nb = p.scr_nb;
   const int64_t d = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x;
@@ -974,15 +954,8 @@ cudaError_t launch_stream_batch(const StreamParams& p, int32_t n_rings, bool raw
     // slices per frame multiplied the integer atomics on pacc: 78 us / 16)
     k_stream_proj_acc<<<dim3(n_rings, XG_PZ_BATCH, nb), 256, 0, s>>>(p);
     k_stream_proj_fin<<<dim3(n_rings, nb), 128, 0, s>>>(p);
-    // 16 history rows per warp for k <= 128 (the reduction amortised over
-    // twice the rows), 8 for the two-chunk k <= 256 (registers)
-    if (p.kq / 4 <= 32) {
-      const dim3 grid(static_cast<unsigned>((rows + 16 * 8 - 1) / (16 * 8)), n_rings);
-      k_stream_cmp_batch<1, 16><<<grid, SR_THREADS, 0, s>>>(p);
-    } else {
-      const dim3 grid(static_cast<unsigned>((rows + 8 * 8 - 1) / (8 * 8)), n_rings);
-      k_stream_cmp_batch<2, 8><<<grid, SR_THREADS, 0, s>>>(p);
-    }
+    if (p.kq > TC_KMAX) return cudaErrorInvalidValue;
+    k_stream_cmp_tc<2><<<dim3(static_cast<unsigned>((rows + 127) / 128), n_rings), 256, 0, s>>>(p);
     k_stream_fold<false><<<fold_grid, 256, 0, s>>>(p);
   }
   if (raw) {
@@ -1030,14 +1003,19 @@ cudaError_t launch_stream_raw(const StreamParams& p, int32_t n_rings, int64_t ma
 }
 
 cudaError_t launch_stream_cmp(const StreamParams& p, int32_t n_rings, cudaStream_t s, bool pdl) {
+  // one frame: K6a (projection) -> K6 on tensor cores (one n-tile, scratch
+  // column) -> the lag fold, PDL-chained (p.scr_nb = 1)
+  if (p.kq > TC_KMAX || p.scr_nb != 1) return cudaErrorInvalidValue;
   cudaError_t e = launch_maybe_pdl(k_stream_proj_acc, dim3(n_rings, PZ), dim3(256), s, pdl, p);
   if (e != cudaSuccess) return e;
   e = launch_maybe_pdl(k_stream_proj_fin, dim3(n_rings), dim3(128), s, pdl, p);
   if (e != cudaSuccess) return e;
-  dim3 grid(static_cast<unsigned>((p.t + 1 + SR_ROWS - 1) / SR_ROWS), n_rings);
-  const int nv = p.kq / 4;  // float4 chunks per coefficient row (k <= 256)
-  if (nv <= 32) return launch_maybe_pdl(k_stream_cmp<1>, grid, dim3(SR_THREADS), s, pdl, p);
-  return launch_maybe_pdl(k_stream_cmp<2>, grid, dim3(SR_THREADS), s, pdl, p);
+  const int64_t rows = p.t + 1;
+  e = launch_maybe_pdl(k_stream_cmp_tc<1>, dim3(static_cast<unsigned>((rows + 127) / 128), n_rings),
+                       dim3(256), s, pdl, p);
+  if (e != cudaSuccess) return e;
+  return launch_maybe_pdl(k_stream_fold<false>, dim3(static_cast<unsigned>((rows + 255) / 256), n_rings),
+                          dim3(256), s, pdl, p);
 }
 
 }  // namespace xg

@@ -2896,6 +2896,8 @@ static StreamParams column_params(const xg_stream* s) {
   return sp;
 }
 
+constexpr int kIngestBatchMax = 16;  // frames per push_many batch (kIngestBatch below)
+
 // One push.  slot >= 0: photon-event batch member whose ingest already ran
 // (xg_stream_push_batch), its nonzero lists in batch slot `slot`.
 static int push_one(xg_stream* s, const uint8_t* frame, int on_device, int slot) {
@@ -2974,8 +2976,13 @@ static int push_one(xg_stream* s, const uint8_t* frame, int on_device, int slot)
     XG_CUDA(c, cudaStreamWaitEvent(s->side, s->ev_fork, 0));
   }
   if (s->B) {
+    if (!s->d_cscr)  // the compressed column's scratch (frame plane 0 of a batch's)
+      XG_CUDA(c, dalloc(&s->d_cscr, (size_t)L->rings * kIngestBatchMax * s->tp));
+    sp.cscr = s->d_cscr;
+    sp.scr_ld = s->tp;
+    sp.scr_nb = 1;
     XG_CUDA(c, launch_stream_cmp(sp, L->rings, fork ? s->side : c->stream, pdl));
-    c->launches += 3;
+    c->launches += 4;
   }
   if (raw) {
     if (s->flags & XG_STREAM_SPARSE)
@@ -3006,7 +3013,7 @@ int xg_stream_push(xg_stream* s, const uint8_t* frame, int on_device) {
 // compressed columns with every history row read once for the whole batch,
 // and the lag sums folded in frame order -- bitwise the same as n pushes.
 // XG_STREAM_BATCH_COLUMNS=0 runs each frame's columns as in a push instead.
-constexpr int kIngestBatch = 16;
+constexpr int kIngestBatch = kIngestBatchMax;
 constexpr int kEvL1 = 8;  // level-0 blocks per level-1 event segment
 
 static void free_event_pools(xg_stream* s) {
@@ -3190,7 +3197,7 @@ int xg_stream_push_batch(xg_stream* s, const uint8_t* frames, int64_t n, int on_
         const size_t cols = (size_t)L->rings * kIngestBatch * s->tp;
         if (raw) XG_CUDA(c, dalloc(&s->d_gscr, cols));
         if (s->B) {
-          XG_CUDA(c, dalloc(&s->d_cscr, cols));
+          if (!s->d_cscr) XG_CUDA(c, dalloc(&s->d_cscr, cols));
           XG_CUDA(c, dalloc(&s->d_paccb, (size_t)kIngestBatch * L->rings * 768));
           XG_CUDA(c, cudaMemsetAsync(s->d_paccb, 0,
                                      (size_t)kIngestBatch * L->rings * 768 * sizeof(int32_t),
