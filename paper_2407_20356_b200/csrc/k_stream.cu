@@ -21,7 +21,6 @@
 //   K6b cmp:  C~(s,t) = y_s . y_t over an fp32 copy of the coefficient
 //             history (C~ is fp32-accurate by contract), g2 accumulated like
 //             K5 in f64.  HBM-bound: t * Q * k * 4 B.
-#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -502,51 +501,57 @@ __global__ void __launch_bounds__(32 * SS_W, SS_MINB) k_stream_sparse(StreamPara
 
 // K6: the compressed columns C~(s, t + j) of nb <= 16 new frames (a single
 // push: nb = 1) on tensor cores, grid (ceil((t + nb) / 128), rings), a warp
-// per 16 history rows: mma.sync m16n8k16 bf16 -> fp32 over the history
-// rows (A, from global) and the new rows (B, shared memory), each fp32 value
-// split into three bf16 planes (h + m + l carries its 24 bits) and six of
-// the nine plane products accumulated (the dropped ones are ~2^-24
-// relative, as K4).  Every (s, t) entry depends only on its two rows and the
-// fixed k order, so single pushes (one 8-frame n-tile, one column used) and
-// batches (two n-tiles) give the same bits.  HBM-bound: the history is read
-// once per launch (per 16 frames in a batch).
-__device__ __forceinline__ void split3(float x, __nv_bfloat16& h, __nv_bfloat16& m,
-                                       __nv_bfloat16& l) {
-  h = __float2bfloat16_rn(x);
-  const float r1 = x - __bfloat162float(h);
-  m = __float2bfloat16_rn(r1);
-  l = __float2bfloat16_rn(r1 - __bfloat162float(m));
-}
-__device__ __forceinline__ uint32_t pack_bf16(__nv_bfloat16 lo, __nv_bfloat16 hi) {
-  __nv_bfloat162 v = __halves2bfloat162(lo, hi);
-  return *reinterpret_cast<uint32_t*>(&v);
-}
-__device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0,
-                                         uint32_t b1) {
+// per 16 history rows: mma.sync m16n8k8 tf32 -> fp32 with the history rows
+// as A (straight from global into registers) and the new rows as B (shared
+// memory).  3xTF32: every fp32 value x = big + small with big = x's top 19
+// bits (what the tensor core reads) and small = x - big (exact); big*big +
+// big*small + small*big carry ~2^-21 relative (small*small dropped), the
+// fp32-accurate contract's 1e-5 with margin.  Inside each 8-wide k-step
+// thread q of a quad reads physical columns (2q, 2q+1) as logical k (q,
+// q+4), so its A and B fragments are single 8-byte loads; the set of
+// products summed is unchanged.  Every (s, t) entry depends only on its two
+// rows and the fixed k order, so single pushes (one 8-frame n-tile) and
+// batches (two) give the same bits.  HBM-bound: the history is read once
+// per launch (per 16 frames in a batch).
+__device__ __forceinline__ void mma1688(float (&c)[4], const uint32_t (&a)[4], uint32_t b0,
+                                        uint32_t b1) {
   asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
       "{%8,%9}, {%0,%1,%2,%3};"
       : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
+__device__ __forceinline__ void tf32_split(float x, uint32_t& big, uint32_t& small) {
+  big = __float_as_uint(x) & 0xFFFFE000u;
+  small = __float_as_uint(x - __uint_as_float(big));
+}
 constexpr int CB_MAXNB = 16;
 constexpr int TC_KMAX = 256;
-constexpr int TC_BLD = TC_KMAX + 8;  // padded plane rows: conflict-free B fragment loads
-constexpr int TC_KG = 4;             // k-steps of A loaded before their MMAs
+constexpr int TC_BLD = TC_KMAX + 8;  // plane row pitch: conflict-free 8-byte B loads
+#ifndef XG_TC_KG
+#define XG_TC_KG 4
+#endif
+#ifndef XG_TC_MINB
+#define XG_TC_MINB 4
+#endif
+constexpr int TC_KG = XG_TC_KG;      // k-steps of A loaded before their MMAs
 template <int NT>
-__global__ void __launch_bounds__(256) k_stream_cmp_tc(StreamParams p) {
-  __shared__ __align__(16) __nv_bfloat16 bpl[3][8 * NT][TC_BLD];
+__global__ void __launch_bounds__(256, XG_TC_MINB) k_stream_cmp_tc(StreamParams p) {
+  __shared__ __align__(16) float bsm[2][8 * NT][TC_BLD];  // big / small planes of the new rows
   const int r = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gid = lane >> 2, tig = lane & 3;
   pdl_wait();  // proj_fin: the new rows
   pdl_launch_dependents();
-  const int kq = p.kq, ks = (kq + 15) >> 4, nb = p.scr_nb;
+  const int kq = p.kq, ks = (kq + 7) >> 3, nb = p.scr_nb;
   const float* ybase = p.yf + static_cast<int64_t>(r) * p.y_ld * kq;
-  for (int i = threadIdx.x; i < 8 * NT * ks * 16; i += 256) {
-    const int jj = i / (ks * 16), kk = i % (ks * 16);
+  for (int i = threadIdx.x; i < 8 * NT * ks * 8; i += 256) {
+    const int jj = i / (ks * 8), kk = i % (ks * 8);
     const float v = (jj < nb && kk < kq) ? ybase[(p.t + jj) * kq + kk] : 0.f;
-    split3(v, bpl[0][jj][kk], bpl[1][jj][kk], bpl[2][jj][kk]);
+    uint32_t bg, sm;
+    tf32_split(v, bg, sm);
+    bsm[0][jj][kk] = __uint_as_float(bg);
+    bsm[1][jj][kk] = __uint_as_float(sm);
   }
   __syncthreads();
   const int64_t t_last = p.t + nb - 1;
@@ -556,53 +561,40 @@ __global__ void __launch_bounds__(256) k_stream_cmp_tc(StreamParams p) {
   const float* rowa = ybase + ra * kq;
   const float* rowb = ybase + rb * kq;
   const bool va = ra <= t_last, vb = rb <= t_last;
-  float acc[NT][4];
+  // two accumulator chains per n-tile (the cross products; big * big),
+  // summed at the end
+  float acc[NT][4], acs[NT][4];
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-    for (int q = 0; q < 4; ++q) acc[nt][q] = 0.f;
+    for (int q = 0; q < 4; ++q) acc[nt][q] = acs[nt][q] = 0.f;
   for (int kb0 = 0; kb0 < ks; kb0 += TC_KG) {
-    float2 ld[TC_KG][4];
+    float2 la[TC_KG], lb[TC_KG];
 #pragma unroll
     for (int g = 0; g < TC_KG; ++g) {
-      const int c0 = (kb0 + g) * 16 + tig * 2, c1 = c0 + 8;
+      const int c = (kb0 + g) * 8 + 2 * tig;
       const float2 z = make_float2(0.f, 0.f);
-      ld[g][0] = (va && c0 < kq) ? __ldcs(reinterpret_cast<const float2*>(rowa + c0)) : z;
-      ld[g][1] = (vb && c0 < kq) ? __ldcs(reinterpret_cast<const float2*>(rowb + c0)) : z;
-      ld[g][2] = (va && c1 < kq) ? __ldcs(reinterpret_cast<const float2*>(rowa + c1)) : z;
-      ld[g][3] = (vb && c1 < kq) ? __ldcs(reinterpret_cast<const float2*>(rowb + c1)) : z;
+      la[g] = (va && c < kq) ? __ldcs(reinterpret_cast<const float2*>(rowa + c)) : z;
+      lb[g] = (vb && c < kq) ? __ldcs(reinterpret_cast<const float2*>(rowb + c)) : z;
     }
 #pragma unroll
     for (int g = 0; g < TC_KG; ++g) {
       const int kb = kb0 + g;
       if (kb >= ks) break;
-      uint32_t ah[4], am[4], al[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        __nv_bfloat16 h0, m0, l0, h1, m1, l1;
-        split3(ld[g][q].x, h0, m0, l0);
-        split3(ld[g][q].y, h1, m1, l1);
-        ah[q] = pack_bf16(h0, h1);
-        am[q] = pack_bf16(m0, m1);
-        al[q] = pack_bf16(l0, l1);
-      }
-      const int kc = kb * 16 + tig * 2;
+      uint32_t ab[4], as[4];
+      tf32_split(la[g].x, ab[0], as[0]);  // (row gid,     logical k q)
+      tf32_split(lb[g].x, ab[1], as[1]);  // (row gid + 8, logical k q)
+      tf32_split(la[g].y, ab[2], as[2]);  // (row gid,     logical k q + 4)
+      tf32_split(lb[g].y, ab[3], as[3]);  // (row gid + 8, logical k q + 4)
+      const int c = kb * 8 + 2 * tig;
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
         const int n = nt * 8 + gid;
-        const uint32_t bh0 = *reinterpret_cast<const uint32_t*>(&bpl[0][n][kc]);
-        const uint32_t bh1 = *reinterpret_cast<const uint32_t*>(&bpl[0][n][kc + 8]);
-        const uint32_t bm0 = *reinterpret_cast<const uint32_t*>(&bpl[1][n][kc]);
-        const uint32_t bm1 = *reinterpret_cast<const uint32_t*>(&bpl[1][n][kc + 8]);
-        const uint32_t bl0 = *reinterpret_cast<const uint32_t*>(&bpl[2][n][kc]);
-        const uint32_t bl1 = *reinterpret_cast<const uint32_t*>(&bpl[2][n][kc + 8]);
-        // small products first
-        mma16816(acc[nt], am, bm0, bm1);
-        mma16816(acc[nt], al, bh0, bh1);
-        mma16816(acc[nt], ah, bl0, bl1);
-        mma16816(acc[nt], am, bh0, bh1);
-        mma16816(acc[nt], ah, bm0, bm1);
-        mma16816(acc[nt], ah, bh0, bh1);
+        const float2 bb = *reinterpret_cast<const float2*>(&bsm[0][n][c]);
+        const float2 bs = *reinterpret_cast<const float2*>(&bsm[1][n][c]);
+        mma1688(acs[nt], as, __float_as_uint(bb.x), __float_as_uint(bb.y));
+        mma1688(acs[nt], ab, __float_as_uint(bs.x), __float_as_uint(bs.y));
+        mma1688(acc[nt], ab, __float_as_uint(bb.x), __float_as_uint(bb.y));
       }
     }
   }
@@ -610,14 +602,30 @@ __global__ void __launch_bounds__(256) k_stream_cmp_tc(StreamParams p) {
   for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
+      const float v = acc[nt][q] + acs[nt][q];
       const int j = nt * 8 + tig * 2 + (q & 1);
       const int64_t srow = q < 2 ? ra : rb;
       const int64_t t = p.t + j;
       if (j < nb && srow <= t) {
-        p.cscr[(static_cast<int64_t>(r) * nb + j) * p.scr_ld + srow] = acc[nt][q];
-        if (p.ccol) p.ccol[static_cast<int64_t>(r) * p.col_ring_stride + srow * p.col_ld + t] = acc[nt][q];
+        p.cscr[(static_cast<int64_t>(r) * nb + j) * p.scr_ld + srow] = v;
+        if (p.ccol) p.ccol[static_cast<int64_t>(r) * p.col_ring_stride + srow * p.col_ld + t] = v;
       }
     }
+}
+
+template <int NT>
+static cudaError_t launch_cmp_tc(const StreamParams& p, int32_t n_rings, cudaStream_t s, bool pdl) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>((p.t + p.scr_nb + 127) / 128), n_rings);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k_stream_cmp_tc<NT>, p);
 }
 
 // ---------------------------------------------------------- event history
@@ -955,7 +963,8 @@ cudaError_t launch_stream_batch(const StreamParams& p, int32_t n_rings, bool raw
     k_stream_proj_acc<<<dim3(n_rings, XG_PZ_BATCH, nb), 256, 0, s>>>(p);
     k_stream_proj_fin<<<dim3(n_rings, nb), 128, 0, s>>>(p);
     if (p.kq > TC_KMAX) return cudaErrorInvalidValue;
-    k_stream_cmp_tc<2><<<dim3(static_cast<unsigned>((rows + 127) / 128), n_rings), 256, 0, s>>>(p);
+    const cudaError_t e = launch_cmp_tc<2>(p, n_rings, s, false);
+    if (e != cudaSuccess) return e;
     k_stream_fold<false><<<fold_grid, 256, 0, s>>>(p);
   }
   if (raw) {
@@ -1011,8 +1020,7 @@ cudaError_t launch_stream_cmp(const StreamParams& p, int32_t n_rings, cudaStream
   e = launch_maybe_pdl(k_stream_proj_fin, dim3(n_rings), dim3(128), s, pdl, p);
   if (e != cudaSuccess) return e;
   const int64_t rows = p.t + 1;
-  e = launch_maybe_pdl(k_stream_cmp_tc<1>, dim3(static_cast<unsigned>((rows + 127) / 128), n_rings),
-                       dim3(256), s, pdl, p);
+  e = launch_cmp_tc<1>(p, n_rings, s, pdl);
   if (e != cudaSuccess) return e;
   return launch_maybe_pdl(k_stream_fold<false>, dim3(static_cast<unsigned>((rows + 255) / 256), n_rings),
                           dim3(256), s, pdl, p);
