@@ -27,7 +27,7 @@ ONLY="store+fused g2" $NCU -k regex:"k_project" -c 1 -o $O/${R}_project python t
 DEPTH=18960 K=128 ncu --metrics gpu__time_duration.sum --clock-control none --csv -s 9000 -c 300 \
     --log-file $O/${R}_c3_launches.csv python tools/time_batch.py > /dev/null 2>&1
 DEPTH=18960 $NCU -k regex:"k_stream_events" -s 1500 -c 1 -o $O/${R}_stream_events python tools/time_batch.py > /dev/null 2>&1
-DEPTH=18960 K=128 RAW=0 $NCU -k regex:"k_stream_cmp_batch" -s 1190 -c 1 -o $O/${R}_stream_cmp_batch python tools/time_batch.py > /dev/null 2>&1
+DEPTH=18960 K=128 RAW=0 $NCU -k regex:"k_stream_cmp_tc" -s 1190 -c 1 -o $O/${R}_stream_cmp_tc python tools/time_batch.py > /dev/null 2>&1
 $NCU -k regex:"k_stream_sparse" -s 8200 -c 1 -o $O/${R}_stream_sparse python tools/prof_r2.py c3single > /dev/null 2>&1
 $NCU -k regex:"k_gram2" -s 1 -c 1 -o $O/${R}_c4_gram python tools/prof_r2.py c4 > /dev/null 2>&1
 $NCU -k regex:"k_ingest" -s 2 -c 1 -o $O/${R}_c5_ingest python tools/prof_r2.py c5 64 > /dev/null 2>&1

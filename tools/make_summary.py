@@ -31,7 +31,7 @@ def main():
                   "# overlap on two streams live)",
                   run("tools/launches.py", c3).rstrip(), ""]
     for name in ("ingest", "gram_raw", "project", "gram_cmp", "stream_dense", "stream_sparse",
-                 "stream_cmp", "stream_events", "stream_cmp_batch", "c4_gram", "c5_ingest",
+                 "stream_cmp", "stream_events", "stream_cmp_tc", "c4_gram", "c5_ingest",
                  "c5_project"):
         rep = os.path.join(PROF, f"{rnd}_{name}.ncu-rep")
         if not os.path.exists(rep):

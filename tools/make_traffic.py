@@ -20,7 +20,7 @@ REPS = {
     "k_gram2<1>": ("gram_cmp", "C2 k=64: f32 C~ upper triangle + bf16 planes", 1124335616),
     "k_stream_sparse": ("stream_sparse", "C3 single push at depth 8200: nnz x t history bytes", None),
     "k_stream_events": ("stream_events", "C3 push_many: one K5e launch (16 frames x 64 rings x the level's segments)", None),
-    "k_stream_cmp_batch": ("stream_cmp_batch", "C3 push_many k=128: every coefficient row read once for 16 frames", None),
+    "k_stream_cmp_tc": ("stream_cmp_tc", "C3 push_many k=128: every coefficient row read once for 16 frames (3xTF32 mma)", None),
     "k_gram2<0> C4": ("c4_gram", "C4: T=16384, 1024^2, Q=100", None),
     "k_ingest C5": ("c5_ingest", "C5 chunk of 4096 frames", None),
     "k_project C5": ("c5_project", "C5 chunk of 4096 frames, k=64", None),
