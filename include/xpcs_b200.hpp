@@ -227,6 +227,16 @@ class Series {
   void ttc_raw_host(const uint8_t* frames, int64_t n, uint32_t flags = 0) {
     L_.ctx().check(xg_series_ttc_raw_host(h_, frames, n, flags));
   }
+  // Photon-event frames (CSR by frame: offsets[n + 1], raster pixel,
+  // count): the same series as load() of the dense frames
+  void load_events(const int64_t* frame_off, const int32_t* pix, const uint8_t* val, int64_t n,
+                   bool on_device = false) {
+    L_.ctx().check(xg_series_load_events(h_, frame_off, pix, val, n, on_device ? 1 : 0));
+  }
+  void ttc_raw_events_host(const int64_t* frame_off, const int32_t* pix, const uint8_t* val,
+                           int64_t n, uint32_t flags = 0) {
+    L_.ctx().check(xg_series_ttc_raw_events_host(h_, frame_off, pix, val, n, flags));
+  }
   void compress(const Basis& b, uint32_t flags = 0) { L_.ctx().check(xg_compress(h_, b.get(), flags)); }
   void ttc_compressed(uint32_t flags = 0) { L_.ctx().check(xg_ttc_compressed(h_, flags)); }
   int64_t frames() const { return xg_series_frames(h_); }
