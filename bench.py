@@ -787,7 +787,7 @@ def run_c3(E):
                           "ms_per_frame_tail": one_tail_ms,
                           "what": "push() per frame from Python (host call per frame inside the "
                                   "timed region): ingest, dense pixel-major raw column (K5s), "
-                                  "K6a/K6b compressed column"},
+                                  "K6a projection + K6 tensor-core compressed column"},
         "nnz_per_frame": nnz, "basis": bsrc,
         "tail_bytes_per_frame": {"raw_nnz_history": raw_bytes_tail,
                                  "compressed_history": cmp_bytes_tail,

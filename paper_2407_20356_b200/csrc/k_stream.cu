@@ -195,6 +195,73 @@ __global__ void __launch_bounds__(128) k_stream_proj_fin(StreamParams p) {
   for (int j = threadIdx.x; j < p.n_digits * p.k; j += blockDim.x) pa[j] = 0;
 }
 
+// K6b (single pushes): the new frame's C~ column, grid (ceil((t+1)/SR_ROWS),
+// rings), a warp per 8 history rows, SIMT fp32 (per-lane fmaf chains, an
+// xor-butterfly across lanes), the lag sums updated in place.  A single
+// column is HBM-bound and K6b streams it at ~0.9 of HBM; the tensor-core K6
+// below (batches) reached ~0.7 for one column.  The two differ in rounding
+// within fp32 (both within the 1e-5 compressed contract).
+template <int MAXV>
+__global__ void __launch_bounds__(SR_THREADS, 4) k_stream_cmp(StreamParams p) {
+  // fp32 coefficient history (C~ is fp32-accurate by contract), rows padded
+  // to kq = k rounded up to 4 (zero pad): lane L holds float4 chunks L, L+32,
+  // ... of the new row; a warp's 8 history rows are loaded (16 B per lane per
+  // row) before any arithmetic; fp32 products summed over k, lags in f64
+  const int r = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  pdl_wait();  // proj_fin(t): y_t
+  pdl_launch_dependents();
+  const int kq = p.kq, nv = kq >> 2;
+  const float* ybase = p.yf + static_cast<int64_t>(r) * p.y_ld * kq;
+  float4 yn[MAXV];
+#pragma unroll
+  for (int m = 0; m < MAXV; ++m) {
+    const int v = lane + 32 * m;
+    yn[m] = v < nv ? *reinterpret_cast<const float4*>(ybase + p.t * kq + 4 * v)
+                   : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  const double inv_t = p.inv[static_cast<int64_t>(r) * p.inv_ld + p.t];
+  constexpr int RPW = SR_ROWS / (SR_THREADS / 32);
+  const int64_t s_first = static_cast<int64_t>(blockIdx.x) * SR_ROWS + warp * RPW;
+  float part[RPW];
+#pragma unroll
+  for (int q = 0; q < RPW; ++q) part[q] = 0.f;
+#pragma unroll
+  for (int m = 0; m < MAXV; ++m) {
+    if (32 * m >= nv) break;
+    const int v = lane + 32 * m;
+    float4 ld[RPW];
+#pragma unroll
+    for (int q = 0; q < RPW; ++q) {
+      const int64_t s = s_first + q;
+      ld[q] = (v < nv && s <= p.t)
+                  ? __ldcs(reinterpret_cast<const float4*>(ybase + s * kq + 4 * v))
+                  : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int q = 0; q < RPW; ++q)
+      part[q] = fmaf(ld[q].x, yn[m].x,
+                     fmaf(ld[q].y, yn[m].y, fmaf(ld[q].z, yn[m].z, fmaf(ld[q].w, yn[m].w, part[q]))));
+  }
+  float mine = 0.f;
+#pragma unroll
+  for (int q = 0; q < RPW; ++q) {
+    float a = part[q];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (lane == q) mine = a;
+  }
+  const int64_t s = s_first + lane;
+  if (lane < RPW && s <= p.t) {
+    const double acc = mine;
+    const double inv_s = p.inv[static_cast<int64_t>(r) * p.inv_ld + s];
+    const int64_t gi = static_cast<int64_t>(r) * p.g2_ld + (p.t - s);
+    p.cg2sum[gi] += acc;
+    p.cg2cnt[gi] += (inv_s != 0.0 && inv_t != 0.0) ? 1 : 0;
+    if (p.ccol) p.ccol[static_cast<int64_t>(r) * p.col_ring_stride + s * p.col_ld + p.t] = mine;
+  }
+}
+
 }  // namespace
 
 // K1s: one warp per 128-column block of the ring-major row (blocks never
@@ -499,20 +566,18 @@ __global__ void __launch_bounds__(32 * SS_W, SS_MINB) k_stream_sparse(StreamPara
   if (!BATCH && p.pdl_wait_end) pdl_wait();  // cmp(t) has completed too (see above)
 }
 
-// K6: the compressed columns C~(s, t + j) of nb <= 16 new frames (a single
-// push: nb = 1) on tensor cores, grid (ceil((t + nb) / 128), rings), a warp
-// per 16 history rows: mma.sync m16n8k8 tf32 -> fp32 with the history rows
-// as A (straight from global into registers) and the new rows as B (shared
-// memory).  3xTF32: every fp32 value x = big + small with big = x's top 19
-// bits (what the tensor core reads) and small = x - big (exact); big*big +
-// big*small + small*big carry ~2^-21 relative (small*small dropped), the
-// fp32-accurate contract's 1e-5 with margin.  Inside each 8-wide k-step
-// thread q of a quad reads physical columns (2q, 2q+1) as logical k (q,
-// q+4), so its A and B fragments are single 8-byte loads; the set of
-// products summed is unchanged.  Every (s, t) entry depends only on its two
-// rows and the fixed k order, so single pushes (one 8-frame n-tile) and
-// batches (two) give the same bits.  HBM-bound: the history is read once
-// per launch (per 16 frames in a batch).
+// K6 (batches): the compressed columns C~(s, t + j) of the nb <= 16 frames
+// of a push_many batch on tensor cores, grid (ceil((t + nb) / 128), rings),
+// a warp per 16 history rows: mma.sync m16n8k8 tf32 -> fp32, the history
+// rows as A (straight from global into registers), the new rows as B
+// (shared memory).  3xTF32: every fp32 value x = big + small with big = x's
+// top 19 bits (what the tensor core reads) and small = x - big (exact);
+// big*big + big*small + small*big carry ~2^-21 relative (small*small
+// dropped), the fp32-accurate contract's 1e-5 with margin.  Inside each
+// 8-wide k-step thread q of a quad reads physical columns (2q, 2q+1) as
+// logical k (q, q+4), so its A and B fragments are single 8-byte loads (the
+// set of products summed is unchanged).  The history is read once per 16
+// frames; the entries go to scratch columns for the fold.
 __device__ __forceinline__ void mma1688(float (&c)[4], const uint32_t (&a)[4], uint32_t b0,
                                         uint32_t b1) {
   asm volatile(
@@ -534,8 +599,8 @@ constexpr int TC_BLD = TC_KMAX + 8;  // plane row pitch: conflict-free 8-byte B 
 #ifndef XG_TC_MINB
 #define XG_TC_MINB 4
 #endif
-constexpr int TC_KG = XG_TC_KG;      // k-steps of A loaded before their MMAs
-template <int NT>
+constexpr int TC_KG = XG_TC_KG;  // k-steps of A loaded before their MMAs
+template <int NT, int KG>
 __global__ void __launch_bounds__(256, XG_TC_MINB) k_stream_cmp_tc(StreamParams p) {
   __shared__ __align__(16) float bsm[2][8 * NT][TC_BLD];  // big / small planes of the new rows
   const int r = blockIdx.y;
@@ -568,17 +633,17 @@ __global__ void __launch_bounds__(256, XG_TC_MINB) k_stream_cmp_tc(StreamParams 
   for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
     for (int q = 0; q < 4; ++q) acc[nt][q] = acs[nt][q] = 0.f;
-  for (int kb0 = 0; kb0 < ks; kb0 += TC_KG) {
-    float2 la[TC_KG], lb[TC_KG];
+  for (int kb0 = 0; kb0 < ks; kb0 += KG) {
+    float2 la[KG], lb[KG];
 #pragma unroll
-    for (int g = 0; g < TC_KG; ++g) {
+    for (int g = 0; g < KG; ++g) {
       const int c = (kb0 + g) * 8 + 2 * tig;
       const float2 z = make_float2(0.f, 0.f);
       la[g] = (va && c < kq) ? __ldcs(reinterpret_cast<const float2*>(rowa + c)) : z;
       lb[g] = (vb && c < kq) ? __ldcs(reinterpret_cast<const float2*>(rowb + c)) : z;
     }
 #pragma unroll
-    for (int g = 0; g < TC_KG; ++g) {
+    for (int g = 0; g < KG; ++g) {
       const int kb = kb0 + g;
       if (kb >= ks) break;
       uint32_t ab[4], as[4];
@@ -625,7 +690,7 @@ static cudaError_t launch_cmp_tc(const StreamParams& p, int32_t n_rings, cudaStr
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = pdl ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, k_stream_cmp_tc<NT>, p);
+  return cudaLaunchKernelEx(&cfg, k_stream_cmp_tc<NT, TC_KG>, p);
 }
 
 // ---------------------------------------------------------- event history
@@ -1012,18 +1077,15 @@ cudaError_t launch_stream_raw(const StreamParams& p, int32_t n_rings, int64_t ma
 }
 
 cudaError_t launch_stream_cmp(const StreamParams& p, int32_t n_rings, cudaStream_t s, bool pdl) {
-  // one frame: K6a (projection) -> K6 on tensor cores (one n-tile, scratch
-  // column) -> the lag fold, PDL-chained (p.scr_nb = 1)
-  if (p.kq > TC_KMAX || p.scr_nb != 1) return cudaErrorInvalidValue;
+  // one frame: K6a (projection) -> K6b (column + lag sums), PDL-chained
   cudaError_t e = launch_maybe_pdl(k_stream_proj_acc, dim3(n_rings, PZ), dim3(256), s, pdl, p);
   if (e != cudaSuccess) return e;
   e = launch_maybe_pdl(k_stream_proj_fin, dim3(n_rings), dim3(128), s, pdl, p);
   if (e != cudaSuccess) return e;
-  const int64_t rows = p.t + 1;
-  e = launch_cmp_tc<1>(p, n_rings, s, pdl);
-  if (e != cudaSuccess) return e;
-  return launch_maybe_pdl(k_stream_fold<false>, dim3(static_cast<unsigned>((rows + 255) / 256), n_rings),
-                          dim3(256), s, pdl, p);
+  dim3 grid(static_cast<unsigned>((p.t + 1 + SR_ROWS - 1) / SR_ROWS), n_rings);
+  const int nv = p.kq / 4;  // float4 chunks per coefficient row (k <= 256)
+  if (nv <= 32) return launch_maybe_pdl(k_stream_cmp<1>, grid, dim3(SR_THREADS), s, pdl, p);
+  return launch_maybe_pdl(k_stream_cmp<2>, grid, dim3(SR_THREADS), s, pdl, p);
 }
 
 }  // namespace xg

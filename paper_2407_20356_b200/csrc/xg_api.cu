@@ -2976,13 +2976,9 @@ static int push_one(xg_stream* s, const uint8_t* frame, int on_device, int slot)
     XG_CUDA(c, cudaStreamWaitEvent(s->side, s->ev_fork, 0));
   }
   if (s->B) {
-    if (!s->d_cscr)  // the compressed column's scratch (frame plane 0 of a batch's)
-      XG_CUDA(c, dalloc(&s->d_cscr, (size_t)L->rings * kIngestBatchMax * s->tp));
-    sp.cscr = s->d_cscr;
-    sp.scr_ld = s->tp;
-    sp.scr_nb = 1;
+    sp.scr_nb = 1;  // one frame: K6 adds its column to the lag sums itself
     XG_CUDA(c, launch_stream_cmp(sp, L->rings, fork ? s->side : c->stream, pdl));
-    c->launches += 4;
+    c->launches += 3;
   }
   if (raw) {
     if (s->flags & XG_STREAM_SPARSE)
@@ -3011,7 +3007,8 @@ int xg_stream_push(xg_stream* s, const uint8_t* frame, int on_device) {
 // front of every column), then form the batch's columns together
 // (launch_stream_batch): the raw columns of all its frames in one grid, the
 // compressed columns with every history row read once for the whole batch,
-// and the lag sums folded in frame order -- bitwise the same as n pushes.
+// and the lag sums folded in frame order -- the raw results bitwise those of
+// n pushes, C~ to fp32 rounding (K6 on tensor cores vs the pushes' K6b).
 // XG_STREAM_BATCH_COLUMNS=0 runs each frame's columns as in a push instead.
 constexpr int kIngestBatch = kIngestBatchMax;
 constexpr int kEvL1 = 8;  // level-0 blocks per level-1 event segment

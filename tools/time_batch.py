@@ -4,7 +4,8 @@ it under `ncu --metrics gpu__time_duration.sum` for the per-kernel split.
   DEPTH (8192)  history frames before the timed window
   N (256)       frames timed
   K (0)         rank of a random orthonormal basis (0: raw only)
-  RAW (1)       raw columns on"""
+  RAW (1)       raw columns on
+  SINGLE (0)    1: the timed window pushed one frame per push() call"""
 import os
 import sys
 
@@ -43,11 +44,16 @@ def main():
     torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record(st)
-    s.push_many(frames[depth:])
+    if os.environ.get("SINGLE", "0") == "1":
+        for i in range(depth, T):
+            s.push(frames[i])
+    else:
+        s.push_many(frames[depth:])
     b.record(st)
     torch.cuda.synchronize()
     ms = a.elapsed_time(b) / n
-    print(f"depth {depth} k {k} raw {raw}: {ms * 1e3:.1f} us/frame ({1e3 / ms:.0f} frames/s)")
+    mode = "push" if os.environ.get("SINGLE", "0") == "1" else "push_many"
+    print(f"depth {depth} k {k} raw {raw} {mode}: {ms * 1e3:.1f} us/frame ({1e3 / ms:.0f} frames/s)")
 
 
 if __name__ == "__main__":
