@@ -108,7 +108,10 @@ constexpr int PZ = 8;
 #define XG_PZ_BATCH 2
 #endif
 constexpr int PA_MAXW = 6;  // 32-bit digit words per lane: 3 digits x k <= 768
-constexpr int PA_U = 4;     // pixels in flight per warp
+#ifndef XG_PA_U
+#define XG_PA_U 4
+#endif
+constexpr int PA_U = XG_PA_U;  // pixels in flight per warp
 __global__ void __launch_bounds__(256) k_stream_proj_acc(StreamParams p) {
   // warp w of the CTA takes nonzeros zb + w, zb + w + 8, ...; lane L holds
   // the 32-bit digit words L, L + 32, ... of the pixel's row (4 digits per
