@@ -186,7 +186,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "50"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -196,6 +196,20 @@ class ClockSampler:
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
+
+    def wait_first(self, timeout: float = 10.0):
+        """Block until nvidia-smi has produced a sample (its start-up can take
+        longer than a short timed region), then mark where the region starts."""
+        t0 = time.time()
+        while self.proc and not self.lines and time.time() - t0 < timeout:
+            time.sleep(0.01)
+        self.i0 = max(0, len(self.lines) - 1)  # the last sample before the region
+
+    def settle(self, timeout: float = 0.5):
+        """After the region: wait for one sample taken after it ended."""
+        n, t0 = len(self.lines), time.time()
+        while self.proc and len(self.lines) <= n and time.time() - t0 < timeout:
+            time.sleep(0.005)
 
     def stop(self):
         if not self.proc:
@@ -207,7 +221,7 @@ class ClockSampler:
             self.proc.kill()
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        for ln in self.lines[getattr(self, "i0", 0):]:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 7:
                 continue
@@ -220,7 +234,9 @@ class ClockSampler:
                 if v.lower().startswith("active"):
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "window": "nvidia-smi every 20 ms, from the last sample before the timed "
+                          "steps to the first after them"}
 
 
 def measure_int8_peak(torch, dev):
@@ -385,7 +401,7 @@ def time_raw(E, sh, series, frames, steps, warmup, clocks=False):
     if clocks:
         sampler = ClockSampler(E.local)
         sampler.start()
-        time.sleep(0.15)
+        sampler.wait_first()
     E.barrier()
     E.torch.cuda.synchronize()
     l0 = E.ctx.kernel_launches
@@ -396,6 +412,8 @@ def time_raw(E, sh, series, frames, steps, warmup, clocks=False):
     b.record(E.stream)
     E.torch.cuda.synchronize()
     E.barrier()
+    if sampler:
+        sampler.settle()
     clk = sampler.stop() if sampler else None
     launches = E.ctx.kernel_launches - l0
     E.ctx.synchronize()
