@@ -1022,8 +1022,8 @@ def main():
         return
 
     E = Env(args)
-    if args.only == "c3":  # development: the streaming section alone
-        print(json.dumps(run_c3(E)), flush=True)
+    if args.only in ("c3", "c5"):  # development: one section alone
+        print(json.dumps(run_c3(E) if args.only == "c3" else run_c5(E)), flush=True)
         return
     line = {"metric": METRIC, "value": None, "unit": "frames/s", "n_gpus": E.world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
