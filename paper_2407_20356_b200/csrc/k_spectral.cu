@@ -19,7 +19,8 @@
 //
 // Everything is f64 (the FFT's error is ~log2(L) eps of sum |y|^2, far
 // inside the compressed path's 1e-5 contract; C~ itself is only
-// fp32-accurate).  The FFT: radix-2, 8192 points in shared memory (128 KB),
+// fp32-accurate).  The FFT: radix-4 passes (+ one radix-2), 8192 points in
+// padded shared memory (148 KB),
 // 1024 threads, twiddles from a table built once with sincospi.
 #include <cuda_runtime.h>
 
@@ -43,22 +44,59 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
 
 __device__ __forceinline__ int bitrev13(int j) { return static_cast<int>(__brev(static_cast<unsigned>(j)) >> (32 - SPLOG)); }
 
-// In-place radix-2 DIT over shared memory (input already in bit-reversed
-// order).  inverse: conjugate twiddles (no 1/L scaling here).
+// Shared-memory slot of element i: one pad slot per 8 elements and one per
+// 256, so the radix-4 passes' strided quads (stride 1, 4, 16 elements) and
+// the bit-reversed scatter each hit all 32 banks (an unpadded layout had 2-
+// to 32-way conflicts: L1 94% busy, 0.87 G conflicts per C5 launch).
+__device__ __forceinline__ int pidx(int i) { return i + (i >> 3) + (i >> 8); }
+constexpr int SPL_PAD = SPL + SPL / 8 + SPL / 256;
+
+// In-place DIT over shared memory (input already in bit-reversed order):
+// stages s and s + 1 fused into radix-4 passes (the two radix-2 stages'
+// exact operations, half the barriers and shared-memory round trips), the
+// last stage radix-2.  inverse: conjugate twiddles (no 1/L scaling here).
 __device__ void fft_smem(double2* x, const double2* __restrict__ tw, bool inverse) {
-  for (int s = 1; s <= SPLOG; ++s) {
+  int s = 1;
+  for (; s + 1 <= SPLOG; s += 2) {
+    const int h = 1 << (s - 1);
+    const int st1 = SPL >> s, st2 = SPL >> (s + 1);
+    __syncthreads();
+    for (int q = threadIdx.x; q < SPL / 4; q += SPT) {
+      const int grp = q >> (s - 1), pos = q & (h - 1);
+      const int i0 = (grp << (s + 1)) + pos;
+      double2 w1 = __ldg(tw + pos * st1), w2a = __ldg(tw + pos * st2), w2b = __ldg(tw + (pos + h) * st2);
+      if (inverse) {
+        w1.y = -w1.y;
+        w2a.y = -w2a.y;
+        w2b.y = -w2b.y;
+      }
+      const double2 x0 = x[pidx(i0)], x1 = x[pidx(i0 + h)], x2 = x[pidx(i0 + 2 * h)],
+                    x3 = x[pidx(i0 + 3 * h)];
+      // stage s: (i0, i0 + h) and (i0 + 2h, i0 + 3h), twiddle w1
+      const double2 t1 = cmul(w1, x1), t3 = cmul(w1, x3);
+      const double2 a = make_double2(x0.x + t1.x, x0.y + t1.y), b = make_double2(x0.x - t1.x, x0.y - t1.y);
+      const double2 c = make_double2(x2.x + t3.x, x2.y + t3.y), d = make_double2(x2.x - t3.x, x2.y - t3.y);
+      // stage s + 1: (i0, i0 + 2h) twiddle w2a, (i0 + h, i0 + 3h) twiddle w2b
+      const double2 tc = cmul(w2a, c), td = cmul(w2b, d);
+      x[pidx(i0)] = make_double2(a.x + tc.x, a.y + tc.y);
+      x[pidx(i0 + 2 * h)] = make_double2(a.x - tc.x, a.y - tc.y);
+      x[pidx(i0 + h)] = make_double2(b.x + td.x, b.y + td.y);
+      x[pidx(i0 + 3 * h)] = make_double2(b.x - td.x, b.y - td.y);
+    }
+  }
+  for (; s <= SPLOG; ++s) {  // the remaining radix-2 stage
     const int half = 1 << (s - 1);
-    const int step = SPL >> s;  // twiddle stride
+    const int step = SPL >> s;
     __syncthreads();
     for (int bf = threadIdx.x; bf < SPL / 2; bf += SPT) {
       const int grp = bf >> (s - 1), pos = bf & (half - 1);
       const int i = (grp << s) + pos, j = i + half;
       double2 w = __ldg(tw + pos * step);
       if (inverse) w.y = -w.y;
-      const double2 t = cmul(w, x[j]);
-      const double2 u = x[i];
-      x[i] = make_double2(u.x + t.x, u.y + t.y);
-      x[j] = make_double2(u.x - t.x, u.y - t.y);
+      const double2 t = cmul(w, x[pidx(j)]);
+      const double2 u = x[pidx(i)];
+      x[pidx(i)] = make_double2(u.x + t.x, u.y + t.y);
+      x[pidx(j)] = make_double2(u.x - t.x, u.y - t.y);
     }
   }
   __syncthreads();
@@ -93,11 +131,11 @@ __global__ void __launch_bounds__(SPT) k_spec_fwd(SpecParams p) {
     }
   }
 #pragma unroll
-  for (int u = 0; u < PER; ++u) xs[bitrev13(threadIdx.x + u * SPT)] = z[u];
-  for (int j = SPEC_B + threadIdx.x; j < SPL; j += SPT) xs[bitrev13(j)] = make_double2(0.0, 0.0);
+  for (int u = 0; u < PER; ++u) xs[pidx(bitrev13(threadIdx.x + u * SPT))] = z[u];
+  for (int j = SPEC_B + threadIdx.x; j < SPL; j += SPT) xs[pidx(bitrev13(j))] = make_double2(0.0, 0.0);
   fft_smem(xs, p.tw, false);
   double2* out = p.spec + ((static_cast<int64_t>(r) * p.nb + a) * p.nm + m) * SPL;
-  for (int j = threadIdx.x; j < SPL; j += SPT) out[j] = xs[j];
+  for (int j = threadIdx.x; j < SPL; j += SPT) out[j] = xs[pidx(j)];
 }
 
 // grid (block pairs, rings): the pair's cross-spectrum summed over the
@@ -121,11 +159,11 @@ __global__ void __launch_bounds__(SPT) k_spec_pair(SpecParams p) {
       acc.x += u.x * v.x + u.y * v.y;  // conj(u) v
       acc.y += u.x * v.y - u.y * v.x;
     }
-    xs[bitrev13(f)] = acc;
+    xs[pidx(bitrev13(f))] = acc;
   }
   fft_smem(xs, p.tw, true);
   double* out = p.corr + (static_cast<int64_t>(r) * p.npairs + pr) * SPL;
-  for (int j = threadIdx.x; j < SPL; j += SPT) out[j] = xs[j].x * (1.0 / SPL);
+  for (int j = threadIdx.x; j < SPL; j += SPT) out[j] = xs[pidx(j)].x * (1.0 / SPL);
 }
 
 // grid (ceil(n / 256), rings): lag d sums the block pairs (a, a + D) with
@@ -188,7 +226,7 @@ cudaError_t launch_spectral_g2(SpecParams p, void* scratch, cudaStream_t s) {
   p.spec = reinterpret_cast<double2*>(base + static_cast<size_t>(SPL / 2) * 16);
   p.corr = reinterpret_cast<double*>(reinterpret_cast<uint8_t*>(p.spec) +
                                      static_cast<size_t>(p.n_rings) * p.nb * p.nm * SPL * 16);
-  const size_t smem = static_cast<size_t>(SPL) * sizeof(double2);
+  const size_t smem = static_cast<size_t>(SPL_PAD) * sizeof(double2);
   cudaError_t e = cudaFuncSetAttribute(k_spec_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_spec_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
