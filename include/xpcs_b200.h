@@ -266,19 +266,24 @@ XG_API int64_t xg_series_frames(const xg_series* s);
  * exact integer accumulation, f64 combination.  xg_ttc_compressed =
  * ttc_compressed (correlate.cpp:27-35): C~_q = Y_q Y_q^T on tcgen05 bf16 tensor
  * cores (bf16x3 split, or XG_CMP_BF16) + fused g2. */
-/* Basis construction (host, f64; untimed setup).  The reference's
- * encoder_from_rows (encoder.cpp:13-28): row_normalize -> Gram-trick SVD
- * (linalg.cpp:279-439, cyclic Jacobi, measured sigma, rank at 1e-12 sigma_max,
- * 2x MGS, largest entry positive) -> first k right vectors.  k = 0 keeps the
- * full numerical rank (build_offline).  Returns XG_ERR_RANK with the
- * achievable rank in *rank_out when k exceeds it, XG_ERR_NORMALIZATION with
- * the zero frame in *rank_out. */
+/* Basis construction from f64 training rows of any values (host buffers in,
+ * computed on the CURRENT CUDA device by K9; untimed setup).  The reference's
+ * encoder_from_rows (encoder.cpp:13-28): row_normalize and S = Xn Xn^T in the
+ * reference's f64 order (k_exact.cu) -> parallel-order Jacobi (linalg.cpp:
+ * 234-276) -> measured sigma, rank at 1e-12 sigma_max -> 2x Cholesky-QR ->
+ * largest entry positive -> first k right vectors.  k = 0 keeps the full
+ * numerical rank (build_offline).  2 <= n <= 2048 rows.  Returns XG_ERR_RANK
+ * with the achievable rank in *rank_out when k exceeds it,
+ * XG_ERR_NORMALIZATION with the zero frame in *rank_out, XG_ERR_CUDA without
+ * a device.  Photon-count series use xg_series_build_basis (exact Gram). */
 XG_API int xg_build_basis(const double* x, int64_t n, int64_t m, int32_t k, double* v_out,
                           double* sigma_out, int64_t* rank_out);
 /* content_hash_u64 (model.cpp:99-114): 64-bit FNV-1a over "XENC", the mode
  * byte (0 offline, 1 online-related, 2 online-unrelated), n_pixels, k and the
  * f64 bits of V (m x k row-major), little-endian.  The store binding id. */
 XG_API uint64_t xg_content_hash(const double* v, int64_t m, int64_t k, int32_t mode);
+/* Every ring at once (x_ring[r]: n x m_ring[r]); threads is ignored (one
+ * device pass). */
 XG_API int xg_build_basis_batch(int32_t n_rings, const double* const* x_ring, int64_t n,
                                 const int64_t* m_ring, int32_t k, double* const* v_ring,
                                 int32_t threads, int64_t* rank_out);

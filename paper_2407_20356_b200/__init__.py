@@ -324,7 +324,8 @@ class RingLayout:
 # ------------------------------------------------------------------ basis
 def build_online_from_frames(prior: np.ndarray, k: int) -> np.ndarray:
     """V (m x k) from a prior series (encoder.cpp:53-60); k = 0 -> full
-    numerical rank (build_offline, encoder.cpp:32-37).  Host f64 setup."""
+    numerical rank (build_offline, encoder.cpp:32-37).  Runs on the current
+    CUDA device (K9 over f64 rows, xg_build_basis); at most 2048 rows."""
     x = np.ascontiguousarray(prior, dtype=np.float64)
     n, m = x.shape
     if n < 2:
@@ -342,15 +343,17 @@ def build_online_from_frames(prior: np.ndarray, k: int) -> np.ndarray:
                         int(rank.value))
     if rc == _abi.ERR_NORMALIZATION:
         raise NormalizationError(f"frame {rank.value} has zero norm", int(rank.value))
+    if rc in (_abi.ERR_CUDA, _abi.ERR_DEVICE):
+        raise DeviceError(f"build_basis needs a CUDA device (status {rc})")
     if rc != _abi.OK:
-        raise ContractError(f"build_basis failed with status {rc}")
+        raise ContractError(f"build_basis failed with status {rc} (n <= 2048 rows, m >= 1)")
     if k == 0:
         v = np.ascontiguousarray(v.ravel()[: m * rank.value].reshape(m, rank.value))
     return v
 
 
 def build_ring_bases(prior_per_ring: Sequence[np.ndarray], k: int, threads: int = 0):
-    """build_online_from_frames for every ring on parallel host threads."""
+    """build_online_from_frames for every ring in one device pass (K9)."""
     xs = [np.ascontiguousarray(x, dtype=np.float64) for x in prior_per_ring]
     n = xs[0].shape[0]
     vs = [np.empty((x.shape[1], k), np.float64) for x in xs]
@@ -363,6 +366,8 @@ def build_ring_bases(prior_per_ring: Sequence[np.ndarray], k: int, threads: int 
                                   ranks.ctypes.data_as(_abi.PI64))
     if rc == _abi.ERR_RANK:
         raise RankError(f"k = {k} exceeds a ring's numerical rank", int(ranks.min()))
+    if rc in (_abi.ERR_CUDA, _abi.ERR_DEVICE):
+        raise DeviceError(f"build_ring_bases needs a CUDA device (status {rc})")
     if rc != _abi.OK:
         raise ContractError(f"build_ring_bases failed with status {rc}")
     return vs

@@ -169,9 +169,13 @@ __global__ void k_basis_s(BasisSParams p) {
   double v = 0.0;
   if (i < p.n && j < p.n) {
     const int a = min(i, j), b = max(i, j);
-    const int32_t g = p.gram[(int64_t)ring * p.ring_stride + ttc_off(a, b, p.ld, p.nb)];
-    const double* inv = p.inv + ring * p.inv_ld;
-    v = static_cast<double>(g) * inv[a] * inv[b];
+    if (p.s64) {
+      v = p.s64[(int64_t)ring * p.n * p.n + (int64_t)a * p.n + b];
+    } else {
+      const int32_t g = p.gram[(int64_t)ring * p.ring_stride + ttc_off(a, b, p.ld, p.nb)];
+      const double* inv = p.inv + ring * p.inv_ld;
+      v = static_cast<double>(g) * inv[a] * inv[b];
+    }
   }
   p.a[ring * rs + (int64_t)si * np + sj] = v;
   // V: row = coordinate si, column = slot sj holding index j

@@ -1960,31 +1960,29 @@ void for_rings(int32_t n, F f) {
   for (auto& t : pool) t.join();
 }
 
-}  // namespace
-extern "C" {
+// Per-ring inputs of the device basis builder: the training rows X_r (n x
+// kpad_r on the device: ring-major u8 frames or f64 rows), the offset of each
+// ring's columns in the shared W / Q buffers (ktot columns in all), the W
+// column of every mask-order pixel, and 1/|x_t| per frame (host copy).
+struct BasisJob {
+  int32_t Q = 0;
+  int64_t n = 0;
+  BasisSParams sp{};  // S source; n, np, a, v are set by basis_run
+  bool x_u8 = true;
+  std::vector<const void*> x;
+  std::vector<int64_t> ldx, kpad, koff, mq;
+  std::vector<const int64_t*> col;
+  int64_t ktot = 0;
+  std::vector<double> inv;
+  int64_t inv_ld = 0;
+};
 
-int xg_series_build_basis(xg_series* s, int32_t k, double* const* v_out, double* sigma_out,
-                          int64_t sigma_ld, int64_t* rank_out, xg_basis* B) {
-  if (!s || !rank_out) return XG_ERR_INVALID;
-  xg_ctx* c = s->ctx;
-  const xg_layout* L = s->L;
-  const int32_t Q = L->rings;
-  const int64_t n = s->t;
-  if (k < 0) return fail(c, XG_ERR_CONTRACT, "build_online_from_frames: k must be >= 1");
-  if (n < 2) return fail(c, XG_ERR_CONTRACT, "build_online_from_frames: need at least 2 frames");
-  if (n > 2048) return fail(c, XG_ERR_CONTRACT, "build_basis: at most 2048 training frames");
-  if (s->x_row0 != 0 || n > s->xmax)
-    return fail(c, XG_ERR_CONTRACT, "build_basis: every training frame must be resident");
-  if (B && (B->L != L || B->k != k || k == 0))
-    return fail(c, XG_ERR_CONTRACT, "build_basis: basis of rank %d does not match k = %d",
-                B ? B->k : 0, k);
-  if (sigma_out && sigma_ld < n) return fail(c, XG_ERR_SHAPE, "build_basis: sigma_ld < frames");
-  int rc = strict_zero_check(s, "row_normalize");  // encoder_from_rows -> row_normalize
-  if (rc) return rc;
-  if (!(s->have_raw && s->raw_stored)) {
-    rc = xg_ttc_raw(s, 0);  // the exact Gram of the training frames (K2)
-    if (rc) return rc;
-  }
+// The device Gram-trick SVD (K9) from S onwards, shared by the series
+// builder (counts, S from the exact int32 Gram) and the f64-row builders.
+int basis_run(xg_ctx* c, const BasisJob& J, int32_t k, double* const* v_out, double* sigma_out,
+              int64_t sigma_ld, int64_t* rank_out, xg_basis* B) {
+  const int32_t Q = J.Q;
+  const int64_t n = J.n;
   cudaStream_t st = c->stream;
   const int np = static_cast<int>(n + (n & 1));
   const int64_t rs = (int64_t)np * np;
@@ -2006,8 +2004,11 @@ int xg_series_build_basis(xg_series* s, int32_t k, double* const* v_out, double*
     XG_CUDA(c, db.get(&d_v[b], (size_t)Q * rs));
   }
   XG_CUDA(c, db.get(&d_state, (size_t)Q));
-  BasisSParams sp{s->d_gram, static_cast<int32_t>(s->tp), s->d_inv, s->tp,
-                  static_cast<int32_t>(n), np, d_a[0], d_v[0], ttc_nb(s), slab_elems(s)};
+  BasisSParams sp = J.sp;
+  sp.n = static_cast<int32_t>(n);
+  sp.np = np;
+  sp.a = d_a[0];
+  sp.v = d_v[0];
   phase("gram");
   XG_CUDA(c, launch_basis_s(sp, Q, st));
   c->launches++;
@@ -2051,12 +2052,11 @@ int xg_series_build_basis(xg_series* s, int32_t k, double* const* v_out, double*
   XG_CUDA(c, cudaMemcpyAsync(d_aptr, a_ptr.data(), Q * sizeof(double*), cudaMemcpyHostToDevice, st));
   XG_CUDA(c, launch_jacobi_diag(d_aptr, d_eig, np, Q, st));
   c->launches++;
-  std::vector<double> eig((size_t)Q * np), hv((size_t)Q * rs), inv((size_t)Q * s->tp);
+  std::vector<double> eig((size_t)Q * np), hv((size_t)Q * rs);
   XG_CUDA(c, cudaMemcpyAsync(eig.data(), d_eig, eig.size() * 8, cudaMemcpyDeviceToHost, st));
   for (int32_t r = 0; r < Q; ++r)
     XG_CUDA(c, cudaMemcpyAsync(hv.data() + r * rs, d_v[final_buf[r]] + r * rs, rs * 8,
                                cudaMemcpyDeviceToHost, st));
-  XG_CUDA(c, cudaMemcpyAsync(inv.data(), s->d_inv, inv.size() * 8, cudaMemcpyDeviceToHost, st));
   XG_CUDA(c, cudaStreamSynchronize(st));
   // Bt[j][t] = inv_t U[t][order_j]: eigenvectors in descending eigenvalue
   // order (stable in the index, linalg.cpp:262-266), rows scaled by 1/|x_t|
@@ -2070,32 +2070,32 @@ int xg_series_build_basis(xg_series* s, int32_t k, double* const* v_out, double*
     double* o = bt.data() + (size_t)r * n * n;
     for (int64_t j = 0; j < n; ++j) {
       const int sl = index_slot(static_cast<int>(ord[j]), 0, np);
-      for (int64_t t = 0; t < n; ++t) o[j * n + t] = inv[r * s->tp + t] * v[t * np + sl];
+      for (int64_t t = 0; t < n; ++t) o[j * n + t] = J.inv[r * J.inv_ld + t] * v[t * np + sl];
     }
   });
   phase("eig+Bt");
   double *d_bt, *d_w;
   XG_CUDA(c, db.get(&d_bt, bt.size()));
-  XG_CUDA(c, db.get(&d_w, (size_t)n * L->ktot));
+  XG_CUDA(c, db.get(&d_w, (size_t)n * J.ktot));
   XG_CUDA(c, cudaMemcpyAsync(d_bt, bt.data(), bt.size() * 8, cudaMemcpyHostToDevice, st));
-  // ---- W_r = Bt_r X_r  (n x kpad_r), X = the ring-major u8 frames
+  // ---- W_r = Bt_r X_r  (n x kpad_r), X = the ring-major u8 frames or f64 rows
   int64_t kpad_max = 0;
   std::vector<DGemmRing> gr(Q);
   for (int32_t r = 0; r < Q; ++r) {
-    kpad_max = std::max(kpad_max, L->kpad[r]);
-    gr[r] = DGemmRing{d_bt + (size_t)r * n * n, n, s->d_x + ring_base(L, s->xmax, r), ring_ld(L, r),
-                      d_w + n * L->koff[r], L->kpad[r], (int32_t)n, (int32_t)L->kpad[r], (int32_t)n};
+    kpad_max = std::max(kpad_max, J.kpad[r]);
+    gr[r] = DGemmRing{d_bt + (size_t)r * n * n, n, J.x[r], J.ldx[r],
+                      d_w + n * J.koff[r], J.kpad[r], (int32_t)n, (int32_t)J.kpad[r], (int32_t)n};
   }
   DGemmRing* d_gr;
   XG_CUDA(c, db.get(&d_gr, (size_t)Q));
   XG_CUDA(c, cudaMemcpyAsync(d_gr, gr.data(), Q * sizeof(DGemmRing), cudaMemcpyHostToDevice, st));
-  XG_CUDA(c, launch_dgemm_nn(d_gr, Q, (int)n, (int)kpad_max, true, st));
+  XG_CUDA(c, launch_dgemm_nn(d_gr, Q, (int)n, (int)kpad_max, J.x_u8, st));
   c->launches++;
   // ---- measured singular values |W_j| (linalg.cpp:312-320)
   double* d_nrm;
   XG_CUDA(c, db.get(&d_nrm, (size_t)Q * n));
-  for (int32_t r = 0; r < Q; ++r) gr[r] = DGemmRing{d_w + n * L->koff[r], L->kpad[r], nullptr, 0,
-                                                    nullptr, 0, (int32_t)n, (int32_t)L->kpad[r], 0};
+  for (int32_t r = 0; r < Q; ++r) gr[r] = DGemmRing{d_w + n * J.koff[r], J.kpad[r], nullptr, 0,
+                                                    nullptr, 0, (int32_t)n, (int32_t)J.kpad[r], 0};
   XG_CUDA(c, cudaMemcpyAsync(d_gr, gr.data(), Q * sizeof(DGemmRing), cudaMemcpyHostToDevice, st));
   XG_CUDA(c, launch_row_norm2(d_gr, Q, (int)n, d_nrm, n, st));
   c->launches++;
@@ -2147,16 +2147,16 @@ int xg_series_build_basis(xg_series* s, int32_t k, double* const* v_out, double*
   const int64_t part_stride = (int64_t)max_chunks * kkmax * kkmax;
   XG_CUDA(c, db.get(&d_idx, hidx.size()));
   XG_CUDA(c, db.get(&d_sc, hsc.size()));
-  XG_CUDA(c, db.get(&d_q[0], (size_t)kkmax * L->ktot));
-  XG_CUDA(c, db.get(&d_q[1], (size_t)kkmax * L->ktot));
+  XG_CUDA(c, db.get(&d_q[0], (size_t)kkmax * J.ktot));
+  XG_CUDA(c, db.get(&d_q[1], (size_t)kkmax * J.ktot));
   XG_CUDA(c, db.get(&d_g, (size_t)Q * kkmax * kkmax));
   XG_CUDA(c, db.get(&d_part, (size_t)Q * part_stride));
   XG_CUDA(c, db.get(&d_mt, (size_t)Q * kkmax * kkmax));
   XG_CUDA(c, cudaMemcpyAsync(d_idx, hidx.data(), hidx.size() * 4, cudaMemcpyHostToDevice, st));
   XG_CUDA(c, cudaMemcpyAsync(d_sc, hsc.data(), hsc.size() * 8, cudaMemcpyHostToDevice, st));
   for (int32_t r = 0; r < Q; ++r)
-    gr[r] = DGemmRing{d_w + n * L->koff[r], L->kpad[r], nullptr, 0, d_q[0] + kkmax * L->koff[r],
-                      L->kpad[r], (int32_t)kk[r], (int32_t)L->kpad[r], 0};
+    gr[r] = DGemmRing{d_w + n * J.koff[r], J.kpad[r], nullptr, 0, d_q[0] + kkmax * J.koff[r],
+                      J.kpad[r], (int32_t)kk[r], (int32_t)J.kpad[r], 0};
   XG_CUDA(c, cudaMemcpyAsync(d_gr, gr.data(), Q * sizeof(DGemmRing), cudaMemcpyHostToDevice, st));
   XG_CUDA(c, launch_gather_rows(d_gr, d_idx, d_sc, kkmax, Q, (int)kkmax, (int)kpad_max, st));
   c->launches++;
@@ -2170,9 +2170,9 @@ int xg_series_build_basis(xg_series* s, int32_t k, double* const* v_out, double*
     double* qin = d_q[pass];
     double* qout = d_q[pass ^ 1];
     for (int32_t r = 0; r < Q; ++r)
-      gr[r] = DGemmRing{qin + kkmax * L->koff[r], L->kpad[r], nullptr, 0,
+      gr[r] = DGemmRing{qin + kkmax * J.koff[r], J.kpad[r], nullptr, 0,
                         d_g + (size_t)r * kkmax * kkmax, kk[r], (int32_t)kk[r],
-                        (int32_t)L->kpad[r], 0};
+                        (int32_t)J.kpad[r], 0};
     XG_CUDA(c, cudaMemcpyAsync(d_gr, gr.data(), Q * sizeof(DGemmRing), cudaMemcpyHostToDevice, st));
     XG_CUDA(c, launch_dsyrk(d_gr, Q, (int)kkmax, max_chunks, d_part, part_stride, st));
     XG_CUDA(c, launch_dsyrk_sum(d_gr, Q, (int)kkmax, max_chunks, d_part, part_stride, st));
@@ -2203,21 +2203,21 @@ int xg_series_build_basis(xg_series* s, int32_t k, double* const* v_out, double*
       }
     XG_CUDA(c, cudaMemcpyAsync(d_mt, hmt.data(), hmt.size() * 8, cudaMemcpyHostToDevice, st));
     for (int32_t r = 0; r < Q; ++r)
-      gr[r] = DGemmRing{d_mt + (size_t)r * kkmax * kkmax, kk[r], qin + kkmax * L->koff[r],
-                        L->kpad[r], qout + kkmax * L->koff[r], L->kpad[r], (int32_t)kk[r],
-                        (int32_t)L->kpad[r], (int32_t)kk[r]};
+      gr[r] = DGemmRing{d_mt + (size_t)r * kkmax * kkmax, kk[r], qin + kkmax * J.koff[r],
+                        J.kpad[r], qout + kkmax * J.koff[r], J.kpad[r], (int32_t)kk[r],
+                        (int32_t)J.kpad[r], (int32_t)kk[r]};
     XG_CUDA(c, cudaMemcpyAsync(d_gr, gr.data(), Q * sizeof(DGemmRing), cudaMemcpyHostToDevice, st));
     XG_CUDA(c, launch_dgemm_nn(d_gr, Q, (int)kkmax, (int)kpad_max, false, st));
     c->launches++;
   }
   phase("cholqr2");
   // ---- orthonormal columns (d_q[0] after two passes) to the host
-  std::vector<double> hq((size_t)kkmax * L->ktot);
+  std::vector<double> hq((size_t)kkmax * J.ktot);
   XG_CUDA(c, cudaMemcpyAsync(hq.data(), d_q[0], hq.size() * 8, cudaMemcpyDeviceToHost, st));
   XG_CUDA(c, cudaStreamSynchronize(st));
   std::vector<int> set_rc(Q, XG_OK);
   for_rings(Q, [&](int32_t r) {
-    const int64_t m = kk[r], kout = k == 0 ? rank[r] : k, mq = L->ring_pixels[r];
+    const int64_t m = kk[r], kout = k == 0 ? rank[r] : k, mq = J.mq[r];
     // sigma_j = |a_j|, a = u_kept r_total^T with orthonormal u: the row norms
     // of r_total times |W_j| (linalg.cpp:377-383); near-ties re-sorted (:387-391)
     std::vector<double> sig(m);
@@ -2245,22 +2245,22 @@ int xg_series_build_basis(xg_series* s, int32_t k, double* const* v_out, double*
       vloc.resize(mq * kout);
       vo = vloc.data();
     }
-    const int64_t* col = L->colpos.data() + L->mask_off[r];
-    const double* qb = hq.data() + kkmax * L->koff[r];
+    const int64_t* col = J.col[r];
+    const double* qb = hq.data() + kkmax * J.koff[r];
     for (int64_t j = 0; j < kout; ++j) {
-      const double* qrow = qb + perm[j] * L->kpad[r];
+      const double* qrow = qb + perm[j] * J.kpad[r];
       // sign: largest-magnitude entry positive, first in mask order (linalg.cpp:421-436)
       int64_t arg = 0;
       double best = -1.0;
       for (int64_t i = 0; i < mq; ++i) {
-        const double mag = std::fabs(qrow[col[i] - L->koff[r]]);
+        const double mag = std::fabs(qrow[col[i] - J.koff[r]]);
         if (mag > best) {
           best = mag;
           arg = i;
         }
       }
-      const double sg = qrow[col[arg] - L->koff[r]] < 0.0 ? -1.0 : 1.0;
-      for (int64_t i = 0; i < mq; ++i) vo[i * kout + j] = sg * qrow[col[i] - L->koff[r]];
+      const double sg = qrow[col[arg] - J.koff[r]] < 0.0 ? -1.0 : 1.0;
+      for (int64_t i = 0; i < mq; ++i) vo[i * kout + j] = sg * qrow[col[i] - J.koff[r]];
     }
     if (B) set_rc[r] = xg_basis_set_ring(B, r, vo);
   });
@@ -2268,6 +2268,135 @@ int xg_series_build_basis(xg_series* s, int32_t k, double* const* v_out, double*
   for (int32_t r = 0; r < Q; ++r)
     if (set_rc[r]) return set_rc[r];
   return XG_OK;
+}
+
+
+}  // namespace
+extern "C" {
+
+int xg_series_build_basis(xg_series* s, int32_t k, double* const* v_out, double* sigma_out,
+                          int64_t sigma_ld, int64_t* rank_out, xg_basis* B) {
+  if (!s || !rank_out) return XG_ERR_INVALID;
+  xg_ctx* c = s->ctx;
+  const xg_layout* L = s->L;
+  const int32_t Q = L->rings;
+  const int64_t n = s->t;
+  if (k < 0) return fail(c, XG_ERR_CONTRACT, "build_online_from_frames: k must be >= 1");
+  if (n < 2) return fail(c, XG_ERR_CONTRACT, "build_online_from_frames: need at least 2 frames");
+  if (n > 2048) return fail(c, XG_ERR_CONTRACT, "build_basis: at most 2048 training frames");
+  if (s->x_row0 != 0 || n > s->xmax)
+    return fail(c, XG_ERR_CONTRACT, "build_basis: every training frame must be resident");
+  if (B && (B->L != L || B->k != k || k == 0))
+    return fail(c, XG_ERR_CONTRACT, "build_basis: basis of rank %d does not match k = %d",
+                B ? B->k : 0, k);
+  if (sigma_out && sigma_ld < n) return fail(c, XG_ERR_SHAPE, "build_basis: sigma_ld < frames");
+  int rc = strict_zero_check(s, "row_normalize");  // encoder_from_rows -> row_normalize
+  if (rc) return rc;
+  if (!(s->have_raw && s->raw_stored)) {
+    rc = xg_ttc_raw(s, 0);  // the exact Gram of the training frames (K2)
+    if (rc) return rc;
+  }
+  BasisJob J;
+  J.Q = Q;
+  J.n = n;
+  J.sp = BasisSParams{s->d_gram, static_cast<int32_t>(s->tp), s->d_inv, s->tp, 0, 0, nullptr,
+                      nullptr, ttc_nb(s), slab_elems(s), nullptr};
+  J.x_u8 = true;
+  J.ktot = L->ktot;
+  for (int32_t r = 0; r < Q; ++r) {
+    J.x.push_back(s->d_x + ring_base(L, s->xmax, r));
+    J.ldx.push_back(ring_ld(L, r));
+    J.kpad.push_back(L->kpad[r]);
+    J.koff.push_back(L->koff[r]);
+    J.mq.push_back(L->ring_pixels[r]);
+    J.col.push_back(L->colpos.data() + L->mask_off[r]);
+  }
+  J.inv_ld = s->tp;
+  J.inv.resize((size_t)Q * s->tp);
+  XG_CUDA(c, cudaMemcpyAsync(J.inv.data(), s->d_inv, J.inv.size() * 8, cudaMemcpyDeviceToHost,
+                             c->stream));
+  XG_CUDA(c, cudaStreamSynchronize(c->stream));
+  return basis_run(c, J, k, v_out, sigma_out, sigma_ld, rank_out, B);
+}
+
+// build_online_from_frames / build_offline over f64 training rows of any
+// values (encoder.cpp:32-60 -> gram_svd, linalg.cpp:184-439), on the device:
+// row_normalize and S = Xn Xn^T by the reference-order f64 kernels
+// (k_exact.cu, so S carries the reference's bits), then the same Jacobi /
+// W / Cholesky-QR pipeline as the count builder.  Rings (x_ring[r]: n x
+// m_ring[r], host, row-major) are factorised together; v_ring[r] receives
+// m_ring[r] x kk (kk = k, or the ring's numerical rank when k = 0).
+// rank_out[r]: the rank, or the first zero-norm row (XG_ERR_NORMALIZATION),
+// or the achievable rank (XG_ERR_RANK).
+static int basis_f64(int32_t Q, const double* const* x_ring, int64_t n, const int64_t* m_ring,
+                     int32_t k, double* const* v_ring, double* sigma_out, int64_t* rank_out) {
+  if (Q < 1 || !x_ring || !m_ring || !rank_out || n < 2 || k < 0) return XG_ERR_CONTRACT;
+  if (n > 2048) return XG_ERR_CONTRACT;  // the device Jacobi's training-row limit
+  for (int32_t r = 0; r < Q; ++r)
+    if (!x_ring[r] || m_ring[r] < 1) return XG_ERR_CONTRACT;
+  xg_ctx cx;
+  xg_ctx* c = &cx;
+  if (cudaGetDevice(&c->device) != cudaSuccess) return XG_ERR_CUDA;
+  cudaStream_t st = nullptr;
+  BasisJob J;
+  J.Q = Q;
+  J.n = n;
+  J.x_u8 = false;
+  for (int32_t r = 0; r < Q; ++r) {
+    J.koff.push_back(J.ktot);
+    J.kpad.push_back(m_ring[r]);
+    J.ldx.push_back(m_ring[r]);
+    J.mq.push_back(m_ring[r]);
+    J.ktot += m_ring[r];
+  }
+  std::vector<int64_t> colv(J.ktot);
+  std::iota(colv.begin(), colv.end(), int64_t{0});
+  DevBufs db;
+  double *d_x, *d_xn, *d_norm, *d_s;
+  unsigned long long* d_bad;
+  XG_CUDA(c, db.get(&d_x, (size_t)n * J.ktot));
+  XG_CUDA(c, db.get(&d_xn, (size_t)n * J.ktot));
+  XG_CUDA(c, db.get(&d_norm, (size_t)Q * n));
+  XG_CUDA(c, db.get(&d_s, (size_t)Q * n * n));
+  XG_CUDA(c, db.get(&d_bad, (size_t)Q));
+  XG_CUDA(c, cudaMemsetAsync(d_bad, 0xff, Q * sizeof(unsigned long long), st));
+  for (int32_t r = 0; r < Q; ++r) {
+    double* xr = d_x + n * J.koff[r];
+    XG_CUDA(c, cudaMemcpyAsync(xr, x_ring[r], (size_t)n * m_ring[r] * 8, cudaMemcpyHostToDevice, st));
+    XG_CUDA(c, launch_exact_rownorm(xr, n, m_ring[r], d_xn + n * J.koff[r], d_norm + r * n,
+                                    d_bad + r, st));
+    XG_CUDA(c, launch_exact_gram(d_xn + n * J.koff[r], n, m_ring[r], d_s + (size_t)r * n * n, st));
+    J.x.push_back(xr);
+    J.col.push_back(colv.data() + J.koff[r]);
+  }
+  std::vector<unsigned long long> bad(Q);
+  J.inv.resize((size_t)Q * n);
+  J.inv_ld = n;
+  XG_CUDA(c, cudaMemcpyAsync(bad.data(), d_bad, Q * sizeof(unsigned long long),
+                             cudaMemcpyDeviceToHost, st));
+  XG_CUDA(c, cudaMemcpyAsync(J.inv.data(), d_norm, J.inv.size() * 8, cudaMemcpyDeviceToHost, st));
+  XG_CUDA(c, cudaStreamSynchronize(st));
+  for (int32_t r = 0; r < Q; ++r)
+    if (bad[r] != ~0ull) {  // row_normalize (linalg.cpp:441-456): first zero row
+      rank_out[r] = static_cast<int64_t>(bad[r]);
+      return XG_ERR_NORMALIZATION;
+    }
+  for (double& v : J.inv) v = 1.0 / v;
+  J.sp = BasisSParams{nullptr, 0, nullptr, 0, 0, 0, nullptr, nullptr, 0, 0, d_s};
+  return basis_run(c, J, k, v_ring, sigma_out, n, rank_out, nullptr);
+}
+
+int xg_build_basis(const double* x, int64_t n, int64_t m, int32_t k, double* v_out,
+                   double* sigma_out, int64_t* rank_out) {
+  if (!x || !rank_out || n < 2 || m < 1 || k < 0) return XG_ERR_CONTRACT;
+  return basis_f64(1, &x, n, &m, k, &v_out, sigma_out, rank_out);
+}
+
+int xg_build_basis_batch(int32_t n_rings, const double* const* x_ring, int64_t n,
+                         const int64_t* m_ring, int32_t k, double* const* v_ring,
+                         int32_t /*threads: one device pass over all rings*/, int64_t* rank_out) {
+  if (n_rings < 1 || !v_ring) return XG_ERR_CONTRACT;
+  return basis_f64(n_rings, x_ring, n, m_ring, k, v_ring, nullptr, rank_out);
 }
 
 int xg_compress(xg_series* s, const xg_basis* Bc, uint32_t flags) {

@@ -625,6 +625,7 @@ struct BasisSParams {
   double* v;                 // [ring][np][np] identity in slot layout
   int32_t nb;                // packed-tile row length (ttc_off)
   int64_t ring_stride;       // elements per ring slab
+  const double* s64;         // non-null: S given in f64, [ring][n][n] (gram/inv unused)
 };
 cudaError_t launch_basis_s(const BasisSParams& p, int n_rings, cudaStream_t s);
 // diag of the converged A (slot layout of step 0) -> eig [ring][np]

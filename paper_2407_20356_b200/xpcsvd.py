@@ -35,7 +35,7 @@ import enum
 
 import numpy as np
 
-from . import (BindingError, ContractError, Context, Error, FormatError,  # noqa: F401
+from . import (BindingError, ContractError, Context, DeviceError, Error, FormatError,  # noqa: F401
                MaskError, NormalizationError, RankError, ShapeError)
 from . import _abi
 from . import compress_frame as _compress_frame
@@ -201,7 +201,9 @@ def _encoder_from_rows(x: np.ndarray, mode: EncoderMode, k: int) -> EncodingMatr
     x = np.ascontiguousarray(x, dtype=np.float64)
     n, m = x.shape
     u8 = _as_counts(x) if n <= 2048 else None
-    if u8 is not None:  # counts: the device Gram-trick SVD (K9)
+    # both branches run K9 on the device: counts from their exact int32 Gram,
+    # other rows from the reference-order f64 S (xg_build_basis)
+    if u8 is not None:
         vs, sig, rank = _one_ring_series(u8).build_basis(k)
         return EncodingMatrix(vs[0], sig[0], mode)
     kk = k if k > 0 else n
@@ -216,6 +218,8 @@ def _encoder_from_rows(x: np.ndarray, mode: EncoderMode, k: int) -> EncodingMatr
                         r)
     if rc == _abi.ERR_NORMALIZATION:
         raise NormalizationError(f"frame {r} has zero norm", r)
+    if rc in (_abi.ERR_CUDA, _abi.ERR_DEVICE):
+        raise DeviceError(f"basis construction needs a CUDA device (status {rc})")
     if rc != _abi.OK:
         raise ContractError(f"basis construction failed with status {rc}")
     if k == 0:

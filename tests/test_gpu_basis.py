@@ -91,3 +91,36 @@ def test_device_basis_drives_compression(ctx, orc):
     s.compress(b_host)
     for r in range(q):
         assert np.array_equal(y_dev[r], s.coeffs(r)[0])
+
+
+# ---- f64 training rows of any values (xg_build_basis / _batch): row_normalize
+# and S in the reference's own f64 order on the device, then the same K9
+# pipeline.  Same bar as the count builder.
+@pytest.mark.parametrize("n,m,k,seed", [(16, 64, 8, 1), (40, 500, 20, 2), (64, 3000, 32, 3)])
+def test_f64_rows_basis_builder_matches_reference(orc, ref, n, m, k, seed):
+    x = orc.random_positive_matrix(n, m, seed)
+    v = xg.build_online_from_frames(x, k)
+    vr, _ = ref.build_online_from_frames(x, k)
+    assert np.abs(v - vr).max() <= 1e-10
+    assert np.abs(v.T @ v - np.eye(k)).max() <= 1e-10
+
+
+def test_f64_rows_basis_builder_full_rank_and_errors(orc, ref):
+    x = orc.random_positive_matrix(12, 48, 5)
+    v = xg.build_online_from_frames(x, 0)
+    assert np.abs(v - ref.build_offline(x)).max() <= 1e-10
+    with pytest.raises(xg.RankError) as ei:
+        xg.build_online_from_frames(np.ones((4, 8)), 2)      # rank-1 corpus
+    assert ei.value.achievable_rank == 1
+    z = orc.random_positive_matrix(5, 10, 1)
+    z[3] = 0.0
+    with pytest.raises(xg.NormalizationError) as ei:
+        xg.build_online_from_frames(z, 2)
+    assert ei.value.frame_index == 3
+
+
+def test_f64_rows_ring_bases_batch_equals_single(orc):
+    xs = [orc.random_positive_matrix(24, m, 10 + m) for m in (50, 77, 120)]
+    par = xg.build_ring_bases(xs, 6, threads=3)
+    for x, v in zip(xs, par):
+        assert np.array_equal(v, xg.build_online_from_frames(x, 6))

@@ -1,6 +1,6 @@
 """Host-side checks that need no GPU: the C-ABI library loads and exports
 every symbol include/xpcs_b200.h declares, fails loudly without a B200,
-the basis builder matches the reference, geometry helpers, sharding."""
+the basis builder refuses to run without one, geometry helpers, sharding."""
 import numpy as np
 import pytest
 
@@ -32,36 +32,14 @@ def test_annular_rings_match_oracle(orc):
         assert np.array_equal(xg.annular_rings(h, w, q), r)
 
 
-@pytest.mark.skipif(not oracle.ref_available(), reason="oracle/_ref not built")
-@pytest.mark.parametrize("n,m,k,seed", [(16, 64, 8, 1), (40, 500, 20, 2), (64, 3000, 32, 3)])
-def test_basis_builder_matches_reference(orc, ref, n, m, k, seed):
-    x = orc.random_positive_matrix(n, m, seed)
-    v = xg.build_online_from_frames(x, k)
-    vr, _ = ref.build_online_from_frames(x, k)
-    assert np.abs(v - vr).max() <= 1e-10
-    assert np.abs(v.T @ v - np.eye(k)).max() <= 1e-10
+def test_basis_builder_fails_loudly_without_gpu(orc):
+    """The f64-row basis builder runs on the device (K9); no host fallback."""
+    from conftest import gpu_available
 
-
-@pytest.mark.skipif(not oracle.ref_available(), reason="oracle/_ref not built")
-def test_basis_builder_full_rank_and_errors(orc, ref):
-    x = orc.random_positive_matrix(12, 48, 5)
-    v = xg.build_online_from_frames(x, 0)
-    assert np.abs(v - ref.build_offline(x)).max() <= 1e-10
-    with pytest.raises(xg.RankError) as ei:
-        xg.build_online_from_frames(np.ones((4, 8)), 2)      # rank-1 corpus
-    assert ei.value.achievable_rank == 1
-    z = orc.random_positive_matrix(5, 10, 1)
-    z[3] = 0.0
-    with pytest.raises(xg.NormalizationError) as ei:
-        xg.build_online_from_frames(z, 2)
-    assert ei.value.frame_index == 3
-
-
-def test_build_ring_bases_parallel_equals_serial(orc):
-    xs = [orc.random_positive_matrix(24, m, 10 + m) for m in (50, 77, 120)]
-    par = xg.build_ring_bases(xs, 6, threads=3)
-    for x, v in zip(xs, par):
-        assert np.array_equal(v, xg.build_online_from_frames(x, 6))
+    if gpu_available():
+        pytest.skip("GPU present")
+    with pytest.raises(xg.DeviceError):
+        xg.build_online_from_frames(orc.random_positive_matrix(8, 16, 1), 4)
 
 
 def test_shard_rings_lpt():
