@@ -500,15 +500,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<MODE>::NUM_THRE
             // every column is a frame: the precomputed walk, no mask; four
             // interleaved partial sums (l mod 4) shorten the dependent chain
             float ch[4] = {0.f, 0.f, 0.f, 0.f}, nx[4] = {0.f, 0.f, 0.f, 0.f};
+            // all 32 elements into ch, the starting window's into nx: one
+            // select per element instead of two; ch - nx finishes window c
 #pragma unroll
             for (int l = 0; l < 32; ++l) {
               const float v = __uint_as_float(S[wtab[l]]);
-              const bool fin = lane + 1 + l >= 32;
-              ch[l & 3] += fin ? v : 0.f;
-              nx[l & 3] += fin ? 0.f : v;
+              ch[l & 3] += v;
+              nx[l & 3] += lane + 1 + l >= 32 ? 0.f : v;
             }
-            cur_h += (ch[0] + ch[1]) + (ch[2] + ch[3]);
-            nxt_h += (nx[0] + nx[1]) + (nx[2] + nx[3]);
+            const float nsum = (nx[0] + nx[1]) + (nx[2] + nx[3]);
+            cur_h += ((ch[0] + ch[1]) + (ch[2] + ch[3])) - nsum;
+            nxt_h += nsum;
           } else
 #pragma unroll
           for (int l = 0; l < 32; ++l) {
