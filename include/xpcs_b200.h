@@ -367,6 +367,11 @@ XG_API int xg_f64_g2_from_ttc(const double* g, int64_t n, double period, double*
                               double* values, int64_t* counts);
 XG_API int xg_f64_compress_series(const double* x, int64_t n, int64_t m, const double* v,
                                   int64_t k, double* coeffs, double* norms);
+/* The same over integer photon counts packed to u8 by the caller (1 B per
+ * pixel over PCIe, widened to f64 on the device): results bitwise those of
+ * xg_f64_compress_series on the same values. */
+XG_API int xg_f64_compress_series_u8(const uint8_t* x, int64_t n, int64_t m, const double* v,
+                                     int64_t k, double* coeffs, double* norms);
 XG_API int xg_f64_compress_frame(const double* frame, int64_t m, const double* v, int64_t k,
                                  double* coeffs, double* norm);
 XG_API int xg_f64_ttc_rel_error(const double* a, const double* b, int64_t count, double* out);

@@ -19,10 +19,12 @@
 #ifndef XPCS_B200_ENGINE_HPP_
 #define XPCS_B200_ENGINE_HPP_
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
 #include <mutex>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -39,13 +41,34 @@ inline bool exact_only() {
 }
 
 // True when every value is an integer count in [0, 255]; packs them to u8.
+// Branch-free per element (the range and integrality test folded into one
+// flag, so the loop vectorises) over contiguous slices on XPCS_THREADS (the
+// reference's own thread knob, linalg.cpp:62-91) or all hardware threads.
 inline bool pack_counts(const double* x, std::size_t n, std::vector<uint8_t>& out) {
   out.resize(n);
-  for (std::size_t i = 0; i < n; ++i) {
-    const double v = x[i];
-    if (!(v >= 0.0 && v <= 255.0) || v != std::floor(v)) return false;
-    out[i] = static_cast<uint8_t>(v);
-  }
+  auto slice = [x, &out](std::size_t lo, std::size_t hi) {
+    bool ok = true;
+    uint8_t* o = out.data();
+    for (std::size_t i = lo; i < hi; ++i) {
+      const double v = x[i];
+      const double c = v >= 0.0 && v <= 255.0 ? v : 0.0;
+      const uint8_t b = static_cast<uint8_t>(static_cast<int>(c));
+      ok &= (static_cast<double>(b) == v);  // NaN, out of range, fractional -> false
+      o[i] = b;
+    }
+    return ok;
+  };
+  unsigned nt = std::thread::hardware_concurrency();
+  if (const char* e = std::getenv("XPCS_THREADS")) nt = static_cast<unsigned>(std::atoi(e));
+  nt = std::max(1u, std::min<unsigned>(nt ? nt : 1u, static_cast<unsigned>(n / (1u << 20) + 1)));
+  if (nt == 1) return slice(0, n);
+  std::vector<char> ok(nt, 0);
+  std::vector<std::thread> pool;
+  for (unsigned t = 0; t < nt; ++t)
+    pool.emplace_back([&, t] { ok[t] = slice(n * t / nt, n * (t + 1) / nt) ? 1 : 0; });
+  for (auto& th : pool) th.join();
+  for (char v : ok)
+    if (!v) return false;
   return true;
 }
 

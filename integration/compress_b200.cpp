@@ -1,13 +1,16 @@
 // compress_b200.cpp -- drop-in replacement for /root/reference/proj/src/
 // compress.cpp: compress_series / compress_frame on the B200 through the
 // xg_f64_* reference-order entries of libxpcs_b200.so (bit-identical to the
-// reference, including zero-pixel skipping and the first-zero-frame error).
+// reference, including zero-pixel skipping and the first-zero-frame error);
+// series of integer photon counts are shipped as u8 and widened on the device.
 // decompress is validation-only (out of scope): it stays a
 // host loop over the reference's own xpcs::dot.
 #include "xpcsvd/compress.hpp"
 
 #include <string>
+#include <vector>
 
+#include "b200_engine.hpp"
 #include "xpcs_b200.h"
 
 namespace xpcs {
@@ -47,9 +50,18 @@ CompressedSeries compress_series(const FrameSeries& frames, const EncodingMatrix
   check_pixels(frames.n_pixels(), enc);
   const std::size_t n = frames.n_frames(), k = enc.k();
   std::vector<double> coeffs(n * k), norms(n);
-  check(xg_f64_compress_series(frames.intensities.data().data(), static_cast<int64_t>(n),
-                               static_cast<int64_t>(frames.n_pixels()), enc.v().data().data(),
-                               static_cast<int64_t>(k), coeffs.data(), norms.data()));
+  const double* x = frames.intensities.data().data();
+  const int64_t m = static_cast<int64_t>(frames.n_pixels());
+  // integer photon counts cross PCIe as u8 (1 B instead of 8 per pixel) and
+  // are widened on the device: the same kernels, the same bits
+  std::vector<uint8_t> u8;
+  if (!xpcs_b200_dropin::exact_only() && n > 0 &&
+      xpcs_b200_dropin::pack_counts(x, n * frames.n_pixels(), u8))
+    check(xg_f64_compress_series_u8(u8.data(), static_cast<int64_t>(n), m, enc.v().data().data(),
+                                    static_cast<int64_t>(k), coeffs.data(), norms.data()));
+  else
+    check(xg_f64_compress_series(x, static_cast<int64_t>(n), m, enc.v().data().data(),
+                                 static_cast<int64_t>(k), coeffs.data(), norms.data()));
   return CompressedSeries(k, content_hash_u64(enc), std::move(coeffs), std::move(norms));
 }
 

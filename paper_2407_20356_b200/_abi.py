@@ -96,6 +96,7 @@ _sigs = {
     "xg_f64_ttc_extend": (C.c_int, [PD, I64, PD, I64, PD, PD, C.POINTER(C.c_int)]),
     "xg_f64_g2_from_ttc": (C.c_int, [PD, I64, C.c_double, PD, PD, PI64]),
     "xg_f64_compress_series": (C.c_int, [PD, I64, I64, PD, I64, PD, PD]),
+    "xg_f64_compress_series_u8": (C.c_int, [P, I64, I64, PD, I64, PD, PD]),
     "xg_f64_compress_frame": (C.c_int, [PD, I64, PD, I64, PD, PD]),
     "xg_f64_ttc_rel_error": (C.c_int, [PD, PD, I64, PD]),
     "xg_basis_create": (C.c_int, [P, P, I32, I32, C.POINTER(P)]),

@@ -265,7 +265,30 @@ __global__ void __launch_bounds__(32) k_exact_relerr(const double* a, const doub
   if (lane == 0) out[0] = den == 0.0 ? -1.0 : sqrt(__ddiv_rn(num, den));
 }
 
+// u8 photon counts -> f64 (exact): the drop-in ships counts over PCIe at 1 B
+// per pixel instead of 8 and widens them here, 16 per thread.
+__global__ void k_exact_widen_u8(const uint8_t* x, int64_t count, double* out) {
+  const int64_t i0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 16;
+  if (i0 + 16 <= count && (reinterpret_cast<uintptr_t>(x) & 15) == 0) {
+    const uint4 w = *reinterpret_cast<const uint4*>(x + i0);
+    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) out[i0 + 4 * q + b] = static_cast<double>((ws[q] >> (8 * b)) & 0xFFu);
+  } else {
+    for (int64_t i = i0; i < count && i < i0 + 16; ++i) out[i] = static_cast<double>(x[i]);
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_exact_widen_u8(const uint8_t* x, int64_t count, double* out, cudaStream_t s) {
+  if (count < 1) return cudaSuccess;
+  k_exact_widen_u8<<<static_cast<unsigned>((count + 16 * 256 - 1) / (16 * 256)), 256, 0, s>>>(x, count,
+                                                                                          out);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_exact_rownorm(const double* x, int64_t n, int64_t m, double* xn, double* norms,
                                  unsigned long long* bad, cudaStream_t s) {

@@ -195,21 +195,53 @@ XG_API int xg_f64_g2_from_ttc(const double* g, int64_t n, double period, double*
 
 // compress_series (compress.cpp:48-81): all norms first (first zero frame
 // reported), then every row like compress_frame.  v is m x k.
+namespace {
+int compress_series_impl(const double* x, const uint8_t* x8, int64_t n, int64_t m,
+                         const double* v, int64_t k, double* coeffs, double* norms);
+}  // namespace
+
 XG_API int xg_f64_compress_series(const double* x, int64_t n, int64_t m, const double* v,
                                   int64_t k, double* coeffs, double* norms) {
   SlotScope slots_;
   if (!x || !v || !coeffs || !norms) return XG_ERR_INVALID;
   if (k < 1) return err(XG_ERR_CONTRACT, "compress: k must be >= 1");
   if (n == 0) return XG_OK;  // an empty store (compress.cpp:48-81 loops over no frames)
+  return compress_series_impl(x, nullptr, n, m, v, k, coeffs, norms);
+}
+
+// The same over photon counts the caller packed to u8 (integer counts in
+// [0, 255], what the drop-in's compress_series detects): 1 B per pixel over
+// PCIe, widened to f64 on the device, then the identical kernels -- the
+// coefficients and norms are those of xg_f64_compress_series on the same
+// values, bit for bit.
+XG_API int xg_f64_compress_series_u8(const uint8_t* x, int64_t n, int64_t m, const double* v,
+                                     int64_t k, double* coeffs, double* norms) {
+  SlotScope slots_;
+  if (!x || !v || !coeffs || !norms) return XG_ERR_INVALID;
+  if (k < 1) return err(XG_ERR_CONTRACT, "compress: k must be >= 1");
+  if (n == 0) return XG_OK;
+  return compress_series_impl(nullptr, x, n, m, v, k, coeffs, norms);
+}
+
+namespace {
+int compress_series_impl(const double* x, const uint8_t* x8, int64_t n, int64_t m,
+                         const double* v, int64_t k, double* coeffs, double* norms) {
   DBuf<double> dx, dxn, dn, dv, dc;
   DBuf<unsigned long long> dbad;
+  DBuf<uint8_t> d8;
   XG_TRY(dx.alloc(n * m));
   XG_TRY(dxn.alloc(n * m));
   XG_TRY(dn.alloc(n));
   XG_TRY(dv.alloc(m * k));
   XG_TRY(dc.alloc(n * k));
   XG_TRY(dbad.alloc(1));
-  XG_TRY(cudaMemcpy(dx.p, x, n * m * 8, cudaMemcpyHostToDevice));
+  if (x8) {
+    XG_TRY(d8.alloc(n * m));
+    XG_TRY(cudaMemcpy(d8.p, x8, n * m, cudaMemcpyHostToDevice));
+    XG_TRY(launch_exact_widen_u8(d8.p, n * m, dx.p, 0));
+  } else {
+    XG_TRY(cudaMemcpy(dx.p, x, n * m * 8, cudaMemcpyHostToDevice));
+  }
   XG_TRY(cudaMemcpy(dv.p, v, m * k * 8, cudaMemcpyHostToDevice));
   XG_TRY(cudaMemset(dbad.p, 0xFF, 8));
   XG_TRY(launch_exact_rownorm(dx.p, n, m, dxn.p, dn.p, dbad.p, 0));
@@ -222,6 +254,7 @@ XG_API int xg_f64_compress_series(const double* x, int64_t n, int64_t m, const d
   XG_TRY(cudaMemcpy(norms, dn.p, n * 8, cudaMemcpyDeviceToHost));
   return XG_OK;
 }
+}  // namespace
 
 // compress_frame (compress.cpp:34-46).
 XG_API int xg_f64_compress_frame(const double* frame, int64_t m, const double* v, int64_t k,

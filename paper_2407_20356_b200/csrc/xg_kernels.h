@@ -405,6 +405,7 @@ cudaError_t launch_g2_div(const double* sum, const int64_t* cnt, double* out, in
                           cudaStream_t s);
 
 // ------------------------------------------- K9 reference-order f64 replicas
+cudaError_t launch_exact_widen_u8(const uint8_t* x, int64_t count, double* out, cudaStream_t s);
 cudaError_t launch_exact_rownorm(const double* x, int64_t n, int64_t m, double* xn, double* norms,
                                  unsigned long long* bad, cudaStream_t s);
 cudaError_t launch_exact_gram(const double* x, int64_t n, int64_t m, double* g, cudaStream_t s);

@@ -42,6 +42,40 @@ def test_compress_series_frame_bitwise(ctx, orc):
         assert np.array_equal(c, y[i])            # stream == batch (compress.cpp:64)
 
 
+def test_compress_series_u8_counts_bitwise(ctx, orc):
+    """xg_f64_compress_series_u8 (the drop-in's route for integer counts: u8
+    over PCIe, widened on the device) == the f64 entry == the oracle, bit for
+    bit, at sizes where the widening kernel's 16-byte body and ragged tail
+    both run; a zero frame keeps its index."""
+    import ctypes as C
+
+    from paper_2407_20356_b200 import _abi
+
+    def run(fn, x, v):
+        n, m = x.shape
+        k = v.shape[1]
+        y = np.empty((n, k))
+        nr = np.empty(n)
+        rc = fn(x.ctypes.data_as(C.c_void_p if x.dtype == np.uint8 else _abi.PD), n, m,
+                v.ctypes.data_as(_abi.PD), k, y.ctypes.data_as(_abi.PD), nr.ctypes.data_as(_abi.PD))
+        return rc, y, nr
+
+    for (t, h, w, mu, k, seed) in [(64, 24, 24, 0.5, 12, 3), (33, 17, 13, 3.0, 7, 4)]:
+        f8 = orc.gen_speckle(t, h, w, 1, mu, seed)
+        f = f8.astype(np.float64)
+        v = np.linalg.qr(np.random.default_rng(seed).standard_normal((h * w, k)))[0]
+        rc8, y8, n8 = run(_abi.lib.xg_f64_compress_series_u8, np.ascontiguousarray(f8), v)
+        rc, y, n = run(_abi.lib.xg_f64_compress_series, f, v)
+        assert rc8 == 0 and rc == 0
+        y0, n0 = orc.compress_series(f, v)
+        assert np.array_equal(y8, y) and np.array_equal(n8, n)
+        assert np.array_equal(y8, y0) and np.array_equal(n8, n0)
+    f8 = np.ascontiguousarray(f8)
+    f8[5] = 0
+    rc8, _, _ = run(_abi.lib.xg_f64_compress_series_u8, f8, v)
+    assert rc8 == _abi.ERR_NORMALIZATION and _abi.lib.xg_f64_last_payload() == 5
+
+
 def test_ttc_compressed_extend_g2_bitwise(ctx, orc):
     x = orc.random_positive_matrix(50, 128, 8)
     v = np.linalg.qr(np.random.default_rng(1).standard_normal((128, 5)))[0]
