@@ -1053,6 +1053,8 @@ def synth_speckle(ctx: Context, out_device_ptr: int, n_frames: int, height: int,
                   n_rings: int, mu: float, seed: int, gamma_mode: int = 0,
                   gamma_a: float = 0.002) -> None:
     """Seeded synthetic speckle counts written straight into device memory
-    (benchmark input generator, K8)."""
+    (benchmark input generator, K8).  Returns once the frames are written:
+    K8 runs on the library's stream, and callers read the buffer from torch's."""
     _check(ctx.h, lib.xg_synth_speckle(ctx.h, n_frames, height, width, n_rings, mu, gamma_mode,
                                        gamma_a, seed, C.c_void_p(out_device_ptr)))
+    ctx.synchronize()

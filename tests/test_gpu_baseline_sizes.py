@@ -21,6 +21,9 @@ SURVEY 8(d)), not only at toy sizes.
     compress_series + ttc_compressed on the SAME V (device-built basis read
     back), within 1e-5.  Pins: acceptance_main.cpp:329-353 (stream == batch),
     test_correlate.cpp:138-157.
+  * C4 in full (T=16384, 1024x1024, Q=100): three rings' int32 Grams bitwise
+    against an exact device product; the smallest ring's C and g2 against
+    the reference at T=16384.
 """
 import numpy as np
 import pytest
@@ -142,3 +145,50 @@ def test_c3_stream_to_depth_4352(ctx, orc, ref):
         cc_ref = ref.ttc_compressed(y_ref)[0]
         cc = st.ttc(r, compressed=True)[np.ix_(keep, keep)]
         assert np.abs(cc - cc_ref).max() <= 1e-5 * np.abs(cc_ref).max(), r
+
+
+def test_c4_full_size_rings(ctx, orc, ref):
+    """C4 (BASELINE configs[3]) at its own size: T=16384 frames of 1024x1024,
+    Q=100 rings, Gamma_q log-spaced (the bench's frames, K8, seed 4).  Three
+    rings' exact int32 Grams -- the smallest, a mid-size and the largest, so
+    K2's wave-gated tile schedule with 64 row blocks and a 10k-pixel K loop is
+    covered -- equal BITWISE an independent exact product (cuBLAS f64 on the
+    device: every partial sum of counts < 2^53, so exact in any order).  The
+    smallest ring without a zero frame: its C and g2 within 1e-12 of the
+    unmodified reference's ttc_raw / g2_from_ttc at T=16384."""
+    import torch
+
+    t, h, w, q, mu = 16384, 1024, 1024, 100, 0.05
+    dev = torch.empty((t, h * w), dtype=torch.uint8, device="cuda")
+    xg.synth_speckle(ctx, dev.data_ptr(), t, h, w, q, mu, 4, 1, 2e-4)
+    ctx.synchronize()
+    ring = xg.annular_rings(h, w, q)
+    sizes = np.bincount(ring, minlength=q)
+    lay = xg.RingLayout.from_ring_map(ctx, ring, q)
+    s = xg.FrameSeries(lay, t).load(dev).ttc_raw()
+    r_small, r_big = int(np.argmin(sizes)), int(np.argmax(sizes))
+    g = torch.empty((t, t), dtype=torch.int32, device="cuda")
+    for r in (r_small, 50, r_big):
+        cols = torch.from_numpy(np.flatnonzero(ring == r)).cuda()
+        xq = torch.index_select(dev, 1, cols).double()
+        exact = (xq @ xq.T).to(torch.int64)
+        s.ttc(r, "gram", out=g)
+        assert torch.equal(g.to(torch.int64), exact), (r, int(sizes[r]))
+        del xq, exact
+    # the reference's ttc_raw throws on a zero frame (linalg.cpp:446-449):
+    # compare on the smallest ring whose 16384 frames all carry photons
+    r_ref = None
+    for r in np.argsort(sizes, kind="stable"):
+        xs = dev[:, torch.from_numpy(np.flatnonzero(ring == r)).cuda()].cpu().numpy()
+        if xs.any(axis=1).all():
+            r_ref = int(r)
+            break
+    assert r_ref is not None and sizes[r_ref] < 4000
+    del dev, g
+    torch.cuda.empty_cache()
+    c_ref = ref.ttc_raw(xs.astype(np.float64))
+    assert np.abs(s.ttc(r_ref, "f64") - c_ref).max() <= 1e-12
+    _, g2_ref, cnt_ref = ref.g2_from_ttc(c_ref)
+    _, g2, cnt = s.g2(r_ref)
+    assert np.array_equal(cnt, cnt_ref)
+    assert np.abs(g2 - g2_ref).max() <= 1e-12

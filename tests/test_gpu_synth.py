@@ -21,7 +21,7 @@ def _device_frames(ctx, t, h, w, q, mu, seed, gamma_mode=0, gamma_a=0.002):
 
     dev = torch.empty((t, h * w), dtype=torch.uint8, device="cuda")
     xg.synth_speckle(ctx, dev.data_ptr(), t, h, w, q, mu, seed, gamma_mode, gamma_a)
-    torch.cuda.synchronize()
+    ctx.synchronize()
     return dev.cpu().numpy()
 
 
@@ -72,6 +72,7 @@ def test_k8_at_c2_geometry_full_T(ctx, orc):
                                   for r in range(q)]))
     dev = torch.empty((t, h * w), dtype=torch.uint8, device="cuda")
     xg.synth_speckle(ctx, dev.data_ptr(), t, h, w, q, mu, seed)
+    ctx.synchronize()  # K8 runs on the library's stream, torch reads on its own
     sub = dev[:, torch.from_numpy(pix).cuda()].cpu().numpy()
     host = orc.gen_speckle_pixels(t, h, w, q, mu, seed, pix)
     _compare(sub, host, ring[pix], q)
