@@ -24,6 +24,13 @@ SURVEY 8(d)), not only at toy sizes.
   * C4 in full (T=16384, 1024x1024, Q=100): three rings' int32 Grams bitwise
     against an exact device product; the smallest ring's C and g2 against
     the reference at T=16384.
+  * C5 geometry (1536x2048, Q=128, mu=0.01; T=8192 of its 65536 frames, fed
+    as two of the bench's 4096-frame chunks through a 4096-frame buffer) at
+    k=16 and k=256: sampled rings' coefficients within 1e-6 of the oracle's
+    compress_series on the same V (strided frames; every frame of one ring
+    against the unmodified reference), norms bitwise; the homomorphic g2
+    with no C~ stored -- through the K4 tiles and in the Fourier domain --
+    within 1e-5 of the reference's g2_from_ttc(ttc_compressed(...)).
 """
 import numpy as np
 import pytest
@@ -192,3 +199,84 @@ def test_c4_full_size_rings(ctx, orc, ref):
     _, g2, cnt = s.g2(r_ref)
     assert np.array_equal(cnt, cnt_ref)
     assert np.abs(g2 - g2_ref).max() <= 1e-12
+
+
+@pytest.mark.parametrize("k", [16, 256])
+def test_c5_geometry_chunked(ctx, orc, ref, k):
+    """C5 (BASELINE configs[4]) geometry through the path the bench times:
+    compress_chunk of 4096-frame chunks (K1 + K3, frames never resident as a
+    whole) and ttc_compressed(store=False) both ways.  T is 8192, not 65536:
+    the checker needs the reference's T x T matrix.  Pins: compress.cpp:122-191
+    (project_row / compress_series), correlate.cpp:27-35,67-85."""
+    import torch
+
+    t, ch, h, w, q, mu = 8192, 4096, 1536, 2048, 128, 0.01
+    dev = torch.empty((t, h * w), dtype=torch.uint8, device="cuda")
+    for j in range(t // ch):  # the bench's chunk recipe: a fresh stretch per chunk
+        xg.synth_speckle(ctx, dev[j * ch].data_ptr(), ch, h, w, q, mu, 5000 + j)
+    ctx.synchronize()
+    ring = xg.annular_rings(h, w, q)
+    sizes = np.bincount(ring, minlength=q)
+    lay = xg.RingLayout.from_ring_map(ctx, ring, q)
+    # one ring checked on every frame against the reference: the smallest
+    # that holds k columns and has no zero frame (compress_series raises on one)
+    cols = {}
+    r_ref = None
+    for r in np.argsort(sizes, kind="stable"):
+        if sizes[r] < max(k, 2000):
+            continue
+        c = torch.from_numpy(np.flatnonzero(ring == r)).cuda()
+        if bool((torch.index_select(dev, 1, c).sum(1, dtype=torch.int64) > 0).all()):
+            r_ref, cols[int(r)] = int(r), c
+            break
+    assert r_ref is not None and sizes[r_ref] < 8000
+    r_big = int(np.argmax(sizes))
+    sampled = [r_ref, 64, r_big]
+    rng = np.random.default_rng(50 + k)
+    basis = xg.Basis(lay, k)
+    vs = {}
+    for r in range(q):
+        m = int(sizes[r])
+        if r in sampled:
+            v, _ = np.linalg.qr(rng.standard_normal((m, k)))
+            vs[r] = v
+        else:  # orthonormal and cheap: k unit vectors
+            v = np.zeros((m, k))
+            idx = np.arange(min(m, k))
+            v[idx, idx] = 1.0
+        basis.set_ring(r, v)
+    s = xg.FrameSeries(lay, t, x_frames=ch)
+    for j in range(t // ch):
+        s.compress_chunk(basis, dev[j * ch:(j + 1) * ch], first=(j == 0))
+    stride = 32
+    for r in sampled:
+        c = cols.get(r)
+        if c is None:
+            c = torch.from_numpy(np.flatnonzero(ring == r)).cuda()
+        y, nr = s.coeffs(r)
+        if r == r_ref:
+            xq = torch.index_select(dev, 1, c).cpu().numpy().astype(np.float64)
+            y_ref, n_ref = ref.compress_series(xq, vs[r])
+            assert np.array_equal(nr, n_ref)
+            assert np.abs(y - y_ref).max() <= 1e-6 * np.abs(y_ref).max(), r
+        else:
+            xq = torch.index_select(dev[::stride], 1, c).cpu().numpy().astype(np.float64)
+            keep = xq.sum(1) > 0
+            y_o, n_o = orc.compress_series(xq[keep], vs[r])
+            assert np.array_equal(nr[::stride][keep], n_o)
+            assert np.abs(y[::stride][keep] - y_o).max() <= 1e-6 * np.abs(y_o).max(), r
+            assert np.all(nr[::stride][~keep] == 0)
+        del xq
+    del dev
+    torch.cuda.empty_cache()
+    cc_ref = ref.ttc_compressed(y_ref)[0]
+    _, g2_ref, cnt_ref = ref.g2_from_ttc(cc_ref)
+    del cc_ref
+    scale = np.abs(g2_ref).max()
+    s.ttc_compressed(store=False)
+    _, g2_t, cnt_t = s.cg2(r_ref)
+    s.ttc_compressed(store=False, spectral=True)
+    _, g2_s, cnt_s = s.cg2(r_ref)
+    assert np.array_equal(cnt_t, cnt_ref) and np.array_equal(cnt_s, cnt_ref)
+    assert np.abs(g2_t - g2_ref).max() <= 1e-5 * scale
+    assert np.abs(g2_s - g2_ref).max() <= 1e-5 * scale
