@@ -201,14 +201,19 @@ def test_c4_full_size_rings(ctx, orc, ref):
     assert np.abs(g2 - g2_ref).max() <= 1e-12
 
 
-@pytest.mark.parametrize("k", [16, 256])
-def test_c5_geometry_chunked(ctx, orc, ref, k):
+@pytest.mark.parametrize("k,digits", [(16, 3), (256, 3), (256, 2)])
+def test_c5_geometry_chunked(ctx, orc, ref, k, digits):
     """C5 (BASELINE configs[4]) geometry through the path the bench times:
     compress_chunk of 4096-frame chunks (K1 + K3, frames never resident as a
     whole) and ttc_compressed(store=False) both ways.  T is 8192, not 65536:
     the checker needs the reference's T x T matrix.  Pins: compress.cpp:122-191
-    (project_row / compress_series), correlate.cpp:27-35,67-85."""
+    (project_row / compress_series), correlate.cpp:27-35,67-85.
+    digits=2 is the reduced-precision projection the bench times at k=256
+    (V as 2 int8 digits, ~8e-6 of max|V|): coefficients within 5e-5, g2
+    within 1e-3 -- inside the 1e-2 BASELINE allows C5's bf16 projection."""
     import torch
+
+    ytol, gtol = (1e-6, 1e-5) if digits == 3 else (5e-5, 1e-3)
 
     t, ch, h, w, q, mu = 8192, 4096, 1536, 2048, 128, 0.01
     dev = torch.empty((t, h * w), dtype=torch.uint8, device="cuda")
@@ -233,7 +238,7 @@ def test_c5_geometry_chunked(ctx, orc, ref, k):
     r_big = int(np.argmax(sizes))
     sampled = [r_ref, 64, r_big]
     rng = np.random.default_rng(50 + k)
-    basis = xg.Basis(lay, k)
+    basis = xg.Basis(lay, k, digits=digits)
     vs = {}
     for r in range(q):
         m = int(sizes[r])
@@ -258,13 +263,13 @@ def test_c5_geometry_chunked(ctx, orc, ref, k):
             xq = torch.index_select(dev, 1, c).cpu().numpy().astype(np.float64)
             y_ref, n_ref = ref.compress_series(xq, vs[r])
             assert np.array_equal(nr, n_ref)
-            assert np.abs(y - y_ref).max() <= 1e-6 * np.abs(y_ref).max(), r
+            assert np.abs(y - y_ref).max() <= ytol * np.abs(y_ref).max(), r
         else:
             xq = torch.index_select(dev[::stride], 1, c).cpu().numpy().astype(np.float64)
             keep = xq.sum(1) > 0
             y_o, n_o = orc.compress_series(xq[keep], vs[r])
             assert np.array_equal(nr[::stride][keep], n_o)
-            assert np.abs(y[::stride][keep] - y_o).max() <= 1e-6 * np.abs(y_o).max(), r
+            assert np.abs(y[::stride][keep] - y_o).max() <= ytol * np.abs(y_o).max(), r
             assert np.all(nr[::stride][~keep] == 0)
         del xq
     del dev
@@ -278,5 +283,5 @@ def test_c5_geometry_chunked(ctx, orc, ref, k):
     s.ttc_compressed(store=False, spectral=True)
     _, g2_s, cnt_s = s.cg2(r_ref)
     assert np.array_equal(cnt_t, cnt_ref) and np.array_equal(cnt_s, cnt_ref)
-    assert np.abs(g2_t - g2_ref).max() <= 1e-5 * scale
-    assert np.abs(g2_s - g2_ref).max() <= 1e-5 * scale
+    assert np.abs(g2_t - g2_ref).max() <= gtol * scale
+    assert np.abs(g2_s - g2_ref).max() <= gtol * scale
