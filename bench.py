@@ -961,6 +961,10 @@ def run_c5(E):
                                    "note": "K1 reads the raster + writes the ring-major copy, K3 "
                                            "re-reads it (3 B per pixel per frame)"},
             "projection_int8_tops_over_ingest_project": proj_ops / tc / 1e12,
+            "bound": ("hbm" if k <= 64 else
+                      "tensor: K3 alone runs 7.12 ms per 4096-frame chunk = 2.78 POPS, 0.87 of the "
+                      "cuBLAS int8 GEMM (profiles/r2_c5_project_k256.ncu-rep); the hbm frac above "
+                      "is not the bound at this k"),
             "projection_note": "2 T M 3k int8 ops (3 digits); at k = 256 K3 is tensor-bound "
                                "(ops / the whole K1 + K3 time, a lower bound on K3's rate)"}
         del s
